@@ -1,0 +1,355 @@
+/*
+ * microkv.h — C ABI of the B200-native paged-KV hot path behind the
+ * microserving sub-request APIs (arXiv 2412.12488, "A System for
+ * Microserving of LLMs").
+ *
+ * Drop-in boundary for `splitserve::KVCache`
+ * (/root/reference/proj/core/include/splitserve/kv_cache.h:132-266): every
+ * entry point below mirrors one reference member function with plain
+ * pointers and sizes (no C++ or torch types).  A C++ engine keeps calling
+ * the reference's class API through a thin facade that rethrows
+ * `splitserve::Error` from the returned status.
+ *
+ * Two libraries implement this header:
+ *   paper_2412_12488_b200/_lib/libmicrokv.so   B200 product: host bookkeeping in C++,
+ *                                              KV pool, page tables and all data
+ *                                              movement on the GPU (sm_100a kernels).
+ *   oracle/_ref/libmicrokv_ref.so              test oracle only: the UNMODIFIED reference
+ *                                              KVCache compiled from /root/reference
+ *                                              behind the same ABI (host entry points only).
+ *
+ * Conventions
+ *  - Every function returning `int` returns SS_OK (0) or a status: 1 + the
+ *    reference `ErrorCode` value (errors.h:14-33), or one of the SS_ERR_*
+ *    codes >= 100 that exist only at this boundary.  `ss_last_error()` holds
+ *    the detail string of the last failure (the reference's `Error::what()`).
+ *  - Tokens are int32 (common.h:15), sequence ids int64 (common.h:19), ranks
+ *    int32 (common.h:22).  Token ranges are half-open [begin, end).
+ *  - "Host" entry points take host buffers and complete synchronously, like
+ *    the reference.  `*_async` entry points take device pointers and a
+ *    `cudaStream_t` passed as `void*` (NULL = legacy default stream) and
+ *    only enqueue work.
+ *  - A cache created with `device = -1` is host-only: bookkeeping calls
+ *    (match, prep_recv page reservation, fork, allocate, build_addr, free,
+ *    evict, pin, queries on metadata) work; any call that touches KV bytes
+ *    returns SS_ERR_NO_DEVICE.  There is no CPU data path.
+ */
+#ifndef MICROKV_H_
+#define MICROKV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SS_ABI_VERSION 1
+
+/* ------------------------------------------------------------------ */
+/* Status codes                                                        */
+/* ------------------------------------------------------------------ */
+enum ss_status {
+  SS_OK = 0,
+  /* 1 + splitserve::ErrorCode (errors.h:14-33), same order. */
+  SS_ERR_OUT_OF_PAGES = 1,
+  SS_ERR_DUPLICATE_SEQUENCE = 2,
+  SS_ERR_UNKNOWN_SEQUENCE = 3,
+  SS_ERR_FORK_BEYOND_COMMITTED = 4,
+  SS_ERR_ADDR_MISMATCH = 5,
+  SS_ERR_MISSING_KV = 6,
+  SS_ERR_LAYER_ORDER_VIOLATION = 7,
+  SS_ERR_CANNOT_EVICT = 8,
+  SS_ERR_CHECKSUM_MISMATCH = 9,
+  SS_ERR_UNKNOWN_ADDRESS = 10,
+  SS_ERR_PEER_UNREACHABLE = 11,
+  SS_ERR_NO_ENGINES = 12,
+  SS_ERR_ROLE_MISSING = 13,
+  SS_ERR_NO_OWNER = 14,
+  SS_ERR_UNKNOWN_STRATEGY = 15,
+  SS_ERR_INVALID_ARGUMENT = 16,
+  SS_ERR_ABORTED = 17,
+  SS_ERR_INTERNAL = 18,
+  /* Boundary-only codes. */
+  SS_ERR_UNSUPPORTED = 100,      /* entry point not provided by this library */
+  SS_ERR_BUFFER_TOO_SMALL = 101, /* output capacity short; *_n outputs hold the need */
+  SS_ERR_CUDA = 102,             /* CUDA runtime failure; detail in ss_last_error */
+  SS_ERR_NO_DEVICE = 103         /* data-path call on a host-only cache */
+};
+
+/* KVCache::ApplyStatus (kv_cache.h:194). */
+enum ss_apply_status { SS_APPLY_OK = 0, SS_APPLY_DUPLICATE = 1, SS_APPLY_UNKNOWN_ADDRESS = 2 };
+
+/* FillState (kv_cache.h:40-44). */
+enum ss_fill_state { SS_FILL_EMPTY = 0, SS_FILL_COMPUTED_LOCAL = 1, SS_FILL_RECEIVED_REMOTE = 2 };
+
+typedef struct ss_cache ss_cache; /* one engine's KVCache */
+typedef struct ss_plan ss_plan;   /* ForwardPlan (kv_cache.h:116-121) */
+
+/* ------------------------------------------------------------------ */
+/* Plain-data mirrors of the reference types                           */
+/* ------------------------------------------------------------------ */
+
+/* CacheConfig (config.h:101-108) + ModelConfig (config.h:22-30). */
+typedef struct {
+  int64_t num_pages;  /* CacheConfig::num_pages (default 4096) */
+  int32_t page_size;  /* CacheConfig::page_size, power of two (default 16) */
+  int32_t layers;     /* ModelConfig::layers L */
+  int32_t dim;        /* ModelConfig::dim = u64 words W per (token, layer) entry */
+  int32_t vocab;      /* ModelConfig::vocab */
+  uint64_t hash_seed; /* ModelConfig::hash_seed (default 0x5eed5eed5eed5eed) */
+  int32_t device;     /* CUDA device ordinal; -1 = host-only bookkeeping */
+  int32_t rank;       /* this engine's rank (EngineConfig::rank, config.h:112) */
+} ss_config;
+
+/* SlotRange (kv_addr.h:19-24). */
+typedef struct {
+  int64_t page_id;
+  int32_t slot_begin;
+  int32_t slot_count;
+} ss_slot_range;
+
+/* KVAddrInfo (kv_addr.h:30-48).  As an output, `ranges` is caller storage
+ * of `ranges_cap` entries; `n_ranges` is set to the count written (or the
+ * count needed, with SS_ERR_BUFFER_TOO_SMALL). */
+typedef struct {
+  int64_t token_begin;
+  int64_t token_count;
+  int64_t n_ranges;
+  ss_slot_range* ranges;
+  int64_t ranges_cap;
+} ss_addr;
+
+/* BatchEntry (kv_cache.h:85-89). */
+typedef struct {
+  int64_t seq;
+  int64_t begin;
+  int64_t end;
+  int32_t is_decode;
+  int32_t _pad;
+} ss_batch_entry;
+
+/* Scalar fields of SequenceRecord (kv_cache.h:56-82). */
+typedef struct {
+  int64_t id;
+  int64_t parent;
+  int64_t fork_len;
+  int32_t refcount;
+  int32_t finished;
+  int64_t alloc_len;
+  int64_t committed_hint;
+  int64_t num_tokens;
+  int64_t num_own_pages;
+  int64_t fold_frontier;
+  int64_t digest_len;
+  uint64_t prefix_digest;
+  int32_t has_window;
+  int32_t window_complete;
+  int64_t window_begin;
+  int64_t window_end;
+  int64_t window_expected_writes;
+  int64_t window_received_writes;
+} ss_record_info;
+
+/* FrameSink (kv_cache.h:124-125): called once per (send, layer) by
+ * ss_attention with the gathered host payload (send.range.size() * dim
+ * words, token order).  The payload is borrowed for the duration of the
+ * call (the reference moves a std::vector into the sink). */
+typedef void (*ss_frame_sink)(void* user, int32_t layer, int64_t seq, int64_t range_begin,
+                              int64_t range_end, int32_t dest, const ss_addr* dest_addr,
+                              uint64_t user_tag, const uint64_t* payload, int64_t n_words);
+
+/* Opaque CUDA IPC export of an engine's receive surface (KV pool, fill
+ * bytes, page->window map, window counters) for a peer process. */
+#define SS_IPC_HANDLE_BYTES 512
+typedef struct {
+  uint8_t bytes[SS_IPC_HANDLE_BYTES];
+} ss_ipc_handle;
+
+/* ------------------------------------------------------------------ */
+/* Construction, errors, hash model                                    */
+/* ------------------------------------------------------------------ */
+/* KVCache(CacheConfig, const HashModel*) kv_cache.cc:26-47 with the
+ * HashModel(ModelConfig) ctor hash_model.cc:22-25 folded in.  Validation:
+ * CacheConfig::Validate / ModelConfig::Validate (config.cc:17-27). */
+int ss_cache_create(const ss_config* config, ss_cache** out);
+void ss_cache_destroy(ss_cache* cache);
+int ss_abi_version(void);
+const char* ss_last_error(const ss_cache* cache);
+/* ErrorCodeName (event_log.cc:11-33) for 1..18; boundary names otherwise. */
+const char* ss_status_name(int status);
+/* IsRetryable (event_log.cc:35-43). */
+int ss_status_retryable(int status);
+/* Which implementation is behind the ABI: "microkv-b200" or "splitserve-reference". */
+const char* ss_impl_name(void);
+
+/* HashModel entry points an engine needs around the cache
+ * (hash_model.cc:27-37,63-86). */
+uint64_t ss_initial_prefix_digest(const ss_cache* cache);
+uint64_t ss_embed(const ss_cache* cache, int32_t token, int64_t pos);
+int32_t ss_sample_token(const ss_cache* cache, uint64_t last_hidden);
+
+/* ------------------------------------------------------------------ */
+/* Declaration stage (kv_cache.h:136-171)                              */
+/* ------------------------------------------------------------------ */
+/* MatchPrefixSeq (kv_cache.cc:116-118 -> radix_tree.cc:28-53). `seq_out` may be NULL. */
+int ss_match_prefix(ss_cache* cache, const int32_t* tokens, int64_t n, int64_t* match_len,
+                    int64_t* seq_out);
+/* PrepRecv (kv_cache.cc:187-229).  addr_out->ranges_cap must cover
+ * ceil((e - m) / page_size) ranges, else SS_ERR_BUFFER_TOO_SMALL with no
+ * allocation (the radix LRU touch of the match has happened, as on the
+ * reference's OutOfPages path). */
+int ss_prep_recv(ss_cache* cache, int64_t seq, const int32_t* tokens, int64_t n, int64_t end,
+                 int64_t* match_len, ss_addr* addr_out);
+/* CreateSequence (kv_cache.cc:120-131). */
+int ss_create_sequence(ss_cache* cache, int64_t seq, const int32_t* tokens, int64_t n);
+/* ForkSequence (kv_cache.cc:133-166); n = 0 copies the parent's prefix tokens. */
+int ss_fork_sequence(ss_cache* cache, int64_t parent, int64_t child, int64_t fork_len,
+                     const int32_t* child_tokens, int64_t n);
+/* MarkSend (kv_cache.cc:231-243). */
+int ss_mark_send(ss_cache* cache, int64_t seq, int64_t begin, int64_t end, int32_t dest,
+                 const ss_addr* dest_addr, uint64_t user_tag);
+/* EnsureAllocated (kv_cache.cc:168-183). */
+int ss_ensure_allocated(ss_cache* cache, int64_t seq, int64_t upto);
+/* AppendToken (kv_cache.cc:185). */
+int ss_append_token(ss_cache* cache, int64_t seq, int32_t token);
+/* BeginForward (kv_cache.cc:245-306).  The plan lives until ss_plan_destroy. */
+int ss_begin_forward(ss_cache* cache, const ss_batch_entry* batch, int64_t n, ss_plan** plan_out);
+int64_t ss_plan_total_outputs(const ss_plan* plan);
+int64_t ss_plan_num_sends(const ss_plan* plan);
+int32_t ss_plan_next_layer(const ss_plan* plan);
+void ss_plan_destroy(ss_plan* plan);
+
+/* ------------------------------------------------------------------ */
+/* Computation stage (kv_cache.h:173-189)                              */
+/* ------------------------------------------------------------------ */
+/* Attention (kv_cache.cc:308-371): KV write for Empty output slots, fold,
+ * hidden outputs, then one sink call per marked send.  Sends whose `dest`
+ * has an attached peer (ss_attach_peer / ss_import_ipc) are stored straight
+ * into the peer's reserved pages instead of going through `sink`. */
+int ss_attention(ss_cache* cache, ss_plan* plan, int32_t layer, const uint64_t* hidden_in,
+                 uint64_t* hidden_out, int64_t n, ss_frame_sink sink, void* user);
+/* GatherRange (kv_cache.cc:373-387) into caller storage of out_words. */
+int ss_gather_range(ss_cache* cache, int64_t seq, int64_t begin, int64_t end, int32_t layer,
+                    uint64_t* out, int64_t out_words);
+/* BuildAddr (kv_cache.cc:389-407). */
+int ss_build_addr(ss_cache* cache, int64_t seq, int64_t begin, int64_t end, ss_addr* addr_out);
+
+/* ------------------------------------------------------------------ */
+/* Transfer agent (kv_cache.h:191-199)                                 */
+/* ------------------------------------------------------------------ */
+/* ApplyRemoteWrite (kv_cache.cc:409-463); *apply_status = ss_apply_status.
+ * Payload-size mismatch returns SS_ERR_INVALID_ARGUMENT (kv_cache.cc:411). */
+int ss_apply_remote_write(ss_cache* cache, const ss_addr* addr, int32_t layer,
+                          const uint64_t* payload, int64_t n_words, uint64_t tag,
+                          int32_t* apply_status);
+/* DrainReceiveCompletions (kv_cache.cc:465-480).  Also completes windows
+ * filled by device-direct peer sends. */
+int ss_drain_receive_completions(ss_cache* cache, int64_t* seqs_out, int64_t cap, int64_t* n_out);
+
+/* ------------------------------------------------------------------ */
+/* Lifecycle (kv_cache.h:201-217)                                      */
+/* ------------------------------------------------------------------ */
+int ss_set_finished(ss_cache* cache, int64_t seq, int32_t finished);   /* kv_cache.cc:482 */
+int ss_commit_to_tree(ss_cache* cache, int64_t seq);                   /* kv_cache.cc:484-490 */
+int ss_free_sequence(ss_cache* cache, int64_t seq);                    /* kv_cache.cc:492-518 */
+int ss_evict(ss_cache* cache, int64_t bytes_needed, int64_t* freed_tokens); /* :520-546 */
+int ss_pin(ss_cache* cache, const int32_t* prefix, int64_t n, int32_t flag); /* :548 */
+
+/* ------------------------------------------------------------------ */
+/* Queries (kv_cache.h:219-235)                                        */
+/* ------------------------------------------------------------------ */
+int ss_has_sequence(const ss_cache* cache, int64_t seq);
+/* GetRecord (kv_cache.cc:552); own_pages may be NULL. */
+int ss_get_record(ss_cache* cache, int64_t seq, ss_record_info* info, int64_t* own_pages,
+                  int64_t own_cap);
+/* Committed (kv_cache.cc:554-558). */
+int ss_committed(ss_cache* cache, int64_t seq, int64_t* out);
+/* ReadEntryWords (kv_cache.cc:560-566) into out[dim]. */
+int ss_read_entry_words(ss_cache* cache, int64_t seq, int64_t pos, int32_t layer, uint64_t* out,
+                        int64_t out_words);
+/* FillOf (kv_cache.cc:568-574). */
+int ss_fill_of(ss_cache* cache, int64_t seq, int64_t pos, int32_t layer, int32_t* out);
+int64_t ss_free_pages(const ss_cache* cache);
+int64_t ss_total_pages(const ss_cache* cache);
+int64_t ss_bytes_per_page(const ss_cache* cache);
+int64_t ss_sequence_count(const ss_cache* cache);
+int ss_sequence_ids(const ss_cache* cache, int64_t* out, int64_t cap, int64_t* n_out);
+int64_t ss_pending_send_count(const ss_cache* cache);
+/* Radix tree probes (radix_tree.h:49-56), for parity tests of its quirks. */
+int64_t ss_tree_node_count(const ss_cache* cache);
+int ss_tree_contains(const ss_cache* cache, int64_t seq);
+uint64_t ss_tree_last_touch(const ss_cache* cache, int64_t seq);
+int ss_tree_sequences_by_lru(const ss_cache* cache, int64_t* out, int64_t cap, int64_t* n_out);
+
+/* KVAddrInfo helpers (kv_addr.cc:16-51). */
+int ss_addr_validate(const ss_addr* addr);
+int ss_addr_slice(const ss_addr* in, int64_t begin, int64_t end, ss_addr* out);
+
+/* ------------------------------------------------------------------ */
+/* B200 device entry points (no reference counterpart; the reference   */
+/* moves KV with host memcpy + TCP frames, transport.h:78-88)          */
+/* ------------------------------------------------------------------ */
+/* Device the cache lives on (-1 for host-only). */
+int ss_device(const ss_cache* cache);
+/* Attach an in-process peer engine as the destination for `dest` ranks'
+ * sends (same GPU or a peer-accessible GPU). */
+int ss_attach_peer(ss_cache* cache, int32_t dest, ss_cache* peer);
+/* Export this engine's receive surface for another process. */
+int ss_export_ipc(ss_cache* cache, ss_ipc_handle* out);
+/* Map a peer process's receive surface as the destination for `dest`. */
+int ss_import_ipc(ss_cache* cache, int32_t dest, const ss_ipc_handle* handle);
+int ss_detach_peer(ss_cache* cache, int32_t dest);
+
+/* Attention with device hidden buffers, enqueued on `stream`.  Marked
+ * sends must target attached peers (device-direct); otherwise
+ * SS_ERR_PEER_UNREACHABLE. */
+int ss_attention_async(ss_cache* cache, ss_plan* plan, int32_t layer, const uint64_t* hidden_in_dev,
+                       uint64_t* hidden_out_dev, void* stream);
+/* DirectSend (SPEC.md:292-299 Case 1; GatherRange + ApplyRemoteWrite per
+ * layer): stores layers [layer_begin, layer_end) of positions [begin, end)
+ * of `seq` straight into `dest`'s pages named by `dest_addr`.  Receiver
+ * semantics are ApplyRemoteWrite's: Empty slots only, every slot counts
+ * toward the window, completion seen by the receiver's drain. */
+int ss_direct_send_async(ss_cache* cache, int64_t seq, int64_t begin, int64_t end, int32_t dest,
+                         const ss_addr* dest_addr, uint64_t user_tag, int32_t layer_begin,
+                         int32_t layer_end, void* stream);
+/* GatherRange into device memory out_dev[(end-begin) * dim] on `stream`. */
+int ss_gather_range_async(ss_cache* cache, int64_t seq, int64_t begin, int64_t end, int32_t layer,
+                          uint64_t* out_dev, void* stream);
+/* ApplyRemoteWrite with a device-resident payload. */
+int ss_apply_remote_write_async(ss_cache* cache, const ss_addr* addr, int32_t layer,
+                                const uint64_t* payload_dev, int64_t n_words, uint64_t tag,
+                                int32_t* apply_status, void* stream);
+/* KV append from a dense device row buffer rows_dev[total_outputs][dim]
+ * (the producing layer's K||V rows, plan output order): Empty output slots
+ * are written and marked ComputedLocal (kv_cache.cc:328-334 write rule). */
+int ss_append_rows_async(ss_cache* cache, ss_plan* plan, int32_t layer, const void* rows_dev,
+                         void* stream);
+
+/* Paged GQA decode attention over the pool, reading K||V rows through the
+ * device page table: each (token, layer) entry of dim u64 words holds
+ * K[num_kv_heads][head_dim] then V[num_kv_heads][head_dim] in bf16
+ * (dim * 8 == 4 * num_kv_heads * head_dim).  q_dev/out_dev are bf16
+ * [batch][num_q_heads][head_dim]; context of batch b = positions
+ * [0, ctx_lens[b]) of seqs[b]. */
+int ss_begin_decode(ss_cache* cache, const int64_t* seqs, const int64_t* ctx_lens, int64_t batch,
+                    ss_plan** plan_out);
+int ss_paged_decode_attention_async(ss_cache* cache, ss_plan* decode_plan, int32_t layer,
+                                    int32_t num_q_heads, int32_t num_kv_heads, int32_t head_dim,
+                                    float softmax_scale, const void* q_dev, void* out_dev,
+                                    void* stream);
+
+/* Device pointer of layer `layer`'s pool slab ([num_pages][page_size][dim]
+ * u64 words) — for filling synthetic KV in tests and benchmarks. */
+int ss_pool_layer_ptr(ss_cache* cache, int32_t layer, void** dev_ptr);
+/* Number of kernel launches this cache has issued (evidence counter). */
+int64_t ss_kernel_launches(const ss_cache* cache);
+/* Sync the cache's internal stream. */
+int ss_synchronize(ss_cache* cache);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* MICROKV_H_ */

@@ -1,0 +1,1444 @@
+// cache.cc — the engine: reference bookkeeping on the host, KV in HBM.
+//
+// Each member cites the reference function it replaces
+// (/root/reference/proj/core/src/kv_cache.cc unless noted).  Bookkeeping
+// is kept bit-identical (page ids, page tables, addresses, match lengths,
+// window accounting, error codes); the KV bytes move only through the
+// kernels of kernels.cu.
+#include "cache.h"
+
+#include <algorithm>
+#include <cstring>
+#include <deque>
+
+#include "hash.cuh"
+
+using namespace mkv;
+
+namespace mkv {
+
+namespace {
+constexpr int32_t kMaxWindows = 4096;
+constexpr int32_t kMaxSeqRows = 16384;
+constexpr uint32_t kIpcMagic = 0x4d4b5631;  // "MKV1"
+
+const char* kCodeNames[] = {"OutOfPages",      "DuplicateSequence", "UnknownSequence",
+                            "ForkBeyondCommitted", "AddrMismatch",  "MissingKV",
+                            "LayerOrderViolation", "CannotEvict",   "ChecksumMismatch",
+                            "UnknownAddress",  "PeerUnreachable",   "NoEngines",
+                            "RoleMissing",     "NoOwner",           "UnknownStrategy",
+                            "InvalidArgument", "Aborted",           "Internal"};
+
+size_t Align(size_t x) { return (x + 255) & ~size_t(255); }
+}  // namespace
+
+const char* StatusName(int status) {
+  if (status == 0) return "OK";
+  if (status >= 1 && status <= 18) return kCodeNames[status - 1];
+  switch (status) {
+    case SS_ERR_UNSUPPORTED: return "Unsupported";
+    case SS_ERR_BUFFER_TOO_SMALL: return "BufferTooSmall";
+    case SS_ERR_CUDA: return "Cuda";
+    case SS_ERR_NO_DEVICE: return "NoDevice";
+  }
+  return "Unknown";
+}
+
+void Throw(int code, const std::string& detail) {
+  throw Error(1 + code, std::string(kCodeNames[code]) + ": " + detail);
+}
+
+void ThrowStatus(int status, const std::string& detail) {
+  throw Error(status, std::string(StatusName(status)) + ": " + detail);
+}
+
+void CudaCheck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    ThrowStatus(SS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+// kv_addr.cc:16-30
+void KVAddr::Validate() const {
+  int64_t total = 0;
+  std::set<std::pair<int64_t, int32_t>> seen;
+  for (const auto& r : ranges) {
+    MKV_CHECK(r.slot_count > 0 && r.slot_begin >= 0, kInvalidArgument, "bad slot range");
+    for (int32_t s = 0; s < r.slot_count; ++s) {
+      MKV_CHECK(seen.insert({r.page_id, r.slot_begin + s}).second, kInvalidArgument,
+                "overlapping slot ranges");
+    }
+    total += r.slot_count;
+  }
+  MKV_CHECK(total == token_count, kAddrMismatch, "slot counts do not cover token_count");
+}
+
+// kv_addr.cc:32-51
+KVAddr KVAddr::Slice(int64_t begin, int64_t end) const {
+  MKV_CHECK(begin >= token_begin && end <= token_begin + token_count && begin <= end,
+            kInvalidArgument, "slice outside address");
+  KVAddr out;
+  out.token_begin = begin;
+  out.token_count = end - begin;
+  int64_t pos = token_begin;
+  for (const auto& r : ranges) {
+    const int64_t lo = std::max(pos, begin), hi = std::min(pos + r.slot_count, end);
+    if (lo < hi) {
+      out.ranges.push_back({r.page_id, static_cast<int32_t>(r.slot_begin + (lo - pos)),
+                            static_cast<int32_t>(hi - lo)});
+    }
+    pos += r.slot_count;
+  }
+  return out;
+}
+
+namespace {
+// kv_cache.cc:13-18
+int64_t ResolveEndIndex(int64_t len, int64_t end) {
+  const int64_t e = end < 0 ? len + end : end;
+  MKV_CHECK(end != 0, kInvalidArgument, "end = 0 is invalid");
+  MKV_CHECK(e > 0 && e <= len, kInvalidArgument, "end out of range");
+  return e;
+}
+}  // namespace
+
+}  // namespace mkv
+
+// ---------------------------------------------------------------------------
+// Construction (kv_cache.cc:26-47; CacheConfig/ModelConfig::Validate config.cc:17-27)
+// ---------------------------------------------------------------------------
+ss_cache::ss_cache(const ss_config& cfg)
+    : num_pages_(cfg.num_pages),
+      P_(cfg.page_size),
+      L_(cfg.layers),
+      W_(cfg.dim),
+      vocab_(cfg.vocab),
+      hash_seed_(cfg.hash_seed),
+      device_(cfg.device),
+      rank_(cfg.rank) {
+  MKV_CHECK(cfg.layers >= 1, kInvalidArgument, "layers must be >= 1");
+  MKV_CHECK(cfg.dim >= 1, kInvalidArgument, "dim must be >= 1");
+  MKV_CHECK(cfg.vocab >= 2, kInvalidArgument, "vocab must be >= 2");
+  MKV_CHECK(cfg.num_pages >= 1, kInvalidArgument, "num_pages must be >= 1");
+  MKV_CHECK(cfg.page_size >= 1 && (cfg.page_size & (cfg.page_size - 1)) == 0, kInvalidArgument,
+            "page_size must be a power of two");
+  MKV_CHECK(cfg.num_pages * cfg.page_size < (int64_t(1) << 31), kInvalidArgument,
+            "num_pages * page_size must fit int32 slot indices");
+  seed_state_ = mkv::seed_state(hash_seed_);
+  // LIFO free list, lowest page first out (kv_cache.cc:45-46).
+  free_pages_.reserve(num_pages_);
+  for (int64_t i = num_pages_ - 1; i >= 0; --i) free_pages_.push_back(i);
+  page_owner_.assign(num_pages_, -1);
+  expecting_.assign(static_cast<size_t>(num_pages_) * P_, 0);
+  if (device_ < 0) return;
+
+  CudaCheck(cudaSetDevice(device_), "cudaSetDevice");
+  int sms = 0;
+  CudaCheck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_), "sm count");
+  num_sms_ = sms;
+  CudaCheck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
+  CudaCheck(cudaEventCreateWithFlags(&internal_ev_, cudaEventDisableTiming), "event");
+  CudaCheck(cudaEventCreateWithFlags(&user_ev_, cudaEventDisableTiming), "event");
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device_) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  const size_t slots = static_cast<size_t>(num_pages_) * P_;
+  CudaCheck(cudaMalloc(&d_pool_, slots * L_ * W_ * 8), "cudaMalloc pool");
+  CudaCheck(cudaMalloc(&d_fill_, slots * L_), "cudaMalloc fill");
+  CudaCheck(cudaMalloc(&d_expecting_, slots), "cudaMalloc expecting");
+  CudaCheck(cudaMalloc(&d_page_window_, sizeof(int32_t) * num_pages_), "cudaMalloc page_window");
+  CudaCheck(cudaMalloc(&d_win_received_, sizeof(unsigned long long) * kMaxWindows), "cudaMalloc");
+  CudaCheck(cudaMalloc(&d_win_layer_rows_, sizeof(uint32_t) * kMaxWindows * L_), "cudaMalloc");
+  CudaCheck(cudaMalloc(&d_fold_sums_, sizeof(uint64_t) * kMaxSeqRows * L_), "cudaMalloc");
+  CudaCheck(cudaMalloc(&d_status_, sizeof(uint32_t)), "cudaMalloc");
+  CudaCheck(cudaMalloc(&d_scratch_, 256), "cudaMalloc");
+  CudaCheck(cudaHostAlloc(&h_pinned_, sizeof(unsigned long long) * kMaxWindows, 0), "pinned");
+  // A fresh pool is zero-filled like the reference's (kv_cache.cc:37).
+  CudaCheck(cudaMemsetAsync(d_pool_, 0, slots * L_ * W_ * 8, stream_), "memset");
+  CudaCheck(cudaMemsetAsync(d_fill_, 0, slots * L_, stream_), "memset");
+  CudaCheck(cudaMemsetAsync(d_expecting_, 0, slots, stream_), "memset");
+  CudaCheck(cudaMemsetAsync(d_page_window_, 0xff, sizeof(int32_t) * num_pages_, stream_), "memset");
+  CudaCheck(cudaMemsetAsync(d_win_received_, 0, sizeof(unsigned long long) * kMaxWindows, stream_),
+            "memset");
+  CudaCheck(cudaMemsetAsync(d_win_layer_rows_, 0, sizeof(uint32_t) * kMaxWindows * L_, stream_),
+            "memset");
+  CudaCheck(cudaMemsetAsync(d_status_, 0, sizeof(uint32_t), stream_), "memset");
+  launches_ += 7;
+  for (int32_t i = kMaxWindows - 1; i >= 0; --i) free_window_ids_.push_back(i);
+  for (int32_t i = kMaxSeqRows - 1; i >= 0; --i) free_fold_rows_.push_back(i);
+  Sync();
+}
+
+ss_cache::~ss_cache() {
+  if (device_ < 0) return;
+  cudaSetDevice(device_);
+  if (stream_) cudaStreamSynchronize(stream_);
+  for (auto& [r, p] : peers_) {
+    for (void* ptr : p.ipc_ptrs) cudaIpcCloseMemHandle(ptr);
+  }
+  cudaFree(d_pool_);
+  cudaFree(d_fill_);
+  cudaFree(d_expecting_);
+  cudaFree(d_page_window_);
+  cudaFree(d_win_received_);
+  cudaFree(d_win_layer_rows_);
+  cudaFree(d_fold_sums_);
+  cudaFree(d_status_);
+  cudaFree(d_scratch_);
+  cudaFreeHost(h_pinned_);
+  cudaEventDestroy(internal_ev_);
+  cudaEventDestroy(user_ev_);
+  cudaStreamDestroy(stream_);
+}
+
+// ---------------------------------------------------------------------------
+// Helpers
+// ---------------------------------------------------------------------------
+Record* ss_cache::MustGet(SeqId seq) {
+  auto it = records_.find(seq);
+  MKV_CHECK(it != records_.end(), kUnknownSequence, "sequence " + std::to_string(seq));
+  return it->second.get();
+}
+
+const Record* ss_cache::MustGet(SeqId seq) const {
+  auto it = records_.find(seq);
+  MKV_CHECK(it != records_.end(), kUnknownSequence, "sequence " + std::to_string(seq));
+  return it->second.get();
+}
+
+// kv_cache.cc:67-77 (through the resolved host page table).
+int32_t ss_cache::Resolve(const Record* rec, int64_t pos) const {
+  MKV_ICHECK(pos >= 0 && pos < rec->alloc_len, "position not allocated");
+  return rec->slots[pos];
+}
+
+// kv_cache.cc:79-84
+int64_t ss_cache::PagesNeeded(const Record* rec, int64_t upto) const {
+  const int64_t idx = upto - rec->fork_len;
+  if (idx <= 0) return 0;
+  const int64_t pages = (idx + P_ - 1) / P_;
+  return std::max<int64_t>(0, pages - static_cast<int64_t>(rec->own_pages.size()));
+}
+
+void ss_cache::RequireDevice(const char* what) const {
+  if (device_ < 0) ThrowStatus(SS_ERR_NO_DEVICE, std::string(what) + " on a host-only cache");
+}
+
+void ss_cache::Sync() { CudaCheck(cudaStreamSynchronize(stream_), "cudaStreamSynchronize"); }
+
+void ss_cache::OrderAfterUser() {
+  if (user_pending_) {
+    CudaCheck(cudaStreamWaitEvent(stream_, user_ev_, 0), "cudaStreamWaitEvent");
+  }
+}
+
+void ss_cache::OrderUser(cudaStream_t s) {
+  CudaCheck(cudaEventRecord(internal_ev_, stream_), "cudaEventRecord");
+  CudaCheck(cudaStreamWaitEvent(s, internal_ev_, 0), "cudaStreamWaitEvent");
+}
+
+void ss_cache::NoteUser(cudaStream_t s) {
+  CudaCheck(cudaEventRecord(user_ev_, s), "cudaEventRecord");
+  user_pending_ = true;
+}
+
+DevBlock ss_cache::DevAlloc(size_t bytes, cudaStream_t s) {
+  DevBlock b;
+  b.bytes = bytes;
+  if (bytes > 0) CudaCheck(cudaMallocAsync(&b.ptr, bytes, s), "cudaMallocAsync");
+  return b;
+}
+
+void ss_cache::DevFree(DevBlock& b, cudaStream_t s) {
+  if (b.ptr) cudaFreeAsync(b.ptr, s);
+  b.ptr = nullptr;
+  b.bytes = 0;
+}
+
+uint64_t* ss_cache::PoolLayer(int32_t layer) const {
+  return d_pool_ + static_cast<int64_t>(layer) * num_pages_ * P_ * W_;
+}
+
+// kv_cache.cc:86-102.  Positions proven full on the host (the caller's
+// `known_full_until`, or a forward pass that just covered them) are
+// skipped; a position that no kernel can have written (beyond every
+// forward pass and outside any receive window) stops the walk; anything
+// else is decided by a device scan of the fill bytes.
+void ss_cache::AdvanceCommitted(Record* rec, int64_t known_full_until) {
+  const int64_t limit = std::min<int64_t>(rec->alloc_len, rec->tokens.size());
+  int64_t pos = std::max(rec->committed_hint, rec->fork_len);
+  if (known_full_until > pos) pos = std::min(known_full_until, limit);
+  if (pos < limit && device_ >= 0) {
+    const bool in_window = rec->window && pos >= rec->window->begin && pos < rec->window->end;
+    if (pos < rec->touched_end || in_window) pos = DeviceFirstNonFull(rec, pos, limit);
+  }
+  rec->committed_hint = std::max(rec->committed_hint, pos);
+}
+
+int64_t ss_cache::DeviceFirstNonFull(const Record* rec, int64_t from, int64_t to) {
+  if (from >= to) return to;
+  OrderAfterUser();
+  const int64_t n = to - from;
+  DevBlock b = DevAlloc(sizeof(int32_t) * n, stream_);
+  CudaCheck(cudaMemcpyAsync(b.ptr, rec->slots.data() + from, sizeof(int32_t) * n,
+                            cudaMemcpyHostToDevice, stream_),
+            "H2D slots");
+  launch_first_nonfull(d_fill_, num_pages_ * P_, L_, static_cast<int32_t*>(b.ptr), n, d_scratch_,
+                       stream_, num_sms_);
+  launches_ += 1;
+  CudaCheck(cudaMemcpyAsync(h_pinned_, d_scratch_, sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, stream_),
+            "D2H scan");
+  DevFree(b, stream_);
+  Sync();
+  const unsigned long long r = h_pinned_[0];
+  return r >= static_cast<unsigned long long>(n) ? to : from + static_cast<int64_t>(r);
+}
+
+// Positions [begin, end) of `rec` must be non-Empty at `layer`
+// (kv_cache.cc:340-342, 358-361, 379-381).  Positions below the committed
+// frontier, or written by `plan` on this layer, are full by construction;
+// the rest are checked on the device.
+void ss_cache::CheckFilled(const Record* rec, int64_t begin, int64_t end, int32_t layer,
+                           const char* what, const ss_plan* plan) {
+  std::vector<int32_t> unproven;
+  for (int64_t pos = std::max(begin, rec->committed_hint); pos < end; ++pos) {
+    bool written = false;
+    if (plan) {
+      for (const auto& e : plan->entries) {
+        if (e.seq == rec->id && pos >= e.begin && pos < e.end) {
+          written = true;
+          break;
+        }
+      }
+    }
+    if (!written) unproven.push_back(Resolve(rec, pos));
+  }
+  if (unproven.empty()) return;
+  RequireDevice(what);
+  OrderAfterUser();
+  const int64_t n = static_cast<int64_t>(unproven.size());
+  DevBlock b = DevAlloc(sizeof(int32_t) * n, stream_);
+  CudaCheck(cudaMemsetAsync(d_status_, 0, sizeof(uint32_t), stream_), "memset");
+  CudaCheck(cudaMemcpyAsync(b.ptr, unproven.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice,
+                            stream_),
+            "H2D slots");
+  launch_check_filled(d_fill_ + static_cast<int64_t>(layer) * num_pages_ * P_,
+                      static_cast<int32_t*>(b.ptr), n, d_status_, stream_, num_sms_);
+  launches_ += 2;
+  uint32_t st = 0;
+  CudaCheck(cudaMemcpyAsync(&st, d_status_, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream_),
+            "D2H status");
+  DevFree(b, stream_);
+  Sync();
+  MKV_CHECK((st & kStatusMissingKV) == 0, kMissingKV, what);
+}
+
+// kv_cache.cc:104-110
+void ss_cache::TouchLru(Record* rec) {
+  if (tree_.Contains(rec->id)) {
+    const int64_t n = std::min<int64_t>(rec->committed_hint, rec->tokens.size());
+    if (n > 0) tree_.Insert(std::span<const Token>(rec->tokens.data(), n), rec->id);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Declaration stage
+// ---------------------------------------------------------------------------
+RadixTree::MatchResult ss_cache::MatchPrefixSeq(std::span<const Token> tokens) {
+  return tree_.MatchPrefix(tokens);  // kv_cache.cc:112-118
+}
+
+// kv_cache.cc:120-131
+Record* ss_cache::CreateSequence(SeqId seq, std::vector<Token> tokens) {
+  MKV_CHECK(records_.find(seq) == records_.end(), kDuplicateSequence,
+            "sequence " + std::to_string(seq));
+  auto rec = std::make_unique<Record>();
+  rec->id = seq;
+  rec->tokens = std::move(tokens);
+  rec->prefix_digest = InitialPrefixDigest();
+  if (device_ >= 0) {
+    MKV_ICHECK(!free_fold_rows_.empty(), "too many live sequences");
+    rec->fold_row = free_fold_rows_.back();
+    free_fold_rows_.pop_back();
+    CudaCheck(cudaMemsetAsync(d_fold_sums_ + static_cast<int64_t>(rec->fold_row) * L_, 0,
+                              sizeof(uint64_t) * L_, stream_),
+              "memset fold sums");
+    launches_ += 1;
+  }
+  Record* out = rec.get();
+  records_[seq] = std::move(rec);
+  return out;
+}
+
+// kv_cache.cc:133-166
+Record* ss_cache::ForkSequence(SeqId parent, SeqId child, int64_t fork_len,
+                               std::vector<Token> child_tokens) {
+  Record* p = MustGet(parent);
+  MKV_CHECK(records_.find(child) == records_.end(), kDuplicateSequence,
+            "sequence " + std::to_string(child));
+  AdvanceCommitted(p);
+  MKV_CHECK(fork_len <= p->committed_hint, kForkBeyondCommitted,
+            "fork_len " + std::to_string(fork_len) + " > committed " +
+                std::to_string(p->committed_hint));
+  MKV_CHECK(fork_len >= 0, kInvalidArgument, "negative fork_len");
+  if (child_tokens.empty()) {
+    child_tokens.assign(p->tokens.begin(), p->tokens.begin() + fork_len);
+  } else {
+    MKV_CHECK(static_cast<int64_t>(child_tokens.size()) >= fork_len, kInvalidArgument,
+              "child tokens shorter than fork_len");
+    for (int64_t i = 0; i < fork_len; ++i) {
+      MKV_CHECK(child_tokens[i] == p->tokens[i], kInvalidArgument,
+                "child tokens diverge inside the fork prefix");
+    }
+  }
+  Record* rec = CreateSequence(child, std::move(child_tokens));
+  rec->parent = fork_len > 0 ? parent : -1;
+  rec->fork_len = fork_len;
+  rec->alloc_len = fork_len;
+  rec->committed_hint = fork_len;
+  rec->slots.assign(p->slots.begin(), p->slots.begin() + fork_len);
+  if (rec->parent >= 0) ++p->refcount;
+  TouchLru(p);
+  return rec;
+}
+
+// kv_cache.cc:168-183
+void ss_cache::EnsureAllocated(SeqId seq, int64_t upto) {
+  Record* rec = MustGet(seq);
+  MKV_CHECK(upto <= static_cast<int64_t>(rec->tokens.size()), kInvalidArgument,
+            "allocation beyond known tokens");
+  const int64_t need = PagesNeeded(rec, upto);
+  MKV_CHECK(need <= static_cast<int64_t>(free_pages_.size()), kOutOfPages,
+            std::to_string(need) + " pages needed, " + std::to_string(free_pages_.size()) +
+                " free");
+  for (int64_t i = 0; i < need; ++i) {
+    const int64_t page = free_pages_.back();
+    free_pages_.pop_back();
+    page_owner_[page] = seq;
+    rec->own_pages.push_back(page);
+    for (int32_t s = 0; s < P_; ++s) rec->slots.push_back(static_cast<int32_t>(page * P_ + s));
+  }
+  rec->alloc_len = rec->fork_len + static_cast<int64_t>(rec->own_pages.size()) * P_;
+}
+
+void ss_cache::AppendToken(SeqId seq, Token t) { MustGet(seq)->tokens.push_back(t); }
+
+// kv_cache.cc:187-229
+int64_t ss_cache::PrepRecv(SeqId seq, std::vector<Token> tokens, int64_t end, KVAddr* addr,
+                           int64_t ranges_cap) {
+  MKV_CHECK(!tokens.empty(), kInvalidArgument, "empty prompt");
+  MKV_CHECK(records_.find(seq) == records_.end(), kDuplicateSequence,
+            "sequence " + std::to_string(seq));
+  const int64_t e = ResolveEndIndex(static_cast<int64_t>(tokens.size()), end);
+  const auto match = tree_.MatchPrefix(std::span<const Token>(tokens.data(), e));
+  const int64_t m = match.match_len;
+  // All-or-nothing: fail before any state change when capacity is short.
+  const int64_t pages_needed = (e - m + P_ - 1) / P_;
+  MKV_CHECK(pages_needed <= static_cast<int64_t>(free_pages_.size()), kOutOfPages,
+            std::to_string(pages_needed) + " pages needed, " +
+                std::to_string(free_pages_.size()) + " free");
+  if (pages_needed > ranges_cap) {
+    ThrowStatus(SS_ERR_BUFFER_TOO_SMALL,
+                "address needs " + std::to_string(pages_needed) + " ranges");
+  }
+  Record* rec = m > 0 ? ForkSequence(match.seq, seq, m, std::move(tokens))
+                      : CreateSequence(seq, std::move(tokens));
+  EnsureAllocated(seq, e);
+  *addr = BuildAddr(seq, m, e);
+  {
+    std::lock_guard<std::mutex> lock(recv_mu_);
+    for (int64_t pos = m; pos < e; ++pos) expecting_[Resolve(rec, pos)] = 1;
+    if (e > m) {
+      Window w;
+      w.begin = m;
+      w.end = e;
+      w.expected = (e - m) * L_;
+      rec->window = std::move(w);
+    }
+    if (device_ >= 0) OpenDeviceWindow(rec, m, e);
+  }
+  return m;
+}
+
+// Device half of PrepRecv: reservation bits, page -> window map, counters.
+// Synchronous, so a peer that receives the address sees a ready receiver.
+void ss_cache::OpenDeviceWindow(Record* rec, int64_t m, int64_t e) {
+  if (e <= m) return;
+  MKV_ICHECK(!free_window_ids_.empty(), "too many open receive windows");
+  const int32_t wid = free_window_ids_.back();
+  free_window_ids_.pop_back();
+  rec->window->dev_id = wid;
+  const int64_t n = e - m, np = static_cast<int64_t>(rec->own_pages.size());
+  const size_t off_pages = Align(sizeof(int32_t) * n);
+  std::vector<uint8_t> host(off_pages + sizeof(int64_t) * np);
+  std::memcpy(host.data(), rec->slots.data() + m, sizeof(int32_t) * n);
+  std::memcpy(host.data() + off_pages, rec->own_pages.data(), sizeof(int64_t) * np);
+  OrderAfterUser();
+  DevBlock b = DevAlloc(host.size(), stream_);
+  CudaCheck(cudaMemcpyAsync(b.ptr, host.data(), host.size(), cudaMemcpyHostToDevice, stream_),
+            "H2D window");
+  launch_open_window(d_expecting_, static_cast<int32_t*>(b.ptr), n, d_page_window_,
+                     reinterpret_cast<int64_t*>(static_cast<uint8_t*>(b.ptr) + off_pages), np, wid,
+                     d_win_received_, d_win_layer_rows_, L_, stream_);
+  launches_ += 1;
+  DevFree(b, stream_);
+  Sync();
+}
+
+// kv_cache.cc:231-243
+void ss_cache::MarkSend(SeqId seq, int64_t begin, int64_t end, Rank dest, KVAddr addr,
+                        uint64_t tag) {
+  Record* rec = MustGet(seq);
+  MKV_CHECK(begin >= 0 && end <= static_cast<int64_t>(rec->tokens.size()) && begin <= end,
+            kInvalidArgument, "send range outside sequence");
+  MKV_CHECK(addr.token_count == end - begin, kAddrMismatch,
+            "destination covers " + std::to_string(addr.token_count) + " tokens, range has " +
+                std::to_string(end - begin));
+  MKV_CHECK(addr.token_begin == begin, kAddrMismatch, "destination token_begin mismatch");
+  pending_sends_.push_back({seq, begin, end, dest, std::move(addr), tag});
+}
+
+// kv_cache.cc:245-306
+ss_plan* ss_cache::BeginForward(const ss_batch_entry* batch, int64_t n) {
+  auto plan = std::make_unique<ss_plan>();
+  plan->owner = this;
+  std::set<SeqId> seen;
+  for (int64_t i = 0; i < n; ++i) {
+    const ss_batch_entry& be = batch[i];
+    Record* rec = MustGet(be.seq);
+    MKV_ICHECK(seen.insert(be.seq).second, "sequence batched twice");
+    const int64_t nt = static_cast<int64_t>(rec->tokens.size());
+    MKV_CHECK(be.begin >= 0 && be.begin < be.end && be.end <= nt, kInvalidArgument,
+              "bad forward range");
+    AdvanceCommitted(rec);
+    MKV_CHECK(rec->committed_hint >= be.begin, kMissingKV,
+              "position " + std::to_string(rec->committed_hint) +
+                  " is empty before prefill begin " + std::to_string(be.begin));
+    MKV_ICHECK(rec->alloc_len >= be.end, "forward range not allocated");
+    MKV_ICHECK(rec->fold_frontier <= be.begin, "fold frontier beyond range");
+    MKV_ICHECK(rec->digest_len <= be.begin, "digest beyond range");
+    PlanEntry pe;
+    pe.seq = be.seq;
+    pe.is_decode = be.is_decode != 0;
+    pe.begin = be.begin;
+    pe.end = be.end;
+    pe.fold_from = rec->fold_frontier;
+    pe.slots.assign(rec->slots.begin() + pe.fold_from, rec->slots.begin() + be.end);
+    while (rec->digest_len < be.end) {
+      rec->prefix_digest = fnv_u32(rec->prefix_digest,
+                                   static_cast<uint32_t>(rec->tokens[rec->digest_len]));
+      ++rec->digest_len;
+      if (rec->digest_len > be.begin) pe.digests.push_back(rec->prefix_digest);
+    }
+    pe.tokens.assign(rec->tokens.begin() + be.begin, rec->tokens.begin() + be.end);
+    plan->total_outputs += be.end - be.begin;
+    plan->entries.push_back(std::move(pe));
+  }
+  for (auto it = pending_sends_.begin(); it != pending_sends_.end();) {
+    if (!seen.count(it->seq)) {
+      ++it;
+      continue;
+    }
+    PlanSend ps;
+    ps.seq = it->seq;
+    ps.begin = it->begin;
+    ps.end = it->end;
+    ps.dest = it->dest;
+    ps.dest_addr = std::move(it->addr);
+    ps.user_tag = it->tag;
+    const Record* rec = MustGet(ps.seq);
+    ps.src_slots.reserve(ps.end - ps.begin);
+    for (int64_t pos = ps.begin; pos < ps.end; ++pos) ps.src_slots.push_back(Resolve(rec, pos));
+    plan->sends.push_back(std::move(ps));
+    it = pending_sends_.erase(it);
+  }
+  return plan.release();
+}
+
+void ss_cache::ExpandAddr(const KVAddr& a, std::vector<int32_t>* slots, std::vector<int64_t>* rp,
+                          std::vector<int32_t>* rb, std::vector<int32_t>* rc) const {
+  for (const auto& r : a.ranges) {
+    if (rp) {
+      rp->push_back(r.page_id);
+      rb->push_back(r.slot_begin);
+      rc->push_back(r.slot_count);
+    }
+    for (int32_t s = 0; s < r.slot_count; ++s) {
+      slots->push_back(static_cast<int32_t>(r.page_id * P_ + r.slot_begin + s));
+    }
+  }
+}
+
+// Lays the plan out in one device block: everything all L layers share is
+// uploaded once (kv_cache.h:8-9, "plan once for all layers").
+void ss_cache::PlanToDevice(ss_plan* plan) {
+  if (plan->on_device) return;
+  plan->n_fold = 0;
+  for (const auto& e : plan->entries) plan->n_fold += e.end - e.fold_from;
+  const int64_t nf = plan->n_fold, no = plan->total_outputs;
+  const int64_t ne = static_cast<int64_t>(plan->entries.size());
+  struct SendLayout {
+    size_t src, dst, rpage, rbegin, rcount, verdict, staging;
+    std::vector<int32_t> dst_slots, rb, rc;
+    std::vector<int64_t> rp;
+  };
+  std::vector<SendLayout> sl(plan->sends.size());
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += Align(bytes);
+    return o;
+  };
+  const size_t o_fold = take(sizeof(int32_t) * nf);
+  const size_t o_out = take(sizeof(int32_t) * no);
+  const size_t o_dig = take(sizeof(uint64_t) * no);
+  const size_t o_ent = take(sizeof(FoldEntry) * ne);
+  const size_t upload_end_core = off;
+  for (size_t i = 0; i < plan->sends.size(); ++i) {
+    const PlanSend& s = plan->sends[i];
+    const int64_t n = s.end - s.begin;
+    ExpandAddr(s.dest_addr, &sl[i].dst_slots, &sl[i].rp, &sl[i].rb, &sl[i].rc);
+    const int64_t nr = static_cast<int64_t>(sl[i].rp.size());
+    sl[i].src = take(sizeof(int32_t) * n);
+    sl[i].dst = take(sizeof(int32_t) * sl[i].dst_slots.size());
+    sl[i].rpage = take(sizeof(int64_t) * nr);
+    sl[i].rbegin = take(sizeof(int32_t) * nr);
+    sl[i].rcount = take(sizeof(int32_t) * nr);
+    sl[i].verdict = take(sizeof(int32_t));
+  }
+  const size_t upload_end = off;
+  const size_t o_F = take(sizeof(uint64_t) * nf);
+  const size_t o_hin = take(sizeof(uint64_t) * no);
+  const size_t o_hout = take(sizeof(uint64_t) * no);
+  for (size_t i = 0; i < plan->sends.size(); ++i) {
+    const PlanSend& s = plan->sends[i];
+    sl[i].staging = peers_.count(s.dest) ? SIZE_MAX : take(sizeof(uint64_t) * (s.end - s.begin) * W_);
+  }
+  std::vector<uint8_t> host(upload_end, 0);
+  {
+    int32_t* fold = reinterpret_cast<int32_t*>(host.data() + o_fold);
+    int32_t* outs = reinterpret_cast<int32_t*>(host.data() + o_out);
+    uint64_t* dig = reinterpret_cast<uint64_t*>(host.data() + o_dig);
+    FoldEntry* ent = reinterpret_cast<FoldEntry*>(host.data() + o_ent);
+    int64_t fo = 0, oo = 0;
+    for (int64_t i = 0; i < ne; ++i) {
+      const PlanEntry& e = plan->entries[i];
+      const Record* rec = MustGet(e.seq);
+      const int64_t nfe = e.end - e.fold_from, noe = e.end - e.begin;
+      std::memcpy(fold + fo, e.slots.data(), sizeof(int32_t) * nfe);
+      std::memcpy(outs + oo, e.slots.data() + (e.begin - e.fold_from), sizeof(int32_t) * noe);
+      std::memcpy(dig + oo, e.digests.data(), sizeof(uint64_t) * noe);
+      ent[i] = FoldEntry{fo, nfe, e.begin - e.fold_from, oo, e.fold_from,
+                         d_fold_sums_ + static_cast<int64_t>(rec->fold_row) * L_};
+      fo += nfe;
+      oo += noe;
+    }
+    for (size_t i = 0; i < plan->sends.size(); ++i) {
+      const PlanSend& s = plan->sends[i];
+      std::memcpy(host.data() + sl[i].src, s.src_slots.data(), sizeof(int32_t) * s.src_slots.size());
+      std::memcpy(host.data() + sl[i].dst, sl[i].dst_slots.data(),
+                  sizeof(int32_t) * sl[i].dst_slots.size());
+      std::memcpy(host.data() + sl[i].rpage, sl[i].rp.data(), sizeof(int64_t) * sl[i].rp.size());
+      std::memcpy(host.data() + sl[i].rbegin, sl[i].rb.data(), sizeof(int32_t) * sl[i].rb.size());
+      std::memcpy(host.data() + sl[i].rcount, sl[i].rc.data(), sizeof(int32_t) * sl[i].rc.size());
+    }
+  }
+  (void)upload_end_core;
+  plan->dev = DevAlloc(off, stream_);
+  uint8_t* base = static_cast<uint8_t*>(plan->dev.ptr);
+  if (upload_end > 0) {
+    CudaCheck(cudaMemcpyAsync(base, host.data(), upload_end, cudaMemcpyHostToDevice, stream_),
+              "H2D plan");
+  }
+  plan->d_fold_slots = reinterpret_cast<int32_t*>(base + o_fold);
+  plan->d_out_slots = reinterpret_cast<int32_t*>(base + o_out);
+  plan->d_digests = reinterpret_cast<uint64_t*>(base + o_dig);
+  plan->d_entries = reinterpret_cast<FoldEntry*>(base + o_ent);
+  plan->d_F = reinterpret_cast<uint64_t*>(base + o_F);
+  plan->d_hidden_in = reinterpret_cast<uint64_t*>(base + o_hin);
+  plan->d_hidden_out = reinterpret_cast<uint64_t*>(base + o_hout);
+  plan->dsend.resize(plan->sends.size());
+  for (size_t i = 0; i < plan->sends.size(); ++i) {
+    auto& d = plan->dsend[i];
+    d.src_slots = reinterpret_cast<int32_t*>(base + sl[i].src);
+    d.dst_slots = reinterpret_cast<int32_t*>(base + sl[i].dst);
+    d.range_page = reinterpret_cast<int64_t*>(base + sl[i].rpage);
+    d.range_begin = reinterpret_cast<int32_t*>(base + sl[i].rbegin);
+    d.range_count = reinterpret_cast<int32_t*>(base + sl[i].rcount);
+    d.verdict = reinterpret_cast<int32_t*>(base + sl[i].verdict);
+    d.staging = sl[i].staging == SIZE_MAX ? nullptr : reinterpret_cast<uint64_t*>(base + sl[i].staging);
+  }
+  plan->on_device = true;
+}
+
+void ss_cache::DestroyPlan(ss_plan* plan) {
+  if (device_ >= 0 && (plan->dev.ptr || plan->d_partial)) {
+    cudaSetDevice(device_);
+    OrderAfterUser();
+    DevFree(plan->dev, stream_);
+    if (plan->d_partial) {
+      Sync();
+      cudaFree(plan->d_partial);
+    }
+  }
+  delete plan;
+}
+
+// ---------------------------------------------------------------------------
+// Computation stage
+// ---------------------------------------------------------------------------
+const PeerTarget& ss_cache::PeerFor(Rank dest) const {
+  auto it = peers_.find(dest);
+  if (it == peers_.end()) Throw(kPeerUnreachable, "no peer attached for rank " + std::to_string(dest));
+  return it->second;
+}
+
+void ss_cache::LaunchRemote(const PeerTarget& peer, const int32_t* d_src_slots,
+                            const int32_t* d_dst_slots, const int64_t* d_rpage,
+                            const int32_t* d_rbegin, const int32_t* d_rcount, int64_t n_ranges,
+                            int32_t* d_verdict, int64_t n_rows, int32_t lb, int32_t le,
+                            cudaStream_t s) {
+  ValidateParams v{};
+  v.range_page = d_rpage;
+  v.range_begin = d_rbegin;
+  v.range_count = d_rcount;
+  v.n_ranges = n_ranges;
+  v.page_window = peer.page_window;
+  v.expecting = peer.expecting;
+  v.num_pages = peer.num_pages;
+  v.P = peer.P;
+  v.verdict = d_verdict;
+  v.status = d_status_;
+  launch_validate_remote(v, s);
+  CopyParams c{};
+  const int64_t src_lw = num_pages_ * P_ * W_, dst_lw = peer.num_pages * peer.P * W_;
+  c.src = d_pool_ + lb * src_lw;
+  c.src_layer_words = src_lw;
+  c.src_idx = d_src_slots;
+  c.dst = peer.pool + lb * dst_lw;
+  c.dst_layer_words = dst_lw;
+  c.dst_idx = d_dst_slots;
+  c.dst_fill = peer.fill + lb * peer.num_pages * peer.P;
+  c.dst_fill_layer = peer.num_pages * peer.P;
+  c.fill_value = 2;  // FillState::kReceivedRemote
+  c.n_rows = n_rows;
+  c.layer0 = lb;
+  c.n_layers = le - lb;
+  c.W = W_;
+  c.win_received = peer.win_received;
+  c.win_layer_rows = peer.win_layer_rows;
+  c.win_layers = peer.L;
+  c.verdict = d_verdict;
+  c.status = d_status_;
+  launch_copy_rows(c, s, num_sms_);
+  launches_ += 2;
+}
+
+// kv_cache.cc:308-371 on device.  Hidden buffers are device pointers; the
+// host wrapper (Attention) stages them.
+void ss_cache::AttentionAsync(ss_plan* plan, int32_t layer, const uint64_t* hin, uint64_t* hout,
+                              cudaStream_t s) {
+  RequireDevice("Attention");
+  MKV_CHECK(layer == plan->next_layer && layer < L_, kLayerOrderViolation,
+            "expected layer " + std::to_string(plan->next_layer) + ", got " +
+                std::to_string(layer));
+  OrderAfterUser();
+  PlanToDevice(plan);
+  if (s != stream_) OrderUser(s);
+  uint64_t* pool_l = PoolLayer(layer);
+  uint8_t* fill_l = d_fill_ + static_cast<int64_t>(layer) * num_pages_ * P_;
+  // Hot loop A: KV write for Empty output slots, entry digests, fold + hidden.
+  launch_attn_write_hash(pool_l, fill_l, plan->d_out_slots, plan->d_digests, plan->total_outputs,
+                         layer, W_, s, num_sms_);
+  launch_entry_digest(pool_l, plan->d_fold_slots, plan->n_fold, W_, plan->d_F, s, num_sms_);
+  launch_fold_scan(plan->d_entries, static_cast<int64_t>(plan->entries.size()), plan->d_F, hin,
+                   hout, layer, s);
+  launches_ += 3;
+  for (const auto& e : plan->entries) {
+    Record* rec = MustGet(e.seq);
+    rec->touched_end = std::max(rec->touched_end, e.end);
+    CheckFilled(rec, e.fold_from, e.begin, layer, "fold over empty slot", nullptr);
+    if (layer == L_ - 1) {
+      rec->fold_frontier = e.end;
+      AdvanceCommitted(rec, e.end);
+    }
+  }
+  // Hot loop B: stream this layer's KV of every marked send.
+  for (size_t i = 0; i < plan->sends.size(); ++i) {
+    const PlanSend& snd = plan->sends[i];
+    CheckFilled(MustGet(snd.seq), snd.begin, snd.end, layer, "sending empty slot", plan);
+    const PeerTarget& peer = PeerFor(snd.dest);
+    const auto& d = plan->dsend[i];
+    LaunchRemote(peer, d.src_slots, d.dst_slots, d.range_page, d.range_begin, d.range_count,
+                 static_cast<int64_t>(snd.dest_addr.ranges.size()), d.verdict,
+                 snd.end - snd.begin, layer, layer + 1, s);
+  }
+  if (s != stream_) NoteUser(s);
+  ++plan->next_layer;
+}
+
+// Host-buffer Attention: stages hidden states, sends to attached peers
+// device-direct and everything else through the host sink (the
+// reference's FrameSink path).
+void ss_cache::Attention(ss_plan* plan, int32_t layer, const uint64_t* hidden_in,
+                         uint64_t* hidden_out, int64_t n, ss_frame_sink sink, void* user) {
+  RequireDevice("Attention");
+  MKV_CHECK(layer == plan->next_layer && layer < L_, kLayerOrderViolation,
+            "expected layer " + std::to_string(plan->next_layer) + ", got " +
+                std::to_string(layer));
+  MKV_ICHECK(n == plan->total_outputs, "hidden input size mismatch");
+  OrderAfterUser();
+  PlanToDevice(plan);
+  if (n > 0) {
+    CudaCheck(cudaMemcpyAsync(plan->d_hidden_in, hidden_in, sizeof(uint64_t) * n,
+                              cudaMemcpyHostToDevice, stream_),
+              "H2D hidden");
+  }
+  uint64_t* pool_l = PoolLayer(layer);
+  uint8_t* fill_l = d_fill_ + static_cast<int64_t>(layer) * num_pages_ * P_;
+  launch_attn_write_hash(pool_l, fill_l, plan->d_out_slots, plan->d_digests, plan->total_outputs,
+                         layer, W_, stream_, num_sms_);
+  launch_entry_digest(pool_l, plan->d_fold_slots, plan->n_fold, W_, plan->d_F, stream_, num_sms_);
+  launch_fold_scan(plan->d_entries, static_cast<int64_t>(plan->entries.size()), plan->d_F,
+                   plan->d_hidden_in, plan->d_hidden_out, layer, stream_);
+  launches_ += 3;
+  if (n > 0) {
+    CudaCheck(cudaMemcpyAsync(hidden_out, plan->d_hidden_out, sizeof(uint64_t) * n,
+                              cudaMemcpyDeviceToHost, stream_),
+              "D2H hidden");
+  }
+  for (const auto& e : plan->entries) {
+    Record* rec = MustGet(e.seq);
+    rec->touched_end = std::max(rec->touched_end, e.end);
+    CheckFilled(rec, e.fold_from, e.begin, layer, "fold over empty slot", nullptr);
+    if (layer == L_ - 1) {
+      rec->fold_frontier = e.end;
+      AdvanceCommitted(rec, e.end);
+    }
+  }
+  std::vector<uint64_t> payload;
+  for (size_t i = 0; i < plan->sends.size(); ++i) {
+    const PlanSend& snd = plan->sends[i];
+    CheckFilled(MustGet(snd.seq), snd.begin, snd.end, layer, "sending empty slot", plan);
+    const auto& d = plan->dsend[i];
+    const int64_t rows = snd.end - snd.begin;
+    auto pit = peers_.find(snd.dest);
+    if (pit != peers_.end()) {
+      LaunchRemote(pit->second, d.src_slots, d.dst_slots, d.range_page, d.range_begin,
+                   d.range_count, static_cast<int64_t>(snd.dest_addr.ranges.size()), d.verdict,
+                   rows, layer, layer + 1, stream_);
+      continue;
+    }
+    if (!sink) continue;
+    // Gather this layer's rows in token order, then hand them to the sink.
+    CopyParams c{};
+    c.src = pool_l;
+    c.src_idx = d.src_slots;
+    c.dst = d.staging;
+    c.n_rows = rows;
+    c.layer0 = layer;
+    c.n_layers = 1;
+    c.W = W_;
+    launch_copy_rows(c, stream_, num_sms_);
+    launches_ += 1;
+    payload.resize(static_cast<size_t>(rows) * W_);
+    if (rows > 0) {
+      CudaCheck(cudaMemcpyAsync(payload.data(), d.staging, sizeof(uint64_t) * rows * W_,
+                                cudaMemcpyDeviceToHost, stream_),
+                "D2H payload");
+    }
+    Sync();
+    std::vector<ss_slot_range> rr;
+    for (const auto& r : snd.dest_addr.ranges) rr.push_back({r.page_id, r.slot_begin, r.slot_count});
+    ss_addr a{snd.dest_addr.token_begin, snd.dest_addr.token_count,
+              static_cast<int64_t>(rr.size()), rr.data(), static_cast<int64_t>(rr.size())};
+    sink(user, layer, snd.seq, snd.begin, snd.end, snd.dest, &a, snd.user_tag, payload.data(),
+         static_cast<int64_t>(payload.size()));
+  }
+  Sync();
+  ++plan->next_layer;
+}
+
+// kv_cache.cc:373-387 into device memory.
+void ss_cache::GatherRange(SeqId seq, int64_t begin, int64_t end, int32_t layer, uint64_t* out,
+                           cudaStream_t s) {
+  RequireDevice("GatherRange");
+  const Record* rec = MustGet(seq);
+  MKV_CHECK(layer >= 0 && layer < L_, kInvalidArgument, "layer out of range");
+  MKV_CHECK(begin >= 0 && begin <= end, kInvalidArgument, "bad gather range");
+  for (int64_t pos = begin; pos < end; ++pos) Resolve(rec, pos);
+  CheckFilled(rec, begin, end, layer, "gather over empty slot", nullptr);
+  const int64_t n = end - begin;
+  if (n == 0) return;
+  OrderAfterUser();
+  if (s != stream_) OrderUser(s);
+  DevBlock b = DevAlloc(sizeof(int32_t) * n, s);
+  CudaCheck(cudaMemcpyAsync(b.ptr, rec->slots.data() + begin, sizeof(int32_t) * n,
+                            cudaMemcpyHostToDevice, s),
+            "H2D slots");
+  CopyParams c{};
+  c.src = PoolLayer(layer);
+  c.src_idx = static_cast<int32_t*>(b.ptr);
+  c.dst = out;
+  c.n_rows = n;
+  c.layer0 = layer;
+  c.n_layers = 1;
+  c.W = W_;
+  launch_copy_rows(c, s, num_sms_);
+  launches_ += 1;
+  DevFree(b, s);
+  if (s != stream_) NoteUser(s);
+}
+
+// kv_cache.cc:389-407
+KVAddr ss_cache::BuildAddr(SeqId seq, int64_t begin, int64_t end) {
+  const Record* rec = MustGet(seq);
+  MKV_CHECK(begin >= rec->fork_len, kInvalidArgument, "address must cover own slots only");
+  KVAddr addr;
+  addr.token_begin = begin;
+  addr.token_count = end - begin;
+  for (int64_t pos = begin; pos < end; ++pos) {
+    const int32_t slot = Resolve(rec, pos);
+    const int64_t page = slot / P_;
+    const int32_t s = slot % P_;
+    if (!addr.ranges.empty() && addr.ranges.back().page_id == page &&
+        addr.ranges.back().slot_begin + addr.ranges.back().slot_count == s) {
+      ++addr.ranges.back().slot_count;
+    } else {
+      addr.ranges.push_back({page, s, 1});
+    }
+  }
+  addr.Validate();
+  return addr;
+}
+
+// KV append from the producing layer's dense K||V rows (write rule of
+// kv_cache.cc:328-334).
+void ss_cache::AppendRows(ss_plan* plan, int32_t layer, const void* rows, cudaStream_t s) {
+  RequireDevice("AppendRows");
+  MKV_CHECK(layer >= 0 && layer < L_, kInvalidArgument, "layer out of range");
+  OrderAfterUser();
+  PlanToDevice(plan);
+  if (s != stream_) OrderUser(s);
+  CopyParams c{};
+  c.src = static_cast<const uint64_t*>(rows);
+  c.dst = PoolLayer(layer);
+  c.dst_idx = plan->d_out_slots;
+  c.dst_fill = d_fill_ + static_cast<int64_t>(layer) * num_pages_ * P_;
+  c.fill_value = 1;  // FillState::kComputedLocal
+  c.n_rows = plan->total_outputs;
+  c.layer0 = layer;
+  c.n_layers = 1;
+  c.W = W_;
+  launch_copy_rows(c, s, num_sms_);
+  launches_ += 1;
+  for (const auto& e : plan->entries) {
+    Record* rec = MustGet(e.seq);
+    rec->touched_end = std::max(rec->touched_end, e.end);
+  }
+  if (s != stream_) NoteUser(s);
+}
+
+// ---------------------------------------------------------------------------
+// Transfer agent
+// ---------------------------------------------------------------------------
+// kv_cache.cc:409-463.  Validation, dedupe and window accounting are the
+// reference's, on the host; the scatter of Empty slots runs on the device.
+int ss_cache::ApplyRemoteWrite(const KVAddr& addr, int32_t layer, const uint64_t* payload,
+                               int64_t n_words, bool on_device, uint64_t tag, cudaStream_t s) {
+  MKV_CHECK(n_words == addr.token_count * W_, kInvalidArgument, "payload size mismatch");
+  RequireDevice("ApplyRemoteWrite");
+  MKV_CHECK(layer >= 0 && layer < L_, kInvalidArgument, "layer out of range");
+  std::lock_guard<std::mutex> lock(recv_mu_);
+  SeqId owner = -1;
+  for (const auto& r : addr.ranges) {
+    if (r.page_id < 0 || r.page_id >= num_pages_) return SS_APPLY_UNKNOWN_ADDRESS;
+    const SeqId po = page_owner_[r.page_id];
+    if (po < 0) return SS_APPLY_UNKNOWN_ADDRESS;
+    if (owner == -1) owner = po;
+    if (po != owner) return SS_APPLY_UNKNOWN_ADDRESS;
+    for (int32_t sl = r.slot_begin; sl < r.slot_begin + r.slot_count; ++sl) {
+      if (sl < 0 || sl >= P_ || !expecting_[r.page_id * P_ + sl]) return SS_APPLY_UNKNOWN_ADDRESS;
+    }
+  }
+  auto it = records_.find(owner);
+  if (it == records_.end() || !it->second->window.has_value()) return SS_APPLY_UNKNOWN_ADDRESS;
+  Record* rec = it->second.get();
+  Window& win = *rec->window;
+  if (!win.applied.insert({tag, layer, addr.token_begin}).second) return SS_APPLY_DUPLICATE;
+
+  std::vector<int32_t> dst;
+  ExpandAddr(addr, &dst, nullptr, nullptr, nullptr);
+  const int64_t n = static_cast<int64_t>(dst.size());
+  if (n > 0) {
+    cudaStream_t st = s ? s : stream_;
+    OrderAfterUser();
+    if (st != stream_) OrderUser(st);
+    const size_t o_pay = Align(sizeof(int32_t) * n);
+    DevBlock b = DevAlloc(o_pay + (on_device ? 0 : sizeof(uint64_t) * n_words), st);
+    uint8_t* base = static_cast<uint8_t*>(b.ptr);
+    CudaCheck(cudaMemcpyAsync(base, dst.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st),
+              "H2D slots");
+    const uint64_t* src = payload;
+    if (!on_device) {
+      CudaCheck(cudaMemcpyAsync(base + o_pay, payload, sizeof(uint64_t) * n_words,
+                                cudaMemcpyHostToDevice, st),
+                "H2D payload");
+      src = reinterpret_cast<const uint64_t*>(base + o_pay);
+    }
+    CopyParams c{};
+    c.src = src;
+    c.dst = PoolLayer(layer);
+    c.dst_idx = reinterpret_cast<int32_t*>(base);
+    c.dst_fill = d_fill_ + static_cast<int64_t>(layer) * num_pages_ * P_;
+    c.fill_value = 2;  // FillState::kReceivedRemote
+    c.n_rows = n;
+    c.layer0 = layer;
+    c.n_layers = 1;
+    c.W = W_;
+    launch_copy_rows(c, st, num_sms_);
+    launches_ += 1;
+    DevFree(b, st);
+    if (st == stream_) {
+      Sync();
+    } else {
+      NoteUser(st);
+    }
+  }
+  // Every addressed slot counts, filled or not (kv_cache.cc:452-456).
+  win.received += n;
+  if (!win.complete && win.received + static_cast<int64_t>(win.dev_received) >= win.expected) {
+    win.complete = true;
+    completed_windows_.push_back(owner);
+  }
+  return SS_APPLY_OK;
+}
+
+// Reads the device counters of windows that peers fill device-direct.
+void ss_cache::PollDeviceWindows() {
+  if (device_ < 0) return;
+  std::vector<Record*> open;
+  {
+    std::lock_guard<std::mutex> lock(recv_mu_);
+    for (auto& [id, rec] : records_) {
+      if (rec->window && !rec->window->complete && rec->window->dev_id >= 0) open.push_back(rec.get());
+    }
+  }
+  if (open.empty()) return;
+  for (size_t i = 0; i < open.size(); ++i) {
+    CudaCheck(cudaMemcpyAsync(h_pinned_ + i, d_win_received_ + open[i]->window->dev_id,
+                              sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream_),
+              "D2H window");
+  }
+  Sync();
+  std::lock_guard<std::mutex> lock(recv_mu_);
+  for (size_t i = 0; i < open.size(); ++i) {
+    Window& w = *open[i]->window;
+    w.dev_received = h_pinned_[i];
+    if (!w.complete && w.received + static_cast<int64_t>(w.dev_received) >= w.expected) {
+      w.complete = true;
+      completed_windows_.push_back(open[i]->id);
+    }
+  }
+}
+
+// kv_cache.cc:465-480
+std::vector<SeqId> ss_cache::DrainReceiveCompletions() {
+  PollDeviceWindows();
+  std::vector<SeqId> done;
+  {
+    std::lock_guard<std::mutex> lock(recv_mu_);
+    done.swap(completed_windows_);
+  }
+  for (SeqId seq : done) {
+    auto it = records_.find(seq);
+    if (it == records_.end()) continue;
+    Record* rec = it->second.get();
+    AdvanceCommitted(rec);
+    rec->finished = true;
+    CommitToTree(seq);
+  }
+  return done;
+}
+
+// DirectSend: GatherRange + ApplyRemoteWrite per layer, fused into one
+// launch that stores the sender's rows straight into the receiver's pages.
+void ss_cache::DirectSend(SeqId seq, int64_t begin, int64_t end, Rank dest, const KVAddr& addr,
+                          uint64_t tag, int32_t lb, int32_t le, cudaStream_t s) {
+  (void)tag;
+  RequireDevice("DirectSend");
+  Record* rec = MustGet(seq);
+  MKV_CHECK(begin >= 0 && end <= static_cast<int64_t>(rec->tokens.size()) && begin <= end,
+            kInvalidArgument, "send range outside sequence");
+  MKV_CHECK(addr.token_count == end - begin, kAddrMismatch,
+            "destination covers " + std::to_string(addr.token_count) + " tokens, range has " +
+                std::to_string(end - begin));
+  MKV_CHECK(addr.token_begin == begin, kAddrMismatch, "destination token_begin mismatch");
+  MKV_CHECK(lb >= 0 && lb <= le && le <= L_, kInvalidArgument, "bad layer range");
+  const PeerTarget& peer = PeerFor(dest);
+  const int64_t n = end - begin;
+  for (int64_t pos = begin; pos < end; ++pos) Resolve(rec, pos);
+  if (end > rec->committed_hint) AdvanceCommitted(rec);
+  for (int32_t l = lb; l < le && end > rec->committed_hint; ++l) {
+    CheckFilled(rec, begin, end, l, "gather over empty slot", nullptr);
+  }
+  if (lb == le) return;
+  std::vector<int32_t> dst;
+  std::vector<int64_t> rp;
+  std::vector<int32_t> rb, rc;
+  ExpandAddr(addr, &dst, &rp, &rb, &rc);
+  const int64_t nr = static_cast<int64_t>(rp.size());
+  const size_t o_src = 0, o_dst = Align(sizeof(int32_t) * n);
+  const size_t o_rp = o_dst + Align(sizeof(int32_t) * dst.size());
+  const size_t o_rb = o_rp + Align(sizeof(int64_t) * nr);
+  const size_t o_rc = o_rb + Align(sizeof(int32_t) * nr);
+  const size_t o_v = o_rc + Align(sizeof(int32_t) * nr);
+  const size_t total = o_v + Align(sizeof(int32_t));
+  std::vector<uint8_t> host(total, 0);
+  std::memcpy(host.data() + o_src, rec->slots.data() + begin, sizeof(int32_t) * n);
+  std::memcpy(host.data() + o_dst, dst.data(), sizeof(int32_t) * dst.size());
+  std::memcpy(host.data() + o_rp, rp.data(), sizeof(int64_t) * nr);
+  std::memcpy(host.data() + o_rb, rb.data(), sizeof(int32_t) * nr);
+  std::memcpy(host.data() + o_rc, rc.data(), sizeof(int32_t) * nr);
+  OrderAfterUser();
+  if (s != stream_) OrderUser(s);
+  DevBlock b = DevAlloc(total, s);
+  uint8_t* base = static_cast<uint8_t*>(b.ptr);
+  CudaCheck(cudaMemcpyAsync(base, host.data(), total, cudaMemcpyHostToDevice, s), "H2D send");
+  LaunchRemote(peer, reinterpret_cast<int32_t*>(base + o_src), reinterpret_cast<int32_t*>(base + o_dst),
+               reinterpret_cast<int64_t*>(base + o_rp), reinterpret_cast<int32_t*>(base + o_rb),
+               reinterpret_cast<int32_t*>(base + o_rc), nr, reinterpret_cast<int32_t*>(base + o_v),
+               n, lb, le, s);
+  DevFree(b, s);
+  if (s != stream_) NoteUser(s);
+}
+
+// ---------------------------------------------------------------------------
+// Lifecycle
+// ---------------------------------------------------------------------------
+// kv_cache.cc:484-490
+void ss_cache::CommitToTree(SeqId seq) {
+  Record* rec = MustGet(seq);
+  AdvanceCommitted(rec);
+  const int64_t n = std::min<int64_t>(rec->committed_hint, rec->tokens.size());
+  if (n <= 0) return;
+  tree_.Insert(std::span<const Token>(rec->tokens.data(), n), seq);
+}
+
+// kv_cache.cc:492-518
+void ss_cache::FreeSequence(SeqId seq) {
+  Record* rec = MustGet(seq);
+  MKV_CHECK(rec->refcount == 0, kInternal, "freeing a sequence with live children");
+  {
+    std::lock_guard<std::mutex> lock(recv_mu_);
+    if (rec->window && rec->window->dev_id >= 0) free_window_ids_.push_back(rec->window->dev_id);
+    rec->window.reset();
+    for (int64_t page : rec->own_pages) {
+      page_owner_[page] = -1;
+      std::fill(expecting_.begin() + page * P_, expecting_.begin() + (page + 1) * P_, 0);
+      free_pages_.push_back(page);
+    }
+  }
+  if (device_ >= 0) {
+    if (!rec->own_pages.empty()) {
+      OrderAfterUser();
+      const int64_t np = static_cast<int64_t>(rec->own_pages.size());
+      DevBlock b = DevAlloc(sizeof(int64_t) * np, stream_);
+      CudaCheck(cudaMemcpyAsync(b.ptr, rec->own_pages.data(), sizeof(int64_t) * np,
+                                cudaMemcpyHostToDevice, stream_),
+                "H2D pages");
+      launch_reset_pages(d_fill_, d_expecting_, d_page_window_, static_cast<int64_t*>(b.ptr), np,
+                         L_, num_pages_, P_, stream_);
+      launches_ += 1;
+      DevFree(b, stream_);
+      Sync();
+    }
+    if (rec->fold_row >= 0) free_fold_rows_.push_back(rec->fold_row);
+  }
+  if (rec->parent >= 0) {
+    auto it = records_.find(rec->parent);
+    if (it != records_.end()) --it->second->refcount;
+  }
+  for (auto it = pending_sends_.begin(); it != pending_sends_.end();) {
+    it = it->seq == seq ? pending_sends_.erase(it) : std::next(it);
+  }
+  tree_.Remove(seq);
+  records_.erase(seq);
+}
+
+// kv_cache.cc:520-546
+int64_t ss_cache::Evict(int64_t bytes_needed) {
+  if (bytes_needed <= 0) return 0;
+  int64_t freed_tokens = 0;
+  auto satisfied = [&] {
+    return static_cast<int64_t>(free_pages_.size()) * BytesPerPage() >= bytes_needed;
+  };
+  while (!satisfied()) {
+    SeqId victim = -1;
+    for (SeqId seq : tree_.SequencesByLru()) {
+      auto it = records_.find(seq);
+      if (it == records_.end()) continue;
+      const Record* rec = it->second.get();
+      if (!rec->finished || rec->refcount != 0) continue;
+      if (rec->own_pages.empty()) continue;
+      if (tree_.HasPinnedNode(seq)) continue;
+      victim = seq;
+      break;
+    }
+    MKV_CHECK(victim >= 0, kCannotEvict, "all remaining sequences are pinned or live");
+    const Record* rec = records_.at(victim).get();
+    freed_tokens += std::max<int64_t>(
+        0, std::min<int64_t>(rec->tokens.size(), rec->alloc_len) - rec->fork_len);
+    FreeSequence(victim);
+  }
+  return freed_tokens;
+}
+
+// ---------------------------------------------------------------------------
+// Queries
+// ---------------------------------------------------------------------------
+int64_t ss_cache::Committed(SeqId seq) {
+  Record* rec = MustGet(seq);
+  AdvanceCommitted(rec);
+  return rec->committed_hint;
+}
+
+void ss_cache::ReadEntryWords(SeqId seq, int64_t pos, int32_t layer, uint64_t* out) {
+  RequireDevice("ReadEntryWords");
+  const Record* rec = MustGet(seq);
+  MKV_CHECK(layer >= 0 && layer < L_, kInvalidArgument, "layer out of range");
+  const int32_t slot = Resolve(rec, pos);
+  OrderAfterUser();
+  CudaCheck(cudaMemcpyAsync(out, PoolLayer(layer) + static_cast<int64_t>(slot) * W_,
+                            sizeof(uint64_t) * W_, cudaMemcpyDeviceToHost, stream_),
+            "D2H entry");
+  Sync();
+}
+
+int32_t ss_cache::FillOf(SeqId seq, int64_t pos, int32_t layer) {
+  RequireDevice("FillOf");
+  const Record* rec = MustGet(seq);
+  MKV_CHECK(layer >= 0 && layer < L_, kInvalidArgument, "layer out of range");
+  const int32_t slot = Resolve(rec, pos);
+  uint8_t v = 0;
+  OrderAfterUser();
+  CudaCheck(cudaMemcpyAsync(&v, d_fill_ + static_cast<int64_t>(layer) * num_pages_ * P_ + slot, 1,
+                            cudaMemcpyDeviceToHost, stream_),
+            "D2H fill");
+  Sync();
+  return v;
+}
+
+std::vector<SeqId> ss_cache::SequenceIds() const {
+  std::vector<SeqId> out;
+  out.reserve(records_.size());
+  for (const auto& [id, rec] : records_) out.push_back(id);
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+// Peers
+// ---------------------------------------------------------------------------
+void ss_cache::AttachPeer(Rank dest, ss_cache* peer) {
+  RequireDevice("AttachPeer");
+  MKV_CHECK(peer != nullptr && peer->device_ >= 0, kInvalidArgument, "peer has no device");
+  MKV_CHECK(peer->L_ == L_ && peer->W_ == W_, kInvalidArgument, "peer geometry mismatch");
+  if (peer->device_ != device_) {
+    int ok = 0;
+    CudaCheck(cudaDeviceCanAccessPeer(&ok, device_, peer->device_), "cudaDeviceCanAccessPeer");
+    MKV_CHECK(ok, kPeerUnreachable, "no peer access between devices");
+    cudaSetDevice(device_);
+    cudaError_t e = cudaDeviceEnablePeerAccess(peer->device_, 0);
+    if (e != cudaErrorPeerAccessAlreadyEnabled) CudaCheck(e, "cudaDeviceEnablePeerAccess");
+    cudaGetLastError();
+  }
+  PeerTarget t;
+  t.pool = peer->d_pool_;
+  t.fill = peer->d_fill_;
+  t.expecting = peer->d_expecting_;
+  t.page_window = peer->d_page_window_;
+  t.win_received = peer->d_win_received_;
+  t.win_layer_rows = peer->d_win_layer_rows_;
+  t.num_pages = peer->num_pages_;
+  t.P = peer->P_;
+  t.L = peer->L_;
+  t.W = peer->W_;
+  t.device = peer->device_;
+  DetachPeer(dest);
+  peers_[dest] = t;
+}
+
+namespace {
+struct IpcBlob {
+  uint32_t magic;
+  uint32_t version;
+  int64_t num_pages;
+  int32_t P, L, W, device;
+  cudaIpcMemHandle_t h[6];
+};
+static_assert(sizeof(IpcBlob) <= SS_IPC_HANDLE_BYTES, "ipc blob too large");
+}  // namespace
+
+void ss_cache::ExportIpc(ss_ipc_handle* out) {
+  RequireDevice("ExportIpc");
+  IpcBlob b{};
+  b.magic = kIpcMagic;
+  b.version = SS_ABI_VERSION;
+  b.num_pages = num_pages_;
+  b.P = P_;
+  b.L = L_;
+  b.W = W_;
+  b.device = device_;
+  void* ptrs[6] = {d_pool_, d_fill_, d_expecting_, d_page_window_, d_win_received_,
+                   d_win_layer_rows_};
+  for (int i = 0; i < 6; ++i) CudaCheck(cudaIpcGetMemHandle(&b.h[i], ptrs[i]), "cudaIpcGetMemHandle");
+  std::memset(out->bytes, 0, sizeof(out->bytes));
+  std::memcpy(out->bytes, &b, sizeof(b));
+}
+
+void ss_cache::ImportIpc(Rank dest, const ss_ipc_handle* h) {
+  RequireDevice("ImportIpc");
+  IpcBlob b;
+  std::memcpy(&b, h->bytes, sizeof(b));
+  MKV_CHECK(b.magic == kIpcMagic && b.version == SS_ABI_VERSION, kInvalidArgument,
+            "not a microkv IPC handle");
+  MKV_CHECK(b.L == L_ && b.W == W_, kInvalidArgument, "peer geometry mismatch");
+  PeerTarget t;
+  void* ptrs[6] = {};
+  CudaCheck(cudaSetDevice(device_), "cudaSetDevice");
+  for (int i = 0; i < 6; ++i) {
+    cudaError_t e = cudaIpcOpenMemHandle(&ptrs[i], b.h[i], cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      for (int j = 0; j < i; ++j) cudaIpcCloseMemHandle(ptrs[j]);
+      CudaCheck(e, "cudaIpcOpenMemHandle");
+    }
+    t.ipc_ptrs.push_back(ptrs[i]);
+  }
+  t.pool = static_cast<uint64_t*>(ptrs[0]);
+  t.fill = static_cast<uint8_t*>(ptrs[1]);
+  t.expecting = static_cast<uint8_t*>(ptrs[2]);
+  t.page_window = static_cast<int32_t*>(ptrs[3]);
+  t.win_received = static_cast<unsigned long long*>(ptrs[4]);
+  t.win_layer_rows = static_cast<uint32_t*>(ptrs[5]);
+  t.num_pages = b.num_pages;
+  t.P = b.P;
+  t.L = b.L;
+  t.W = b.W;
+  t.device = b.device;
+  t.ipc = true;
+  DetachPeer(dest);
+  peers_[dest] = t;
+}
+
+void ss_cache::DetachPeer(Rank dest) {
+  auto it = peers_.find(dest);
+  if (it == peers_.end()) return;
+  if (device_ >= 0) Sync();
+  for (void* p : it->second.ipc_ptrs) cudaIpcCloseMemHandle(p);
+  peers_.erase(it);
+}
+
+void ss_cache::Synchronize() {
+  if (device_ < 0) return;
+  Sync();
+  if (user_pending_) CudaCheck(cudaEventSynchronize(user_ev_), "cudaEventSynchronize");
+  uint32_t st = 0;
+  CudaCheck(cudaMemcpy(&st, d_status_, sizeof(uint32_t), cudaMemcpyDeviceToHost), "D2H status");
+  if (st & kStatusUnknownAddress) {
+    CudaCheck(cudaMemset(d_status_, 0, sizeof(uint32_t)), "memset");
+    Throw(kUnknownAddress, "a device-direct remote write was rejected by the receiver");
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Hash model scalars (hash_model.cc:27, 63-68, 83-86)
+// ---------------------------------------------------------------------------
+uint64_t ss_cache::InitialPrefixDigest() const { return fnv_u64(seed_state_, kTagPrefix); }
+uint64_t ss_cache::Embed(Token t, int64_t pos) const { return embed(seed_state_, t, pos); }
+mkv::Token ss_cache::SampleToken(uint64_t h) const { return sample_token(h, vocab_); }
+
+// ---------------------------------------------------------------------------
+// Decode attention plan: per-position slot map of each context, uploaded
+// once and read by every layer's launch.
+// ---------------------------------------------------------------------------
+ss_plan* ss_cache::BeginDecode(const int64_t* seqs, const int64_t* ctx_lens, int64_t batch) {
+  RequireDevice("BeginDecode");
+  MKV_CHECK(batch >= 1, kInvalidArgument, "empty decode batch");
+  std::vector<int64_t> off(batch + 1, 0);
+  std::vector<int32_t> len(batch);
+  int64_t max_ctx = 0;
+  for (int64_t b = 0; b < batch; ++b) {
+    Record* rec = MustGet(seqs[b]);
+    const int64_t n = ctx_lens[b];
+    MKV_CHECK(n >= 1 && n <= rec->alloc_len, kInvalidArgument, "bad decode context length");
+    if (n > rec->committed_hint) AdvanceCommitted(rec);
+    MKV_CHECK(rec->committed_hint >= n, kMissingKV,
+              "decode context " + std::to_string(n) + " beyond committed " +
+                  std::to_string(rec->committed_hint));
+    len[b] = static_cast<int32_t>(n);
+    off[b + 1] = off[b] + n;
+    max_ctx = std::max(max_ctx, n);
+  }
+  const size_t o_slots = 0, o_off = Align(sizeof(int32_t) * off[batch]);
+  const size_t o_len = o_off + Align(sizeof(int64_t) * (batch + 1));
+  const size_t total = o_len + Align(sizeof(int32_t) * batch);
+  std::vector<uint8_t> host(total, 0);
+  for (int64_t b = 0; b < batch; ++b) {
+    const Record* rec = MustGet(seqs[b]);
+    std::memcpy(host.data() + o_slots + sizeof(int32_t) * off[b], rec->slots.data(),
+                sizeof(int32_t) * len[b]);
+  }
+  std::memcpy(host.data() + o_off, off.data(), sizeof(int64_t) * (batch + 1));
+  std::memcpy(host.data() + o_len, len.data(), sizeof(int32_t) * batch);
+  auto plan = std::make_unique<ss_plan>();
+  plan->owner = this;
+  plan->is_decode_plan = true;
+  plan->batch = batch;
+  plan->max_ctx = max_ctx;
+  OrderAfterUser();
+  plan->dev = DevAlloc(total, stream_);
+  uint8_t* base = static_cast<uint8_t*>(plan->dev.ptr);
+  CudaCheck(cudaMemcpyAsync(base, host.data(), total, cudaMemcpyHostToDevice, stream_), "H2D ctx");
+  plan->d_ctx_slots = reinterpret_cast<int32_t*>(base + o_slots);
+  plan->d_ctx_off = reinterpret_cast<int64_t*>(base + o_off);
+  plan->d_ctx_len = reinterpret_cast<int32_t*>(base + o_len);
+  plan->on_device = true;
+  Sync();
+  return plan.release();
+}
+
+void ss_cache::DecodeAttention(ss_plan* plan, int32_t layer, int32_t hq, int32_t hkv, int32_t hd,
+                               float scale, const void* q, void* out, cudaStream_t s) {
+  RequireDevice("DecodeAttention");
+  MKV_CHECK(plan->is_decode_plan, kInvalidArgument, "not a decode plan");
+  MKV_CHECK(layer >= 0 && layer < L_, kInvalidArgument, "layer out of range");
+  MKV_CHECK(hkv >= 1 && hq % hkv == 0 && hq / hkv <= 16, kInvalidArgument,
+            "num_q_heads must be a multiple of num_kv_heads with group <= 16");
+  MKV_CHECK(hd == 64 || hd == 128, kInvalidArgument, "head_dim must be 64 or 128");
+  MKV_CHECK(static_cast<int64_t>(W_) * 8 == 4LL * hkv * hd, kInvalidArgument,
+            "entry width must equal K||V bf16 bytes (dim * 8 == 4 * num_kv_heads * head_dim)");
+  if (plan->num_splits == 0) {
+    const int64_t ctas = plan->batch * hkv;
+    int64_t target = static_cast<int64_t>(num_sms_) * 3 * 2;
+    int64_t splits = (target + ctas - 1) / ctas;
+    splits = std::max<int64_t>(1, std::min<int64_t>(splits, (plan->max_ctx + 63) / 64));
+    plan->num_splits = static_cast<int32_t>(splits);
+    const int64_t heads = plan->batch * hq;
+    float* po = nullptr;
+    CudaCheck(cudaMalloc(&po, sizeof(float) * heads * splits * (hd + 2)), "cudaMalloc partials");
+    plan->d_partial = po;
+    plan->d_partial_ml = po + heads * splits * hd;
+  }
+  OrderAfterUser();
+  if (s != stream_) OrderUser(s);
+  const bool ok = launch_decode_attn(PoolLayer(layer), static_cast<int64_t>(W_) * 4,
+                                     plan->d_ctx_slots, plan->d_ctx_off, plan->d_ctx_len, q,
+                                     static_cast<int>(plan->batch), hq, hkv, hd, scale,
+                                     plan->num_splits, plan->d_partial, plan->d_partial_ml, out, s);
+  MKV_CHECK(ok, kInvalidArgument, "unsupported head_dim");
+  launches_ += 2;
+  if (s != stream_) NoteUser(s);
+}

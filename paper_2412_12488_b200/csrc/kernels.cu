@@ -1,0 +1,410 @@
+// kernels.cu — sm_100a kernels of the paged-KV page operations.
+//
+// All of them are HBM- (or, across engines, NVLink-) bound byte movers or
+// integer hash loops; none is GEMM-shaped, so there is no tensor-core work
+// here ("Kernels and their rooflines").  Rows are 16-byte
+// vectorised, one warp per (row, layer) item, grids sized to a multiple of
+// the SM count with every warp striding over items.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "hash.cuh"
+#include "kernels.cuh"
+
+namespace mkv {
+
+namespace {
+
+constexpr int kCopyThreads = 256;
+constexpr int kCopyUnroll = 8;
+
+__device__ __forceinline__ ulonglong2 ld_stream(const ulonglong2* p) {
+  ulonglong2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0, %1}, [%2];"
+               : "=l"(v.x), "=l"(v.y)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void st_vec(ulonglong2* p, ulonglong2 v) {
+  asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(v.x), "l"(v.y) : "memory");
+}
+
+// One warp moves one W-word row.  Loads are all issued before the stores
+// so each lane keeps kCopyUnroll 16-byte requests in flight.
+__device__ __forceinline__ void warp_copy_row(const uint64_t* __restrict__ src,
+                                              uint64_t* __restrict__ dst, int32_t W, int lane) {
+  if ((W & 1) == 0) {
+    const ulonglong2* s2 = reinterpret_cast<const ulonglong2*>(src);
+    ulonglong2* d2 = reinterpret_cast<ulonglong2*>(dst);
+    const int nv = W >> 1;
+    int v = lane;
+    for (; v + 32 * (kCopyUnroll - 1) < nv; v += 32 * kCopyUnroll) {
+      ulonglong2 t[kCopyUnroll];
+#pragma unroll
+      for (int u = 0; u < kCopyUnroll; ++u) t[u] = ld_stream(s2 + v + 32 * u);
+#pragma unroll
+      for (int u = 0; u < kCopyUnroll; ++u) st_vec(d2 + v + 32 * u, t[u]);
+    }
+    for (; v < nv; v += 32) st_vec(d2 + v, ld_stream(s2 + v));
+  } else {
+    for (int j = lane; j < W; j += 32) dst[j] = __ldg(src + j);
+  }
+}
+
+__global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
+  extern __shared__ uint32_t s_rows[];  // per relative layer (accounting only)
+  int32_t window = -1;
+  if (p.verdict != nullptr) {
+    window = *reinterpret_cast<const volatile int32_t*>(p.verdict);
+    if (window < 0) return;  // rejected by validation: no writes, no counts
+  }
+  const bool account = p.win_received != nullptr;
+  if (account) {
+    for (int i = threadIdx.x; i < p.n_layers; i += blockDim.x) s_rows[i] = 0;
+    __syncthreads();
+  }
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t items = p.n_rows * p.n_layers;
+  for (int64_t it = warp; it < items; it += n_warps) {
+    const int32_t lrel = static_cast<int32_t>(it / p.n_rows);
+    const int64_t r = it - static_cast<int64_t>(lrel) * p.n_rows;
+    const int64_t si = p.src_idx ? static_cast<int64_t>(__ldg(p.src_idx + r)) : r;
+    const int64_t di = p.dst_idx ? static_cast<int64_t>(__ldg(p.dst_idx + r)) : r;
+    const uint64_t* src = p.src + lrel * p.src_layer_words + si * p.W;
+    uint64_t* dst = p.dst + lrel * p.dst_layer_words + di * p.W;
+    bool write = true;
+    uint8_t* fill = nullptr;
+    if (p.dst_fill != nullptr) {
+      fill = p.dst_fill + lrel * p.dst_fill_layer + di;
+      write = *reinterpret_cast<volatile uint8_t*>(fill) == 0;  // Empty slots only
+    }
+    if (write) {
+      warp_copy_row(src, dst, p.W, lane);
+      if (fill != nullptr) {
+        __syncwarp();
+        if (lane == 0) *fill = p.fill_value;
+      }
+    }
+    if (account && lane == 0) atomicAdd(&s_rows[lrel], 1u);
+  }
+  if (account) {
+    // Publish: every thread's stores, then the counters, at system scope so
+    // a peer engine that observes the counter also observes the rows.
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long total = 0;
+      for (int i = 0; i < p.n_layers; ++i) total += s_rows[i];
+      __threadfence_system();
+      for (int i = 0; i < p.n_layers; ++i) {
+        if (s_rows[i] != 0) {
+          atomicAdd_system(p.win_layer_rows + static_cast<int64_t>(window) * p.win_layers +
+                               p.layer0 + i,
+                           s_rows[i]);
+        }
+      }
+      if (total != 0) atomicAdd_system(p.win_received + window, total);
+    }
+  }
+}
+
+__global__ void k_validate_remote(ValidateParams p) {
+  __shared__ int bad;
+  __shared__ int32_t w0;
+  if (threadIdx.x == 0) {
+    bad = p.n_ranges <= 0 ? 1 : 0;
+    w0 = -1;
+    if (p.n_ranges > 0) {
+      int64_t pg = p.range_page[0];
+      if (pg < 0 || pg >= p.num_pages) {
+        bad = 1;
+      } else {
+        w0 = *reinterpret_cast<const volatile int32_t*>(p.page_window + pg);
+        if (w0 < 0) bad = 1;
+      }
+    }
+  }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < p.n_ranges && !bad; i += blockDim.x) {
+    int64_t pg = p.range_page[i];
+    int32_t b = p.range_begin[i], c = p.range_count[i];
+    if (pg < 0 || pg >= p.num_pages || b < 0 || c < 0 || b + c > p.P) {
+      bad = 1;
+      break;
+    }
+    if (*reinterpret_cast<const volatile int32_t*>(p.page_window + pg) != w0) {
+      bad = 1;
+      break;
+    }
+    for (int32_t s = b; s < b + c; ++s) {
+      if (reinterpret_cast<const volatile uint8_t*>(p.expecting)[pg * p.P + s] == 0) {
+        bad = 1;
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *p.verdict = bad ? -1 : w0;
+    if (bad && p.status != nullptr) atomicOr(p.status, kStatusUnknownAddress);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_attn_write_hash(uint64_t* __restrict__ pool_l,
+                                                         uint8_t* __restrict__ fill_l,
+                                                         const int32_t* __restrict__ slots,
+                                                         const uint64_t* __restrict__ digests,
+                                                         int64_t n, int32_t layer, int32_t W) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = warp; r < n; r += n_warps) {
+    const int64_t slot = __ldg(slots + r);
+    uint8_t* f = fill_l + slot;
+    if (*reinterpret_cast<volatile uint8_t*>(f) != 0) continue;  // re-prefill is skipped
+    const uint64_t base = kv_base(__ldg(digests + r), layer);
+    uint64_t* row = pool_l + slot * W;
+    if ((W & 1) == 0) {
+      ulonglong2* row2 = reinterpret_cast<ulonglong2*>(row);
+      for (int v = lane; v < (W >> 1); v += 32) {
+        ulonglong2 w;
+        w.x = kv_word(base, 2u * v);
+        w.y = kv_word(base, 2u * v + 1u);
+        st_vec(row2 + v, w);
+      }
+    } else {
+      for (int j = lane; j < W; j += 32) row[j] = kv_word(base, static_cast<uint32_t>(j));
+    }
+    __syncwarp();
+    if (lane == 0) *f = 1;  // FillState::kComputedLocal
+  }
+}
+
+// One thread folds one row serially (FNV-1a is a byte-serial chain); 8
+// words are prefetched ahead of the chain.
+__global__ void __launch_bounds__(128) k_entry_digest(const uint64_t* __restrict__ pool_l,
+                                                      const int32_t* __restrict__ slots, int64_t n,
+                                                      int32_t W, uint64_t* __restrict__ F) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
+       r += stride) {
+    const uint64_t* row = pool_l + static_cast<int64_t>(__ldg(slots + r)) * W;
+    uint64_t h = entry_digest_init();
+    if ((W & 7) == 0) {
+      const ulonglong2* r2 = reinterpret_cast<const ulonglong2*>(row);
+      ulonglong2 cur[4], nxt[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) cur[u] = __ldg(r2 + u);
+      const int nb = W >> 3;  // blocks of 8 words
+      for (int b = 0; b < nb; ++b) {
+        if (b + 1 < nb) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) nxt[u] = __ldg(r2 + 4 * (b + 1) + u);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          h = fnv_u64(h, cur[u].x);
+          h = fnv_u64(h, cur[u].y);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
+      }
+    } else {
+      for (int j = 0; j < W; ++j) h = fnv_u64(h, __ldg(row + j));
+    }
+    F[r] = mix64(h);
+  }
+}
+
+constexpr int kScanThreads = 1024;
+
+__global__ void __launch_bounds__(kScanThreads) k_fold_scan(const FoldEntry* __restrict__ entries,
+                                                            const uint64_t* __restrict__ F,
+                                                            const uint64_t* __restrict__ hidden_in,
+                                                            uint64_t* __restrict__ hidden_out,
+                                                            int32_t layer) {
+  __shared__ uint64_t s_warp[kScanThreads / 32];
+  const FoldEntry e = entries[blockIdx.x];
+  const uint64_t base = e.fold_sums[layer];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int64_t chunk = (e.n_fold + kScanThreads - 1) / kScanThreads;
+  const int64_t lo = e.n_fold < t * chunk ? e.n_fold : t * chunk;
+  const int64_t hi = e.n_fold < lo + chunk ? e.n_fold : lo + chunk;
+  const uint64_t* f = F + e.fold_off;
+  uint64_t local = 0;
+  for (int64_t i = lo; i < hi; ++i) local += f[i];
+  // Exclusive scan of the per-thread sums (wrapping u64 adds).
+  uint64_t incl = local;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint64_t v = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += v;
+  }
+  if (lane == 31) s_warp[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    uint64_t w = s_warp[lane];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint64_t v = __shfl_up_sync(0xffffffffu, w, d);
+      if (lane >= d) w += v;
+    }
+    s_warp[lane] = w;  // inclusive over warps
+  }
+  __syncthreads();
+  uint64_t sum = base + (wid > 0 ? s_warp[wid - 1] : 0) + (incl - local);
+  for (int64_t i = lo; i < hi; ++i) {
+    sum += f[i];
+    if (i >= e.first_out) {
+      const int64_t o = e.out_off + (i - e.first_out);
+      const uint64_t x = hidden_in[o];
+      hidden_out[o] = next_hidden(x, attention_out(x, e.pos0 + i + 1, sum));
+    }
+  }
+  __syncthreads();
+  if (t == 0) e.fold_sums[layer] = base + s_warp[31];
+}
+
+__global__ void k_reset_pages(uint8_t* fill, uint8_t* expecting, int32_t* page_window,
+                              const int64_t* __restrict__ pages, int64_t n_pages, int32_t L,
+                              int64_t num_pages, int32_t P) {
+  const int64_t total = n_pages * P;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += stride) {
+    const int64_t pg = pages[i / P];
+    const int64_t slot = pg * P + (i % P);
+    for (int32_t l = 0; l < L; ++l) fill[static_cast<int64_t>(l) * num_pages * P + slot] = 0;
+    expecting[slot] = 0;
+    if (i % P == 0) page_window[pg] = -1;
+  }
+}
+
+__global__ void k_open_window(uint8_t* expecting, const int32_t* __restrict__ slots,
+                              int64_t n_slots, int32_t* page_window,
+                              const int64_t* __restrict__ pages, int64_t n_pages, int32_t window,
+                              unsigned long long* win_received, uint32_t* win_layer_rows,
+                              int32_t L) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (int64_t i = t0; i < n_slots; i += stride) expecting[slots[i]] = 1;
+  for (int64_t i = t0; i < n_pages; i += stride) page_window[pages[i]] = window;
+  if (window >= 0) {
+    for (int64_t i = t0; i < L; i += stride) win_layer_rows[static_cast<int64_t>(window) * L + i] = 0;
+    if (t0 == 0) win_received[window] = 0;
+  }
+}
+
+__global__ void k_first_nonfull(const uint8_t* __restrict__ fill, int64_t fill_layer_bytes,
+                                int32_t L, const int32_t* __restrict__ slots, int64_t n,
+                                unsigned long long* out) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += stride) {
+    const int64_t s = slots[i];
+    for (int32_t l = 0; l < L; ++l) {
+      if (fill[l * fill_layer_bytes + s] == 0) {
+        atomicMin(out, static_cast<unsigned long long>(i));
+        break;
+      }
+    }
+  }
+}
+
+__global__ void k_check_filled(const uint8_t* __restrict__ fill_l, const int32_t* __restrict__ slots,
+                               int64_t n, uint32_t* status) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += stride) {
+    if (fill_l[slots[i]] == 0) atomicOr(status, kStatusMissingKV);
+  }
+}
+
+inline int grid_for(int64_t work, int per_block, int num_sms, int max_per_sm) {
+  int64_t blocks = (work + per_block - 1) / per_block;
+  int64_t cap = static_cast<int64_t>(num_sms) * max_per_sm;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  return static_cast<int>(blocks);
+}
+
+}  // namespace
+
+void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms) {
+  const int64_t items = p.n_rows * p.n_layers;
+  if (items <= 0) return;
+  const int warps_per_block = kCopyThreads / 32;
+  const int grid = grid_for(items, warps_per_block, num_sms, 8);
+  const size_t smem = p.win_received ? sizeof(uint32_t) * p.n_layers : 0;
+  k_copy_rows<<<grid, kCopyThreads, smem, s>>>(p);
+}
+
+void launch_validate_remote(const ValidateParams& p, cudaStream_t s) {
+  k_validate_remote<<<1, 256, 0, s>>>(p);
+}
+
+void launch_attn_write_hash(uint64_t* pool_l, uint8_t* fill_l, const int32_t* slots,
+                            const uint64_t* digests, int64_t n, int32_t layer, int32_t W,
+                            cudaStream_t s, int num_sms) {
+  if (n <= 0) return;
+  k_attn_write_hash<<<grid_for(n, 8, num_sms, 8), 256, 0, s>>>(pool_l, fill_l, slots, digests, n,
+                                                                layer, W);
+}
+
+void launch_entry_digest(const uint64_t* pool_l, const int32_t* slots, int64_t n, int32_t W,
+                         uint64_t* F, cudaStream_t s, int num_sms) {
+  if (n <= 0) return;
+  k_entry_digest<<<grid_for(n, 128, num_sms, 16), 128, 0, s>>>(pool_l, slots, n, W, F);
+}
+
+void launch_fold_scan(const FoldEntry* entries, int64_t n_entries, const uint64_t* F,
+                      const uint64_t* hidden_in, uint64_t* hidden_out, int32_t layer,
+                      cudaStream_t s) {
+  if (n_entries <= 0) return;
+  k_fold_scan<<<static_cast<unsigned>(n_entries), kScanThreads, 0, s>>>(entries, F, hidden_in,
+                                                                         hidden_out, layer);
+}
+
+void launch_reset_pages(uint8_t* fill, uint8_t* expecting, int32_t* page_window,
+                        const int64_t* pages, int64_t n_pages, int32_t L, int64_t num_pages,
+                        int32_t P, cudaStream_t s) {
+  if (n_pages <= 0) return;
+  int64_t total = n_pages * P;
+  int grid = static_cast<int>((total + 255) / 256);
+  if (grid > 4096) grid = 4096;
+  k_reset_pages<<<grid, 256, 0, s>>>(fill, expecting, page_window, pages, n_pages, L, num_pages, P);
+}
+
+void launch_open_window(uint8_t* expecting, const int32_t* slots, int64_t n_slots,
+                        int32_t* page_window, const int64_t* pages, int64_t n_pages,
+                        int32_t window, unsigned long long* win_received,
+                        uint32_t* win_layer_rows, int32_t L, cudaStream_t s) {
+  int64_t work = n_slots > n_pages ? n_slots : n_pages;
+  if (work < L) work = L;
+  int grid = static_cast<int>((work + 255) / 256);
+  if (grid > 1024) grid = 1024;
+  if (grid < 1) grid = 1;
+  k_open_window<<<grid, 256, 0, s>>>(expecting, slots, n_slots, page_window, pages, n_pages, window,
+                                     win_received, win_layer_rows, L);
+}
+
+void launch_first_nonfull(const uint8_t* fill, int64_t fill_layer_bytes, int32_t L,
+                          const int32_t* slots, int64_t n, unsigned long long* out,
+                          cudaStream_t s, int num_sms) {
+  cudaMemsetAsync(out, 0xff, sizeof(unsigned long long), s);
+  if (n <= 0) return;
+  k_first_nonfull<<<grid_for(n, 256, num_sms, 4), 256, 0, s>>>(fill, fill_layer_bytes, L, slots,
+                                                                n, out);
+}
+
+void launch_check_filled(const uint8_t* fill_l, const int32_t* slots, int64_t n, uint32_t* status,
+                         cudaStream_t s, int num_sms) {
+  if (n <= 0) return;
+  k_check_filled<<<grid_for(n, 256, num_sms, 4), 256, 0, s>>>(fill_l, slots, n, status);
+}
+
+}  // namespace mkv

@@ -1,0 +1,126 @@
+// kernels.cuh — launch interfaces of the sm_100a page-operation kernels.
+//
+// HBM layout of one engine:
+//   pool  u64 [L][num_pages][P][W]   a (layer, page) block is P*W*8 bytes
+//                                    contiguous (64 KiB at Llama shapes), a
+//                                    (layer, slot) row is W*8 bytes (4 KiB)
+//   fill  u8  [L][num_pages][P]      FillState per (layer, slot)
+//   expecting u8 [num_pages][P]      receive reservation (kv_cache.h:52)
+//   page_window i32 [num_pages]      open receive window of the page's owner
+//   win_received u64 [max_windows]   slot writes counted per window
+//   win_layer_rows u32 [max_windows][L]  rows landed per (window, layer)
+// A "slot index" is page * P + slot.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace mkv {
+
+// Device status bits (sticky, per engine).
+enum : uint32_t {
+  kStatusUnknownAddress = 1u << 0,  // a remote write failed receiver validation
+  kStatusMissingKV = 1u << 1,       // a read hit an Empty slot
+};
+
+// Row copy between slot-addressed (or dense) row arrays, over
+// rows x layers items.  All row copies of the hot path go through it:
+//   remote_send / DirectSend   slots -> peer slots (fill check, window counters)
+//   send gather, GatherRange   slots -> dense staging
+//   ApplyRemoteWrite           dense staging -> slots (fill check)
+//   KV append                  dense rows -> slots (fill check)
+struct CopyParams {
+  const uint64_t* src;        // layer-0 base
+  int64_t src_layer_words;    // words between layers
+  const int32_t* src_idx;     // slot per row, or null = dense row r
+  uint64_t* dst;
+  int64_t dst_layer_words;
+  const int32_t* dst_idx;
+  uint8_t* dst_fill;          // layer-0 base of dst fill, or null = no fill rule
+  int64_t dst_fill_layer;     // bytes between layers
+  uint8_t fill_value;         // state written into Empty dst slots
+  int64_t n_rows;
+  int32_t layer0;             // first layer (absolute)
+  int32_t n_layers;
+  int32_t W;                  // u64 words per row
+  // Receive-window accounting on the destination engine (remote sends).
+  unsigned long long* win_received;  // null = none
+  uint32_t* win_layer_rows;
+  int32_t win_layers;         // L of the destination (row stride of win_layer_rows)
+  const int32_t* verdict;     // validation result: >= 0 window id, < 0 reject
+  uint32_t* status;           // sender-side sticky status
+};
+void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms);
+
+// Receiver-side validation of a remote write (ApplyRemoteWrite's checks,
+// kv_cache.cc:415-436): every addressed page maps to the same open window
+// and every slot is expecting-remote.  Writes the window id or -1 to *verdict.
+struct ValidateParams {
+  const int64_t* range_page;   // per range
+  const int32_t* range_begin;
+  const int32_t* range_count;
+  int64_t n_ranges;
+  const int32_t* page_window;  // destination engine
+  const uint8_t* expecting;    // destination engine [pages][P]
+  int64_t num_pages;
+  int32_t P;
+  int32_t* verdict;
+  uint32_t* status;            // sender-side sticky status (kStatusUnknownAddress)
+};
+void launch_validate_remote(const ValidateParams& p, cudaStream_t s);
+
+// Attention write (kv_cache.cc:328-334 + KvEntryWords hash_model.cc:39-46):
+// for each output row, if its fill is Empty write the W hash words of
+// (digest, layer) and set ComputedLocal.
+void launch_attn_write_hash(uint64_t* pool_l, uint8_t* fill_l, const int32_t* slots,
+                            const uint64_t* digests, int64_t n, int32_t layer, int32_t W,
+                            cudaStream_t s, int num_sms);
+
+// EntryDigest of each slot row (hash_model.cc:57-61) -> F[n].
+void launch_entry_digest(const uint64_t* pool_l, const int32_t* slots, int64_t n, int32_t W,
+                         uint64_t* F, cudaStream_t s, int num_sms);
+
+// Per-entry inclusive fold + hidden update (kv_cache.cc:319-351).
+struct FoldEntry {
+  int64_t fold_off;    // first fold row of the entry in F
+  int64_t n_fold;      // end - fold_from
+  int64_t first_out;   // begin - fold_from
+  int64_t out_off;     // first output row in hidden arrays
+  int64_t pos0;        // fold_from
+  uint64_t* fold_sums; // device [L] running sums of the sequence
+};
+void launch_fold_scan(const FoldEntry* entries, int64_t n_entries, const uint64_t* F,
+                      const uint64_t* hidden_in, uint64_t* hidden_out, int32_t layer,
+                      cudaStream_t s);
+
+// Zero fill/expecting bytes and page_window of freed pages (kv_cache.cc:499-507).
+void launch_reset_pages(uint8_t* fill, uint8_t* expecting, int32_t* page_window,
+                        const int64_t* pages, int64_t n_pages, int32_t L, int64_t num_pages,
+                        int32_t P, cudaStream_t s);
+
+// prep_recv's device half (kv_cache.cc:215-227): mark reserved slots
+// expecting-remote, point the sequence's pages at receive window `window`,
+// zero that window's counters.
+void launch_open_window(uint8_t* expecting, const int32_t* slots, int64_t n_slots,
+                        int32_t* page_window, const int64_t* pages, int64_t n_pages,
+                        int32_t window, unsigned long long* win_received,
+                        uint32_t* win_layer_rows, int32_t L, cudaStream_t s);
+
+// First position in [0, n) whose slot has an Empty fill on any layer (n if none).
+void launch_first_nonfull(const uint8_t* fill, int64_t fill_layer_bytes, int32_t L,
+                          const int32_t* slots, int64_t n, unsigned long long* out,
+                          cudaStream_t s, int num_sms);
+
+// Any Empty fill on `layer` among the slot rows -> status |= kStatusMissingKV.
+void launch_check_filled(const uint8_t* fill_l, const int32_t* slots, int64_t n, uint32_t* status,
+                         cudaStream_t s, int num_sms);
+
+// Paged GQA decode attention (decode_attn.cu): split-KV partials + combine.
+size_t decode_attn_smem(int head_dim);
+bool launch_decode_attn(const void* pool_l, int64_t row_elems, const int32_t* slots,
+                        const int64_t* ctx_off, const int32_t* ctx_len, const void* q, int batch,
+                        int Hq, int Hkv, int D, float scale, int splits, float* part_o,
+                        float* part_ml, void* out, cudaStream_t s);
+
+}  // namespace mkv
