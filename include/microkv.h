@@ -303,7 +303,10 @@ int ss_detach_peer(ss_cache* cache, int32_t dest);
 
 /* Attention with device hidden buffers, enqueued on `stream`.  Marked
  * sends must target attached peers (device-direct); otherwise
- * SS_ERR_PEER_UNREACHABLE. */
+ * SS_ERR_PEER_UNREACHABLE.  Each layer's sends run on the engine's
+ * communication stream, ordered after that layer's KV writes, so layer l's
+ * transfer overlaps layer l+1's compute;
+ * ss_synchronize waits for them. */
 int ss_attention_async(ss_cache* cache, ss_plan* plan, int32_t layer, const uint64_t* hidden_in_dev,
                        uint64_t* hidden_out_dev, void* stream);
 /* DirectSend (SPEC.md:292-299 Case 1; GatherRange + ApplyRemoteWrite per
@@ -314,6 +317,16 @@ int ss_attention_async(ss_cache* cache, ss_plan* plan, int32_t layer, const uint
 int ss_direct_send_async(ss_cache* cache, int64_t seq, int64_t begin, int64_t end, int32_t dest,
                          const ss_addr* dest_addr, uint64_t user_tag, int32_t layer_begin,
                          int32_t layer_end, void* stream);
+/* The same DirectSend split into the reference's two stages
+ * (kv_cache.h:6-10): ss_begin_direct_send resolves both page tables and
+ * uploads the row maps once (declaration); ss_launch_direct_send_async
+ * enqueues only the validation + copy kernels for a layer range
+ * (computation) and may be called repeatedly, e.g. once per layer as the
+ * producing layer finishes.  The plan is freed with ss_plan_destroy. */
+int ss_begin_direct_send(ss_cache* cache, int64_t seq, int64_t begin, int64_t end, int32_t dest,
+                         const ss_addr* dest_addr, uint64_t user_tag, ss_plan** plan_out);
+int ss_launch_direct_send_async(ss_cache* cache, ss_plan* plan, int32_t layer_begin,
+                                int32_t layer_end, void* stream);
 /* GatherRange into device memory out_dev[(end-begin) * dim] on `stream`. */
 int ss_gather_range_async(ss_cache* cache, int64_t seq, int64_t begin, int64_t end, int32_t layer,
                           uint64_t* out_dev, void* stream);
@@ -343,6 +356,14 @@ int ss_paged_decode_attention_async(ss_cache* cache, ss_plan* decode_plan, int32
 /* Device pointer of layer `layer`'s pool slab ([num_pages][page_size][dim]
  * u64 words) — for filling synthetic KV in tests and benchmarks. */
 int ss_pool_layer_ptr(ss_cache* cache, int32_t layer, void** dev_ptr);
+/* Enqueue on `stream` a device-side wait until the receive window of
+ * `seq` has counted all its expected slot writes (device-direct sends from
+ * peers), so receiver work queued behind it starts without a host round
+ * trip.  Gives up after timeout_ms (sets the sticky status reported by
+ * ss_synchronize as SS_ERR_ABORTED) so a lost sender cannot hang the GPU. */
+int ss_wait_receive_async(ss_cache* cache, int64_t seq, int64_t timeout_ms, void* stream);
+/* Host<->device bytes this cache has copied (evidence counters). */
+int ss_copy_counters(const ss_cache* cache, int64_t* h2d_bytes, int64_t* d2h_bytes);
 /* Number of kernel launches this cache has issued (evidence counter). */
 int64_t ss_kernel_launches(const ss_cache* cache);
 /* Sync the cache's internal stream. */

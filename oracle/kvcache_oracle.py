@@ -389,9 +389,9 @@ class KVCache:
             rec.window = _Window((m, e), (e - m) * self.layers)
         return PrepRecvResult(m, addr)
 
-    def MarkSend(self, seq, range, dest, dest_addr, user_tag=0):  # kv_cache.cc:231-243
+    def MarkSend(self, seq, token_range, dest, dest_addr, user_tag=0):  # kv_cache.cc:231-243
         rec = self._get(seq)
-        b, e = range
+        b, e = token_range
         if not (b >= 0 and e <= len(rec.tokens) and b <= e):
             raise _err(ErrorCode.InvalidArgument, "send range outside sequence")
         if dest_addr.token_count != e - b:
@@ -489,19 +489,19 @@ class KVCache:
         plan.next_layer += 1
         return np.asarray(out, dtype=np.uint64)
 
-    def GatherRange(self, seq, range, layer):  # kv_cache.cc:373-387
+    def GatherRange(self, seq, token_range, layer):  # kv_cache.cc:373-387
         rec = self._get(seq)
         rows = []
-        for pos in range(*range):
+        for pos in range(*token_range):
             pg, sl = self._resolve(rec, pos)
             if self.fill[pg, sl, layer] == 0:
                 raise _err(ErrorCode.MissingKV, "gather over empty slot")
             rows.append(self.values[pg, sl, layer])
         return np.concatenate(rows) if rows else np.zeros(0, np.uint64)
 
-    def BuildAddr(self, seq, range):  # kv_cache.cc:389-407
+    def BuildAddr(self, seq, token_range):  # kv_cache.cc:389-407
         rec = self._get(seq)
-        b, e = range
+        b, e = token_range
         if b < rec.fork_len:
             raise _err(ErrorCode.InvalidArgument, "address must cover own slots only")
         ranges = []

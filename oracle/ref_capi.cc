@@ -24,6 +24,7 @@
 #include <cstdio>
 #include <cstring>
 #include <deque>
+#include <set>
 #include <memory>
 #include <string>
 #include <thread>
@@ -36,7 +37,10 @@
 
 using namespace splitserve;
 
+struct ss_plan;
 struct ss_cache {
+  ~ss_cache();
+  std::set<ss_plan*> plans;  // released with the cache if still live
   std::unique_ptr<HashModel> model;
   std::unique_ptr<KVCache> cache;
   std::string err;
@@ -46,7 +50,12 @@ struct ss_cache {
 
 struct ss_plan {
   ForwardPlan plan;
+  ss_cache* owner = nullptr;
 };
+
+ss_cache::~ss_cache() {
+  for (ss_plan* p : plans) delete p;
+}
 
 namespace {
 
@@ -213,6 +222,8 @@ int ss_begin_forward(ss_cache* c, const ss_batch_entry* batch, int64_t n, ss_pla
     }
     auto p = std::make_unique<ss_plan>();
     p->plan = c->cache->BeginForward(b);
+    p->owner = c;
+    c->plans.insert(p.get());
     *plan_out = p.release();
     return SS_OK;
   });
@@ -221,7 +232,11 @@ int ss_begin_forward(ss_cache* c, const ss_batch_entry* batch, int64_t n, ss_pla
 int64_t ss_plan_total_outputs(const ss_plan* p) { return p->plan.total_outputs; }
 int64_t ss_plan_num_sends(const ss_plan* p) { return static_cast<int64_t>(p->plan.sends.size()); }
 int32_t ss_plan_next_layer(const ss_plan* p) { return p->plan.next_layer; }
-void ss_plan_destroy(ss_plan* p) { delete p; }
+void ss_plan_destroy(ss_plan* p) {
+  if (!p) return;
+  if (p->owner) p->owner->plans.erase(p);
+  delete p;
+}
 
 int ss_attention(ss_cache* c, ss_plan* p, int32_t layer, const uint64_t* hidden_in,
                  uint64_t* hidden_out, int64_t n, ss_frame_sink sink, void* user) {
@@ -421,6 +436,13 @@ int ss_direct_send_async(ss_cache*, int64_t, int64_t, int64_t, int32_t, const ss
                          int32_t, int32_t, void*) {
   return SS_ERR_UNSUPPORTED;
 }
+int ss_begin_direct_send(ss_cache*, int64_t, int64_t, int64_t, int32_t, const ss_addr*, uint64_t,
+                         ss_plan**) {
+  return SS_ERR_UNSUPPORTED;
+}
+int ss_launch_direct_send_async(ss_cache*, ss_plan*, int32_t, int32_t, void*) {
+  return SS_ERR_UNSUPPORTED;
+}
 int ss_gather_range_async(ss_cache*, int64_t, int64_t, int64_t, int32_t, uint64_t*, void*) {
   return SS_ERR_UNSUPPORTED;
 }
@@ -439,6 +461,12 @@ int ss_paged_decode_attention_async(ss_cache*, ss_plan*, int32_t, int32_t, int32
   return SS_ERR_UNSUPPORTED;
 }
 int ss_pool_layer_ptr(ss_cache*, int32_t, void**) { return SS_ERR_UNSUPPORTED; }
+int ss_wait_receive_async(ss_cache*, int64_t, int64_t, void*) { return SS_ERR_UNSUPPORTED; }
+int ss_copy_counters(const ss_cache*, int64_t* h2d, int64_t* d2h) {
+  *h2d = 0;
+  *d2h = 0;
+  return SS_OK;
+}
 int64_t ss_kernel_launches(const ss_cache*) { return 0; }
 int ss_synchronize(ss_cache*) { return SS_OK; }
 

@@ -139,6 +139,15 @@ ss_cache::ss_cache(const ss_config& cfg)
   CudaCheck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
   CudaCheck(cudaEventCreateWithFlags(&internal_ev_, cudaEventDisableTiming), "event");
   CudaCheck(cudaEventCreateWithFlags(&user_ev_, cudaEventDisableTiming), "event");
+  CudaCheck(cudaEventCreateWithFlags(&comm_ev_, cudaEventDisableTiming), "event");
+  CudaCheck(cudaEventCreateWithFlags(&layer_ev_, cudaEventDisableTiming), "event");
+  {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    // Transfers get the higher priority so a layer's send is not starved by
+    // the next layer's compute (the overlap of PAPER.md:339-344).
+    CudaCheck(cudaStreamCreateWithPriority(&comm_stream_, cudaStreamNonBlocking, hi), "stream");
+  }
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device_) == cudaSuccess) {
     uint64_t thr = UINT64_MAX;
@@ -172,6 +181,29 @@ ss_cache::ss_cache(const ss_config& cfg)
 }
 
 ss_cache::~ss_cache() {
+  // Order-independent teardown: unlink in-process peer relations both ways,
+  // then release plans still alive (their handles become invalid).
+  for (ss_cache* a : attached_by_) {
+    for (auto it = a->peer_engines_.begin(); it != a->peer_engines_.end();) {
+      if (it->second == this) {
+        a->peers_.erase(it->first);
+        it = a->peer_engines_.erase(it);
+      } else {
+        ++it;
+      }
+    }
+  }
+  for (auto& [r, e] : peer_engines_) e->attached_by_.erase(this);
+  if (device_ >= 0) {
+    cudaSetDevice(device_);
+    cudaStreamSynchronize(comm_stream_);
+    cudaStreamSynchronize(stream_);
+  }
+  for (ss_plan* p : live_plans_) {
+    if (device_ >= 0) FreePlanDevice(p);
+    delete p;
+  }
+  live_plans_.clear();
   if (device_ < 0) return;
   cudaSetDevice(device_);
   if (stream_) cudaStreamSynchronize(stream_);
@@ -190,6 +222,10 @@ ss_cache::~ss_cache() {
   cudaFreeHost(h_pinned_);
   cudaEventDestroy(internal_ev_);
   cudaEventDestroy(user_ev_);
+  cudaStreamSynchronize(comm_stream_);
+  cudaEventDestroy(comm_ev_);
+  cudaEventDestroy(layer_ev_);
+  cudaStreamDestroy(comm_stream_);
   cudaStreamDestroy(stream_);
 }
 
@@ -228,9 +264,22 @@ void ss_cache::RequireDevice(const char* what) const {
 
 void ss_cache::Sync() { CudaCheck(cudaStreamSynchronize(stream_), "cudaStreamSynchronize"); }
 
+void ss_cache::H2D(void* dst, const void* src, size_t bytes, cudaStream_t s, const char* what) {
+  CudaCheck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s), what);
+  h2d_bytes_ += static_cast<int64_t>(bytes);
+}
+
+void ss_cache::D2H(void* dst, const void* src, size_t bytes, cudaStream_t s, const char* what) {
+  CudaCheck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s), what);
+  d2h_bytes_ += static_cast<int64_t>(bytes);
+}
+
 void ss_cache::OrderAfterUser() {
   if (user_pending_) {
     CudaCheck(cudaStreamWaitEvent(stream_, user_ev_, 0), "cudaStreamWaitEvent");
+  }
+  if (comm_pending_) {
+    CudaCheck(cudaStreamWaitEvent(stream_, comm_ev_, 0), "cudaStreamWaitEvent");
   }
 }
 
@@ -282,15 +331,11 @@ int64_t ss_cache::DeviceFirstNonFull(const Record* rec, int64_t from, int64_t to
   OrderAfterUser();
   const int64_t n = to - from;
   DevBlock b = DevAlloc(sizeof(int32_t) * n, stream_);
-  CudaCheck(cudaMemcpyAsync(b.ptr, rec->slots.data() + from, sizeof(int32_t) * n,
-                            cudaMemcpyHostToDevice, stream_),
-            "H2D slots");
+  H2D(b.ptr, rec->slots.data() + from, sizeof(int32_t) * n, stream_, "H2D slots");
   launch_first_nonfull(d_fill_, num_pages_ * P_, L_, static_cast<int32_t*>(b.ptr), n, d_scratch_,
                        stream_, num_sms_);
   launches_ += 1;
-  CudaCheck(cudaMemcpyAsync(h_pinned_, d_scratch_, sizeof(unsigned long long),
-                            cudaMemcpyDeviceToHost, stream_),
-            "D2H scan");
+  D2H(h_pinned_, d_scratch_, sizeof(unsigned long long), stream_, "D2H scan");
   DevFree(b, stream_);
   Sync();
   const unsigned long long r = h_pinned_[0];
@@ -322,15 +367,12 @@ void ss_cache::CheckFilled(const Record* rec, int64_t begin, int64_t end, int32_
   const int64_t n = static_cast<int64_t>(unproven.size());
   DevBlock b = DevAlloc(sizeof(int32_t) * n, stream_);
   CudaCheck(cudaMemsetAsync(d_status_, 0, sizeof(uint32_t), stream_), "memset");
-  CudaCheck(cudaMemcpyAsync(b.ptr, unproven.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice,
-                            stream_),
-            "H2D slots");
+  H2D(b.ptr, unproven.data(), sizeof(int32_t) * n, stream_, "H2D slots");
   launch_check_filled(d_fill_ + static_cast<int64_t>(layer) * num_pages_ * P_,
                       static_cast<int32_t*>(b.ptr), n, d_status_, stream_, num_sms_);
   launches_ += 2;
   uint32_t st = 0;
-  CudaCheck(cudaMemcpyAsync(&st, d_status_, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream_),
-            "D2H status");
+  D2H(&st, d_status_, sizeof(uint32_t), stream_, "D2H status");
   DevFree(b, stream_);
   Sync();
   MKV_CHECK((st & kStatusMissingKV) == 0, kMissingKV, what);
@@ -478,8 +520,7 @@ void ss_cache::OpenDeviceWindow(Record* rec, int64_t m, int64_t e) {
   std::memcpy(host.data() + off_pages, rec->own_pages.data(), sizeof(int64_t) * np);
   OrderAfterUser();
   DevBlock b = DevAlloc(host.size(), stream_);
-  CudaCheck(cudaMemcpyAsync(b.ptr, host.data(), host.size(), cudaMemcpyHostToDevice, stream_),
-            "H2D window");
+  H2D(b.ptr, host.data(), host.size(), stream_, "H2D window");
   launch_open_window(d_expecting_, static_cast<int32_t*>(b.ptr), n, d_page_window_,
                      reinterpret_cast<int64_t*>(static_cast<uint8_t*>(b.ptr) + off_pages), np, wid,
                      d_win_received_, d_win_layer_rows_, L_, stream_);
@@ -555,6 +596,7 @@ ss_plan* ss_cache::BeginForward(const ss_batch_entry* batch, int64_t n) {
     plan->sends.push_back(std::move(ps));
     it = pending_sends_.erase(it);
   }
+  live_plans_.insert(plan.get());
   return plan.release();
 }
 
@@ -650,8 +692,7 @@ void ss_cache::PlanToDevice(ss_plan* plan) {
   plan->dev = DevAlloc(off, stream_);
   uint8_t* base = static_cast<uint8_t*>(plan->dev.ptr);
   if (upload_end > 0) {
-    CudaCheck(cudaMemcpyAsync(base, host.data(), upload_end, cudaMemcpyHostToDevice, stream_),
-              "H2D plan");
+    H2D(base, host.data(), upload_end, stream_, "H2D plan");
   }
   plan->d_fold_slots = reinterpret_cast<int32_t*>(base + o_fold);
   plan->d_out_slots = reinterpret_cast<int32_t*>(base + o_out);
@@ -674,7 +715,23 @@ void ss_cache::PlanToDevice(ss_plan* plan) {
   plan->on_device = true;
 }
 
+void ss_cache::FreePlanDevice(ss_plan* plan) {
+  if (plan->dev.ptr) {
+    cudaStreamSynchronize(comm_stream_);
+    if (user_pending_) cudaEventSynchronize(user_ev_);
+    cudaStreamSynchronize(stream_);
+    cudaFree(plan->dev.ptr);
+    plan->dev = DevBlock{};
+  }
+  if (plan->d_partial) {
+    cudaDeviceSynchronize();
+    cudaFree(plan->d_partial);
+    plan->d_partial = nullptr;
+  }
+}
+
 void ss_cache::DestroyPlan(ss_plan* plan) {
+  live_plans_.erase(plan);
   if (device_ >= 0 && (plan->dev.ptr || plan->d_partial)) {
     cudaSetDevice(device_);
     OrderAfterUser();
@@ -766,15 +823,25 @@ void ss_cache::AttentionAsync(ss_plan* plan, int32_t layer, const uint64_t* hin,
       AdvanceCommitted(rec, e.end);
     }
   }
-  // Hot loop B: stream this layer's KV of every marked send.
-  for (size_t i = 0; i < plan->sends.size(); ++i) {
-    const PlanSend& snd = plan->sends[i];
-    CheckFilled(MustGet(snd.seq), snd.begin, snd.end, layer, "sending empty slot", plan);
-    const PeerTarget& peer = PeerFor(snd.dest);
-    const auto& d = plan->dsend[i];
-    LaunchRemote(peer, d.src_slots, d.dst_slots, d.range_page, d.range_begin, d.range_count,
-                 static_cast<int64_t>(snd.dest_addr.ranges.size()), d.verdict,
-                 snd.end - snd.begin, layer, layer + 1, s);
+  // Hot loop B: stream this layer's KV of every marked send, on the
+  // communication stream, ordered after this layer's writes only.
+  if (!plan->sends.empty()) {
+    for (size_t i = 0; i < plan->sends.size(); ++i) {
+      const PlanSend& snd = plan->sends[i];
+      CheckFilled(MustGet(snd.seq), snd.begin, snd.end, layer, "sending empty slot", plan);
+      PeerFor(snd.dest);
+    }
+    CudaCheck(cudaEventRecord(layer_ev_, s), "cudaEventRecord");
+    CudaCheck(cudaStreamWaitEvent(comm_stream_, layer_ev_, 0), "cudaStreamWaitEvent");
+    for (size_t i = 0; i < plan->sends.size(); ++i) {
+      const PlanSend& snd = plan->sends[i];
+      const auto& d = plan->dsend[i];
+      LaunchRemote(PeerFor(snd.dest), d.src_slots, d.dst_slots, d.range_page, d.range_begin,
+                   d.range_count, static_cast<int64_t>(snd.dest_addr.ranges.size()), d.verdict,
+                   snd.end - snd.begin, layer, layer + 1, comm_stream_);
+    }
+    CudaCheck(cudaEventRecord(comm_ev_, comm_stream_), "cudaEventRecord");
+    comm_pending_ = true;
   }
   if (s != stream_) NoteUser(s);
   ++plan->next_layer;
@@ -793,9 +860,7 @@ void ss_cache::Attention(ss_plan* plan, int32_t layer, const uint64_t* hidden_in
   OrderAfterUser();
   PlanToDevice(plan);
   if (n > 0) {
-    CudaCheck(cudaMemcpyAsync(plan->d_hidden_in, hidden_in, sizeof(uint64_t) * n,
-                              cudaMemcpyHostToDevice, stream_),
-              "H2D hidden");
+    H2D(plan->d_hidden_in, hidden_in, sizeof(uint64_t) * n, stream_, "H2D hidden");
   }
   uint64_t* pool_l = PoolLayer(layer);
   uint8_t* fill_l = d_fill_ + static_cast<int64_t>(layer) * num_pages_ * P_;
@@ -806,9 +871,7 @@ void ss_cache::Attention(ss_plan* plan, int32_t layer, const uint64_t* hidden_in
                    plan->d_hidden_in, plan->d_hidden_out, layer, stream_);
   launches_ += 3;
   if (n > 0) {
-    CudaCheck(cudaMemcpyAsync(hidden_out, plan->d_hidden_out, sizeof(uint64_t) * n,
-                              cudaMemcpyDeviceToHost, stream_),
-              "D2H hidden");
+    D2H(hidden_out, plan->d_hidden_out, sizeof(uint64_t) * n, stream_, "D2H hidden");
   }
   for (const auto& e : plan->entries) {
     Record* rec = MustGet(e.seq);
@@ -846,9 +909,7 @@ void ss_cache::Attention(ss_plan* plan, int32_t layer, const uint64_t* hidden_in
     launches_ += 1;
     payload.resize(static_cast<size_t>(rows) * W_);
     if (rows > 0) {
-      CudaCheck(cudaMemcpyAsync(payload.data(), d.staging, sizeof(uint64_t) * rows * W_,
-                                cudaMemcpyDeviceToHost, stream_),
-                "D2H payload");
+      D2H(payload.data(), d.staging, sizeof(uint64_t) * rows * W_, stream_, "D2H payload");
     }
     Sync();
     std::vector<ss_slot_range> rr;
@@ -870,15 +931,14 @@ void ss_cache::GatherRange(SeqId seq, int64_t begin, int64_t end, int32_t layer,
   MKV_CHECK(layer >= 0 && layer < L_, kInvalidArgument, "layer out of range");
   MKV_CHECK(begin >= 0 && begin <= end, kInvalidArgument, "bad gather range");
   for (int64_t pos = begin; pos < end; ++pos) Resolve(rec, pos);
+  if (end > rec->committed_hint) AdvanceCommitted(MustGet(seq));
   CheckFilled(rec, begin, end, layer, "gather over empty slot", nullptr);
   const int64_t n = end - begin;
   if (n == 0) return;
   OrderAfterUser();
   if (s != stream_) OrderUser(s);
   DevBlock b = DevAlloc(sizeof(int32_t) * n, s);
-  CudaCheck(cudaMemcpyAsync(b.ptr, rec->slots.data() + begin, sizeof(int32_t) * n,
-                            cudaMemcpyHostToDevice, s),
-            "H2D slots");
+  H2D(b.ptr, rec->slots.data() + begin, sizeof(int32_t) * n, s, "H2D slots");
   CopyParams c{};
   c.src = PoolLayer(layer);
   c.src_idx = static_cast<int32_t*>(b.ptr);
@@ -980,13 +1040,10 @@ int ss_cache::ApplyRemoteWrite(const KVAddr& addr, int32_t layer, const uint64_t
     const size_t o_pay = Align(sizeof(int32_t) * n);
     DevBlock b = DevAlloc(o_pay + (on_device ? 0 : sizeof(uint64_t) * n_words), st);
     uint8_t* base = static_cast<uint8_t*>(b.ptr);
-    CudaCheck(cudaMemcpyAsync(base, dst.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st),
-              "H2D slots");
+    H2D(base, dst.data(), sizeof(int32_t) * n, st, "H2D slots");
     const uint64_t* src = payload;
     if (!on_device) {
-      CudaCheck(cudaMemcpyAsync(base + o_pay, payload, sizeof(uint64_t) * n_words,
-                                cudaMemcpyHostToDevice, st),
-                "H2D payload");
+      H2D(base + o_pay, payload, sizeof(uint64_t) * n_words, st, "H2D payload");
       src = reinterpret_cast<const uint64_t*>(base + o_pay);
     }
     CopyParams c{};
@@ -1029,9 +1086,8 @@ void ss_cache::PollDeviceWindows() {
   }
   if (open.empty()) return;
   for (size_t i = 0; i < open.size(); ++i) {
-    CudaCheck(cudaMemcpyAsync(h_pinned_ + i, d_win_received_ + open[i]->window->dev_id,
-                              sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream_),
-              "D2H window");
+    D2H(h_pinned_ + i, d_win_received_ + open[i]->window->dev_id,
+                              sizeof(unsigned long long), stream_, "D2H window");
   }
   Sync();
   std::lock_guard<std::mutex> lock(recv_mu_);
@@ -1066,9 +1122,10 @@ std::vector<SeqId> ss_cache::DrainReceiveCompletions() {
 
 // DirectSend: GatherRange + ApplyRemoteWrite per layer, fused into one
 // launch that stores the sender's rows straight into the receiver's pages.
-void ss_cache::DirectSend(SeqId seq, int64_t begin, int64_t end, Rank dest, const KVAddr& addr,
-                          uint64_t tag, int32_t lb, int32_t le, cudaStream_t s) {
-  (void)tag;
+// Declaration: resolve the source page table and expand the destination
+// address once, upload both row maps with the range table in one copy.
+ss_plan* ss_cache::BeginDirectSend(SeqId seq, int64_t begin, int64_t end, Rank dest,
+                                   const KVAddr& addr, uint64_t tag) {
   RequireDevice("DirectSend");
   Record* rec = MustGet(seq);
   MKV_CHECK(begin >= 0 && end <= static_cast<int64_t>(rec->tokens.size()) && begin <= end,
@@ -1077,20 +1134,23 @@ void ss_cache::DirectSend(SeqId seq, int64_t begin, int64_t end, Rank dest, cons
             "destination covers " + std::to_string(addr.token_count) + " tokens, range has " +
                 std::to_string(end - begin));
   MKV_CHECK(addr.token_begin == begin, kAddrMismatch, "destination token_begin mismatch");
-  MKV_CHECK(lb >= 0 && lb <= le && le <= L_, kInvalidArgument, "bad layer range");
-  const PeerTarget& peer = PeerFor(dest);
-  const int64_t n = end - begin;
+  PeerFor(dest);
   for (int64_t pos = begin; pos < end; ++pos) Resolve(rec, pos);
-  if (end > rec->committed_hint) AdvanceCommitted(rec);
-  for (int32_t l = lb; l < le && end > rec->committed_hint; ++l) {
-    CheckFilled(rec, begin, end, l, "gather over empty slot", nullptr);
-  }
-  if (lb == le) return;
+  auto plan = std::make_unique<ss_plan>();
+  plan->owner = this;
+  PlanSend ps;
+  ps.seq = seq;
+  ps.begin = begin;
+  ps.end = end;
+  ps.dest = dest;
+  ps.dest_addr = addr;
+  ps.user_tag = tag;
+  plan->sends.push_back(std::move(ps));
   std::vector<int32_t> dst;
   std::vector<int64_t> rp;
   std::vector<int32_t> rb, rc;
   ExpandAddr(addr, &dst, &rp, &rb, &rc);
-  const int64_t nr = static_cast<int64_t>(rp.size());
+  const int64_t n = end - begin, nr = static_cast<int64_t>(rp.size());
   const size_t o_src = 0, o_dst = Align(sizeof(int32_t) * n);
   const size_t o_rp = o_dst + Align(sizeof(int32_t) * dst.size());
   const size_t o_rb = o_rp + Align(sizeof(int64_t) * nr);
@@ -1104,16 +1164,57 @@ void ss_cache::DirectSend(SeqId seq, int64_t begin, int64_t end, Rank dest, cons
   std::memcpy(host.data() + o_rb, rb.data(), sizeof(int32_t) * nr);
   std::memcpy(host.data() + o_rc, rc.data(), sizeof(int32_t) * nr);
   OrderAfterUser();
+  plan->dev = DevAlloc(total, stream_);
+  uint8_t* base = static_cast<uint8_t*>(plan->dev.ptr);
+  H2D(base, host.data(), total, stream_, "H2D send");
+  plan->dsend.resize(1);
+  auto& d = plan->dsend[0];
+  d.src_slots = reinterpret_cast<int32_t*>(base + o_src);
+  d.dst_slots = reinterpret_cast<int32_t*>(base + o_dst);
+  d.range_page = reinterpret_cast<int64_t*>(base + o_rp);
+  d.range_begin = reinterpret_cast<int32_t*>(base + o_rb);
+  d.range_count = reinterpret_cast<int32_t*>(base + o_rc);
+  d.verdict = reinterpret_cast<int32_t*>(base + o_v);
+  plan->on_device = true;
+  plan->is_direct_send = true;
+  CudaCheck(cudaEventRecord(internal_ev_, stream_), "cudaEventRecord");
+  live_plans_.insert(plan.get());
+  return plan.release();
+}
+
+// Computation: validation + one copy launch over rows x [lb, le).  The
+// source rows must be non-Empty (GatherRange's MissingKV, kv_cache.cc:379).
+void ss_cache::LaunchDirectSend(ss_plan* plan, int32_t lb, int32_t le, cudaStream_t s) {
+  RequireDevice("DirectSend");
+  MKV_CHECK(plan->is_direct_send, kInvalidArgument, "not a direct-send plan");
+  MKV_CHECK(lb >= 0 && lb <= le && le <= L_, kInvalidArgument, "bad layer range");
+  const PlanSend& snd = plan->sends[0];
+  Record* rec = MustGet(snd.seq);
+  if (snd.end > rec->committed_hint) AdvanceCommitted(rec);
+  for (int32_t l = lb; l < le && snd.end > rec->committed_hint; ++l) {
+    CheckFilled(rec, snd.begin, snd.end, l, "gather over empty slot", nullptr);
+  }
+  if (lb == le) return;
+  const PeerTarget& peer = PeerFor(snd.dest);
+  OrderAfterUser();
   if (s != stream_) OrderUser(s);
-  DevBlock b = DevAlloc(total, s);
-  uint8_t* base = static_cast<uint8_t*>(b.ptr);
-  CudaCheck(cudaMemcpyAsync(base, host.data(), total, cudaMemcpyHostToDevice, s), "H2D send");
-  LaunchRemote(peer, reinterpret_cast<int32_t*>(base + o_src), reinterpret_cast<int32_t*>(base + o_dst),
-               reinterpret_cast<int64_t*>(base + o_rp), reinterpret_cast<int32_t*>(base + o_rb),
-               reinterpret_cast<int32_t*>(base + o_rc), nr, reinterpret_cast<int32_t*>(base + o_v),
-               n, lb, le, s);
-  DevFree(b, s);
+  const auto& d = plan->dsend[0];
+  LaunchRemote(peer, d.src_slots, d.dst_slots, d.range_page, d.range_begin, d.range_count,
+               static_cast<int64_t>(snd.dest_addr.ranges.size()), d.verdict, snd.end - snd.begin,
+               lb, le, s);
   if (s != stream_) NoteUser(s);
+}
+
+void ss_cache::DirectSend(SeqId seq, int64_t begin, int64_t end, Rank dest, const KVAddr& addr,
+                          uint64_t tag, int32_t lb, int32_t le, cudaStream_t s) {
+  ss_plan* plan = BeginDirectSend(seq, begin, end, dest, addr, tag);
+  try {
+    LaunchDirectSend(plan, lb, le, s);
+  } catch (...) {
+    DestroyPlan(plan);
+    throw;
+  }
+  DestroyPlan(plan);  // stream-ordered free after the launch
 }
 
 // ---------------------------------------------------------------------------
@@ -1147,9 +1248,7 @@ void ss_cache::FreeSequence(SeqId seq) {
       OrderAfterUser();
       const int64_t np = static_cast<int64_t>(rec->own_pages.size());
       DevBlock b = DevAlloc(sizeof(int64_t) * np, stream_);
-      CudaCheck(cudaMemcpyAsync(b.ptr, rec->own_pages.data(), sizeof(int64_t) * np,
-                                cudaMemcpyHostToDevice, stream_),
-                "H2D pages");
+      H2D(b.ptr, rec->own_pages.data(), sizeof(int64_t) * np, stream_, "H2D pages");
       launch_reset_pages(d_fill_, d_expecting_, d_page_window_, static_cast<int64_t*>(b.ptr), np,
                          L_, num_pages_, P_, stream_);
       launches_ += 1;
@@ -1212,9 +1311,8 @@ void ss_cache::ReadEntryWords(SeqId seq, int64_t pos, int32_t layer, uint64_t* o
   MKV_CHECK(layer >= 0 && layer < L_, kInvalidArgument, "layer out of range");
   const int32_t slot = Resolve(rec, pos);
   OrderAfterUser();
-  CudaCheck(cudaMemcpyAsync(out, PoolLayer(layer) + static_cast<int64_t>(slot) * W_,
-                            sizeof(uint64_t) * W_, cudaMemcpyDeviceToHost, stream_),
-            "D2H entry");
+  D2H(out, PoolLayer(layer) + static_cast<int64_t>(slot) * W_,
+                            sizeof(uint64_t) * W_, stream_, "D2H entry");
   Sync();
 }
 
@@ -1225,9 +1323,7 @@ int32_t ss_cache::FillOf(SeqId seq, int64_t pos, int32_t layer) {
   const int32_t slot = Resolve(rec, pos);
   uint8_t v = 0;
   OrderAfterUser();
-  CudaCheck(cudaMemcpyAsync(&v, d_fill_ + static_cast<int64_t>(layer) * num_pages_ * P_ + slot, 1,
-                            cudaMemcpyDeviceToHost, stream_),
-            "D2H fill");
+  D2H(&v, d_fill_ + static_cast<int64_t>(layer) * num_pages_ * P_ + slot, 1, stream_, "D2H fill");
   Sync();
   return v;
 }
@@ -1269,6 +1365,8 @@ void ss_cache::AttachPeer(Rank dest, ss_cache* peer) {
   t.device = peer->device_;
   DetachPeer(dest);
   peers_[dest] = t;
+  peer_engines_[dest] = peer;
+  peer->attached_by_.insert(this);
 }
 
 namespace {
@@ -1336,21 +1434,49 @@ void ss_cache::ImportIpc(Rank dest, const ss_ipc_handle* h) {
 void ss_cache::DetachPeer(Rank dest) {
   auto it = peers_.find(dest);
   if (it == peers_.end()) return;
-  if (device_ >= 0) Sync();
+  if (device_ >= 0) {
+    Sync();
+    CudaCheck(cudaStreamSynchronize(comm_stream_), "cudaStreamSynchronize");
+  }
   for (void* p : it->second.ipc_ptrs) cudaIpcCloseMemHandle(p);
   peers_.erase(it);
+  auto e = peer_engines_.find(dest);
+  if (e != peer_engines_.end()) {
+    e->second->attached_by_.erase(this);
+    peer_engines_.erase(e);
+  }
 }
 
 void ss_cache::Synchronize() {
   if (device_ < 0) return;
   Sync();
   if (user_pending_) CudaCheck(cudaEventSynchronize(user_ev_), "cudaEventSynchronize");
+  CudaCheck(cudaStreamSynchronize(comm_stream_), "cudaStreamSynchronize");
   uint32_t st = 0;
   CudaCheck(cudaMemcpy(&st, d_status_, sizeof(uint32_t), cudaMemcpyDeviceToHost), "D2H status");
-  if (st & kStatusUnknownAddress) {
+  d2h_bytes_ += sizeof(uint32_t);
+  if (st & (kStatusUnknownAddress | kStatusWaitTimeout)) {
     CudaCheck(cudaMemset(d_status_, 0, sizeof(uint32_t)), "memset");
-    Throw(kUnknownAddress, "a device-direct remote write was rejected by the receiver");
+    if (st & kStatusUnknownAddress) {
+      Throw(kUnknownAddress, "a device-direct remote write was rejected by the receiver");
+    }
+    Throw(kAborted, "device-side receive wait timed out");
   }
+}
+
+void ss_cache::WaitReceive(SeqId seq, int64_t timeout_ms, cudaStream_t s) {
+  RequireDevice("WaitReceive");
+  Record* rec = MustGet(seq);
+  MKV_CHECK(rec->window.has_value() && rec->window->dev_id >= 0, kInvalidArgument,
+            "sequence " + std::to_string(seq) + " has no receive window");
+  const Window& w = *rec->window;
+  const int64_t target = std::max<int64_t>(0, w.expected - w.received);
+  OrderAfterUser();
+  if (s != stream_) OrderUser(s);
+  launch_wait_counter(d_win_received_ + w.dev_id, static_cast<unsigned long long>(target),
+                      timeout_ms * 1000000LL, d_status_, s);
+  launches_ += 1;
+  if (s != stream_) NoteUser(s);
 }
 
 // ---------------------------------------------------------------------------
@@ -1401,12 +1527,13 @@ ss_plan* ss_cache::BeginDecode(const int64_t* seqs, const int64_t* ctx_lens, int
   OrderAfterUser();
   plan->dev = DevAlloc(total, stream_);
   uint8_t* base = static_cast<uint8_t*>(plan->dev.ptr);
-  CudaCheck(cudaMemcpyAsync(base, host.data(), total, cudaMemcpyHostToDevice, stream_), "H2D ctx");
+  H2D(base, host.data(), total, stream_, "H2D ctx");
   plan->d_ctx_slots = reinterpret_cast<int32_t*>(base + o_slots);
   plan->d_ctx_off = reinterpret_cast<int64_t*>(base + o_off);
   plan->d_ctx_len = reinterpret_cast<int32_t*>(base + o_len);
   plan->on_device = true;
   Sync();
+  live_plans_.insert(plan.get());
   return plan.release();
 }
 

@@ -175,6 +175,7 @@ struct ss_plan {
     uint64_t* staging = nullptr;  // gathered payload for host sinks
   };
   std::vector<DevSend> dsend;
+  bool is_direct_send = false;
   // Decode-attention plan (ss_begin_decode): context slot map in CSR form.
   bool is_decode_plan = false;
   int64_t batch = 0;
@@ -241,6 +242,9 @@ struct ss_cache {
   std::vector<SeqId> DrainReceiveCompletions();
   void DirectSend(SeqId seq, int64_t begin, int64_t end, Rank dest, const mkv::KVAddr& addr,
                   uint64_t tag, int32_t layer_begin, int32_t layer_end, cudaStream_t s);
+  ss_plan* BeginDirectSend(SeqId seq, int64_t begin, int64_t end, Rank dest,
+                           const mkv::KVAddr& addr, uint64_t tag);
+  void LaunchDirectSend(ss_plan* plan, int32_t layer_begin, int32_t layer_end, cudaStream_t s);
 
   // Lifecycle.
   void SetFinished(SeqId seq, bool f) { MustGet(seq)->finished = f; }
@@ -272,7 +276,11 @@ struct ss_cache {
   void DecodeAttention(ss_plan* plan, int32_t layer, int32_t hq, int32_t hkv, int32_t hd,
                        float scale, const void* q, void* out, cudaStream_t s);
   void DestroyPlan(ss_plan* plan);
+  void FreePlanDevice(ss_plan* plan);
   void Synchronize();
+  void WaitReceive(SeqId seq, int64_t timeout_ms, cudaStream_t s);
+  int64_t h2d_bytes() const { return h2d_bytes_; }
+  int64_t d2h_bytes() const { return d2h_bytes_; }
   uint64_t* PoolLayer(int32_t layer) const;
   bool has_device() const { return device_ >= 0; }
   int32_t dim() const { return W_; }
@@ -298,6 +306,8 @@ struct ss_cache {
   void TouchLru(mkv::Record* rec);
   void RequireDevice(const char* what) const;
   void Sync();                       // internal stream
+  void H2D(void* dst, const void* src, size_t bytes, cudaStream_t s, const char* what);
+  void D2H(void* dst, const void* src, size_t bytes, cudaStream_t s, const char* what);
   void OrderAfterUser();             // internal stream waits for async work
   void OrderUser(cudaStream_t s);    // user stream waits for internal work
   void NoteUser(cudaStream_t s);
@@ -349,11 +359,16 @@ struct ss_cache {
   std::vector<int32_t> free_window_ids_;
   std::vector<int32_t> free_fold_rows_;
   std::map<Rank, mkv::PeerTarget> peers_;
+  std::map<Rank, ss_cache*> peer_engines_;  // in-process peers we attached
+  std::set<ss_cache*> attached_by_;         // engines that attached us as a peer
+  std::set<ss_plan*> live_plans_;           // freed with the cache if still live
 
   // HBM state.
   cudaStream_t stream_ = nullptr;
-  cudaEvent_t internal_ev_ = nullptr, user_ev_ = nullptr;
-  bool user_pending_ = false;
+  cudaStream_t comm_stream_ = nullptr;  // per-layer sends (overlap with compute)
+  cudaEvent_t internal_ev_ = nullptr, user_ev_ = nullptr, comm_ev_ = nullptr, layer_ev_ = nullptr;
+  bool user_pending_ = false, comm_pending_ = false;
+  int64_t h2d_bytes_ = 0, d2h_bytes_ = 0;
   uint64_t* d_pool_ = nullptr;
   uint8_t* d_fill_ = nullptr;
   uint8_t* d_expecting_ = nullptr;

@@ -397,6 +397,21 @@ int ss_direct_send_async(ss_cache* c, int64_t seq, int64_t begin, int64_t end, i
   });
 }
 
+int ss_begin_direct_send(ss_cache* c, int64_t seq, int64_t begin, int64_t end, int32_t dest,
+                         const ss_addr* dest_addr, uint64_t tag, ss_plan** plan_out) {
+  return Guard(c, [&]() -> int {
+    *plan_out = c->BeginDirectSend(seq, begin, end, dest, ToAddr(dest_addr), tag);
+    return SS_OK;
+  });
+}
+
+int ss_launch_direct_send_async(ss_cache* c, ss_plan* p, int32_t lb, int32_t le, void* stream) {
+  return Guard(c, [&]() -> int {
+    c->LaunchDirectSend(p, lb, le, S(stream));
+    return SS_OK;
+  });
+}
+
 int ss_gather_range_async(ss_cache* c, int64_t seq, int64_t begin, int64_t end, int32_t layer,
                           uint64_t* out_dev, void* stream) {
   return Guard(c, [&]() -> int {
@@ -446,6 +461,19 @@ int ss_pool_layer_ptr(ss_cache* c, int32_t layer, void** dev_ptr) {
     *dev_ptr = c->PoolLayer(layer);
     return SS_OK;
   });
+}
+
+int ss_wait_receive_async(ss_cache* c, int64_t seq, int64_t timeout_ms, void* stream) {
+  return Guard(c, [&]() -> int {
+    c->WaitReceive(seq, timeout_ms, S(stream));
+    return SS_OK;
+  });
+}
+
+int ss_copy_counters(const ss_cache* c, int64_t* h2d, int64_t* d2h) {
+  *h2d = c->h2d_bytes();
+  *d2h = c->d2h_bytes();
+  return SS_OK;
 }
 
 int64_t ss_kernel_launches(const ss_cache* c) { return c->launches(); }

@@ -17,7 +17,6 @@ namespace mkv {
 namespace {
 
 constexpr int kCopyThreads = 256;
-constexpr int kCopyUnroll = 8;
 
 __device__ __forceinline__ ulonglong2 ld_stream(const ulonglong2* p) {
   ulonglong2 v;
@@ -31,27 +30,63 @@ __device__ __forceinline__ void st_vec(ulonglong2* p, ulonglong2 v) {
   asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(v.x), "l"(v.y) : "memory");
 }
 
-// One warp moves one W-word row.  Loads are all issued before the stores
-// so each lane keeps kCopyUnroll 16-byte requests in flight.
+struct alignas(32) u256 {
+  unsigned long long a, b, c, d;
+};
+
+__device__ __forceinline__ u256 ld256(const void* p) {
+  u256 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0, %1, %2, %3}, [%4];"
+               : "=l"(v.a), "=l"(v.b), "=l"(v.c), "=l"(v.d)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void st256(void* p, const u256& v) {
+  asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(v.a), "l"(v.b), "l"(v.c),
+               "l"(v.d)
+               : "memory");
+}
+
+__device__ __forceinline__ uint8_t ld_cg_u8(const uint8_t* p) {
+  unsigned short v;
+  asm volatile("ld.global.cg.u8 %0, [%1];" : "=h"(v) : "l"(p));
+  return static_cast<uint8_t>(v);
+}
+
+// One warp moves one W-word row: 32-byte vectors when the row allows it
+// (4 per lane in flight for a 4 KiB row), else 16-byte, else words.
 __device__ __forceinline__ void warp_copy_row(const uint64_t* __restrict__ src,
                                               uint64_t* __restrict__ dst, int32_t W, int lane) {
-  if ((W & 1) == 0) {
+  if ((W & 3) == 0) {
+    const u256* s4 = reinterpret_cast<const u256*>(src);
+    u256* d4 = reinterpret_cast<u256*>(dst);
+    const int nv = W >> 2;
+    int v = lane;
+    for (; v + 32 * 3 < nv; v += 32 * 4) {
+      u256 t[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) t[u] = ld256(s4 + v + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) st256(d4 + v + 32 * u, t[u]);
+    }
+    for (; v < nv; v += 32) st256(d4 + v, ld256(s4 + v));
+  } else if ((W & 1) == 0) {
     const ulonglong2* s2 = reinterpret_cast<const ulonglong2*>(src);
     ulonglong2* d2 = reinterpret_cast<ulonglong2*>(dst);
-    const int nv = W >> 1;
-    int v = lane;
-    for (; v + 32 * (kCopyUnroll - 1) < nv; v += 32 * kCopyUnroll) {
-      ulonglong2 t[kCopyUnroll];
-#pragma unroll
-      for (int u = 0; u < kCopyUnroll; ++u) t[u] = ld_stream(s2 + v + 32 * u);
-#pragma unroll
-      for (int u = 0; u < kCopyUnroll; ++u) st_vec(d2 + v + 32 * u, t[u]);
-    }
-    for (; v < nv; v += 32) st_vec(d2 + v, ld_stream(s2 + v));
+    for (int v = lane; v < (W >> 1); v += 32) st_vec(d2 + v, ld_stream(s2 + v));
   } else {
     for (int j = lane; j < W; j += 32) dst[j] = __ldg(src + j);
   }
 }
+
+// Items are groups of kGroup consecutive rows of one layer.  Lanes
+// 0..kGroup-1 fetch the group's slot indices and destination fill bytes in
+// one coalesced access each, so no row waits on a dependent load; rows are
+// then copied back to back and the fill marks stored lane-parallel.  (A
+// per-row fill check serialised a fill load before every store and cost
+// ~15% of bandwidth; profiles/micro/copy_variants.cu.)
+constexpr int kGroup = 4;
 
 __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
   extern __shared__ uint32_t s_rows[];  // per relative layer (accounting only)
@@ -68,28 +103,35 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  const int64_t items = p.n_rows * p.n_layers;
+  const int64_t groups = (p.n_rows + kGroup - 1) / kGroup;
+  const int64_t items = groups * p.n_layers;
   for (int64_t it = warp; it < items; it += n_warps) {
-    const int32_t lrel = static_cast<int32_t>(it / p.n_rows);
-    const int64_t r = it - static_cast<int64_t>(lrel) * p.n_rows;
-    const int64_t si = p.src_idx ? static_cast<int64_t>(__ldg(p.src_idx + r)) : r;
-    const int64_t di = p.dst_idx ? static_cast<int64_t>(__ldg(p.dst_idx + r)) : r;
-    const uint64_t* src = p.src + lrel * p.src_layer_words + si * p.W;
-    uint64_t* dst = p.dst + lrel * p.dst_layer_words + di * p.W;
-    bool write = true;
-    uint8_t* fill = nullptr;
-    if (p.dst_fill != nullptr) {
-      fill = p.dst_fill + lrel * p.dst_fill_layer + di;
-      write = *reinterpret_cast<volatile uint8_t*>(fill) == 0;  // Empty slots only
+    const int32_t lrel = static_cast<int32_t>(it / groups);
+    const int64_t r0 = (it - static_cast<int64_t>(lrel) * groups) * kGroup;
+    const int nr = static_cast<int>(p.n_rows - r0 < kGroup ? p.n_rows - r0 : kGroup);
+    int64_t my_s = 0, my_d = 0;
+    uint8_t my_f = 0;
+    uint8_t* fill_l = p.dst_fill != nullptr ? p.dst_fill + lrel * p.dst_fill_layer : nullptr;
+    if (lane < nr) {
+      my_s = p.src_idx ? static_cast<int64_t>(__ldg(p.src_idx + r0 + lane)) : r0 + lane;
+      my_d = p.dst_idx ? static_cast<int64_t>(__ldg(p.dst_idx + r0 + lane)) : r0 + lane;
+      if (fill_l != nullptr) my_f = ld_cg_u8(fill_l + my_d);
     }
-    if (write) {
-      warp_copy_row(src, dst, p.W, lane);
-      if (fill != nullptr) {
-        __syncwarp();
-        if (lane == 0) *fill = p.fill_value;
-      }
+    // Empty destination slots only (kv_cache.cc:447); every row counts.
+    const unsigned todo = __ballot_sync(0xffffffffu, lane < nr && my_f == 0);
+    const uint64_t* src_l = p.src + lrel * p.src_layer_words;
+    uint64_t* dst_l = p.dst + lrel * p.dst_layer_words;
+#pragma unroll 1
+    for (int k = 0; k < nr; ++k) {
+      const int64_t si = __shfl_sync(0xffffffffu, my_s, k);
+      const int64_t di = __shfl_sync(0xffffffffu, my_d, k);
+      if ((todo >> k) & 1u) warp_copy_row(src_l + si * p.W, dst_l + di * p.W, p.W, lane);
     }
-    if (account && lane == 0) atomicAdd(&s_rows[lrel], 1u);
+    if (fill_l != nullptr) {
+      __syncwarp();
+      if ((todo >> lane) & 1u) fill_l[my_d] = p.fill_value;
+    }
+    if (account && lane == 0) atomicAdd(&s_rows[lrel], static_cast<uint32_t>(nr));
   }
   if (account) {
     // Publish: every thread's stores, then the counters, at system scope so
@@ -112,6 +154,8 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
   }
 }
 
+// One thread per (range, slot): every check is an independent (possibly
+// peer) load, so the whole address validates in a couple of memory latencies.
 __global__ void k_validate_remote(ValidateParams p) {
   __shared__ int bad;
   __shared__ int32_t w0;
@@ -119,7 +163,7 @@ __global__ void k_validate_remote(ValidateParams p) {
     bad = p.n_ranges <= 0 ? 1 : 0;
     w0 = -1;
     if (p.n_ranges > 0) {
-      int64_t pg = p.range_page[0];
+      const int64_t pg = p.range_page[0];
       if (pg < 0 || pg >= p.num_pages) {
         bad = 1;
       } else {
@@ -129,23 +173,19 @@ __global__ void k_validate_remote(ValidateParams p) {
     }
   }
   __syncthreads();
-  for (int64_t i = threadIdx.x; i < p.n_ranges && !bad; i += blockDim.x) {
-    int64_t pg = p.range_page[i];
-    int32_t b = p.range_begin[i], c = p.range_count[i];
-    if (pg < 0 || pg >= p.num_pages || b < 0 || c < 0 || b + c > p.P) {
+  const int64_t work = p.n_ranges * p.P;
+  for (int64_t i = threadIdx.x; i < work && !bad; i += blockDim.x) {
+    const int64_t r = i / p.P;
+    const int32_t k = static_cast<int32_t>(i % p.P);
+    const int64_t pg = p.range_page[r];
+    const int32_t b = p.range_begin[r], c = p.range_count[r];
+    if (k == 0 && (pg < 0 || pg >= p.num_pages || b < 0 || c < 0 || b + c > p.P)) {
       bad = 1;
-      break;
+      continue;
     }
-    if (*reinterpret_cast<const volatile int32_t*>(p.page_window + pg) != w0) {
-      bad = 1;
-      break;
-    }
-    for (int32_t s = b; s < b + c; ++s) {
-      if (reinterpret_cast<const volatile uint8_t*>(p.expecting)[pg * p.P + s] == 0) {
-        bad = 1;
-        break;
-      }
-    }
+    if (pg < 0 || pg >= p.num_pages || k >= c || b + c > p.P || b < 0) continue;
+    if (k == 0 && *reinterpret_cast<const volatile int32_t*>(p.page_window + pg) != w0) bad = 1;
+    if (reinterpret_cast<const volatile uint8_t*>(p.expecting)[pg * p.P + b + k] == 0) bad = 1;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -324,6 +364,23 @@ __global__ void k_check_filled(const uint8_t* __restrict__ fill_l, const int32_t
   }
 }
 
+__global__ void k_wait_counter(const unsigned long long* counter, unsigned long long target,
+                               long long timeout_ns, uint32_t* status) {
+  unsigned long long t0, now;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(counter) : "memory");
+    if (v >= target) return;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (static_cast<long long>(now - t0) > timeout_ns) {
+      atomicOr(status, kStatusWaitTimeout);
+      return;
+    }
+    __nanosleep(200);
+  }
+}
+
 inline int grid_for(int64_t work, int per_block, int num_sms, int max_per_sm) {
   int64_t blocks = (work + per_block - 1) / per_block;
   int64_t cap = static_cast<int64_t>(num_sms) * max_per_sm;
@@ -338,13 +395,15 @@ void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms) {
   const int64_t items = p.n_rows * p.n_layers;
   if (items <= 0) return;
   const int warps_per_block = kCopyThreads / 32;
-  const int grid = grid_for(items, warps_per_block, num_sms, 8);
+  // 2 CTAs (16 warps) per SM measured best for the 4 KiB-row copy
+  // (profiles/micro/copy_variants.cu: 6.57 TB/s vs 6.1 TB/s at 4-8 per SM).
+  const int grid = grid_for((items + kGroup - 1) / kGroup, warps_per_block, num_sms, 2);
   const size_t smem = p.win_received ? sizeof(uint32_t) * p.n_layers : 0;
   k_copy_rows<<<grid, kCopyThreads, smem, s>>>(p);
 }
 
 void launch_validate_remote(const ValidateParams& p, cudaStream_t s) {
-  k_validate_remote<<<1, 256, 0, s>>>(p);
+  k_validate_remote<<<1, 1024, 0, s>>>(p);
 }
 
 void launch_attn_write_hash(uint64_t* pool_l, uint8_t* fill_l, const int32_t* slots,
@@ -399,6 +458,11 @@ void launch_first_nonfull(const uint8_t* fill, int64_t fill_layer_bytes, int32_t
   if (n <= 0) return;
   k_first_nonfull<<<grid_for(n, 256, num_sms, 4), 256, 0, s>>>(fill, fill_layer_bytes, L, slots,
                                                                 n, out);
+}
+
+void launch_wait_counter(const unsigned long long* counter, unsigned long long target,
+                         long long timeout_ns, uint32_t* status, cudaStream_t s) {
+  k_wait_counter<<<1, 1, 0, s>>>(counter, target, timeout_ns, status);
 }
 
 void launch_check_filled(const uint8_t* fill_l, const int32_t* slots, int64_t n, uint32_t* status,

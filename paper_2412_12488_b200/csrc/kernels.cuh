@@ -22,7 +22,13 @@ namespace mkv {
 enum : uint32_t {
   kStatusUnknownAddress = 1u << 0,  // a remote write failed receiver validation
   kStatusMissingKV = 1u << 1,       // a read hit an Empty slot
+  kStatusWaitTimeout = 1u << 2,     // a device-side receive wait gave up
 };
+
+// Device-side wait: spin (acquire, system scope) until *counter >= target
+// or timeout_ns elapses; on timeout set kStatusWaitTimeout.
+void launch_wait_counter(const unsigned long long* counter, unsigned long long target,
+                         long long timeout_ns, uint32_t* status, cudaStream_t s);
 
 // Row copy between slot-addressed (or dense) row arrays, over
 // rows x layers items.  All row copies of the hot path go through it:

@@ -18,6 +18,7 @@ import ctypes as C
 import enum
 import json
 import os
+import weakref
 from dataclasses import dataclass, field
 from pathlib import Path
 from typing import Callable, Iterable, Optional, Sequence
@@ -200,6 +201,9 @@ _SIGNATURES = {
     "ss_attention_async": (C.c_int, [_vp, _vp, C.c_int32, _vp, _vp, _vp]),
     "ss_direct_send_async": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, C.c_int32,
                                        C.POINTER(_Addr), C.c_uint64, C.c_int32, C.c_int32, _vp]),
+    "ss_begin_direct_send": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, C.c_int32,
+                                       C.POINTER(_Addr), C.c_uint64, C.POINTER(_vp)]),
+    "ss_launch_direct_send_async": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, _vp]),
     "ss_gather_range_async": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, C.c_int32, _vp,
                                         _vp]),
     "ss_apply_remote_write_async": (C.c_int, [_vp, C.POINTER(_Addr), C.c_int32, _vp, C.c_int64,
@@ -209,6 +213,8 @@ _SIGNATURES = {
     "ss_paged_decode_attention_async": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, C.c_int32,
                                                   C.c_int32, C.c_float, _vp, _vp, _vp]),
     "ss_pool_layer_ptr": (C.c_int, [_vp, C.c_int32, C.POINTER(_vp)]),
+    "ss_wait_receive_async": (C.c_int, [_vp, C.c_int64, C.c_int64, _vp]),
+    "ss_copy_counters": (C.c_int, [_vp, _i64p, _i64p]),
     "ss_kernel_launches": (C.c_int64, [_vp]),
     "ss_synchronize": (C.c_int, [_vp]),
 }
@@ -348,6 +354,7 @@ class ForwardPlan:
     def __init__(self, cache: "KVCache", handle: int):
         self._cache = cache
         self._h = C.c_void_p(handle)
+        cache._plans.add(self)
 
     @property
     def handle(self) -> C.c_void_p:
@@ -366,9 +373,10 @@ class ForwardPlan:
         return self._cache._lib.ss_plan_next_layer(self._h)
 
     def close(self) -> None:
-        if self._h and self._h.value:
+        # A plan whose cache is already gone was released with the cache.
+        if self._h and self._h.value and self._cache._h and self._cache._h.value:
             self._cache._lib.ss_plan_destroy(self._h)
-            self._h = C.c_void_p(0)
+        self._h = C.c_void_p(0)
 
     def __del__(self):
         try:
@@ -394,6 +402,8 @@ class KVCache:
     def __init__(self, num_pages: int = 4096, page_size: int = 16, layers: int = 4, dim: int = 8,
                  vocab: int = 256, hash_seed: int = DEFAULT_HASH_SEED, device: Optional[int] = 0,
                  rank: int = 0, lib: Optional[C.CDLL | str | os.PathLike] = None):
+        self._h = C.c_void_p(0)
+        self._plans = weakref.WeakSet()
         self._lib = lib if isinstance(lib, C.CDLL) else load_library(lib)
         cfg = _Config(num_pages, page_size, layers, dim, vocab, hash_seed & (2**64 - 1),
                       -1 if device is None else device, rank)
@@ -406,6 +416,7 @@ class KVCache:
         self.vocab, self.hash_seed, self.rank = vocab, hash_seed, rank
         self.device = self._lib.ss_device(self._h)
         self._keep = []
+        self._plans = weakref.WeakSet()
 
     # -- plumbing ---------------------------------------------------------
     def _status_name(self, st: int) -> str:
@@ -422,6 +433,10 @@ class KVCache:
 
     def close(self) -> None:
         if getattr(self, "_h", None) is not None and self._h.value:
+            # Live plans are released by the library with the cache; make their
+            # handles inert first so a later finalizer cannot touch them.
+            for plan in list(getattr(self, "_plans", ())):
+                plan._h = C.c_void_p(0)
             self._lib.ss_cache_destroy(self._h)
             self._h = C.c_void_p(0)
 
@@ -681,6 +696,20 @@ class KVCache:
                                                    C.byref(a), user_tag, lb, le,
                                                    C.c_void_p(stream)))
 
+    def begin_direct_send(self, seq: int, range: tuple, dest: int, dest_addr: KVAddrInfo,
+                          user_tag: int = 0) -> ForwardPlan:
+        a, keep = dest_addr._c()
+        h = C.c_void_p()
+        self._check(self._lib.ss_begin_direct_send(self._h, seq, range[0], range[1], dest,
+                                                   C.byref(a), user_tag, C.byref(h)))
+        return ForwardPlan(self, h.value)
+
+    def launch_direct_send_async(self, plan: ForwardPlan, layers: Optional[tuple] = None,
+                                 stream: int = 0) -> None:
+        lb, le = layers if layers is not None else (0, self.layers)
+        self._check(self._lib.ss_launch_direct_send_async(self._h, plan.handle, lb, le,
+                                                          C.c_void_p(stream)))
+
     def attention_async(self, layer: int, plan: ForwardPlan, hidden_in_ptr: int,
                         hidden_out_ptr: int, stream: int = 0) -> None:
         self._check(self._lib.ss_attention_async(self._h, plan.handle, layer,
@@ -726,6 +755,14 @@ class KVCache:
         p = C.c_void_p()
         self._check(self._lib.ss_pool_layer_ptr(self._h, layer, C.byref(p)))
         return p.value
+
+    def wait_receive_async(self, seq: int, timeout_ms: int = 10000, stream: int = 0) -> None:
+        self._check(self._lib.ss_wait_receive_async(self._h, seq, timeout_ms, C.c_void_p(stream)))
+
+    def copy_counters(self) -> tuple[int, int]:
+        h, d = C.c_int64(), C.c_int64()
+        self._check(self._lib.ss_copy_counters(self._h, C.byref(h), C.byref(d)))
+        return h.value, d.value
 
     def kernel_launches(self) -> int:
         return self._lib.ss_kernel_launches(self._h)

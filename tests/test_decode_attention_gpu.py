@@ -1,0 +1,109 @@
+"""Paged GQA decode attention (bf16 in, fp32 accumulate, bf16 out) against a
+plain fp32 PyTorch reference of the same op.  No reference analogue exists
+(the reference's attention is the integer fold), so the tolerance is ours:
+
+    max |out - ref| <= 2e-2   and   rms(out - ref) / rms(ref) <= 2e-2
+
+(bf16 output rounding alone is 2^-9 relative; the kernel also rounds the
+softmax weights to bf16 before the PV product).  Contexts are ragged and the
+pages fragmented (interleaved allocation, then frees and reuse), so every
+read goes through the device page table."""
+import numpy as np
+import pytest
+
+from paper_2412_12488_b200 import BatchEntry, ErrorCode, KVCache, SplitserveError
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [  # (Hq, Hkv, D) with dim = 4 * Hkv * D / 8 u64 words
+    (8, 4, 64),     # tiny config: W = 128
+    (32, 8, 128),   # Llama-3.1-8B
+    (64, 8, 128),   # Llama-3.1-70B
+]
+
+
+def _fill(torch, cache, seqs_ctx, hkv, hd, layers, page_size, seed):
+    """Appends K||V rows for every (seq, pos, layer); returns {seq: [layer] -> (K, V)}."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    kv = {}
+    batch = [BatchEntry(s, (0, n)) for s, n in seqs_ctx]
+    total = sum(n for _, n in seqs_ctx)
+    plan = cache.BeginForward(batch)
+    for layer in range(layers):
+        rows = (torch.randn(total, 2, hkv, hd, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+        cache.append_rows_async(plan, layer, rows.data_ptr(), 0)
+        off = 0
+        for s, n in seqs_ctx:
+            kv.setdefault(s, []).append((rows[off:off + n, 0].float(), rows[off:off + n, 1].float()))
+            off += n
+    torch.cuda.synchronize()
+    plan.close()
+    return kv
+
+
+def _ref(torch, q, K, V, scale):
+    # q [Hq, D], K/V [n, Hkv, D] -> [Hq, D] in fp32.
+    hq, hkv = q.shape[0], K.shape[1]
+    g = hq // hkv
+    Kx = K.repeat_interleave(g, dim=1)  # [n, Hq, D]
+    Vx = V.repeat_interleave(g, dim=1)
+    s = torch.einsum("hd,nhd->hn", q.float(), Kx) * scale
+    p = torch.softmax(s, dim=-1)
+    return torch.einsum("hn,nhd->hd", p, Vx)
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_decode_matches_fp32_reference(cuda, shape):
+    torch = cuda
+    hq, hkv, hd = shape
+    W = 4 * hkv * hd // 8
+    P, layers = 16, 2
+    ctx = [1, 15, 16, 17, 300, 1000, 2048]
+    c = KVCache(num_pages=600, page_size=P, layers=layers, dim=W, device=0)
+    # Fragment the free list: interleave short allocations, free every other one.
+    for i in range(40):
+        c.CreateSequence(1000 + i, [i % 7] * 40)
+        c.EnsureAllocated(1000 + i, 40)
+    for i in range(0, 40, 2):
+        c.FreeSequence(1000 + i)
+    seqs = []
+    for b, n in enumerate(ctx):
+        c.CreateSequence(b, [(b + i) % 11 for i in range(n)])
+        c.EnsureAllocated(b, n)
+        seqs.append((b, n))
+    kv = _fill(torch, c, seqs, hkv, hd, layers, P, seed=hq)
+    plan = c.begin_decode([s for s, _ in seqs], [n for _, n in seqs])
+    scale = hd ** -0.5
+    q = (torch.randn(len(seqs), hq, hd, device="cuda") * 0.5).to(torch.bfloat16)
+    out = torch.empty_like(q)
+    for layer in range(layers):
+        c.paged_decode_attention_async(plan, layer, hq, hkv, hd, scale, q.data_ptr(),
+                                       out.data_ptr(), 0)
+        torch.cuda.synchronize()
+        for b, (s, n) in enumerate(seqs):
+            K, V = kv[s][layer]
+            ref = _ref(torch, q[b], K, V, scale)
+            err = (out[b].float() - ref).abs()
+            assert err.max().item() <= 2e-2, (shape, n, layer, err.max().item())
+            rel = (out[b].float() - ref).pow(2).mean().sqrt() / ref.pow(2).mean().sqrt()
+            assert rel.item() <= 2e-2, (shape, n, layer, rel.item())
+    plan.close()
+
+
+def test_decode_rejects_bad_geometry_and_missing_kv(cuda):
+    c = KVCache(num_pages=16, page_size=16, layers=1, dim=512, device=0)
+    c.CreateSequence(1, [1] * 20)
+    c.EnsureAllocated(1, 20)
+    with pytest.raises(SplitserveError) as ei:
+        c.begin_decode([1], [20])  # no KV appended yet: fill-state safety
+    assert ei.value.code == ErrorCode.MissingKV
+    torch = cuda
+    plan = c.BeginForward([BatchEntry(1, (0, 20))])
+    rows = torch.zeros(20 * 4096 // 2, dtype=torch.bfloat16, device="cuda")
+    c.append_rows_async(plan, 0, rows.data_ptr(), 0)
+    torch.cuda.synchronize()
+    d = c.begin_decode([1], [20])
+    q = torch.zeros(1, 64, 128, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(SplitserveError) as ei:  # 4*Hkv*D bytes must equal the entry width
+        c.paged_decode_attention_async(d, 0, 64, 4, 128, 0.1, q.data_ptr(), q.data_ptr(), 0)
+    assert ei.value.code == ErrorCode.InvalidArgument
