@@ -63,9 +63,9 @@ def _peaks() -> tuple[float, str]:
         return FALLBACK_HBM, "fallback"
 
 
-def _prompt(seed: int = 1) -> list:
+def _prompt(seed: int = 1) -> np.ndarray:
     rng = np.random.Generator(np.random.MT19937(seed))
-    return [int(x) for x in rng.integers(0, 256, PROMPT)]
+    return rng.integers(0, 256, PROMPT).astype(np.int32)
 
 
 class ClockSampler:
@@ -267,21 +267,28 @@ def our_arm(args, rank: int, world: int) -> None:
     def step(i: int, timed_dev: list) -> None:
         seq = 100 + i
         if role == "both":
+            t0 = time.perf_counter()
             r = D.PrepRecv(seq, prompt, -1)
+            t1 = time.perf_counter()
             # Declaration (resolve + upload row maps) then computation (the
             # validation + copy launch), as in the reference's two stages.
             plan = P.begin_direct_send(1, (r.match_len, e), 1, r.addr, i)
+            t2 = time.perf_counter()
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ev0.record(stream)
             P.launch_direct_send_async(plan, (0, L), sid)
             ev1.record(stream)
+            t3 = time.perf_counter()
             timed_dev.append((ev0, ev1))
             done = []
             while not done:
                 done = D.DrainReceiveCompletions()
             assert done == [seq]
+            t4 = time.perf_counter()
             plan.close()
             D.FreeSequence(seq)
+            t5 = time.perf_counter()
+            phases.append((t1 - t0, t2 - t1, t3 - t2, t4 - t3, t5 - t4))
         elif role == "D":
             r = D.PrepRecv(seq, prompt, -1)
             dist.send_object_list([(r.match_len, r.addr)], dst=peer_rank)
@@ -303,6 +310,7 @@ def our_arm(args, rank: int, world: int) -> None:
             plan.close()
 
     # Warm-up.
+    phases: list = []
     scratch: list = []
     for i in range(args.warmup):
         step(i, scratch)
@@ -322,6 +330,7 @@ def our_arm(args, rank: int, world: int) -> None:
     l0 = sum(x.kernel_launches() for x in engines)
     c0 = [x.copy_counters() for x in engines]
     timed: list = []
+    phases.clear()
     sampler = ClockSampler(local)
     with sampler:
         barrier()
@@ -402,6 +411,10 @@ def our_arm(args, rank: int, world: int) -> None:
         "cpu_baseline": cpu_baseline,
         "clocks": sampler.summary(),
         "gpu_launches": int(launches),
+        "e2e_phases_us": None if not phases else {
+            k: round(1e6 * float(np.median([ph[j] for ph in phases])), 1)
+            for j, k in enumerate(["prep_recv", "begin_direct_send", "launch",
+                                   "wait_and_drain", "close_and_free"])},
         "secondary": secondary,
     }
     print(json.dumps(line), flush=True)

@@ -184,13 +184,13 @@ def addr_validate(a: KVAddrInfo):
 def addr_slice(a: KVAddrInfo, begin, end) -> KVAddrInfo:
     if not (begin >= a.token_begin and end <= a.token_begin + a.token_count and begin <= end):
         raise _err(ErrorCode.InvalidArgument, "slice outside address")
-    out, pos = KVAddrInfo([], begin, end - begin), a.token_begin
+    ranges, pos = [], a.token_begin
     for (p, b, c) in a.ranges:
         lo, hi = max(pos, begin), min(pos + c, end)
         if lo < hi:
-            out.ranges.append((p, b + (lo - pos), hi - lo))
+            ranges.append((p, b + (lo - pos), hi - lo))
         pos += c
-    return out
+    return KVAddrInfo(ranges, begin, end - begin)
 
 
 # ---------------------------------------------------------------------------

@@ -58,17 +58,30 @@ void CudaCheck(cudaError_t e, const char* what) {
   }
 }
 
-// kv_addr.cc:16-30
+// kv_addr.cc:16-30.  Same checks in the same order of precedence (a bad
+// range or an overlap raises InvalidArgument before the AddrMismatch total
+// check); overlaps are found on the ranges sorted by (page, begin) instead
+// of a per-slot set, O(R log R) in the number of ranges.
 void KVAddr::Validate() const {
   int64_t total = 0;
-  std::set<std::pair<int64_t, int32_t>> seen;
   for (const auto& r : ranges) {
     MKV_CHECK(r.slot_count > 0 && r.slot_begin >= 0, kInvalidArgument, "bad slot range");
-    for (int32_t s = 0; s < r.slot_count; ++s) {
-      MKV_CHECK(seen.insert({r.page_id, r.slot_begin + s}).second, kInvalidArgument,
-                "overlapping slot ranges");
-    }
     total += r.slot_count;
+  }
+  std::vector<std::pair<int64_t, int64_t>> iv;  // (page, begin) -> end via index
+  iv.reserve(ranges.size());
+  for (size_t i = 0; i < ranges.size(); ++i) iv.push_back({ranges[i].page_id, static_cast<int64_t>(i)});
+  std::sort(iv.begin(), iv.end(), [&](const auto& a, const auto& b) {
+    const auto& ra = ranges[a.second];
+    const auto& rb = ranges[b.second];
+    return ra.page_id != rb.page_id ? ra.page_id < rb.page_id : ra.slot_begin < rb.slot_begin;
+  });
+  for (size_t i = 1; i < iv.size(); ++i) {
+    const auto& prev = ranges[iv[i - 1].second];
+    const auto& cur = ranges[iv[i].second];
+    MKV_CHECK(!(prev.page_id == cur.page_id &&
+                static_cast<int64_t>(prev.slot_begin) + prev.slot_count > cur.slot_begin),
+              kInvalidArgument, "overlapping slot ranges");
   }
   MKV_CHECK(total == token_count, kAddrMismatch, "slot counts do not cover token_count");
 }
@@ -204,6 +217,11 @@ ss_cache::~ss_cache() {
     delete p;
   }
   live_plans_.clear();
+  if (device_ >= 0) {
+    for (auto& [id, rec] : records_) {
+      if (rec->d_slots != nullptr) cudaFree(rec->d_slots);
+    }
+  }
   if (device_ < 0) return;
   cudaSetDevice(device_);
   if (stream_) cudaStreamSynchronize(stream_);
@@ -274,23 +292,36 @@ void ss_cache::D2H(void* dst, const void* src, size_t bytes, cudaStream_t s, con
   d2h_bytes_ += static_cast<int64_t>(bytes);
 }
 
+// Cross-stream ordering between the internal stream (bookkeeping uploads,
+// resets) and caller streams (async data path).  Event records and waits
+// are skipped when nothing new was enqueued on the other side.
 void ss_cache::OrderAfterUser() {
-  if (user_pending_) {
+  if (user_pending_ && user_gen_ != user_waited_gen_) {
     CudaCheck(cudaStreamWaitEvent(stream_, user_ev_, 0), "cudaStreamWaitEvent");
+    user_waited_gen_ = user_gen_;
   }
-  if (comm_pending_) {
+  if (comm_pending_ && comm_gen_ != comm_waited_gen_) {
     CudaCheck(cudaStreamWaitEvent(stream_, comm_ev_, 0), "cudaStreamWaitEvent");
+    comm_waited_gen_ = comm_gen_;
   }
+  ++internal_gen_;  // the caller is about to enqueue internal work
 }
 
 void ss_cache::OrderUser(cudaStream_t s) {
-  CudaCheck(cudaEventRecord(internal_ev_, stream_), "cudaEventRecord");
+  if (internal_gen_ != internal_recorded_gen_) {
+    CudaCheck(cudaEventRecord(internal_ev_, stream_), "cudaEventRecord");
+    internal_recorded_gen_ = internal_gen_;
+  }
+  auto it = user_stream_seen_.find(s);
+  if (it != user_stream_seen_.end() && it->second == internal_recorded_gen_) return;
   CudaCheck(cudaStreamWaitEvent(s, internal_ev_, 0), "cudaStreamWaitEvent");
+  user_stream_seen_[s] = internal_recorded_gen_;
 }
 
 void ss_cache::NoteUser(cudaStream_t s) {
   CudaCheck(cudaEventRecord(user_ev_, s), "cudaEventRecord");
   user_pending_ = true;
+  ++user_gen_;
 }
 
 DevBlock ss_cache::DevAlloc(size_t bytes, cudaStream_t s) {
@@ -330,13 +361,10 @@ int64_t ss_cache::DeviceFirstNonFull(const Record* rec, int64_t from, int64_t to
   if (from >= to) return to;
   OrderAfterUser();
   const int64_t n = to - from;
-  DevBlock b = DevAlloc(sizeof(int32_t) * n, stream_);
-  H2D(b.ptr, rec->slots.data() + from, sizeof(int32_t) * n, stream_, "H2D slots");
-  launch_first_nonfull(d_fill_, num_pages_ * P_, L_, static_cast<int32_t*>(b.ptr), n, d_scratch_,
-                       stream_, num_sms_);
+  launch_first_nonfull(d_fill_, num_pages_ * P_, L_, rec->d_slots + from, n, d_scratch_, stream_,
+                       num_sms_);
   launches_ += 1;
   D2H(h_pinned_, d_scratch_, sizeof(unsigned long long), stream_, "D2H scan");
-  DevFree(b, stream_);
   Sync();
   const unsigned long long r = h_pinned_[0];
   return r >= static_cast<unsigned long long>(n) ? to : from + static_cast<int64_t>(r);
@@ -378,6 +406,34 @@ void ss_cache::CheckFilled(const Record* rec, int64_t begin, int64_t end, int32_
   MKV_CHECK((st & kStatusMissingKV) == 0, kMissingKV, what);
 }
 
+// Grows the sequence's HBM page table to alloc_len and uploads the newly
+// resolved positions [old_len, alloc_len) (stream-ordered on the internal
+// stream; async users are ordered after it by OrderUser).
+void ss_cache::SyncDeviceTable(Record* rec, int64_t old_len) {
+  if (device_ < 0) return;
+  const int64_t need = rec->alloc_len;
+  OrderAfterUser();
+  if (need > rec->d_cap) {
+    const int64_t cap = std::max<int64_t>({need, 2 * rec->d_cap, 256});
+    int32_t* nt = nullptr;
+    CudaCheck(cudaMallocAsync(&nt, sizeof(int32_t) * cap, stream_), "cudaMallocAsync table");
+    if (rec->d_slots != nullptr) {
+      if (old_len > 0) {
+        CudaCheck(cudaMemcpyAsync(nt, rec->d_slots, sizeof(int32_t) * old_len,
+                                  cudaMemcpyDeviceToDevice, stream_),
+                  "D2D table");
+      }
+      cudaFreeAsync(rec->d_slots, stream_);
+    }
+    rec->d_slots = nt;
+    rec->d_cap = cap;
+  }
+  if (need > old_len) {
+    H2D(rec->d_slots + old_len, rec->slots.data() + old_len, sizeof(int32_t) * (need - old_len),
+        stream_, "H2D table");
+  }
+}
+
 // kv_cache.cc:104-110
 void ss_cache::TouchLru(Record* rec) {
   if (tree_.Contains(rec->id)) {
@@ -405,6 +461,7 @@ Record* ss_cache::CreateSequence(SeqId seq, std::vector<Token> tokens) {
     MKV_ICHECK(!free_fold_rows_.empty(), "too many live sequences");
     rec->fold_row = free_fold_rows_.back();
     free_fold_rows_.pop_back();
+    OrderAfterUser();
     CudaCheck(cudaMemsetAsync(d_fold_sums_ + static_cast<int64_t>(rec->fold_row) * L_, 0,
                               sizeof(uint64_t) * L_, stream_),
               "memset fold sums");
@@ -442,6 +499,7 @@ Record* ss_cache::ForkSequence(SeqId parent, SeqId child, int64_t fork_len,
   rec->alloc_len = fork_len;
   rec->committed_hint = fork_len;
   rec->slots.assign(p->slots.begin(), p->slots.begin() + fork_len);
+  SyncDeviceTable(rec, 0);
   if (rec->parent >= 0) ++p->refcount;
   TouchLru(p);
   return rec;
@@ -456,6 +514,7 @@ void ss_cache::EnsureAllocated(SeqId seq, int64_t upto) {
   MKV_CHECK(need <= static_cast<int64_t>(free_pages_.size()), kOutOfPages,
             std::to_string(need) + " pages needed, " + std::to_string(free_pages_.size()) +
                 " free");
+  const int64_t old_len = rec->alloc_len;
   for (int64_t i = 0; i < need; ++i) {
     const int64_t page = free_pages_.back();
     free_pages_.pop_back();
@@ -464,6 +523,7 @@ void ss_cache::EnsureAllocated(SeqId seq, int64_t upto) {
     for (int32_t s = 0; s < P_; ++s) rec->slots.push_back(static_cast<int32_t>(page * P_ + s));
   }
   rec->alloc_len = rec->fork_len + static_cast<int64_t>(rec->own_pages.size()) * P_;
+  if (need > 0) SyncDeviceTable(rec, old_len);
 }
 
 void ss_cache::AppendToken(SeqId seq, Token t) { MustGet(seq)->tokens.push_back(t); }
@@ -842,6 +902,7 @@ void ss_cache::AttentionAsync(ss_plan* plan, int32_t layer, const uint64_t* hin,
     }
     CudaCheck(cudaEventRecord(comm_ev_, comm_stream_), "cudaEventRecord");
     comm_pending_ = true;
+    ++comm_gen_;
   }
   if (s != stream_) NoteUser(s);
   ++plan->next_layer;
@@ -930,18 +991,16 @@ void ss_cache::GatherRange(SeqId seq, int64_t begin, int64_t end, int32_t layer,
   const Record* rec = MustGet(seq);
   MKV_CHECK(layer >= 0 && layer < L_, kInvalidArgument, "layer out of range");
   MKV_CHECK(begin >= 0 && begin <= end, kInvalidArgument, "bad gather range");
-  for (int64_t pos = begin; pos < end; ++pos) Resolve(rec, pos);
+  MKV_ICHECK(end <= rec->alloc_len, "position not allocated");
   if (end > rec->committed_hint) AdvanceCommitted(MustGet(seq));
   CheckFilled(rec, begin, end, layer, "gather over empty slot", nullptr);
   const int64_t n = end - begin;
   if (n == 0) return;
   OrderAfterUser();
   if (s != stream_) OrderUser(s);
-  DevBlock b = DevAlloc(sizeof(int32_t) * n, s);
-  H2D(b.ptr, rec->slots.data() + begin, sizeof(int32_t) * n, s, "H2D slots");
   CopyParams c{};
   c.src = PoolLayer(layer);
-  c.src_idx = static_cast<int32_t*>(b.ptr);
+  c.src_idx = rec->d_slots + begin;
   c.dst = out;
   c.n_rows = n;
   c.layer0 = layer;
@@ -949,7 +1008,6 @@ void ss_cache::GatherRange(SeqId seq, int64_t begin, int64_t end, int32_t layer,
   c.W = W_;
   launch_copy_rows(c, s, num_sms_);
   launches_ += 1;
-  DevFree(b, s);
   if (s != stream_) NoteUser(s);
 }
 
@@ -1135,7 +1193,7 @@ ss_plan* ss_cache::BeginDirectSend(SeqId seq, int64_t begin, int64_t end, Rank d
                 std::to_string(end - begin));
   MKV_CHECK(addr.token_begin == begin, kAddrMismatch, "destination token_begin mismatch");
   PeerFor(dest);
-  for (int64_t pos = begin; pos < end; ++pos) Resolve(rec, pos);
+  MKV_ICHECK(end <= rec->alloc_len, "position not allocated");
   auto plan = std::make_unique<ss_plan>();
   plan->owner = this;
   PlanSend ps;
@@ -1150,15 +1208,14 @@ ss_plan* ss_cache::BeginDirectSend(SeqId seq, int64_t begin, int64_t end, Rank d
   std::vector<int64_t> rp;
   std::vector<int32_t> rb, rc;
   ExpandAddr(addr, &dst, &rp, &rb, &rc);
-  const int64_t n = end - begin, nr = static_cast<int64_t>(rp.size());
-  const size_t o_src = 0, o_dst = Align(sizeof(int32_t) * n);
+  const int64_t nr = static_cast<int64_t>(rp.size());
+  const size_t o_dst = 0;
   const size_t o_rp = o_dst + Align(sizeof(int32_t) * dst.size());
   const size_t o_rb = o_rp + Align(sizeof(int64_t) * nr);
   const size_t o_rc = o_rb + Align(sizeof(int32_t) * nr);
   const size_t o_v = o_rc + Align(sizeof(int32_t) * nr);
   const size_t total = o_v + Align(sizeof(int32_t));
   std::vector<uint8_t> host(total, 0);
-  std::memcpy(host.data() + o_src, rec->slots.data() + begin, sizeof(int32_t) * n);
   std::memcpy(host.data() + o_dst, dst.data(), sizeof(int32_t) * dst.size());
   std::memcpy(host.data() + o_rp, rp.data(), sizeof(int64_t) * nr);
   std::memcpy(host.data() + o_rb, rb.data(), sizeof(int32_t) * nr);
@@ -1169,7 +1226,7 @@ ss_plan* ss_cache::BeginDirectSend(SeqId seq, int64_t begin, int64_t end, Rank d
   H2D(base, host.data(), total, stream_, "H2D send");
   plan->dsend.resize(1);
   auto& d = plan->dsend[0];
-  d.src_slots = reinterpret_cast<int32_t*>(base + o_src);
+  d.src_slots = nullptr;  // read from the sender's HBM page table at launch
   d.dst_slots = reinterpret_cast<int32_t*>(base + o_dst);
   d.range_page = reinterpret_cast<int64_t*>(base + o_rp);
   d.range_begin = reinterpret_cast<int32_t*>(base + o_rb);
@@ -1199,9 +1256,9 @@ void ss_cache::LaunchDirectSend(ss_plan* plan, int32_t lb, int32_t le, cudaStrea
   OrderAfterUser();
   if (s != stream_) OrderUser(s);
   const auto& d = plan->dsend[0];
-  LaunchRemote(peer, d.src_slots, d.dst_slots, d.range_page, d.range_begin, d.range_count,
-               static_cast<int64_t>(snd.dest_addr.ranges.size()), d.verdict, snd.end - snd.begin,
-               lb, le, s);
+  LaunchRemote(peer, rec->d_slots + snd.begin, d.dst_slots, d.range_page, d.range_begin,
+               d.range_count, static_cast<int64_t>(snd.dest_addr.ranges.size()), d.verdict,
+               snd.end - snd.begin, lb, le, s);
   if (s != stream_) NoteUser(s);
 }
 
@@ -1256,6 +1313,11 @@ void ss_cache::FreeSequence(SeqId seq) {
       Sync();
     }
     if (rec->fold_row >= 0) free_fold_rows_.push_back(rec->fold_row);
+    if (rec->d_slots != nullptr) {
+      OrderAfterUser();
+      cudaFreeAsync(rec->d_slots, stream_);
+      rec->d_slots = nullptr;
+    }
   }
   if (rec->parent >= 0) {
     auto it = records_.find(rec->parent);
@@ -1508,17 +1570,19 @@ ss_plan* ss_cache::BeginDecode(const int64_t* seqs, const int64_t* ctx_lens, int
     off[b + 1] = off[b] + n;
     max_ctx = std::max(max_ctx, n);
   }
-  const size_t o_slots = 0, o_off = Align(sizeof(int32_t) * off[batch]);
+  const size_t o_off = 0;
   const size_t o_len = o_off + Align(sizeof(int64_t) * (batch + 1));
-  const size_t total = o_len + Align(sizeof(int32_t) * batch);
-  std::vector<uint8_t> host(total, 0);
-  for (int64_t b = 0; b < batch; ++b) {
-    const Record* rec = MustGet(seqs[b]);
-    std::memcpy(host.data() + o_slots + sizeof(int32_t) * off[b], rec->slots.data(),
-                sizeof(int32_t) * len[b]);
-  }
+  const size_t o_tab = o_len + Align(sizeof(int32_t) * batch);
+  const size_t o_slots = o_tab + Align(sizeof(int32_t*) * batch);
+  const size_t upload = o_slots;
+  const size_t total = o_slots + Align(sizeof(int32_t) * off[batch]);
+  std::vector<uint8_t> host(upload, 0);
   std::memcpy(host.data() + o_off, off.data(), sizeof(int64_t) * (batch + 1));
   std::memcpy(host.data() + o_len, len.data(), sizeof(int32_t) * batch);
+  for (int64_t b = 0; b < batch; ++b) {
+    const int32_t* t = MustGet(seqs[b])->d_slots;
+    std::memcpy(host.data() + o_tab + sizeof(int32_t*) * b, &t, sizeof(t));
+  }
   auto plan = std::make_unique<ss_plan>();
   plan->owner = this;
   plan->is_decode_plan = true;
@@ -1527,7 +1591,12 @@ ss_plan* ss_cache::BeginDecode(const int64_t* seqs, const int64_t* ctx_lens, int
   OrderAfterUser();
   plan->dev = DevAlloc(total, stream_);
   uint8_t* base = static_cast<uint8_t*>(plan->dev.ptr);
-  H2D(base, host.data(), total, stream_, "H2D ctx");
+  H2D(base, host.data(), upload, stream_, "H2D ctx");
+  launch_gather_tables(reinterpret_cast<const int32_t* const*>(base + o_tab),
+                       reinterpret_cast<const int64_t*>(base + o_off),
+                       reinterpret_cast<const int32_t*>(base + o_len), batch, off[batch],
+                       reinterpret_cast<int32_t*>(base + o_slots), stream_, num_sms_);
+  launches_ += 1;
   plan->d_ctx_slots = reinterpret_cast<int32_t*>(base + o_slots);
   plan->d_ctx_off = reinterpret_cast<int64_t*>(base + o_off);
   plan->d_ctx_len = reinterpret_cast<int32_t*>(base + o_len);
@@ -1548,10 +1617,23 @@ void ss_cache::DecodeAttention(ss_plan* plan, int32_t layer, int32_t hq, int32_t
   MKV_CHECK(static_cast<int64_t>(W_) * 8 == 4LL * hkv * hd, kInvalidArgument,
             "entry width must equal K||V bf16 bytes (dim * 8 == 4 * num_kv_heads * head_dim)");
   if (plan->num_splits == 0) {
-    const int64_t ctas = plan->batch * hkv;
-    int64_t target = static_cast<int64_t>(num_sms_) * 3 * 2;
-    int64_t splits = (target + ctas - 1) / ctas;
-    splits = std::max<int64_t>(1, std::min<int64_t>(splits, (plan->max_ctx + 63) / 64));
+    // Persistent grid of resident CTAs; ~6 (split, head, batch) items each
+    // so ragged contexts and the last round balance out.
+    plan->decode_grid = decode_attn_resident_ctas(hd, num_sms_);
+    const int64_t pairs = plan->batch * hkv, grid = plan->decode_grid;
+    // Splits minimising rounds x per-item time, with a per-item overhead
+    // worth ~128 tokens (Q load, warp merge, partial write).
+    const int64_t max_splits = std::max<int64_t>(1, (plan->max_ctx + 63) / 64);
+    int64_t splits = 1;
+    double best = 1e300;
+    for (int64_t sp = 1; sp <= max_splits; ++sp) {
+      const double rounds = static_cast<double>((pairs * sp + grid - 1) / grid);
+      const double t = rounds * (static_cast<double>(plan->max_ctx) / sp + 128.0);
+      if (t < best - 1e-9) {
+        best = t;
+        splits = sp;
+      }
+    }
     plan->num_splits = static_cast<int32_t>(splits);
     const int64_t heads = plan->batch * hq;
     float* po = nullptr;
@@ -1564,7 +1646,8 @@ void ss_cache::DecodeAttention(ss_plan* plan, int32_t layer, int32_t hq, int32_t
   const bool ok = launch_decode_attn(PoolLayer(layer), static_cast<int64_t>(W_) * 4,
                                      plan->d_ctx_slots, plan->d_ctx_off, plan->d_ctx_len, q,
                                      static_cast<int>(plan->batch), hq, hkv, hd, scale,
-                                     plan->num_splits, plan->d_partial, plan->d_partial_ml, out, s);
+                                     plan->num_splits, plan->d_partial, plan->d_partial_ml, out,
+                                     plan->decode_grid, s);
   MKV_CHECK(ok, kInvalidArgument, "unsupported head_dim");
   launches_ += 2;
   if (s != stream_) NoteUser(s);

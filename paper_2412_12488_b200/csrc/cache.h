@@ -117,6 +117,10 @@ struct Record {
   // prefix at fork time, which is equivalent since shared prefixes are
   // immutable while referenced).
   std::vector<int32_t> slots;
+  // The same page table in HBM (device-resident, grown with the host copy):
+  // every kernel that walks a sequence's positions reads it directly.
+  int32_t* d_slots = nullptr;
+  int64_t d_cap = 0;
   int32_t fold_row = -1;     // row of this sequence in the device fold-sum table
   int64_t touched_end = 0;   // positions >= this were never written by a forward pass
 };
@@ -186,6 +190,7 @@ struct ss_plan {
   float* d_partial = nullptr;       // split-KV partial outputs
   float* d_partial_ml = nullptr;    // split-KV (max, sum) per head
   int32_t num_splits = 0;
+  int32_t decode_grid = 0;
 };
 
 namespace mkv {
@@ -327,6 +332,7 @@ struct ss_cache {
   void ExpandAddr(const mkv::KVAddr& a, std::vector<int32_t>* slots, std::vector<int64_t>* rp,
                   std::vector<int32_t>* rb, std::vector<int32_t>* rc) const;
   void OpenDeviceWindow(mkv::Record* rec, int64_t m, int64_t e);
+  void SyncDeviceTable(mkv::Record* rec, int64_t old_len);
   void PollDeviceWindows();
   void ThrowIfDeviceStatus();
 
@@ -368,6 +374,9 @@ struct ss_cache {
   cudaStream_t comm_stream_ = nullptr;  // per-layer sends (overlap with compute)
   cudaEvent_t internal_ev_ = nullptr, user_ev_ = nullptr, comm_ev_ = nullptr, layer_ev_ = nullptr;
   bool user_pending_ = false, comm_pending_ = false;
+  uint64_t user_gen_ = 0, user_waited_gen_ = 0, comm_gen_ = 0, comm_waited_gen_ = 0;
+  uint64_t internal_gen_ = 1, internal_recorded_gen_ = 0;
+  std::map<cudaStream_t, uint64_t> user_stream_seen_;
   int64_t h2d_bytes_ = 0, d2h_bytes_ = 0;
   uint64_t* d_pool_ = nullptr;
   uint8_t* d_fill_ = nullptr;

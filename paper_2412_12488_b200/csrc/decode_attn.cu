@@ -84,13 +84,19 @@ __global__ void __launch_bounds__(kWarps * 32) k_decode_attn(
     const __nv_bfloat16* __restrict__ pool_l, int64_t row_elems, const int32_t* __restrict__ slots,
     const int64_t* __restrict__ ctx_off, const int32_t* __restrict__ ctx_len,
     const __nv_bfloat16* __restrict__ q, int Hq, int Hkv, float scale_log2, int splits,
-    float* __restrict__ part_o, float* __restrict__ part_ml) {
+    int n_batch, float* __restrict__ part_o, float* __restrict__ part_ml) {
   static_assert(D % 16 == 0 && D <= 256, "head_dim");
   constexpr int kChunks = D / 8;             // 16-byte chunks per row
   constexpr int kTileBytes = kTile * D * 2;  // one K or V tile
   extern __shared__ __align__(128) uint8_t smem[];
-  const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int G = Hq / Hkv;
+  const int64_t n_items = static_cast<int64_t>(splits) * Hkv * n_batch;
+  // Persistent CTAs walk (split, kv_head, batch) items round-robin.
+  for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+  const int split = static_cast<int>(item % splits);
+  const int h = static_cast<int>((item / splits) % Hkv);
+  const int b = static_cast<int>(item / (static_cast<int64_t>(splits) * Hkv));
+  __syncthreads();  // the previous item's reduction used the tile buffers
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int len = ctx_len[b];
   int chunk = (len + splits - 1) / splits;
@@ -272,6 +278,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_decode_attn(
       part_ml[(qh * splits + split) * 2 + 1] = lsum;
     }
   }
+  }  // items
 }
 
 // Merge split partials: out = sum_s w_s O_s / sum_s w_s, w_s = l_s 2^(m_s - M).
@@ -304,27 +311,39 @@ size_t decode_attn_smem(int head_dim) {
   return tiles > red ? tiles : red;
 }
 
+int decode_attn_resident_ctas(int head_dim, int num_sms) {
+  const size_t smem = decode_attn_smem(head_dim);
+  int per_sm = 1;
+  if (head_dim == 128) {
+    cudaFuncSetAttribute(k_decode_attn<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_decode_attn<128>, kWarps * 32, smem);
+  } else {
+    cudaFuncSetAttribute(k_decode_attn<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_decode_attn<64>, kWarps * 32, smem);
+  }
+  return (per_sm < 1 ? 1 : per_sm) * num_sms;
+}
+
 bool launch_decode_attn(const void* pool_l, int64_t row_elems, const int32_t* slots,
                         const int64_t* ctx_off, const int32_t* ctx_len, const void* q, int batch,
                         int Hq, int Hkv, int D, float scale, int splits, float* part_o,
-                        float* part_ml, void* out, cudaStream_t s) {
+                        float* part_ml, void* out, int grid, cudaStream_t s) {
   const float scale_log2 = scale * 1.4426950408889634f;
-  const dim3 grid(splits, Hkv, batch);
+  const int64_t items = static_cast<int64_t>(splits) * Hkv * batch;
+  const int g = static_cast<int>(items < grid ? items : grid);
   const size_t smem = decode_attn_smem(D);
   auto q16 = static_cast<const __nv_bfloat16*>(q);
   auto pool16 = static_cast<const __nv_bfloat16*>(pool_l);
   if (D == 128) {
-    cudaFuncSetAttribute(k_decode_attn<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    k_decode_attn<128><<<grid, kWarps * 32, smem, s>>>(pool16, row_elems, slots, ctx_off, ctx_len,
-                                                       q16, Hq, Hkv, scale_log2, splits, part_o,
-                                                       part_ml);
+    k_decode_attn<128><<<g, kWarps * 32, smem, s>>>(pool16, row_elems, slots, ctx_off, ctx_len,
+                                                    q16, Hq, Hkv, scale_log2, splits, batch,
+                                                    part_o, part_ml);
   } else if (D == 64) {
-    cudaFuncSetAttribute(k_decode_attn<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    k_decode_attn<64><<<grid, kWarps * 32, smem, s>>>(pool16, row_elems, slots, ctx_off, ctx_len,
-                                                      q16, Hq, Hkv, scale_log2, splits, part_o,
-                                                      part_ml);
+    k_decode_attn<64><<<g, kWarps * 32, smem, s>>>(pool16, row_elems, slots, ctx_off, ctx_len,
+                                                   q16, Hq, Hkv, scale_log2, splits, batch,
+                                                   part_o, part_ml);
   } else {
     return false;
   }

@@ -92,7 +92,9 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
   extern __shared__ uint32_t s_rows[];  // per relative layer (accounting only)
   int32_t window = -1;
   if (p.verdict != nullptr) {
-    window = *reinterpret_cast<const volatile int32_t*>(p.verdict);
+    window = reinterpret_cast<const volatile int32_t*>(p.verdict)[1] != 0
+                 ? -1
+                 : reinterpret_cast<const volatile int32_t*>(p.verdict)[0];
     if (window < 0) return;  // rejected by validation: no writes, no counts
   }
   const bool account = p.win_received != nullptr;
@@ -154,43 +156,40 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
   }
 }
 
-// One thread per (range, slot): every check is an independent (possibly
-// peer) load, so the whole address validates in a couple of memory latencies.
+// One thread per (range, slot) across as many CTAs as needed: every check
+// is an independent (possibly peer) load, so the address validates in about
+// one memory latency.  verdict[0] = window of the first page (block 0),
+// verdict[1] = any failure (zeroed by the launcher).
 __global__ void k_validate_remote(ValidateParams p) {
-  __shared__ int bad;
-  __shared__ int32_t w0;
-  if (threadIdx.x == 0) {
-    bad = p.n_ranges <= 0 ? 1 : 0;
-    w0 = -1;
-    if (p.n_ranges > 0) {
-      const int64_t pg = p.range_page[0];
-      if (pg < 0 || pg >= p.num_pages) {
-        bad = 1;
-      } else {
-        w0 = *reinterpret_cast<const volatile int32_t*>(p.page_window + pg);
-        if (w0 < 0) bad = 1;
-      }
+  const int64_t work = p.n_ranges * p.P;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  int32_t w0 = -1;
+  bool bad = p.n_ranges <= 0;
+  if (p.n_ranges > 0) {
+    const int64_t pg0 = p.range_page[0];
+    if (pg0 < 0 || pg0 >= p.num_pages) {
+      bad = true;
+    } else {
+      w0 = *reinterpret_cast<const volatile int32_t*>(p.page_window + pg0);
+      if (w0 < 0) bad = true;
     }
   }
-  __syncthreads();
-  const int64_t work = p.n_ranges * p.P;
-  for (int64_t i = threadIdx.x; i < work && !bad; i += blockDim.x) {
+  if (i == 0) p.verdict[0] = w0;
+  if (!bad && i < work) {
     const int64_t r = i / p.P;
     const int32_t k = static_cast<int32_t>(i % p.P);
     const int64_t pg = p.range_page[r];
     const int32_t b = p.range_begin[r], c = p.range_count[r];
-    if (k == 0 && (pg < 0 || pg >= p.num_pages || b < 0 || c < 0 || b + c > p.P)) {
-      bad = 1;
-      continue;
+    if (pg < 0 || pg >= p.num_pages || b < 0 || c < 0 || b + c > p.P) {
+      bad = true;
+    } else if (k < c) {
+      if (k == 0 && *reinterpret_cast<const volatile int32_t*>(p.page_window + pg) != w0) bad = true;
+      if (reinterpret_cast<const volatile uint8_t*>(p.expecting)[pg * p.P + b + k] == 0) bad = true;
     }
-    if (pg < 0 || pg >= p.num_pages || k >= c || b + c > p.P || b < 0) continue;
-    if (k == 0 && *reinterpret_cast<const volatile int32_t*>(p.page_window + pg) != w0) bad = 1;
-    if (reinterpret_cast<const volatile uint8_t*>(p.expecting)[pg * p.P + b + k] == 0) bad = 1;
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    *p.verdict = bad ? -1 : w0;
-    if (bad && p.status != nullptr) atomicOr(p.status, kStatusUnknownAddress);
+  if (bad && (i < work || i == 0)) {
+    atomicOr(reinterpret_cast<unsigned int*>(p.verdict + 1), 1u);
+    if (p.status != nullptr) atomicOr(p.status, kStatusUnknownAddress);
   }
 }
 
@@ -355,6 +354,19 @@ __global__ void k_first_nonfull(const uint8_t* __restrict__ fill, int64_t fill_l
   }
 }
 
+__global__ void k_gather_tables(const int32_t* const* __restrict__ tables,
+                                const int64_t* __restrict__ off, const int32_t* __restrict__ len,
+                                int64_t batch, int32_t* __restrict__ out) {
+  for (int64_t b = blockIdx.y; b < batch; b += gridDim.y) {
+    const int32_t* t = tables[b];
+    const int64_t o = off[b];
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < len[b];
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+      out[o + i] = t[i];
+    }
+  }
+}
+
 __global__ void k_check_filled(const uint8_t* __restrict__ fill_l, const int32_t* __restrict__ slots,
                                int64_t n, uint32_t* status) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -397,13 +409,20 @@ void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms) {
   const int warps_per_block = kCopyThreads / 32;
   // 2 CTAs (16 warps) per SM measured best for the 4 KiB-row copy
   // (profiles/micro/copy_variants.cu: 6.57 TB/s vs 6.1 TB/s at 4-8 per SM).
-  const int grid = grid_for((items + kGroup - 1) / kGroup, warps_per_block, num_sms, 2);
+  const int64_t groups = (p.n_rows + kGroup - 1) / kGroup * p.n_layers;
+  const int per_sm = groups >= static_cast<int64_t>(num_sms) * 2 * warps_per_block * 8 ? 2 : 8;
+  const int grid = grid_for(groups, warps_per_block, num_sms, per_sm);
   const size_t smem = p.win_received ? sizeof(uint32_t) * p.n_layers : 0;
   k_copy_rows<<<grid, kCopyThreads, smem, s>>>(p);
 }
 
 void launch_validate_remote(const ValidateParams& p, cudaStream_t s) {
-  k_validate_remote<<<1, 1024, 0, s>>>(p);
+  cudaMemsetAsync(p.verdict + 1, 0, sizeof(int32_t), s);
+  int64_t work = p.n_ranges * p.P;
+  int64_t grid = (work + 255) / 256;
+  if (grid < 1) grid = 1;
+  if (grid > 65535) grid = 65535;
+  k_validate_remote<<<static_cast<unsigned>(grid), 256, 0, s>>>(p);
 }
 
 void launch_attn_write_hash(uint64_t* pool_l, uint8_t* fill_l, const int32_t* slots,
@@ -463,6 +482,16 @@ void launch_first_nonfull(const uint8_t* fill, int64_t fill_layer_bytes, int32_t
 void launch_wait_counter(const unsigned long long* counter, unsigned long long target,
                          long long timeout_ns, uint32_t* status, cudaStream_t s) {
   k_wait_counter<<<1, 1, 0, s>>>(counter, target, timeout_ns, status);
+}
+
+void launch_gather_tables(const int32_t* const* tables, const int64_t* off, const int32_t* len,
+                          int64_t batch, int64_t total, int32_t* out, cudaStream_t s, int num_sms) {
+  if (batch <= 0 || total <= 0) return;
+  const int64_t per = (total / batch + 255) / 256;
+  dim3 grid(static_cast<unsigned>(per < 64 ? (per < 1 ? 1 : per) : 64),
+            static_cast<unsigned>(batch < 1024 ? batch : 1024));
+  (void)num_sms;
+  k_gather_tables<<<grid, 256, 0, s>>>(tables, off, len, batch, out);
 }
 
 void launch_check_filled(const uint8_t* fill_l, const int32_t* slots, int64_t n, uint32_t* status,

@@ -71,7 +71,7 @@ struct ValidateParams {
   const uint8_t* expecting;    // destination engine [pages][P]
   int64_t num_pages;
   int32_t P;
-  int32_t* verdict;
+  int32_t* verdict;            // [0] window id, [1] failure flag
   uint32_t* status;            // sender-side sticky status (kStatusUnknownAddress)
 };
 void launch_validate_remote(const ValidateParams& p, cudaStream_t s);
@@ -118,15 +118,21 @@ void launch_first_nonfull(const uint8_t* fill, int64_t fill_layer_bytes, int32_t
                           const int32_t* slots, int64_t n, unsigned long long* out,
                           cudaStream_t s, int num_sms);
 
+// Concatenate per-sequence device page tables into a CSR slot map:
+// out[off[b] + t] = tables[b][t] for t < len[b].
+void launch_gather_tables(const int32_t* const* tables, const int64_t* off, const int32_t* len,
+                          int64_t batch, int64_t total, int32_t* out, cudaStream_t s, int num_sms);
+
 // Any Empty fill on `layer` among the slot rows -> status |= kStatusMissingKV.
 void launch_check_filled(const uint8_t* fill_l, const int32_t* slots, int64_t n, uint32_t* status,
                          cudaStream_t s, int num_sms);
 
 // Paged GQA decode attention (decode_attn.cu): split-KV partials + combine.
 size_t decode_attn_smem(int head_dim);
+int decode_attn_resident_ctas(int head_dim, int num_sms);
 bool launch_decode_attn(const void* pool_l, int64_t row_elems, const int32_t* slots,
                         const int64_t* ctx_off, const int32_t* ctx_len, const void* q, int batch,
                         int Hq, int Hkv, int D, float scale, int splits, float* part_o,
-                        float* part_ml, void* out, cudaStream_t s);
+                        float* part_ml, void* out, int grid, cudaStream_t s);
 
 }  // namespace mkv

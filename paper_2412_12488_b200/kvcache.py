@@ -250,8 +250,12 @@ def load_library(path: Optional[os.PathLike | str] = None) -> C.CDLL:
 
 
 def _tok(tokens: Iterable[int]) -> np.ndarray:
-    return np.ascontiguousarray(np.asarray(list(tokens) if not isinstance(tokens, np.ndarray)
-                                           else tokens, dtype=np.int32))
+    if isinstance(tokens, np.ndarray) and tokens.dtype == np.int32 and tokens.flags.c_contiguous:
+        return tokens
+    if isinstance(tokens, np.ndarray):
+        return np.ascontiguousarray(tokens, dtype=np.int32)
+    return np.fromiter(tokens, dtype=np.int32) if not isinstance(tokens, (list, tuple)) else \
+        np.array(tokens, dtype=np.int32)
 
 
 def _ptr(a: np.ndarray, ctype):
@@ -261,26 +265,70 @@ def _ptr(a: np.ndarray, ctype):
 # ---------------------------------------------------------------------------
 # Plain-data types
 # ---------------------------------------------------------------------------
-@dataclass
-class KVAddrInfo:
-    """KVAddrInfo (kv_addr.h:30-48): run-length (page_id, slot_begin, slot_count)."""
+SLOT_RANGE_DTYPE = np.dtype([("page_id", "<i8"), ("slot_begin", "<i4"), ("slot_count", "<i4")])
+assert SLOT_RANGE_DTYPE.itemsize == C.sizeof(_SlotRange)
 
-    ranges: list = field(default_factory=list)
-    token_begin: int = 0
-    token_count: int = 0
+
+class KVAddrInfo:
+    """KVAddrInfo (kv_addr.h:30-48): run-length (page_id, slot_begin, slot_count).
+
+    The ranges live in a numpy array laid out like ``ss_slot_range`` so an
+    address returned by prep_recv goes back into mark_send / direct_send
+    without per-range Python work; ``ranges`` gives the tuples."""
+
+    __slots__ = ("_arr", "token_begin", "token_count", "_list")
+
+    def __init__(self, ranges=(), token_begin: int = 0, token_count: int = 0):
+        if isinstance(ranges, np.ndarray) and ranges.dtype == SLOT_RANGE_DTYPE:
+            self._arr = np.ascontiguousarray(ranges)
+        else:
+            rl = [tuple(int(v) for v in r) for r in ranges]
+            self._arr = np.array(rl, dtype=SLOT_RANGE_DTYPE) if rl else np.zeros(0, SLOT_RANGE_DTYPE)
+        self.token_begin = int(token_begin)
+        self.token_count = int(token_count)
+        self._list = None
+
+    @property
+    def ranges(self) -> list:
+        if self._list is None:
+            self._list = [(int(p), int(b), int(c)) for p, b, c in self._arr.tolist()]
+        return self._list
+
+    @property
+    def array(self) -> np.ndarray:
+        return self._arr
+
+    def __eq__(self, other) -> bool:
+        return (isinstance(other, KVAddrInfo) and self.token_begin == other.token_begin
+                and self.token_count == other.token_count
+                and np.array_equal(self._arr, other._arr))
+
+    def __repr__(self) -> str:
+        return (f"KVAddrInfo(ranges={self.ranges}, token_begin={self.token_begin}, "
+                f"token_count={self.token_count})")
+
+    def __getstate__(self):
+        return (self._arr, self.token_begin, self.token_count)
+
+    def __setstate__(self, st):
+        self._arr, self.token_begin, self.token_count = st
+        self._list = None
 
     def _c(self) -> tuple[_Addr, object]:
-        arr = (_SlotRange * max(1, len(self.ranges)))()
-        for i, (p, b, c) in enumerate(self.ranges):
-            arr[i].page_id, arr[i].slot_begin, arr[i].slot_count = int(p), int(b), int(c)
-        a = _Addr(int(self.token_begin), int(self.token_count), len(self.ranges), arr,
-                  len(self.ranges))
+        arr = self._arr if len(self._arr) else np.zeros(1, SLOT_RANGE_DTYPE)
+        a = _Addr(self.token_begin, self.token_count, len(self._arr),
+                  arr.ctypes.data_as(C.POINTER(_SlotRange)), len(self._arr))
         return a, arr
 
     @staticmethod
     def _from_c(a: _Addr) -> "KVAddrInfo":
-        return KVAddrInfo([(a.ranges[i].page_id, a.ranges[i].slot_begin, a.ranges[i].slot_count)
-                           for i in range(a.n_ranges)], a.token_begin, a.token_count)
+        n = int(a.n_ranges)
+        if n:
+            raw = C.string_at(a.ranges, n * SLOT_RANGE_DTYPE.itemsize)
+            arr = np.frombuffer(raw, dtype=SLOT_RANGE_DTYPE).copy()
+        else:
+            arr = np.zeros(0, SLOT_RANGE_DTYPE)
+        return KVAddrInfo(arr, a.token_begin, a.token_count)
 
     def Validate(self, lib: Optional[C.CDLL] = None) -> None:  # kv_addr.cc:16-30
         lib = lib or load_library()
@@ -292,7 +340,7 @@ class KVAddrInfo:
     def Slice(self, begin: int, end: int, lib: Optional[C.CDLL] = None) -> "KVAddrInfo":
         lib = lib or load_library()  # kv_addr.cc:32-51
         a, keep = self._c()
-        cap = max(1, len(self.ranges))
+        cap = max(1, len(self._arr))
         out_arr = (_SlotRange * cap)()
         out = _Addr(0, 0, 0, out_arr, cap)
         st = lib.ss_addr_slice(C.byref(a), begin, end, C.byref(out))
@@ -301,9 +349,9 @@ class KVAddrInfo:
         return KVAddrInfo._from_c(out)
 
     def ToJson(self) -> str:  # kv_addr.cc:53-58 (nlohmann dump: sorted keys, no spaces)
-        return json.dumps({"ranges": [list(map(int, r)) for r in self.ranges],
-                           "token_begin": int(self.token_begin),
-                           "token_count": int(self.token_count)}, separators=(",", ":"))
+        return json.dumps({"ranges": [list(r) for r in self.ranges],
+                           "token_begin": self.token_begin,
+                           "token_count": self.token_count}, separators=(",", ":"))
 
     @staticmethod
     def FromJson(text: str) -> "KVAddrInfo":  # kv_addr.cc:60-70
