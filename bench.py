@@ -228,6 +228,8 @@ def our_arm(args, rank: int, world: int) -> None:
     from paper_2412_12488_b200 import KVCache
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("MICROKV_SHARE_DEVICE") == "1":
+        local = 0  # test hook: run the N>1 pair protocol with every rank on cuda:0
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("gloo")
@@ -517,7 +519,11 @@ def measure_append_gather(torch) -> dict:
     plan = C_.BeginForward([BatchEntry(1, (0, n))])
     rows = torch.randint(-2**62, 2**62, (n * W,), dtype=torch.int64, device="cuda")
     s = torch.cuda.Stream()
+    # The per-layer launches are queued behind a sleep kernel so they run back
+    # to back: the events time the device work, not the host's launch rate.
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    with torch.cuda.stream(s):
+        torch.cuda._sleep(30_000_000)
     ev[0].record(s)
     for layer in range(L):
         C_.append_rows_async(plan, layer, rows.data_ptr(), s.cuda_stream)
@@ -525,7 +531,11 @@ def measure_append_gather(torch) -> dict:
     torch.cuda.synchronize()
     app_s = ev[0].elapsed_time(ev[1]) / 1e3
     out = torch.empty(n * W, dtype=torch.int64, device="cuda")
+    C_.gather_range_async(1, (0, n), 0, out.data_ptr(), s.cuda_stream)  # committed scan, once
+    torch.cuda.synchronize()
     g = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    with torch.cuda.stream(s):
+        torch.cuda._sleep(30_000_000)
     g[0].record(s)
     for layer in range(L):
         C_.gather_range_async(1, (0, n), layer, out.data_ptr(), s.cuda_stream)
@@ -538,7 +548,8 @@ def measure_append_gather(torch) -> dict:
     return {"append_gbs": round(alg / app_s / 1e9, 1), "append_frac": round(alg / app_s / 1e9 / peak, 4),
             "gather_gbs": round(alg / gat_s / 1e9, 1), "gather_frac": round(alg / gat_s / 1e9 / peak, 4),
             "tokens": n, "layers": L, "launches_per_op": L,
-            "algorithmic_bytes": alg, "note": "read+write bytes; 80 launches each"}
+            "algorithmic_bytes": alg,
+            "note": "read+write bytes; 80 per-layer launches each, queued back to back"}
 
 
 def measure_decode(torch) -> dict:
@@ -548,7 +559,7 @@ def measure_decode(torch) -> dict:
     peak, _ = _peaks()
     res = {}
     Ld = 2
-    for (B, ctx) in ((8, 8192), (32, 8192), (128, 4096)):
+    for (B, ctx) in ((8, 8192), (32, 8192), (128, 4096), (8, 32768)):
         pages = B * (ctx // PAGE) + 16
         Cd = KVCache(num_pages=pages, page_size=PAGE, layers=Ld, dim=W, device=0)
         rng = np.random.default_rng(5)
@@ -570,6 +581,8 @@ def measure_decode(torch) -> dict:
                                             o.data_ptr(), s.cuda_stream)
         reps = 10
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        with torch.cuda.stream(s):
+            torch.cuda._sleep(20_000_000)
         ev[0].record(s)
         for i in range(reps):
             Cd.paged_decode_attention_async(dplan, i % Ld, HQ, HKV, HD, HD ** -0.5, q.data_ptr(),

@@ -8,6 +8,7 @@
 #include "cache.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 
@@ -1588,6 +1589,7 @@ ss_plan* ss_cache::BeginDecode(const int64_t* seqs, const int64_t* ctx_lens, int
   plan->is_decode_plan = true;
   plan->batch = batch;
   plan->max_ctx = max_ctx;
+  plan->ctx_lens = len;
   OrderAfterUser();
   plan->dev = DevAlloc(total, stream_);
   uint8_t* base = static_cast<uint8_t*>(plan->dev.ptr);
@@ -1616,38 +1618,41 @@ void ss_cache::DecodeAttention(ss_plan* plan, int32_t layer, int32_t hq, int32_t
   MKV_CHECK(hd == 64 || hd == 128, kInvalidArgument, "head_dim must be 64 or 128");
   MKV_CHECK(static_cast<int64_t>(W_) * 8 == 4LL * hkv * hd, kInvalidArgument,
             "entry width must equal K||V bf16 bytes (dim * 8 == 4 * num_kv_heads * head_dim)");
-  if (plan->num_splits == 0) {
-    // Persistent grid of resident CTAs; ~6 (split, head, batch) items each
-    // so ragged contexts and the last round balance out.
+  if (plan->decode_grid == 0 || plan->decode_hkv != hkv || plan->decode_hq != hq ||
+      plan->decode_hd != hd) {
+    // Tile prefix sums over segments (batch, kv head) for the stream-K split,
+    // and partial storage for at most grid + segments pieces.
     plan->decode_grid = decode_attn_resident_ctas(hd, num_sms_);
-    const int64_t pairs = plan->batch * hkv, grid = plan->decode_grid;
-    // Splits minimising rounds x per-item time, with a per-item overhead
-    // worth ~128 tokens (Q load, warp merge, partial write).
-    const int64_t max_splits = std::max<int64_t>(1, (plan->max_ctx + 63) / 64);
-    int64_t splits = 1;
-    double best = 1e300;
-    for (int64_t sp = 1; sp <= max_splits; ++sp) {
-      const double rounds = static_cast<double>((pairs * sp + grid - 1) / grid);
-      const double t = rounds * (static_cast<double>(plan->max_ctx) / sp + 128.0);
-      if (t < best - 1e-9) {
-        best = t;
-        splits = sp;
-      }
+    const int64_t n_seg = plan->batch * hkv;
+    std::vector<int64_t> seg(n_seg + 1, 0);
+    for (int64_t b = 0; b < plan->batch; ++b) {
+      const int64_t tiles = (plan->ctx_lens[b] + 15) / 16;
+      for (int32_t h = 0; h < hkv; ++h) seg[b * hkv + h + 1] = seg[b * hkv + h] + tiles;
     }
-    plan->num_splits = static_cast<int32_t>(splits);
-    const int64_t heads = plan->batch * hq;
-    float* po = nullptr;
-    CudaCheck(cudaMalloc(&po, sizeof(float) * heads * splits * (hd + 2)), "cudaMalloc partials");
-    plan->d_partial = po;
-    plan->d_partial_ml = po + heads * splits * hd;
+    plan->total_tiles = seg[n_seg];
+    Sync();
+    if (plan->d_partial) cudaFree(plan->d_partial);
+    const int64_t pieces = plan->decode_grid + n_seg;
+    const int64_t G = hq / hkv;
+    const size_t bytes_o = sizeof(float) * pieces * G * hd, bytes_ml = sizeof(float) * pieces * G * 2;
+    uint8_t* buf = nullptr;
+    CudaCheck(cudaMalloc(&buf, bytes_o + bytes_ml + sizeof(int64_t) * (n_seg + 1)), "cudaMalloc partials");
+    plan->d_partial = reinterpret_cast<float*>(buf);
+    plan->d_partial_ml = reinterpret_cast<float*>(buf + bytes_o);
+    plan->d_seg_start = reinterpret_cast<int64_t*>(buf + bytes_o + bytes_ml);
+    H2D(plan->d_seg_start, seg.data(), sizeof(int64_t) * (n_seg + 1), stream_, "H2D segments");
+    plan->decode_hkv = hkv;
+    plan->decode_hq = hq;
+    plan->decode_hd = hd;
   }
   OrderAfterUser();
   if (s != stream_) OrderUser(s);
   const bool ok = launch_decode_attn(PoolLayer(layer), static_cast<int64_t>(W_) * 4,
-                                     plan->d_ctx_slots, plan->d_ctx_off, plan->d_ctx_len, q,
+                                     plan->d_ctx_slots, plan->d_ctx_off, plan->d_ctx_len,
+                                     plan->d_seg_start, plan->batch * hkv, plan->total_tiles, q,
                                      static_cast<int>(plan->batch), hq, hkv, hd, scale,
-                                     plan->num_splits, plan->d_partial, plan->d_partial_ml, out,
-                                     plan->decode_grid, s);
+                                     plan->d_partial, plan->d_partial_ml, out, plan->decode_grid,
+                                     s);
   MKV_CHECK(ok, kInvalidArgument, "unsupported head_dim");
   launches_ += 2;
   if (s != stream_) NoteUser(s);

@@ -187,9 +187,12 @@ struct ss_plan {
   int32_t* d_ctx_slots = nullptr;
   int64_t* d_ctx_off = nullptr;
   int32_t* d_ctx_len = nullptr;
-  float* d_partial = nullptr;       // split-KV partial outputs
-  float* d_partial_ml = nullptr;    // split-KV (max, sum) per head
-  int32_t num_splits = 0;
+  std::vector<int32_t> ctx_lens;
+  float* d_partial = nullptr;       // per-piece partial outputs (stream-K)
+  float* d_partial_ml = nullptr;    // per-piece (max, sum) per head
+  int64_t* d_seg_start = nullptr;   // tile prefix sums over (batch, kv head)
+  int64_t total_tiles = 0;
+  int32_t decode_hkv = 0, decode_hq = 0, decode_hd = 0;
   int32_t decode_grid = 0;
 };
 

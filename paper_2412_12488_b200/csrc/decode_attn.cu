@@ -1,22 +1,30 @@
 // decode_attn.cu — paged GQA decode attention over the KV pool (sm_100a).
 //
 // No reference analogue (the reference's "attention" is the integer fold,
-// kv_cache.cc:319-351); numerics are checked against a CPU fp32
-// restatement (tests/test_decode_attention_gpu.py, tolerance stated there).
+// kv_cache.cc:319-351); numerics are checked against a plain fp32 PyTorch
+// reference (tests/test_decode_attention_gpu.py, tolerance stated there).
 //
 // Each (token, layer) entry of the pool is one row of dim u64 words holding
 // K[Hkv][D] then V[Hkv][D] in bf16, addressed through the decode plan's
-// per-position slot map (the device page table).  Split-KV (flash-decoding):
-// CTA (split, kv_head, batch) folds its token chunk for the G = Hq/Hkv query
-// heads of that KV head, 4 warps x 16-token tiles, then a combine kernel
-// merges the splits.
+// per-position slot map (gathered from the device page tables).
+//
+// Work split (stream-K): segment s = (batch b, kv head h) owns
+// ceil(ctx_b / 16) tiles of 16 tokens; seg_start[] is their prefix sum (T
+// tiles in all).  A resident-sized grid gives CTA c the equal share
+// [c*T/grid, (c+1)*T/grid), which may finish one segment and start the
+// next.  Each (CTA, segment) piece folds its tiles for the G = Hq/Hkv query
+// heads of that KV head (4 warps, 16-token tiles, double-buffered cp.async)
+// and writes one normalised partial (O, m, l) at index c + s — unique,
+// because pieces are ordered by both c and s.  A combine kernel merges each
+// segment's pieces.  Equal shares remove the wave-quantisation loss of
+// per-(split, head, batch) work items.
 //
 // Why tensor cores: per 4 KiB token row the group does 2*G*D*Hkv = 16 K
 // FMAs at the 70B shape (G = 8), i.e. 26 T FMA/s at the 6.5 TB/s HBM
 // roofline — 72% of the FP32 CUDA-core peak before any softmax or
-// conversion work — so QK^T and PV run as bf16 mma.sync m16n8k16 with
-// fp32 accumulation (M = query heads of the group, padded to 16).  The
-// kernel is HBM-bound; the MMA pipe is far from saturated.
+// conversion work — so QK^T and PV run as bf16 mma.sync m16n8k16 with fp32
+// accumulation (M = query heads of the group, padded to 16).  The kernel is
+// HBM-bound; the MMA pipe is far from saturated.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -79,227 +87,310 @@ __device__ __forceinline__ uint32_t tile_off(int r, int c) {
   return static_cast<uint32_t>(r * (D * 2) + ((c ^ (r & 7)) * 16));
 }
 
+__host__ __device__ __forceinline__ int64_t cta_tile_start(int64_t c, int64_t T, int64_t grid) {
+  return c * T / grid;
+}
+
+// Shared memory per CTA: [warp][stage][K|V][16][D] tiles, then Q [16][D]
+// (swizzled like the tiles; rows >= G zero).  The end-of-piece warp merge
+// reuses the tile area.
 template <int D>
-__global__ void __launch_bounds__(kWarps * 32) k_decode_attn(
+__host__ __device__ constexpr size_t tiles_bytes() {
+  return static_cast<size_t>(kWarps) * 4 * kTile * D * 2;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kWarps * 32, 3) k_decode_attn(
     const __nv_bfloat16* __restrict__ pool_l, int64_t row_elems, const int32_t* __restrict__ slots,
     const int64_t* __restrict__ ctx_off, const int32_t* __restrict__ ctx_len,
-    const __nv_bfloat16* __restrict__ q, int Hq, int Hkv, float scale_log2, int splits,
-    int n_batch, float* __restrict__ part_o, float* __restrict__ part_ml) {
+    const int64_t* __restrict__ seg_start, int64_t n_seg, const __nv_bfloat16* __restrict__ q,
+    int Hq, int Hkv, float scale_log2, float* __restrict__ part_o, float* __restrict__ part_ml,
+    __nv_bfloat16* __restrict__ out) {
   static_assert(D % 16 == 0 && D <= 256, "head_dim");
   constexpr int kChunks = D / 8;             // 16-byte chunks per row
   constexpr int kTileBytes = kTile * D * 2;  // one K or V tile
   extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* q_sm = smem + tiles_bytes<D>();
   const int G = Hq / Hkv;
-  const int64_t n_items = static_cast<int64_t>(splits) * Hkv * n_batch;
-  // Persistent CTAs walk (split, kv_head, batch) items round-robin.
-  for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
-  const int split = static_cast<int>(item % splits);
-  const int h = static_cast<int>((item / splits) % Hkv);
-  const int b = static_cast<int>(item / (static_cast<int64_t>(splits) * Hkv));
-  __syncthreads();  // the previous item's reduction used the tile buffers
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int len = ctx_len[b];
-  int chunk = (len + splits - 1) / splits;
-  chunk = (chunk + kTile - 1) / kTile * kTile;
-  const int t_begin = split * chunk;
-  const int t_end = min(len, t_begin + chunk);
-  const int32_t* sl = slots + ctx_off[b];
-
-  // Q fragments (A operand, rows = query heads of this group, zero-padded).
-  uint32_t qa[D / 16][4];
-  {
-    const int r0 = lane >> 2, r1 = r0 + 8, c = 2 * (lane & 3);
-    const __nv_bfloat16* qb = q + (static_cast<int64_t>(b) * Hq + static_cast<int64_t>(h) * G) * D;
-#pragma unroll
-    for (int kk = 0; kk < D / 16; ++kk) {
-      auto ld2 = [&](int r, int col) -> uint32_t {
-        if (r >= G) return 0u;
-        return *reinterpret_cast<const uint32_t*>(qb + static_cast<int64_t>(r) * D + col);
-      };
-      qa[kk][0] = ld2(r0, kk * 16 + c);
-      qa[kk][1] = ld2(r1, kk * 16 + c);
-      qa[kk][2] = ld2(r0, kk * 16 + c + 8);
-      qa[kk][3] = ld2(r1, kk * 16 + c + 8);
-    }
+  const int64_t T = seg_start[n_seg];
+  int64_t t0 = cta_tile_start(blockIdx.x, T, gridDim.x);
+  const int64_t t1 = cta_tile_start(blockIdx.x + 1, T, gridDim.x);
+  if (t0 >= t1) return;
+  // Last segment whose first tile is <= t0 (binary search on the prefix sums).
+  int64_t lo = 0, hi = n_seg - 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) >> 1;
+    if (seg_start[mid] <= t0) lo = mid; else hi = mid - 1;
   }
-
-  float o[D / 8][4];
-#pragma unroll
-  for (int j = 0; j < D / 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
-
-  uint8_t* wsm = smem + warp * (4 * kTileBytes);  // [stage][K|V][16][D]
-  const int n_tiles = t_end > t_begin ? (t_end - t_begin + kTile - 1) / kTile : 0;
-  const int64_t k_off = static_cast<int64_t>(h) * D, v_off = static_cast<int64_t>(Hkv + h) * D;
-
-  auto load_tile = [&](int tile, int stage) {
-    const int t0 = t_begin + tile * kTile;
-    const uint32_t kbase = smem_u32(wsm + stage * 2 * kTileBytes);
-    const uint32_t vbase = kbase + kTileBytes;
-#pragma unroll
-    for (int i = lane; i < kTile * kChunks; i += 32) {
-      const int r = i / kChunks, c = i % kChunks;
-      const int t = t0 + r;
-      const bool valid = t < t_end;
-      const int64_t slot = valid ? static_cast<int64_t>(__ldg(sl + t)) : 0;
-      const __nv_bfloat16* row = pool_l + slot * row_elems;
-      cp_async16(kbase + tile_off<D>(r, c), row + k_off + c * 8, valid);
-      cp_async16(vbase + tile_off<D>(r, c), row + v_off + c * 8, valid);
+  for (int64_t sgi = lo; t0 < t1 && sgi < n_seg; ++sgi) {
+    const int64_t s_begin = seg_start[sgi], s_end = seg_start[sgi + 1];
+    if (s_end <= t0) continue;  // empty segment
+    const int64_t pe = s_end < t1 ? s_end : t1;
+    const int b = static_cast<int>(sgi / Hkv), h = static_cast<int>(sgi % Hkv);
+    const int len = ctx_len[b];
+    const int first_tile = static_cast<int>(t0 - s_begin);
+    const int n_tiles = static_cast<int>(pe - t0);
+    const int tok0 = first_tile * kTile;
+    const int tok_end = min(len, (first_tile + n_tiles) * kTile);
+    const int32_t* sl = slots + ctx_off[b];
+    __syncthreads();  // the previous piece's merge used the tile area
+    {  // Stage the group's Q rows (coalesced 16-byte loads).
+      const __nv_bfloat16* qb =
+          q + (static_cast<int64_t>(b) * Hq + static_cast<int64_t>(h) * G) * D;
+      for (int i = threadIdx.x; i < kTile * kChunks; i += blockDim.x) {
+        const int r = i / kChunks, c = i % kChunks;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (r < G) v = *reinterpret_cast<const uint4*>(qb + static_cast<int64_t>(r) * D + c * 8);
+        *reinterpret_cast<uint4*>(q_sm + tile_off<D>(r, c)) = v;
+      }
     }
-  };
+    __syncthreads();
 
-  int my = 0;  // tiles handled by this warp: warp, warp + 4, ...
-  if (warp < n_tiles) load_tile(warp, 0);
-  cp_async_commit();
-  for (int tile = warp; tile < n_tiles; tile += kWarps, ++my) {
-    const int stage = my & 1;
-    if (tile + kWarps < n_tiles) load_tile(tile + kWarps, stage ^ 1);
+    float o[D / 8][4];
+#pragma unroll
+    for (int j = 0; j < D / 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+
+    uint8_t* wsm = smem + warp * (4 * kTileBytes);  // [stage][K|V][16][D]
+    const int64_t k_off = static_cast<int64_t>(h) * D, v_off = static_cast<int64_t>(Hkv + h) * D;
+    const uint32_t q_base = smem_u32(q_sm);
+    // Lanes 0..15 hold the slot of row `lane` of a tile (fetched a tile ahead).
+    auto fetch_slot = [&](int tile) -> int32_t {
+      const int t = tok0 + tile * kTile + (lane & 15);
+      return (tile < n_tiles && t < tok_end) ? __ldg(sl + t) : 0;
+    };
+    auto load_tile = [&](int tile, int stage, int32_t my_slot) {
+      const int r0 = tok0 + tile * kTile;
+      const uint32_t kbase = smem_u32(wsm + stage * 2 * kTileBytes);
+      const uint32_t vbase = kbase + kTileBytes;
+#pragma unroll
+      for (int i = lane; i < kTile * kChunks; i += 32) {
+        const int r = i / kChunks, c = i % kChunks;
+        const int64_t slot = __shfl_sync(0xffffffffu, my_slot, r);
+        const bool valid = r0 + r < tok_end;
+        const __nv_bfloat16* row = pool_l + slot * row_elems;
+        cp_async16(kbase + tile_off<D>(r, c), row + k_off + c * 8, valid);
+        cp_async16(vbase + tile_off<D>(r, c), row + v_off + c * 8, valid);
+      }
+    };
+
+    int my = 0;  // tiles of this piece handled by this warp: warp, warp + 4, ...
+    int32_t nxt = fetch_slot(warp);
+    if (warp < n_tiles) load_tile(warp, 0, nxt);
     cp_async_commit();
-    cp_async_wait<1>();
-    __syncwarp();
-    const uint32_t kbase = smem_u32(wsm + stage * 2 * kTileBytes);
-    const uint32_t vbase = kbase + kTileBytes;
+    nxt = fetch_slot(warp + kWarps);
+    for (int tile = warp; tile < n_tiles; tile += kWarps, ++my) {
+      const int stage = my & 1;
+      if (tile + kWarps < n_tiles) load_tile(tile + kWarps, stage ^ 1, nxt);
+      cp_async_commit();
+      nxt = fetch_slot(tile + 2 * kWarps);
+      cp_async_wait<1>();
+      __syncwarp();
+      const uint32_t kbase = smem_u32(wsm + stage * 2 * kTileBytes);
+      const uint32_t vbase = kbase + kTileBytes;
 
-    // S = Q K^T over 16 tokens (two n8 tiles).
-    float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      // S = Q K^T over 16 tokens (two n8 tiles); Q fragments via ldmatrix.
+      float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
-    for (int kk = 0; kk < D / 16; ++kk) {
-      const int mi = lane >> 3, r = (lane & 7) + ((mi >> 1) << 3);
-      const int c = 2 * kk + (mi & 1);
-      uint32_t b0, b1, b2, b3;
-      ldmatrix_x4(kbase + tile_off<D>(r, c), b0, b1, b2, b3);
-      mma_bf16(s[0], qa[kk], b0, b1);
-      mma_bf16(s[1], qa[kk], b2, b3);
+      for (int kk = 0; kk < D / 16; ++kk) {
+        uint32_t qa[4];
+        {
+          const int mi = lane >> 3, r = (lane & 7) + ((mi & 1) << 3);
+          const int c = 2 * kk + (mi >> 1);
+          ldmatrix_x4(q_base + tile_off<D>(r, c), qa[0], qa[1], qa[2], qa[3]);
+        }
+        const int mi = lane >> 3, r = (lane & 7) + ((mi >> 1) << 3);
+        const int c = 2 * kk + (mi & 1);
+        uint32_t b0, b1, b2, b3;
+        ldmatrix_x4(kbase + tile_off<D>(r, c), b0, b1, b2, b3);
+        mma_bf16(sc[0], qa, b0, b1);
+        mma_bf16(sc[1], qa, b2, b3);
+      }
+      // Mask tokens past the piece, scale, online softmax per query row.
+      const int tt = tok0 + tile * kTile;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int t = tt + 8 * j + 2 * (lane & 3) + (e & 1);
+          sc[j][e] = t < tok_end ? sc[j][e] * scale_log2 : -INFINITY;
+        }
+      }
+      float mx0 = fmaxf(fmaxf(sc[0][0], sc[0][1]), fmaxf(sc[1][0], sc[1][1]));
+      float mx1 = fmaxf(fmaxf(sc[0][2], sc[0][3]), fmaxf(sc[1][2], sc[1][3]));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+      const float nm0 = fmaxf(m0, mx0), nm1 = fmaxf(m1, mx1);
+      const float a0 = exp2f(m0 - nm0), a1 = exp2f(m1 - nm1);
+      m0 = nm0;
+      m1 = nm1;
+      float p[2][4];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        p[j][0] = exp2f(sc[j][0] - m0);
+        p[j][1] = exp2f(sc[j][1] - m0);
+        p[j][2] = exp2f(sc[j][2] - m1);
+        p[j][3] = exp2f(sc[j][3] - m1);
+      }
+      float rs0 = p[0][0] + p[0][1] + p[1][0] + p[1][1];
+      float rs1 = p[0][2] + p[0][3] + p[1][2] + p[1][3];
+      rs0 += __shfl_xor_sync(0xffffffffu, rs0, 1);
+      rs0 += __shfl_xor_sync(0xffffffffu, rs0, 2);
+      rs1 += __shfl_xor_sync(0xffffffffu, rs1, 1);
+      rs1 += __shfl_xor_sync(0xffffffffu, rs1, 2);
+      l0 = l0 * a0 + rs0;
+      l1 = l1 * a1 + rs1;
+#pragma unroll
+      for (int j = 0; j < D / 8; ++j) {
+        o[j][0] *= a0;
+        o[j][1] *= a0;
+        o[j][2] *= a1;
+        o[j][3] *= a1;
+      }
+      // O += P V (P: A operand from the S accumulators; V via ldmatrix.trans).
+      uint32_t pa[4];
+      pa[0] = pack_bf16(p[0][0], p[0][1]);
+      pa[1] = pack_bf16(p[0][2], p[0][3]);
+      pa[2] = pack_bf16(p[1][0], p[1][1]);
+      pa[3] = pack_bf16(p[1][2], p[1][3]);
+#pragma unroll
+      for (int j = 0; j < D / 8; j += 2) {
+        const int mi = lane >> 3, r = (lane & 7) + ((mi & 1) << 3);
+        const int c = j + (mi >> 1);
+        uint32_t b0, b1, b2, b3;
+        ldmatrix_x4_trans(vbase + tile_off<D>(r, c), b0, b1, b2, b3);
+        mma_bf16(o[j], pa, b0, b1);
+        mma_bf16(o[j + 1], pa, b2, b3);
+      }
+      __syncwarp();
     }
-    // Mask tokens past the context, scale, online softmax per query row.
-    const int t0 = t_begin + tile * kTile;
+    cp_async_wait<0>();
+    __syncthreads();
+
+    // Merge the 4 warps' (m, l, O) in shared memory, rows < G only.
+    float* red = reinterpret_cast<float*>(smem);  // [warp][16][D] then m,l [warp][16][2]
+    float* red_ml = red + kWarps * 16 * D;
+    {
+      const int r0 = lane >> 2, r1 = r0 + 8;
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int t = t0 + 8 * j + 2 * (lane & 3) + (e & 1);
-        s[j][e] = t < t_end ? s[j][e] * scale_log2 : -INFINITY;
+      for (int j = 0; j < D / 8; ++j) {
+        const int c = 8 * j + 2 * (lane & 3);
+        *reinterpret_cast<float2*>(&red[(warp * 16 + r0) * D + c]) = make_float2(o[j][0], o[j][1]);
+        *reinterpret_cast<float2*>(&red[(warp * 16 + r1) * D + c]) = make_float2(o[j][2], o[j][3]);
+      }
+      if ((lane & 3) == 0) {
+        red_ml[(warp * 16 + r0) * 2] = m0;
+        red_ml[(warp * 16 + r0) * 2 + 1] = l0;
+        red_ml[(warp * 16 + r1) * 2] = m1;
+        red_ml[(warp * 16 + r1) * 2 + 1] = l1;
       }
     }
-    float mx0 = fmaxf(fmaxf(s[0][0], s[0][1]), fmaxf(s[1][0], s[1][1]));
-    float mx1 = fmaxf(fmaxf(s[0][2], s[0][3]), fmaxf(s[1][2], s[1][3]));
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
-    const float nm0 = fmaxf(m0, mx0), nm1 = fmaxf(m1, mx1);
-    const float a0 = exp2f(m0 - nm0), a1 = exp2f(m1 - nm1);
-    m0 = nm0;
-    m1 = nm1;
-    float p[2][4];
+    __syncthreads();
+    const int64_t piece = static_cast<int64_t>(blockIdx.x) + sgi;
+    // A piece that is the whole segment is final: write the bf16 output.
+    const bool whole = t0 == s_begin && pe == s_end;
+    for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
+      const int r = i / D, c = i % D;
+      float M = -INFINITY;
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      p[j][0] = exp2f(s[j][0] - m0);
-      p[j][1] = exp2f(s[j][1] - m0);
-      p[j][2] = exp2f(s[j][2] - m1);
-      p[j][3] = exp2f(s[j][3] - m1);
-    }
-    float rs0 = p[0][0] + p[0][1] + p[1][0] + p[1][1];
-    float rs1 = p[0][2] + p[0][3] + p[1][2] + p[1][3];
-    rs0 += __shfl_xor_sync(0xffffffffu, rs0, 1);
-    rs0 += __shfl_xor_sync(0xffffffffu, rs0, 2);
-    rs1 += __shfl_xor_sync(0xffffffffu, rs1, 1);
-    rs1 += __shfl_xor_sync(0xffffffffu, rs1, 2);
-    l0 = l0 * a0 + rs0;
-    l1 = l1 * a1 + rs1;
+      for (int w = 0; w < kWarps; ++w) M = fmaxf(M, red_ml[(w * 16 + r) * 2]);
+      float acc = 0.f, lsum = 0.f;
+      if (M != -INFINITY) {
 #pragma unroll
-    for (int j = 0; j < D / 8; ++j) {
-      o[j][0] *= a0;
-      o[j][1] *= a0;
-      o[j][2] *= a1;
-      o[j][3] *= a1;
-    }
-    // O += P V (P: A operand from the S accumulators; V via ldmatrix.trans).
-    uint32_t pa[4];
-    pa[0] = pack_bf16(p[0][0], p[0][1]);
-    pa[1] = pack_bf16(p[0][2], p[0][3]);
-    pa[2] = pack_bf16(p[1][0], p[1][1]);
-    pa[3] = pack_bf16(p[1][2], p[1][3]);
-#pragma unroll
-    for (int j = 0; j < D / 8; j += 2) {
-      const int mi = lane >> 3, r = (lane & 7) + ((mi & 1) << 3);
-      const int c = j + (mi >> 1);
-      uint32_t b0, b1, b2, b3;
-      ldmatrix_x4_trans(vbase + tile_off<D>(r, c), b0, b1, b2, b3);
-      mma_bf16(o[j], pa, b0, b1);
-      mma_bf16(o[j + 1], pa, b2, b3);
-    }
-    __syncwarp();
-  }
-  cp_async_wait<0>();
-  __syncthreads();
-
-  // Merge the 4 warps' (m, l, O) in shared memory, rows < G only.
-  float* red = reinterpret_cast<float*>(smem);  // [warp][16][D] then m,l [warp][16][2]
-  float* red_ml = red + kWarps * 16 * D;
-  {
-    const int r0 = lane >> 2, r1 = r0 + 8;
-#pragma unroll
-    for (int j = 0; j < D / 8; ++j) {
-      const int c = 8 * j + 2 * (lane & 3);
-      red[(warp * 16 + r0) * D + c] = o[j][0];
-      red[(warp * 16 + r0) * D + c + 1] = o[j][1];
-      red[(warp * 16 + r1) * D + c] = o[j][2];
-      red[(warp * 16 + r1) * D + c + 1] = o[j][3];
-    }
-    if ((lane & 3) == 0) {
-      red_ml[(warp * 16 + r0) * 2] = m0;
-      red_ml[(warp * 16 + r0) * 2 + 1] = l0;
-      red_ml[(warp * 16 + r1) * 2] = m1;
-      red_ml[(warp * 16 + r1) * 2 + 1] = l1;
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
-    const int r = i / D, c = i % D;
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) M = fmaxf(M, red_ml[(w * 16 + r) * 2]);
-    float acc = 0.f, lsum = 0.f;
-    if (M != -INFINITY) {
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) {
-        const float mw = red_ml[(w * 16 + r) * 2];
-        if (mw == -INFINITY) continue;
-        const float sc = exp2f(mw - M);
-        acc += sc * red[(w * 16 + r) * D + c];
-        lsum += sc * red_ml[(w * 16 + r) * 2 + 1];
+        for (int w = 0; w < kWarps; ++w) {
+          const float mw = red_ml[(w * 16 + r) * 2];
+          if (mw == -INFINITY) continue;
+          const float scl = exp2f(mw - M);
+          acc += scl * red[(w * 16 + r) * D + c];
+          lsum += scl * red_ml[(w * 16 + r) * 2 + 1];
+        }
+      }
+      if (whole) {
+        out[((static_cast<int64_t>(b) * Hq + static_cast<int64_t>(h) * G + r) * D) + c] =
+            __float2bfloat16_rn(lsum > 0.f ? acc / lsum : 0.f);
+        continue;
+      }
+      part_o[(piece * G + r) * D + c] = lsum > 0.f ? acc / lsum : 0.f;
+      if (c == 0) {
+        part_ml[(piece * G + r) * 2] = M;
+        part_ml[(piece * G + r) * 2 + 1] = lsum;
       }
     }
-    const int64_t qh = static_cast<int64_t>(b) * Hq + static_cast<int64_t>(h) * G + r;
-    part_o[(qh * splits + split) * D + c] = lsum > 0.f ? acc / lsum : 0.f;
-    if (c == 0) {
-      part_ml[(qh * splits + split) * 2] = M;
-      part_ml[(qh * splits + split) * 2 + 1] = lsum;
-    }
+    t0 = pe;
   }
-  }  // items
 }
 
-// Merge split partials: out = sum_s w_s O_s / sum_s w_s, w_s = l_s 2^(m_s - M).
-__global__ void k_decode_combine(const float* __restrict__ part_o, const float* __restrict__ part_ml,
-                                 int splits, int D, __nv_bfloat16* __restrict__ out) {
-  const int64_t qh = blockIdx.x;
-  float M = -INFINITY;
-  for (int s = 0; s < splits; ++s) M = fmaxf(M, part_ml[(qh * splits + s) * 2]);
-  for (int c = threadIdx.x; c < D; c += blockDim.x) {
-    float acc = 0.f, wsum = 0.f;
-    if (M != -INFINITY) {
-      for (int s = 0; s < splits; ++s) {
-        const float ms = part_ml[(qh * splits + s) * 2];
-        const float ls = part_ml[(qh * splits + s) * 2 + 1];
-        if (ms == -INFINITY || ls <= 0.f) continue;
-        const float w = ls * exp2f(ms - M);
-        acc += w * part_o[(qh * splits + s) * D + c];
-        wsum += w;
-      }
+// Merge a segment's pieces, one CTA per segment (batch, kv head) covering
+// its G query heads: out = sum_p w_p O_p / sum_p w_p, w_p = l_p 2^(m_p - M).
+// Segments finished by a single piece were written by the main kernel.
+constexpr int kCombineThreads = 256;
+
+__global__ void __launch_bounds__(kCombineThreads) k_decode_combine(
+    const float* __restrict__ part_o, const float* __restrict__ part_ml,
+    const int64_t* __restrict__ seg_start, int64_t n_seg, int Hq, int Hkv, int D, int grid,
+    __nv_bfloat16* __restrict__ out) {
+  extern __shared__ float cw[];  // [rows][n] weights, then [rows] max and [rows] sums
+  const int64_t s = blockIdx.x;
+  const int rpc = (Hq / Hkv + gridDim.y - 1) / gridDim.y;  // query rows of this CTA
+  const int r_base = blockIdx.y * rpc;
+  const int b = static_cast<int>(s / Hkv), h = static_cast<int>(s % Hkv);
+  const int G = Hq / Hkv;
+  const int64_t T = seg_start[n_seg];
+  const int64_t x0 = seg_start[s], x1 = seg_start[s + 1] - 1;
+  if (x1 < x0) return;
+  auto cta_of = [&](int64_t x) {  // CTA whose tile range holds tile x
+    int64_t c = x * grid / T;
+    while (c + 1 < grid && cta_tile_start(c + 1, T, grid) <= x) ++c;
+    while (c > 0 && cta_tile_start(c, T, grid) > x) --c;
+    return c;
+  };
+  const int64_t c0 = cta_of(x0);
+  const int n = static_cast<int>(cta_of(x1) - c0 + 1);
+  if (n == 1) return;
+  const int rows = min(rpc, G - r_base);
+  if (rows <= 0) return;
+  float* mx = cw + rows * n;
+  float* sm = mx + rows;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int rr = wid; rr < rows; rr += blockDim.x / 32) {
+    const int r = r_base + rr;
+    float m = -INFINITY;
+    for (int p = lane; p < n; p += 32) m = fmaxf(m, part_ml[((c0 + p + s) * G + r) * 2]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float wl = 0.f;
+    for (int p = lane; p < n; p += 32) {
+      const float ms = part_ml[((c0 + p + s) * G + r) * 2];
+      const float ls = part_ml[((c0 + p + s) * G + r) * 2 + 1];
+      const float w = (m == -INFINITY || ms == -INFINITY || ls <= 0.f) ? 0.f : ls * exp2f(ms - m);
+      cw[rr * n + p] = w;
+      wl += w;
     }
-    out[qh * D + c] = __float2bfloat16_rn(wsum > 0.f ? acc / wsum : 0.f);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wl += __shfl_xor_sync(0xffffffffu, wl, o);
+    if (lane == 0) {
+      mx[rr] = m;
+      sm[rr] = wl;
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < rows * D; e += blockDim.x) {
+    const int rr = e / D, d = e % D, r = r_base + rr;
+    float acc0 = 0.f, acc1 = 0.f;
+    int p = 0;
+#pragma unroll 8
+    for (; p + 1 < n; p += 2) {
+      acc0 += cw[rr * n + p] * part_o[((c0 + p + s) * G + r) * D + d];
+      acc1 += cw[rr * n + p + 1] * part_o[((c0 + p + 1 + s) * G + r) * D + d];
+    }
+    if (p < n) acc0 += cw[rr * n + p] * part_o[((c0 + p + s) * G + r) * D + d];
+    const float acc = acc0 + acc1;
+    const float wsum = sm[rr];
+    out[(static_cast<int64_t>(b) * Hq + static_cast<int64_t>(h) * G + r) * D + d] =
+        __float2bfloat16_rn(wsum > 0.f ? acc / wsum : 0.f);
   }
 }
 
@@ -308,7 +399,7 @@ __global__ void k_decode_combine(const float* __restrict__ part_o, const float* 
 size_t decode_attn_smem(int head_dim) {
   const size_t tiles = static_cast<size_t>(kWarps) * 4 * kTile * head_dim * 2;
   const size_t red = static_cast<size_t>(kWarps) * 16 * head_dim * 4 + kWarps * 16 * 2 * 4;
-  return tiles > red ? tiles : red;
+  return (tiles > red ? tiles : red) + static_cast<size_t>(kTile) * head_dim * 2;
 }
 
 int decode_attn_resident_ctas(int head_dim, int num_sms) {
@@ -327,28 +418,36 @@ int decode_attn_resident_ctas(int head_dim, int num_sms) {
 }
 
 bool launch_decode_attn(const void* pool_l, int64_t row_elems, const int32_t* slots,
-                        const int64_t* ctx_off, const int32_t* ctx_len, const void* q, int batch,
-                        int Hq, int Hkv, int D, float scale, int splits, float* part_o,
-                        float* part_ml, void* out, int grid, cudaStream_t s) {
+                        const int64_t* ctx_off, const int32_t* ctx_len, const int64_t* seg_start,
+                        int64_t n_seg, int64_t total_tiles, const void* q, int batch, int Hq,
+                        int Hkv, int D, float scale, float* part_o, float* part_ml, void* out,
+                        int grid, cudaStream_t s) {
   const float scale_log2 = scale * 1.4426950408889634f;
-  const int64_t items = static_cast<int64_t>(splits) * Hkv * batch;
-  const int g = static_cast<int>(items < grid ? items : grid);
+  const int g = static_cast<int>(total_tiles < grid ? (total_tiles < 1 ? 1 : total_tiles) : grid);
   const size_t smem = decode_attn_smem(D);
   auto q16 = static_cast<const __nv_bfloat16*>(q);
   auto pool16 = static_cast<const __nv_bfloat16*>(pool_l);
+  auto out16 = static_cast<__nv_bfloat16*>(out);
   if (D == 128) {
     k_decode_attn<128><<<g, kWarps * 32, smem, s>>>(pool16, row_elems, slots, ctx_off, ctx_len,
-                                                    q16, Hq, Hkv, scale_log2, splits, batch,
-                                                    part_o, part_ml);
+                                                    seg_start, n_seg, q16, Hq, Hkv, scale_log2,
+                                                    part_o, part_ml, out16);
   } else if (D == 64) {
     k_decode_attn<64><<<g, kWarps * 32, smem, s>>>(pool16, row_elems, slots, ctx_off, ctx_len,
-                                                   q16, Hq, Hkv, scale_log2, splits, batch,
-                                                   part_o, part_ml);
+                                                   seg_start, n_seg, q16, Hq, Hkv, scale_log2,
+                                                   part_o, part_ml, out16);
   } else {
     return false;
   }
-  k_decode_combine<<<batch * Hq, 128, 0, s>>>(part_o, part_ml, splits, D,
-                                              static_cast<__nv_bfloat16*>(out));
+  // Few segments -> one query row per CTA (more parallel merge work); many
+  // segments -> all G rows per CTA (fewer, fuller CTAs).
+  const int G = Hq / Hkv;
+  const int row_groups = n_seg * G <= 4096 ? G : 1;
+  const int rpc = (G + row_groups - 1) / row_groups;
+  const size_t csmem = sizeof(float) * (static_cast<size_t>(rpc) * (g + 1) + 2 * rpc);
+  k_decode_combine<<<dim3(static_cast<unsigned>(n_seg), row_groups),
+                     rpc == 1 ? 128 : kCombineThreads, csmem, s>>>(part_o, part_ml, seg_start,
+                                                                  n_seg, Hq, Hkv, D, g, out16);
   return true;
 }
 

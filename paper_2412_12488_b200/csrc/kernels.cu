@@ -86,7 +86,7 @@ __device__ __forceinline__ void warp_copy_row(const uint64_t* __restrict__ src,
 // then copied back to back and the fill marks stored lane-parallel.  (A
 // per-row fill check serialised a fill load before every store and cost
 // ~15% of bandwidth; profiles/micro/copy_variants.cu.)
-constexpr int kGroup = 4;
+constexpr int kGroup = 4;  // rows per item for long launches (1 for launches within one wave)
 
 __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
   extern __shared__ uint32_t s_rows[];  // per relative layer (accounting only)
@@ -105,12 +105,13 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  const int64_t groups = (p.n_rows + kGroup - 1) / kGroup;
+  const int group = p.group > 0 ? p.group : kGroup;
+  const int64_t groups = (p.n_rows + group - 1) / group;
   const int64_t items = groups * p.n_layers;
   for (int64_t it = warp; it < items; it += n_warps) {
     const int32_t lrel = static_cast<int32_t>(it / groups);
-    const int64_t r0 = (it - static_cast<int64_t>(lrel) * groups) * kGroup;
-    const int nr = static_cast<int>(p.n_rows - r0 < kGroup ? p.n_rows - r0 : kGroup);
+    const int64_t r0 = (it - static_cast<int64_t>(lrel) * groups) * group;
+    const int nr = static_cast<int>(p.n_rows - r0 < group ? p.n_rows - r0 : group);
     int64_t my_s = 0, my_d = 0;
     uint8_t my_f = 0;
     uint8_t* fill_l = p.dst_fill != nullptr ? p.dst_fill + lrel * p.dst_fill_layer : nullptr;
@@ -409,11 +410,18 @@ void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms) {
   const int warps_per_block = kCopyThreads / 32;
   // 2 CTAs (16 warps) per SM measured best for the 4 KiB-row copy
   // (profiles/micro/copy_variants.cu: 6.57 TB/s vs 6.1 TB/s at 4-8 per SM).
-  const int64_t groups = (p.n_rows + kGroup - 1) / kGroup * p.n_layers;
-  const int per_sm = groups >= static_cast<int64_t>(num_sms) * 2 * warps_per_block * 8 ? 2 : 8;
+  // Long launches: 4-row groups on 2 CTAs per SM (measured best for the
+  // 80-layer DirectSend).  Launches that fit one wave of resident warps
+  // (per-layer append / gather): one row per warp, 8 CTAs per SM, so no
+  // warp chains several rows' load latencies.
+  CopyParams q = p;
+  const int64_t one_wave = static_cast<int64_t>(num_sms) * 8 * warps_per_block;
+  q.group = items <= one_wave ? 1 : kGroup;
+  const int64_t groups = (q.n_rows + q.group - 1) / q.group * q.n_layers;
+  const int per_sm = q.group == 1 ? 8 : (groups >= static_cast<int64_t>(num_sms) * 2 * warps_per_block * 8 ? 2 : 8);
   const int grid = grid_for(groups, warps_per_block, num_sms, per_sm);
-  const size_t smem = p.win_received ? sizeof(uint32_t) * p.n_layers : 0;
-  k_copy_rows<<<grid, kCopyThreads, smem, s>>>(p);
+  const size_t smem = q.win_received ? sizeof(uint32_t) * q.n_layers : 0;
+  k_copy_rows<<<grid, kCopyThreads, smem, s>>>(q);
 }
 
 void launch_validate_remote(const ValidateParams& p, cudaStream_t s) {

@@ -56,6 +56,7 @@ struct CopyParams {
   int32_t win_layers;         // L of the destination (row stride of win_layer_rows)
   const int32_t* verdict;     // validation result: >= 0 window id, < 0 reject
   uint32_t* status;           // sender-side sticky status
+  int32_t group;              // rows per warp item (set by the launcher)
 };
 void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms);
 
@@ -127,12 +128,14 @@ void launch_gather_tables(const int32_t* const* tables, const int64_t* off, cons
 void launch_check_filled(const uint8_t* fill_l, const int32_t* slots, int64_t n, uint32_t* status,
                          cudaStream_t s, int num_sms);
 
-// Paged GQA decode attention (decode_attn.cu): split-KV partials + combine.
+// Paged GQA decode attention (decode_attn.cu): stream-K split over the
+// (batch, kv head, 16-token tile) space, partials + combine.
 size_t decode_attn_smem(int head_dim);
 int decode_attn_resident_ctas(int head_dim, int num_sms);
 bool launch_decode_attn(const void* pool_l, int64_t row_elems, const int32_t* slots,
-                        const int64_t* ctx_off, const int32_t* ctx_len, const void* q, int batch,
-                        int Hq, int Hkv, int D, float scale, int splits, float* part_o,
-                        float* part_ml, void* out, int grid, cudaStream_t s);
+                        const int64_t* ctx_off, const int32_t* ctx_len, const int64_t* seg_start,
+                        int64_t n_seg, int64_t total_tiles, const void* q, int batch, int Hq,
+                        int Hkv, int D, float scale, float* part_o, float* part_ml, void* out,
+                        int grid, cudaStream_t s);
 
 }  // namespace mkv
