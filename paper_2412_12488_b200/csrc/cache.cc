@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <unordered_map>
 
 #include "hash.cuh"
 
@@ -59,30 +60,63 @@ void CudaCheck(cudaError_t e, const char* what) {
   }
 }
 
-// kv_addr.cc:16-30.  Same checks in the same order of precedence (a bad
-// range or an overlap raises InvalidArgument before the AddrMismatch total
-// check); overlaps are found on the ranges sorted by (page, begin) instead
-// of a per-slot set, O(R log R) in the number of ranges.
+// kv_addr.cc:16-30.  Same checks and error precedence as the reference (a
+// bad range or an overlap is InvalidArgument before the AddrMismatch total
+// check).  Overlap needs two ranges on one page: pages are marked in a
+// generation-stamped array (O(R)), and only ranges on repeated pages are
+// sorted and compared.
 void KVAddr::Validate() const {
-  int64_t total = 0;
+  int64_t total = 0, max_page = -1;
   for (const auto& r : ranges) {
     MKV_CHECK(r.slot_count > 0 && r.slot_begin >= 0, kInvalidArgument, "bad slot range");
     total += r.slot_count;
+    max_page = std::max(max_page, r.page_id);
   }
-  std::vector<std::pair<int64_t, int64_t>> iv;  // (page, begin) -> end via index
-  iv.reserve(ranges.size());
-  for (size_t i = 0; i < ranges.size(); ++i) iv.push_back({ranges[i].page_id, static_cast<int64_t>(i)});
-  std::sort(iv.begin(), iv.end(), [&](const auto& a, const auto& b) {
-    const auto& ra = ranges[a.second];
-    const auto& rb = ranges[b.second];
-    return ra.page_id != rb.page_id ? ra.page_id < rb.page_id : ra.slot_begin < rb.slot_begin;
-  });
-  for (size_t i = 1; i < iv.size(); ++i) {
-    const auto& prev = ranges[iv[i - 1].second];
-    const auto& cur = ranges[iv[i].second];
-    MKV_CHECK(!(prev.page_id == cur.page_id &&
-                static_cast<int64_t>(prev.slot_begin) + prev.slot_count > cur.slot_begin),
-              kInvalidArgument, "overlapping slot ranges");
+  std::vector<size_t> repeated;  // indices of ranges on pages seen more than once
+  bool negative = false;
+  for (const auto& r : ranges) negative |= r.page_id < 0;
+  if (!negative && max_page < (int64_t(1) << 26)) {
+    thread_local std::vector<uint32_t> stamp;
+    thread_local std::vector<int32_t> first;
+    thread_local uint32_t gen = 0;
+    if (static_cast<int64_t>(stamp.size()) <= max_page) {
+      stamp.assign(max_page + 1, 0);
+      first.assign(max_page + 1, -1);
+      gen = 0;
+    }
+    if (++gen == 0) {
+      std::fill(stamp.begin(), stamp.end(), 0);
+      gen = 1;
+    }
+    for (size_t i = 0; i < ranges.size(); ++i) {
+      const int64_t pg = ranges[i].page_id;
+      if (stamp[pg] != gen) {
+        stamp[pg] = gen;
+        first[pg] = static_cast<int32_t>(i);
+      } else {
+        if (first[pg] >= 0) {
+          repeated.push_back(static_cast<size_t>(first[pg]));
+          first[pg] = -1;
+        }
+        repeated.push_back(i);
+      }
+    }
+  } else {
+    for (size_t i = 0; i < ranges.size(); ++i) repeated.push_back(i);
+  }
+  if (!repeated.empty()) {
+    std::sort(repeated.begin(), repeated.end(), [&](size_t a, size_t b) {
+      const auto& ra = ranges[a];
+      const auto& rb = ranges[b];
+      return ra.page_id != rb.page_id ? ra.page_id < rb.page_id : ra.slot_begin < rb.slot_begin;
+    });
+    for (size_t i = 1; i < repeated.size(); ++i) {
+      const auto& prev = ranges[repeated[i - 1]];
+      const auto& cur = ranges[repeated[i]];
+      MKV_CHECK(!(prev.page_id == cur.page_id &&
+                  static_cast<int64_t>(prev.slot_begin) + prev.slot_count > cur.slot_begin),
+                kInvalidArgument, "overlapping slot ranges");
+    }
   }
   MKV_CHECK(total == token_count, kAddrMismatch, "slot counts do not cover token_count");
 }
@@ -139,6 +173,7 @@ ss_cache::ss_cache(const ss_config& cfg)
   MKV_CHECK(cfg.num_pages * cfg.page_size < (int64_t(1) << 31), kInvalidArgument,
             "num_pages * page_size must fit int32 slot indices");
   seed_state_ = mkv::seed_state(hash_seed_);
+  while ((1 << page_shift_) < P_) ++page_shift_;
   // LIFO free list, lowest page first out (kv_cache.cc:45-46).
   free_pages_.reserve(num_pages_);
   for (int64_t i = num_pages_ - 1; i >= 0; --i) free_pages_.push_back(i);
@@ -553,7 +588,7 @@ int64_t ss_cache::PrepRecv(SeqId seq, std::vector<Token> tokens, int64_t end, KV
   *addr = BuildAddr(seq, m, e);
   {
     std::lock_guard<std::mutex> lock(recv_mu_);
-    for (int64_t pos = m; pos < e; ++pos) expecting_[Resolve(rec, pos)] = 1;
+    for (int64_t pos = m; pos < e; ++pos) expecting_[rec->slots[pos]] = 1;
     if (e > m) {
       Window w;
       w.begin = m;
@@ -1019,16 +1054,26 @@ KVAddr ss_cache::BuildAddr(SeqId seq, int64_t begin, int64_t end) {
   KVAddr addr;
   addr.token_begin = begin;
   addr.token_count = end - begin;
-  for (int64_t pos = begin; pos < end; ++pos) {
-    const int32_t slot = Resolve(rec, pos);
-    const int64_t page = slot / P_;
-    const int32_t s = slot % P_;
+  if (end > begin) {
+    MKV_ICHECK(begin >= 0 && end <= rec->alloc_len, "position not allocated");
+    addr.ranges.reserve((end - begin) / P_ + 2);
+  }
+  const int32_t* table = rec->slots.data();
+  for (int64_t pos = begin; pos < end;) {
+    const int32_t slot = table[pos];
+    const int64_t page = slot >> page_shift_;  // page_size is a power of two
+    const int32_t s = slot & (P_ - 1);
+    // Own pages are filled slot 0..P-1 in position order, so a run usually
+    // spans to the page end; confirm the run end, else step one position.
+    int64_t run = std::min<int64_t>(P_ - s, end - pos);
+    if (run > 1 && table[pos + run - 1] != slot + run - 1) run = 1;
     if (!addr.ranges.empty() && addr.ranges.back().page_id == page &&
         addr.ranges.back().slot_begin + addr.ranges.back().slot_count == s) {
-      ++addr.ranges.back().slot_count;
+      addr.ranges.back().slot_count += static_cast<int32_t>(run);
     } else {
-      addr.ranges.push_back({page, s, 1});
+      addr.ranges.push_back({page, s, static_cast<int32_t>(run)});
     }
+    pos += run;
   }
   addr.Validate();
   return addr;

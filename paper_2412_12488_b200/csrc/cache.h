@@ -350,6 +350,7 @@ struct ss_cache {
   // Geometry.
   int64_t num_pages_;
   int32_t P_, L_, W_, vocab_;
+  int32_t page_shift_ = 0;  // log2(P_)
   uint64_t hash_seed_, seed_state_;
   int device_;
   int32_t rank_;

@@ -34,11 +34,16 @@ struct alignas(32) u256 {
   unsigned long long a, b, c, d;
 };
 
+// Coherent (not .nc) 32-byte load: ptxas may not sink it below a store that
+// could alias, so a row's loads stay grouped ahead of its stores and each
+// lane keeps 4 requests in flight (with .nc, ptxas interleaved them 1:1 and
+// the copy lost ~12%; profiles/micro/lib_kernel.cu).
 __device__ __forceinline__ u256 ld256(const void* p) {
   u256 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0, %1, %2, %3}, [%4];"
+  asm volatile("ld.global.L1::no_allocate.v4.u64 {%0, %1, %2, %3}, [%4];"
                : "=l"(v.a), "=l"(v.b), "=l"(v.c), "=l"(v.d)
-               : "l"(p));
+               : "l"(p)
+               : "memory");
   return v;
 }
 
@@ -88,6 +93,25 @@ __device__ __forceinline__ void warp_copy_row(const uint64_t* __restrict__ src,
 // ~15% of bandwidth; profiles/micro/copy_variants.cu.)
 constexpr int kGroup = 4;  // rows per item for long launches (1 for launches within one wave)
 
+// kVec > 0: rows are exactly kVec 32-byte vectors per lane (W = 128*kVec
+// words), fully unrolled; kVec == 0: any W.
+template <int kVec>
+__device__ __forceinline__ void copy_row(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
+                                         int32_t W, int lane) {
+  if constexpr (kVec > 0) {
+    const u256* s4 = reinterpret_cast<const u256*>(src) + lane;
+    u256* d4 = reinterpret_cast<u256*>(dst) + lane;
+    u256 t[kVec];
+#pragma unroll
+    for (int u = 0; u < kVec; ++u) t[u] = ld256(s4 + 32 * u);
+#pragma unroll
+    for (int u = 0; u < kVec; ++u) st256(d4 + 32 * u, t[u]);
+  } else {
+    warp_copy_row(src, dst, W, lane);
+  }
+}
+
+template <int kVec>
 __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
   extern __shared__ uint32_t s_rows[];  // per relative layer (accounting only)
   int32_t window = -1;
@@ -112,12 +136,12 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
     const int32_t lrel = static_cast<int32_t>(it / groups);
     const int64_t r0 = (it - static_cast<int64_t>(lrel) * groups) * group;
     const int nr = static_cast<int>(p.n_rows - r0 < group ? p.n_rows - r0 : group);
-    int64_t my_s = 0, my_d = 0;
+    int32_t my_s = 0, my_d = 0;  // slot indices fit int32 (checked at cache creation)
     uint8_t my_f = 0;
     uint8_t* fill_l = p.dst_fill != nullptr ? p.dst_fill + lrel * p.dst_fill_layer : nullptr;
     if (lane < nr) {
-      my_s = p.src_idx ? static_cast<int64_t>(__ldg(p.src_idx + r0 + lane)) : r0 + lane;
-      my_d = p.dst_idx ? static_cast<int64_t>(__ldg(p.dst_idx + r0 + lane)) : r0 + lane;
+      my_s = p.src_idx ? __ldg(p.src_idx + r0 + lane) : static_cast<int32_t>(r0 + lane);
+      my_d = p.dst_idx ? __ldg(p.dst_idx + r0 + lane) : static_cast<int32_t>(r0 + lane);
       if (fill_l != nullptr) my_f = ld_cg_u8(fill_l + my_d);
     }
     // Empty destination slots only (kv_cache.cc:447); every row counts.
@@ -127,8 +151,8 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
 #pragma unroll 1
     for (int k = 0; k < nr; ++k) {
       const int64_t si = __shfl_sync(0xffffffffu, my_s, k);
-      const int64_t di = __shfl_sync(0xffffffffu, my_d, k);
-      if ((todo >> k) & 1u) warp_copy_row(src_l + si * p.W, dst_l + di * p.W, p.W, lane);
+      const int64_t di = __shfl_sync(0xffffffffu, my_d, k);  // int32 shuffles, widened
+      if ((todo >> k) & 1u) copy_row<kVec>(src_l + si * p.W, dst_l + di * p.W, p.W, lane);
     }
     if (fill_l != nullptr) {
       __syncwarp();
@@ -421,7 +445,13 @@ void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms) {
   const int per_sm = q.group == 1 ? 8 : (groups >= static_cast<int64_t>(num_sms) * 2 * warps_per_block * 8 ? 2 : 8);
   const int grid = grid_for(groups, warps_per_block, num_sms, per_sm);
   const size_t smem = q.win_received ? sizeof(uint32_t) * q.n_layers : 0;
-  k_copy_rows<<<grid, kCopyThreads, smem, s>>>(q);
+  if (q.W == 512) {  // Llama 8B/70B KV rows: 4 KiB
+    k_copy_rows<4><<<grid, kCopyThreads, smem, s>>>(q);
+  } else if (q.W == 128) {  // tiny config rows: 1 KiB
+    k_copy_rows<1><<<grid, kCopyThreads, smem, s>>>(q);
+  } else {
+    k_copy_rows<0><<<grid, kCopyThreads, smem, s>>>(q);
+  }
 }
 
 void launch_validate_remote(const ValidateParams& p, cudaStream_t s) {

@@ -494,10 +494,13 @@ class KVCache:
         except Exception:
             pass
 
-    def _addr_out(self, cap: int) -> tuple[_Addr, object]:
-        cap = max(1, cap)
-        arr = (_SlotRange * cap)()
-        return _Addr(0, 0, 0, arr, cap), arr
+    def _addr_out(self, cap: int) -> tuple[_Addr, np.ndarray]:
+        arr = np.empty(max(1, cap), dtype=SLOT_RANGE_DTYPE)
+        return _Addr(0, 0, 0, arr.ctypes.data_as(C.POINTER(_SlotRange)), len(arr)), arr
+
+    @staticmethod
+    def _addr_in(a: _Addr, arr: np.ndarray) -> "KVAddrInfo":
+        return KVAddrInfo(arr[:a.n_ranges].copy(), a.token_begin, a.token_count)
 
     # -- hash model scalars (hash_model.cc) --------------------------------
     def InitialPrefixDigest(self) -> int:
@@ -527,7 +530,7 @@ class KVCache:
         m = C.c_int64()
         self._check(self._lib.ss_prep_recv(self._h, seq_id, _ptr(t, C.c_int32), len(t), end,
                                            C.byref(m), C.byref(a)))
-        return PrepRecvResult(m.value, KVAddrInfo._from_c(a))
+        return PrepRecvResult(m.value, self._addr_in(a, keep))
 
     def ForkSequence(self, parent: int, child: int, fork_len: int, child_tokens=()) -> None:
         t = _tok(child_tokens)
@@ -596,7 +599,7 @@ class KVCache:
     def BuildAddr(self, seq: int, range: tuple) -> KVAddrInfo:
         a, keep = self._addr_out(max(0, range[1] - range[0]))
         self._check(self._lib.ss_build_addr(self._h, seq, range[0], range[1], C.byref(a)))
-        return KVAddrInfo._from_c(a)
+        return self._addr_in(a, keep)
 
     # -- transfer agent -----------------------------------------------------------
     def ApplyRemoteWrite(self, addr: KVAddrInfo, layer: int, payload, tag: int) -> ApplyStatus:

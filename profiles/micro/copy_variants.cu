@@ -401,6 +401,13 @@ int main() {
   for (int64_t i = 0; i < n_rows; ++i) h[i] = int32_t(i);
   CK(cudaMemcpy(si, h.data(), 4 * n_rows, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(di, h.data(), 4 * n_rows, cudaMemcpyHostToDevice));
+  // LIFO reuse after a free hands the decode engine its pages in descending
+  // order (kv_cache.cc:499-507): rows ascend within a page, pages descend.
+  std::vector<int32_t> hdesc(n_rows);
+  for (int64_t i = 0; i < n_rows; ++i) hdesc[i] = int32_t(((511 - i / 16) * 16) + i % 16);
+  int32_t* di_desc;
+  CK(cudaMalloc(&di_desc, 4 * n_rows));
+  CK(cudaMemcpy(di_desc, hdesc.data(), 4 * n_rows, cudaMemcpyHostToDevice));
   CK(cudaMemset(src, 1, bytes));
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -462,7 +469,13 @@ int main() {
       timeit(nm, [&] { v5<<<sms * 4, 256>>>(p, rpc); });
     }
     timeit("v6 32B cg-fill .cs stores", [&] { v6<<<sms * 4, 256>>>(p); });
-    for (int mult : {2, 4, 8}) {
+    {
+      P pd = p;
+      pd.di = di_desc;
+      timeit("v8 G=4 x2 descending dst", [&] { v8<4><<<sms * 2, 256>>>(pd); });
+      timeit("v8 G=4 x2 ascending  dst", [&] { v8<4><<<sms * 2, 256>>>(p); });
+    }
+    for (int mult : {2}) {
       char nm[64];
       snprintf(nm, 64, "v8 G=4 x%d", mult);
       timeit(nm, [&] { v8<4><<<sms * mult, 256>>>(p); });
