@@ -435,9 +435,17 @@ def secondary_measurements(P, D, prompt, torch) -> dict:
     """Handoff latency with per-layer overlap, KV append, local gather, decode attention."""
     out = {}
     try:
-        out["handoff"] = measure_handoff(torch)
+        out["handoff"] = measure_handoff_gemm(torch)
     except Exception as ex:
         out["handoff"] = {"error": str(ex)}
+    try:
+        out["handoff_toy_prefill"] = measure_handoff(torch)
+    except Exception as ex:
+        out["handoff_toy_prefill"] = {"error": str(ex)}
+    try:
+        out["transfer_sweep"] = measure_sweep(torch)
+    except Exception as ex:
+        out["transfer_sweep"] = {"error": str(ex)}
     try:
         out["append_gather"] = measure_append_gather(torch)
     except Exception as ex:
@@ -447,6 +455,77 @@ def secondary_measurements(P, D, prompt, torch) -> dict:
     except Exception as ex:
         out["decode_attention"] = {"error": str(ex)}
     return out
+
+
+def measure_handoff_gemm(torch) -> dict:
+    """1P1D PrefillThenSend at the 70B shape with a compute-bound prefill
+    stand-in: per layer one bf16 GEMM of a Llama-3.1-70B layer's FLOPs at
+    8,191 tokens (X[8191, 8192] @ W[8192, 104448], ~14 TFLOP), then the
+    layer's K||V rows are appended to P's pages and that layer is sent to D's
+    reserved pages on the communication stream (overlapping the next layer's
+    GEMM).  Reports P's prefill time with vs without sends
+    and the exposed tail: P's last-layer compute end -> D's device-side wait
+    sees every row of every layer."""
+    from paper_2412_12488_b200 import BatchEntry, KVCache
+
+    prompt = _prompt(4)
+    e = PROMPT - 1
+    pages = PROMPT // PAGE + 16
+    P = KVCache(num_pages=pages, page_size=PAGE, layers=L, dim=W, device=0, rank=0)
+    D = KVCache(num_pages=pages, page_size=PAGE, layers=L, dim=W, device=0, rank=1)
+    P.attach_peer(1, D)
+    X = torch.randn(e, 8192, device="cuda", dtype=torch.bfloat16)
+    Wt = torch.randn(8192, 104448, device="cuda", dtype=torch.bfloat16) * 0.01
+    Y = torch.empty(e, 104448, device="cuda", dtype=torch.bfloat16)
+    rows = torch.randint(-2**62, 2**62, (e * W,), dtype=torch.int64, device="cuda")
+    cs, ms, ds = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    res, base = {}, None
+    for run, send in enumerate((False, True, False, True)):
+        seq = 10 + run
+        if send:
+            r = D.PrepRecv(seq, prompt, -1)
+        P.CreateSequence(seq, prompt)
+        P.EnsureAllocated(seq, e)
+        plan = P.BeginForward([BatchEntry(seq, (0, e))])
+        dplan = P.begin_direct_send(seq, (0, e), 1, r.addr, 7) if send else None
+        torch.cuda.synchronize()
+        t0, tc, td = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        layer_done = [torch.cuda.Event() for _ in range(L)]
+        t0.record(cs)
+        for layer in range(L):
+            with torch.cuda.stream(cs):
+                torch.matmul(X, Wt, out=Y)
+            P.append_rows_async(plan, layer, rows.data_ptr(), cs.cuda_stream)
+            if send:
+                layer_done[layer].record(cs)
+                ms.wait_event(layer_done[layer])
+                P.launch_direct_send_async(dplan, (layer, layer + 1), ms.cuda_stream)
+        tc.record(cs)
+        if send:
+            ds.wait_event(t0)
+            D.wait_receive_async(seq, 60000, ds.cuda_stream)
+            td.record(ds)
+        torch.cuda.synchronize()
+        P.synchronize()
+        if send:
+            D.synchronize()
+            assert D.DrainReceiveCompletions() == [seq]
+            res = {"prefill_ms_with_sends": round(t0.elapsed_time(tc), 3),
+                   "exposed_tail_us": round(1e3 * max(0.0, tc.elapsed_time(td)), 1)}
+            D.FreeSequence(seq)
+            dplan.close()
+        else:
+            base = t0.elapsed_time(tc)
+        plan.close()
+        P.FreeSequence(seq)
+    res["prefill_ms_without_sends"] = round(base, 3)
+    res["slowdown_pct"] = round(100 * (res["prefill_ms_with_sends"] / base - 1), 2)
+    res["per_layer_payload_mb"] = round(e * BPT / 1e6, 2)
+    res["note"] = ("70B-layer-FLOP bf16 GEMM per layer (cuBLAS, compute stand-in) + KV append; "
+                   "per-layer DirectSend on a second stream; P and D on one GPU")
+    del P, D, X, Wt, Y, rows
+    torch.cuda.empty_cache()
+    return res
 
 
 def measure_handoff(torch) -> dict:
@@ -505,6 +584,61 @@ def measure_handoff(torch) -> dict:
                    "P and D on one GPU")
     del P, D
     return res
+
+
+def measure_sweep(torch) -> dict:
+    """Config 5: DirectSend of n tokens x 80 layers (70B shape), n = 16 (one
+    page) ... 32768, P and D on one GPU; device time per migration (one
+    validation + one copy launch), median of 5."""
+    from paper_2412_12488_b200 import KVCache
+
+    peak, _ = _peaks()
+    out = {}
+    nmax = 32768
+    prompt = np.random.Generator(np.random.MT19937(9)).integers(0, 256, nmax + 1).astype(np.int32)
+    pages = nmax // PAGE + 16
+    P = KVCache(num_pages=pages, page_size=PAGE, layers=L, dim=W, device=0, rank=0)
+    D = KVCache(num_pages=pages, page_size=PAGE, layers=L, dim=W, device=0, rank=1)
+    P.attach_peer(1, D)
+    r = P.PrepRecv(1, prompt, nmax + 1)
+    g = torch.empty(r.addr.token_count * W, dtype=torch.int64, device="cuda").random_()
+    for layer in range(L):
+        P.apply_remote_write_async(r.addr, layer, g.data_ptr(), r.addr.token_count * W, 0, 0)
+    torch.cuda.synchronize()
+    P.synchronize()
+    assert P.DrainReceiveCompletions() == [1]
+    del g
+    s = torch.cuda.Stream()
+    seq = 100
+    for n in (16, 64, 256, 1024, 4096, 8192, 16384, 32768):
+        times, walls = [], []
+        for rep in range(5):
+            seq += 1
+            rr = D.PrepRecv(seq, prompt[:n + 1], -1)
+            plan = P.begin_direct_send(1, (0, n), 1, rr.addr, rep)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            # Device time: the launch is queued behind a short sleep so host
+            # launch latency stays outside e0..e1; wall time: call to sync.
+            with torch.cuda.stream(s):
+                torch.cuda._sleep(100_000)
+            e0.record(s)
+            w0 = time.perf_counter()
+            P.launch_direct_send_async(plan, (0, L), s.cuda_stream)
+            e1.record(s)
+            s.synchronize()
+            walls.append(time.perf_counter() - w0)
+            assert D.DrainReceiveCompletions() == [seq]
+            times.append(e0.elapsed_time(e1) / 1e3)
+            plan.close()
+            D.FreeSequence(seq)
+        t, wt = float(np.median(times)), float(np.median(walls))
+        payload = n * L * BPT
+        out[str(n)] = {"device_us": round(1e6 * t, 1), "payload_gbs": round(payload / t / 1e9, 1),
+                       "hbm_frac": round(2 * payload / t / 1e9 / peak, 4),
+                       "api_wall_us": round(1e6 * wt, 1)}
+    del P, D
+    torch.cuda.empty_cache()
+    return out
 
 
 def measure_append_gather(torch) -> dict:
