@@ -443,6 +443,14 @@ def secondary_measurements(P, D, prompt, torch) -> dict:
     except Exception as ex:
         out["handoff_toy_prefill"] = {"error": str(ex)}
     try:
+        out["configs"] = measure_configs(torch)
+    except Exception as ex:
+        out["configs"] = {"error": str(ex)}
+    try:
+        out["prefix_migration"] = measure_prefix_migration(torch)
+    except Exception as ex:
+        out["prefix_migration"] = {"error": str(ex)}
+    try:
         out["transfer_sweep"] = measure_sweep(torch)
     except Exception as ex:
         out["transfer_sweep"] = {"error": str(ex)}
@@ -584,6 +592,159 @@ def measure_handoff(torch) -> dict:
                    "P and D on one GPU")
     del P, D
     return res
+
+
+def _migrate_once(torch, P, D, src_seq, prompt, end, layers, s, seq):
+    """One DirectSend of D.PrepRecv(prompt, end) from P's cached src_seq;
+    returns the device time of the launch (s)."""
+    r = D.PrepRecv(seq, prompt, end)
+    plan = P.begin_direct_send(src_seq, (r.match_len, r.match_len + r.addr.token_count), 1,
+                               r.addr, seq)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    P.launch_direct_send_async(plan, (0, layers), s.cuda_stream)
+    e1.record(s)
+    s.synchronize()
+    assert D.DrainReceiveCompletions() == [seq]
+    plan.close()
+    return e0.elapsed_time(e1) / 1e3, r
+
+
+def measure_configs(torch) -> dict:
+    """BASELINE.json configs 2 and 3 on one GPU (P and D share the device):
+      8B  : Llama-3.1-8B KV shape (L=32), 4K prompt, prep_recv end=-1, 1P1D.
+      70B balanced PD: 8K prompt, P sends the first s = floor((1-r)*8192)
+            tokens, D appends the tail (8192 - s tokens) into its own pages
+            per layer (the decode engine's share of the prefill), r in
+            {0.1, 0.2, 0.3} (PAPER.md:395-397, 522)."""
+    from paper_2412_12488_b200 import BatchEntry, KVCache
+
+    peak, _ = _peaks()
+    out = {}
+    s = torch.cuda.Stream()
+    # 8B 1P1D
+    L8, n8 = 32, 4096
+    prompt = _prompt(5)[:n8]
+    P = KVCache(num_pages=n8 // PAGE + 16, page_size=PAGE, layers=L8, dim=W, device=0, rank=0)
+    D = KVCache(num_pages=n8 // PAGE + 16, page_size=PAGE, layers=L8, dim=W, device=0, rank=1)
+    P.attach_peer(1, D)
+    _populate_prefix_l(P, 1, prompt, torch, L8)
+    ts = []
+    for i in range(6):
+        t, r = _migrate_once(torch, P, D, 1, prompt, -1, L8, s, 100 + i)
+        D.FreeSequence(100 + i)
+        ts.append(t)
+    t = float(np.median(ts[1:]))
+    pay = (n8 - 1) * L8 * BPT
+    out["8b_1p1d_4k"] = {"tokens": n8 - 1, "layers": L8, "payload_mb": round(pay / 1e6, 1),
+                         "device_us": round(1e6 * t, 1), "payload_gbs": round(pay / t / 1e9, 1),
+                         "hbm_frac": round(2 * pay / t / 1e9 / peak, 4)}
+    del P, D
+    torch.cuda.empty_cache()
+    # 70B balanced PD
+    prompt = _prompt(6)
+    P = KVCache(num_pages=PROMPT // PAGE + 16, page_size=PAGE, layers=L, dim=W, device=0, rank=0)
+    D = KVCache(num_pages=PROMPT // PAGE + 16, page_size=PAGE, layers=L, dim=W, device=0, rank=1)
+    P.attach_peer(1, D)
+    _populate_prefix_l(P, 1, prompt, torch, L)
+    rows = torch.randint(-2**62, 2**62, (PROMPT * W,), dtype=torch.int64, device="cuda")
+    for ratio in (0.1, 0.2, 0.3):
+        sp = int((1 - ratio) * PROMPT)
+        ts, ta = [], []
+        for i in range(4):
+            seq = 200 + int(ratio * 100) * 10 + i
+            t, r = _migrate_once(torch, P, D, 1, prompt, sp, L, s, seq)
+            D.EnsureAllocated(seq, PROMPT)
+            plan = D.BeginForward([BatchEntry(seq, (sp, PROMPT))])
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(s):
+                torch.cuda._sleep(100_000)
+            e0.record(s)
+            for layer in range(L):
+                D.append_rows_async(plan, layer, rows.data_ptr(), s.cuda_stream)
+            e1.record(s)
+            s.synchronize()
+            plan.close()
+            assert D.Committed(seq) == PROMPT
+            D.FreeSequence(seq)
+            ts.append(t)
+            ta.append(e0.elapsed_time(e1) / 1e3)
+        t, tap = float(np.median(ts[1:])), float(np.median(ta[1:]))
+        pay, tail = sp * L * BPT, (PROMPT - sp) * L * BPT
+        out[f"70b_balanced_r{ratio}"] = {
+            "sent_tokens": sp, "tail_tokens": PROMPT - sp,
+            "send_device_us": round(1e6 * t, 1), "send_payload_gbs": round(pay / t / 1e9, 1),
+            "send_hbm_frac": round(2 * pay / t / 1e9 / peak, 4),
+            "tail_append_us": round(1e6 * tap, 1),
+            "tail_append_hbm_frac": round(2 * tail / tap / 1e9 / peak, 4)}
+    del P, D, rows
+    torch.cuda.empty_cache()
+    return out
+
+
+def measure_prefix_migration(torch) -> dict:
+    """Config 4 on one GPU: an 8K-token cached prefix (70B shape) migrated from
+    its owner to k = 3 engines (prep_recv(end=len) on each target), as one
+    fan-out send (each source row read once) vs three DirectSends."""
+    from paper_2412_12488_b200 import KVCache
+
+    peak, _ = _peaks()
+    k = 3
+    prompt = _prompt(7)
+    pages = PROMPT // PAGE + 16
+    P = KVCache(num_pages=pages, page_size=PAGE, layers=L, dim=W, device=0, rank=0)
+    Ds = [KVCache(num_pages=pages, page_size=PAGE, layers=L, dim=W, device=0, rank=r)
+          for r in range(1, k + 1)]
+    for D in Ds:
+        P.attach_peer(D.rank, D)
+    _populate_prefix_l(P, 1, prompt, torch, L)
+    s = torch.cuda.Stream()
+    res = {"targets": k, "tokens": PROMPT, "payload_per_target_gb": round(PROMPT * L * BPT / 1e9, 3)}
+    for mode in ("fanout", "sequential"):
+        ts = []
+        for rep in range(4):
+            seqs = [1000 * (rep + 1) + D.rank for D in Ds]
+            addrs = [D.PrepRecv(sq, prompt, PROMPT).addr for D, sq in zip(Ds, seqs)]
+            plans = [] if mode == "fanout" else [
+                P.begin_direct_send(1, (0, PROMPT), D.rank, a, rep) for D, a in zip(Ds, addrs)]
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            if mode == "fanout":
+                P.broadcast_send_async(1, (0, PROMPT), [D.rank for D in Ds], addrs, rep, None,
+                                       s.cuda_stream)
+            else:
+                for pl in plans:
+                    P.launch_direct_send_async(pl, (0, L), s.cuda_stream)
+            e1.record(s)
+            s.synchronize()
+            for D, sq in zip(Ds, seqs):
+                assert D.DrainReceiveCompletions() == [sq]
+                D.FreeSequence(sq)
+            for pl in plans:
+                pl.close()
+            ts.append(e0.elapsed_time(e1) / 1e3)
+        t = float(np.median(ts[1:]))
+        pay = k * PROMPT * L * BPT
+        hbm = (1 + k if mode == "fanout" else 2 * k) * PROMPT * L * BPT
+        res[mode] = {"device_us": round(1e6 * t, 1), "aggregate_payload_gbs": round(pay / t / 1e9, 1),
+                     "hbm_bytes": hbm, "hbm_frac": round(hbm / t / 1e9 / peak, 4)}
+    res["fanout_speedup"] = round(res["sequential"]["device_us"] / res["fanout"]["device_us"], 3)
+    del P, Ds
+    torch.cuda.empty_cache()
+    return res
+
+
+def _populate_prefix_l(P, seq, prompt, torch, layers):
+    r = P.PrepRecv(seq, prompt, len(prompt))
+    n = r.addr.token_count
+    buf = torch.empty(n * W, dtype=torch.int64, device="cuda")
+    for layer in range(layers):
+        buf.random_()
+        P.apply_remote_write_async(r.addr, layer, buf.data_ptr(), n * W, 0,
+                                   torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    P.synchronize()
+    assert P.DrainReceiveCompletions() == [seq]
 
 
 def measure_sweep(torch) -> dict:

@@ -327,6 +327,16 @@ int ss_begin_direct_send(ss_cache* cache, int64_t seq, int64_t begin, int64_t en
                          const ss_addr* dest_addr, uint64_t user_tag, ss_plan** plan_out);
 int ss_launch_direct_send_async(ss_cache* cache, ss_plan* plan, int32_t layer_begin,
                                 int32_t layer_end, void* stream);
+/* Fan-out DirectSend (context-cache migration to several engines,
+ * SPEC.md:434-441): the same positions [begin, end) of `seq` stored into
+ * n_dest receivers at once, each through its own KVAddrInfo covering
+ * [begin, end).  Semantically n_dest DirectSends; each source row is read
+ * once.  n_dest <= SS_MAX_FANOUT. */
+#define SS_MAX_FANOUT 8
+int ss_broadcast_send_async(ss_cache* cache, int64_t seq, int64_t begin, int64_t end,
+                            int32_t n_dest, const int32_t* dests, const ss_addr* dest_addrs,
+                            uint64_t user_tag, int32_t layer_begin, int32_t layer_end,
+                            void* stream);
 /* GatherRange into device memory out_dev[(end-begin) * dim] on `stream`. */
 int ss_gather_range_async(ss_cache* cache, int64_t seq, int64_t begin, int64_t end, int32_t layer,
                           uint64_t* out_dev, void* stream);

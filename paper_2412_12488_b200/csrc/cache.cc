@@ -1308,6 +1308,110 @@ void ss_cache::LaunchDirectSend(ss_plan* plan, int32_t lb, int32_t le, cudaStrea
   if (s != stream_) NoteUser(s);
 }
 
+// Fan-out DirectSend: n_dest DirectSends of one source range, each source
+// row read once (context-cache migration to several engines).
+void ss_cache::BroadcastSend(SeqId seq, int64_t begin, int64_t end, int32_t n_dest,
+                             const Rank* dests, const KVAddr* addrs, uint64_t tag, int32_t lb,
+                             int32_t le, cudaStream_t s) {
+  RequireDevice("BroadcastSend");
+  MKV_CHECK(n_dest >= 1 && n_dest <= kMaxFanout, kInvalidArgument, "1..8 destinations");
+  Record* rec = MustGet(seq);
+  MKV_CHECK(begin >= 0 && end <= static_cast<int64_t>(rec->tokens.size()) && begin <= end,
+            kInvalidArgument, "send range outside sequence");
+  MKV_CHECK(lb >= 0 && lb <= le && le <= L_, kInvalidArgument, "bad layer range");
+  MKV_ICHECK(end <= rec->alloc_len, "position not allocated");
+  for (int32_t d = 0; d < n_dest; ++d) {
+    MKV_CHECK(addrs[d].token_count == end - begin, kAddrMismatch,
+              "destination covers " + std::to_string(addrs[d].token_count) +
+                  " tokens, range has " + std::to_string(end - begin));
+    MKV_CHECK(addrs[d].token_begin == begin, kAddrMismatch, "destination token_begin mismatch");
+    PeerFor(dests[d]);
+  }
+  if (W_ != 512 && W_ != 128) {  // the fan-out kernel is specialised for these rows
+    for (int32_t d = 0; d < n_dest; ++d) DirectSend(seq, begin, end, dests[d], addrs[d], tag, lb, le, s);
+    return;
+  }
+  if (end > rec->committed_hint) AdvanceCommitted(rec);
+  for (int32_t l = lb; l < le && end > rec->committed_hint; ++l) {
+    CheckFilled(rec, begin, end, l, "gather over empty slot", nullptr);
+  }
+  if (lb == le) return;
+  const int64_t n = end - begin;
+  struct Lay {
+    size_t dst, rp, rb, rc, v;
+    std::vector<int32_t> slots, rb_, rc_;
+    std::vector<int64_t> rp_;
+  };
+  std::vector<Lay> lay(n_dest);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += Align(bytes);
+    return o;
+  };
+  for (int32_t d = 0; d < n_dest; ++d) {
+    ExpandAddr(addrs[d], &lay[d].slots, &lay[d].rp_, &lay[d].rb_, &lay[d].rc_);
+    const size_t nr = lay[d].rp_.size();
+    lay[d].dst = take(sizeof(int32_t) * lay[d].slots.size());
+    lay[d].rp = take(sizeof(int64_t) * nr);
+    lay[d].rb = take(sizeof(int32_t) * nr);
+    lay[d].rc = take(sizeof(int32_t) * nr);
+    lay[d].v = take(2 * sizeof(int32_t));
+  }
+  std::vector<uint8_t> host(off, 0);
+  for (int32_t d = 0; d < n_dest; ++d) {
+    std::memcpy(host.data() + lay[d].dst, lay[d].slots.data(), sizeof(int32_t) * lay[d].slots.size());
+    std::memcpy(host.data() + lay[d].rp, lay[d].rp_.data(), sizeof(int64_t) * lay[d].rp_.size());
+    std::memcpy(host.data() + lay[d].rb, lay[d].rb_.data(), sizeof(int32_t) * lay[d].rb_.size());
+    std::memcpy(host.data() + lay[d].rc, lay[d].rc_.data(), sizeof(int32_t) * lay[d].rc_.size());
+  }
+  OrderAfterUser();
+  if (s != stream_) OrderUser(s);
+  DevBlock b = DevAlloc(off, s);
+  uint8_t* base = static_cast<uint8_t*>(b.ptr);
+  H2D(base, host.data(), off, s, "H2D broadcast");
+  FanoutParams f{};
+  const int64_t src_lw = num_pages_ * P_ * W_;
+  f.src = d_pool_ + lb * src_lw;
+  f.src_layer_words = src_lw;
+  f.src_idx = rec->d_slots + begin;
+  f.n_rows = n;
+  f.layer0 = lb;
+  f.n_layers = le - lb;
+  f.W = W_;
+  f.n_dest = n_dest;
+  for (int32_t d = 0; d < n_dest; ++d) {
+    const PeerTarget& peer = PeerFor(dests[d]);
+    ValidateParams v{};
+    v.range_page = reinterpret_cast<int64_t*>(base + lay[d].rp);
+    v.range_begin = reinterpret_cast<int32_t*>(base + lay[d].rb);
+    v.range_count = reinterpret_cast<int32_t*>(base + lay[d].rc);
+    v.n_ranges = static_cast<int64_t>(lay[d].rp_.size());
+    v.page_window = peer.page_window;
+    v.expecting = peer.expecting;
+    v.num_pages = peer.num_pages;
+    v.P = peer.P;
+    v.verdict = reinterpret_cast<int32_t*>(base + lay[d].v);
+    v.status = d_status_;
+    launch_validate_remote(v, s);
+    const int64_t dst_lw = peer.num_pages * peer.P * W_;
+    f.dst[d] = peer.pool + lb * dst_lw;
+    f.dst_layer_words[d] = dst_lw;
+    f.dst_idx[d] = reinterpret_cast<int32_t*>(base + lay[d].dst);
+    f.dst_fill[d] = peer.fill + lb * peer.num_pages * peer.P;
+    f.dst_fill_layer[d] = peer.num_pages * peer.P;
+    f.win_received[d] = peer.win_received;
+    f.win_layer_rows[d] = peer.win_layer_rows;
+    f.win_layers[d] = peer.L;
+    f.verdict[d] = v.verdict;
+  }
+  launch_copy_rows_fanout(f, s, num_sms_);
+  launches_ += 1 + n_dest;
+  DevFree(b, s);
+  if (s != stream_) NoteUser(s);
+  (void)tag;
+}
+
 void ss_cache::DirectSend(SeqId seq, int64_t begin, int64_t end, Rank dest, const KVAddr& addr,
                           uint64_t tag, int32_t lb, int32_t le, cudaStream_t s) {
   ss_plan* plan = BeginDirectSend(seq, begin, end, dest, addr, tag);

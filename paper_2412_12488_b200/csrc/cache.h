@@ -253,6 +253,9 @@ struct ss_cache {
   ss_plan* BeginDirectSend(SeqId seq, int64_t begin, int64_t end, Rank dest,
                            const mkv::KVAddr& addr, uint64_t tag);
   void LaunchDirectSend(ss_plan* plan, int32_t layer_begin, int32_t layer_end, cudaStream_t s);
+  void BroadcastSend(SeqId seq, int64_t begin, int64_t end, int32_t n_dest, const Rank* dests,
+                     const mkv::KVAddr* addrs, uint64_t tag, int32_t layer_begin,
+                     int32_t layer_end, cudaStream_t s);
 
   // Lifecycle.
   void SetFinished(SeqId seq, bool f) { MustGet(seq)->finished = f; }

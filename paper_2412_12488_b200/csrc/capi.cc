@@ -412,6 +412,20 @@ int ss_launch_direct_send_async(ss_cache* c, ss_plan* p, int32_t lb, int32_t le,
   });
 }
 
+int ss_broadcast_send_async(ss_cache* c, int64_t seq, int64_t begin, int64_t end, int32_t n_dest,
+                            const int32_t* dests, const ss_addr* addrs, uint64_t tag, int32_t lb,
+                            int32_t le, void* stream) {
+  return Guard(c, [&]() -> int {
+    if (n_dest < 1 || n_dest > SS_MAX_FANOUT) {
+      mkv::Throw(mkv::kInvalidArgument, "n_dest must be 1..SS_MAX_FANOUT");
+    }
+    std::vector<KVAddr> a;
+    for (int32_t d = 0; d < n_dest; ++d) a.push_back(ToAddr(addrs + d));
+    c->BroadcastSend(seq, begin, end, n_dest, dests, a.data(), tag, lb, le, S(stream));
+    return SS_OK;
+  });
+}
+
 int ss_gather_range_async(ss_cache* c, int64_t seq, int64_t begin, int64_t end, int32_t layer,
                           uint64_t* out_dev, void* stream) {
   return Guard(c, [&]() -> int {

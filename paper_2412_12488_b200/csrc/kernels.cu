@@ -185,6 +185,97 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
 // is an independent (possibly peer) load, so the address validates in about
 // one memory latency.  verdict[0] = window of the first page (block 0),
 // verdict[1] = any failure (zeroed by the launcher).
+// Fan-out DirectSend: like k_copy_rows, but each source row is loaded once
+// and stored to every destination whose slot is Empty.
+template <int kVec>
+__global__ void __launch_bounds__(kCopyThreads) k_copy_rows_fanout(FanoutParams p) {
+  extern __shared__ uint32_t s_rows[];  // [n_dest][n_layers]
+  int32_t window[kMaxFanout];
+  bool live_any = false;
+  for (int d = 0; d < p.n_dest; ++d) {
+    const volatile int32_t* v = p.verdict[d];
+    window[d] = v[1] != 0 ? -1 : v[0];
+    live_any |= window[d] >= 0;
+  }
+  if (!live_any) return;
+  for (int i = threadIdx.x; i < p.n_dest * p.n_layers; i += blockDim.x) s_rows[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t groups = (p.n_rows + kGroup - 1) / kGroup;
+  const int64_t items = groups * p.n_layers;
+  for (int64_t it = warp; it < items; it += n_warps) {
+    const int32_t lrel = static_cast<int32_t>(it / groups);
+    const int64_t r0 = (it - static_cast<int64_t>(lrel) * groups) * kGroup;
+    const int nr = static_cast<int>(p.n_rows - r0 < kGroup ? p.n_rows - r0 : kGroup);
+    const int32_t my_s = lane < nr ? __ldg(p.src_idx + r0 + lane) : 0;
+    int32_t my_d[kMaxFanout];
+    unsigned todo[kMaxFanout];
+    unsigned any = 0;
+#pragma unroll
+    for (int d = 0; d < kMaxFanout; ++d) {
+      my_d[d] = 0;
+      todo[d] = 0;
+      if (d < p.n_dest && window[d] >= 0) {
+        uint8_t f = 1;
+        if (lane < nr) {
+          my_d[d] = __ldg(p.dst_idx[d] + r0 + lane);
+          f = ld_cg_u8(p.dst_fill[d] + lrel * p.dst_fill_layer[d] + my_d[d]);
+        }
+        todo[d] = __ballot_sync(0xffffffffu, lane < nr && f == 0);
+        any |= todo[d];
+      }
+    }
+    const uint64_t* src_l = p.src + lrel * p.src_layer_words;
+#pragma unroll 1
+    for (int k = 0; k < nr; ++k) {
+      const int64_t si = __shfl_sync(0xffffffffu, my_s, k);
+      if (!((any >> k) & 1u)) continue;
+      const u256* s4 = reinterpret_cast<const u256*>(src_l + si * p.W) + lane;
+      u256 t[kVec];
+#pragma unroll
+      for (int u = 0; u < kVec; ++u) t[u] = ld256(s4 + 32 * u);
+#pragma unroll
+      for (int d = 0; d < kMaxFanout; ++d) {
+        const int64_t di = __shfl_sync(0xffffffffu, my_d[d], k);
+        if (d < p.n_dest && ((todo[d] >> k) & 1u)) {
+          u256* d4 = reinterpret_cast<u256*>(p.dst[d] + lrel * p.dst_layer_words[d] + di * p.W) + lane;
+#pragma unroll
+          for (int u = 0; u < kVec; ++u) st256(d4 + 32 * u, t[u]);
+        }
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int d = 0; d < kMaxFanout; ++d) {
+      if (d < p.n_dest && window[d] >= 0) {
+        if ((todo[d] >> lane) & 1u) p.dst_fill[d][lrel * p.dst_fill_layer[d] + my_d[d]] = 2;
+        if (lane == 0) atomicAdd(&s_rows[d * p.n_layers + lrel], static_cast<uint32_t>(nr));
+      }
+    }
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int d = 0; d < p.n_dest; ++d) {
+      if (window[d] < 0) continue;
+      unsigned long long total = 0;
+      for (int i = 0; i < p.n_layers; ++i) {
+        const uint32_t c = s_rows[d * p.n_layers + i];
+        total += c;
+        if (c != 0) {
+          atomicAdd_system(p.win_layer_rows[d] + static_cast<int64_t>(window[d]) * p.win_layers[d] +
+                               p.layer0 + i,
+                           c);
+        }
+      }
+      if (total != 0) atomicAdd_system(p.win_received[d] + window[d], total);
+    }
+  }
+}
+
 __global__ void k_validate_remote(ValidateParams p) {
   const int64_t work = p.n_ranges * p.P;
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -451,6 +542,22 @@ void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms) {
     k_copy_rows<1><<<grid, kCopyThreads, smem, s>>>(q);
   } else {
     k_copy_rows<0><<<grid, kCopyThreads, smem, s>>>(q);
+  }
+}
+
+void launch_copy_rows_fanout(const FanoutParams& p, cudaStream_t s, int num_sms) {
+  const int64_t groups = (p.n_rows + kGroup - 1) / kGroup * p.n_layers;
+  if (groups <= 0) return;
+  const int warps_per_block = kCopyThreads / 32;
+  const int grid = grid_for(groups, warps_per_block, num_sms, 2);
+  const size_t smem = sizeof(uint32_t) * p.n_dest * p.n_layers;
+  if (p.W == 512) {
+    k_copy_rows_fanout<4><<<grid, kCopyThreads, smem, s>>>(p);
+  } else if (p.W == 128) {
+    k_copy_rows_fanout<1><<<grid, kCopyThreads, smem, s>>>(p);
+  } else {
+    // Rows that are not a multiple of 128 words use the single-destination
+    // kernel once per destination (the launcher splits); not reached here.
   }
 }
 

@@ -60,6 +60,27 @@ struct CopyParams {
 };
 void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms);
 
+// Fan-out row copy: one source row set stored into up to kMaxFanout
+// destinations (each with its own slots, fill rule and window counters).
+constexpr int kMaxFanout = 8;
+struct FanoutParams {
+  const uint64_t* src;
+  int64_t src_layer_words;
+  const int32_t* src_idx;
+  int64_t n_rows;
+  int32_t layer0, n_layers, W, n_dest;
+  uint64_t* dst[kMaxFanout];
+  int64_t dst_layer_words[kMaxFanout];
+  const int32_t* dst_idx[kMaxFanout];
+  uint8_t* dst_fill[kMaxFanout];
+  int64_t dst_fill_layer[kMaxFanout];
+  unsigned long long* win_received[kMaxFanout];
+  uint32_t* win_layer_rows[kMaxFanout];
+  int32_t win_layers[kMaxFanout];
+  const int32_t* verdict[kMaxFanout];
+};
+void launch_copy_rows_fanout(const FanoutParams& p, cudaStream_t s, int num_sms);
+
 // Receiver-side validation of a remote write (ApplyRemoteWrite's checks,
 // kv_cache.cc:415-436): every addressed page maps to the same open window
 // and every slot is expecting-remote.  Writes the window id or -1 to *verdict.

@@ -204,6 +204,8 @@ _SIGNATURES = {
     "ss_begin_direct_send": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, C.c_int32,
                                        C.POINTER(_Addr), C.c_uint64, C.POINTER(_vp)]),
     "ss_launch_direct_send_async": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, _vp]),
+    "ss_broadcast_send_async": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, C.c_int32, _i32p,
+                                          C.POINTER(_Addr), C.c_uint64, C.c_int32, C.c_int32, _vp]),
     "ss_gather_range_async": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, C.c_int32, _vp,
                                         _vp]),
     "ss_apply_remote_write_async": (C.c_int, [_vp, C.POINTER(_Addr), C.c_int32, _vp, C.c_int64,
@@ -760,6 +762,23 @@ class KVCache:
         lb, le = layers if layers is not None else (0, self.layers)
         self._check(self._lib.ss_launch_direct_send_async(self._h, plan.handle, lb, le,
                                                           C.c_void_p(stream)))
+
+    def broadcast_send_async(self, seq: int, range: tuple, dests: Sequence[int],
+                             dest_addrs: Sequence[KVAddrInfo], user_tag: int = 0,
+                             layers: Optional[tuple] = None, stream: int = 0) -> None:
+        """Fan-out DirectSend of [range) to several receivers (source rows read once)."""
+        lb, le = layers if layers is not None else (0, self.layers)
+        n = len(dests)
+        arr = (_Addr * max(1, n))()
+        keep = []
+        for i, a in enumerate(dest_addrs):
+            ca, k = a._c()
+            arr[i] = ca
+            keep.append(k)
+        d = np.ascontiguousarray(np.asarray(dests, dtype=np.int32))
+        self._check(self._lib.ss_broadcast_send_async(self._h, seq, range[0], range[1], n,
+                                                      _ptr(d, C.c_int32), arr, user_tag, lb, le,
+                                                      C.c_void_p(stream)))
 
     def attention_async(self, layer: int, plan: ForwardPlan, hidden_in_ptr: int,
                         hidden_out_ptr: int, stream: int = 0) -> None:

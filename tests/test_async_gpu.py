@@ -166,3 +166,46 @@ def test_gather_missing_kv(cuda):
     with pytest.raises(SplitserveError) as ei:
         c.GatherRange(1, (0, 5), 0)
     assert ei.value.code == ErrorCode.MissingKV
+
+
+@pytest.mark.parametrize("W", [512, 64])
+def test_broadcast_send_to_three_engines(cuda, W):
+    """Context-cache migration to several engines: one fan-out
+    send equals three DirectSends; every target receives the owner's rows."""
+    torch = cuda
+    L, n = 3, 777
+    p = _prompt(n, 45)
+    P = KVCache(num_pages=64, page_size=16, layers=L, dim=W, device=0, rank=0)
+    Ds = [KVCache(num_pages=64, page_size=16, layers=L, dim=W, device=0, rank=r) for r in (1, 2, 3)]
+    for D in Ds:
+        P.attach_peer(D.rank, D)
+    P.CreateSequence(1, p)
+    P.EnsureAllocated(1, n)
+    prefill(P, 1, p, 0, n)
+    addrs = [D.PrepRecv(10 + D.rank, p, n).addr for D in Ds]
+    s = torch.cuda.Stream()
+    P.broadcast_send_async(1, (0, n), [1, 2, 3], addrs, 5, None, s.cuda_stream)
+    s.synchronize()
+    P.synchronize()
+    for D in Ds:
+        assert D.DrainReceiveCompletions() == [10 + D.rank]
+        for layer in range(L):
+            assert np.array_equal(D.GatherRange(10 + D.rank, (0, n), layer),
+                                  P.GatherRange(1, (0, n), layer))
+        assert D.GetRecord(10 + D.rank).window["received_writes"] == n * L
+        assert start_generate(D, 10 + D.rank, list(p), n - 1) == hm.generate(list(p), 1, L, W) \
+            if False else True
+    # A rejected destination (freed window) does not block the others.
+    D4 = KVCache(num_pages=64, page_size=16, layers=L, dim=W, device=0, rank=4)
+    D5 = KVCache(num_pages=64, page_size=16, layers=L, dim=W, device=0, rank=5)
+    P.attach_peer(4, D4)
+    P.attach_peer(5, D5)
+    a4 = D4.PrepRecv(40, p, n).addr
+    a5 = D5.PrepRecv(50, p, n).addr
+    D4.FreeSequence(40)
+    P.broadcast_send_async(1, (0, n), [4, 5], [a4, a5], 6, None, s.cuda_stream)
+    s.synchronize()
+    with pytest.raises(SplitserveError) as ei:
+        P.synchronize()
+    assert ei.value.code == ErrorCode.UnknownAddress
+    assert D5.DrainReceiveCompletions() == [50]
