@@ -464,6 +464,10 @@ int ss_paged_decode_attention_async(ss_cache*, ss_plan*, int32_t, int32_t, int32
                                     const void*, void*, void*) {
   return SS_ERR_UNSUPPORTED;
 }
+int ss_paged_prefill_attention_async(ss_cache*, int64_t, int64_t, int64_t, int32_t, int32_t,
+                                     int32_t, int32_t, float, const void*, void*, void*) {
+  return SS_ERR_UNSUPPORTED;
+}
 int ss_pool_layer_ptr(ss_cache*, int32_t, void**) { return SS_ERR_UNSUPPORTED; }
 int ss_wait_receive_async(ss_cache*, int64_t, int64_t, void*) { return SS_ERR_UNSUPPORTED; }
 int ss_copy_counters(const ss_cache*, int64_t* h2d, int64_t* d2h) {

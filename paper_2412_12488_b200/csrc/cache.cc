@@ -1806,3 +1806,32 @@ void ss_cache::DecodeAttention(ss_plan* plan, int32_t layer, int32_t hq, int32_t
   launches_ += 2;
   if (s != stream_) NoteUser(s);
 }
+
+// Causal prefill attention of queries [q_begin, q_end) of `seq` over keys
+// [0, q_end) of this layer, read through the sequence's HBM page table
+// (balanced-PD tail prefill on the decode engine).  The
+// caller has written this layer's K||V rows for [0, q_end) (the queries' own
+// rows through ss_append_rows_async, the prefix by a receive or earlier
+// prefill); per-layer fill is not re-checked here.
+void ss_cache::PrefillAttention(int64_t seq, int64_t q_begin, int64_t q_end, int32_t layer,
+                                int32_t hq, int32_t hkv, int32_t hd, float scale, const void* q,
+                                void* out, cudaStream_t s) {
+  RequireDevice("PrefillAttention");
+  Record* rec = MustGet(seq);
+  MKV_CHECK(layer >= 0 && layer < L_, kInvalidArgument, "layer out of range");
+  MKV_CHECK(0 <= q_begin && q_begin < q_end && q_end <= rec->alloc_len, kInvalidArgument,
+            "query range must be non-empty and allocated");
+  MKV_CHECK(q_end <= INT32_MAX, kInvalidArgument, "context too long");
+  MKV_CHECK(hd == 128 && hkv >= 1 && hq == 8 * hkv, kInvalidArgument,
+            "prefill attention supports head_dim 128 with 8 query heads per kv head");
+  MKV_CHECK(static_cast<int64_t>(W_) * 8 == 4LL * hkv * hd, kInvalidArgument,
+            "entry width must equal K||V bf16 bytes (dim * 8 == 4 * num_kv_heads * head_dim)");
+  OrderAfterUser();
+  if (s != stream_) OrderUser(s);
+  const bool ok = launch_prefill_attn(PoolLayer(layer), static_cast<int64_t>(W_) * 4, rec->d_slots,
+                                      q, static_cast<int>(q_begin),
+                                      static_cast<int>(q_end - q_begin), hq, hkv, hd, scale, out, s);
+  MKV_CHECK(ok, kInvalidArgument, "unsupported prefill attention shape");
+  launches_ += 1;
+  if (s != stream_) NoteUser(s);
+}

@@ -284,6 +284,9 @@ struct ss_cache {
   void ImportIpc(Rank dest, const ss_ipc_handle* h);
   void DetachPeer(Rank dest);
   ss_plan* BeginDecode(const int64_t* seqs, const int64_t* ctx_lens, int64_t batch);
+  void PrefillAttention(int64_t seq, int64_t q_begin, int64_t q_end, int32_t layer, int32_t hq,
+                        int32_t hkv, int32_t hd, float scale, const void* q, void* out,
+                        cudaStream_t s);
   void DecodeAttention(ss_plan* plan, int32_t layer, int32_t hq, int32_t hkv, int32_t hd,
                        float scale, const void* q, void* out, cudaStream_t s);
   void DestroyPlan(ss_plan* plan);

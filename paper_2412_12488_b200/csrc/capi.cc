@@ -468,6 +468,15 @@ int ss_paged_decode_attention_async(ss_cache* c, ss_plan* plan, int32_t layer, i
   });
 }
 
+int ss_paged_prefill_attention_async(ss_cache* c, int64_t seq, int64_t q_begin, int64_t q_end,
+                                     int32_t layer, int32_t hq, int32_t hkv, int32_t hd,
+                                     float scale, const void* q, void* out, void* stream) {
+  return Guard(c, [&]() -> int {
+    c->PrefillAttention(seq, q_begin, q_end, layer, hq, hkv, hd, scale, q, out, S(stream));
+    return SS_OK;
+  });
+}
+
 int ss_pool_layer_ptr(ss_cache* c, int32_t layer, void** dev_ptr) {
   return Guard(c, [&]() -> int {
     if (c->device() < 0) mkv::ThrowStatus(SS_ERR_NO_DEVICE, "pool on a host-only cache");

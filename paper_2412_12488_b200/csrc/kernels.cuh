@@ -159,4 +159,11 @@ bool launch_decode_attn(const void* pool_l, int64_t row_elems, const int32_t* sl
                         int Hkv, int D, float scale, float* part_o, float* part_ml, void* out,
                         int grid, cudaStream_t s);
 
+// Paged causal GQA prefill attention on tcgen05 (prefill_attn.cu): queries
+// [q_pos0, q_pos0 + n_q) of one sequence over keys [0, q_pos0 + n_q).
+// Requires head_dim 128 and Hq == 8 * Hkv; returns false otherwise.
+bool launch_prefill_attn(const void* pool_l, int64_t row_elems, const int32_t* slots,
+                         const void* q, int q_pos0, int n_q, int Hq, int Hkv, int D, float scale,
+                         void* out, cudaStream_t s);
+
 }  // namespace mkv

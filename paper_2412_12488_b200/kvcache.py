@@ -214,6 +214,9 @@ _SIGNATURES = {
     "ss_begin_decode": (C.c_int, [_vp, _i64p, _i64p, C.c_int64, C.POINTER(_vp)]),
     "ss_paged_decode_attention_async": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, C.c_int32,
                                                   C.c_int32, C.c_float, _vp, _vp, _vp]),
+    "ss_paged_prefill_attention_async": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64,
+                                                   C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                                   C.c_float, _vp, _vp, _vp]),
     "ss_pool_layer_ptr": (C.c_int, [_vp, C.c_int32, C.POINTER(_vp)]),
     "ss_wait_receive_async": (C.c_int, [_vp, C.c_int64, C.c_int64, _vp]),
     "ss_copy_counters": (C.c_int, [_vp, _i64p, _i64p]),
@@ -818,6 +821,17 @@ class KVCache:
                                      q_ptr: int, out_ptr: int, stream: int = 0) -> None:
         self._check(self._lib.ss_paged_decode_attention_async(
             self._h, plan.handle, layer, num_q_heads, num_kv_heads, head_dim,
+            C.c_float(softmax_scale), C.c_void_p(q_ptr), C.c_void_p(out_ptr),
+            C.c_void_p(stream)))
+
+    def paged_prefill_attention_async(self, seq: int, q_range, layer: int, num_q_heads: int,
+                                      num_kv_heads: int, head_dim: int, softmax_scale: float,
+                                      q_ptr: int, out_ptr: int, stream: int = 0) -> None:
+        """Causal attention of positions [q_range) of `seq` over keys [0, q_end)
+        (tcgen05 kernel; q/out bf16 [n_q][num_q_heads][head_dim])."""
+        b, e = q_range
+        self._check(self._lib.ss_paged_prefill_attention_async(
+            self._h, seq, b, e, layer, num_q_heads, num_kv_heads, head_dim,
             C.c_float(softmax_scale), C.c_void_p(q_ptr), C.c_void_p(out_ptr),
             C.c_void_p(stream)))
 
