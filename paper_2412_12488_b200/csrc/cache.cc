@@ -1822,14 +1822,25 @@ void ss_cache::PrefillAttention(int64_t seq, int64_t q_begin, int64_t q_end, int
   MKV_CHECK(0 <= q_begin && q_begin < q_end && q_end <= rec->alloc_len, kInvalidArgument,
             "query range must be non-empty and allocated");
   MKV_CHECK(q_end <= INT32_MAX, kInvalidArgument, "context too long");
-  MKV_CHECK(hd == 128 && hkv >= 1 && hq == 8 * hkv, kInvalidArgument,
-            "prefill attention supports head_dim 128 with 8 query heads per kv head");
+  MKV_CHECK(prefill_attn_supported(P_, hq, hkv, hd), kInvalidArgument,
+            "prefill attention supports head_dim 128, 8 query heads per kv head and a page size "
+            "in {8, 16, 32, 64, 128}");
   MKV_CHECK(static_cast<int64_t>(W_) * 8 == 4LL * hkv * hd, kInvalidArgument,
             "entry width must equal K||V bf16 bytes (dim * 8 == 4 * num_kv_heads * head_dim)");
+  if (!tmaps_ready_) {
+    const int64_t rows = num_pages_ * P_;
+    auto* pm = reinterpret_cast<PoolTensorMap*>(tmap_page_);
+    auto* rm = reinterpret_cast<PoolTensorMap*>(tmap_row_);
+    if (!make_pool_tensor_map(d_pool_, L_, rows, W_, P_, pm) ||
+        !make_pool_tensor_map(d_pool_, L_, rows, W_, 1, rm))
+      mkv::ThrowStatus(SS_ERR_CUDA, "cuTensorMapEncodeTiled failed for the pool");
+    tmaps_ready_ = true;
+  }
   OrderAfterUser();
   if (s != stream_) OrderUser(s);
-  const bool ok = launch_prefill_attn(PoolLayer(layer), static_cast<int64_t>(W_) * 4, rec->d_slots,
-                                      q, static_cast<int>(q_begin),
+  const bool ok = launch_prefill_attn(*reinterpret_cast<const PoolTensorMap*>(tmap_page_),
+                                      *reinterpret_cast<const PoolTensorMap*>(tmap_row_), layer, P_,
+                                      rec->d_slots, q, static_cast<int>(q_begin),
                                       static_cast<int>(q_end - q_begin), hq, hkv, hd, scale, out, s);
   MKV_CHECK(ok, kInvalidArgument, "unsupported prefill attention shape");
   launches_ += 1;

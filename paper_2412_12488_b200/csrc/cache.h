@@ -398,4 +398,8 @@ struct ss_cache {
   uint32_t* d_status_ = nullptr;
   unsigned long long* d_scratch_ = nullptr;
   unsigned long long* h_pinned_ = nullptr;  // small pinned readback area
+  // TMA tensor maps of the pool for prefill attention (page box, row box),
+  // built on first use (mkv::PoolTensorMap layout).
+  alignas(64) unsigned char tmap_page_[128] = {}, tmap_row_[128] = {};
+  bool tmaps_ready_ = false;
 };

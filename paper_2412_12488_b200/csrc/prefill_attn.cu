@@ -3,52 +3,85 @@
 // The decode engine's tail prefill in balanced PD (SURVEY
 // §8(f) #2): queries at positions [q_begin, q_end) of a sequence attend to
 // keys [0, pos] read from the KV pool through the sequence's HBM page table.
-// Unlike decode, this is a dense contraction (e.g. 1,639 queries x 8,192
+// Unlike decode, this is a dense contraction (e.g. 1,638 queries x 8,192
 // keys x 64 heads at the 70B shape), so QK^T and PV run on the 5th-gen
-// tensor cores:
+// tensor cores.
 //
-//   CTA = (16 query tokens x the 8 query heads of one KV head) = M 128 rows.
-//   per 128-key tile:  S[128x128] = Q K^T      tcgen05.mma kind::f16, D in TMEM
-//                      softmax rows (thread = TMEM lane = row), P -> smem bf16
-//                      O[128x128] += P V       tcgen05.mma, V as MN-major B
-//   O stays in TMEM (columns 128..255) across tiles; rescaled in place when a
-//   row max grows; written once at the end.
+// CTA = one KV head x 32 query tokens, as two M=128 query tiles (16 tokens x
+// the 8 query heads sharing the KV head), warp-specialised:
 //
-// Shared memory operands use the UMMA SWIZZLE_128B canonical layout: 8-row
-// x 128-byte atoms whose 16-byte chunks are XORed with the row (bits 4-6 ^
-// bits 7-9 of the address), atoms 1024-byte aligned; a 128-element row spans
-// two atom columns.  K and V tiles are the same bytes ([key][d], d
-// contiguous): K is read as a K-major B operand, V as an MN-major one.
-// Tiles are gathered row by row (paged, 256 B per (key, kv head)) with
-// cp.async, double-buffered.
+//   warp 8      producer: per 128-key tile, one TMA box per (page, 64-dim
+//               half) of K and of V straight from the paged pool (a page's P
+//               rows of one head are a 2-D box of the pool's tensor map), into
+//               SWIZZLE_128B shared tiles; 2 stages each for K and V.
+//   warp 9      MMA issuer (one thread): S_i = Q_i K^T into TMEM, O_i += P_i V
+//               with P_i read from TMEM (A operand in tensor memory), in the
+//               order S0(j) PV1(j-1) S1(j) PV0(j) so each softmax warpgroup has
+//               two MMA slots of time while the tensor core stays busy.
+//   warps 0-3   softmax of query tile 0, thread = TMEM lane = row;
+//   warps 4-7   softmax of query tile 1.  Each reads its S row from TMEM,
+//               masks (causal), keeps a running max (O rescaled in TMEM only
+//               when the max grows by more than 2^8 — exact, since l and O
+//               share the stale max), writes P = exp2(.) as packed bf16 over
+//               the S columns, and signals the MMA warp.
+//
+// TMEM (512 columns): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512); P_i
+// aliases the first 64 columns of S_i.
+//
+// Shared-memory operands use the UMMA SWIZZLE_128B canonical layout (8-row x
+// 128-byte atoms, 16-byte chunks XOR row, 1024-byte aligned); a 128-element
+// row spans two atom columns.  K and V tiles are the same bytes ([key][d]): K
+// is read as a K-major B operand, V as an MN-major one.  Keys past the end
+// of the sequence in the last tile are zeroed in V (P is 0 there, but pool
+// words of other pages may hold any bit pattern, NaN included).
 //
 // Numerics: bf16 inputs, fp32 accumulation in TMEM, P rounded to bf16 for
 // the PV product; checked against fp32 PyTorch in
 // tests/test_prefill_attention_gpu.py.
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstring>
+
+#include "kernels.cuh"
 
 namespace mkv {
 
 namespace {
 
-constexpr int kRows = 128;     // M: 16 tokens x 8 heads
-constexpr int kTokens = 16;    // query tokens per CTA
-constexpr int kKeys = 128;     // N of S / K of PV per tile
+constexpr int kRows = 128;     // M of one query tile: 16 tokens x 8 heads
+constexpr int kTokens = 16;    // query tokens per query tile
+constexpr int kQTiles = 2;     // query tiles per CTA
+constexpr int kKeys = 128;     // keys per KV tile (N of S, K of PV)
 constexpr int kD = 128;        // head dim (K of S, N of PV)
-constexpr int kThreads = 128;  // 4 warps, thread = TMEM lane = row
 constexpr int kAtom = kRows * 128;  // one 64-element atom column of a 128-row tile (16 KiB)
 constexpr int kTile = 2 * kAtom;    // a [128][128] bf16 tile (32 KiB)
+constexpr int kStages = 2;
+constexpr int kSoftmaxThreads = 256;
+constexpr int kThreads = kSoftmaxThreads + 64;  // + producer warp + MMA warp
 
-// Shared memory map (bytes, 1024-aligned regions).
-constexpr int kOffQ = 0;
-constexpr int kOffK = kOffQ + kTile;       // 2 stages
-constexpr int kOffV = kOffK + 2 * kTile;   // 2 stages
-constexpr int kOffP = kOffV + 2 * kTile;
-constexpr int kOffBar = kOffP + kTile;     // mbarriers + tmem base
-constexpr int kSmem = kOffBar + 64;
+// Shared memory map (bytes; tiles 1024-aligned).
+constexpr int kOffQ = 0;                             // 2 query tiles
+constexpr int kOffK = kOffQ + kQTiles * kTile;       // kStages K tiles
+constexpr int kOffV = kOffK + kStages * kTile;       // kStages V tiles
+constexpr int kOffBar = kOffV + kStages * kTile;     // mbarriers + tmem base
+constexpr int kSmem = kOffBar + 256;
+
+// mbarrier slots (8 bytes each) from kOffBar.
+enum : int {
+  kBarQ = 0,                    // softmax threads loaded Q (count 256)
+  kBarKFull = 1,                // +stage: TMA bytes landed
+  kBarVFull = kBarKFull + kStages,
+  kBarKEmpty = kBarVFull + kStages,  // +stage: MMAs reading it retired
+  kBarVEmpty = kBarKEmpty + kStages,
+  kBarSFull = kBarVEmpty + kStages,  // +tile: S_i ready in TMEM
+  kBarPFull = kBarSFull + 2,         // +tile: P_i written, O_i rescaled (count 128)
+  kBarOFull = kBarPFull + 2,         // +tile: last PV_i retired
+  kBarCount = kBarOFull + 2,
+};
+static_assert(kBarCount * 8 + 8 <= 256, "barrier area");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -78,12 +111,22 @@ __host__ __device__ constexpr uint32_t idesc_bf16(bool b_mn_major) {
          ((kKeys >> 3) << 17) | ((kRows >> 4) << 24);
 }
 
+// D[tmem] (+)= A[smem] * B[smem]
 __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
                                          uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+// D[tmem] (+)= A[tmem] * B[smem]
+__device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
@@ -95,8 +138,18 @@ __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
 
-// Bounded wait: a tensor-core completion that never arrives traps (the
-// launch fails with an error) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+               "r"(bytes)
+               : "memory");
+}
+
+// Bounded wait: a completion that never arrives traps (the launch fails with
+// an error) instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
   uint32_t done = 0;
   const long long t0 = clock64();
@@ -123,7 +176,17 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// 16 consecutive fp32 columns of this thread's TMEM lane.
+// TMA: a {64 elements, rows, 1} box of the pool's 3-D tensor map.
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+
+// 16 consecutive fp32 columns of this thread's TMEM lane (waits).
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   uint32_t r[16];
   asm volatile(
@@ -138,18 +201,39 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+// 16 columns, no wait (the caller issues tmem_wait_ld once for a batch).
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_st16_nowait(uint32_t taddr, const uint32_t* r) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
       "%11, %12, %13, %14, %15, %16};" ::"r"(taddr),
-      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
-      "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
-      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
-      "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
-      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
-      "r"(__float_as_uint(v[15]))
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15])
       : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+  uint32_t r[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(v[i]);
+  tmem_st16_nowait(taddr, r);
+  tmem_wait_st();
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
@@ -157,219 +241,381 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_prefill_attn_tc(
-    const __nv_bfloat16* __restrict__ pool_l, int64_t row_elems, const int32_t* __restrict__ slots,
-    const __nv_bfloat16* __restrict__ q, int q_pos0, int n_q, int Hq, int Hkv,
-    float scale_log2, __nv_bfloat16* __restrict__ out) {
+struct PrefillArgs {
+  const int32_t* slots;       // sequence page table: slot of each position
+  const __nv_bfloat16* q;     // [n_q][Hq][128]
+  __nv_bfloat16* out;         // [n_q][Hq][128]
+  int layer, page_size, q_pos0, n_q, Hq, Hkv, n_blocks;
+  float scale_log2;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_prefill_attn_tc(const __grid_constant__ CUtensorMap pool_map,
+                      const __grid_constant__ CUtensorMap row_map, const PrefillArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // Operand atoms need 1024-byte alignment of the dynamic smem base.
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int qb = blockIdx.x, h = blockIdx.y;
-  const int G = Hq / Hkv;  // 8 (checked by the launcher)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // Heaviest (latest) query blocks first: causal work grows with position.
+  const int qb = a.n_blocks - 1 - static_cast<int>(blockIdx.x);
+  const int h = blockIdx.y;
   const uint32_t sQ = smem_u32(smem + kOffQ), sK = smem_u32(smem + kOffK);
-  const uint32_t sV = smem_u32(smem + kOffV), sP = smem_u32(smem + kOffP);
-  const uint32_t bar_s = smem_u32(smem + kOffBar), bar_o = bar_s + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + 16);
+  const uint32_t sV = smem_u32(smem + kOffV), bars = smem_u32(smem + kOffBar);
+  auto bar = [&](int i) { return bars + 8u * static_cast<uint32_t>(i); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + 8 * kBarCount);
 
-  // Row r of the tile = (token r / 8, head r % 8) of this query block.
-  const int r = tid;
-  const int tok = r / G, g = r % G;
-  const int qt = qb * kTokens + tok;          // query index within [0, n_q)
-  const bool row_valid = qt < n_q;
-  const int q_pos = q_pos0 + qt;              // absolute position (causal bound)
-  const int last_pos = q_pos0 + min(n_q, (qb + 1) * kTokens) - 1;
-  const int n_keys = last_pos + 1;            // keys [0, n_keys) needed by this block
+  const int tok_first = qb * kQTiles * kTokens;
+  const int tok_last = min(a.n_q, tok_first + kQTiles * kTokens) - 1;
+  const int n_keys = a.q_pos0 + tok_last + 1;  // keys [0, n_keys) needed by this CTA
   const int n_tiles = (n_keys + kKeys - 1) / kKeys;
 
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+  if (warp == 9) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                      smem_u32(tmem_slot))
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  if (tid == 0) {
-    mbar_init(bar_s, 1);
-    mbar_init(bar_o, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  // Q tile (zero rows past n_q).
-  {
-    const __nv_bfloat16* qrow =
-        q + (static_cast<int64_t>(qt) * Hq + static_cast<int64_t>(h) * G + g) * kD;
-#pragma unroll
-    for (int c = 0; c < 16; ++c) cp_async16(sQ + sw128(r, c), qrow + c * 8, row_valid);
-  }
-  auto load_kv = [&](int tile, int stage) {
-    const uint32_t kb = sK + stage * kTile, vb = sV + stage * kTile;
-    const int64_t k_off = static_cast<int64_t>(h) * kD, v_off = static_cast<int64_t>(Hkv + h) * kD;
-    // 128 keys x 16 chunks per operand over 128 threads.
-#pragma unroll 4
-    for (int i = tid; i < kKeys * 16; i += kThreads) {
-      const int kk = i >> 4, c = i & 15;
-      const int pos = tile * kKeys + kk;
-      const bool valid = pos < n_keys;
-      const int64_t slot = valid ? static_cast<int64_t>(__ldg(slots + pos)) : 0;
-      const __nv_bfloat16* row = pool_l + slot * row_elems;
-      cp_async16(kb + sw128(kk, c), row + k_off + c * 8, valid);
-      cp_async16(vb + sw128(kk, c), row + v_off + c * 8, valid);
+  if (tid == kSoftmaxThreads) {
+    mbar_init(bar(kBarQ), kSoftmaxThreads);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(bar(kBarKFull + s), 1);
+      mbar_init(bar(kBarVFull + s), 1);
+      mbar_init(bar(kBarKEmpty + s), 1);
+      mbar_init(bar(kBarVEmpty + s), 1);
     }
-  };
-  load_kv(0, 0);
-  asm volatile("cp.async.commit_group;" ::: "memory");
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(kBarSFull + i), 1);
+      mbar_init(bar(kBarPFull + i), kRows);
+      mbar_init(bar(kBarOFull + i), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&pool_map))
+                 : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&row_map))
+                 : "memory");
+  }
   fence_before();
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS = tmem, tO = tmem + 128;
-  const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;  // this warp's TMEM lanes
 
-  float m = -INFINITY, l = 0.f;
-  uint32_t ph_s = 0, ph_o = 0;
-  constexpr uint32_t kIdescS = idesc_bf16(false), kIdescO = idesc_bf16(true);
-  for (int j = 0; j < n_tiles; ++j) {
-    const int stage = j & 1;
-    // PV(j-1) read stage (j+1)&1's V and the P buffer: wait before reusing them.
-    if (j > 0) {
-      mbar_wait(bar_o, ph_o);
-      ph_o ^= 1;
+  if (warp == 8) {
+    // ---------------- producer: paged K/V tiles by TMA ----------------
+    // Lane l owns tile positions 4l..4l+3; a chunk of P positions (one page
+    // when the sequence is page-aligned) whose slots are consecutive rows is
+    // one P-row box; otherwise (a fork at a non-page-aligned length) its
+    // rows are loaded one by one.  Positions >= n_keys are don't-care.
+    const int P = a.page_size, lanes_per_chunk = P / 4;
+    const uint32_t chunk_mask = lanes_per_chunk >= 32 ? 0xffffffffu : ((1u << lanes_per_chunk) - 1u);
+    const int my_chunk_lane0 = lane - lane % lanes_per_chunk;
+    const int ck = h * kD, cv = (a.Hkv + h) * kD;  // element column of K / V of this head
+    for (int j = 0; j < n_tiles; ++j) {
+      const int s = j & 1;
+      const int p0 = j * kKeys + lane * 4;
+      int sl[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) sl[t] = p0 + t < n_keys ? __ldg(a.slots + p0 + t) : -1;
+      const int prev_last = __shfl_up_sync(0xffffffffu, sl[3], 1);
+      bool ok = true;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const bool chunk_start = ((lane * 4 + t) % P) == 0;
+        const int prev = t > 0 ? sl[t - 1] : prev_last;
+        if (!chunk_start && sl[t] >= 0) ok = ok && sl[t] == prev + 1;
+      }
+      const uint32_t ballot = __ballot_sync(0xffffffffu, ok);
+      const bool contiguous = ((ballot >> my_chunk_lane0) & chunk_mask) == chunk_mask;
+      const int chunk_row = __shfl_sync(0xffffffffu, sl[0], my_chunk_lane0);
+      for (int op = 0; op < 2; ++op) {  // K then V
+        const uint32_t base = (op == 0 ? sK : sV) + s * kTile;
+        const uint32_t full = bar((op == 0 ? kBarKFull : kBarVFull) + s);
+        const int col = op == 0 ? ck : cv;
+        if (lane == 0) {
+          if (j >= kStages) mbar_wait(bar((op == 0 ? kBarKEmpty : kBarVEmpty) + s), ((j >> 1) + 1) & 1);
+          mbar_expect_tx(full, kTile);
+        }
+        __syncwarp();
+        if (contiguous) {
+          if (lane == my_chunk_lane0) {
+            const uint32_t dst = base + (lane * 4) * 128;
+            const int row = chunk_row >= 0 ? chunk_row : 0;
+            tma_load_3d(dst, &pool_map, col, row, a.layer, full);
+            tma_load_3d(dst + kAtom, &pool_map, col + 64, row, a.layer, full);
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const uint32_t dst = base + (lane * 4 + t) * 128;
+            const int row = sl[t] >= 0 ? sl[t] : 0;
+            tma_load_3d(dst, &row_map, col, row, a.layer, full);
+            tma_load_3d(dst + kAtom, &row_map, col + 64, row, a.layer, full);
+          }
+        }
+      }
     }
-    if (j + 1 < n_tiles) load_kv(j + 1, stage ^ 1);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
-    fence_proxy_async();  // cp.async bytes -> visible to the tensor core (async proxy)
-    fence_before();
-    __syncthreads();
-    fence_after();
-    if (tid == 0) {
-      const uint32_t kb = sK + stage * kTile;
+  } else if (warp == 9) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t kIdescS = idesc_bf16(false), kIdescO = idesc_bf16(true);
+    const uint32_t tS[2] = {tmem, tmem + 128}, tO[2] = {tmem + 256, tmem + 384};
+    auto issue_s = [&](int i, int j) {
+      const uint32_t kb = sK + (j & 1) * kTile, qa = sQ + i * kTile;
 #pragma unroll
       for (int k = 0; k < kD / 16; ++k) {
         const uint32_t off = (k >> 2) * kAtom + (k & 3) * 32;
-        mma_bf16(tS, umma_desc(sQ + off, 16, 1024), umma_desc(kb + off, 16, 1024), kIdescS,
+        mma_bf16(tS[i], umma_desc(qa + off, 16, 1024), umma_desc(kb + off, 16, 1024), kIdescS,
                  k > 0 ? 1u : 0u);
       }
-      mma_commit(bar_s);
-    }
-    mbar_wait(bar_s, ph_s);
-    ph_s ^= 1;
-    fence_after();
-    // Row softmax over this tile's 128 keys (two passes over TMEM columns).
-    const int key0 = j * kKeys;
-    float tmax = -INFINITY;
-#pragma unroll
-    for (int c0 = 0; c0 < kKeys; c0 += 16) {
-      float v[16];
-      tmem_ld16(tS + lane_off + c0, v);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const bool ok = row_valid && key0 + c0 + i <= q_pos;
-        tmax = fmaxf(tmax, ok ? v[i] * scale_log2 : -INFINITY);
-      }
-    }
-    const float m_new = fmaxf(m, tmax);
-    const float alpha = m_new == -INFINITY ? 1.f : exp2f(m - m_new);
-    float psum = 0.f;
-#pragma unroll
-    for (int c0 = 0; c0 < kKeys; c0 += 16) {
-      float v[16];
-      tmem_ld16(tS + lane_off + c0, v);
-      uint32_t pk[8];
-#pragma unroll
-      for (int i = 0; i < 16; i += 2) {
-        const bool ok0 = row_valid && key0 + c0 + i <= q_pos;
-        const bool ok1 = row_valid && key0 + c0 + i + 1 <= q_pos;
-        const float p0 = ok0 ? exp2f(v[i] * scale_log2 - m_new) : 0.f;
-        const float p1 = ok1 ? exp2f(v[i + 1] * scale_log2 - m_new) : 0.f;
-        psum += p0 + p1;
-        pk[i / 2] = pack_bf16(p0, p1);
-      }
-      // P row r, keys c0..c0+15 = chunks c0/8 and c0/8+1 of the SW128 tile.
-      const int c = c0 >> 3;
-      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sP + sw128(r, c)), "r"(pk[0]),
-                   "r"(pk[1]), "r"(pk[2]), "r"(pk[3])
-                   : "memory");
-      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sP + sw128(r, c + 1)),
-                   "r"(pk[4]), "r"(pk[5]), "r"(pk[6]), "r"(pk[7])
-                   : "memory");
-    }
-    l = l * alpha + psum;
-    m = m_new;
-    // Rescale the running O rows in TMEM when this tile raised a max.  The
-    // TMEM load/store are warp-collective, so the decision is per warp.
-    if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-#pragma unroll
-      for (int c0 = 0; c0 < kD; c0 += 16) {
-        float v[16];
-        tmem_ld16(tO + lane_off + c0, v);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] *= alpha;
-        tmem_st16(tO + lane_off + c0, v);
-      }
-    }
-    fence_proxy_async();  // P stores -> async proxy
-    fence_before();
-    __syncthreads();
-    fence_after();
-    if (tid == 0) {
-      const uint32_t vb = sV + stage * kTile;
+      mma_commit(bar(kBarSFull + i));
+    };
+    auto issue_pv = [&](int i, int j) {
+      const uint32_t vb = sV + (j & 1) * kTile;
 #pragma unroll
       for (int k = 0; k < kKeys / 16; ++k) {
-        // A = P [128 rows x 128 keys] K-major; B = V [128 keys x 128 d] MN-major:
-        // 16 keys per step = two 8-key atoms (SBO 1024 B apart); the two
-        // 64-d halves are LBO = one atom column (16 KiB) apart.
-        const uint32_t a_off = (k >> 2) * kAtom + (k & 3) * 32;
-        mma_bf16(tO, umma_desc(sP + a_off, 16, 1024), umma_desc(vb + k * 2048, kAtom, 1024),
-                 kIdescO, (j > 0 || k > 0) ? 1u : 0u);
+        // A = P_i in TMEM (bf16 pairs: 8 columns per 16 keys); B = V MN-major:
+        // 16 keys = two 8-key atoms (SBO 1024 B), d halves LBO = 16 KiB apart.
+        mma_bf16_ts(tO[i], tS[i] + k * 8, umma_desc(vb + k * 2048, kAtom, 1024), kIdescO,
+                    (j > 0 || k > 0) ? 1u : 0u);
       }
-      mma_commit(bar_o);
+    };
+    // Keys past n_keys in the last tile: zero their V rows (both halves).
+    auto zero_tail = [&](int j) {
+      const int valid = n_keys - j * kKeys;
+      if (valid >= kKeys) return;
+      uint8_t* vb = smem + kOffV + (j & 1) * kTile;
+      for (int i = lane; i < (kKeys - valid) * 16; i += 32) {
+        const int r = valid + (i >> 4), c = i & 15;
+        *reinterpret_cast<uint4*>(vb + (c >> 3) * kAtom + r * 128 + (c & 7) * 16) =
+            make_uint4(0, 0, 0, 0);
+      }
+      fence_proxy_async();
+      __syncwarp();
+    };
+    mbar_wait(bar(kBarQ), 0);
+    for (int j = 0; j < n_tiles; ++j) {
+      const int s = j & 1;
+      mbar_wait(bar(kBarKFull + s), (j >> 1) & 1);
+      fence_after();
+      if (lane == 0) issue_s(0, j);
+      if (j > 0) {
+        // PV1(j-1): V stage of tile j-1, P1 of tile j-1.
+        mbar_wait(bar(kBarPFull + 1), (j - 1) & 1);
+        fence_after();
+        if (lane == 0) {
+          issue_pv(1, j - 1);
+          mma_commit(bar(kBarVEmpty + ((j - 1) & 1)));
+        }
+      }
+      if (lane == 0) {
+        issue_s(1, j);
+        mma_commit(bar(kBarKEmpty + s));
+      }
+      mbar_wait(bar(kBarVFull + s), (j >> 1) & 1);
+      if (j == n_tiles - 1) zero_tail(j);
+      mbar_wait(bar(kBarPFull + 0), j & 1);
+      fence_after();
+      if (lane == 0) issue_pv(0, j);
+      __syncwarp();
     }
-  }
-  mbar_wait(bar_o, ph_o);
-  fence_after();
-  // O row / l -> bf16 -> out[token][head][d].
-  {
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    __nv_bfloat16* orow = out + (static_cast<int64_t>(qt) * Hq + static_cast<int64_t>(h) * G + g) * kD;
+    const int jl = n_tiles - 1;
+    if (lane == 0) mma_commit(bar(kBarOFull + 0));
+    mbar_wait(bar(kBarPFull + 1), jl & 1);
+    fence_after();
+    if (lane == 0) {
+      issue_pv(1, jl);
+      mma_commit(bar(kBarVEmpty + (jl & 1)));
+      mma_commit(bar(kBarOFull + 1));
+    }
+    __syncwarp();
+  } else {
+    // ---------------- softmax warpgroups ----------------
+    const int i = warp >> 2;              // query tile
+    const int r = tid & (kRows - 1);      // row = TMEM lane
+    const int G = a.Hq / a.Hkv;           // 8
+    const int tok = tok_first + i * kTokens + r / G, g = r % G;
+    const bool row_valid = tok < a.n_q;
+    const int q_pos = a.q_pos0 + tok;
+    const int tile_min_pos = a.q_pos0 + tok_first + i * kTokens;  // smallest position of tile i
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + i * 128 + lane_off, tO = tmem + 256 + i * 128 + lane_off;
+    {
+      const __nv_bfloat16* qrow =
+          a.q + (static_cast<int64_t>(tok) * a.Hq + static_cast<int64_t>(h) * G + g) * kD;
+      const uint32_t qa = sQ + i * kTile;
 #pragma unroll
-    for (int c0 = 0; c0 < kD; c0 += 16) {
-      float v[16];
-      tmem_ld16(tO + lane_off + c0, v);  // warp-collective: every lane loads
-      if (!row_valid) continue;
-      uint4 w0, w1;
-      w0.x = pack_bf16(v[0] * inv, v[1] * inv);
-      w0.y = pack_bf16(v[2] * inv, v[3] * inv);
-      w0.z = pack_bf16(v[4] * inv, v[5] * inv);
-      w0.w = pack_bf16(v[6] * inv, v[7] * inv);
-      w1.x = pack_bf16(v[8] * inv, v[9] * inv);
-      w1.y = pack_bf16(v[10] * inv, v[11] * inv);
-      w1.z = pack_bf16(v[12] * inv, v[13] * inv);
-      w1.w = pack_bf16(v[14] * inv, v[15] * inv);
-      *reinterpret_cast<uint4*>(orow + c0) = w0;
-      *reinterpret_cast<uint4*>(orow + c0 + 8) = w1;
+      for (int c = 0; c < 16; ++c) cp_async16(qa + sw128(r, c), qrow + c * 8, row_valid);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      fence_proxy_async();
+      mbar_arrive(bar(kBarQ));
+    }
+    const float sl2 = a.scale_log2;
+    float m = -INFINITY, l = 0.f;  // running max (scaled log2 domain) and sum
+    for (int j = 0; j < n_tiles; ++j) {
+      mbar_wait(bar(kBarSFull + i), j & 1);
+      fence_after();
+      uint32_t sr[kKeys];
+#pragma unroll
+      for (int c0 = 0; c0 < kKeys; c0 += 16) tmem_ld16_nowait(tS + c0, sr + c0);
+      tmem_wait_ld();
+      const int key0 = j * kKeys;
+      // Causal mask only where this tile crosses the diagonal of query tile i.
+      const bool need_mask = key0 + kKeys - 1 > tile_min_pos || !row_valid;
+      float tmax = -INFINITY;
+      if (need_mask) {
+#pragma unroll
+        for (int c = 0; c < kKeys; ++c) {
+          const bool ok = row_valid && key0 + c <= q_pos;
+          const float x = ok ? __uint_as_float(sr[c]) * sl2 : -INFINITY;
+          sr[c] = __float_as_uint(x);
+          tmax = fmaxf(tmax, x);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < kKeys; ++c) {
+          const float x = __uint_as_float(sr[c]) * sl2;
+          sr[c] = __float_as_uint(x);
+          tmax = fmaxf(tmax, x);
+        }
+      }
+      // Keep the stale max unless this tile exceeds it by > 8 (p <= 2^8 then).
+      const bool bump = tmax > m + 8.f;
+      const float m_new = bump ? tmax : m;
+      const float alpha = (bump && m != -INFINITY) ? exp2f(m - m_new) : 1.f;
+      const float mref = m_new == -INFINITY ? 0.f : m_new;
+      float psum = 0.f;
+      uint32_t pk[kKeys / 2];
+#pragma unroll
+      for (int c = 0; c < kKeys; c += 2) {
+        const float p0 = exp2f(__uint_as_float(sr[c]) - mref);
+        const float p1 = exp2f(__uint_as_float(sr[c + 1]) - mref);
+        psum += p0 + p1;
+        pk[c / 2] = pack_bf16(p0, p1);
+      }
+      // P_i over the first 64 columns of S_i.
+#pragma unroll
+      for (int c0 = 0; c0 < kKeys / 2; c0 += 16) tmem_st16_nowait(tS + c0, pk + c0);
+      l = l * alpha + psum;
+      m = m_new;
+      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+        for (int c0 = 0; c0 < kD; c0 += 32) {
+          uint32_t o[32];
+          tmem_ld16_nowait(tO + c0, o);
+          tmem_ld16_nowait(tO + c0 + 16, o + 16);
+          tmem_wait_ld();
+#pragma unroll
+          for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
+          tmem_st16_nowait(tO + c0, o);
+          tmem_st16_nowait(tO + c0 + 16, o + 16);
+        }
+      }
+      tmem_wait_st();
+      fence_before();
+      mbar_arrive(bar(kBarPFull + i));
+    }
+    mbar_wait(bar(kBarOFull + i), 0);
+    fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    __nv_bfloat16* orow =
+        a.out + (static_cast<int64_t>(tok) * a.Hq + static_cast<int64_t>(h) * G + g) * kD;
+#pragma unroll
+    for (int c0 = 0; c0 < kD; c0 += 32) {
+      uint32_t o[32];
+      tmem_ld16_nowait(tO + c0, o);
+      tmem_ld16_nowait(tO + c0 + 16, o + 16);
+      tmem_wait_ld();
+      if (row_valid) {
+        uint4 w[4];
+        uint32_t* wp = reinterpret_cast<uint32_t*>(w);
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          wp[k] = pack_bf16(__uint_as_float(o[2 * k]) * inv, __uint_as_float(o[2 * k + 1]) * inv);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) reinterpret_cast<uint4*>(orow + c0)[k] = w[k];
+      }
     }
   }
   fence_before();
   __syncthreads();
-  if (warp == 0) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+  if (warp == 9) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeTiledFn>(nullptr);
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
 }
 
 }  // namespace
 
-bool launch_prefill_attn(const void* pool_l, int64_t row_elems, const int32_t* slots,
+bool make_pool_tensor_map(void* pool, int64_t layers, int64_t rows, int64_t row_u64,
+                          int box_rows, PoolTensorMap* out) {
+  static_assert(sizeof(CUtensorMap) <= sizeof(out->bytes), "tensor map size");
+  EncodeTiledFn fn = encode_fn();
+  if (fn == nullptr) return false;
+  CUtensorMap map;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(row_u64 * 4), static_cast<cuuint64_t>(rows),
+                              static_cast<cuuint64_t>(layers)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(row_u64 * 8),
+                                 static_cast<cuuint64_t>(rows * row_u64 * 8)};
+  const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, pool, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  std::memcpy(out->bytes, &map, sizeof(map));
+  return true;
+}
+
+bool prefill_attn_supported(int page_size, int Hq, int Hkv, int D) {
+  return D == kD && Hkv >= 1 && Hq == 8 * Hkv && page_size >= 8 && page_size <= kKeys &&
+         kKeys % page_size == 0;
+}
+
+bool launch_prefill_attn(const PoolTensorMap& page_map, const PoolTensorMap& row_map, int layer,
+                         int page_size, const int32_t* slots,
                          const void* q, int q_pos0, int n_q, int Hq, int Hkv, int D, float scale,
                          void* out, cudaStream_t s) {
-  if (D != kD || Hkv <= 0 || Hq != Hkv * 8 || n_q <= 0) return false;
+  if (!prefill_attn_supported(page_size, Hq, Hkv, D) || n_q <= 0) return false;
   const int smem = kSmem + 1024;  // + alignment slack
-  cudaFuncSetAttribute(k_prefill_attn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  const dim3 grid((n_q + kTokens - 1) / kTokens, Hkv);
-  k_prefill_attn_tc<<<grid, kThreads, smem, s>>>(
-      static_cast<const __nv_bfloat16*>(pool_l), row_elems, slots,
-      static_cast<const __nv_bfloat16*>(q), q_pos0, n_q, Hq, Hkv, scale * 1.4426950408889634f,
-      static_cast<__nv_bfloat16*>(out));
+  static bool attr = [] {
+    return cudaFuncSetAttribute(k_prefill_attn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kSmem + 1024) == cudaSuccess;
+  }();
+  if (!attr) return false;
+  PrefillArgs a;
+  a.slots = slots;
+  a.q = static_cast<const __nv_bfloat16*>(q);
+  a.out = static_cast<__nv_bfloat16*>(out);
+  a.layer = layer;
+  a.page_size = page_size;
+  a.q_pos0 = q_pos0;
+  a.n_q = n_q;
+  a.Hq = Hq;
+  a.Hkv = Hkv;
+  a.n_blocks = (n_q + kQTiles * kTokens - 1) / (kQTiles * kTokens);
+  a.scale_log2 = scale * 1.4426950408889634f;
+  CUtensorMap m, mr;
+  std::memcpy(&m, page_map.bytes, sizeof(m));
+  std::memcpy(&mr, row_map.bytes, sizeof(mr));
+  const dim3 grid(a.n_blocks, Hkv);
+  k_prefill_attn_tc<<<grid, kThreads, smem, s>>>(m, mr, a);
   return true;
 }
 

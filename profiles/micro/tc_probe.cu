@@ -194,7 +194,14 @@ int main(int argc, char** argv) {
     CK(cudaMemset(dO, 0xFF, 2 * q.size()));
     printf("launching prefill n=%d qb=%d\n", n, qb);
     fflush(stdout);
-    const bool ok = launch_prefill_attn(dP, row, dS, dQ, qb, nq, Hq, Hkv, 128, 0.0883883f, dO, 0);
+    PoolTensorMap pm, rm;
+    const int64_t rows = n;
+    if (!make_pool_tensor_map(dP, 1, rows, row / 4, 16, &pm) ||
+        !make_pool_tensor_map(dP, 1, rows, row / 4, 1, &rm)) {
+      printf("tensor map encode failed\n");
+      return 1;
+    }
+    const bool ok = launch_prefill_attn(pm, rm, 0, 16, dS, dQ, qb, nq, Hq, Hkv, 128, 0.0883883f, dO, 0);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     printf("prefill ok=%d done\n", ok);
