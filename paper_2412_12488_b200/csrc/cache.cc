@@ -1823,15 +1823,15 @@ void ss_cache::PrefillAttention(int64_t seq, int64_t q_begin, int64_t q_end, int
             "query range must be non-empty and allocated");
   MKV_CHECK(q_end <= INT32_MAX, kInvalidArgument, "context too long");
   MKV_CHECK(prefill_attn_supported(P_, hq, hkv, hd), kInvalidArgument,
-            "prefill attention supports head_dim 128, 8 query heads per kv head and a page size "
-            "in {8, 16, 32, 64, 128}");
+            "prefill attention supports head_dim 128, 8 query heads per kv head and a "
+            "power-of-two page size >= 8");
   MKV_CHECK(static_cast<int64_t>(W_) * 8 == 4LL * hkv * hd, kInvalidArgument,
             "entry width must equal K||V bf16 bytes (dim * 8 == 4 * num_kv_heads * head_dim)");
   if (!tmaps_ready_) {
     const int64_t rows = num_pages_ * P_;
     auto* pm = reinterpret_cast<PoolTensorMap*>(tmap_page_);
     auto* rm = reinterpret_cast<PoolTensorMap*>(tmap_row_);
-    if (!make_pool_tensor_map(d_pool_, L_, rows, W_, P_, pm) ||
+    if (!make_pool_tensor_map(d_pool_, L_, rows, W_, prefill_attn_box_rows(P_), pm) ||
         !make_pool_tensor_map(d_pool_, L_, rows, W_, 1, rm))
       mkv::ThrowStatus(SS_ERR_CUDA, "cuTensorMapEncodeTiled failed for the pool");
     tmaps_ready_ = true;

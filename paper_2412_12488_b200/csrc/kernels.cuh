@@ -162,7 +162,7 @@ bool launch_decode_attn(const void* pool_l, int64_t row_elems, const int32_t* sl
 // Paged causal GQA prefill attention on tcgen05 (prefill_attn.cu): queries
 // [q_pos0, q_pos0 + n_q) of one sequence over keys [0, q_pos0 + n_q).  K/V
 // come by TMA through two tensor maps of the whole pool viewed as bf16
-// [layers][rows][row_u64 * 4]: boxes of {64, page_size, 1} (one page chunk)
+// [layers][rows][row_u64 * 4]: boxes of {64, prefill_attn_box_rows(P), 1} (a page chunk)
 // and {64, 1, 1} (one row, for chunks whose slots are not consecutive).
 struct alignas(64) PoolTensorMap {
   unsigned char bytes[128];
@@ -170,6 +170,7 @@ struct alignas(64) PoolTensorMap {
 bool make_pool_tensor_map(void* pool, int64_t layers, int64_t rows, int64_t row_u64,
                           int box_rows, PoolTensorMap* out);
 bool prefill_attn_supported(int page_size, int Hq, int Hkv, int D);
+int prefill_attn_box_rows(int page_size);  // rows of the page-chunk box
 bool launch_prefill_attn(const PoolTensorMap& page_map, const PoolTensorMap& row_map, int layer,
                          int page_size, const int32_t* slots, const void* q, int q_pos0, int n_q,
                          int Hq, int Hkv, int D, float scale, void* out, cudaStream_t s);

@@ -44,6 +44,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <type_traits>
 
 #include "kernels.cuh"
 
@@ -54,32 +55,34 @@ namespace {
 constexpr int kRows = 128;     // M of one query tile: 16 tokens x 8 heads
 constexpr int kTokens = 16;    // query tokens per query tile
 constexpr int kQTiles = 2;     // query tiles per CTA
-constexpr int kKeys = 128;     // keys per KV tile (N of S, K of PV)
+constexpr int kKeys = 64;      // keys per KV tile (N of S, K of PV)
 constexpr int kD = 128;        // head dim (K of S, N of PV)
-constexpr int kAtom = kRows * 128;  // one 64-element atom column of a 128-row tile (16 KiB)
-constexpr int kTile = 2 * kAtom;    // a [128][128] bf16 tile (32 KiB)
-constexpr int kStages = 2;
+constexpr int kAtom = kRows * 128;   // one 64-element atom column of a 128-row tile (16 KiB)
+constexpr int kTile = 2 * kAtom;     // a [128][128] bf16 query tile (32 KiB)
+constexpr int kKvAtom = kKeys * 128; // atom column of a [64][128] K or V tile (8 KiB)
+constexpr int kKvTile = 2 * kKvAtom; // 16 KiB
+constexpr int kStages = 4;           // K and V ring depth
 constexpr int kSoftmaxThreads = 256;
 constexpr int kThreads = kSoftmaxThreads + 64;  // + producer warp + MMA warp
 
 // Shared memory map (bytes; tiles 1024-aligned).
 constexpr int kOffQ = 0;                             // 2 query tiles
 constexpr int kOffK = kOffQ + kQTiles * kTile;       // kStages K tiles
-constexpr int kOffV = kOffK + kStages * kTile;       // kStages V tiles
-constexpr int kOffBar = kOffV + kStages * kTile;     // mbarriers + tmem base
+constexpr int kOffV = kOffK + kStages * kKvTile;     // kStages V tiles
+constexpr int kOffBar = kOffV + kStages * kKvTile;   // mbarriers + tmem base
 constexpr int kSmem = kOffBar + 256;
 
 // mbarrier slots (8 bytes each) from kOffBar.
 enum : int {
-  kBarQ = 0,                    // softmax threads loaded Q (count 256)
-  kBarKFull = 1,                // +stage: TMA bytes landed
+  kBarQ = 0,                         // softmax threads loaded Q (count 256)
+  kBarKFull = 1,                     // +stage: TMA bytes landed
   kBarVFull = kBarKFull + kStages,
   kBarKEmpty = kBarVFull + kStages,  // +stage: MMAs reading it retired
   kBarVEmpty = kBarKEmpty + kStages,
-  kBarSFull = kBarVEmpty + kStages,  // +tile: S_i ready in TMEM
-  kBarPFull = kBarSFull + 2,         // +tile: P_i written, O_i rescaled (count 128)
-  kBarOFull = kBarPFull + 2,         // +tile: last PV_i retired
-  kBarCount = kBarOFull + 2,
+  kBarSFull = kBarVEmpty + kStages,  // +tile: S_i(j) ready in TMEM
+  kBarPFull = kBarSFull + 2,         // +tile: P_i(j) written, O_i rescaled (count 128)
+  kBarPVDone = kBarPFull + 2,        // +tile: PV_i(j) retired (O_i stable)
+  kBarCount = kBarPVDone + 2,
 };
 static_assert(kBarCount * 8 + 8 <= 256, "barrier area");
 
@@ -105,10 +108,10 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint3
          (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (2ull << 61);
 }
 
-// Instruction descriptor: D f32, A/B bf16, M=128, N=128, A K-major, B K- or MN-major.
-__host__ __device__ constexpr uint32_t idesc_bf16(bool b_mn_major) {
+// Instruction descriptor: D f32, A/B bf16, M=128, N=n, A K-major, B K- or MN-major.
+__host__ __device__ constexpr uint32_t idesc_bf16(bool b_mn_major, int n = 128) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn_major ? 1u : 0u) << 16) |
-         ((kKeys >> 3) << 17) | ((kRows >> 4) << 24);
+         ((static_cast<uint32_t>(n) >> 3) << 17) | ((kRows >> 4) << 24);
 }
 
 // D[tmem] (+)= A[smem] * B[smem]
@@ -127,6 +130,43 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, ui
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
       "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+// Warp-converged issue: one elected lane issues; descriptors are passed as
+// (lo, hi) halves so a uniform base plus compile-time offsets stays in
+// uniform registers (no per-instruction R2UR broadcast loop).
+__device__ __forceinline__ void mma_ss_elect(uint32_t tmem_d, uint32_t a_lo, uint32_t b_lo,
+                                             uint32_t hi, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 da, db;\n\t"
+      "mov.b64 da, {%1, %3};\n\tmov.b64 db, {%2, %3};\n\t"
+      "setp.ne.b32 p, %5, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %4, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(a_lo), "r"(b_lo), "r"(hi), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_ts_elect(uint32_t tmem_d, uint32_t tmem_a, uint32_t b_lo,
+                                             uint32_t b_hi, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 db;\n\t"
+      "mov.b64 db, {%2, %3};\n\t"
+      "setp.ne.b32 p, %5, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], db, %4, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void commit_elect(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
+          bar)
+      : "memory");
+}
+
+// Low / high 32 bits of a SWIZZLE_128B descriptor (see umma_desc).
+__host__ __device__ constexpr uint32_t desc_lo(uint32_t addr, uint32_t lbo) {
+  return ((addr >> 4) & 0x3FFFu) | (((lbo >> 4) & 0x3FFFu) << 16);
+}
+__host__ __device__ constexpr uint32_t desc_hi(uint32_t sbo) {
+  return ((sbo >> 4) & 0x3FFFu) | (1u << 14) | (2u << 29);
 }
 
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
@@ -236,6 +276,28 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) 
   tmem_wait_st();
 }
 
+// 2^x on the MUFU unit (ftz: no denormal fix-up instructions).
+__device__ __forceinline__ float ex2_mufu(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// 2^x on the FMA pipe: round-to-nearest split x = j + f, f in [-0.5, 0.5],
+// 2^f by its degree-3 Taylor polynomial (relative error < 7e-4, below
+// bf16's 2^-9 rounding of P), 2^j added to the exponent.  x is clamped at
+// -125 (2^-125 ~ 0 next to the row maximum's 1); callers use it only for
+// unmasked scores (x <= 8).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -125.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23: low mantissa bits = round(x)
+  const float f = x - (t - 12582912.f);
+  float p = fmaf(f, 0.0555041087f, 0.240226507f);
+  p = fmaf(p, f, 0.693147181f);
+  p = fmaf(p, f, 1.f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -286,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar(kBarSFull + i), 1);
       mbar_init(bar(kBarPFull + i), kRows);
-      mbar_init(bar(kBarOFull + i), 1);
+      mbar_init(bar(kBarPVDone + i), 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&pool_map))
@@ -297,29 +359,33 @@ __global__ void __launch_bounds__(kThreads, 1)
   fence_before();
   __syncthreads();
   fence_after();
-  const uint32_t tmem = *tmem_slot;
+  // The CTA owns all 512 columns, so the allocation starts at lane 0,
+  // column 0: a compile-time constant keeps TMEM addresses uniform.
+  constexpr uint32_t tmem = 0;
+  if (tid == 0 && *tmem_slot != 0u) __trap();
 
   if (warp == 8) {
     // ---------------- producer: paged K/V tiles by TMA ----------------
-    // Lane l owns tile positions 4l..4l+3; a chunk of P positions (one page
-    // when the sequence is page-aligned) whose slots are consecutive rows is
-    // one P-row box; otherwise (a fork at a non-page-aligned length) its
-    // rows are loaded one by one.  Positions >= n_keys are don't-care.
-    const int P = a.page_size, lanes_per_chunk = P / 4;
+    // Lane l owns tile positions 2l, 2l+1.  A chunk of C = min(P, 64)
+    // positions whose slots are consecutive rows (a page, when the sequence
+    // is page-aligned) is one C-row box; otherwise (a fork at a
+    // non-page-aligned length) its rows are loaded one by one.  Positions
+    // >= n_keys are don't-care (masked; V zeroed by the MMA warp).
+    const int C = min(a.page_size, kKeys), lanes_per_chunk = C / 2;
     const uint32_t chunk_mask = lanes_per_chunk >= 32 ? 0xffffffffu : ((1u << lanes_per_chunk) - 1u);
     const int my_chunk_lane0 = lane - lane % lanes_per_chunk;
     const int ck = h * kD, cv = (a.Hkv + h) * kD;  // element column of K / V of this head
     for (int j = 0; j < n_tiles; ++j) {
-      const int s = j & 1;
-      const int p0 = j * kKeys + lane * 4;
-      int sl[4];
+      const int s = j % kStages;
+      const int p0 = j * kKeys + lane * 2;
+      int sl[2];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) sl[t] = p0 + t < n_keys ? __ldg(a.slots + p0 + t) : -1;
-      const int prev_last = __shfl_up_sync(0xffffffffu, sl[3], 1);
+      for (int t = 0; t < 2; ++t) sl[t] = p0 + t < n_keys ? __ldg(a.slots + p0 + t) : -1;
+      const int prev_last = __shfl_up_sync(0xffffffffu, sl[1], 1);
       bool ok = true;
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const bool chunk_start = ((lane * 4 + t) % P) == 0;
+      for (int t = 0; t < 2; ++t) {
+        const bool chunk_start = ((lane * 2 + t) % C) == 0;
         const int prev = t > 0 ? sl[t - 1] : prev_last;
         if (!chunk_start && sl[t] >= 0) ok = ok && sl[t] == prev + 1;
       }
@@ -327,105 +393,105 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool contiguous = ((ballot >> my_chunk_lane0) & chunk_mask) == chunk_mask;
       const int chunk_row = __shfl_sync(0xffffffffu, sl[0], my_chunk_lane0);
       for (int op = 0; op < 2; ++op) {  // K then V
-        const uint32_t base = (op == 0 ? sK : sV) + s * kTile;
+        const uint32_t base = (op == 0 ? sK : sV) + s * kKvTile;
         const uint32_t full = bar((op == 0 ? kBarKFull : kBarVFull) + s);
         const int col = op == 0 ? ck : cv;
         if (lane == 0) {
-          if (j >= kStages) mbar_wait(bar((op == 0 ? kBarKEmpty : kBarVEmpty) + s), ((j >> 1) + 1) & 1);
-          mbar_expect_tx(full, kTile);
+          if (j >= kStages)
+            mbar_wait(bar((op == 0 ? kBarKEmpty : kBarVEmpty) + s), ((j / kStages) + 1) & 1);
+          mbar_expect_tx(full, kKvTile);
         }
         __syncwarp();
         if (contiguous) {
           if (lane == my_chunk_lane0) {
-            const uint32_t dst = base + (lane * 4) * 128;
+            const uint32_t dst = base + (lane * 2) * 128;
             const int row = chunk_row >= 0 ? chunk_row : 0;
             tma_load_3d(dst, &pool_map, col, row, a.layer, full);
-            tma_load_3d(dst + kAtom, &pool_map, col + 64, row, a.layer, full);
+            tma_load_3d(dst + kKvAtom, &pool_map, col + 64, row, a.layer, full);
           }
         } else {
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const uint32_t dst = base + (lane * 4 + t) * 128;
+          for (int t = 0; t < 2; ++t) {
+            const uint32_t dst = base + (lane * 2 + t) * 128;
             const int row = sl[t] >= 0 ? sl[t] : 0;
             tma_load_3d(dst, &row_map, col, row, a.layer, full);
-            tma_load_3d(dst + kAtom, &row_map, col + 64, row, a.layer, full);
+            tma_load_3d(dst + kKvAtom, &row_map, col + 64, row, a.layer, full);
           }
         }
       }
     }
   } else if (warp == 9) {
     // ---------------- MMA issuer ----------------
-    constexpr uint32_t kIdescS = idesc_bf16(false), kIdescO = idesc_bf16(true);
-    const uint32_t tS[2] = {tmem, tmem + 128}, tO[2] = {tmem + 256, tmem + 384};
+    // TMEM: query tile i owns columns [128 i, 128 i + 128) as two 64-column S
+    // slots (tile j uses slot j & 1; P_i(j) overwrites the first 32 columns
+    // of its slot), O_i at 256 + 128 i.  Issue order per KV tile j:
+    //   S0(j) S1(j) | PV0(j-1) PV1(j-1)
+    // so S(j) runs on the tensor core while the softmax warpgroups work on
+    // tile j-1.  S_i(j) reuses the slot of P_i(j-2), consumed by PV_i(j-2),
+    // issued one iteration earlier (tcgen05 MMAs of one thread run in order).
+    constexpr uint32_t kIdescS = idesc_bf16(false, kKeys), kIdescO = idesc_bf16(true, kD);
+    constexpr uint32_t kHi = desc_hi(1024);  // SBO 1024 B (8-row groups), version 1, SW128
+    auto tS = [&](int i, int j) { return tmem + i * 128 + (j & 1) * 64; };
+    auto tO = [&](int i) { return tmem + 256 + i * 128; };
+    // Low descriptor words of the tile bases; K-step offsets are added in
+    // 16-byte units (start address field, no carry: smem < 256 KiB).
+    const uint32_t q_lo = desc_lo(sQ, 16), k_lo = desc_lo(sK, 16), v_lo = desc_lo(sV, kKvAtom);
     auto issue_s = [&](int i, int j) {
-      const uint32_t kb = sK + (j & 1) * kTile, qa = sQ + i * kTile;
+      const uint32_t a0 = q_lo + ((i * kTile) >> 4), b0 = k_lo + (((j % kStages) * kKvTile) >> 4);
 #pragma unroll
       for (int k = 0; k < kD / 16; ++k) {
-        const uint32_t off = (k >> 2) * kAtom + (k & 3) * 32;
-        mma_bf16(tS[i], umma_desc(qa + off, 16, 1024), umma_desc(kb + off, 16, 1024), kIdescS,
-                 k > 0 ? 1u : 0u);
+        const uint32_t ao = ((k >> 2) * kAtom + (k & 3) * 32) >> 4;
+        const uint32_t bo = ((k >> 2) * kKvAtom + (k & 3) * 32) >> 4;
+        mma_ss_elect(tS(i, j), a0 + ao, b0 + bo, kHi, kIdescS, k > 0 ? 1u : 0u);
       }
-      mma_commit(bar(kBarSFull + i));
+      commit_elect(bar(kBarSFull + i));
     };
     auto issue_pv = [&](int i, int j) {
-      const uint32_t vb = sV + (j & 1) * kTile;
+      mbar_wait(bar(kBarPFull + i), j & 1);
+      fence_after();
+      const uint32_t b0 = v_lo + (((j % kStages) * kKvTile) >> 4);
 #pragma unroll
       for (int k = 0; k < kKeys / 16; ++k) {
         // A = P_i in TMEM (bf16 pairs: 8 columns per 16 keys); B = V MN-major:
-        // 16 keys = two 8-key atoms (SBO 1024 B), d halves LBO = 16 KiB apart.
-        mma_bf16_ts(tO[i], tS[i] + k * 8, umma_desc(vb + k * 2048, kAtom, 1024), kIdescO,
-                    (j > 0 || k > 0) ? 1u : 0u);
+        // 16 keys = two 8-key atoms (SBO 1024 B), d halves LBO = 8 KiB apart.
+        mma_ts_elect(tO(i), tS(i, j) + k * 8, b0 + ((k * 2048) >> 4), kHi, kIdescO,
+                     (j > 0 || k > 0) ? 1u : 0u);
       }
+      commit_elect(bar(kBarPVDone + i));
     };
     // Keys past n_keys in the last tile: zero their V rows (both halves).
     auto zero_tail = [&](int j) {
       const int valid = n_keys - j * kKeys;
       if (valid >= kKeys) return;
-      uint8_t* vb = smem + kOffV + (j & 1) * kTile;
-      for (int i = lane; i < (kKeys - valid) * 16; i += 32) {
-        const int r = valid + (i >> 4), c = i & 15;
-        *reinterpret_cast<uint4*>(vb + (c >> 3) * kAtom + r * 128 + (c & 7) * 16) =
+      uint8_t* vb = smem + kOffV + (j % kStages) * kKvTile;
+      for (int e = lane; e < (kKeys - valid) * 16; e += 32) {
+        const int r = valid + (e >> 4), c = e & 15;
+        *reinterpret_cast<uint4*>(vb + (c >> 3) * kKvAtom + r * 128 + (c & 7) * 16) =
             make_uint4(0, 0, 0, 0);
       }
       fence_proxy_async();
       __syncwarp();
     };
     mbar_wait(bar(kBarQ), 0);
-    for (int j = 0; j < n_tiles; ++j) {
-      const int s = j & 1;
-      mbar_wait(bar(kBarKFull + s), (j >> 1) & 1);
-      fence_after();
-      if (lane == 0) issue_s(0, j);
-      if (j > 0) {
-        // PV1(j-1): V stage of tile j-1, P1 of tile j-1.
-        mbar_wait(bar(kBarPFull + 1), (j - 1) & 1);
+    for (int j = 0; j <= n_tiles; ++j) {
+      if (j < n_tiles) {
+        const int s = j % kStages;
+        mbar_wait(bar(kBarKFull + s), (j / kStages) & 1);
         fence_after();
-        if (lane == 0) {
-          issue_pv(1, j - 1);
-          mma_commit(bar(kBarVEmpty + ((j - 1) & 1)));
-        }
-      }
-      if (lane == 0) {
+        issue_s(0, j);
         issue_s(1, j);
-        mma_commit(bar(kBarKEmpty + s));
+        commit_elect(bar(kBarKEmpty + s));
       }
-      mbar_wait(bar(kBarVFull + s), (j >> 1) & 1);
-      if (j == n_tiles - 1) zero_tail(j);
-      mbar_wait(bar(kBarPFull + 0), j & 1);
-      fence_after();
-      if (lane == 0) issue_pv(0, j);
-      __syncwarp();
+      if (j > 0) {
+        const int jp = j - 1, sp = jp % kStages;
+        mbar_wait(bar(kBarVFull + sp), (jp / kStages) & 1);
+        if (jp == n_tiles - 1) zero_tail(jp);
+        fence_after();
+        issue_pv(0, jp);
+        issue_pv(1, jp);
+        commit_elect(bar(kBarVEmpty + sp));
+      }
     }
-    const int jl = n_tiles - 1;
-    if (lane == 0) mma_commit(bar(kBarOFull + 0));
-    mbar_wait(bar(kBarPFull + 1), jl & 1);
-    fence_after();
-    if (lane == 0) {
-      issue_pv(1, jl);
-      mma_commit(bar(kBarVEmpty + (jl & 1)));
-      mma_commit(bar(kBarOFull + 1));
-    }
-    __syncwarp();
   } else {
     // ---------------- softmax warpgroups ----------------
     const int i = warp >> 2;              // query tile
@@ -436,7 +502,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q_pos = a.q_pos0 + tok;
     const int tile_min_pos = a.q_pos0 + tok_first + i * kTokens;  // smallest position of tile i
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    const uint32_t tS = tmem + i * 128 + lane_off, tO = tmem + 256 + i * 128 + lane_off;
+    const uint32_t tSi = tmem + i * 128 + lane_off, tO = tmem + 256 + i * 128 + lane_off;
     {
       const __nv_bfloat16* qrow =
           a.q + (static_cast<int64_t>(tok) * a.Hq + static_cast<int64_t>(h) * G + g) * kD;
@@ -451,6 +517,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float sl2 = a.scale_log2;
     float m = -INFINITY, l = 0.f;  // running max (scaled log2 domain) and sum
     for (int j = 0; j < n_tiles; ++j) {
+      const uint32_t tS = tSi + (j & 1) * 64;
       mbar_wait(bar(kBarSFull + i), j & 1);
       fence_after();
       uint32_t sr[kKeys];
@@ -459,61 +526,69 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_wait_ld();
       const int key0 = j * kKeys;
       // Causal mask only where this tile crosses the diagonal of query tile i.
-      const bool need_mask = key0 + kKeys - 1 > tile_min_pos || !row_valid;
-      float tmax = -INFINITY;
+      // Warp-uniform: the two P paths below hold warp-collective TMEM stores.
+      const bool need_mask =
+          __any_sync(0xffffffffu, key0 + kKeys - 1 > tile_min_pos || !row_valid);
       if (need_mask) {
+        const int lim = row_valid ? q_pos - key0 : -1;  // last visible column
 #pragma unroll
-        for (int c = 0; c < kKeys; ++c) {
-          const bool ok = row_valid && key0 + c <= q_pos;
-          const float x = ok ? __uint_as_float(sr[c]) * sl2 : -INFINITY;
-          sr[c] = __float_as_uint(x);
-          tmax = fmaxf(tmax, x);
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < kKeys; ++c) {
-          const float x = __uint_as_float(sr[c]) * sl2;
-          sr[c] = __float_as_uint(x);
-          tmax = fmaxf(tmax, x);
-        }
+        for (int c = 0; c < kKeys; ++c)
+          sr[c] = c > lim ? __float_as_uint(-INFINITY) : sr[c];
       }
+      float rmax = -INFINITY;  // raw (unscaled) max
+#pragma unroll
+      for (int c = 0; c < kKeys; c += 2)
+        rmax = fmaxf(rmax, fmaxf(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])));
+      const float tmax = rmax * sl2;
       // Keep the stale max unless this tile exceeds it by > 8 (p <= 2^8 then).
       const bool bump = tmax > m + 8.f;
       const float m_new = bump ? tmax : m;
-      const float alpha = (bump && m != -INFINITY) ? exp2f(m - m_new) : 1.f;
-      const float mref = m_new == -INFINITY ? 0.f : m_new;
+      const float alpha = (bump && m != -INFINITY) ? ex2_mufu(m - m_new) : 1.f;
+      const float neg_m = m_new == -INFINITY ? 0.f : -m_new;
       float psum = 0.f;
-      uint32_t pk[kKeys / 2];
+      // P = 2^(s*scale - m) packed in place (pair c/2 overwrites S[c/2],
+      // already consumed).  In unmasked tiles every 4th exponential runs on
+      // the FMA pipe (polynomial) to relieve the MUFU unit.
+      auto make_p = [&](auto poly) {
 #pragma unroll
-      for (int c = 0; c < kKeys; c += 2) {
-        const float p0 = exp2f(__uint_as_float(sr[c]) - mref);
-        const float p1 = exp2f(__uint_as_float(sr[c + 1]) - mref);
-        psum += p0 + p1;
-        pk[c / 2] = pack_bf16(p0, p1);
-      }
-      // P_i over the first 64 columns of S_i.
+        for (int c = 0; c < kKeys; c += 2) {
+          const float x0 = fmaf(__uint_as_float(sr[c]), sl2, neg_m);
+          const float x1 = fmaf(__uint_as_float(sr[c + 1]), sl2, neg_m);
+          const float p0 = ex2_mufu(x0);
+          const float p1 = (decltype(poly)::value && (c & 2)) ? ex2_poly(x1) : ex2_mufu(x1);
+          psum += p0 + p1;
+          sr[c / 2] = pack_bf16(p0, p1);
+        }
+      };
+      if (need_mask) make_p(std::false_type{});
+      else make_p(std::true_type{});
 #pragma unroll
-      for (int c0 = 0; c0 < kKeys / 2; c0 += 16) tmem_st16_nowait(tS + c0, pk + c0);
-      l = l * alpha + psum;
-      m = m_new;
-      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+      for (int c0 = 0; c0 < kKeys / 2; c0 += 16) tmem_st16_nowait(tS + c0, sr + c0);
+      // O_i must be stable (PV_i(j-1) retired) before it is rescaled for tile j.
+      if (j > 0) {
+        mbar_wait(bar(kBarPVDone + i), (j - 1) & 1);
+        fence_after();
+        if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll
-        for (int c0 = 0; c0 < kD; c0 += 32) {
-          uint32_t o[32];
-          tmem_ld16_nowait(tO + c0, o);
-          tmem_ld16_nowait(tO + c0 + 16, o + 16);
-          tmem_wait_ld();
+          for (int c0 = 0; c0 < kD; c0 += 32) {
+            uint32_t o[32];
+            tmem_ld16_nowait(tO + c0, o);
+            tmem_ld16_nowait(tO + c0 + 16, o + 16);
+            tmem_wait_ld();
 #pragma unroll
-          for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
-          tmem_st16_nowait(tO + c0, o);
-          tmem_st16_nowait(tO + c0 + 16, o + 16);
+            for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
+            tmem_st16_nowait(tO + c0, o);
+            tmem_st16_nowait(tO + c0 + 16, o + 16);
+          }
         }
       }
       tmem_wait_st();
       fence_before();
       mbar_arrive(bar(kBarPFull + i));
+      l = l * alpha + psum;
+      m = m_new;
     }
-    mbar_wait(bar(kBarOFull + i), 0);
+    mbar_wait(bar(kBarPVDone + i), (n_tiles - 1) & 1);
     fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
     __nv_bfloat16* orow =
@@ -525,13 +600,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld16_nowait(tO + c0 + 16, o + 16);
       tmem_wait_ld();
       if (row_valid) {
-        uint4 w[4];
-        uint32_t* wp = reinterpret_cast<uint32_t*>(w);
 #pragma unroll
-        for (int k = 0; k < 16; ++k)
-          wp[k] = pack_bf16(__uint_as_float(o[2 * k]) * inv, __uint_as_float(o[2 * k + 1]) * inv);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) reinterpret_cast<uint4*>(orow + c0)[k] = w[k];
+        for (int k = 0; k < 4; ++k) {
+          auto pk = [&](int e) {
+            return pack_bf16(__uint_as_float(o[8 * k + e]) * inv,
+                             __uint_as_float(o[8 * k + e + 1]) * inv);
+          };
+          reinterpret_cast<uint4*>(orow + c0)[k] = make_uint4(pk(0), pk(2), pk(4), pk(6));
+        }
       }
     }
   }
@@ -584,9 +660,11 @@ bool make_pool_tensor_map(void* pool, int64_t layers, int64_t rows, int64_t row_
 }
 
 bool prefill_attn_supported(int page_size, int Hq, int Hkv, int D) {
-  return D == kD && Hkv >= 1 && Hq == 8 * Hkv && page_size >= 8 && page_size <= kKeys &&
-         kKeys % page_size == 0;
+  const bool pow2 = page_size > 0 && (page_size & (page_size - 1)) == 0;
+  return D == kD && Hkv >= 1 && Hq == 8 * Hkv && pow2 && page_size >= 8 && page_size <= 1024;
 }
+
+int prefill_attn_box_rows(int page_size) { return page_size < kKeys ? page_size : kKeys; }
 
 bool launch_prefill_attn(const PoolTensorMap& page_map, const PoolTensorMap& row_map, int layer,
                          int page_size, const int32_t* slots,

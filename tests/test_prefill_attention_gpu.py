@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 
 def _setup(torch, hkv, hd, n, layers=2, P=16, seed=0):
     W = 4 * hkv * hd // 8
-    pages = (n + P - 1) // P + 64
+    pages = (n + P - 1) // P + 8
     c = KVCache(num_pages=pages + 40, page_size=P, layers=layers, dim=W, device=0)
     for i in range(40):  # fragment the free list
         c.CreateSequence(1000 + i, [i % 7] * P)
@@ -80,6 +80,58 @@ def test_prefill_matches_fp32_reference(cuda, case):
         assert err.max().item() <= 2e-2, (case, layer, err.max().item())
         rel = (out.float() - ref).pow(2).mean().sqrt() / ref.pow(2).mean().sqrt()
         assert rel.item() <= 2e-2, (case, layer, rel.item())
+
+
+@pytest.mark.parametrize("page_size", [8, 32, 64, 128, 256])
+def test_prefill_page_sizes(cuda, page_size):
+    torch = cuda
+    hq, hkv, hd, n, qb = 64, 8, 128, 777, 500
+    c, kv = _setup(torch, hkv, hd, n, layers=1, P=page_size, seed=page_size)
+    q = (torch.randn(n - qb, hq, hd, device="cuda") * 0.5).to(torch.bfloat16)
+    out = torch.empty_like(q)
+    c.paged_prefill_attention_async(1, (qb, n), 0, hq, hkv, hd, hd ** -0.5, q.data_ptr(),
+                                    out.data_ptr(), 0)
+    torch.cuda.synchronize()
+    ref = _ref(torch, q, kv[0][0], kv[0][1], qb, hd ** -0.5)
+    assert (out.float() - ref).abs().max().item() <= 2e-2
+
+
+@pytest.mark.parametrize("fork_len", [37, 64, 129])
+def test_prefill_over_forked_sequence(cuda, fork_len):
+    """A child forked at a non-page-aligned length reads [0, fork_len) through
+    the parent's pages and the rest through its own, so position chunks are
+    not one contiguous page: the per-row load path."""
+    torch = cuda
+    hq, hkv, hd, P = 64, 8, 128, 16
+    n_parent, n = 300, 700
+    W = 4 * hkv * hd // 8
+    c = KVCache(num_pages=128, page_size=P, layers=1, dim=W, device=0)
+    toks = [i % 13 for i in range(n)]
+    c.CreateSequence(1, toks[:n_parent])
+    c.EnsureAllocated(1, n_parent)
+    rows_p = (torch.randn(n_parent, 2, hkv, hd, device="cuda") * 0.5).to(torch.bfloat16)
+    plan = c.BeginForward([BatchEntry(1, (0, n_parent))])
+    c.append_rows_async(plan, 0, rows_p.data_ptr(), 0)
+    torch.cuda.synchronize()
+    plan.close()
+    c.ForkSequence(1, 2, fork_len, toks)
+    c.EnsureAllocated(2, n)
+    rows_c = (torch.randn(n - fork_len, 2, hkv, hd, device="cuda") * 0.5).to(torch.bfloat16)
+    plan = c.BeginForward([BatchEntry(2, (fork_len, n))])
+    c.append_rows_async(plan, 0, rows_c.data_ptr(), 0)
+    torch.cuda.synchronize()
+    plan.close()
+    K = torch.cat([rows_p[:fork_len, 0], rows_c[:, 0]]).float()
+    V = torch.cat([rows_p[:fork_len, 1], rows_c[:, 1]]).float()
+    qb = 5
+    q = (torch.randn(n - qb, hq, hd, device="cuda") * 0.5).to(torch.bfloat16)
+    out = torch.empty_like(q)
+    c.paged_prefill_attention_async(2, (qb, n), 0, hq, hkv, hd, hd ** -0.5, q.data_ptr(),
+                                    out.data_ptr(), 0)
+    torch.cuda.synchronize()
+    ref = _ref(torch, q, K, V, qb, hd ** -0.5)
+    err = (out.float() - ref).abs()
+    assert err.max().item() <= 2e-2, err.max().item()
 
 
 def test_prefill_last_query_equals_decode(cuda):
