@@ -657,8 +657,10 @@ def measure_configs(torch) -> dict:
             D.EnsureAllocated(seq, PROMPT)
             plan = D.BeginForward([BatchEntry(seq, (sp, PROMPT))])
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            # Queue all 80 launches behind a sleep so the events time the
+            # device, not the host's per-call launch cost.
             with torch.cuda.stream(s):
-                torch.cuda._sleep(100_000)
+                torch.cuda._sleep(20_000_000)
             e0.record(s)
             for layer in range(L):
                 D.append_rows_async(plan, layer, rows.data_ptr(), s.cuda_stream)
@@ -773,23 +775,28 @@ def measure_sweep(torch) -> dict:
     seq = 100
     for n in (16, 64, 256, 1024, 4096, 8192, 16384, 32768):
         times, walls = [], []
-        for rep in range(5):
+        for rep in range(10):
             seq += 1
             rr = D.PrepRecv(seq, prompt[:n + 1], -1)
             plan = P.begin_direct_send(1, (0, n), 1, rr.addr, rep)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            # Device time: the launch is queued behind a short sleep so host
-            # launch latency stays outside e0..e1; wall time: call to sync.
-            with torch.cuda.stream(s):
-                torch.cuda._sleep(100_000)
+            # Even reps, device time: the launch is queued behind a sleep
+            # longer than the host's launch path so host latency stays outside
+            # e0..e1.  Odd reps, wall time: launch call to stream sync.
+            timed_dev = rep % 2 == 0
+            if timed_dev:
+                with torch.cuda.stream(s):
+                    torch.cuda._sleep(4_000_000)
             e0.record(s)
             w0 = time.perf_counter()
             P.launch_direct_send_async(plan, (0, L), s.cuda_stream)
             e1.record(s)
             s.synchronize()
-            walls.append(time.perf_counter() - w0)
+            if timed_dev:
+                times.append(e0.elapsed_time(e1) / 1e3)
+            else:
+                walls.append(time.perf_counter() - w0)
             assert D.DrainReceiveCompletions() == [seq]
-            times.append(e0.elapsed_time(e1) / 1e3)
             plan.close()
             D.FreeSequence(seq)
         t, wt = float(np.median(times)), float(np.median(walls))
