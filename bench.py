@@ -462,6 +462,14 @@ def secondary_measurements(P, D, prompt, torch) -> dict:
         out["decode_attention"] = measure_decode(torch)
     except Exception as ex:
         out["decode_attention"] = {"error": str(ex)}
+    try:
+        out["prefill_attention"] = measure_prefill(torch)
+    except Exception as ex:
+        out["prefill_attention"] = {"error": str(ex)}
+    try:
+        out["frames"] = measure_frames(torch)
+    except Exception as ex:
+        out["frames"] = {"error": str(ex)}
     return out
 
 
@@ -898,6 +906,149 @@ def measure_decode(torch) -> dict:
         dplan.close()
         del Cd
         torch.cuda.empty_cache()
+    return res
+
+
+def _bf16_peak() -> float:
+    try:
+        return float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["bf16_tflops"])
+    except Exception:
+        return 2250.0
+
+
+def measure_prefill(torch) -> dict:
+    """tcgen05 paged causal prefill attention (70B heads: Hq=64, Hkv=8,
+    D=128): the decode engine's tail prefill in balanced PD (queries
+    [6554, 8192) over 8K keys, r = 0.2) and a full 8K prefill.  FLOPs =
+    4 * D * Hq * sum over queries of (position + 1)."""
+    from paper_2412_12488_b200 import BatchEntry, KVCache
+
+    peak = _bf16_peak()
+    res = {}
+    for ctx, qb in ((8192, 6554), (8192, 0)):
+        nq = ctx - qb
+        c = KVCache(num_pages=ctx // PAGE + 16, page_size=PAGE, layers=1, dim=W, device=0)
+        c.CreateSequence(1, np.zeros(ctx, np.int32))
+        c.EnsureAllocated(1, ctx)
+        plan = c.BeginForward([BatchEntry(1, (0, ctx))])
+        rows = (torch.randn(ctx, 2, HKV, HD, device="cuda") * 0.5).to(torch.bfloat16)
+        c.append_rows_async(plan, 0, rows.data_ptr(), 0)
+        torch.cuda.synchronize()
+        plan.close()
+        q = (torch.randn(nq, HQ, HD, device="cuda") * 0.5).to(torch.bfloat16)
+        o = torch.empty_like(q)
+        s = torch.cuda.Stream()
+        fn = lambda: c.paged_prefill_attention_async(1, (qb, ctx), 0, HQ, HKV, HD, HD ** -0.5,  # noqa: E731
+                                                     q.data_ptr(), o.data_ptr(), s.cuda_stream)
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        reps = 10
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        with torch.cuda.stream(s):
+            torch.cuda._sleep(20_000_000)
+        ev[0].record(s)
+        for _ in range(reps):
+            fn()
+        ev[1].record(s)
+        torch.cuda.synchronize()
+        t = ev[0].elapsed_time(ev[1]) / 1e3 / reps
+        flops = 4.0 * HD * HQ * sum(range(qb + 1, ctx + 1))
+        res[f"q{qb}-{ctx}_ctx{ctx}"] = {"us": round(1e6 * t, 1),
+                                        "tflops": round(flops / t / 1e12, 1),
+                                        "frac_bf16_peak": round(flops / t / 1e12 / peak, 4)}
+        del c, rows, q, o
+        torch.cuda.empty_cache()
+    res["peak_tflops"] = peak
+    return res
+
+
+def measure_frames(torch) -> dict:
+    """Wire formats at the 70B shape: CRC-32 of one layer's payload (8,191
+    tokens x 4 KiB = 33.5 MB) on the device, a write frame encoded into
+    device memory (gather + CRC), into host memory (+ D2H), and received
+    from host memory (H2D + CRC + apply); the reference's host Crc32 on the
+    same bytes for scale."""
+    import ctypes as C
+
+    from paper_2412_12488_b200 import BatchEntry, KVCache
+    from paper_2412_12488_b200.kvcache import frame_write_header_size
+
+    tokens = PROMPT - 1
+    payload = tokens * W * 8
+    res = {"tokens": tokens, "payload_mb": round(payload / 1e6, 2)}
+    s = torch.cuda.Stream()
+    P = KVCache(num_pages=tokens // PAGE + 8, page_size=PAGE, layers=1, dim=W, device=0, rank=0)
+    D = KVCache(num_pages=tokens // PAGE + 8, page_size=PAGE, layers=1, dim=W, device=0, rank=1)
+    prompt = _prompt(7)
+    P.CreateSequence(1, prompt)
+    P.EnsureAllocated(1, tokens)
+    plan = P.BeginForward([BatchEntry(1, (0, tokens))])
+    rows = torch.empty(tokens * W, dtype=torch.int64, device="cuda").random_()
+    P.append_rows_async(plan, 0, rows.data_ptr(), 0)
+    torch.cuda.synchronize()
+    plan.close()
+    r = D.PrepRecv(1, prompt, -1)
+    out = torch.zeros(1, dtype=torch.int64, device="cuda")
+
+    def dev_time(fn, reps=20):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        with torch.cuda.stream(s):
+            torch.cuda._sleep(20_000_000)
+        ev[0].record(s)
+        for _ in range(reps):
+            fn()
+        ev[1].record(s)
+        torch.cuda.synchronize()
+        return ev[0].elapsed_time(ev[1]) / 1e3 / reps
+
+    t = dev_time(lambda: P.crc32_async(rows.data_ptr(), payload, out.data_ptr(), s.cuda_stream))
+    res["crc32_us"] = round(1e6 * t, 1)
+    res["crc32_gbs"] = round(payload / t / 1e9, 1)
+    hdr = frame_write_header_size(len(r.addr.ranges))
+    fb = torch.empty(payload + hdr + 64, dtype=torch.uint8, device="cuda")
+    off = (-(fb.data_ptr() + hdr)) % 32
+    t = dev_time(lambda: P.encode_write_frame_async(1, (0, tokens), 0, 7, r.addr,
+                                                    fb.data_ptr() + off, payload + hdr + 64 - off,
+                                                    s.cuda_stream))
+    res["frame_device_us"] = round(1e6 * t, 1)
+    res["frame_device_payload_gbs"] = round(payload / t / 1e9, 1)
+    # Host frames in a pinned, reused buffer (what a socket sender keeps).
+    flen = hdr + payload + 4
+    hb = torch.empty(flen, dtype=torch.uint8, pin_memory=True)
+    walls = []
+    for _ in range(6):
+        w0 = time.perf_counter()
+        P.encode_write_frame_into(1, (0, tokens), 0, 7, r.addr, hb.data_ptr(), flen)
+        walls.append(time.perf_counter() - w0)
+    tw = float(np.median(walls[1:]))
+    res["frame_host_ms"] = round(1e3 * tw, 3)
+    res["frame_host_payload_gbs"] = round(payload / tw / 1e9, 1)
+    f = bytes(hb.numpy())
+    walls = []
+    for i in range(4):
+        w0 = time.perf_counter()
+        D.receive_write_frame_from(hb.data_ptr(), flen)
+        walls.append(time.perf_counter() - w0)
+    tw = float(np.median(walls[1:]))
+    res["receive_host_ms"] = round(1e3 * tw, 3)
+    res["receive_host_payload_gbs"] = round(payload / tw / 1e9, 1)
+    try:
+        lib = C.CDLL(str(ROOT / "oracle" / "_ref" / "libmicrokv_ref.so"))
+        lib.ssref_crc32.restype = C.c_uint32
+        lib.ssref_crc32.argtypes = [C.c_char_p, C.c_int64]
+        w0 = time.perf_counter()
+        want = lib.ssref_crc32(f[hdr:hdr + payload], payload)
+        tw = time.perf_counter() - w0
+        assert want == int.from_bytes(f[-4:], "little"), "frame CRC differs from the reference's"
+        res["reference_crc32_gbs_1core"] = round(payload / tw / 1e9, 3)
+    except OSError:
+        pass
+    del P, D, rows, fb
+    torch.cuda.empty_cache()
     return res
 
 

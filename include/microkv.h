@@ -390,6 +390,83 @@ int64_t ss_kernel_launches(const ss_cache* cache);
 /* Sync the cache's internal stream. */
 int ss_synchronize(ss_cache* cache);
 
+/* ------------------------------------------------------------------ */
+/* Wire formats (transport.h:6-12; kv_addr.cc:53-118;                   */
+/* transport.cc:14-107) — byte-identical to the reference's encodings   */
+/* ------------------------------------------------------------------ */
+#define SS_FRAME_MAGIC 0x4B565452u /* "KVTR", transport.h:32 */
+#define SS_WIRE_VERSION 1          /* transport.h:33 */
+#define SS_ACK_FRAME_BYTES 26
+enum ss_frame_type { SS_FRAME_WRITE = 0, SS_FRAME_ACK = 1 };       /* FrameType */
+enum ss_ack_status {                                                /* AckStatus */
+  SS_ACK_OK = 0,
+  SS_ACK_CHECKSUM_MISMATCH = 1,
+  SS_ACK_UNKNOWN_ADDRESS = 2
+};
+
+/* DecodeFrame (transport.cc:76-107) without the payload copy: the payload
+ * stays in the frame at payload_offset; its CRC is the device's job
+ * (ss_crc32_async / ss_receive_write_frame).  For a write frame `addr`
+ * receives the address (caller sets addr.ranges / addr.ranges_cap). */
+typedef struct {
+  int32_t type;           /* ss_frame_type */
+  int32_t layer;
+  uint64_t seq_tag;
+  ss_addr addr;           /* write */
+  int64_t payload_offset; /* write: byte offset of the payload in the frame */
+  int64_t payload_bytes;  /* write */
+  uint32_t wire_crc;      /* write: the frame's CRC-32 field */
+  int32_t ack_status;     /* ack: ss_ack_status */
+  int64_t token_begin;    /* ack */
+} ss_frame_info;
+
+/* KVAddrInfo::EncodeTo / DecodeFrom (kv_addr.cc:90-118): 20 + 8 n bytes,
+ * little-endian.  Decode starts at *pos and advances it; it validates the
+ * address (kv_addr.cc:16-30) like the reference. */
+int ss_addr_encode(const ss_addr* addr, uint8_t* out, int64_t cap, int64_t* len);
+int ss_addr_decode(const uint8_t* data, int64_t size, int64_t* pos, ss_addr* out);
+/* KVAddrInfo::ToJson / FromJson (kv_addr.cc:53-70); `len` excludes the NUL
+ * written after the text when it fits.  Malformed JSON returns
+ * SS_ERR_INTERNAL, as the reference's nlohmann exception does at this ABI. */
+int ss_addr_to_json(const ss_addr* addr, char* out, int64_t cap, int64_t* len);
+int ss_addr_from_json(const char* text, int64_t len, ss_addr* out);
+/* Bytes of a write frame before its payload: 41 + 8 * n_ranges. */
+int64_t ss_frame_write_header_size(int64_t n_ranges);
+/* EncodeAckFrame (transport.cc:64-74) into out[SS_ACK_FRAME_BYTES]. */
+int ss_frame_encode_ack(uint64_t seq_tag, int32_t layer, int64_t token_begin, int32_t status,
+                        uint8_t* out, int64_t cap, int64_t* len);
+int ss_frame_decode(const uint8_t* frame, int64_t size, ss_frame_info* info);
+/* CRC-32 (Crc32, transport.cc:14-28: IEEE 802.3, reflected, 0xEDB88320)
+ * of n_bytes of device memory (any alignment), written as a uint32 to
+ * crc_dev, enqueued on `stream`.  One sm_100a launch. */
+int ss_crc32_async(ss_cache* cache, const void* data_dev, int64_t n_bytes, uint32_t* crc_dev,
+                   void* stream);
+/* EncodeWriteFrame(WriteFrame{seq_tag, layer, dest_addr,
+ * GatherRange(seq, [begin, end), layer)}) (transport.cc:46-62): the layer's
+ * rows are gathered through the page table and checksummed on the GPU.
+ * dest_addr must cover exactly [begin, end) (SS_ERR_ADDR_MISMATCH, as
+ * MarkSend).  Host variant: `frame` is host memory, returns when the frame
+ * is complete.  Device variant: `frame_dev` is device memory with
+ * frame_dev + ss_frame_write_header_size(n_ranges) 32-byte aligned;
+ * enqueued on `stream`.  Either way *frame_len = the frame's size
+ * (header + payload + 4); short `cap` returns SS_ERR_BUFFER_TOO_SMALL with
+ * *frame_len = the size needed. */
+int ss_encode_write_frame(ss_cache* cache, int64_t seq, int64_t begin, int64_t end, int32_t layer,
+                          uint64_t seq_tag, const ss_addr* dest_addr, uint8_t* frame, int64_t cap,
+                          int64_t* frame_len);
+int ss_encode_write_frame_async(ss_cache* cache, int64_t seq, int64_t begin, int64_t end,
+                                int32_t layer, uint64_t seq_tag, const ss_addr* dest_addr,
+                                void* frame_dev, int64_t cap, int64_t* frame_len, void* stream);
+/* The transfer agent's step for one received write frame in host memory
+ * (TCP fabric inbound loop, tcp_fabric.cc:144-168): decode, payload to the
+ * device, CRC-32 on the device; on a mismatch the ack is ChecksumMismatch
+ * and nothing is applied (*apply_status = -1); otherwise ApplyRemoteWrite
+ * (addr, layer, payload, seq_tag) runs and the ack is UnknownAddress or Ok
+ * (*apply_status = ss_apply_status).  ack_out receives the 26-byte ack
+ * frame to send back.  Framing errors return SS_ERR_INVALID_ARGUMENT. */
+int ss_receive_write_frame(ss_cache* cache, const uint8_t* frame, int64_t size, uint8_t* ack_out,
+                           int32_t* apply_status);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

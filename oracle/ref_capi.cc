@@ -34,6 +34,7 @@
 #include "splitserve/errors.h"
 #include "splitserve/hash_model.h"
 #include "splitserve/kv_cache.h"
+#include "splitserve/transport.h"
 
 using namespace splitserve;
 
@@ -477,6 +478,150 @@ int ss_copy_counters(const ss_cache*, int64_t* h2d, int64_t* d2h) {
 }
 int64_t ss_kernel_launches(const ss_cache*) { return 0; }
 int ss_synchronize(ss_cache*) { return SS_OK; }
+
+/* ------------------------------------------------------------------ */
+/* Wire formats: the reference codec (kv_addr.cc:53-118,               */
+/* transport.cc:14-107) behind the same entry points.                  */
+/* ------------------------------------------------------------------ */
+int ss_addr_encode(const ss_addr* a, uint8_t* out, int64_t cap, int64_t* len) {
+  return Guard(nullptr, [&]() -> int {
+    std::vector<uint8_t> b;
+    ToAddr(a).EncodeTo(&b);
+    *len = static_cast<int64_t>(b.size());
+    if (*len > cap) return SS_ERR_BUFFER_TOO_SMALL;
+    std::copy(b.begin(), b.end(), out);
+    return SS_OK;
+  });
+}
+
+int ss_addr_decode(const uint8_t* data, int64_t size, int64_t* pos, ss_addr* out) {
+  return Guard(nullptr, [&]() -> int {
+    size_t p = static_cast<size_t>(*pos);
+    KVAddrInfo a = KVAddrInfo::DecodeFrom(data, static_cast<size_t>(size), &p);
+    int st = FromAddr(nullptr, a, out);
+    if (st == SS_OK) *pos = static_cast<int64_t>(p);
+    return st;
+  });
+}
+
+int ss_addr_to_json(const ss_addr* a, char* out, int64_t cap, int64_t* len) {
+  return Guard(nullptr, [&]() -> int {
+    std::string j = ToAddr(a).ToJson();
+    *len = static_cast<int64_t>(j.size());
+    if (*len + 1 > cap) return SS_ERR_BUFFER_TOO_SMALL;
+    std::memcpy(out, j.c_str(), j.size() + 1);
+    return SS_OK;
+  });
+}
+
+int ss_addr_from_json(const char* text, int64_t len, ss_addr* out) {
+  return Guard(nullptr, [&]() -> int {
+    return FromAddr(nullptr, KVAddrInfo::FromJson(std::string(text, static_cast<size_t>(len))), out);
+  });
+}
+
+int64_t ss_frame_write_header_size(int64_t n_ranges) {
+  WriteFrame f;
+  f.addr.ranges.resize(static_cast<size_t>(n_ranges));
+  return static_cast<int64_t>(EncodeWriteFrame(f).size()) - 4;  // minus the CRC of an empty payload
+}
+
+int ss_frame_encode_ack(uint64_t seq_tag, int32_t layer, int64_t token_begin, int32_t status,
+                        uint8_t* out, int64_t cap, int64_t* len) {
+  return Guard(nullptr, [&]() -> int {
+    AckFrame a;
+    a.seq_tag = seq_tag;
+    a.layer = layer;
+    a.token_begin = token_begin;
+    a.status = static_cast<AckStatus>(status);
+    auto b = EncodeAckFrame(a);
+    *len = static_cast<int64_t>(b.size());
+    if (*len > cap) return SS_ERR_BUFFER_TOO_SMALL;
+    std::copy(b.begin(), b.end(), out);
+    return SS_OK;
+  });
+}
+
+int ss_frame_decode(const uint8_t* frame, int64_t size, ss_frame_info* info) {
+  return Guard(nullptr, [&]() -> int {
+    DecodedFrame d = DecodeFrame(frame, static_cast<size_t>(size));
+    info->type = static_cast<int32_t>(d.type);
+    if (d.type == FrameType::kWrite) {
+      info->seq_tag = d.write.seq_tag;
+      info->layer = d.write.layer;
+      info->payload_offset = 41 + 8 * static_cast<int64_t>(d.write.addr.ranges.size());
+      info->payload_bytes = static_cast<int64_t>(d.write.payload.size()) * 8;
+      const uint8_t* c = frame + info->payload_offset + info->payload_bytes;
+      info->wire_crc = c[0] | (c[1] << 8) | (c[2] << 16) | (static_cast<uint32_t>(c[3]) << 24);
+      return FromAddr(nullptr, d.write.addr, &info->addr);
+    }
+    info->seq_tag = d.ack.seq_tag;
+    info->layer = d.ack.layer;
+    info->token_begin = d.ack.token_begin;
+    info->ack_status = static_cast<int32_t>(d.ack.status);
+    info->addr.n_ranges = 0;
+    return SS_OK;
+  });
+}
+
+int ss_crc32_async(ss_cache*, const void*, int64_t, uint32_t*, void*) { return SS_ERR_UNSUPPORTED; }
+
+// WriteFrame{tag, layer, dest, GatherRange(seq, range, layer)} with
+// MarkSend's address rule (kv_cache.cc:231-243), then EncodeWriteFrame.
+int ss_encode_write_frame(ss_cache* c, int64_t seq, int64_t begin, int64_t end, int32_t layer,
+                          uint64_t seq_tag, const ss_addr* dest_addr, uint8_t* frame, int64_t cap,
+                          int64_t* frame_len) {
+  return Guard(c, [&]() -> int {
+    WriteFrame f;
+    f.seq_tag = seq_tag;
+    f.layer = layer;
+    f.addr = ToAddr(dest_addr);
+    SPLITSERVE_CHECK(f.addr.token_count == end - begin && f.addr.token_begin == begin,
+                     ErrorCode::kAddrMismatch, "destination does not cover the range");
+    f.addr.Validate();
+    f.payload = c->cache->GatherRange(seq, {begin, end}, layer);
+    auto b = EncodeWriteFrame(f);
+    *frame_len = static_cast<int64_t>(b.size());
+    if (*frame_len > cap) return Fail(c, SS_ERR_BUFFER_TOO_SMALL, "frame buffer too small");
+    std::copy(b.begin(), b.end(), frame);
+    return SS_OK;
+  });
+}
+
+int ss_encode_write_frame_async(ss_cache*, int64_t, int64_t, int64_t, int32_t, uint64_t,
+                                const ss_addr*, void*, int64_t, int64_t*, void*) {
+  return SS_ERR_UNSUPPORTED;
+}
+
+// The TCP fabric's inbound step (tcp_fabric.cc:144-168) with
+// apply = ApplyRemoteWrite(addr, layer, payload, seq_tag).
+int ss_receive_write_frame(ss_cache* c, const uint8_t* frame, int64_t size, uint8_t* ack_out,
+                           int32_t* apply_status) {
+  return Guard(c, [&]() -> int {
+    DecodedFrame d = DecodeFrame(frame, static_cast<size_t>(size));
+    SPLITSERVE_CHECK(d.type == FrameType::kWrite, ErrorCode::kInvalidArgument, "not a write frame");
+    AckFrame ack;
+    ack.seq_tag = d.write.seq_tag;
+    ack.layer = d.write.layer;
+    ack.token_begin = d.write.addr.token_begin;
+    *apply_status = -1;
+    if (!d.crc_ok) {
+      ack.status = AckStatus::kChecksumMismatch;
+    } else {
+      auto st = c->cache->ApplyRemoteWrite(d.write.addr, d.write.layer, d.write.payload,
+                                           d.write.seq_tag);
+      *apply_status = static_cast<int32_t>(st);
+      ack.status = st == KVCache::ApplyStatus::kUnknownAddress ? AckStatus::kUnknownAddress
+                                                                : AckStatus::kOk;
+    }
+    auto b = EncodeAckFrame(ack);
+    std::copy(b.begin(), b.end(), ack_out);
+    return SS_OK;
+  });
+}
+
+/* Host CRC-32 of the reference (transport.cc:14-28), for tests. */
+uint32_t ssref_crc32(const uint8_t* data, int64_t n) { return Crc32(data, static_cast<size_t>(n)); }
 
 /* ------------------------------------------------------------------ */
 /* Reference arm of bench.py: DirectSend KV migration through the      */

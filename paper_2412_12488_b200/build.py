@@ -20,8 +20,8 @@ LIB = OUT_DIR / "libmicrokv.so"
 INCLUDE = HERE.parent / "include"
 CUDA_HOME = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 
-HOST_SRCS = ["radix_tree.cc", "cache.cc", "capi.cc"]
-CUDA_SRCS = ["kernels.cu", "decode_attn.cu", "prefill_attn.cu"]
+HOST_SRCS = ["radix_tree.cc", "cache.cc", "wire.cc", "frames.cc", "capi.cc"]
+CUDA_SRCS = ["kernels.cu", "decode_attn.cu", "prefill_attn.cu", "crc32.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -289,6 +289,16 @@ struct ss_cache {
                         cudaStream_t s);
   void DecodeAttention(ss_plan* plan, int32_t layer, int32_t hq, int32_t hkv, int32_t hd,
                        float scale, const void* q, void* out, cudaStream_t s);
+  // Wire formats (frames.cc): CRC-32 of device bytes; a KV write frame of
+  // GatherRange(seq, [begin, end), layer) encoded byte-identical to the
+  // reference's EncodeWriteFrame with gather + CRC on the device; the
+  // transfer agent's receive step for one frame (tcp_fabric.cc:144-168).
+  void Crc32(const void* data_dev, int64_t n, uint32_t* crc_dev, cudaStream_t s);
+  int64_t EncodeWriteFrame(SeqId seq, int64_t begin, int64_t end, int32_t layer, uint64_t tag,
+                           const mkv::KVAddr& dest, uint8_t* frame, int64_t cap,
+                           bool frame_on_device, cudaStream_t s);
+  void ReceiveWriteFrame(const uint8_t* frame, int64_t size, uint8_t* ack_out,
+                         int32_t* apply_status);
   void DestroyPlan(ss_plan* plan);
   void FreePlanDevice(ss_plan* plan);
   void Synchronize();

@@ -12,6 +12,7 @@
 
 #include "../../include/microkv.h"
 #include "cache.h"
+#include "wire.h"
 
 using mkv::KVAddr;
 
@@ -504,6 +505,120 @@ int64_t ss_kernel_launches(const ss_cache* c) { return c->launches(); }
 int ss_synchronize(ss_cache* c) {
   return Guard(c, [&]() -> int {
     c->Synchronize();
+    return SS_OK;
+  });
+}
+
+// ---------------------------------------------------------------------------
+// Wire formats (wire.cc, frames.cc)
+// ---------------------------------------------------------------------------
+int ss_addr_encode(const ss_addr* a, uint8_t* out, int64_t cap, int64_t* len) {
+  return Guard(nullptr, [&]() -> int {
+    std::vector<uint8_t> b;
+    mkv::EncodeAddr(ToAddr(a), &b);
+    *len = static_cast<int64_t>(b.size());
+    if (*len > cap) return SS_ERR_BUFFER_TOO_SMALL;
+    if (!b.empty()) std::memcpy(out, b.data(), b.size());
+    return SS_OK;
+  });
+}
+
+int ss_addr_decode(const uint8_t* data, int64_t size, int64_t* pos, ss_addr* out) {
+  return Guard(nullptr, [&]() -> int {
+    MKV_CHECK(size >= 0 && *pos >= 0 && *pos <= size, mkv::kInvalidArgument, "bad position");
+    size_t p = static_cast<size_t>(*pos);
+    const KVAddr a = mkv::DecodeAddr(data, static_cast<size_t>(size), &p);
+    const int st = FromAddr(nullptr, a, out);
+    if (st == SS_OK) *pos = static_cast<int64_t>(p);
+    return st;
+  });
+}
+
+int ss_addr_to_json(const ss_addr* a, char* out, int64_t cap, int64_t* len) {
+  return Guard(nullptr, [&]() -> int {
+    const std::string j = mkv::AddrToJson(ToAddr(a));
+    *len = static_cast<int64_t>(j.size());
+    if (*len + 1 > cap) return SS_ERR_BUFFER_TOO_SMALL;
+    std::memcpy(out, j.c_str(), j.size() + 1);
+    return SS_OK;
+  });
+}
+
+int ss_addr_from_json(const char* text, int64_t len, ss_addr* out) {
+  return Guard(nullptr, [&]() -> int {
+    return FromAddr(nullptr, mkv::AddrFromJson(std::string(text, static_cast<size_t>(len))), out);
+  });
+}
+
+int64_t ss_frame_write_header_size(int64_t n_ranges) {
+  return static_cast<int64_t>(mkv::WriteHeaderSize(static_cast<size_t>(n_ranges)));
+}
+
+int ss_frame_encode_ack(uint64_t seq_tag, int32_t layer, int64_t token_begin, int32_t status,
+                        uint8_t* out, int64_t cap, int64_t* len) {
+  return Guard(nullptr, [&]() -> int {
+    const auto b = mkv::EncodeAck(seq_tag, layer, token_begin, static_cast<uint8_t>(status));
+    *len = static_cast<int64_t>(b.size());
+    if (*len > cap) return SS_ERR_BUFFER_TOO_SMALL;
+    std::memcpy(out, b.data(), b.size());
+    return SS_OK;
+  });
+}
+
+int ss_frame_decode(const uint8_t* frame, int64_t size, ss_frame_info* info) {
+  return Guard(nullptr, [&]() -> int {
+    MKV_CHECK(size >= 0, mkv::kInvalidArgument, "negative frame size");
+    const mkv::FrameView f = mkv::DecodeFrameHeader(frame, static_cast<size_t>(size));
+    info->type = f.type;
+    info->layer = f.layer;
+    info->seq_tag = f.seq_tag;
+    info->payload_offset = static_cast<int64_t>(f.payload_offset);
+    info->payload_bytes = static_cast<int64_t>(f.payload_bytes);
+    info->wire_crc = f.wire_crc;
+    info->ack_status = f.ack_status;
+    info->token_begin = f.token_begin;
+    if (f.type == mkv::kFrameWrite) return FromAddr(nullptr, f.addr, &info->addr);
+    info->addr.n_ranges = 0;
+    return SS_OK;
+  });
+}
+
+int ss_crc32_async(ss_cache* c, const void* data_dev, int64_t n, uint32_t* crc_dev, void* stream) {
+  return Guard(c, [&]() -> int {
+    c->Crc32(data_dev, n, crc_dev, S(stream));
+    return SS_OK;
+  });
+}
+
+int ss_encode_write_frame(ss_cache* c, int64_t seq, int64_t begin, int64_t end, int32_t layer,
+                          uint64_t seq_tag, const ss_addr* dest_addr, uint8_t* frame, int64_t cap,
+                          int64_t* frame_len) {
+  return Guard(c, [&]() -> int {
+    const KVAddr a = ToAddr(dest_addr);
+    *frame_len = static_cast<int64_t>(mkv::WriteHeaderSize(a.ranges.size())) +
+                 (end - begin) * c->dim() * 8 + 4;
+    *frame_len = c->EncodeWriteFrame(seq, begin, end, layer, seq_tag, a, frame, cap, false, nullptr);
+    return SS_OK;
+  });
+}
+
+int ss_encode_write_frame_async(ss_cache* c, int64_t seq, int64_t begin, int64_t end,
+                                int32_t layer, uint64_t seq_tag, const ss_addr* dest_addr,
+                                void* frame_dev, int64_t cap, int64_t* frame_len, void* stream) {
+  return Guard(c, [&]() -> int {
+    const KVAddr a = ToAddr(dest_addr);
+    *frame_len = static_cast<int64_t>(mkv::WriteHeaderSize(a.ranges.size())) +
+                 (end - begin) * c->dim() * 8 + 4;
+    *frame_len = c->EncodeWriteFrame(seq, begin, end, layer, seq_tag, a,
+                                     static_cast<uint8_t*>(frame_dev), cap, true, S(stream));
+    return SS_OK;
+  });
+}
+
+int ss_receive_write_frame(ss_cache* c, const uint8_t* frame, int64_t size, uint8_t* ack_out,
+                           int32_t* apply_status) {
+  return Guard(c, [&]() -> int {
+    c->ReceiveWriteFrame(frame, size, ack_out, apply_status);
     return SS_OK;
   });
 }

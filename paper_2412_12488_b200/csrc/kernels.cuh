@@ -175,4 +175,12 @@ bool launch_prefill_attn(const PoolTensorMap& page_map, const PoolTensorMap& row
                          int page_size, const int32_t* slots, const void* q, int q_pos0, int n_q,
                          int Hq, int Hkv, int D, float scale, void* out, cudaStream_t s);
 
+// CRC-32 (IEEE, reflected) of n device bytes (crc32.cu): one launch, any
+// alignment and length; workspace of crc32_workspace_bytes(n) device bytes
+// (its first word is reset by the launch).  crc32_x8n(n) = x^(8n) mod P.
+size_t crc32_workspace_bytes(int64_t n, int num_sms);
+void launch_crc32(const void* data, int64_t n, uint32_t* out, void* workspace, cudaStream_t s,
+                  int num_sms);
+uint32_t crc32_x8n(uint64_t n);
+
 }  // namespace mkv

@@ -9,6 +9,7 @@ KVCache calls exactly as SURVEY.md §3 maps them:
                   recv_rank, recv_addr)   -> None (returns when acked) SPEC.md:266-273
   api_start_generate(prompt, begin, n)   -> generated tokens
   compute_transfer_plan(m, begin, end)   -> segments
+  submit(GenRequest) / step()            -> continuous batching
 
 remote_send streams each segment the way SPEC.md prescribes: DirectSend
 segments (already cached on the sender) with one fused copy launch over all
@@ -27,8 +28,9 @@ HashModel::Generate.
 from __future__ import annotations
 
 import itertools
-from dataclasses import dataclass
-from typing import Dict, List, Optional, Sequence
+from collections import deque
+from dataclasses import dataclass, field
+from typing import Callable, Dict, List, Optional, Sequence
 
 import numpy as np
 
@@ -98,6 +100,56 @@ class Fabric:
         self.frames += 1
 
 
+class FrameFabric(Fabric):
+    """The reference's wire path (TCP fabric, tcp_fabric.cc:144-168,266-277)
+    between engines of one process: each (send, layer) travels as an encoded
+    write frame (header + payload + CRC-32, byte-identical to
+    EncodeWriteFrame), the receiver runs its transfer-agent step
+    (ReceiveWriteFrame: CRC, ApplyRemoteWrite, ack) and a ChecksumMismatch
+    ack triggers one retransmit (SPEC.md transport, "single retransmit").
+    On the B200 library the sender gathers and checksums the payload on the
+    GPU (ss_encode_write_frame) and the receiver checks it on the GPU.
+    `fault(frame) -> frame` may corrupt frames in flight (first attempt)."""
+
+    def __init__(self, fault: Optional[Callable[[bytes], bytes]] = None):
+        super().__init__()
+        self.fault = fault
+        self.retransmits = 0
+        self.bytes = 0
+
+    def deliver(self, src: "Engine", seq: int, rng: tuple, layer: int, dest: int,
+                dest_addr: KVAddrInfo, tag: int) -> None:
+        frame = src.cache.EncodeWriteFrame(seq, rng, layer, tag, dest_addr)
+        dst = self.engines[dest].cache
+        for attempt in (1, 2):
+            wire = self.fault(frame) if (self.fault is not None and attempt == 1) else frame
+            ack, st = dst.ReceiveWriteFrame(wire)
+            self.bytes += len(wire)
+            status = ack[-1]  # AckStatus, the ack frame's last byte (transport.cc:73)
+            if status == 1 and attempt == 1:  # ChecksumMismatch: retransmit once
+                self.retransmits += 1
+                continue
+            if status != 0:
+                raise SplitserveError(10 if status == 2 else 9,
+                                      f"frame for layer {layer} rejected (ack status {status})")
+            self.frames += 1
+            return
+
+
+@dataclass
+class GenRequest:
+    """SPEC.md engine GenRequest: prompt[:begin] already present in the cache
+    (received or cached); the engine prefills prompt[begin:] and decodes."""
+    request_id: int
+    prompt: List[int]
+    begin: int
+    max_tokens: int
+    seq: int = -1
+    tokens: List[int] = field(default_factory=list)
+    done: bool = False
+    error: Optional[SplitserveError] = None
+
+
 class Engine:
     """One microserving engine: a KVCache plus request bookkeeping."""
 
@@ -109,6 +161,10 @@ class Engine:
         self.fabric = fabric
         self.peers: Dict[int, "Engine"] = {}
         self.awaiting: Dict[tuple, int] = {}  # prompt key -> seq reserved by prep_recv
+        self.waiting: deque = deque()          # admitted, prefill pending (FIFO)
+        self.running: List[GenRequest] = []    # decoding
+        self.steps = 0
+        self.last_batch: List[BatchEntry] = []
         if fabric is not None:
             fabric.register(self)
 
@@ -129,10 +185,13 @@ class Engine:
         return next(Engine._ids) + 1000 * (self.rank + 1)
 
     # -- api_prep_recv ----------------------------------------------
-    def api_prep_recv(self, prompt: Sequence[int], end: int = -1):
+    def api_prep_recv(self, prompt: Sequence[int], end: int = -1, register: bool = True):
+        """register=False: a context transfer (migration), not a generation
+        the next start_generate of this prompt should bind to."""
         seq = self._new_seq()
         r = self.cache.PrepRecv(seq, prompt, end)
-        self.awaiting[self._key(prompt)] = seq
+        if register:
+            self.awaiting[self._key(prompt)] = seq
         return r.match_len, r.addr
 
     # -- api_remote_send (SPEC.md:266-273) -----------------------------------------
@@ -151,22 +210,37 @@ class Engine:
             self.cache.CreateSequence(seq, list(prompt))
         self.cache.EnsureAllocated(seq, e)
         device = self._device_peer(recv_rank)
+        framed = not device and isinstance(self.fabric, FrameFabric)
+        after_layer = []  # (range, addr) streamed as frames after each layer's compute
         for s in plan:
             if s.kind == DIRECT_SEND:
                 sub = recv_addr.Slice(s.begin, s.end)
                 if device:
                     self.cache.direct_send_async(seq, (s.begin, s.end), recv_rank, sub, tag)
+                elif framed:
+                    for layer in range(self.cache.layers):
+                        self.fabric.deliver(self, seq, (s.begin, s.end), layer, recv_rank, sub,
+                                            tag)
                 else:  # GatherRange + frame per layer
                     for layer in range(self.cache.layers):
                         payload = self.cache.GatherRange(seq, (s.begin, s.end), layer)
                         self.fabric.sink(layer, {"dest": recv_rank, "dest_addr": sub,
                                                  "user_tag": tag}, payload)
             elif s.kind == PREFILL_THEN_SEND:
-                self.cache.MarkSend(seq, (s.begin, s.end), recv_rank,
-                                    recv_addr.Slice(s.begin, s.end), tag)
+                sub = recv_addr.Slice(s.begin, s.end)
+                if framed:
+                    after_layer.append(((s.begin, s.end), sub))
+                else:
+                    self.cache.MarkSend(seq, (s.begin, s.end), recv_rank, sub, tag)
         first = min((s.begin for s in plan if s.kind != DIRECT_SEND), default=None)
         if first is not None:  # one forward pass covers PrefillOnly + PrefillThenSend
-            self._forward(seq, prompt, first, e, None if device else self.fabric.sink)
+            hook = None
+            if after_layer:
+                def hook(layer):  # layer-eager frames (§3.6)
+                    for rng, sub in after_layer:
+                        self.fabric.deliver(self, seq, rng, layer, recv_rank, sub, tag)
+            self._forward(seq, prompt, first, e,
+                          None if (device or framed) else self.fabric.sink, hook)
         if device:
             self.cache.synchronize()  # remote_send returns once the writes landed
         self.cache.SetFinished(seq, True)
@@ -175,45 +249,146 @@ class Engine:
 
     # -- api_start_generate -------------------------------------------
     def api_start_generate(self, prompt: Sequence[int], begin: int, max_tokens: int = 1):
-        n = len(prompt)
-        b = resolve_begin(n, begin)
-        self.cache.DrainReceiveCompletions()
-        seq = self.awaiting.pop(self._key(prompt), None)
+        """Admits the request and runs the step loop until it finishes; other
+        admitted requests advance in the same batches."""
+        req = self.submit(GenRequest(next(Engine._ids), list(prompt), begin, max_tokens))
+        while not req.done:
+            self.step()
+        if req.error is not None:
+            raise req.error
+        return req.tokens
+
+    def submit(self, req: GenRequest) -> GenRequest:
+        """Admission (FIFO): resolve begin, bind the sequence prep_recv
+        reserved for this prompt (or fork the longest cached prefix)."""
+        n = len(req.prompt)
+        req.begin = resolve_begin(n, req.begin)
+        if req.begin >= n:
+            raise SplitserveError(16, "InvalidArgument: begin must leave a token to prefill")
+        seq = self.awaiting.pop(self._key(req.prompt), None)
         if seq is None:  # no reservation: plain generation from the local context
             seq = self._new_seq()
-            m, owner = self.cache.MatchPrefixSeq(list(prompt))
-            m = min(m, b)
+            m, owner = self.cache.MatchPrefixSeq(list(req.prompt))
+            m = min(m, req.begin)
             if m > 0:
-                self.cache.ForkSequence(owner, seq, m, list(prompt))
+                self.cache.ForkSequence(owner, seq, m, list(req.prompt))
             else:
-                self.cache.CreateSequence(seq, list(prompt))
-        self.cache.EnsureAllocated(seq, n)
-        x = self._forward(seq, prompt, b, n, None)
-        out = [self.cache.SampleToken(int(x[-1]))]
-        for k in range(1, max_tokens):
-            t = out[-1]
-            self.cache.AppendToken(seq, t)
-            self.cache.EnsureAllocated(seq, n + k)
-            x = self._forward_tokens(seq, [t], n + k - 1, True)
-            out.append(self.cache.SampleToken(int(x[-1])))
-        self.cache.SetFinished(seq, True)
-        self.cache.CommitToTree(seq)
+                self.cache.CreateSequence(seq, list(req.prompt))
+        req.seq = seq
+        self.waiting.append(req)
+        return req
+
+    def step(self) -> List[tuple]:
+        """SPEC.md engine.step: one batch of every waiting prefill (FIFO, no
+        chunking) and every running decode; BeginForward, Attention over all
+        layers, one sampled token per request.  Returns (request_id, token)
+        events.  Requests whose prefix is missing (MissingKV) or that run out
+        of pages are aborted with that status; the rest of the batch runs."""
+        self.cache.DrainReceiveCompletions()
+        batch: List[GenRequest] = []
+        entries: List[BatchEntry] = []
+        toks: List[int] = []
+        while self.waiting:
+            req = self.waiting.popleft()
+            n = len(req.prompt)
+            try:
+                self.cache.EnsureAllocated(req.seq, n)
+            except SplitserveError as ex:
+                self._abort(req, ex)
+                continue
+            batch.append(req)
+            entries.append(BatchEntry(req.seq, (req.begin, n), False))
+            toks.extend(int(t) for t in req.prompt[req.begin:n])
+        for req in self.running:
+            pos = len(req.prompt) + len(req.tokens) - 1
+            try:
+                self.cache.AppendToken(req.seq, req.tokens[-1])
+                self.cache.EnsureAllocated(req.seq, pos + 1)
+            except SplitserveError as ex:
+                self._abort(req, ex)
+                continue
+            batch.append(req)
+            entries.append(BatchEntry(req.seq, (pos, pos + 1), True))
+            toks.append(req.tokens[-1])
+        self.running = [r for r in self.running if not r.done]
+        if not batch:
+            return []
+        try:
+            plan = self.cache.BeginForward(entries)
+        except SplitserveError:
+            # Find the entries that cannot run (e.g. MissingKV: start_generate
+            # before the transfer completed), abort them, retry the rest.
+            keep_b, keep_e, keep_t, off = [], [], [], 0
+            for req, ent in zip(batch, entries):
+                k = ent.range[1] - ent.range[0]
+                try:
+                    p1 = self.cache.BeginForward([ent])
+                    if hasattr(p1, "close"):
+                        p1.close()
+                    keep_b.append(req)
+                    keep_e.append(ent)
+                    keep_t.extend(toks[off:off + k])
+                except SplitserveError as ex:
+                    self._abort(req, ex)
+                off += k
+            batch, entries, toks = keep_b, keep_e, keep_t
+            self.running = [r for r in self.running if not r.done]
+            if not batch:
+                return []
+            plan = self.cache.BeginForward(entries)
+        x = self._embed(entries, toks)
+        for layer in range(self.cache.layers):
+            x = self.cache.Attention(layer, plan, x)
+        if hasattr(plan, "close"):
+            plan.close()
+        self.last_batch = entries
+        self.steps += 1
+        events, off = [], 0
+        for req, ent in zip(batch, entries):
+            off += ent.range[1] - ent.range[0]
+            tok = self.cache.SampleToken(int(x[off - 1]))
+            req.tokens.append(tok)
+            events.append((req.request_id, tok))
+            if len(req.tokens) >= req.max_tokens:
+                self._finish(req)
+            elif req not in self.running:
+                self.running.append(req)
+        self.running = [r for r in self.running if not r.done]
+        return events
+
+    def _embed(self, entries, toks) -> np.ndarray:
+        out, i = np.empty(len(toks), dtype=np.uint64), 0
+        for e in entries:
+            for pos in range(e.range[0], e.range[1]):
+                out[i] = self.cache.Embed(toks[i], pos)
+                i += 1
         return out
 
+    def _finish(self, req: GenRequest) -> None:
+        req.done = True
+        self.cache.SetFinished(req.seq, True)
+        self.cache.CommitToTree(req.seq)
+
+    def _abort(self, req: GenRequest, ex: SplitserveError) -> None:
+        req.done = True
+        req.error = ex
+
+    def idle(self) -> bool:
+        return not self.waiting and not self.running
+
     # -- forward passes (SPEC.md:284-290 `step`) --------------------------------------------
-    def _forward(self, seq, prompt, begin, end, sink):
+    def _forward(self, seq, prompt, begin, end, sink, after_layer=None):
         return self._run(seq, (begin, end), [int(prompt[i]) for i in range(begin, end)], False,
-                         sink)
+                         sink, after_layer)
 
-    def _forward_tokens(self, seq, toks, pos, is_decode):
-        return self._run(seq, (pos, pos + len(toks)), toks, is_decode, None)
-
-    def _run(self, seq, rng, toks, is_decode, sink):
+    def _run(self, seq, rng, toks, is_decode, sink, after_layer=None):
         plan = self.cache.BeginForward([BatchEntry(seq, rng, is_decode)])
         x = np.array([self.cache.Embed(t, rng[0] + i) for i, t in enumerate(toks)],
                      dtype=np.uint64)
         for layer in range(self.cache.layers):
             x = self.cache.Attention(layer, plan, x, sink)
+            if after_layer is not None:
+                after_layer(layer)
         if hasattr(plan, "close"):
             plan.close()
         return x

@@ -131,6 +131,12 @@ class IpcHandle(C.Structure):
     _fields_ = [("bytes", C.c_uint8 * 512)]
 
 
+class _FrameInfo(C.Structure):  # ss_frame_info (microkv.h)
+    _fields_ = [("type", C.c_int32), ("layer", C.c_int32), ("seq_tag", C.c_uint64),
+                ("addr", _Addr), ("payload_offset", C.c_int64), ("payload_bytes", C.c_int64),
+                ("wire_crc", C.c_uint32), ("ack_status", C.c_int32), ("token_begin", C.c_int64)]
+
+
 _SINK = C.CFUNCTYPE(None, C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.c_int64, C.c_int32,
                     C.POINTER(_Addr), C.c_uint64, C.POINTER(C.c_uint64), C.c_int64)
 
@@ -222,6 +228,21 @@ _SIGNATURES = {
     "ss_copy_counters": (C.c_int, [_vp, _i64p, _i64p]),
     "ss_kernel_launches": (C.c_int64, [_vp]),
     "ss_synchronize": (C.c_int, [_vp]),
+    "ss_addr_encode": (C.c_int, [C.POINTER(_Addr), _vp, C.c_int64, _i64p]),
+    "ss_addr_decode": (C.c_int, [_vp, C.c_int64, _i64p, C.POINTER(_Addr)]),
+    "ss_addr_to_json": (C.c_int, [C.POINTER(_Addr), C.c_char_p, C.c_int64, _i64p]),
+    "ss_addr_from_json": (C.c_int, [C.c_char_p, C.c_int64, C.POINTER(_Addr)]),
+    "ss_frame_write_header_size": (C.c_int64, [C.c_int64]),
+    "ss_frame_encode_ack": (C.c_int, [C.c_uint64, C.c_int32, C.c_int64, C.c_int32, _vp,
+                                      C.c_int64, _i64p]),
+    "ss_frame_decode": (C.c_int, [_vp, C.c_int64, C.POINTER(_FrameInfo)]),
+    "ss_crc32_async": (C.c_int, [_vp, _vp, C.c_int64, _vp, _vp]),
+    "ss_encode_write_frame": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, C.c_int32,
+                                        C.c_uint64, C.POINTER(_Addr), _vp, C.c_int64, _i64p]),
+    "ss_encode_write_frame_async": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, C.c_int32,
+                                              C.c_uint64, C.POINTER(_Addr), _vp, C.c_int64,
+                                              _i64p, _vp]),
+    "ss_receive_write_frame": (C.c_int, [_vp, _vp, C.c_int64, _vp, _i32p]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
@@ -353,20 +374,96 @@ class KVAddrInfo:
             raise SplitserveError(st, "KVAddrInfo.Slice")
         return KVAddrInfo._from_c(out)
 
-    def ToJson(self) -> str:  # kv_addr.cc:53-58 (nlohmann dump: sorted keys, no spaces)
-        return json.dumps({"ranges": [list(r) for r in self.ranges],
-                           "token_begin": self.token_begin,
-                           "token_count": self.token_count}, separators=(",", ":"))
+    def ToJson(self, lib: Optional[C.CDLL] = None) -> str:  # kv_addr.cc:53-58
+        lib = lib or load_library()
+        a, keep = self._c()
+        n = C.c_int64(0)
+        buf = C.create_string_buffer(64 + 40 * len(self._arr))
+        st = lib.ss_addr_to_json(C.byref(a), buf, len(buf), C.byref(n))
+        if st != SS_OK:
+            raise SplitserveError(st, "KVAddrInfo.ToJson")
+        return buf.raw[:n.value].decode()
 
     @staticmethod
-    def FromJson(text: str) -> "KVAddrInfo":  # kv_addr.cc:60-70
-        j = json.loads(text)
-        return KVAddrInfo([tuple(r) for r in j["ranges"]], j["token_begin"], j["token_count"])
+    def FromJson(text: str, lib: Optional[C.CDLL] = None) -> "KVAddrInfo":  # kv_addr.cc:60-70
+        lib = lib or load_library()
+        raw = text.encode()
+        return KVAddrInfo._decoded(lambda out: lib.ss_addr_from_json(raw, len(raw), out),
+                                   max(1, len(raw) // 6), "KVAddrInfo.FromJson")
+
+    def EncodeTo(self, lib: Optional[C.CDLL] = None) -> bytes:  # kv_addr.cc:90-99
+        lib = lib or load_library()
+        a, keep = self._c()
+        n = C.c_int64(0)
+        buf = (C.c_uint8 * (20 + 8 * len(self._arr)))()
+        st = lib.ss_addr_encode(C.byref(a), buf, len(buf), C.byref(n))
+        if st != SS_OK:
+            raise SplitserveError(st, "KVAddrInfo.EncodeTo")
+        return bytes(buf)[:n.value]
+
+    @staticmethod
+    def DecodeFrom(data: bytes, pos: int = 0,
+                   lib: Optional[C.CDLL] = None) -> tuple["KVAddrInfo", int]:  # kv_addr.cc:101-118
+        lib = lib or load_library()
+        p = C.c_int64(pos)
+        addr = KVAddrInfo._decoded(lambda out: lib.ss_addr_decode(data, len(data), C.byref(p), out),
+                                   max(1, (len(data) - pos) // 8), "KVAddrInfo.DecodeFrom")
+        return addr, p.value
+
+    @staticmethod
+    def _decoded(call, cap: int, what: str) -> "KVAddrInfo":
+        arr = (_SlotRange * cap)()
+        out = _Addr(0, 0, 0, arr, cap)
+        st = call(C.byref(out))
+        if st == SS_ERR_BUFFER_TOO_SMALL:
+            arr = (_SlotRange * int(out.n_ranges))()
+            out = _Addr(0, 0, 0, arr, int(out.n_ranges))
+            st = call(C.byref(out))
+        if st != SS_OK:
+            raise SplitserveError(st, what)
+        return KVAddrInfo._from_c(out)
 
     def slots(self, page_size: int) -> np.ndarray:
         """Flat slot indices (page * page_size + slot) in token order."""
         out = [p * page_size + b + k for (p, b, c) in self.ranges for k in range(c)]
         return np.asarray(out, dtype=np.int64)
+
+
+def frame_write_header_size(n_ranges: int, lib: Optional[C.CDLL] = None) -> int:
+    """Bytes of a write frame before its payload (transport.h:6-12)."""
+    return int((lib or load_library()).ss_frame_write_header_size(n_ranges))
+
+
+def EncodeAckFrame(seq_tag: int, layer: int, token_begin: int, status: int,
+                   lib: Optional[C.CDLL] = None) -> bytes:  # transport.cc:64-74
+    lib = lib or load_library()
+    out = (C.c_uint8 * 26)()
+    n = C.c_int64(0)
+    st = lib.ss_frame_encode_ack(seq_tag, layer, token_begin, status, out, 26, C.byref(n))
+    if st != SS_OK:
+        raise SplitserveError(st, "EncodeAckFrame")
+    return bytes(out)[:n.value]
+
+
+def DecodeFrame(frame: bytes, lib: Optional[C.CDLL] = None) -> dict:
+    """DecodeFrame (transport.cc:76-107) without the payload copy and CRC:
+    type, seq_tag, layer and, for writes, addr / payload_offset /
+    payload_bytes / wire_crc; for acks token_begin / status."""
+    lib = lib or load_library()
+    cap = max(1, len(frame) // 8)
+    arr = (_SlotRange * cap)()
+    info = _FrameInfo()
+    info.addr = _Addr(0, 0, 0, arr, cap)
+    st = lib.ss_frame_decode(frame, len(frame), C.byref(info))
+    if st != SS_OK:
+        raise SplitserveError(st, "DecodeFrame")
+    out = {"type": int(info.type), "seq_tag": int(info.seq_tag), "layer": int(info.layer)}
+    if info.type == 0:
+        out.update(addr=KVAddrInfo._from_c(info.addr), payload_offset=int(info.payload_offset),
+                   payload_bytes=int(info.payload_bytes), wire_crc=int(info.wire_crc))
+    else:
+        out.update(token_begin=int(info.token_begin), status=int(info.ack_status))
+    return out
 
 
 @dataclass
@@ -793,6 +890,67 @@ class KVCache:
                            stream: int = 0) -> None:
         self._check(self._lib.ss_gather_range_async(self._h, seq, range[0], range[1], layer,
                                                     C.c_void_p(out_ptr), C.c_void_p(stream)))
+
+    # ---- wire formats (transport.h:6-12): frames for the cross-node path ----
+    def crc32_async(self, data_ptr: int, n_bytes: int, crc_ptr: int, stream: int = 0) -> None:
+        """Crc32 (transport.cc:14-28) of device bytes, written as uint32 at crc_ptr."""
+        self._check(self._lib.ss_crc32_async(self._h, C.c_void_p(data_ptr), n_bytes,
+                                             C.c_void_p(crc_ptr), C.c_void_p(stream)))
+
+    def EncodeWriteFrame(self, seq: int, range: tuple, layer: int, seq_tag: int,
+                         dest_addr: KVAddrInfo) -> bytes:
+        """EncodeWriteFrame(WriteFrame{seq_tag, layer, dest_addr,
+        GatherRange(seq, range, layer)}) (transport.cc:46-62): the frame a
+        socket sends, payload gathered and checksummed on the GPU."""
+        a, keep = dest_addr._c()
+        n = C.c_int64(0)
+        need = self._lib.ss_frame_write_header_size(len(dest_addr.array)) + \
+            (range[1] - range[0]) * self.dim * 8 + 4
+        buf = (C.c_uint8 * max(1, need))()
+        self._check(self._lib.ss_encode_write_frame(self._h, seq, range[0], range[1], layer,
+                                                    seq_tag, C.byref(a), buf, len(buf),
+                                                    C.byref(n)))
+        return bytes(buf)[:n.value]
+
+    def encode_write_frame_into(self, seq: int, range: tuple, layer: int, seq_tag: int,
+                                dest_addr: KVAddrInfo, out_ptr: int, cap: int) -> int:
+        """EncodeWriteFrame into caller host memory (e.g. a pinned, reused
+        socket buffer); returns the frame length."""
+        a, keep = dest_addr._c()
+        n = C.c_int64(0)
+        self._check(self._lib.ss_encode_write_frame(self._h, seq, range[0], range[1], layer,
+                                                    seq_tag, C.byref(a), C.c_void_p(out_ptr),
+                                                    cap, C.byref(n)))
+        return n.value
+
+    def receive_write_frame_from(self, frame_ptr: int, size: int) -> tuple[bytes, int]:
+        """ReceiveWriteFrame of a frame in caller host memory."""
+        ack = (C.c_uint8 * 26)()
+        st = C.c_int32(-1)
+        self._check(self._lib.ss_receive_write_frame(self._h, C.c_void_p(frame_ptr), size, ack,
+                                                     C.byref(st)))
+        return bytes(ack), st.value
+
+    def encode_write_frame_async(self, seq: int, range: tuple, layer: int, seq_tag: int,
+                                 dest_addr: KVAddrInfo, frame_ptr: int, cap: int,
+                                 stream: int = 0) -> int:
+        """Device-memory frame; frame_ptr + header size must be 32-byte aligned.
+        Returns the frame length."""
+        a, keep = dest_addr._c()
+        n = C.c_int64(0)
+        self._check(self._lib.ss_encode_write_frame_async(
+            self._h, seq, range[0], range[1], layer, seq_tag, C.byref(a), C.c_void_p(frame_ptr),
+            cap, C.byref(n), C.c_void_p(stream)))
+        return n.value
+
+    def ReceiveWriteFrame(self, frame: bytes) -> tuple[bytes, int]:
+        """The transfer agent's step for one write frame (tcp_fabric.cc:144-168):
+        returns (ack frame bytes, apply status or -1 when the CRC failed)."""
+        ack = (C.c_uint8 * 26)()
+        st = C.c_int32(-1)
+        self._check(self._lib.ss_receive_write_frame(self._h, frame, len(frame), ack,
+                                                     C.byref(st)))
+        return bytes(ack), st.value
 
     def apply_remote_write_async(self, addr: KVAddrInfo, layer: int, payload_ptr: int,
                                  n_words: int, tag: int, stream: int = 0) -> ApplyStatus:

@@ -107,7 +107,61 @@ def scripts():
     return out
 
 
+def frames():
+    """Write frames the reference encodes (EncodeWriteFrame over
+    GatherRange, transport.cc:46-62) for a 1P1D transfer into a forked
+    receiver (fork-relative pages -> several ranges), the acks its TCP
+    inbound step returns (tcp_fabric.cc:144-168), and CRC-32 check values."""
+    import ctypes as C
+
+    from flows import prefill
+
+    L, W, P = 4, 8, 16
+    p = prompt(40, seed=3)
+    D = KVCache(num_pages=16, page_size=P, layers=L, dim=W, rank=1, lib=REF)
+    D.CreateSequence(1, p[:5])
+    D.EnsureAllocated(1, 5)
+    prefill(D, 1, p, 0, 5)
+    D.CommitToTree(1)
+    r = D.PrepRecv(2, p, -1)
+    m, e = r.match_len, r.match_len + r.addr.token_count
+    Pe = KVCache(num_pages=16, page_size=P, layers=L, dim=W, rank=0, lib=REF)
+    Pe.CreateSequence(20, p)
+    Pe.EnsureAllocated(20, e)
+    prefill(Pe, 20, p, 0, e)
+    tag = 0x1234
+    out = {"config": {"layers": L, "dim": W, "page_size": P, "num_pages": 16},
+           "prompt": p, "match_len": m, "end": e, "tag": tag, "addr_json": r.addr.ToJson(),
+           "frames": [], "acks": []}
+    for layer in range(L):
+        f = Pe.EncodeWriteFrame(20, (m, e), layer, tag, r.addr)
+        ack, st = D.ReceiveWriteFrame(f)
+        crc = int.from_bytes(f[-4:], "little")
+        out["frames"].append({"layer": layer, "hex": f.hex(), "crc": crc, "ack_hex": ack.hex(),
+                              "apply_status": st})
+    bad = bytearray(bytes.fromhex(out["frames"][0]["hex"]))
+    flip = 41 + 8 * len(r.addr.ranges) + 10  # inside the payload
+    bad[flip] ^= 0x40
+    ack, st = D.ReceiveWriteFrame(bytes(bad))
+    out["corrupt_frame0"] = {"flip_byte": flip, "ack_hex": ack.hex(), "apply_status": st}
+    out["completions"] = D.DrainReceiveCompletions()
+    from paper_2412_12488_b200.kvcache import EncodeAckFrame, load_library
+    lib = load_library(REF)
+    for args in ((0x1234, 2, 5, 0), (7, 79, 6553, 1), (1, 0, 0, 2)):
+        out["acks"].append({"args": list(args), "hex": EncodeAckFrame(*args, lib=lib).hex()})
+    lib.ssref_crc32.restype = C.c_uint32
+    lib.ssref_crc32.argtypes = [C.c_char_p, C.c_int64]
+    kat = {"123456789": lib.ssref_crc32(b"123456789", 9)}
+    rng = np.random.Generator(np.random.MT19937(11))
+    for n in (0, 1, 31, 32, 33, 1000, 4096, 65549):
+        buf = rng.integers(0, 256, n, dtype=np.uint8).tobytes()
+        kat[f"mt19937_11_{n}"] = lib.ssref_crc32(buf, n)
+    out["crc32"] = kat
+    return out
+
+
 if __name__ == "__main__":
+    (OUT / "frames.json").write_text(json.dumps(frames(), indent=1))
     (OUT / "tiny_1p1d.json").write_text(json.dumps(tiny_1p1d(), indent=1))
     (OUT / "anchors.json").write_text(json.dumps(anchors(), indent=1))
     (OUT / "scripts.json").write_text(json.dumps(scripts()))
