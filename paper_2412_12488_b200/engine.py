@@ -292,6 +292,11 @@ class Engine:
             req = self.waiting.popleft()
             n = len(req.prompt)
             try:
+                # BeginForward's precondition (kv_cache.cc:255-258), checked per
+                # request so one early start_generate cannot fail the batch.
+                if self.cache.Committed(req.seq) < req.begin:
+                    raise SplitserveError(6, f"MissingKV: positions before {req.begin} "
+                                             "are not all present")
                 self.cache.EnsureAllocated(req.seq, n)
             except SplitserveError as ex:
                 self._abort(req, ex)
@@ -313,29 +318,7 @@ class Engine:
         self.running = [r for r in self.running if not r.done]
         if not batch:
             return []
-        try:
-            plan = self.cache.BeginForward(entries)
-        except SplitserveError:
-            # Find the entries that cannot run (e.g. MissingKV: start_generate
-            # before the transfer completed), abort them, retry the rest.
-            keep_b, keep_e, keep_t, off = [], [], [], 0
-            for req, ent in zip(batch, entries):
-                k = ent.range[1] - ent.range[0]
-                try:
-                    p1 = self.cache.BeginForward([ent])
-                    if hasattr(p1, "close"):
-                        p1.close()
-                    keep_b.append(req)
-                    keep_e.append(ent)
-                    keep_t.extend(toks[off:off + k])
-                except SplitserveError as ex:
-                    self._abort(req, ex)
-                off += k
-            batch, entries, toks = keep_b, keep_e, keep_t
-            self.running = [r for r in self.running if not r.done]
-            if not batch:
-                return []
-            plan = self.cache.BeginForward(entries)
+        plan = self.cache.BeginForward(entries)
         x = self._embed(entries, toks)
         for layer in range(self.cache.layers):
             x = self.cache.Attention(layer, plan, x)

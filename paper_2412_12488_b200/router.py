@@ -187,7 +187,7 @@ class Router:
         load.update(rank for _, rank in self.window)
         hot, cold = max(self.ranks, key=lambda r: (load[r], -r)), min(self.ranks,
                                                                        key=lambda r: (load[r], r))
-        if load[hot] < self.params["threshold"] * max(1, load[cold]) or hot == cold:
+        if load[hot] <= self.params["threshold"] * max(1, load[cold]) or hot == cold:
             return
         demand = Counter(c for c, r in self.window if r == hot)
         for category, _ in demand.most_common():
