@@ -61,6 +61,7 @@ def build(verbose: bool = False) -> Path:
         if _stale(obj, [CSRC / src] + headers):
             _run([nvcc, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC",
                   "-Xptxas", "-v" if verbose else "-O3", f"-I{INCLUDE}",
+                  *os.environ.get("MKV_NVCC_EXTRA", "").split(),
                   "-c", str(CSRC / src), "-o", str(obj)])
     if _stale(LIB, objs):
         _run([nvcc, "-shared", *ARCH, "-cudart", "static", "-o", str(LIB),

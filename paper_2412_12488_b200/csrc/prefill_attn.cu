@@ -10,23 +10,30 @@
 // CTA = one KV head x 32 query tokens, as two M=128 query tiles (16 tokens x
 // the 8 query heads sharing the KV head), warp-specialised:
 //
-//   warp 8      producer: per 128-key tile, one TMA box per (page, 64-dim
+//   warp 8      producer: per 64-key tile, one TMA box per (page, 64-dim
 //               half) of K and of V straight from the paged pool (a page's P
 //               rows of one head are a 2-D box of the pool's tensor map), into
-//               SWIZZLE_128B shared tiles; 2 stages each for K and V.
-//   warp 9      MMA issuer (one thread): S_i = Q_i K^T into TMEM, O_i += P_i V
-//               with P_i read from TMEM (A operand in tensor memory), in the
-//               order S0(j) PV1(j-1) S1(j) PV0(j) so each softmax warpgroup has
-//               two MMA slots of time while the tensor core stays busy.
+//               SWIZZLE_128B shared tiles; a 4-stage ring each for K and V.
+//   warp 9      MMA issuer (one elected lane): S_i = Q_i K^T into TMEM,
+//               O_i += P_i V with P_i read from TMEM (A operand in tensor
+//               memory).  Per KV tile j and query tile i: PV_i(j) as soon as
+//               P_i(j) is ready, then S_i(j+2) into the S slot P_i(j) frees,
+//               so S_i(j+1) is always computed while softmax_i(j) runs and
+//               the two query tiles never wait on each other.
 //   warps 0-3   softmax of query tile 0, thread = TMEM lane = row;
 //   warps 4-7   softmax of query tile 1.  Each reads its S row from TMEM,
 //               masks (causal), keeps a running max (O rescaled in TMEM only
 //               when the max grows by more than 2^8 — exact, since l and O
-//               share the stale max), writes P = exp2(.) as packed bf16 over
-//               the S columns, and signals the MMA warp.
+//               share the stale max; warps with nothing to rescale do not
+//               wait for the previous PV), writes P = exp2(.) as packed bf16
+//               over the S columns (scale/shift and row sums as f32x2 pairs),
+//               and signals the MMA warp.  S-full and P-full barriers are per
+//               (query tile, S slot), so a warp running one tile ahead of its
+//               warpgroup cannot land in the wrong phase.
 //
-// TMEM (512 columns): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512); P_i
-// aliases the first 64 columns of S_i.
+// TMEM (512 columns): query tile i owns [128 i, 128 i + 128) as two 64-column
+// S slots (KV tile j uses slot j & 1; P_i(j) overwrites the slot's first 32
+// columns), O_i at [256 + 128 i, 384 + 128 i).
 //
 // Shared-memory operands use the UMMA SWIZZLE_128B canonical layout (8-row x
 // 128-byte atoms, 16-byte chunks XOR row, 1024-byte aligned); a 128-element
@@ -79,10 +86,16 @@ enum : int {
   kBarVFull = kBarKFull + kStages,
   kBarKEmpty = kBarVFull + kStages,  // +stage: MMAs reading it retired
   kBarVEmpty = kBarKEmpty + kStages,
-  kBarSFull = kBarVEmpty + kStages,  // +tile: S_i(j) ready in TMEM
-  kBarPFull = kBarSFull + 2,         // +tile: P_i(j) written, O_i rescaled (count 128)
-  kBarPVDone = kBarPFull + 2,        // +tile: PV_i(j) retired (O_i stable)
-  kBarCount = kBarPVDone + 2,
+  kBarSFull = kBarVEmpty + kStages,  // +2*tile+slot: S_i(j) ready in TMEM slot j&1
+                                     // (per slot, so S_i(j+1) landing early cannot
+                                     // push a barrier two phases past its waiter)
+  kBarPFull = kBarSFull + 4,         // +2*tile+slot: P_i(j) written, O_i rescaled (count
+                                     // 128).  Per slot: a warp that skips the O wait may
+                                     // run one tile ahead of its warpgroup, and its
+                                     // P_i(j+1) arrival must not land in phase j.
+  kBarPVDone = kBarPFull + 4,        // +tile: PV_i(j) retired (O_i stable)
+  kBarODone = kBarPVDone + 2,        // +tile: the last PV_i retired (single phase)
+  kBarCount = kBarODone + 2,
 };
 static_assert(kBarCount * 8 + 8 <= 256, "barrier area");
 
@@ -298,6 +311,47 @@ __device__ __forceinline__ float ex2_poly(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
+// Packed f32x2 arithmetic (FFMA2 / FADD2 on sm_100): two lanes per instruction.
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.ftz.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.ftz.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// ex2_poly for a pair, the polynomial in packed f32x2 arithmetic.
+__device__ __forceinline__ void ex2_poly2(float x0, float x1, float& y0, float& y1) {
+  const uint64_t x = f2pack(fmaxf(x0, -125.f), fmaxf(x1, -125.f));
+  const uint64_t K = f2pack(12582912.f, 12582912.f);
+  const uint64_t t = fadd2(x, K);
+  const uint64_t f = fsub2(x, fsub2(t, K));
+  uint64_t p = ffma2(f, f2pack(0.0555041087f, 0.0555041087f), f2pack(0.240226507f, 0.240226507f));
+  p = ffma2(p, f, f2pack(0.693147181f, 0.693147181f));
+  p = ffma2(p, f, f2pack(1.f, 1.f));
+  float p0, p1, t0, t1;
+  f2unpack(p, p0, p1);
+  f2unpack(t, t0, t1);
+  y0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+  y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -346,9 +400,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(bar(kBarVEmpty + s), 1);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(bar(kBarSFull + i), 1);
-      mbar_init(bar(kBarPFull + i), kRows);
+      mbar_init(bar(kBarSFull + 2 * i), 1);
+      mbar_init(bar(kBarSFull + 2 * i + 1), 1);
+      mbar_init(bar(kBarPFull + 2 * i), kRows);
+      mbar_init(bar(kBarPFull + 2 * i + 1), kRows);
       mbar_init(bar(kBarPVDone + i), 1);
+      mbar_init(bar(kBarODone + i), 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&pool_map))
@@ -444,10 +501,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t bo = ((k >> 2) * kKvAtom + (k & 3) * 32) >> 4;
         mma_ss_elect(tS(i, j), a0 + ao, b0 + bo, kHi, kIdescS, k > 0 ? 1u : 0u);
       }
-      commit_elect(bar(kBarSFull + i));
+      commit_elect(bar(kBarSFull + 2 * i + (j & 1)));
     };
     auto issue_pv = [&](int i, int j) {
-      mbar_wait(bar(kBarPFull + i), j & 1);
+      mbar_wait(bar(kBarPFull + 2 * i + (j & 1)), (j >> 1) & 1);
       fence_after();
       const uint32_t b0 = v_lo + (((j % kStages) * kKvTile) >> 4);
 #pragma unroll
@@ -473,24 +530,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
     };
     mbar_wait(bar(kBarQ), 0);
-    for (int j = 0; j <= n_tiles; ++j) {
-      if (j < n_tiles) {
-        const int s = j % kStages;
-        mbar_wait(bar(kBarKFull + s), (j / kStages) & 1);
-        fence_after();
-        issue_s(0, j);
-        issue_s(1, j);
-        commit_elect(bar(kBarKEmpty + s));
+    // Prologue: S of KV tiles 0 and 1 for both query tiles.
+    for (int j = 0; j < 2 && j < n_tiles; ++j) {
+      const int s = j % kStages;
+      mbar_wait(bar(kBarKFull + s), (j / kStages) & 1);
+      fence_after();
+      issue_s(0, j);
+      issue_s(1, j);
+      commit_elect(bar(kBarKEmpty + s));
+    }
+    // Steady state, per query tile: PV_i(j) as soon as P_i(j) is ready, then
+    // S_i(j+2) into the slot P_i(j) frees (tcgen05 MMAs of one thread run in
+    // order), so one tile's softmax never waits on the other's.
+    for (int j = 0; j < n_tiles; ++j) {
+      const int sv = j % kStages;
+      mbar_wait(bar(kBarVFull + sv), (j / kStages) & 1);
+      if (j == n_tiles - 1) zero_tail(j);
+      const bool next = j + 2 < n_tiles;
+      const int sk = (j + 2) % kStages;
+      if (next) mbar_wait(bar(kBarKFull + sk), ((j + 2) / kStages) & 1);
+      fence_after();
+      for (int i = 0; i < kQTiles; ++i) {
+        issue_pv(i, j);
+        if (j == n_tiles - 1) commit_elect(bar(kBarODone + i));
+        if (next) issue_s(i, j + 2);
       }
-      if (j > 0) {
-        const int jp = j - 1, sp = jp % kStages;
-        mbar_wait(bar(kBarVFull + sp), (jp / kStages) & 1);
-        if (jp == n_tiles - 1) zero_tail(jp);
-        fence_after();
-        issue_pv(0, jp);
-        issue_pv(1, jp);
-        commit_elect(bar(kBarVEmpty + sp));
-      }
+      commit_elect(bar(kBarVEmpty + sv));
+      if (next) commit_elect(bar(kBarKEmpty + sk));
     }
   } else {
     // ---------------- softmax warpgroups ----------------
@@ -518,7 +584,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     float m = -INFINITY, l = 0.f;  // running max (scaled log2 domain) and sum
     for (int j = 0; j < n_tiles; ++j) {
       const uint32_t tS = tSi + (j & 1) * 64;
-      mbar_wait(bar(kBarSFull + i), j & 1);
+      mbar_wait(bar(kBarSFull + 2 * i + (j & 1)), (j >> 1) & 1);
       fence_after();
       uint32_t sr[kKeys];
 #pragma unroll
@@ -535,60 +601,83 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < kKeys; ++c)
           sr[c] = c > lim ? __float_as_uint(-INFINITY) : sr[c];
       }
-      float rmax = -INFINITY;  // raw (unscaled) max
+      // Row max over 64 columns: four independent 3-input chains.
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int c = 0; c < kKeys; c += 2)
-        rmax = fmaxf(rmax, fmaxf(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])));
+      for (int c = 0; c < kKeys; c += 8) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          mx[k] = fmaxf(mx[k], fmaxf(__uint_as_float(sr[c + 2 * k]), __uint_as_float(sr[c + 2 * k + 1])));
+      }
+      const float rmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));  // raw (unscaled)
       const float tmax = rmax * sl2;
       // Keep the stale max unless this tile exceeds it by > 8 (p <= 2^8 then).
       const bool bump = tmax > m + 8.f;
       const float m_new = bump ? tmax : m;
       const float alpha = (bump && m != -INFINITY) ? ex2_mufu(m - m_new) : 1.f;
       const float neg_m = m_new == -INFINITY ? 0.f : -m_new;
-      float psum = 0.f;
       // P = 2^(s*scale - m) packed in place (pair c/2 overwrites S[c/2],
-      // already consumed).  In unmasked tiles every 4th exponential runs on
+      // already consumed).  Scale/shift and the row sum run as f32x2 pairs;
+      // in unmasked tiles every PF_POLY_EVERY-th pair of exponentials runs on
       // the FMA pipe (polynomial) to relieve the MUFU unit.
+#ifndef PF_POLY_EVERY
+#define PF_POLY_EVERY 0  // measured best: the softmax is issue-bound, not MUFU-bound
+#endif
+      const uint64_t sc2 = f2pack(sl2, sl2), nm2 = f2pack(neg_m, neg_m);
+      uint64_t acc[2] = {0ull, 0ull};
       auto make_p = [&](auto poly) {
 #pragma unroll
         for (int c = 0; c < kKeys; c += 2) {
-          const float x0 = fmaf(__uint_as_float(sr[c]), sl2, neg_m);
-          const float x1 = fmaf(__uint_as_float(sr[c + 1]), sl2, neg_m);
-          const float p0 = ex2_mufu(x0);
-          const float p1 = (decltype(poly)::value && (c & 2)) ? ex2_poly(x1) : ex2_mufu(x1);
-          psum += p0 + p1;
+          float x0, x1, p0, p1;
+          f2unpack(ffma2(f2pack(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), sc2, nm2),
+                   x0, x1);
+          if (decltype(poly)::value && PF_POLY_EVERY > 0 &&
+              ((c >> 1) % (PF_POLY_EVERY > 0 ? PF_POLY_EVERY : 1)) == PF_POLY_EVERY - 1) {
+            ex2_poly2(x0, x1, p0, p1);
+          } else {
+            p0 = ex2_mufu(x0);
+            p1 = ex2_mufu(x1);
+          }
+          acc[(c >> 1) & 1] = fadd2(acc[(c >> 1) & 1], f2pack(p0, p1));
           sr[c / 2] = pack_bf16(p0, p1);
         }
       };
       if (need_mask) make_p(std::false_type{});
       else make_p(std::true_type{});
+      float ps[4];
+      f2unpack(acc[0], ps[0], ps[1]);
+      f2unpack(acc[1], ps[2], ps[3]);
+      const float psum = (ps[0] + ps[1]) + (ps[2] + ps[3]);
 #pragma unroll
       for (int c0 = 0; c0 < kKeys / 2; c0 += 16) tmem_st16_nowait(tS + c0, sr + c0);
-      // O_i must be stable (PV_i(j-1) retired) before it is rescaled for tile j.
-      if (j > 0) {
+      // O_i must be stable (PV_i(j-1) retired) before it is rescaled for
+      // tile j; warps with nothing to rescale skip the wait (parity waits
+      // stay exact: PV_i(j) needs this warpgroup's P_i(j), so the barrier is
+      // at most one phase ahead of any later wait).
+      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
         mbar_wait(bar(kBarPVDone + i), (j - 1) & 1);
         fence_after();
-        if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll
-          for (int c0 = 0; c0 < kD; c0 += 32) {
-            uint32_t o[32];
-            tmem_ld16_nowait(tO + c0, o);
-            tmem_ld16_nowait(tO + c0 + 16, o + 16);
-            tmem_wait_ld();
+        for (int c0 = 0; c0 < kD; c0 += 32) {
+          uint32_t o[32];
+          tmem_ld16_nowait(tO + c0, o);
+          tmem_ld16_nowait(tO + c0 + 16, o + 16);
+          tmem_wait_ld();
 #pragma unroll
-            for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
-            tmem_st16_nowait(tO + c0, o);
-            tmem_st16_nowait(tO + c0 + 16, o + 16);
-          }
+          for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
+          tmem_st16_nowait(tO + c0, o);
+          tmem_st16_nowait(tO + c0 + 16, o + 16);
         }
       }
       tmem_wait_st();
       fence_before();
-      mbar_arrive(bar(kBarPFull + i));
+      mbar_arrive(bar(kBarPFull + 2 * i + (j & 1)));
       l = l * alpha + psum;
       m = m_new;
     }
-    mbar_wait(bar(kBarPVDone + i), (n_tiles - 1) & 1);
+    // The last PV of this tile (PVDone could be one phase behind or ahead
+    // here, which a parity wait cannot tell apart).
+    mbar_wait(bar(kBarODone + i), 0);
     fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
     __nv_bfloat16* orow =
