@@ -781,7 +781,7 @@ def measure_sweep(torch) -> dict:
     del g
     s = torch.cuda.Stream()
     seq = 100
-    for n in (16, 64, 256, 1024, 4096, 8192, 16384, 32768):
+    for n in [int(x) for x in os.environ.get("SWEEP_N", "16,64,256,1024,4096,8192,16384,32768").split(",")]:
         times, walls = [], []
         for rep in range(10):
             seq += 1

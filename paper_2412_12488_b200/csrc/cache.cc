@@ -551,12 +551,20 @@ void ss_cache::EnsureAllocated(SeqId seq, int64_t upto) {
             std::to_string(need) + " pages needed, " + std::to_string(free_pages_.size()) +
                 " free");
   const int64_t old_len = rec->alloc_len;
-  for (int64_t i = 0; i < need; ++i) {
-    const int64_t page = free_pages_.back();
-    free_pages_.pop_back();
-    page_owner_[page] = seq;
-    rec->own_pages.push_back(page);
-    for (int32_t s = 0; s < P_; ++s) rec->slots.push_back(static_cast<int32_t>(page * P_ + s));
+  if (need > 0) {
+    rec->own_pages.reserve(rec->own_pages.size() + need);
+    size_t at = rec->slots.size();
+    rec->slots.resize(at + static_cast<size_t>(need) * P_);
+    int32_t* sl = rec->slots.data() + at;
+    for (int64_t i = 0; i < need; ++i) {
+      const int64_t page = free_pages_.back();
+      free_pages_.pop_back();
+      page_owner_[page] = seq;
+      rec->own_pages.push_back(page);
+      const int32_t base = static_cast<int32_t>(page * P_);
+      for (int32_t s = 0; s < P_; ++s) sl[s] = base + s;
+      sl += P_;
+    }
   }
   rec->alloc_len = rec->fork_len + static_cast<int64_t>(rec->own_pages.size()) * P_;
   if (need > 0) SyncDeviceTable(rec, old_len);
@@ -886,6 +894,7 @@ void ss_cache::LaunchRemote(const PeerTarget& peer, const int32_t* d_src_slots,
   c.win_layers = peer.L;
   c.verdict = d_verdict;
   c.status = d_status_;
+  c.sys_scope = peer.device != device_ ? 1 : 0;
   launch_copy_rows(c, s, num_sms_);
   launches_ += 2;
 }
@@ -1404,6 +1413,7 @@ void ss_cache::BroadcastSend(SeqId seq, int64_t begin, int64_t end, int32_t n_de
     f.win_layer_rows[d] = peer.win_layer_rows;
     f.win_layers[d] = peer.L;
     f.verdict[d] = v.verdict;
+    if (peer.device != device_) f.sys_scope = 1;
   }
   launch_copy_rows_fanout(f, s, num_sms_);
   launches_ += 1 + n_dest;
@@ -1588,6 +1598,7 @@ struct IpcBlob {
   int64_t num_pages;
   int32_t P, L, W, device;
   cudaIpcMemHandle_t h[6];
+  unsigned char uuid[16];  // exporter's GPU: ordinals differ across processes
 };
 static_assert(sizeof(IpcBlob) <= SS_IPC_HANDLE_BYTES, "ipc blob too large");
 }  // namespace
@@ -1602,6 +1613,9 @@ void ss_cache::ExportIpc(ss_ipc_handle* out) {
   b.L = L_;
   b.W = W_;
   b.device = device_;
+  cudaDeviceProp prop{};
+  CudaCheck(cudaGetDeviceProperties(&prop, device_), "cudaGetDeviceProperties");
+  std::memcpy(b.uuid, prop.uuid.bytes, sizeof(b.uuid));
   void* ptrs[6] = {d_pool_, d_fill_, d_expecting_, d_page_window_, d_win_received_,
                    d_win_layer_rows_};
   for (int i = 0; i < 6; ++i) CudaCheck(cudaIpcGetMemHandle(&b.h[i], ptrs[i]), "cudaIpcGetMemHandle");
@@ -1637,7 +1651,11 @@ void ss_cache::ImportIpc(Rank dest, const ss_ipc_handle* h) {
   t.P = b.P;
   t.L = b.L;
   t.W = b.W;
-  t.device = b.device;
+  // Same physical GPU (another process on it) -> device-scope publication
+  // suffices; any other GPU -> system scope.
+  cudaDeviceProp prop{};
+  CudaCheck(cudaGetDeviceProperties(&prop, device_), "cudaGetDeviceProperties");
+  t.device = std::memcmp(prop.uuid.bytes, b.uuid, sizeof(b.uuid)) == 0 ? device_ : -2;
   t.ipc = true;
   DetachPeer(dest);
   peers_[dest] = t;

@@ -53,6 +53,25 @@ __device__ __forceinline__ void st256(void* p, const u256& v) {
                : "memory");
 }
 
+// Fire-and-forget system-scope reductions for the window counters (a
+// returning atomicAdd_system is one full round trip per call; thread 0
+// looping over 80 layers of them cost ~25 us per launch).
+// Scope: system when the counters' observer is another GPU, device when it
+// is this GPU (another engine or process on it): a system-scope fence per
+// launch cost ~20 us even for a 5 MB transfer.
+__device__ __forceinline__ void red_sys_add(uint32_t* p, uint32_t v, bool sys) {
+  if (sys) asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  else asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_sys_add(unsigned long long* p, unsigned long long v, bool sys) {
+  if (sys) asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  else asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void fence_publish(bool sys) {
+  if (sys) asm volatile("fence.acq_rel.sys;" ::: "memory");
+  else asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+
 __device__ __forceinline__ uint8_t ld_cg_u8(const uint8_t* p) {
   unsigned short v;
   asm volatile("ld.global.cg.u8 %0, [%1];" : "=h"(v) : "l"(p));
@@ -161,22 +180,22 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
     if (account && lane == 0) atomicAdd(&s_rows[lrel], static_cast<uint32_t>(nr));
   }
   if (account) {
-    // Publish: every thread's stores, then the counters, at system scope so
-    // a peer engine that observes the counter also observes the rows.
-    __threadfence_system();
+    // Publish: every thread's stores, then the counters (release), so a peer
+    // engine that observes a counter also observes the rows.
+    fence_publish(p.sys_scope != 0);
     __syncthreads();
+    // Per-layer counters in parallel, one thread per layer; the total by
+    // thread 0 (the data fence above orders every row before any counter).
+    for (int i = threadIdx.x; i < p.n_layers; i += blockDim.x) {
+      if (s_rows[i] != 0) {
+        red_sys_add(p.win_layer_rows + static_cast<int64_t>(window) * p.win_layers + p.layer0 + i,
+                    s_rows[i], p.sys_scope != 0);
+      }
+    }
     if (threadIdx.x == 0) {
       unsigned long long total = 0;
       for (int i = 0; i < p.n_layers; ++i) total += s_rows[i];
-      __threadfence_system();
-      for (int i = 0; i < p.n_layers; ++i) {
-        if (s_rows[i] != 0) {
-          atomicAdd_system(p.win_layer_rows + static_cast<int64_t>(window) * p.win_layers +
-                               p.layer0 + i,
-                           s_rows[i]);
-        }
-      }
-      if (total != 0) atomicAdd_system(p.win_received + window, total);
+      if (total != 0) red_sys_add(p.win_received + window, total, p.sys_scope != 0);
     }
   }
 }
@@ -255,23 +274,22 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows_fanout(FanoutParams 
       }
     }
   }
-  __threadfence_system();
+  fence_publish(p.sys_scope != 0);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    for (int d = 0; d < p.n_dest; ++d) {
-      if (window[d] < 0) continue;
-      unsigned long long total = 0;
-      for (int i = 0; i < p.n_layers; ++i) {
-        const uint32_t c = s_rows[d * p.n_layers + i];
-        total += c;
-        if (c != 0) {
-          atomicAdd_system(p.win_layer_rows[d] + static_cast<int64_t>(window[d]) * p.win_layers[d] +
-                               p.layer0 + i,
-                           c);
-        }
+  for (int d = 0; d < p.n_dest; ++d) {
+    if (window[d] < 0) continue;
+    for (int i = threadIdx.x; i < p.n_layers; i += blockDim.x) {
+      const uint32_t c = s_rows[d * p.n_layers + i];
+      if (c != 0) {
+        red_sys_add(p.win_layer_rows[d] + static_cast<int64_t>(window[d]) * p.win_layers[d] +
+                        p.layer0 + i,
+                    c, p.sys_scope != 0);
       }
-      if (total != 0) atomicAdd_system(p.win_received[d] + window[d], total);
+    }
+    if (threadIdx.x == 0) {
+      unsigned long long total = 0;
+      for (int i = 0; i < p.n_layers; ++i) total += s_rows[d * p.n_layers + i];
+      if (total != 0) red_sys_add(p.win_received[d] + window[d], total, p.sys_scope != 0);
     }
   }
 }
@@ -454,19 +472,20 @@ __global__ void k_open_window(uint8_t* expecting, const int32_t* __restrict__ sl
   }
 }
 
+// One thread per (layer, position), positions fastest: a warp reads 32
+// adjacent fill bytes of one layer (a page's slots are consecutive), so the
+// scan is one coalesced pass over n * L bytes instead of L dependent byte
+// loads per position.
 __global__ void k_first_nonfull(const uint8_t* __restrict__ fill, int64_t fill_layer_bytes,
                                 int32_t L, const int32_t* __restrict__ slots, int64_t n,
                                 unsigned long long* out) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += stride) {
-    const int64_t s = slots[i];
-    for (int32_t l = 0; l < L; ++l) {
-      if (fill[l * fill_layer_bytes + s] == 0) {
-        atomicMin(out, static_cast<unsigned long long>(i));
-        break;
-      }
-    }
+  const int64_t total = n * L;
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
+       k += stride) {
+    const int64_t l = k / n, i = k - l * n;
+    if (fill[l * fill_layer_bytes + __ldg(slots + i)] == 0)
+      atomicMin(out, static_cast<unsigned long long>(i));
   }
 }
 
@@ -620,8 +639,8 @@ void launch_first_nonfull(const uint8_t* fill, int64_t fill_layer_bytes, int32_t
                           cudaStream_t s, int num_sms) {
   cudaMemsetAsync(out, 0xff, sizeof(unsigned long long), s);
   if (n <= 0) return;
-  k_first_nonfull<<<grid_for(n, 256, num_sms, 4), 256, 0, s>>>(fill, fill_layer_bytes, L, slots,
-                                                                n, out);
+  k_first_nonfull<<<grid_for(n * L, 256, num_sms, 8), 256, 0, s>>>(fill, fill_layer_bytes, L,
+                                                                    slots, n, out);
 }
 
 void launch_wait_counter(const unsigned long long* counter, unsigned long long target,

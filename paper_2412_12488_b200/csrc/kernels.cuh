@@ -57,6 +57,8 @@ struct CopyParams {
   const int32_t* verdict;     // validation result: >= 0 window id, < 0 reject
   uint32_t* status;           // sender-side sticky status
   int32_t group;              // rows per warp item (set by the launcher)
+  int32_t sys_scope;          // 1: the counters' observer is another GPU (fence/reds at
+                              // system scope); 0: same GPU (device scope is enough)
 };
 void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms);
 
@@ -78,6 +80,7 @@ struct FanoutParams {
   uint32_t* win_layer_rows[kMaxFanout];
   int32_t win_layers[kMaxFanout];
   const int32_t* verdict[kMaxFanout];
+  int32_t sys_scope;          // as CopyParams::sys_scope, for any destination
 };
 void launch_copy_rows_fanout(const FanoutParams& p, cudaStream_t s, int num_sms);
 

@@ -597,12 +597,22 @@ class KVCache:
             pass
 
     def _addr_out(self, cap: int) -> tuple[_Addr, np.ndarray]:
-        arr = np.empty(max(1, cap), dtype=SLOT_RANGE_DTYPE)
-        return _Addr(0, 0, 0, arr.ctypes.data_as(C.POINTER(_SlotRange)), len(arr)), arr
+        """Reusable output address buffer (structured numpy allocation and
+        ctypes pointer construction cost more than the C++ call itself)."""
+        buf = self.__dict__.get("_obuf")
+        if buf is None or len(buf) < cap:
+            buf = np.empty(max(cap, 1024), dtype=SLOT_RANGE_DTYPE)
+            self._obuf = buf
+            self._oaddr = _Addr(0, 0, 0, buf.ctypes.data_as(C.POINTER(_SlotRange)), len(buf))
+        a = self._oaddr
+        a.token_begin = a.token_count = a.n_ranges = 0
+        return a, buf
 
     @staticmethod
     def _addr_in(a: _Addr, arr: np.ndarray) -> "KVAddrInfo":
-        return KVAddrInfo(arr[:a.n_ranges].copy(), a.token_begin, a.token_count)
+        n = int(a.n_ranges)
+        raw = arr.view(np.uint8)[:n * SLOT_RANGE_DTYPE.itemsize].copy()
+        return KVAddrInfo(raw.view(SLOT_RANGE_DTYPE), a.token_begin, a.token_count)
 
     # -- hash model scalars (hash_model.cc) --------------------------------
     def InitialPrefixDigest(self) -> int:
