@@ -50,6 +50,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <type_traits>
 
@@ -68,25 +69,29 @@ constexpr int kAtom = kRows * 128;   // one 64-element atom column of a 128-row 
 constexpr int kTile = 2 * kAtom;     // a [128][128] bf16 query tile (32 KiB)
 constexpr int kKvAtom = kKeys * 128; // atom column of a [64][128] K or V tile (8 KiB)
 constexpr int kKvTile = 2 * kKvAtom; // 16 KiB
-constexpr int kStages = 4;           // K and V ring depth
+constexpr int kStages = 4;           // K ring depth
+#ifndef PF_V_STAGES
+#define PF_V_STAGES 4  // 4, 5, 6 measured equal
+#endif
+constexpr int kStagesV = PF_V_STAGES; // V ring depth (V is released last: PV retires it)
 constexpr int kSoftmaxThreads = 256;
-constexpr int kThreads = kSoftmaxThreads + 64;  // + producer warp + MMA warp
+constexpr int kThreads = kSoftmaxThreads + 96;  // + K producer, MMA, V producer warps
 
 // Shared memory map (bytes; tiles 1024-aligned).
 constexpr int kOffQ = 0;                             // 2 query tiles
 constexpr int kOffK = kOffQ + kQTiles * kTile;       // kStages K tiles
-constexpr int kOffV = kOffK + kStages * kKvTile;     // kStages V tiles
-constexpr int kOffBar = kOffV + kStages * kKvTile;   // mbarriers + tmem base
-constexpr int kSmem = kOffBar + 256;
+constexpr int kOffV = kOffK + kStages * kKvTile;     // kStagesV V tiles
+constexpr int kOffBar = kOffV + kStagesV * kKvTile;  // mbarriers + tmem base
+constexpr int kSmem = kOffBar + 512;
 
 // mbarrier slots (8 bytes each) from kOffBar.
 enum : int {
   kBarQ = 0,                         // softmax threads loaded Q (count 256)
   kBarKFull = 1,                     // +stage: TMA bytes landed
   kBarVFull = kBarKFull + kStages,
-  kBarKEmpty = kBarVFull + kStages,  // +stage: MMAs reading it retired
+  kBarKEmpty = kBarVFull + kStagesV, // +stage: MMAs reading it retired
   kBarVEmpty = kBarKEmpty + kStages,
-  kBarSFull = kBarVEmpty + kStages,  // +2*tile+slot: S_i(j) ready in TMEM slot j&1
+  kBarSFull = kBarVEmpty + kStagesV,  // +2*tile+slot: S_i(j) ready in TMEM slot j&1
                                      // (per slot, so S_i(j+1) landing early cannot
                                      // push a barrier two phases past its waiter)
   kBarPFull = kBarSFull + 4,         // +2*tile+slot: P_i(j) written, O_i rescaled (count
@@ -97,7 +102,8 @@ enum : int {
   kBarODone = kBarPVDone + 2,        // +tile: the last PV_i retired (single phase)
   kBarCount = kBarODone + 2,
 };
-static_assert(kBarCount * 8 + 8 <= 256, "barrier area");
+static_assert(kBarCount * 8 + 8 <= 512, "barrier area");
+static_assert(kSmem + 1024 <= 227 * 1024, "shared memory");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -363,7 +369,21 @@ struct PrefillArgs {
   __nv_bfloat16* out;         // [n_q][Hq][128]
   int layer, page_size, q_pos0, n_q, Hq, Hkv, n_blocks;
   float scale_log2;
+#ifdef PF_TRACE
+  unsigned long long* trace;  // debug timeline of CTA (0, 0): [count][events]
+#endif
 };
+
+// Debug timeline (build with -DPF_TRACE): plain stores of clock64() into a
+// slot fixed by the event code (type, tile, j < 256), CTA (0, 0) only.
+#ifdef PF_TRACE
+#define PF_EV(code)                                                              \
+  do {                                                                           \
+    if (blockIdx.x == 0 && blockIdx.y == 0) a.trace[(code) & 0xffff] = clock64(); \
+  } while (0)
+#else
+#define PF_EV(code) do {} while (0)
+#endif
 
 __global__ void __launch_bounds__(kThreads, 1)
     k_prefill_attn_tc(const __grid_constant__ CUtensorMap pool_map,
@@ -395,8 +415,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(bar(kBarQ), kSoftmaxThreads);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(bar(kBarKFull + s), 1);
-      mbar_init(bar(kBarVFull + s), 1);
       mbar_init(bar(kBarKEmpty + s), 1);
+    }
+    for (int s = 0; s < kStagesV; ++s) {
+      mbar_init(bar(kBarVFull + s), 1);
       mbar_init(bar(kBarVEmpty + s), 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -421,8 +443,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr uint32_t tmem = 0;
   if (tid == 0 && *tmem_slot != 0u) __trap();
 
-  if (warp == 8) {
-    // ---------------- producer: paged K/V tiles by TMA ----------------
+  if (warp == 8 || warp == 10) {
+    // ---------------- producers: paged K (warp 8) / V (warp 10) tiles by TMA ----
+    // Separate warps so K runs ahead of V: with one producer, K(j+2) queued
+    // behind V(j+1), which waits for PV(j-3) to free its stage, and the MMA
+    // warp waited ~900 cycles per tile for K (profiled timeline).
     // Lane l owns tile positions 2l, 2l+1.  A chunk of C = min(P, 64)
     // positions whose slots are consecutive rows (a page, when the sequence
     // is page-aligned) is one C-row box; otherwise (a fork at a
@@ -433,7 +458,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int my_chunk_lane0 = lane - lane % lanes_per_chunk;
     const int ck = h * kD, cv = (a.Hkv + h) * kD;  // element column of K / V of this head
     for (int j = 0; j < n_tiles; ++j) {
-      const int s = j % kStages;
+      const int nst = warp == 8 ? kStages : kStagesV;
+      const int s = j % nst;
       const int p0 = j * kKeys + lane * 2;
       int sl[2];
 #pragma unroll
@@ -449,13 +475,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t ballot = __ballot_sync(0xffffffffu, ok);
       const bool contiguous = ((ballot >> my_chunk_lane0) & chunk_mask) == chunk_mask;
       const int chunk_row = __shfl_sync(0xffffffffu, sl[0], my_chunk_lane0);
-      for (int op = 0; op < 2; ++op) {  // K then V
+      {
+        const int op = warp == 8 ? 0 : 1;
         const uint32_t base = (op == 0 ? sK : sV) + s * kKvTile;
         const uint32_t full = bar((op == 0 ? kBarKFull : kBarVFull) + s);
         const int col = op == 0 ? ck : cv;
         if (lane == 0) {
-          if (j >= kStages)
-            mbar_wait(bar((op == 0 ? kBarKEmpty : kBarVEmpty) + s), ((j / kStages) + 1) & 1);
+          if (j >= nst)
+            mbar_wait(bar((op == 0 ? kBarKEmpty : kBarVEmpty) + s), ((j / nst) + 1) & 1);
+          PF_EV((op == 0 ? 0xA00 : 0xC00) | (j & 0xff));  // producer: stage free, issuing
           mbar_expect_tx(full, kKvTile);
         }
         __syncwarp();
@@ -506,7 +534,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto issue_pv = [&](int i, int j) {
       mbar_wait(bar(kBarPFull + 2 * i + (j & 1)), (j >> 1) & 1);
       fence_after();
-      const uint32_t b0 = v_lo + (((j % kStages) * kKvTile) >> 4);
+      const uint32_t b0 = v_lo + (((j % kStagesV) * kKvTile) >> 4);
 #pragma unroll
       for (int k = 0; k < kKeys / 16; ++k) {
         // A = P_i in TMEM (bf16 pairs: 8 columns per 16 keys); B = V MN-major:
@@ -520,7 +548,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto zero_tail = [&](int j) {
       const int valid = n_keys - j * kKeys;
       if (valid >= kKeys) return;
-      uint8_t* vb = smem + kOffV + (j % kStages) * kKvTile;
+      uint8_t* vb = smem + kOffV + (j % kStagesV) * kKvTile;
       for (int e = lane; e < (kKeys - valid) * 16; e += 32) {
         const int r = valid + (e >> 4), c = e & 15;
         *reinterpret_cast<uint4*>(vb + (c >> 3) * kKvAtom + r * 128 + (c & 7) * 16) =
@@ -543,15 +571,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     // S_i(j+2) into the slot P_i(j) frees (tcgen05 MMAs of one thread run in
     // order), so one tile's softmax never waits on the other's.
     for (int j = 0; j < n_tiles; ++j) {
-      const int sv = j % kStages;
-      mbar_wait(bar(kBarVFull + sv), (j / kStages) & 1);
+      const int sv = j % kStagesV;
+      mbar_wait(bar(kBarVFull + sv), (j / kStagesV) & 1);
+      if (lane == 0) PF_EV(0xE00 | (j & 0xff));  // MMA: V(j) landed
       if (j == n_tiles - 1) zero_tail(j);
       const bool next = j + 2 < n_tiles;
       const int sk = (j + 2) % kStages;
       if (next) mbar_wait(bar(kBarKFull + sk), ((j + 2) / kStages) & 1);
       fence_after();
+      if (lane == 0) PF_EV(0x100 | (j & 0xff));  // MMA: V(j) and K(j+2) ready
       for (int i = 0; i < kQTiles; ++i) {
         issue_pv(i, j);
+        if (lane == 0) PF_EV(0x200 | (i << 8) | (j & 0xff));  // MMA: PV_i(j) issued
         if (j == n_tiles - 1) commit_elect(bar(kBarODone + i));
         if (next) issue_s(i, j + 2);
       }
@@ -584,8 +615,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     float m = -INFINITY, l = 0.f;  // running max (scaled log2 domain) and sum
     for (int j = 0; j < n_tiles; ++j) {
       const uint32_t tS = tSi + (j & 1) * 64;
+      if ((warp & 3) == 0 && lane == 0) PF_EV(0x400 | (i << 8) | (j & 0xff));  // softmax: wait S
       mbar_wait(bar(kBarSFull + 2 * i + (j & 1)), (j >> 1) & 1);
       fence_after();
+      if ((warp & 3) == 0 && lane == 0) PF_EV(0x600 | (i << 8) | (j & 0xff));  // softmax: S ready
       uint32_t sr[kKeys];
 #pragma unroll
       for (int c0 = 0; c0 < kKeys; c0 += 16) tmem_ld16_nowait(tS + c0, sr + c0);
@@ -672,6 +705,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_wait_st();
       fence_before();
       mbar_arrive(bar(kBarPFull + 2 * i + (j & 1)));
+      if ((warp & 3) == 0 && lane == 0) PF_EV(0x800 | (i << 8) | (j & 0xff));  // softmax: P arrived
       l = l * alpha + psum;
       m = m_new;
     }
@@ -782,7 +816,24 @@ bool launch_prefill_attn(const PoolTensorMap& page_map, const PoolTensorMap& row
   std::memcpy(&m, page_map.bytes, sizeof(m));
   std::memcpy(&mr, row_map.bytes, sizeof(mr));
   const dim3 grid(a.n_blocks, Hkv);
+#ifdef PF_TRACE
+  unsigned long long* tr = nullptr;
+  cudaMalloc(&tr, 65536 * sizeof(unsigned long long));
+  cudaMemset(tr, 0, 65536 * sizeof(unsigned long long));
+  a.trace = tr;
+#endif
   k_prefill_attn_tc<<<grid, kThreads, smem, s>>>(m, mr, a);
+#ifdef PF_TRACE
+  cudaDeviceSynchronize();
+  static unsigned long long h[65536];
+  cudaMemcpy(h, tr, sizeof(h), cudaMemcpyDeviceToHost);
+  cudaFree(tr);
+  if (FILE* f = std::fopen("gpurun_out/pf_trace.txt", "w")) {
+    for (int i = 0; i < 65536; ++i)
+      if (h[i]) std::fprintf(f, "%llu %x\n", h[i], i);
+    std::fclose(f);
+  }
+#endif
   return true;
 }
 
