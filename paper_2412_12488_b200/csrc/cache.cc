@@ -190,6 +190,7 @@ ss_cache::ss_cache(const ss_config& cfg)
   CudaCheck(cudaEventCreateWithFlags(&user_ev_, cudaEventDisableTiming), "event");
   CudaCheck(cudaEventCreateWithFlags(&comm_ev_, cudaEventDisableTiming), "event");
   CudaCheck(cudaEventCreateWithFlags(&layer_ev_, cudaEventDisableTiming), "event");
+  CudaCheck(cudaEventCreateWithFlags(&window_ev_, cudaEventDisableTiming), "event");
   {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -275,6 +276,7 @@ ss_cache::~ss_cache() {
   cudaFree(d_scratch_);
   cudaFreeHost(h_pinned_);
   cudaEventDestroy(internal_ev_);
+  cudaEventDestroy(window_ev_);
   cudaEventDestroy(user_ev_);
   cudaStreamSynchronize(comm_stream_);
   cudaEventDestroy(comm_ev_);
@@ -630,7 +632,11 @@ void ss_cache::OpenDeviceWindow(Record* rec, int64_t m, int64_t e) {
                      d_win_received_, d_win_layer_rows_, L_, stream_);
   launches_ += 1;
   DevFree(b, stream_);
-  Sync();
+  if (ipc_exported_) {
+    Sync();  // a peer process sees a ready receiver once it holds the address
+  } else {
+    CudaCheck(cudaEventRecord(window_ev_, stream_), "cudaEventRecord window");
+  }
 }
 
 // kv_cache.cc:231-243
@@ -862,6 +868,8 @@ void ss_cache::LaunchRemote(const PeerTarget& peer, const int32_t* d_src_slots,
                             const int32_t* d_rbegin, const int32_t* d_rcount, int64_t n_ranges,
                             int32_t* d_verdict, int64_t n_rows, int32_t lb, int32_t le,
                             cudaStream_t s) {
+  // The receiver's window must be open on its device before validation.
+  if (peer.local != nullptr) CudaCheck(cudaStreamWaitEvent(s, peer.local->window_ev_, 0), "wait window");
   ValidateParams v{};
   v.range_page = d_rpage;
   v.range_begin = d_rbegin;
@@ -1391,6 +1399,7 @@ void ss_cache::BroadcastSend(SeqId seq, int64_t begin, int64_t end, int32_t n_de
   f.n_dest = n_dest;
   for (int32_t d = 0; d < n_dest; ++d) {
     const PeerTarget& peer = PeerFor(dests[d]);
+    if (peer.local != nullptr) CudaCheck(cudaStreamWaitEvent(s, peer.local->window_ev_, 0), "wait window");
     ValidateParams v{};
     v.range_page = reinterpret_cast<int64_t*>(base + lay[d].rp);
     v.range_begin = reinterpret_cast<int32_t*>(base + lay[d].rb);
@@ -1585,6 +1594,7 @@ void ss_cache::AttachPeer(Rank dest, ss_cache* peer) {
   t.L = peer->L_;
   t.W = peer->W_;
   t.device = peer->device_;
+  t.local = peer;
   DetachPeer(dest);
   peers_[dest] = t;
   peer_engines_[dest] = peer;
@@ -1605,6 +1615,8 @@ static_assert(sizeof(IpcBlob) <= SS_IPC_HANDLE_BYTES, "ipc blob too large");
 
 void ss_cache::ExportIpc(ss_ipc_handle* out) {
   RequireDevice("ExportIpc");
+  ipc_exported_ = true;
+  Sync();  // windows opened so far are visible to the peer process
   IpcBlob b{};
   b.magic = kIpcMagic;
   b.version = SS_ABI_VERSION;
@@ -1791,6 +1803,10 @@ void ss_cache::DecodeAttention(ss_plan* plan, int32_t layer, int32_t hq, int32_t
     // and partial storage for at most grid + segments pieces.
     plan->decode_grid = decode_attn_resident_ctas(hd, num_sms_);
     const int64_t n_seg = plan->batch * hkv;
+    if (const char* g = std::getenv("MICROKV_DECODE_GRID")) {  // tuning experiments
+      const int v = std::atoi(g);
+      if (v > 0 && v < plan->decode_grid) plan->decode_grid = v;
+    }
     std::vector<int64_t> seg(n_seg + 1, 0);
     for (int64_t b = 0; b < plan->batch; ++b) {
       const int64_t tiles = (plan->ctx_lens[b] + 15) / 16;

@@ -211,6 +211,7 @@ struct PeerTarget {
   int32_t device = -1;
   bool ipc = false;
   std::vector<void*> ipc_ptrs;
+  const ss_cache* local = nullptr;  // in-process peer: its window-ready event orders our sends
 };
 
 }  // namespace mkv
@@ -393,6 +394,11 @@ struct ss_cache {
   cudaStream_t stream_ = nullptr;
   cudaStream_t comm_stream_ = nullptr;  // per-layer sends (overlap with compute)
   cudaEvent_t internal_ev_ = nullptr, user_ev_ = nullptr, comm_ev_ = nullptr, layer_ev_ = nullptr;
+  // Recorded after each receive window opens on the device; in-process
+  // senders wait on it instead of PrepRecv synchronizing the host.  Once the
+  // receive surface is exported to another process PrepRecv synchronizes.
+  cudaEvent_t window_ev_ = nullptr;
+  bool ipc_exported_ = false;
   bool user_pending_ = false, comm_pending_ = false;
   uint64_t user_gen_ = 0, user_waited_gen_ = 0, comm_gen_ = 0, comm_waited_gen_ = 0;
   uint64_t internal_gen_ = 1, internal_recorded_gen_ = 0;

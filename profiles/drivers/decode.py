@@ -1,6 +1,6 @@
 """Profiling driver: paged GQA decode attention (70B: Hq=64, Hkv=8, D=128)
 over a sweep of (batch, ctx); device time gated behind a sleep kernel so the
-launches run back to back.  MICROKV_DECODE_SPLITS overrides the split count."""
+launches run back to back.  MICROKV_DECODE_GRID caps the stream-K grid (tuning)."""
 import os
 import sys
 from pathlib import Path
