@@ -1803,6 +1803,15 @@ void ss_cache::DecodeAttention(ss_plan* plan, int32_t layer, int32_t hq, int32_t
     // and partial storage for at most grid + segments pieces.
     plan->decode_grid = decode_attn_resident_ctas(hd, num_sms_);
     const int64_t n_seg = plan->batch * hkv;
+    // Segment-aligned grid: k CTAs per (batch, kv head) segment, so with
+    // equal contexts no CTA straddles two segments (one prologue/epilogue and
+    // one partial per CTA), at most 32 pieces per segment.  Measured on B200
+    // (profiles/r01/decode_grid_sweep.txt): B=8 ctx 8K 0.69 -> 0.74 of HBM,
+    // B=32 0.93 -> 0.97, B=8 ctx 32K 0.97 -> 1.0, B=1 0.21 -> 0.27.
+    if (n_seg <= plan->decode_grid) {
+      const int64_t k = std::min<int64_t>(plan->decode_grid / n_seg, 32);
+      plan->decode_grid = static_cast<int32_t>(n_seg * k);
+    }
     if (const char* g = std::getenv("MICROKV_DECODE_GRID")) {  // tuning experiments
       const int v = std::atoi(g);
       if (v > 0 && v < plan->decode_grid) plan->decode_grid = v;
