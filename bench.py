@@ -656,9 +656,11 @@ def measure_configs(torch) -> dict:
     P.attach_peer(1, D)
     _populate_prefix_l(P, 1, prompt, torch, L)
     rows = torch.randint(-2**62, 2**62, (PROMPT * W,), dtype=torch.int64, device="cuda")
+    max_tail = PROMPT - int(0.7 * PROMPT)
+    rows_all = torch.empty(L * max_tail * W, dtype=torch.int64, device="cuda").random_()
     for ratio in (0.1, 0.2, 0.3):
         sp = int((1 - ratio) * PROMPT)
-        ts, ta = [], []
+        ts, ta, tf = [], [], []
         for i in range(4):
             seq = 200 + int(ratio * 100) * 10 + i
             t, r = _migrate_once(torch, P, D, 1, prompt, sp, L, s, seq)
@@ -676,18 +678,36 @@ def measure_configs(torch) -> dict:
             s.synchronize()
             plan.close()
             assert D.Committed(seq) == PROMPT
-            D.FreeSequence(seq)
-            ts.append(t)
             ta.append(e0.elapsed_time(e1) / 1e3)
-        t, tap = float(np.median(ts[1:])), float(np.median(ta[1:]))
+            # The same tail as one 80-layer launch (a producer holding every
+            # layer's rows, e.g. a batched tail prefill).
+            D.FreeSequence(seq)
+            seq2 = seq + 5000
+            _t2, _ = _migrate_once(torch, P, D, 1, prompt, sp, L, s, seq2)
+            D.EnsureAllocated(seq2, PROMPT)
+            plan = D.BeginForward([BatchEntry(seq2, (sp, PROMPT))])
+            with torch.cuda.stream(s):
+                torch.cuda._sleep(2_000_000)
+            e0.record(s)
+            D.append_rows_layers_async(plan, (0, L), rows_all.data_ptr(), s.cuda_stream)
+            e1.record(s)
+            s.synchronize()
+            plan.close()
+            assert D.Committed(seq2) == PROMPT
+            D.FreeSequence(seq2)
+            tf.append(e0.elapsed_time(e1) / 1e3)
+            ts.append(t)
+        t, tap, tfu = float(np.median(ts[1:])), float(np.median(ta[1:])), float(np.median(tf[1:]))
         pay, tail = sp * L * BPT, (PROMPT - sp) * L * BPT
         out[f"70b_balanced_r{ratio}"] = {
             "sent_tokens": sp, "tail_tokens": PROMPT - sp,
             "send_device_us": round(1e6 * t, 1), "send_payload_gbs": round(pay / t / 1e9, 1),
             "send_hbm_frac": round(2 * pay / t / 1e9 / peak, 4),
             "tail_append_us": round(1e6 * tap, 1),
-            "tail_append_hbm_frac": round(2 * tail / tap / 1e9 / peak, 4)}
-    del P, D, rows
+            "tail_append_hbm_frac": round(2 * tail / tap / 1e9 / peak, 4),
+            "tail_append_one_launch_us": round(1e6 * tfu, 1),
+            "tail_append_one_launch_hbm_frac": round(2 * tail / tfu / 1e9 / peak, 4)}
+    del P, D, rows, rows_all
     torch.cuda.empty_cache()
     return out
 

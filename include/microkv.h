@@ -349,6 +349,11 @@ int ss_apply_remote_write_async(ss_cache* cache, const ss_addr* addr, int32_t la
  * are written and marked ComputedLocal (kv_cache.cc:328-334 write rule). */
 int ss_append_rows_async(ss_cache* cache, ss_plan* plan, int32_t layer, const void* rows_dev,
                          void* stream);
+/* The same append for layers [layer_begin, layer_end) in one launch, from
+ * rows_dev[layer_end - layer_begin][total_outputs][dim] (a producer that
+ * has every layer's rows at once, e.g. a batched prefill or a KV import). */
+int ss_append_rows_layers_async(ss_cache* cache, ss_plan* plan, int32_t layer_begin,
+                                int32_t layer_end, const void* rows_dev, void* stream);
 
 /* Paged GQA decode attention over the pool, reading K||V rows through the
  * device page table: each (token, layer) entry of dim u64 words holds

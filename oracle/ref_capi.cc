@@ -455,6 +455,9 @@ int ss_apply_remote_write_async(ss_cache*, const ss_addr*, int32_t, const uint64
                                 uint64_t, int32_t*, void*) {
   return SS_ERR_UNSUPPORTED;
 }
+int ss_append_rows_layers_async(ss_cache*, ss_plan*, int32_t, int32_t, const void*, void*) {
+  return SS_ERR_UNSUPPORTED;
+}
 int ss_append_rows_async(ss_cache*, ss_plan*, int32_t, const void*, void*) {
   return SS_ERR_UNSUPPORTED;
 }

@@ -1099,20 +1099,28 @@ KVAddr ss_cache::BuildAddr(SeqId seq, int64_t begin, int64_t end) {
 // KV append from the producing layer's dense K||V rows (write rule of
 // kv_cache.cc:328-334).
 void ss_cache::AppendRows(ss_plan* plan, int32_t layer, const void* rows, cudaStream_t s) {
+  AppendRowsLayers(plan, layer, layer + 1, rows, s);
+}
+
+void ss_cache::AppendRowsLayers(ss_plan* plan, int32_t lb, int32_t le, const void* rows,
+                                cudaStream_t s) {
   RequireDevice("AppendRows");
-  MKV_CHECK(layer >= 0 && layer < L_, kInvalidArgument, "layer out of range");
+  MKV_CHECK(lb >= 0 && lb < le && le <= L_, kInvalidArgument, "layer out of range");
   OrderAfterUser();
   PlanToDevice(plan);
   if (s != stream_) OrderUser(s);
   CopyParams c{};
   c.src = static_cast<const uint64_t*>(rows);
-  c.dst = PoolLayer(layer);
+  c.src_layer_words = plan->total_outputs * W_;
+  c.dst = PoolLayer(lb);
+  c.dst_layer_words = num_pages_ * P_ * W_;
   c.dst_idx = plan->d_out_slots;
-  c.dst_fill = d_fill_ + static_cast<int64_t>(layer) * num_pages_ * P_;
+  c.dst_fill = d_fill_ + static_cast<int64_t>(lb) * num_pages_ * P_;
+  c.dst_fill_layer = num_pages_ * P_;
   c.fill_value = 1;  // FillState::kComputedLocal
   c.n_rows = plan->total_outputs;
-  c.layer0 = layer;
-  c.n_layers = 1;
+  c.layer0 = lb;
+  c.n_layers = le - lb;
   c.W = W_;
   launch_copy_rows(c, s, num_sms_);
   launches_ += 1;

@@ -244,6 +244,8 @@ struct ss_cache {
                    cudaStream_t s);
   mkv::KVAddr BuildAddr(SeqId seq, int64_t begin, int64_t end);
   void AppendRows(ss_plan* plan, int32_t layer, const void* rows_dev, cudaStream_t s);
+  void AppendRowsLayers(ss_plan* plan, int32_t layer_begin, int32_t layer_end, const void* rows_dev,
+                        cudaStream_t s);
 
   // Transfer agent.
   int ApplyRemoteWrite(const mkv::KVAddr& addr, int32_t layer, const uint64_t* payload,

@@ -217,6 +217,7 @@ _SIGNATURES = {
     "ss_apply_remote_write_async": (C.c_int, [_vp, C.POINTER(_Addr), C.c_int32, _vp, C.c_int64,
                                               C.c_uint64, _i32p, _vp]),
     "ss_append_rows_async": (C.c_int, [_vp, _vp, C.c_int32, _vp, _vp]),
+    "ss_append_rows_layers_async": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, _vp, _vp]),
     "ss_begin_decode": (C.c_int, [_vp, _i64p, _i64p, C.c_int64, C.POINTER(_vp)]),
     "ss_paged_decode_attention_async": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, C.c_int32,
                                                   C.c_int32, C.c_float, _vp, _vp, _vp]),
@@ -975,6 +976,14 @@ class KVCache:
                           stream: int = 0) -> None:
         self._check(self._lib.ss_append_rows_async(self._h, plan.handle, layer,
                                                    C.c_void_p(rows_ptr), C.c_void_p(stream)))
+
+    def append_rows_layers_async(self, plan: ForwardPlan, layers: tuple, rows_ptr: int,
+                                 stream: int = 0) -> None:
+        """KV append for layers [begin, end) in one launch; rows are
+        [end - begin][total_outputs][dim] u64 words in device memory."""
+        self._check(self._lib.ss_append_rows_layers_async(self._h, plan.handle, layers[0],
+                                                          layers[1], C.c_void_p(rows_ptr),
+                                                          C.c_void_p(stream)))
 
     def begin_decode(self, seqs: Sequence[int], ctx_lens: Sequence[int]) -> ForwardPlan:
         s = np.ascontiguousarray(np.asarray(seqs, dtype=np.int64))
