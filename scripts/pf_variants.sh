@@ -1,6 +1,6 @@
 #!/bin/bash
 cd "$(dirname "$0")/.."
-for v in "-DPF_V_STAGES=4" "-DPF_V_STAGES=5" ""; do
+for v in "-DPF1_POLY_EVERY=0" "-DPF1_POLY_EVERY=4" "-DPF1_POLY_EVERY=3" "-DPF1_POLY_EVERY=2"; do
   rm -f paper_2412_12488_b200/_lib/obj/prefill_attn.cu.o
   MKV_NVCC_EXTRA="$v" python -c "from paper_2412_12488_b200 import build as b; b.build()" > /dev/null 2>&1
   echo "variant [$v]"
