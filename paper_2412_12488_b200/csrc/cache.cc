@@ -214,6 +214,8 @@ ss_cache::ss_cache(const ss_config& cfg)
   CudaCheck(cudaMalloc(&d_status_, sizeof(uint32_t)), "cudaMalloc");
   CudaCheck(cudaMalloc(&d_scratch_, 256), "cudaMalloc");
   CudaCheck(cudaHostAlloc(&h_pinned_, sizeof(unsigned long long) * kMaxWindows, 0), "pinned");
+  CudaCheck(cudaHostAlloc(&h_stage_, kStageSlots * kStageBytes, 0), "pinned staging");
+  for (auto& e : stage_ev_) CudaCheck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   // A fresh pool is zero-filled like the reference's (kv_cache.cc:37).
   CudaCheck(cudaMemsetAsync(d_pool_, 0, slots * L_ * W_ * 8, stream_), "memset");
   CudaCheck(cudaMemsetAsync(d_fill_, 0, slots * L_, stream_), "memset");
@@ -275,6 +277,13 @@ ss_cache::~ss_cache() {
   cudaFree(d_status_);
   cudaFree(d_scratch_);
   cudaFreeHost(h_pinned_);
+  if (h_stage_ != nullptr) {
+    for (int i = 0; i < kStageSlots; ++i) {
+      if (stage_used_[i]) cudaEventSynchronize(stage_ev_[i]);  // copies on user streams
+      cudaEventDestroy(stage_ev_[i]);
+    }
+    cudaFreeHost(h_stage_);
+  }
   cudaEventDestroy(internal_ev_);
   cudaEventDestroy(window_ev_);
   cudaEventDestroy(user_ev_);
@@ -321,8 +330,20 @@ void ss_cache::RequireDevice(const char* what) const {
 void ss_cache::Sync() { CudaCheck(cudaStreamSynchronize(stream_), "cudaStreamSynchronize"); }
 
 void ss_cache::H2D(void* dst, const void* src, size_t bytes, cudaStream_t s, const char* what) {
-  CudaCheck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s), what);
   h2d_bytes_ += static_cast<int64_t>(bytes);
+  if (h_stage_ != nullptr && bytes > 0 && bytes <= kStageBytes) {
+    std::lock_guard<std::mutex> lock(stage_mu_);
+    const int i = stage_next_;
+    stage_next_ = (stage_next_ + 1) % kStageSlots;
+    if (stage_used_[i]) CudaCheck(cudaEventSynchronize(stage_ev_[i]), "staging slot");
+    uint8_t* st = h_stage_ + static_cast<size_t>(i) * kStageBytes;
+    std::memcpy(st, src, bytes);
+    CudaCheck(cudaMemcpyAsync(dst, st, bytes, cudaMemcpyHostToDevice, s), what);
+    CudaCheck(cudaEventRecord(stage_ev_[i], s), "staging event");
+    stage_used_[i] = true;
+    return;
+  }
+  CudaCheck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s), what);
 }
 
 void ss_cache::D2H(void* dst, const void* src, size_t bytes, cudaStream_t s, const char* what) {

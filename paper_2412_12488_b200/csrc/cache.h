@@ -401,6 +401,16 @@ struct ss_cache {
   // receive surface is exported to another process PrepRecv synchronizes.
   cudaEvent_t window_ev_ = nullptr;
   bool ipc_exported_ = false;
+  // Pinned staging ring for small host->device uploads (page tables, row
+  // maps, window slots): a pageable cudaMemcpyAsync blocks the host while the
+  // driver stages it; through the ring the call is a memcpy + an async copy.
+  static constexpr int kStageSlots = 16;
+  static constexpr size_t kStageBytes = size_t(256) << 10;
+  uint8_t* h_stage_ = nullptr;
+  cudaEvent_t stage_ev_[kStageSlots] = {};
+  bool stage_used_[kStageSlots] = {};
+  int stage_next_ = 0;
+  std::mutex stage_mu_;
   bool user_pending_ = false, comm_pending_ = false;
   uint64_t user_gen_ = 0, user_waited_gen_ = 0, comm_gen_ = 0, comm_waited_gen_ = 0;
   uint64_t internal_gen_ = 1, internal_recorded_gen_ = 0;
