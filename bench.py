@@ -883,16 +883,28 @@ def measure_append_gather(torch) -> dict:
 
 
 def measure_decode(torch) -> dict:
-    """bf16 GQA paged decode attention (Hq=64, Hkv=8, D=128) over the pool."""
+    """bf16 GQA paged decode attention over the pool: the 70B heads (Hq=64,
+    Hkv=8, D=128) over (batch, ctx), the same on a fragmented pool (pages in
+    the order the LIFO allocator hands them out after random frees, SURVEY
+    §8(d)), and the 8B heads (Hq=32, Hkv=8); next to it the fp32 attention
+    on the host's cores (torch, all threads) for one case, for scale."""
     from paper_2412_12488_b200 import BatchEntry, KVCache
 
     peak, _ = _peaks()
     res = {}
     Ld = 2
-    for (B, ctx) in ((8, 8192), (32, 8192), (128, 4096), (8, 32768)):
+    cases = [(8, 8192, HQ, False), (32, 8192, HQ, False), (128, 4096, HQ, False),
+             (8, 32768, HQ, False), (8, 8192, HQ, True), (32, 8192, 32, False)]
+    for (B, ctx, hq, frag) in cases:
         pages = B * (ctx // PAGE) + 16
         Cd = KVCache(num_pages=pages, page_size=PAGE, layers=Ld, dim=W, device=0)
         rng = np.random.default_rng(5)
+        if frag:  # take every page, free them in random order: LIFO reuse scatters them
+            for i in range(pages):
+                Cd.CreateSequence(10**6 + i, [0] * PAGE)
+                Cd.EnsureAllocated(10**6 + i, PAGE)
+            for i in rng.permutation(pages):
+                Cd.FreeSequence(10**6 + int(i))
         for b in range(B):
             Cd.CreateSequence(b, [int(x) for x in rng.integers(0, 256, ctx)])
             Cd.EnsureAllocated(b, ctx)
@@ -903,11 +915,11 @@ def measure_decode(torch) -> dict:
         torch.cuda.synchronize()
         plan.close()
         dplan = Cd.begin_decode(list(range(B)), [ctx] * B)
-        q = torch.randn(B, HQ, HD, device="cuda", dtype=torch.bfloat16)
+        q = torch.randn(B, hq, HD, device="cuda", dtype=torch.bfloat16)
         o = torch.empty_like(q)
         s = torch.cuda.Stream()
         for _ in range(3):
-            Cd.paged_decode_attention_async(dplan, 0, HQ, HKV, HD, HD ** -0.5, q.data_ptr(),
+            Cd.paged_decode_attention_async(dplan, 0, hq, HKV, HD, HD ** -0.5, q.data_ptr(),
                                             o.data_ptr(), s.cuda_stream)
         reps = 10
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -915,16 +927,35 @@ def measure_decode(torch) -> dict:
             torch.cuda._sleep(20_000_000)
         ev[0].record(s)
         for i in range(reps):
-            Cd.paged_decode_attention_async(dplan, i % Ld, HQ, HKV, HD, HD ** -0.5, q.data_ptr(),
+            Cd.paged_decode_attention_async(dplan, i % Ld, hq, HKV, HD, HD ** -0.5, q.data_ptr(),
                                             o.data_ptr(), s.cuda_stream)
         ev[1].record(s)
         torch.cuda.synchronize()
         t = ev[0].elapsed_time(ev[1]) / 1e3 / reps
         alg = B * ctx * BPT + 2 * q.numel() * 2
-        res[f"B{B}_ctx{ctx}"] = {"us": round(1e6 * t, 1), "gbs": round(alg / t / 1e9, 1),
-                                 "frac": round(alg / t / 1e9 / peak, 4)}
+        key = f"B{B}_ctx{ctx}" + ("_fragmented" if frag else "") + ("_8b_heads" if hq != HQ else "")
+        res[key] = {"us": round(1e6 * t, 1), "gbs": round(alg / t / 1e9, 1),
+                    "frac": round(alg / t / 1e9 / peak, 4)}
+        if (B, ctx, hq, frag) == (8, 8192, HQ, False):
+            # fp32 GQA decode attention on the host (all torch threads).
+            K = rows.view(B * ctx, 2, HKV, HD)[:, 0].float().cpu().view(B, ctx, HKV, HD)
+            V = rows.view(B * ctx, 2, HKV, HD)[:, 1].float().cpu().view(B, ctx, HKV, HD)
+            qc = q.float().cpu().view(B, HKV, hq // HKV, HD)
+
+            def cpu_attn():
+                sc = torch.einsum("bhgd,bnhd->bhgn", qc, K) * HD ** -0.5
+                return torch.einsum("bhgn,bnhd->bhgd", torch.softmax(sc, -1), V)
+
+            cpu_attn()
+            w0 = time.perf_counter()
+            cpu_attn()
+            tc = time.perf_counter() - w0
+            res["cpu_fp32_B8_ctx8192"] = {"ms": round(1e3 * tc, 2),
+                                          "gbs_bf16_equiv": round(alg / tc / 1e9, 2),
+                                          "threads": torch.get_num_threads()}
+            del K, V
         dplan.close()
-        del Cd
+        del Cd, rows
         torch.cuda.empty_cache()
     return res
 
