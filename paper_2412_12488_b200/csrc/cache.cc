@@ -1912,7 +1912,7 @@ void ss_cache::PrefillAttention(int64_t seq, int64_t q_begin, int64_t q_end, int
   if (s != stream_) OrderUser(s);
   const bool ok = launch_prefill_attn(*reinterpret_cast<const PoolTensorMap*>(tmap_page_),
                                       *reinterpret_cast<const PoolTensorMap*>(tmap_row_), layer, P_,
-                                      rec->d_slots, q, static_cast<int>(q_begin),
+                                      num_pages_ * P_, rec->d_slots, q, static_cast<int>(q_begin),
                                       static_cast<int>(q_end - q_begin), hq, hkv, hd, scale, out, s);
   MKV_CHECK(ok, kInvalidArgument, "unsupported prefill attention shape");
   launches_ += 1;

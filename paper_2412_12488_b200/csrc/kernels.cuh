@@ -175,8 +175,9 @@ bool make_pool_tensor_map(void* pool, int64_t layers, int64_t rows, int64_t row_
 bool prefill_attn_supported(int page_size, int Hq, int Hkv, int D);
 int prefill_attn_box_rows(int page_size);  // rows of the page-chunk box
 bool launch_prefill_attn(const PoolTensorMap& page_map, const PoolTensorMap& row_map, int layer,
-                         int page_size, const int32_t* slots, const void* q, int q_pos0, int n_q,
-                         int Hq, int Hkv, int D, float scale, void* out, cudaStream_t s);
+                         int page_size, int64_t pool_rows, const int32_t* slots, const void* q,
+                         int q_pos0, int n_q, int Hq, int Hkv, int D, float scale, void* out,
+                         cudaStream_t s);
 
 // CRC-32 (IEEE, reflected) of n device bytes (crc32.cu): one launch, any
 // alignment and length; workspace of crc32_workspace_bytes(n) device bytes

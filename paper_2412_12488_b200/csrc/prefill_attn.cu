@@ -51,6 +51,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 
@@ -369,6 +370,7 @@ struct PrefillArgs {
   __nv_bfloat16* out;         // [n_q][Hq][128]
   int layer, page_size, q_pos0, n_q, Hq, Hkv, n_blocks;
   float scale_log2;
+  int pool_rows;              // rows of the pool tensor maps (an OOB row loads zeros)
 #ifdef PF_TRACE
   unsigned long long* trace;  // debug timeline of CTA (0, 0): [count][events]
 #endif
@@ -742,6 +744,442 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+
+// ===========================================================================
+// 2-SM variant (tcgen05 cta_group::2): a cluster of two CTAs on one TPC
+// computes S = Q K^T and O += P V for 256 query rows (2 x [16 tokens x 8
+// heads]) as M = 256 MMAs issued by the leader CTA.  Each CTA keeps its own
+// Q rows, S slots and O in its TMEM, but holds only half of each B operand
+// (K: its 64 of the tile's 128 keys; V: its 64 of the 128 head dims), so the
+// shared-memory traffic per SM per KV tile — the wall both single-CTA
+// layouts hit — drops from ~160 KiB to ~96 KiB.
+//   warps 0-3 softmax (own 128 rows), warp 4 K producer, warp 5 MMA (leader
+//   issues; both allocate TMEM), warp 6 V producer.
+// Cross-CTA signalling: TMA of both CTAs completes on the leader's full
+// barriers (peer bit cleared), the follower's softmax and Q loads arrive on
+// the leader's barriers through shared::cluster addresses, and the leader's
+// commits multicast to both CTAs' S-full / PV-done / stage-empty barriers.
+#ifndef PF2_POLY_EVERY
+#define PF2_POLY_EVERY 3
+#endif
+namespace p2 {
+constexpr int kKeys = 128;                // keys per KV tile
+constexpr int kHalfKeys = kKeys / 2;      // K rows held per CTA
+constexpr int kSlots = 3;                 // S slots (128 columns each) after O
+constexpr int kStages = 4;                // K and V rings
+constexpr int kKTile = kHalfKeys * 256;   // [64 keys][128 d] bf16, two atom columns: 16 KiB
+constexpr int kKAtom = kHalfKeys * 128;   // 8 KiB
+constexpr int kVTile = kKeys * 128;       // [128 keys][64 d] bf16, one atom column: 16 KiB
+constexpr int kThreads = 128 + 96;
+constexpr int kOffQ = 0;                  // [128][128] bf16, 32 KiB
+constexpr int kOffK = kOffQ + kTile;
+constexpr int kOffV = kOffK + kStages * kKTile;
+constexpr int kOffBar = kOffV + kStages * kVTile;
+constexpr int kSmem = kOffBar + 512;
+enum : int {
+  kBarQ = 0,                          // leader: both CTAs' Q rows staged (8 warps)
+  kBarKFull = 1,                      // leader: +stage, 2 arrivals + both CTAs' bytes
+  kBarVFull = kBarKFull + kStages,
+  kBarKEmpty = kBarVFull + kStages,   // both: +stage (multicast commit)
+  kBarVEmpty = kBarKEmpty + kStages,
+  kBarSFull = kBarVEmpty + kStages,   // both: +slot
+  kBarPFull = kBarSFull + kSlots,     // leader: +slot, one arrival per softmax warp (8)
+  kBarPVDone = kBarPFull + kSlots,    // both: +slot
+  kBarODone = kBarPVDone + kSlots,    // both
+  kBarCount = kBarODone + 1,
+};
+static_assert(kBarCount * 8 + 8 <= 512, "barrier area");
+static_assert(kSmem + 1024 <= 227 * 1024, "shared memory");
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// shared::cluster address of the same shared variable in CTA `rank`.
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+__device__ __forceinline__ void expect_tx_cluster(uint32_t cluster_addr, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(
+                   cluster_addr),
+               "r"(bytes)
+               : "memory");
+}
+// Bounded cluster-scope wait (a lost arrival traps instead of hanging).
+__device__ __forceinline__ void wait_cluster(uint32_t bar, uint32_t phase) {
+  uint32_t done = 0;
+  const long long t0 = clock64();
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(phase)
+        : "memory");
+    if (done) return;
+    if (clock64() - t0 > (4ll << 30)) __trap();
+  }
+}
+// 2-SM TMA: lands in this CTA's shared memory, completes bytes on the
+// leader's barrier (peer bit cleared).
+__device__ __forceinline__ void tma2_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                             int c2, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar & 0xFEFFFFFFu)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_ss(uint32_t tmem_d, uint32_t a_lo, uint32_t b_lo, uint32_t hi,
+                                        uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 da, db;\n\t"
+      "mov.b64 da, {%1, %3};\n\tmov.b64 db, {%2, %3};\n\t"
+      "setp.ne.b32 p, %5, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %4, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(a_lo), "r"(b_lo), "r"(hi), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma2_ts(uint32_t tmem_d, uint32_t tmem_a, uint32_t b_lo,
+                                        uint32_t b_hi, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 db;\n\t"
+      "mov.b64 db, {%2, %3};\n\t"
+      "setp.ne.b32 p, %5, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], db, %4, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate));
+}
+// Commit to the barrier at `bar` in both CTAs of the pair.
+__device__ __forceinline__ void commit2(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;\n\t}\n" ::"r"(bar),
+      "h"(static_cast<unsigned short>(3))
+      : "memory");
+}
+// D f32, A/B bf16, M = 256 (2 SMs), N = n, A K-major, B K- or MN-major.
+__host__ __device__ constexpr uint32_t idesc2(bool b_mn_major, int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn_major ? 1u : 0u) << 16) |
+         ((static_cast<uint32_t>(n) >> 3) << 17) | ((256u >> 4) << 24);
+}
+}  // namespace p2
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p2::kThreads, 1)
+    k_prefill_attn_2sm(const __grid_constant__ CUtensorMap pool_map,
+                       const __grid_constant__ CUtensorMap row_map, const PrefillArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = p2::cluster_rank();
+  const bool leader = rank == 0;
+  // Heaviest (latest) pair first; CTA `rank` takes the pair's token half.
+  const int pair = a.n_blocks - 1 - static_cast<int>(blockIdx.x >> 1);
+  const int h = blockIdx.y;
+  const uint32_t sQ = smem_u32(smem + p2::kOffQ), sK = smem_u32(smem + p2::kOffK);
+  const uint32_t sV = smem_u32(smem + p2::kOffV), bars = smem_u32(smem + p2::kOffBar);
+  auto bar = [&](int i) { return bars + 8u * static_cast<uint32_t>(i); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + p2::kOffBar + 8 * p2::kBarCount);
+  const int tok_pair = pair * 2 * kTokens;
+  const int tok_first = tok_pair + static_cast<int>(rank) * kTokens;
+  const int tok_last = min(a.n_q, tok_pair + 2 * kTokens) - 1;  // of the pair
+  const int n_keys = a.q_pos0 + tok_last + 1;
+  const int n_tiles = (n_keys + p2::kKeys - 1) / p2::kKeys;
+
+  if (warp == 5) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  if (tid == 128) {
+    mbar_init(bar(p2::kBarQ), 8);  // one arrival per softmax warp of either CTA
+    for (int s = 0; s < p2::kStages; ++s) {
+      mbar_init(bar(p2::kBarKFull + s), 2);
+      mbar_init(bar(p2::kBarVFull + s), 2);
+      mbar_init(bar(p2::kBarKEmpty + s), 1);
+      mbar_init(bar(p2::kBarVEmpty + s), 1);
+    }
+    for (int k = 0; k < p2::kSlots; ++k) {
+      mbar_init(bar(p2::kBarSFull + k), 1);
+      mbar_init(bar(p2::kBarPFull + k), 8);
+      mbar_init(bar(p2::kBarPVDone + k), 1);
+    }
+    mbar_init(bar(p2::kBarODone), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&pool_map))
+                 : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&row_map))
+                 : "memory");
+  }
+  fence_before();
+  p2::cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
+  fence_after();
+  constexpr uint32_t tmem = 0;
+  if (tid == 0 && *tmem_slot != 0u) __trap();
+
+  if (warp == 4 || warp == 6) {
+    // ---------------- producers ----------------
+    // K (warp 4): keys [j*128 + 64*rank, +64) of tile j, all 128 dims; lane
+    // l owns positions 2l, 2l+1.  V (warp 6): all 128 keys of tile j, dims
+    // [64*rank, +64); lane l owns 4l .. 4l+3.  Chunks of C = min(P, 64)
+    // consecutive rows are one box; otherwise rows one by one, and V rows
+    // past n_keys load an out-of-range row, which TMA fills with zeros.
+    const bool isK = warp == 4;
+    const int per_lane = isK ? 2 : 4;
+    const int C = min(a.page_size, 64), lanes_per_chunk = C / per_lane;
+    const uint32_t chunk_mask =
+        lanes_per_chunk >= 32 ? 0xffffffffu : ((1u << lanes_per_chunk) - 1u);
+    const int my_chunk_lane0 = lane - lane % lanes_per_chunk;
+    const int col = isK ? h * kD : (a.Hkv + h) * kD + 64 * static_cast<int>(rank);
+    const uint32_t lead_full = p2::mapa(bar(isK ? p2::kBarKFull : p2::kBarVFull), 0);
+    for (int j = 0; j < n_tiles; ++j) {
+      const int s = j % p2::kStages;
+      const int p0 = j * p2::kKeys + (isK ? 64 * static_cast<int>(rank) : 0) + lane * per_lane;
+      int sl[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        sl[t] = (t < per_lane && p0 + t < n_keys) ? __ldg(a.slots + p0 + t) : -1;
+      const int prev_last = __shfl_up_sync(0xffffffffu, sl[per_lane - 1], 1);
+      bool ok = true;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if (t >= per_lane) break;
+        const bool chunk_start = ((lane * per_lane + t) % C) == 0;
+        const int prev = t > 0 ? sl[t - 1] : prev_last;
+        if (sl[t] < 0) ok = isK ? ok : false;  // V: invalid rows must load zeros
+        else if (!chunk_start) ok = ok && sl[t] == prev + 1;
+      }
+      const uint32_t ballot = __ballot_sync(0xffffffffu, ok);
+      const bool contiguous = ((ballot >> my_chunk_lane0) & chunk_mask) == chunk_mask;
+      const int chunk_row = __shfl_sync(0xffffffffu, sl[0], my_chunk_lane0);
+      const uint32_t base = isK ? sK + s * p2::kKTile : sV + s * p2::kVTile;
+      const uint32_t bytes = isK ? p2::kKTile : p2::kVTile;
+      if (lane == 0) {
+        if (j >= p2::kStages)
+          mbar_wait(bar((isK ? p2::kBarKEmpty : p2::kBarVEmpty) + s), ((j / p2::kStages) + 1) & 1);
+        p2::expect_tx_cluster(lead_full + 8u * static_cast<uint32_t>(s), bytes);
+      }
+      __syncwarp();
+      const uint32_t full = bar((isK ? p2::kBarKFull : p2::kBarVFull) + s);
+      if (contiguous) {
+        if (lane == my_chunk_lane0) {
+          const uint32_t dst = base + (lane * per_lane) * 128;
+          const int row = chunk_row >= 0 ? chunk_row : 0;
+          p2::tma2_load_3d(dst, &pool_map, col, row, a.layer, full);
+          if (isK) p2::tma2_load_3d(dst + p2::kKAtom, &pool_map, col + 64, row, a.layer, full);
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          if (t >= per_lane) break;
+          const uint32_t dst = base + (lane * per_lane + t) * 128;
+          const int row = sl[t] >= 0 ? sl[t] : (isK ? 0 : a.pool_rows);
+          p2::tma2_load_3d(dst, &row_map, col, row, a.layer, full);
+          if (isK) p2::tma2_load_3d(dst + p2::kKAtom, &row_map, col + 64, row, a.layer, full);
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if (leader) {
+      // ---------------- MMA issuer (leader CTA) ----------------
+      constexpr uint32_t kIdescS = p2::idesc2(false, p2::kKeys), kIdescO = p2::idesc2(true, kD);
+      constexpr uint32_t kHi = desc_hi(1024);
+      auto tS = [&](int j) { return tmem + 128 + (j % p2::kSlots) * 128; };
+      const uint32_t q_lo = desc_lo(sQ, 16), k_lo = desc_lo(sK, 16), v_lo = desc_lo(sV, 16);
+      auto issue_s = [&](int j) {
+        const uint32_t b0 = k_lo + (((j % p2::kStages) * p2::kKTile) >> 4);
+#pragma unroll
+        for (int k = 0; k < kD / 16; ++k) {
+          const uint32_t ao = ((k >> 2) * kAtom + (k & 3) * 32) >> 4;
+          const uint32_t bo = ((k >> 2) * p2::kKAtom + (k & 3) * 32) >> 4;
+          p2::mma2_ss(tS(j), q_lo + ao, b0 + bo, kHi, kIdescS, k > 0 ? 1u : 0u);
+        }
+        p2::commit2(bar(p2::kBarSFull + j % p2::kSlots));
+      };
+      p2::wait_cluster(bar(p2::kBarQ), 0);
+      for (int j = 0; j < p2::kSlots && j < n_tiles; ++j) {
+        const int sk = j % p2::kStages;
+        p2::wait_cluster(bar(p2::kBarKFull + sk), (j / p2::kStages) & 1);
+        fence_after();
+        issue_s(j);
+        p2::commit2(bar(p2::kBarKEmpty + sk));
+      }
+      for (int j = 0; j < n_tiles; ++j) {
+        const int sv = j % p2::kStages;
+        p2::wait_cluster(bar(p2::kBarVFull + sv), (j / p2::kStages) & 1);
+        p2::wait_cluster(bar(p2::kBarPFull + j % p2::kSlots), (j / p2::kSlots) & 1);
+        fence_after();
+        const uint32_t b0 = v_lo + ((sv * p2::kVTile) >> 4);
+#pragma unroll
+        for (int k = 0; k < p2::kKeys / 16; ++k) {
+          // A = P in TMEM (8 columns per 16 keys); B = V MN-major, this CTA's
+          // 64 dims (one atom column), 16 keys = two 8-key groups (SBO 1 KiB).
+          p2::mma2_ts(tmem, tS(j) + k * 8, b0 + ((k * 2048) >> 4), kHi, kIdescO,
+                      (j > 0 || k > 0) ? 1u : 0u);
+        }
+        p2::commit2(bar(p2::kBarPVDone + j % p2::kSlots));
+        p2::commit2(bar(p2::kBarVEmpty + sv));
+        if (j == n_tiles - 1) p2::commit2(bar(p2::kBarODone));
+        const int jn = j + p2::kSlots;
+        if (jn < n_tiles) {
+          const int sk = jn % p2::kStages;
+          p2::wait_cluster(bar(p2::kBarKFull + sk), (jn / p2::kStages) & 1);
+          fence_after();
+          issue_s(jn);
+          p2::commit2(bar(p2::kBarKEmpty + sk));
+        }
+      }
+    }
+  } else {
+    // ---------------- softmax (warps 0-3, own 128 rows) ----------------
+    const int r = tid;
+    const int G = a.Hq / a.Hkv;
+    const int tok = tok_first + r / G, g = r % G;
+    const bool row_valid = tok < a.n_q;
+    const int q_pos = a.q_pos0 + tok;
+    const int tile_min_pos = a.q_pos0 + tok_first;
+    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    const uint32_t tO = tmem + lane_off;
+    const uint32_t lead_q = p2::mapa(bar(p2::kBarQ), 0);
+    const uint32_t lead_p = p2::mapa(bar(p2::kBarPFull), 0);
+    {
+      const __nv_bfloat16* qrow =
+          a.q + (static_cast<int64_t>(row_valid ? tok : 0) * a.Hq + static_cast<int64_t>(h) * G + g) * kD;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) cp_async16(sQ + sw128(r, c), qrow + c * 8, row_valid);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) p2::arrive_cluster(lead_q);
+    }
+    const float sl2 = a.scale_log2;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_tiles; ++j) {
+      const int slot = j % p2::kSlots;
+      const uint32_t tS = tmem + 128 + slot * 128 + lane_off;
+      mbar_wait(bar(p2::kBarSFull + slot), (j / p2::kSlots) & 1);
+      fence_after();
+      uint32_t sr[p2::kKeys];
+#pragma unroll
+      for (int c0 = 0; c0 < p2::kKeys; c0 += 16) tmem_ld16_nowait(tS + c0, sr + c0);
+      tmem_wait_ld();
+      const int key0 = j * p2::kKeys;
+      const bool need_mask =
+          __any_sync(0xffffffffu, key0 + p2::kKeys - 1 > tile_min_pos || !row_valid);
+      if (need_mask) {
+        const int lim = row_valid ? q_pos - key0 : -1;
+#pragma unroll
+        for (int c = 0; c < p2::kKeys; ++c)
+          sr[c] = c > lim ? __float_as_uint(-INFINITY) : sr[c];
+      }
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int c = 0; c < p2::kKeys; c += 8) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          mx[k] = fmaxf(mx[k], fmaxf(__uint_as_float(sr[c + 2 * k]), __uint_as_float(sr[c + 2 * k + 1])));
+      }
+      const float tmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * sl2;
+      const bool bump = tmax > m + 8.f;
+      const float m_new = bump ? tmax : m;
+      const float alpha = (bump && m != -INFINITY) ? ex2_mufu(m - m_new) : 1.f;
+      const float neg_m = m_new == -INFINITY ? 0.f : -m_new;
+      const uint64_t sc2 = f2pack(sl2, sl2), nm2 = f2pack(neg_m, neg_m);
+      uint64_t acc[2] = {0ull, 0ull};
+      // One softmax warp per SM sub-partition: in unmasked tiles every
+      // PF2_POLY_EVERY-th pair of exponentials runs on the FMA pipe.
+      auto make_p = [&](auto poly) {
+#pragma unroll
+        for (int c = 0; c < p2::kKeys; c += 2) {
+          float x0, x1, p0, p1;
+          f2unpack(ffma2(f2pack(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), sc2, nm2),
+                   x0, x1);
+          if (decltype(poly)::value && PF2_POLY_EVERY > 0 &&
+              ((c >> 1) % (PF2_POLY_EVERY > 0 ? PF2_POLY_EVERY : 1)) == PF2_POLY_EVERY - 1) {
+            ex2_poly2(x0, x1, p0, p1);
+          } else {
+            p0 = ex2_mufu(x0);
+            p1 = ex2_mufu(x1);
+          }
+          acc[(c >> 1) & 1] = fadd2(acc[(c >> 1) & 1], f2pack(p0, p1));
+          sr[c / 2] = pack_bf16(p0, p1);
+        }
+      };
+      if (need_mask) make_p(std::false_type{});
+      else make_p(std::true_type{});
+      float ps[4];
+      f2unpack(acc[0], ps[0], ps[1]);
+      f2unpack(acc[1], ps[2], ps[3]);
+      const float psum = (ps[0] + ps[1]) + (ps[2] + ps[3]);
+#pragma unroll
+      for (int c0 = 0; c0 < p2::kKeys / 2; c0 += 16) tmem_st16_nowait(tS + c0, sr + c0);
+      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+        mbar_wait(bar(p2::kBarPVDone + (j - 1) % p2::kSlots), ((j - 1) / p2::kSlots) & 1);
+        fence_after();
+#pragma unroll
+        for (int c0 = 0; c0 < kD; c0 += 32) {
+          uint32_t o[32];
+          tmem_ld16_nowait(tO + c0, o);
+          tmem_ld16_nowait(tO + c0 + 16, o + 16);
+          tmem_wait_ld();
+#pragma unroll
+          for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
+          tmem_st16_nowait(tO + c0, o);
+          tmem_st16_nowait(tO + c0 + 16, o + 16);
+        }
+      }
+      tmem_wait_st();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) p2::arrive_cluster(lead_p + 8u * static_cast<uint32_t>(slot));
+      l = l * alpha + psum;
+      m = m_new;
+    }
+    mbar_wait(bar(p2::kBarODone), 0);
+    fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    __nv_bfloat16* orow =
+        a.out + (static_cast<int64_t>(tok) * a.Hq + static_cast<int64_t>(h) * G + g) * kD;
+#pragma unroll
+    for (int c0 = 0; c0 < kD; c0 += 32) {
+      uint32_t o[32];
+      tmem_ld16_nowait(tO + c0, o);
+      tmem_ld16_nowait(tO + c0 + 16, o + 16);
+      tmem_wait_ld();
+      if (row_valid) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          auto pk = [&](int e) {
+            return pack_bf16(__uint_as_float(o[8 * k + e]) * inv,
+                             __uint_as_float(o[8 * k + e + 1]) * inv);
+          };
+          reinterpret_cast<uint4*>(orow + c0)[k] = make_uint4(pk(0), pk(2), pk(4), pk(6));
+        }
+      }
+    }
+  }
+  fence_before();
+  p2::cluster_sync();  // both CTAs done with TMEM and the peer's barriers
+  if (warp == 5) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -790,14 +1228,18 @@ bool prefill_attn_supported(int page_size, int Hq, int Hkv, int D) {
 int prefill_attn_box_rows(int page_size) { return page_size < kKeys ? page_size : kKeys; }
 
 bool launch_prefill_attn(const PoolTensorMap& page_map, const PoolTensorMap& row_map, int layer,
-                         int page_size, const int32_t* slots,
-                         const void* q, int q_pos0, int n_q, int Hq, int Hkv, int D, float scale,
-                         void* out, cudaStream_t s) {
+                         int page_size, int64_t pool_rows, const int32_t* slots, const void* q,
+                         int q_pos0, int n_q, int Hq, int Hkv, int D, float scale, void* out,
+                         cudaStream_t s) {
   if (!prefill_attn_supported(page_size, Hq, Hkv, D) || n_q <= 0) return false;
-  const int smem = kSmem + 1024;  // + alignment slack
+  // MICROKV_PREFILL_2SM=1: the CTA-pair kernel (A/B while it is evaluated).
+  const char* e2 = std::getenv("MICROKV_PREFILL_2SM");
+  const bool use_2sm = e2 != nullptr && e2[0] == '1';
   static bool attr = [] {
     return cudaFuncSetAttribute(k_prefill_attn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                kSmem + 1024) == cudaSuccess;
+                                kSmem + 1024) == cudaSuccess &&
+           cudaFuncSetAttribute(k_prefill_attn_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                p2::kSmem + 1024) == cudaSuccess;
   }();
   if (!attr) return false;
   PrefillArgs a;
@@ -810,19 +1252,25 @@ bool launch_prefill_attn(const PoolTensorMap& page_map, const PoolTensorMap& row
   a.n_q = n_q;
   a.Hq = Hq;
   a.Hkv = Hkv;
-  a.n_blocks = (n_q + kQTiles * kTokens - 1) / (kQTiles * kTokens);
+  a.n_blocks = (n_q + kQTiles * kTokens - 1) / (kQTiles * kTokens);  // 32 tokens per CTA / pair
   a.scale_log2 = scale * 1.4426950408889634f;
+  a.pool_rows = static_cast<int>(pool_rows);
   CUtensorMap m, mr;
   std::memcpy(&m, page_map.bytes, sizeof(m));
   std::memcpy(&mr, row_map.bytes, sizeof(mr));
-  const dim3 grid(a.n_blocks, Hkv);
 #ifdef PF_TRACE
   unsigned long long* tr = nullptr;
   cudaMalloc(&tr, 65536 * sizeof(unsigned long long));
   cudaMemset(tr, 0, 65536 * sizeof(unsigned long long));
   a.trace = tr;
 #endif
-  k_prefill_attn_tc<<<grid, kThreads, smem, s>>>(m, mr, a);
+  if (use_2sm) {
+    const dim3 grid(2 * a.n_blocks, Hkv);
+    k_prefill_attn_2sm<<<grid, p2::kThreads, p2::kSmem + 1024, s>>>(m, mr, a);
+  } else {
+    const dim3 grid(a.n_blocks, Hkv);
+    k_prefill_attn_tc<<<grid, kThreads, kSmem + 1024, s>>>(m, mr, a);
+  }
 #ifdef PF_TRACE
   cudaDeviceSynchronize();
   static unsigned long long h[65536];

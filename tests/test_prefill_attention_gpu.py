@@ -164,3 +164,12 @@ def test_prefill_rejects_bad_arguments(cuda):
     with pytest.raises(SplitserveError):
         c.paged_prefill_attention_async(99, (0, 8), 0, 64, 8, 128, 0.1, q.data_ptr(),
                                         q.data_ptr(), 0)
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_prefill_2sm_variant_matches_fp32_reference(cuda, case, monkeypatch):
+    """The CTA-pair (tcgen05 cta_group::2) variant, selected per launch by
+    MICROKV_PREFILL_2SM=1: same numerics bar (not the default, it
+    measured slower)."""
+    monkeypatch.setenv("MICROKV_PREFILL_2SM", "1")
+    test_prefill_matches_fp32_reference(cuda, case)
