@@ -94,9 +94,14 @@ __host__ __device__ __forceinline__ int64_t cta_tile_start(int64_t c, int64_t T,
 // Shared memory per CTA: [warp][stage][K|V][16][D] tiles, then Q [16][D]
 // (swizzled like the tiles; rows >= G zero).  The end-of-piece warp merge
 // reuses the tile area.
+#ifndef DA_STAGES
+#define DA_STAGES 2  // 2 measured best (3: -2..4%, 4: fewer resident CTAs, -25%)
+#endif
+constexpr int kStages = DA_STAGES;  // cp.async ring depth per warp (tiles in flight)
+
 template <int D>
 __host__ __device__ constexpr size_t tiles_bytes() {
-  return static_cast<size_t>(kWarps) * 4 * kTile * D * 2;
+  return static_cast<size_t>(kWarps) * 2 * kStages * kTile * D * 2;
 }
 
 template <int D>
@@ -152,7 +157,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_decode_attn(
     for (int j = 0; j < D / 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
     float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
 
-    uint8_t* wsm = smem + warp * (4 * kTileBytes);  // [stage][K|V][16][D]
+    uint8_t* wsm = smem + warp * (2 * kStages * kTileBytes);  // [stage][K|V][16][D]
     const int64_t k_off = static_cast<int64_t>(h) * D, v_off = static_cast<int64_t>(Hkv + h) * D;
     const uint32_t q_base = smem_u32(q_sm);
     // Lanes 0..15 hold the slot of row `lane` of a tile (fetched a tile ahead).
@@ -176,16 +181,22 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_decode_attn(
     };
 
     int my = 0;  // tiles of this piece handled by this warp: warp, warp + 4, ...
+    // Prologue: the first kStages - 1 tiles in flight.
     int32_t nxt = fetch_slot(warp);
-    if (warp < n_tiles) load_tile(warp, 0, nxt);
-    cp_async_commit();
-    nxt = fetch_slot(warp + kWarps);
-    for (int tile = warp; tile < n_tiles; tile += kWarps, ++my) {
-      const int stage = my & 1;
-      if (tile + kWarps < n_tiles) load_tile(tile + kWarps, stage ^ 1, nxt);
+#pragma unroll
+    for (int pre = 0; pre < kStages - 1; ++pre) {
+      const int t = warp + pre * kWarps;
+      if (t < n_tiles) load_tile(t, pre, nxt);
       cp_async_commit();
-      nxt = fetch_slot(tile + 2 * kWarps);
-      cp_async_wait<1>();
+      nxt = fetch_slot(t + kWarps);
+    }
+    for (int tile = warp; tile < n_tiles; tile += kWarps, ++my) {
+      const int stage = my % kStages;
+      const int ahead = tile + (kStages - 1) * kWarps;
+      if (ahead < n_tiles) load_tile(ahead, (my + kStages - 1) % kStages, nxt);
+      cp_async_commit();
+      nxt = fetch_slot(ahead + kWarps);
+      cp_async_wait<kStages - 1>();
       __syncwarp();
       const uint32_t kbase = smem_u32(wsm + stage * 2 * kTileBytes);
       const uint32_t vbase = kbase + kTileBytes;
@@ -411,7 +422,7 @@ __global__ void __launch_bounds__(kCombineThreads) k_decode_combine(
 }  // namespace
 
 size_t decode_attn_smem(int head_dim) {
-  const size_t tiles = static_cast<size_t>(kWarps) * 4 * kTile * head_dim * 2;
+  const size_t tiles = static_cast<size_t>(kWarps) * 2 * kStages * kTile * head_dim * 2;
   const size_t red = static_cast<size_t>(kWarps) * 16 * head_dim * 4 + kWarps * 16 * 2 * 4;
   return (tiles > red ? tiles : red) + static_cast<size_t>(kTile) * head_dim * 2;
 }
