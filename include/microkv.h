@@ -272,6 +272,9 @@ int ss_read_entry_words(ss_cache* cache, int64_t seq, int64_t pos, int32_t layer
 int ss_fill_of(ss_cache* cache, int64_t seq, int64_t pos, int32_t layer, int32_t* out);
 int64_t ss_free_pages(const ss_cache* cache);
 int64_t ss_total_pages(const ss_cache* cache);
+/* cache_config() (kv_cache.h:235) together with the model geometry the
+ * cache was created with (the ss_config it was created from). */
+int ss_cache_config(const ss_cache* cache, ss_config* out);
 int64_t ss_bytes_per_page(const ss_cache* cache);
 int64_t ss_sequence_count(const ss_cache* cache);
 int ss_sequence_ids(const ss_cache* cache, int64_t* out, int64_t cap, int64_t* n_out);

@@ -46,6 +46,7 @@ struct ss_cache {
   std::unique_ptr<KVCache> cache;
   std::string err;
   int32_t rank = 0;
+  ss_config cfg{};
   std::deque<int64_t> drained;  // completions not yet handed out
 };
 
@@ -131,6 +132,10 @@ int ss_cache_create(const ss_config* cfg, ss_cache** out) {
     c->model = std::make_unique<HashModel>(m);
     c->cache = std::make_unique<KVCache>(cc, c->model.get());
     c->rank = cfg->rank;
+    c->cfg = *cfg;
+    c->cfg.num_pages = c->cache->cache_config().num_pages;
+    c->cfg.page_size = c->cache->cache_config().page_size;
+    c->cfg.device = -1;
     return SS_OK;
   });
   if (st != SS_OK) return st;
@@ -391,6 +396,10 @@ int ss_fill_of(ss_cache* c, int64_t seq, int64_t pos, int32_t layer, int32_t* ou
 
 int64_t ss_free_pages(const ss_cache* c) { return c->cache->FreePages(); }
 int64_t ss_total_pages(const ss_cache* c) { return c->cache->TotalPages(); }
+int ss_cache_config(const ss_cache* c, ss_config* out) {  // cache_config(), kv_cache.h:235
+  *out = c->cfg;
+  return SS_OK;
+}
 int64_t ss_bytes_per_page(const ss_cache* c) { return c->cache->BytesPerPage(); }
 int64_t ss_sequence_count(const ss_cache* c) { return static_cast<int64_t>(c->cache->SequenceCount()); }
 int ss_sequence_ids(const ss_cache* c, int64_t* out, int64_t cap, int64_t* n_out) {

@@ -313,6 +313,18 @@ struct ss_cache {
   int32_t dim() const { return W_; }
   int32_t layers() const { return L_; }
   int32_t page_size() const { return P_; }
+  ss_config config() const {
+    ss_config c{};
+    c.num_pages = num_pages_;
+    c.page_size = P_;
+    c.layers = L_;
+    c.dim = W_;
+    c.vocab = vocab_;
+    c.hash_seed = hash_seed_;
+    c.device = device_;
+    c.rank = rank_;
+    return c;
+  }
   int device() const { return device_; }
   int64_t launches() const { return launches_; }
 

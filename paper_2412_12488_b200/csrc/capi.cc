@@ -317,6 +317,10 @@ int ss_fill_of(ss_cache* c, int64_t seq, int64_t pos, int32_t layer, int32_t* ou
 
 int64_t ss_free_pages(const ss_cache* c) { return c->FreePages(); }
 int64_t ss_total_pages(const ss_cache* c) { return c->TotalPages(); }
+int ss_cache_config(const ss_cache* c, ss_config* out) {
+  *out = c->config();
+  return SS_OK;
+}
 int64_t ss_bytes_per_page(const ss_cache* c) { return c->BytesPerPage(); }
 int64_t ss_sequence_count(const ss_cache* c) { return static_cast<int64_t>(c->SequenceCount()); }
 int ss_sequence_ids(const ss_cache* c, int64_t* out, int64_t cap, int64_t* n_out) {

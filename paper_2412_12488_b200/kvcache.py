@@ -189,6 +189,7 @@ _SIGNATURES = {
     "ss_fill_of": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int32, _i32p]),
     "ss_free_pages": (C.c_int64, [_vp]),
     "ss_total_pages": (C.c_int64, [_vp]),
+    "ss_cache_config": (C.c_int, [_vp, C.POINTER(_Config)]),
     "ss_bytes_per_page": (C.c_int64, [_vp]),
     "ss_sequence_count": (C.c_int64, [_vp]),
     "ss_sequence_ids": (C.c_int, [_vp, _i64p, C.c_int64, _i64p]),
@@ -794,6 +795,11 @@ class KVCache:
 
     def FreePages(self) -> int:
         return self._lib.ss_free_pages(self._h)
+
+    def cache_config(self) -> dict:  # kv_cache.h:235 (+ the model geometry)
+        c = _Config()
+        self._check(self._lib.ss_cache_config(self._h, C.byref(c)))
+        return {k: getattr(c, k) for k, _ in _Config._fields_}
 
     def TotalPages(self) -> int:
         return self._lib.ss_total_pages(self._h)

@@ -79,3 +79,12 @@ def test_host_only_cache_has_no_data_path(product_lib):
 def test_missing_product_library_fails_loudly(tmp_path):
     with pytest.raises(FileNotFoundError):
         load_library(tmp_path / "libmicrokv.so")
+
+
+def test_cache_config_mirrors_reference(product_lib, ref_lib):
+    """cache_config() (kv_cache.h:235) plus the model geometry, on both libraries."""
+    for lib in (product_lib, ref_lib):
+        E = KVCache(num_pages=12, page_size=8, layers=3, dim=16, device=-1, rank=2, lib=lib)
+        c = E.cache_config()
+        assert (c["num_pages"], c["page_size"], c["layers"], c["dim"], c["rank"]) == (12, 8, 3, 16, 2)
+        assert c["hash_seed"] == 0x5eed5eed5eed5eed and c["vocab"] == 256
