@@ -197,6 +197,7 @@ ss_cache::ss_cache(const ss_config& cfg)
     // Transfers get the higher priority so a layer's send is not starved by
     // the next layer's compute (the overlap of PAPER.md:339-344).
     CudaCheck(cudaStreamCreateWithPriority(&comm_stream_, cudaStreamNonBlocking, hi), "stream");
+    CudaCheck(cudaStreamCreateWithFlags(&recv_stream_, cudaStreamNonBlocking), "stream");
   }
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device_) == cudaSuccess) {
@@ -215,6 +216,7 @@ ss_cache::ss_cache(const ss_config& cfg)
   CudaCheck(cudaMalloc(&d_scratch_, 256), "cudaMalloc");
   CudaCheck(cudaHostAlloc(&h_pinned_, sizeof(unsigned long long) * kMaxWindows, 0), "pinned");
   CudaCheck(cudaHostAlloc(&h_stage_, kStageSlots * kStageBytes, 0), "pinned staging");
+  CudaCheck(cudaHostAlloc(&h_agent_pinned_, sizeof(uint32_t), 0), "pinned agent");
   for (auto& e : stage_ev_) CudaCheck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   // A fresh pool is zero-filled like the reference's (kv_cache.cc:37).
   CudaCheck(cudaMemsetAsync(d_pool_, 0, slots * L_ * W_ * 8, stream_), "memset");
@@ -264,6 +266,7 @@ ss_cache::~ss_cache() {
   if (device_ < 0) return;
   cudaSetDevice(device_);
   if (stream_) cudaStreamSynchronize(stream_);
+  if (recv_stream_) cudaStreamSynchronize(recv_stream_);
   for (auto& [r, p] : peers_) {
     for (void* ptr : p.ipc_ptrs) cudaIpcCloseMemHandle(ptr);
   }
@@ -277,6 +280,8 @@ ss_cache::~ss_cache() {
   cudaFree(d_status_);
   cudaFree(d_scratch_);
   cudaFreeHost(h_pinned_);
+  if (h_agent_pinned_ != nullptr) cudaFreeHost(h_agent_pinned_);
+  if (recv_stream_ != nullptr) cudaStreamDestroy(recv_stream_);
   if (h_stage_ != nullptr) {
     for (int i = 0; i < kStageSlots; ++i) {
       if (stage_used_[i]) cudaEventSynchronize(stage_ev_[i]);  // copies on user streams
@@ -527,7 +532,10 @@ Record* ss_cache::CreateSequence(SeqId seq, std::vector<Token> tokens) {
     launches_ += 1;
   }
   Record* out = rec.get();
-  records_[seq] = std::move(rec);
+  {
+    std::lock_guard<std::mutex> lock(recv_mu_);  // the transfer agent looks records up
+    records_[seq] = std::move(rec);
+  }
   return out;
 }
 
@@ -575,6 +583,7 @@ void ss_cache::EnsureAllocated(SeqId seq, int64_t upto) {
                 " free");
   const int64_t old_len = rec->alloc_len;
   if (need > 0) {
+    std::lock_guard<std::mutex> lock(recv_mu_);  // page_owner_ is read by the transfer agent
     rec->own_pages.reserve(rec->own_pages.size() + need);
     size_t at = rec->slots.size();
     rec->slots.resize(at + static_cast<size_t>(need) * P_);
@@ -1158,7 +1167,8 @@ void ss_cache::AppendRowsLayers(ss_plan* plan, int32_t lb, int32_t le, const voi
 // kv_cache.cc:409-463.  Validation, dedupe and window accounting are the
 // reference's, on the host; the scatter of Empty slots runs on the device.
 int ss_cache::ApplyRemoteWrite(const KVAddr& addr, int32_t layer, const uint64_t* payload,
-                               int64_t n_words, bool on_device, uint64_t tag, cudaStream_t s) {
+                               int64_t n_words, bool on_device, uint64_t tag, cudaStream_t s,
+                               bool agent) {
   MKV_CHECK(n_words == addr.token_count * W_, kInvalidArgument, "payload size mismatch");
   RequireDevice("ApplyRemoteWrite");
   MKV_CHECK(layer >= 0 && layer < L_, kInvalidArgument, "layer out of range");
@@ -1184,9 +1194,16 @@ int ss_cache::ApplyRemoteWrite(const KVAddr& addr, int32_t layer, const uint64_t
   ExpandAddr(addr, &dst, nullptr, nullptr, nullptr);
   const int64_t n = static_cast<int64_t>(dst.size());
   if (n > 0) {
-    cudaStream_t st = s ? s : stream_;
-    OrderAfterUser();
-    if (st != stream_) OrderUser(st);
+    // Host payload (the transfer agent, possibly on its own thread): the
+    // receive stream, after the windows opened so far; a device payload on a
+    // caller stream (executor thread): ordered with the executor's streams.
+    cudaStream_t st = agent ? recv_stream_ : (s ? s : stream_);
+    if (agent) {
+      CudaCheck(cudaStreamWaitEvent(st, window_ev_, 0), "wait window");
+    } else {
+      OrderAfterUser();
+      if (st != stream_) OrderUser(st);
+    }
     const size_t o_pay = Align(sizeof(int32_t) * n);
     DevBlock b = DevAlloc(o_pay + (on_device ? 0 : sizeof(uint64_t) * n_words), st);
     uint8_t* base = static_cast<uint8_t*>(b.ptr);
@@ -1209,7 +1226,9 @@ int ss_cache::ApplyRemoteWrite(const KVAddr& addr, int32_t layer, const uint64_t
     launch_copy_rows(c, st, num_sms_);
     launches_ += 1;
     DevFree(b, st);
-    if (st == stream_) {
+    if (agent) {
+      CudaCheck(cudaStreamSynchronize(st), "cudaStreamSynchronize recv");
+    } else if (st == stream_) {
       Sync();
     } else {
       NoteUser(st);
@@ -1525,6 +1544,7 @@ void ss_cache::FreeSequence(SeqId seq) {
     it = it->seq == seq ? pending_sends_.erase(it) : std::next(it);
   }
   tree_.Remove(seq);
+  std::lock_guard<std::mutex> lock(recv_mu_);
   records_.erase(seq);
 }
 

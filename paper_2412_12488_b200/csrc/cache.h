@@ -10,6 +10,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <deque>
 #include <map>
@@ -248,8 +249,11 @@ struct ss_cache {
                         cudaStream_t s);
 
   // Transfer agent.
+  // agent = the transfer agent's call (possibly another thread): the
+  // receive stream, ordered after the receive windows only.
   int ApplyRemoteWrite(const mkv::KVAddr& addr, int32_t layer, const uint64_t* payload,
-                       int64_t n_words, bool payload_on_device, uint64_t tag, cudaStream_t s);
+                       int64_t n_words, bool payload_on_device, uint64_t tag, cudaStream_t s,
+                       bool agent = false);
   std::vector<SeqId> DrainReceiveCompletions();
   void DirectSend(SeqId seq, int64_t begin, int64_t end, Rank dest, const mkv::KVAddr& addr,
                   uint64_t tag, int32_t layer_begin, int32_t layer_end, cudaStream_t s);
@@ -386,7 +390,7 @@ struct ss_cache {
   int device_;
   int32_t rank_;
   int num_sms_ = 148;
-  int64_t launches_ = 0;
+  std::atomic<int64_t> launches_{0};
 
   // Host bookkeeping.
   std::vector<int64_t> free_pages_;
@@ -413,6 +417,13 @@ struct ss_cache {
   // receive surface is exported to another process PrepRecv synchronizes.
   cudaEvent_t window_ev_ = nullptr;
   bool ipc_exported_ = false;
+  // The transfer agent's stream: host-payload ApplyRemoteWrite and
+  // ReceiveWriteFrame may run on another thread than the executor
+  // (kv_cache.h:12-15), so they use their own stream, ordered after the
+  // receive windows (window_ev_), and none of the executor's stream-ordering
+  // state.
+  cudaStream_t recv_stream_ = nullptr;
+  uint32_t* h_agent_pinned_ = nullptr;  // the agent's pinned readback word
   // Pinned staging ring for small host->device uploads (page tables, row
   // maps, window slots): a pageable cudaMemcpyAsync blocks the host while the
   // driver stages it; through the ring the call is a memcpy + an async copy.
@@ -427,7 +438,7 @@ struct ss_cache {
   uint64_t user_gen_ = 0, user_waited_gen_ = 0, comm_gen_ = 0, comm_waited_gen_ = 0;
   uint64_t internal_gen_ = 1, internal_recorded_gen_ = 0;
   std::map<cudaStream_t, uint64_t> user_stream_seen_;
-  int64_t h2d_bytes_ = 0, d2h_bytes_ = 0;
+  std::atomic<int64_t> h2d_bytes_{0}, d2h_bytes_{0};
   uint64_t* d_pool_ = nullptr;
   uint8_t* d_fill_ = nullptr;
   uint8_t* d_expecting_ = nullptr;

@@ -208,7 +208,8 @@ int ss_build_addr(ss_cache* c, int64_t seq, int64_t begin, int64_t end, ss_addr*
 int ss_apply_remote_write(ss_cache* c, const ss_addr* addr, int32_t layer, const uint64_t* payload,
                           int64_t n_words, uint64_t tag, int32_t* apply_status) {
   return Guard(c, [&]() -> int {
-    *apply_status = c->ApplyRemoteWrite(ToAddr(addr), layer, payload, n_words, false, tag, nullptr);
+    *apply_status =
+        c->ApplyRemoteWrite(ToAddr(addr), layer, payload, n_words, false, tag, nullptr, true);
     return SS_OK;
   });
 }

@@ -92,17 +92,18 @@ void ss_cache::ReceiveWriteFrame(const uint8_t* frame, int64_t size, uint8_t* ac
   MKV_CHECK(size >= 0, mkv::kInvalidArgument, "negative frame size");
   const mkv::FrameView f = mkv::DecodeFrameHeader(frame, static_cast<size_t>(size));
   MKV_CHECK(f.type == mkv::kFrameWrite, mkv::kInvalidArgument, "not a write frame");
-  cudaStream_t st = stream_;
-  OrderAfterUser();
+  // The transfer agent's stream (this may run on its own thread).
+  cudaStream_t st = recv_stream_;
   const size_t o_crc = Align256(f.payload_bytes);
   mkv::DevBlock stage = DevAlloc(o_crc + 256, st);
   auto* base = static_cast<uint8_t*>(stage.ptr);
   if (f.payload_bytes > 0) H2D(base, frame + f.payload_offset, f.payload_bytes, st, "H2D frame payload");
-  Crc32(base, static_cast<int64_t>(f.payload_bytes), reinterpret_cast<uint32_t*>(base + o_crc), st);
-  uint32_t crc = 0;
-  D2H(h_pinned_, base + o_crc, 4, st, "D2H frame crc");
-  Sync();
-  std::memcpy(&crc, h_pinned_, 4);
+  mkv::launch_crc32(base, static_cast<int64_t>(f.payload_bytes),
+                    reinterpret_cast<uint32_t*>(base + o_crc), nullptr, st, num_sms_);
+  launches_ += 1;
+  D2H(h_agent_pinned_, base + o_crc, 4, st, "D2H frame crc");
+  mkv::CudaCheck(cudaStreamSynchronize(st), "cudaStreamSynchronize recv");
+  const uint32_t crc = *h_agent_pinned_;
   uint8_t ack = mkv::kAckOk;
   int32_t status = -1;
   if (crc != f.wire_crc) {
@@ -110,7 +111,8 @@ void ss_cache::ReceiveWriteFrame(const uint8_t* frame, int64_t size, uint8_t* ac
   } else {
     try {
       status = ApplyRemoteWrite(f.addr, f.layer, reinterpret_cast<const uint64_t*>(base),
-                                static_cast<int64_t>(f.payload_bytes / 8), true, f.seq_tag, st);
+                                static_cast<int64_t>(f.payload_bytes / 8), true, f.seq_tag,
+                                nullptr, true);
     } catch (...) {
       DevFree(stage, st);
       throw;
