@@ -72,7 +72,7 @@ def test_transfer_agent_thread_beside_executor(cuda, rounds):
         # completion (each completion is handed out once): check the record.
         D.DrainReceiveCompletions()
         rec = D.GetRecord(1)
-        assert rec.finished and rec.window_complete and D.Committed(1) == e
+        assert rec.finished and rec.window and rec.window["complete"] and D.Committed(1) == e
         dig = hm.prefix_digests(a[:e])
         for layer in range(L):
             got = D.GatherRange(1, (0, e), layer).reshape(e, W)
