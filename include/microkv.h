@@ -391,6 +391,12 @@ int ss_pool_layer_ptr(ss_cache* cache, int32_t layer, void** dev_ptr);
  * trip.  Gives up after timeout_ms (sets the sticky status reported by
  * ss_synchronize as SS_ERR_ABORTED) so a lost sender cannot hang the GPU. */
 int ss_wait_receive_async(ss_cache* cache, int64_t seq, int64_t timeout_ms, void* stream);
+/* The same for one layer: the wait ends when every position of the window
+ * has landed for `layer` (the per-layer ready flag peers bump after each
+ * layer's rows), so the receiver can start layer-l work while later layers
+ * are still in flight (PAPER.md:339-344 on the receiving side). */
+int ss_wait_receive_layer_async(ss_cache* cache, int64_t seq, int32_t layer, int64_t timeout_ms,
+                                void* stream);
 /* Host<->device bytes this cache has copied (evidence counters). */
 int ss_copy_counters(const ss_cache* cache, int64_t* h2d_bytes, int64_t* d2h_bytes);
 /* Number of kernel launches this cache has issued (evidence counter). */

@@ -483,6 +483,9 @@ int ss_paged_prefill_attention_async(ss_cache*, int64_t, int64_t, int64_t, int32
 }
 int ss_pool_layer_ptr(ss_cache*, int32_t, void**) { return SS_ERR_UNSUPPORTED; }
 int ss_wait_receive_async(ss_cache*, int64_t, int64_t, void*) { return SS_ERR_UNSUPPORTED; }
+int ss_wait_receive_layer_async(ss_cache*, int64_t, int32_t, int64_t, void*) {
+  return SS_ERR_UNSUPPORTED;
+}
 int ss_copy_counters(const ss_cache*, int64_t* h2d, int64_t* d2h) {
   *h2d = 0;
   *d2h = 0;

@@ -185,6 +185,18 @@ ss_cache::ss_cache(const ss_config& cfg)
   int sms = 0;
   CudaCheck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_), "sm count");
   num_sms_ = sms;
+  {
+    // Once per device per process: load every kernel before any receiver
+    // can spin on a window counter (mkv::preload_kernels).
+    static std::mutex mu;
+    static std::vector<bool> loaded;
+    std::lock_guard<std::mutex> g(mu);
+    if (loaded.size() <= static_cast<size_t>(device_)) loaded.resize(device_ + 1, false);
+    if (!loaded[device_]) {
+      mkv::preload_kernels();
+      loaded[device_] = true;
+    }
+  }
   CudaCheck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
   CudaCheck(cudaEventCreateWithFlags(&internal_ev_, cudaEventDisableTiming), "event");
   CudaCheck(cudaEventCreateWithFlags(&user_ev_, cudaEventDisableTiming), "event");
@@ -634,6 +646,7 @@ int64_t ss_cache::PrepRecv(SeqId seq, std::vector<Token> tokens, int64_t end, KV
       w.begin = m;
       w.end = e;
       w.expected = (e - m) * L_;
+      w.received_layer.assign(L_, 0);
       rec->window = std::move(w);
     }
     if (device_ >= 0) OpenDeviceWindow(rec, m, e);
@@ -1236,6 +1249,7 @@ int ss_cache::ApplyRemoteWrite(const KVAddr& addr, int32_t layer, const uint64_t
   }
   // Every addressed slot counts, filled or not (kv_cache.cc:452-456).
   win.received += n;
+  if (static_cast<int32_t>(win.received_layer.size()) == L_) win.received_layer[layer] += n;
   if (!win.complete && win.received + static_cast<int64_t>(win.dev_received) >= win.expected) {
     win.complete = true;
     completed_windows_.push_back(owner);
@@ -1766,6 +1780,27 @@ void ss_cache::WaitReceive(SeqId seq, int64_t timeout_ms, cudaStream_t s) {
   if (s != stream_) OrderUser(s);
   launch_wait_counter(d_win_received_ + w.dev_id, static_cast<unsigned long long>(target),
                       timeout_ms * 1000000LL, d_status_, s);
+  launches_ += 1;
+  if (s != stream_) NoteUser(s);
+}
+
+void ss_cache::WaitReceiveLayer(SeqId seq, int32_t layer, int64_t timeout_ms, cudaStream_t s) {
+  RequireDevice("WaitReceive");
+  MKV_CHECK(layer >= 0 && layer < L_, kInvalidArgument, "layer out of range");
+  Record* rec = MustGet(seq);
+  MKV_CHECK(rec->window.has_value() && rec->window->dev_id >= 0, kInvalidArgument,
+            "sequence " + std::to_string(seq) + " has no receive window");
+  const Window& w = *rec->window;
+  int64_t host_rows = 0;
+  {
+    std::lock_guard<std::mutex> lock(recv_mu_);
+    if (static_cast<int32_t>(w.received_layer.size()) == L_) host_rows = w.received_layer[layer];
+  }
+  const int64_t target = std::max<int64_t>(0, (w.end - w.begin) - host_rows);
+  OrderAfterUser();
+  if (s != stream_) OrderUser(s);
+  launch_wait_counter32(d_win_layer_rows_ + static_cast<int64_t>(w.dev_id) * L_ + layer,
+                        static_cast<uint32_t>(target), timeout_ms * 1000000LL, d_status_, s);
   launches_ += 1;
   if (s != stream_) NoteUser(s);
 }

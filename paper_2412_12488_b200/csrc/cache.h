@@ -92,6 +92,7 @@ struct Window {
   int64_t begin = 0, end = 0;
   int64_t expected = 0;      // (e - m) * L slot writes
   int64_t received = 0;      // host-path writes (ApplyRemoteWrite)
+  std::vector<int64_t> received_layer;  // host-path writes per layer
   uint64_t dev_received = 0; // device-direct writes last read from HBM
   bool complete = false;
   std::set<std::tuple<uint64_t, int32_t, int64_t>> applied;  // (tag, layer, token_begin)
@@ -310,6 +311,7 @@ struct ss_cache {
   void FreePlanDevice(ss_plan* plan);
   void Synchronize();
   void WaitReceive(SeqId seq, int64_t timeout_ms, cudaStream_t s);
+  void WaitReceiveLayer(SeqId seq, int32_t layer, int64_t timeout_ms, cudaStream_t s);
   int64_t h2d_bytes() const { return h2d_bytes_; }
   int64_t d2h_bytes() const { return d2h_bytes_; }
   uint64_t* PoolLayer(int32_t layer) const;

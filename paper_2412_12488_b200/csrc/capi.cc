@@ -507,6 +507,14 @@ int ss_wait_receive_async(ss_cache* c, int64_t seq, int64_t timeout_ms, void* st
   });
 }
 
+int ss_wait_receive_layer_async(ss_cache* c, int64_t seq, int32_t layer, int64_t timeout_ms,
+                                void* stream) {
+  return Guard(c, [&]() -> int {
+    c->WaitReceiveLayer(seq, layer, timeout_ms, S(stream));
+    return SS_OK;
+  });
+}
+
 int ss_copy_counters(const ss_cache* c, int64_t* h2d, int64_t* d2h) {
   *h2d = c->h2d_bytes();
   *d2h = c->d2h_bytes();

@@ -306,4 +306,10 @@ void launch_crc32(const void* data, int64_t n, uint32_t* out, void*, cudaStream_
   k_crc32<<<static_cast<unsigned>(pl.grid), kCrcThreads, kCrcSmem, s>>>(p);
 }
 
+
+void preload_crc32_kernels() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, k_crc32);
+}
+
 }  // namespace mkv

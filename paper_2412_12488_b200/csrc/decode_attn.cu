@@ -485,4 +485,12 @@ bool launch_decode_attn(const void* pool_l, int64_t row_elems, const int32_t* sl
   return true;
 }
 
+
+void preload_decode_attn_kernels() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, k_decode_attn<128>);
+  cudaFuncGetAttributes(&a, k_decode_attn<64>);
+  cudaFuncGetAttributes(&a, k_decode_combine);
+}
+
 }  // namespace mkv

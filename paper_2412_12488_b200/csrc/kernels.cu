@@ -528,6 +528,23 @@ __global__ void k_wait_counter(const unsigned long long* counter, unsigned long 
   }
 }
 
+__global__ void k_wait_counter32(const uint32_t* counter, uint32_t target, long long timeout_ns,
+                                 uint32_t* status) {
+  unsigned long long t0, now;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+    if (v >= target) return;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (static_cast<long long>(now - t0) > timeout_ns) {
+      atomicOr(status, kStatusWaitTimeout);
+      return;
+    }
+    __nanosleep(200);
+  }
+}
+
 inline int grid_for(int64_t work, int per_block, int num_sms, int max_per_sm) {
   int64_t blocks = (work + per_block - 1) / per_block;
   int64_t cap = static_cast<int64_t>(num_sms) * max_per_sm;
@@ -648,6 +665,11 @@ void launch_wait_counter(const unsigned long long* counter, unsigned long long t
   k_wait_counter<<<1, 1, 0, s>>>(counter, target, timeout_ns, status);
 }
 
+void launch_wait_counter32(const uint32_t* counter, uint32_t target, long long timeout_ns,
+                           uint32_t* status, cudaStream_t s) {
+  k_wait_counter32<<<1, 1, 0, s>>>(counter, target, timeout_ns, status);
+}
+
 void launch_gather_tables(const int32_t* const* tables, const int64_t* off, const int32_t* len,
                           int64_t batch, int64_t total, int32_t* out, cudaStream_t s, int num_sms) {
   if (batch <= 0 || total <= 0) return;
@@ -662,6 +684,36 @@ void launch_check_filled(const uint8_t* fill_l, const int32_t* slots, int64_t n,
                          cudaStream_t s, int num_sms) {
   if (n <= 0) return;
   k_check_filled<<<grid_for(n, 256, num_sms, 4), 256, 0, s>>>(fill_l, slots, n, status);
+}
+
+
+// Lazy module loading (the CUDA 12 default) loads a kernel at its first
+// launch, and a load can wait for the device to go idle.  A receiver that
+// spins in k_wait_counter32 until a sender's first-ever k_copy_rows lands
+// would then hang until its timeout, so every kernel of the library is
+// loaded up front when a device cache is created.
+void preload_kernels() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, k_copy_rows<4>);
+  cudaFuncGetAttributes(&a, k_copy_rows<1>);
+  cudaFuncGetAttributes(&a, k_copy_rows<0>);
+  cudaFuncGetAttributes(&a, k_copy_rows_fanout<4>);
+  cudaFuncGetAttributes(&a, k_copy_rows_fanout<1>);
+  cudaFuncGetAttributes(&a, k_validate_remote);
+  cudaFuncGetAttributes(&a, k_attn_write_hash);
+  cudaFuncGetAttributes(&a, k_entry_digest);
+  cudaFuncGetAttributes(&a, k_fold_scan);
+  cudaFuncGetAttributes(&a, k_reset_pages);
+  cudaFuncGetAttributes(&a, k_open_window);
+  cudaFuncGetAttributes(&a, k_first_nonfull);
+  cudaFuncGetAttributes(&a, k_gather_tables);
+  cudaFuncGetAttributes(&a, k_check_filled);
+  cudaFuncGetAttributes(&a, k_wait_counter);
+  cudaFuncGetAttributes(&a, k_wait_counter32);
+  preload_decode_attn_kernels();
+  preload_prefill_attn_kernels();
+  preload_crc32_kernels();
+  cudaGetLastError();
 }
 
 }  // namespace mkv

@@ -27,6 +27,14 @@ enum : uint32_t {
 
 // Device-side wait: spin (acquire, system scope) until *counter >= target
 // or timeout_ns elapses; on timeout set kStatusWaitTimeout.
+// Load every kernel of the library into the current context (see kernels.cu).
+void preload_kernels();
+void preload_decode_attn_kernels();
+void preload_prefill_attn_kernels();
+void preload_crc32_kernels();
+
+void launch_wait_counter32(const uint32_t* counter, uint32_t target, long long timeout_ns,
+                           uint32_t* status, cudaStream_t s);
 void launch_wait_counter(const unsigned long long* counter, unsigned long long target,
                          long long timeout_ns, uint32_t* status, cudaStream_t s);
 

@@ -1285,4 +1285,11 @@ bool launch_prefill_attn(const PoolTensorMap& page_map, const PoolTensorMap& row
   return true;
 }
 
+
+void preload_prefill_attn_kernels() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, k_prefill_attn_tc);
+  cudaFuncGetAttributes(&a, k_prefill_attn_2sm);
+}
+
 }  // namespace mkv

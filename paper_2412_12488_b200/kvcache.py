@@ -227,6 +227,7 @@ _SIGNATURES = {
                                                    C.c_float, _vp, _vp, _vp]),
     "ss_pool_layer_ptr": (C.c_int, [_vp, C.c_int32, C.POINTER(_vp)]),
     "ss_wait_receive_async": (C.c_int, [_vp, C.c_int64, C.c_int64, _vp]),
+    "ss_wait_receive_layer_async": (C.c_int, [_vp, C.c_int64, C.c_int32, C.c_int64, _vp]),
     "ss_copy_counters": (C.c_int, [_vp, _i64p, _i64p]),
     "ss_kernel_launches": (C.c_int64, [_vp]),
     "ss_synchronize": (C.c_int, [_vp]),
@@ -1025,6 +1026,13 @@ class KVCache:
 
     def wait_receive_async(self, seq: int, timeout_ms: int = 10000, stream: int = 0) -> None:
         self._check(self._lib.ss_wait_receive_async(self._h, seq, timeout_ms, C.c_void_p(stream)))
+
+    def wait_receive_layer_async(self, seq: int, layer: int, timeout_ms: int = 10000,
+                                 stream: int = 0) -> None:
+        """Device-side wait on `stream` until layer `layer` of seq's receive
+        window has fully landed (the per-layer ready flag)."""
+        self._check(self._lib.ss_wait_receive_layer_async(self._h, seq, layer, timeout_ms,
+                                                          C.c_void_p(stream)))
 
     def copy_counters(self) -> tuple[int, int]:
         h, d = C.c_int64(), C.c_int64()
