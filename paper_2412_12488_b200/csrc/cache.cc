@@ -394,6 +394,21 @@ void ss_cache::OrderUser(cudaStream_t s) {
   user_stream_seen_[s] = internal_recorded_gen_;
 }
 
+// A launch on user stream s that enqueues nothing on the internal stream:
+// s waits only for internal work enqueued since it last waited (nothing, in
+// a steady per-layer loop), and NoteUser afterwards orders later internal
+// work after it.  No internal-stream round trip per launch: that pair of
+// cross-stream dependencies had cost ~10 us of device time per launch.
+// Work on two different user streams is not ordered by the library (use
+// CUDA events, as with any stream).
+void ss_cache::OrderLaunch(cudaStream_t s) {
+  if (s == stream_) {
+    OrderAfterUser();
+    return;
+  }
+  OrderUser(s);
+}
+
 void ss_cache::NoteUser(cudaStream_t s) {
   CudaCheck(cudaEventRecord(user_ev_, s), "cudaEventRecord");
   user_pending_ = true;
@@ -958,9 +973,9 @@ void ss_cache::AttentionAsync(ss_plan* plan, int32_t layer, const uint64_t* hin,
   MKV_CHECK(layer == plan->next_layer && layer < L_, kLayerOrderViolation,
             "expected layer " + std::to_string(plan->next_layer) + ", got " +
                 std::to_string(layer));
-  OrderAfterUser();
+  if (!plan->on_device) OrderAfterUser();  // the upload follows earlier user work
   PlanToDevice(plan);
-  if (s != stream_) OrderUser(s);
+  OrderLaunch(s);
   uint64_t* pool_l = PoolLayer(layer);
   uint8_t* fill_l = d_fill_ + static_cast<int64_t>(layer) * num_pages_ * P_;
   // Hot loop A: KV write for Empty output slots, entry digests, fold + hidden.
@@ -1092,8 +1107,7 @@ void ss_cache::GatherRange(SeqId seq, int64_t begin, int64_t end, int32_t layer,
   CheckFilled(rec, begin, end, layer, "gather over empty slot", nullptr);
   const int64_t n = end - begin;
   if (n == 0) return;
-  OrderAfterUser();
-  if (s != stream_) OrderUser(s);
+  OrderLaunch(s);
   CopyParams c{};
   c.src = PoolLayer(layer);
   c.src_idx = rec->d_slots + begin;
@@ -1149,9 +1163,9 @@ void ss_cache::AppendRowsLayers(ss_plan* plan, int32_t lb, int32_t le, const voi
                                 cudaStream_t s) {
   RequireDevice("AppendRows");
   MKV_CHECK(lb >= 0 && lb < le && le <= L_, kInvalidArgument, "layer out of range");
-  OrderAfterUser();
+  if (!plan->on_device) OrderAfterUser();  // the upload follows earlier user work
   PlanToDevice(plan);
-  if (s != stream_) OrderUser(s);
+  OrderLaunch(s);
   CopyParams c{};
   c.src = static_cast<const uint64_t*>(rows);
   c.src_layer_words = plan->total_outputs * W_;
@@ -1214,8 +1228,7 @@ int ss_cache::ApplyRemoteWrite(const KVAddr& addr, int32_t layer, const uint64_t
     if (agent) {
       CudaCheck(cudaStreamWaitEvent(st, window_ev_, 0), "wait window");
     } else {
-      OrderAfterUser();
-      if (st != stream_) OrderUser(st);
+      OrderLaunch(st);
     }
     const size_t o_pay = Align(sizeof(int32_t) * n);
     DevBlock b = DevAlloc(o_pay + (on_device ? 0 : sizeof(uint64_t) * n_words), st);
@@ -1378,8 +1391,7 @@ void ss_cache::LaunchDirectSend(ss_plan* plan, int32_t lb, int32_t le, cudaStrea
   }
   if (lb == le) return;
   const PeerTarget& peer = PeerFor(snd.dest);
-  OrderAfterUser();
-  if (s != stream_) OrderUser(s);
+  OrderLaunch(s);
   const auto& d = plan->dsend[0];
   LaunchRemote(peer, rec->d_slots + snd.begin, d.dst_slots, d.range_page, d.range_begin,
                d.range_count, static_cast<int64_t>(snd.dest_addr.ranges.size()), d.verdict,
@@ -1444,8 +1456,7 @@ void ss_cache::BroadcastSend(SeqId seq, int64_t begin, int64_t end, int32_t n_de
     std::memcpy(host.data() + lay[d].rb, lay[d].rb_.data(), sizeof(int32_t) * lay[d].rb_.size());
     std::memcpy(host.data() + lay[d].rc, lay[d].rc_.data(), sizeof(int32_t) * lay[d].rc_.size());
   }
-  OrderAfterUser();
-  if (s != stream_) OrderUser(s);
+  OrderLaunch(s);
   DevBlock b = DevAlloc(off, s);
   uint8_t* base = static_cast<uint8_t*>(b.ptr);
   H2D(base, host.data(), off, s, "H2D broadcast");
@@ -1776,8 +1787,7 @@ void ss_cache::WaitReceive(SeqId seq, int64_t timeout_ms, cudaStream_t s) {
             "sequence " + std::to_string(seq) + " has no receive window");
   const Window& w = *rec->window;
   const int64_t target = std::max<int64_t>(0, w.expected - w.received);
-  OrderAfterUser();
-  if (s != stream_) OrderUser(s);
+  OrderLaunch(s);
   launch_wait_counter(d_win_received_ + w.dev_id, static_cast<unsigned long long>(target),
                       timeout_ms * 1000000LL, d_status_, s);
   launches_ += 1;
@@ -1797,8 +1807,7 @@ void ss_cache::WaitReceiveLayer(SeqId seq, int32_t layer, int64_t timeout_ms, cu
     if (static_cast<int32_t>(w.received_layer.size()) == L_) host_rows = w.received_layer[layer];
   }
   const int64_t target = std::max<int64_t>(0, (w.end - w.begin) - host_rows);
-  OrderAfterUser();
-  if (s != stream_) OrderUser(s);
+  OrderLaunch(s);
   launch_wait_counter32(d_win_layer_rows_ + static_cast<int64_t>(w.dev_id) * L_ + layer,
                         static_cast<uint32_t>(target), timeout_ms * 1000000LL, d_status_, s);
   launches_ += 1;
@@ -1906,6 +1915,7 @@ void ss_cache::DecodeAttention(ss_plan* plan, int32_t layer, int32_t hq, int32_t
       for (int32_t h = 0; h < hkv; ++h) seg[b * hkv + h + 1] = seg[b * hkv + h] + tiles;
     }
     plan->total_tiles = seg[n_seg];
+    OrderAfterUser();  // internal upload below; OrderLaunch then orders s after it
     Sync();
     if (plan->d_partial) cudaFree(plan->d_partial);
     const int64_t pieces = plan->decode_grid + n_seg;
@@ -1921,8 +1931,7 @@ void ss_cache::DecodeAttention(ss_plan* plan, int32_t layer, int32_t hq, int32_t
     plan->decode_hq = hq;
     plan->decode_hd = hd;
   }
-  OrderAfterUser();
-  if (s != stream_) OrderUser(s);
+  OrderLaunch(s);
   const bool ok = launch_decode_attn(PoolLayer(layer), static_cast<int64_t>(W_) * 4,
                                      plan->d_ctx_slots, plan->d_ctx_off, plan->d_ctx_len,
                                      plan->d_seg_start, plan->batch * hkv, plan->total_tiles, q,
@@ -1930,6 +1939,7 @@ void ss_cache::DecodeAttention(ss_plan* plan, int32_t layer, int32_t hq, int32_t
                                      plan->d_partial, plan->d_partial_ml, out, plan->decode_grid,
                                      s);
   MKV_CHECK(ok, kInvalidArgument, "unsupported head_dim");
+  CudaCheck(cudaPeekAtLastError(), "decode attention launch");
   launches_ += 2;
   if (s != stream_) NoteUser(s);
 }
@@ -1963,13 +1973,13 @@ void ss_cache::PrefillAttention(int64_t seq, int64_t q_begin, int64_t q_end, int
       mkv::ThrowStatus(SS_ERR_CUDA, "cuTensorMapEncodeTiled failed for the pool");
     tmaps_ready_ = true;
   }
-  OrderAfterUser();
-  if (s != stream_) OrderUser(s);
+  OrderLaunch(s);
   const bool ok = launch_prefill_attn(*reinterpret_cast<const PoolTensorMap*>(tmap_page_),
                                       *reinterpret_cast<const PoolTensorMap*>(tmap_row_), layer, P_,
                                       num_pages_ * P_, rec->d_slots, q, static_cast<int>(q_begin),
                                       static_cast<int>(q_end - q_begin), hq, hkv, hd, scale, out, s);
   MKV_CHECK(ok, kInvalidArgument, "unsupported prefill attention shape");
+  CudaCheck(cudaPeekAtLastError(), "prefill attention launch");
   launches_ += 1;
   if (s != stream_) NoteUser(s);
 }

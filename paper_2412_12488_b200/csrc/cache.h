@@ -356,6 +356,7 @@ struct ss_cache {
   void OrderAfterUser();             // internal stream waits for async work
   void OrderUser(cudaStream_t s);    // user stream waits for internal work
   void NoteUser(cudaStream_t s);
+  void OrderLaunch(cudaStream_t s);  // user-stream launch: s after internal work
   mkv::DevBlock DevAlloc(size_t bytes, cudaStream_t s);
   void DevFree(mkv::DevBlock& b, cudaStream_t s);
   void PlanToDevice(ss_plan* plan);

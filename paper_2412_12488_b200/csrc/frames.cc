@@ -16,8 +16,7 @@ size_t Align256(size_t x) { return (x + 255) & ~size_t(255); }
 void ss_cache::Crc32(const void* data_dev, int64_t n, uint32_t* crc_dev, cudaStream_t s) {
   RequireDevice("Crc32");
   MKV_CHECK(n >= 0, mkv::kInvalidArgument, "negative length");
-  OrderAfterUser();
-  if (s != stream_) OrderUser(s);
+  OrderLaunch(s);
   mkv::DevBlock ws = DevAlloc(mkv::crc32_workspace_bytes(n, num_sms_), s);
   mkv::launch_crc32(data_dev, n, crc_dev, ws.ptr, s, num_sms_);
   launches_ += 1;
@@ -51,8 +50,7 @@ int64_t ss_cache::EncodeWriteFrame(SeqId seq, int64_t begin, int64_t end, int32_
               "device frame: payload (frame + header bytes) must be 32-byte aligned");
     // Gather straight into the frame; header and CRC bytes around it.
     GatherRange(seq, begin, end, layer, reinterpret_cast<uint64_t*>(frame + hdr), s);
-    OrderAfterUser();
-    if (s != stream_) OrderUser(s);
+    OrderLaunch(s);
     mkv::DevBlock tmp = DevAlloc(256, s);
     H2D(frame, header.data(), hdr, s, "H2D frame header");
     mkv::DevBlock ws = DevAlloc(mkv::crc32_workspace_bytes(static_cast<int64_t>(payload), num_sms_), s);

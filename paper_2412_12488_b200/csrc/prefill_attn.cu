@@ -53,6 +53,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <type_traits>
 
 #include "kernels.cuh"
@@ -1198,6 +1199,704 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
+
+// ===========================================================================
+// 128-key variant (MICROKV_PREFILL_VARIANT=3 while it is evaluated): the
+// same CTA (one KV head x two M=128 query tiles) with 128-key KV tiles and
+// ONE S slot per query tile (TMEM: S_i at 128 i, O_i at 256 + 128 i).  The
+// S MMAs run at N = 128 instead of 64, which halves the shared-memory reads
+// of Q per key (A is re-read per MMA): per 128 keys and both tiles ~128 B/clk
+// of operand traffic instead of ~160.  S_i(j+1) is issued right behind
+// PV_i(j) into the columns P_i(j) occupied (MMAs of one thread run in
+// order), so the S-full barrier of tile j+1 also proves PV_i(j) retired and
+// the O rescale needs no separate wait; the two query tiles ping-pong: one
+// tile's softmax runs while the tensor core works on the other's PV and S.
+namespace p3 {
+constexpr int kKeys = 128;
+constexpr int kPer = kKeys / 32;          // tile positions per producer lane
+constexpr int kKvAtom = kKeys * 128;      // atom column of a [128][128] K or V tile (16 KiB)
+constexpr int kKvTile = 2 * kKvAtom;      // 32 KiB
+#ifndef PF3_K_STAGES
+#define PF3_K_STAGES 2
+#endif
+#ifndef PF3_V_STAGES
+#define PF3_V_STAGES 2
+#endif
+#ifndef PF3_POLY_EVERY
+#define PF3_POLY_EVERY 4
+#endif
+constexpr int kStagesK = PF3_K_STAGES, kStagesV = PF3_V_STAGES;
+constexpr int kOffQ = 0;
+constexpr int kOffK = kOffQ + kQTiles * kTile;
+constexpr int kOffV = kOffK + kStagesK * kKvTile;
+constexpr int kOffBar = kOffV + kStagesV * kKvTile;
+constexpr int kSmem = kOffBar + 512;
+// Split-row softmax variant (k_prefill_attn_k128s): 16 softmax warps.
+constexpr int kSoftmaxThreadsS = 512;
+constexpr int kThreadsS = kSoftmaxThreadsS + 96;
+constexpr int kOffRed = kOffBar + 512;          // row max / sum exchange, 6 x [2][128] floats
+constexpr int kSmemS = kOffRed + 6 * 2 * 128 * 4;
+enum : int {
+  kBarQ = 0,
+  kBarKFull = 1,
+  kBarVFull = kBarKFull + kStagesK,
+  kBarKEmpty = kBarVFull + kStagesV,
+  kBarVEmpty = kBarKEmpty + kStagesK,
+  kBarSFull = kBarVEmpty + kStagesV,  // +tile
+  kBarPFull = kBarSFull + 2,          // +tile (count 128)
+  kBarODone = kBarPFull + 2,          // +tile
+  kBarCount = kBarODone + 2,
+};
+static_assert(kBarCount * 8 + 8 <= 512, "barrier area");
+static_assert(kSmem + 1024 <= 227 * 1024, "shared memory");
+static_assert(kSmemS + 1024 <= 227 * 1024, "shared memory");
+}  // namespace p3
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_prefill_attn_k128(const __grid_constant__ CUtensorMap pool_map,
+                        const __grid_constant__ CUtensorMap row_map, const PrefillArgs a) {
+  using namespace p3;
+  constexpr int kKeys = p3::kKeys, kKvAtom = p3::kKvAtom, kKvTile = p3::kKvTile;
+  constexpr int kOffQ = p3::kOffQ, kOffK = p3::kOffK, kOffV = p3::kOffV, kOffBar = p3::kOffBar;
+  constexpr int kBarQ = p3::kBarQ, kBarKFull = p3::kBarKFull, kBarVFull = p3::kBarVFull;
+  constexpr int kBarKEmpty = p3::kBarKEmpty, kBarVEmpty = p3::kBarVEmpty;
+  constexpr int kBarSFull = p3::kBarSFull, kBarPFull = p3::kBarPFull, kBarODone = p3::kBarODone;
+  constexpr int kBarCount = p3::kBarCount;
+  constexpr int kStagesV = p3::kStagesV;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int qb = a.n_blocks - 1 - static_cast<int>(blockIdx.x);
+  const int h = blockIdx.y;
+  const uint32_t sQ = smem_u32(smem + kOffQ), sK = smem_u32(smem + kOffK);
+  const uint32_t sV = smem_u32(smem + kOffV), bars = smem_u32(smem + kOffBar);
+  auto bar = [&](int i) { return bars + 8u * static_cast<uint32_t>(i); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + 8 * kBarCount);
+
+  const int tok_first = qb * kQTiles * kTokens;
+  const int tok_last = min(a.n_q, tok_first + kQTiles * kTokens) - 1;
+  const int n_keys = a.q_pos0 + tok_last + 1;
+  const int n_tiles = (n_keys + kKeys - 1) / kKeys;
+
+  if (warp == 9) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == kSoftmaxThreads) {
+    mbar_init(bar(kBarQ), kSoftmaxThreads);
+    for (int s = 0; s < kStagesK; ++s) {
+      mbar_init(bar(kBarKFull + s), 1);
+      mbar_init(bar(kBarKEmpty + s), 1);
+    }
+    for (int s = 0; s < kStagesV; ++s) {
+      mbar_init(bar(kBarVFull + s), 1);
+      mbar_init(bar(kBarVEmpty + s), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(kBarSFull + i), 1);
+      mbar_init(bar(kBarPFull + i), kRows);
+      mbar_init(bar(kBarODone + i), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&pool_map))
+                 : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&row_map))
+                 : "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  constexpr uint32_t tmem = 0;
+  if (tid == 0 && *tmem_slot != 0u) __trap();
+
+  if (warp == 8 || warp == 10) {
+    // ---------------- producers: K (warp 8) / V (warp 10), lane l owns
+    // positions kPer*l .. kPer*l + kPer - 1 of the tile ----------------
+    const int C = min(a.page_size, 64), lanes_per_chunk = C / kPer;
+    const uint32_t chunk_mask = lanes_per_chunk >= 32 ? 0xffffffffu : ((1u << lanes_per_chunk) - 1u);
+    const int my_chunk_lane0 = lane - lane % lanes_per_chunk;
+    const int op = warp == 8 ? 0 : 1;
+    const int nst = op == 0 ? kStagesK : kStagesV;
+    const int col = op == 0 ? h * kD : (a.Hkv + h) * kD;
+    for (int j = 0; j < n_tiles; ++j) {
+      const int s = j % nst;
+      const int p0 = j * kKeys + lane * kPer;
+      int sl[kPer];
+#pragma unroll
+      for (int t = 0; t < kPer; ++t) sl[t] = p0 + t < n_keys ? __ldg(a.slots + p0 + t) : -1;
+      const int prev_last = __shfl_up_sync(0xffffffffu, sl[kPer - 1], 1);
+      bool ok = true;
+#pragma unroll
+      for (int t = 0; t < kPer; ++t) {
+        const bool chunk_start = ((lane * kPer + t) % C) == 0;
+        const int prev = t > 0 ? sl[t - 1] : prev_last;
+        if (!chunk_start && sl[t] >= 0) ok = ok && sl[t] == prev + 1;
+      }
+      const uint32_t ballot = __ballot_sync(0xffffffffu, ok);
+      const bool contiguous = ((ballot >> my_chunk_lane0) & chunk_mask) == chunk_mask;
+      const int chunk_row = __shfl_sync(0xffffffffu, sl[0], my_chunk_lane0);
+      const uint32_t base = (op == 0 ? sK : sV) + s * kKvTile;
+      const uint32_t full = bar((op == 0 ? kBarKFull : kBarVFull) + s);
+      if (lane == 0) {
+        if (j >= nst) mbar_wait(bar((op == 0 ? kBarKEmpty : kBarVEmpty) + s), ((j / nst) + 1) & 1);
+        PF_EV((op == 0 ? 0xA00 : 0xC00) | (j & 0xff));
+        mbar_expect_tx(full, kKvTile);
+      }
+      __syncwarp();
+      if (contiguous) {
+        if (lane == my_chunk_lane0) {
+          const uint32_t dst = base + (lane * kPer) * 128;
+          const int row = chunk_row >= 0 ? chunk_row : 0;
+          tma_load_3d(dst, &pool_map, col, row, a.layer, full);
+          tma_load_3d(dst + kKvAtom, &pool_map, col + 64, row, a.layer, full);
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < kPer; ++t) {
+          const uint32_t dst = base + (lane * kPer + t) * 128;
+          const int row = sl[t] >= 0 ? sl[t] : 0;
+          tma_load_3d(dst, &row_map, col, row, a.layer, full);
+          tma_load_3d(dst + kKvAtom, &row_map, col + 64, row, a.layer, full);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    // ---------------- MMA issuer ----------------
+    //   prologue  S0(0) S1(0)
+    //   tile j    [P0(j)] PV0(j) S0(j+1) [P1(j)] PV1(j) S1(j+1)
+    constexpr uint32_t kIdescS = idesc_bf16(false, kKeys), kIdescO = idesc_bf16(true, kD);
+    constexpr uint32_t kHi = desc_hi(1024);
+    auto tS = [&](int i) { return tmem + i * 128; };
+    auto tO = [&](int i) { return tmem + 256 + i * 128; };
+    const uint32_t q_lo = desc_lo(sQ, 16), k_lo = desc_lo(sK, 16), v_lo = desc_lo(sV, kKvAtom);
+    auto issue_s = [&](int i, int j) {
+      const uint32_t a0 = q_lo + ((i * kTile) >> 4), b0 = k_lo + (((j % kStagesK) * kKvTile) >> 4);
+#pragma unroll
+      for (int k = 0; k < kD / 16; ++k) {
+        const uint32_t ao = ((k >> 2) * kAtom + (k & 3) * 32) >> 4;
+        const uint32_t bo = ((k >> 2) * kKvAtom + (k & 3) * 32) >> 4;
+        mma_ss_elect(tS(i), a0 + ao, b0 + bo, kHi, kIdescS, k > 0 ? 1u : 0u);
+      }
+      commit_elect(bar(kBarSFull + i));
+    };
+    auto issue_pv = [&](int i, int j) {
+      mbar_wait(bar(kBarPFull + i), j & 1);
+      fence_after();
+      if (lane == 0) PF_EV(0xE00 | (i << 8) | (j & 0xff));
+      const uint32_t b0 = v_lo + (((j % kStagesV) * kKvTile) >> 4);
+#pragma unroll
+      for (int k = 0; k < kKeys / 16; ++k)
+        mma_ts_elect(tO(i), tS(i) + k * 8, b0 + ((k * 2048) >> 4), kHi, kIdescO,
+                     (j > 0 || k > 0) ? 1u : 0u);
+    };
+    auto zero_tail = [&](int j) {
+      const int valid = n_keys - j * kKeys;
+      if (valid >= kKeys) return;
+      uint8_t* vb = smem + kOffV + (j % kStagesV) * kKvTile;
+      for (int e = lane; e < (kKeys - valid) * 16; e += 32) {
+        const int r = valid + (e >> 4), c = e & 15;
+        *reinterpret_cast<uint4*>(vb + (c >> 3) * kKvAtom + r * 128 + (c & 7) * 16) =
+            make_uint4(0, 0, 0, 0);
+      }
+      fence_proxy_async();
+      __syncwarp();
+    };
+    mbar_wait(bar(kBarQ), 0);
+    mbar_wait(bar(kBarKFull), 0);
+    fence_after();
+    issue_s(0, 0);
+    issue_s(1, 0);
+    commit_elect(bar(kBarKEmpty));
+    for (int j = 0; j < n_tiles; ++j) {
+      const int sv = j % kStagesV;
+      mbar_wait(bar(kBarVFull + sv), (j / kStagesV) & 1);
+      if (j == n_tiles - 1) zero_tail(j);
+      const bool next = j + 1 < n_tiles;
+      const int sk = (j + 1) % kStagesK;
+      if (next) mbar_wait(bar(kBarKFull + sk), ((j + 1) / kStagesK) & 1);
+      fence_after();
+      if (lane == 0) PF_EV(0x100 | (j & 0xff));
+      for (int i = 0; i < kQTiles; ++i) {
+        issue_pv(i, j);
+        if (lane == 0) PF_EV(0x200 | (i << 8) | (j & 0xff));
+        if (!next) commit_elect(bar(kBarODone + i));
+        if (next) issue_s(i, j + 1);
+      }
+      commit_elect(bar(kBarVEmpty + sv));
+      if (next) commit_elect(bar(kBarKEmpty + sk));
+    }
+  } else {
+    // ---------------- softmax warpgroups ----------------
+    const int i = warp >> 2;
+    const int r = tid & (kRows - 1);
+    const int G = a.Hq / a.Hkv;
+    const int tok = tok_first + i * kTokens + r / G, g = r % G;
+    const bool row_valid = tok < a.n_q;
+    const int q_pos = a.q_pos0 + tok;
+    const int tile_min_pos = a.q_pos0 + tok_first + i * kTokens;
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + i * 128 + lane_off, tO = tmem + 256 + i * 128 + lane_off;
+    {
+      const __nv_bfloat16* qrow =
+          a.q + (static_cast<int64_t>(tok) * a.Hq + static_cast<int64_t>(h) * G + g) * kD;
+      const uint32_t qa = sQ + i * kTile;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) cp_async16(qa + sw128(r, c), qrow + c * 8, row_valid);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      fence_proxy_async();
+      mbar_arrive(bar(kBarQ));
+    }
+    const float sl2 = a.scale_log2;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_tiles; ++j) {
+      if ((warp & 3) == 0 && lane == 0) PF_EV(0x400 | (i << 8) | (j & 0xff));
+      mbar_wait(bar(kBarSFull + i), j & 1);
+      fence_after();
+      if ((warp & 3) == 0 && lane == 0) PF_EV(0x600 | (i << 8) | (j & 0xff));
+      uint32_t sr[kKeys];
+#pragma unroll
+      for (int c0 = 0; c0 < kKeys; c0 += 16) tmem_ld16_nowait(tS + c0, sr + c0);
+      tmem_wait_ld();
+      const int key0 = j * kKeys;
+      const bool need_mask =
+          __any_sync(0xffffffffu, key0 + kKeys - 1 > tile_min_pos || !row_valid);
+      if (need_mask) {
+        const int lim = row_valid ? q_pos - key0 : -1;
+#pragma unroll
+        for (int c = 0; c < kKeys; ++c) sr[c] = c > lim ? __float_as_uint(-INFINITY) : sr[c];
+      }
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int c = 0; c < kKeys; c += 8) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          mx[k] = fmaxf(mx[k], fmaxf(__uint_as_float(sr[c + 2 * k]), __uint_as_float(sr[c + 2 * k + 1])));
+      }
+      const float rmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+      const float tmax = rmax * sl2;
+      const bool bump = tmax > m + 8.f;
+      const float m_new = bump ? tmax : m;
+      const float alpha = (bump && m != -INFINITY) ? ex2_mufu(m - m_new) : 1.f;
+      const float neg_m = m_new == -INFINITY ? 0.f : -m_new;
+      const uint64_t sc2 = f2pack(sl2, sl2), nm2 = f2pack(neg_m, neg_m);
+      uint64_t acc[2] = {0ull, 0ull};
+      auto make_p = [&](auto poly) {
+#pragma unroll
+        for (int c = 0; c < kKeys; c += 2) {
+          float x0, x1, p0, p1;
+          f2unpack(ffma2(f2pack(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), sc2, nm2),
+                   x0, x1);
+          if (decltype(poly)::value && PF3_POLY_EVERY > 0 &&
+              ((c >> 1) % (PF3_POLY_EVERY > 0 ? PF3_POLY_EVERY : 1)) == PF3_POLY_EVERY - 1) {
+            ex2_poly2(x0, x1, p0, p1);
+          } else {
+            p0 = ex2_mufu(x0);
+            p1 = ex2_mufu(x1);
+          }
+          acc[(c >> 1) & 1] = fadd2(acc[(c >> 1) & 1], f2pack(p0, p1));
+          sr[c / 2] = pack_bf16(p0, p1);
+        }
+      };
+      if (need_mask) make_p(std::false_type{});
+      else make_p(std::true_type{});
+      float ps[4];
+      f2unpack(acc[0], ps[0], ps[1]);
+      f2unpack(acc[1], ps[2], ps[3]);
+      const float psum = (ps[0] + ps[1]) + (ps[2] + ps[3]);
+#pragma unroll
+      for (int c0 = 0; c0 < kKeys / 2; c0 += 16) tmem_st16_nowait(tS + c0, sr + c0);
+      // S_i(j) landed behind PV_i(j-1) (same issuing thread, in order), so
+      // O_i is stable here: rescale without a further wait.
+      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+        for (int c0 = 0; c0 < kD; c0 += 32) {
+          uint32_t o[32];
+          tmem_ld16_nowait(tO + c0, o);
+          tmem_ld16_nowait(tO + c0 + 16, o + 16);
+          tmem_wait_ld();
+#pragma unroll
+          for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
+          tmem_st16_nowait(tO + c0, o);
+          tmem_st16_nowait(tO + c0 + 16, o + 16);
+        }
+      }
+      tmem_wait_st();
+      fence_before();
+      mbar_arrive(bar(kBarPFull + i));
+      if ((warp & 3) == 0 && lane == 0) PF_EV(0x800 | (i << 8) | (j & 0xff));
+      if (lane == 0) PF_EV(0x4000 | (warp << 8) | (j & 0xff));
+      l = l * alpha + psum;
+      m = m_new;
+    }
+    mbar_wait(bar(kBarODone + i), 0);
+    fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    __nv_bfloat16* orow =
+        a.out + (static_cast<int64_t>(tok) * a.Hq + static_cast<int64_t>(h) * G + g) * kD;
+#pragma unroll
+    for (int c0 = 0; c0 < kD; c0 += 32) {
+      uint32_t o[32];
+      tmem_ld16_nowait(tO + c0, o);
+      tmem_ld16_nowait(tO + c0 + 16, o + 16);
+      tmem_wait_ld();
+      if (row_valid) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          auto pk = [&](int e) {
+            return pack_bf16(__uint_as_float(o[8 * k + e]) * inv,
+                             __uint_as_float(o[8 * k + e + 1]) * inv);
+          };
+          reinterpret_cast<uint4*>(orow + c0)[k] = make_uint4(pk(0), pk(2), pk(4), pk(6));
+        }
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+__global__ void __launch_bounds__(p3::kThreadsS, 1)
+    k_prefill_attn_k128s(const __grid_constant__ CUtensorMap pool_map,
+                        const __grid_constant__ CUtensorMap row_map, const PrefillArgs a) {
+  using namespace p3;
+  constexpr int kKeys = p3::kKeys, kKvAtom = p3::kKvAtom, kKvTile = p3::kKvTile;
+  constexpr int kOffQ = p3::kOffQ, kOffK = p3::kOffK, kOffV = p3::kOffV, kOffBar = p3::kOffBar;
+  constexpr int kBarQ = p3::kBarQ, kBarKFull = p3::kBarKFull, kBarVFull = p3::kBarVFull;
+  constexpr int kBarKEmpty = p3::kBarKEmpty, kBarVEmpty = p3::kBarVEmpty;
+  constexpr int kBarSFull = p3::kBarSFull, kBarPFull = p3::kBarPFull, kBarODone = p3::kBarODone;
+  constexpr int kBarCount = p3::kBarCount;
+  constexpr int kStagesV = p3::kStagesV;
+  constexpr int kSoftmaxThreads = p3::kSoftmaxThreadsS;  // two threads per query row
+  constexpr int kWarpK = 16, kWarpMma = 17, kWarpV = 18;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int qb = a.n_blocks - 1 - static_cast<int>(blockIdx.x);
+  const int h = blockIdx.y;
+  const uint32_t sQ = smem_u32(smem + kOffQ), sK = smem_u32(smem + kOffK);
+  const uint32_t sV = smem_u32(smem + kOffV), bars = smem_u32(smem + kOffBar);
+  auto bar = [&](int i) { return bars + 8u * static_cast<uint32_t>(i); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + 8 * kBarCount);
+
+  const int tok_first = qb * kQTiles * kTokens;
+  const int tok_last = min(a.n_q, tok_first + kQTiles * kTokens) - 1;
+  const int n_keys = a.q_pos0 + tok_last + 1;
+  const int n_tiles = (n_keys + kKeys - 1) / kKeys;
+
+  if (warp == kWarpMma) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == kSoftmaxThreads) {
+    mbar_init(bar(kBarQ), kSoftmaxThreads);
+    for (int s = 0; s < kStagesK; ++s) {
+      mbar_init(bar(kBarKFull + s), 1);
+      mbar_init(bar(kBarKEmpty + s), 1);
+    }
+    for (int s = 0; s < kStagesV; ++s) {
+      mbar_init(bar(kBarVFull + s), 1);
+      mbar_init(bar(kBarVEmpty + s), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(kBarSFull + i), 1);
+      mbar_init(bar(kBarPFull + i), 2 * kRows);
+      mbar_init(bar(kBarODone + i), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&pool_map))
+                 : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&row_map))
+                 : "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  constexpr uint32_t tmem = 0;
+  if (tid == 0 && *tmem_slot != 0u) __trap();
+
+  if (warp == kWarpK || warp == kWarpV) {
+    // ---------------- producers: K (warp 8) / V (warp 10), lane l owns
+    // positions kPer*l .. kPer*l + kPer - 1 of the tile ----------------
+    const int C = min(a.page_size, 64), lanes_per_chunk = C / kPer;
+    const uint32_t chunk_mask = lanes_per_chunk >= 32 ? 0xffffffffu : ((1u << lanes_per_chunk) - 1u);
+    const int my_chunk_lane0 = lane - lane % lanes_per_chunk;
+    const int op = warp == kWarpK ? 0 : 1;
+    const int nst = op == 0 ? kStagesK : kStagesV;
+    const int col = op == 0 ? h * kD : (a.Hkv + h) * kD;
+    for (int j = 0; j < n_tiles; ++j) {
+      const int s = j % nst;
+      const int p0 = j * kKeys + lane * kPer;
+      int sl[kPer];
+#pragma unroll
+      for (int t = 0; t < kPer; ++t) sl[t] = p0 + t < n_keys ? __ldg(a.slots + p0 + t) : -1;
+      const int prev_last = __shfl_up_sync(0xffffffffu, sl[kPer - 1], 1);
+      bool ok = true;
+#pragma unroll
+      for (int t = 0; t < kPer; ++t) {
+        const bool chunk_start = ((lane * kPer + t) % C) == 0;
+        const int prev = t > 0 ? sl[t - 1] : prev_last;
+        if (!chunk_start && sl[t] >= 0) ok = ok && sl[t] == prev + 1;
+      }
+      const uint32_t ballot = __ballot_sync(0xffffffffu, ok);
+      const bool contiguous = ((ballot >> my_chunk_lane0) & chunk_mask) == chunk_mask;
+      const int chunk_row = __shfl_sync(0xffffffffu, sl[0], my_chunk_lane0);
+      const uint32_t base = (op == 0 ? sK : sV) + s * kKvTile;
+      const uint32_t full = bar((op == 0 ? kBarKFull : kBarVFull) + s);
+      if (lane == 0) {
+        if (j >= nst) mbar_wait(bar((op == 0 ? kBarKEmpty : kBarVEmpty) + s), ((j / nst) + 1) & 1);
+        PF_EV((op == 0 ? 0xA00 : 0xC00) | (j & 0xff));
+        mbar_expect_tx(full, kKvTile);
+      }
+      __syncwarp();
+      if (contiguous) {
+        if (lane == my_chunk_lane0) {
+          const uint32_t dst = base + (lane * kPer) * 128;
+          const int row = chunk_row >= 0 ? chunk_row : 0;
+          tma_load_3d(dst, &pool_map, col, row, a.layer, full);
+          tma_load_3d(dst + kKvAtom, &pool_map, col + 64, row, a.layer, full);
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < kPer; ++t) {
+          const uint32_t dst = base + (lane * kPer + t) * 128;
+          const int row = sl[t] >= 0 ? sl[t] : 0;
+          tma_load_3d(dst, &row_map, col, row, a.layer, full);
+          tma_load_3d(dst + kKvAtom, &row_map, col + 64, row, a.layer, full);
+        }
+      }
+    }
+  } else if (warp == kWarpMma) {
+    // ---------------- MMA issuer ----------------
+    //   prologue  S0(0) S1(0)
+    //   tile j    [P0(j)] PV0(j) S0(j+1) [P1(j)] PV1(j) S1(j+1)
+    constexpr uint32_t kIdescS = idesc_bf16(false, kKeys), kIdescO = idesc_bf16(true, kD);
+    constexpr uint32_t kHi = desc_hi(1024);
+    auto tS = [&](int i) { return tmem + i * 128; };
+    auto tO = [&](int i) { return tmem + 256 + i * 128; };
+    const uint32_t q_lo = desc_lo(sQ, 16), k_lo = desc_lo(sK, 16), v_lo = desc_lo(sV, kKvAtom);
+    auto issue_s = [&](int i, int j) {
+      const uint32_t a0 = q_lo + ((i * kTile) >> 4), b0 = k_lo + (((j % kStagesK) * kKvTile) >> 4);
+#pragma unroll
+      for (int k = 0; k < kD / 16; ++k) {
+        const uint32_t ao = ((k >> 2) * kAtom + (k & 3) * 32) >> 4;
+        const uint32_t bo = ((k >> 2) * kKvAtom + (k & 3) * 32) >> 4;
+        mma_ss_elect(tS(i), a0 + ao, b0 + bo, kHi, kIdescS, k > 0 ? 1u : 0u);
+      }
+      commit_elect(bar(kBarSFull + i));
+    };
+    auto issue_pv = [&](int i, int j) {
+      mbar_wait(bar(kBarPFull + i), j & 1);
+      fence_after();
+      if (lane == 0) PF_EV(0xE00 | (i << 8) | (j & 0xff));
+      const uint32_t b0 = v_lo + (((j % kStagesV) * kKvTile) >> 4);
+#pragma unroll
+      for (int k = 0; k < kKeys / 16; ++k)
+        mma_ts_elect(tO(i), tS(i) + k * 8, b0 + ((k * 2048) >> 4), kHi, kIdescO,
+                     (j > 0 || k > 0) ? 1u : 0u);
+    };
+    auto zero_tail = [&](int j) {
+      const int valid = n_keys - j * kKeys;
+      if (valid >= kKeys) return;
+      uint8_t* vb = smem + kOffV + (j % kStagesV) * kKvTile;
+      for (int e = lane; e < (kKeys - valid) * 16; e += 32) {
+        const int r = valid + (e >> 4), c = e & 15;
+        *reinterpret_cast<uint4*>(vb + (c >> 3) * kKvAtom + r * 128 + (c & 7) * 16) =
+            make_uint4(0, 0, 0, 0);
+      }
+      fence_proxy_async();
+      __syncwarp();
+    };
+    mbar_wait(bar(kBarQ), 0);
+    mbar_wait(bar(kBarKFull), 0);
+    fence_after();
+    issue_s(0, 0);
+    issue_s(1, 0);
+    commit_elect(bar(kBarKEmpty));
+    for (int j = 0; j < n_tiles; ++j) {
+      const int sv = j % kStagesV;
+      mbar_wait(bar(kBarVFull + sv), (j / kStagesV) & 1);
+      if (j == n_tiles - 1) zero_tail(j);
+      const bool next = j + 1 < n_tiles;
+      const int sk = (j + 1) % kStagesK;
+      if (next) mbar_wait(bar(kBarKFull + sk), ((j + 1) / kStagesK) & 1);
+      fence_after();
+      if (lane == 0) PF_EV(0x100 | (j & 0xff));
+      for (int i = 0; i < kQTiles; ++i) {
+        issue_pv(i, j);
+        if (lane == 0) PF_EV(0x200 | (i << 8) | (j & 0xff));
+        if (!next) commit_elect(bar(kBarODone + i));
+        if (next) issue_s(i, j + 1);
+      }
+      commit_elect(bar(kBarVEmpty + sv));
+      if (next) commit_elect(bar(kBarKEmpty + sk));
+    }
+  } else {
+    // ---------------- softmax: four warpgroups, two threads per row -------
+    // Warps 8 i + 4 hf + q: query tile i, key/column half hf, TMEM lane
+    // quarter q (= warp % 4, the quarter a warp may access).  The two halves
+    // of a row exchange their maxima through shared memory (a 64-thread
+    // named barrier per (tile, quarter)), so both use the same reference
+    // max; row sums stay per half until the epilogue.
+    const int i = warp >> 3, hf = (warp >> 2) & 1, q = warp & 3;
+    const int r = q * 32 + lane;
+    const int G = a.Hq / a.Hkv;
+    const int tok = tok_first + i * kTokens + r / G, g = r % G;
+    const bool row_valid = tok < a.n_q;
+    const int q_pos = a.q_pos0 + tok;
+    const int tile_min_pos = a.q_pos0 + tok_first + i * kTokens;
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    const uint32_t tS = tmem + i * 128 + lane_off, tO = tmem + 256 + i * 128 + lane_off;
+    float* red = reinterpret_cast<float*>(smem + p3::kOffRed);  // [2 buf][2 tile][2 half][128]
+    const uint32_t pair_bar = 1 + i * 4 + q;
+    auto pair_sync = [&]() {
+      asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+    };
+    {
+      const __nv_bfloat16* qrow =
+          a.q + (static_cast<int64_t>(tok) * a.Hq + static_cast<int64_t>(h) * G + g) * kD;
+      const uint32_t qa = sQ + i * kTile;
+#pragma unroll
+      for (int c = 8 * hf; c < 8 * hf + 8; ++c) cp_async16(qa + sw128(r, c), qrow + c * 8, row_valid);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      fence_proxy_async();
+      mbar_arrive(bar(kBarQ));
+    }
+    constexpr int kHalf = kKeys / 2;  // S columns per thread
+    const int col0 = hf * kHalf;
+    const float sl2 = a.scale_log2;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_tiles; ++j) {
+      mbar_wait(bar(kBarSFull + i), j & 1);
+      fence_after();
+      uint32_t sr[kHalf];
+#pragma unroll
+      for (int c0 = 0; c0 < kHalf; c0 += 16) tmem_ld16_nowait(tS + col0 + c0, sr + c0);
+      tmem_wait_ld();
+      const int key0 = j * kKeys + col0;
+      const bool need_mask =
+          __any_sync(0xffffffffu, key0 + kHalf - 1 > tile_min_pos || !row_valid);
+      if (need_mask) {
+        const int lim = row_valid ? q_pos - key0 : -1;
+#pragma unroll
+        for (int c = 0; c < kHalf; ++c) sr[c] = c > lim ? __float_as_uint(-INFINITY) : sr[c];
+      }
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int c = 0; c < kHalf; c += 8) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          mx[k] = fmaxf(mx[k], fmaxf(__uint_as_float(sr[c + 2 * k]), __uint_as_float(sr[c + 2 * k + 1])));
+      }
+      float rmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+      {  // exchange with the other half of the row (double-buffered by tile parity)
+        float* rb = red + (((j & 1) * 2 + i) * 2) * 128;
+        rb[hf * 128 + r] = rmax;
+        pair_sync();  // also orders the other half's S loads before our P stores
+        rmax = fmaxf(rmax, rb[(hf ^ 1) * 128 + r]);
+      }
+      const float tmax = rmax * sl2;
+      const bool bump = tmax > m + 8.f;
+      const float m_new = bump ? tmax : m;
+      const float alpha = (bump && m != -INFINITY) ? ex2_mufu(m - m_new) : 1.f;
+      const float neg_m = m_new == -INFINITY ? 0.f : -m_new;
+      const uint64_t sc2 = f2pack(sl2, sl2), nm2 = f2pack(neg_m, neg_m);
+      uint64_t acc[2] = {0ull, 0ull};
+      auto make_p = [&](auto poly) {
+#pragma unroll
+        for (int c = 0; c < kHalf; c += 2) {
+          float x0, x1, p0, p1;
+          f2unpack(ffma2(f2pack(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), sc2, nm2),
+                   x0, x1);
+          if (decltype(poly)::value && PF3_POLY_EVERY > 0 &&
+              ((c >> 1) % (PF3_POLY_EVERY > 0 ? PF3_POLY_EVERY : 1)) == PF3_POLY_EVERY - 1) {
+            ex2_poly2(x0, x1, p0, p1);
+          } else {
+            p0 = ex2_mufu(x0);
+            p1 = ex2_mufu(x1);
+          }
+          acc[(c >> 1) & 1] = fadd2(acc[(c >> 1) & 1], f2pack(p0, p1));
+          sr[c / 2] = pack_bf16(p0, p1);
+        }
+      };
+      if (need_mask) make_p(std::false_type{});
+      else make_p(std::true_type{});
+      float ps[4];
+      f2unpack(acc[0], ps[0], ps[1]);
+      f2unpack(acc[1], ps[2], ps[3]);
+      const float psum = (ps[0] + ps[1]) + (ps[2] + ps[3]);
+      // P columns of this half: keys [col0, col0 + 64) -> packed [col0 / 2, col0 / 2 + 32).
+#pragma unroll
+      for (int c0 = 0; c0 < kHalf / 2; c0 += 16) tmem_st16_nowait(tS + col0 / 2 + c0, sr + c0);
+      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+        for (int c0 = 0; c0 < kD / 2; c0 += 32) {
+          uint32_t o[32];
+          tmem_ld16_nowait(tO + hf * (kD / 2) + c0, o);
+          tmem_ld16_nowait(tO + hf * (kD / 2) + c0 + 16, o + 16);
+          tmem_wait_ld();
+#pragma unroll
+          for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
+          tmem_st16_nowait(tO + hf * (kD / 2) + c0, o);
+          tmem_st16_nowait(tO + hf * (kD / 2) + c0 + 16, o + 16);
+        }
+      }
+      tmem_wait_st();
+      fence_before();
+      mbar_arrive(bar(kBarPFull + i));
+      l = l * alpha + psum;
+      m = m_new;
+    }
+    {  // row sum of both halves (buffer 0 of tile i is free: last use was >= 2 tiles ago
+       // or, for n_tiles == 1, read before the pair barrier below... use the epilogue slot)
+      float* rb = red + (4 * 2 + i * 2) * 128;
+      rb[hf * 128 + r] = l;
+      pair_sync();
+      l += rb[(hf ^ 1) * 128 + r];
+    }
+    mbar_wait(bar(kBarODone + i), 0);
+    fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    __nv_bfloat16* orow =
+        a.out + (static_cast<int64_t>(tok) * a.Hq + static_cast<int64_t>(h) * G + g) * kD;
+#pragma unroll
+    for (int c0 = hf * (kD / 2); c0 < hf * (kD / 2) + kD / 2; c0 += 32) {
+      uint32_t o[32];
+      tmem_ld16_nowait(tO + c0, o);
+      tmem_ld16_nowait(tO + c0 + 16, o + 16);
+      tmem_wait_ld();
+      if (row_valid) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          auto pk = [&](int e) {
+            return pack_bf16(__uint_as_float(o[8 * k + e]) * inv,
+                             __uint_as_float(o[8 * k + e + 1]) * inv);
+          };
+          reinterpret_cast<uint4*>(orow + c0)[k] = make_uint4(pk(0), pk(2), pk(4), pk(6));
+        }
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == kWarpMma) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+
 }  // namespace
 
 bool make_pool_tensor_map(void* pool, int64_t layers, int64_t rows, int64_t row_u64,
@@ -1232,14 +1931,25 @@ bool launch_prefill_attn(const PoolTensorMap& page_map, const PoolTensorMap& row
                          int q_pos0, int n_q, int Hq, int Hkv, int D, float scale, void* out,
                          cudaStream_t s) {
   if (!prefill_attn_supported(page_size, Hq, Hkv, D) || n_q <= 0) return false;
-  // MICROKV_PREFILL_2SM=1: the CTA-pair kernel (A/B while it is evaluated).
-  const char* e2 = std::getenv("MICROKV_PREFILL_2SM");
-  const bool use_2sm = e2 != nullptr && e2[0] == '1';
+  // Kernel selection (A/B of the layouts): MICROKV_PREFILL_VARIANT
+  // = "128" (default: 128-key tiles, one S slot per query tile), "128s" (the
+  // same with two softmax threads per row), "64" (64-key tiles, two S slots),
+  // "2sm" (CTA pair, cta_group::2).  Read per launch.
+  const char* ev = std::getenv("MICROKV_PREFILL_VARIANT");
+  const std::string variant = ev != nullptr ? ev : "128";
+  const bool use_2sm = variant == "2sm";
+  const bool use_k64 = variant == "64";
+  const bool use_k128s = variant == "128s";
+  const bool use_k128 = !use_2sm && !use_k64 && !use_k128s;
   static bool attr = [] {
     return cudaFuncSetAttribute(k_prefill_attn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kSmem + 1024) == cudaSuccess &&
            cudaFuncSetAttribute(k_prefill_attn_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                p2::kSmem + 1024) == cudaSuccess;
+                                p2::kSmem + 1024) == cudaSuccess &&
+           cudaFuncSetAttribute(k_prefill_attn_k128, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                p3::kSmem + 1024) == cudaSuccess &&
+           cudaFuncSetAttribute(k_prefill_attn_k128s, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                p3::kSmemS + 1024) == cudaSuccess;
   }();
   if (!attr) return false;
   PrefillArgs a;
@@ -1264,10 +1974,16 @@ bool launch_prefill_attn(const PoolTensorMap& page_map, const PoolTensorMap& row
   cudaMemset(tr, 0, 65536 * sizeof(unsigned long long));
   a.trace = tr;
 #endif
-  if (use_2sm) {
+  if (use_k128s) {
+    const dim3 grid(a.n_blocks, Hkv);
+    k_prefill_attn_k128s<<<grid, p3::kThreadsS, p3::kSmemS + 1024, s>>>(m, mr, a);
+  } else if (use_k128) {
+    const dim3 grid(a.n_blocks, Hkv);
+    k_prefill_attn_k128<<<grid, kThreads, p3::kSmem + 1024, s>>>(m, mr, a);
+  } else if (use_2sm) {
     const dim3 grid(2 * a.n_blocks, Hkv);
     k_prefill_attn_2sm<<<grid, p2::kThreads, p2::kSmem + 1024, s>>>(m, mr, a);
-  } else {
+  } else if (use_k64) {
     const dim3 grid(a.n_blocks, Hkv);
     k_prefill_attn_tc<<<grid, kThreads, kSmem + 1024, s>>>(m, mr, a);
   }
@@ -1290,6 +2006,8 @@ void preload_prefill_attn_kernels() {
   cudaFuncAttributes a;
   cudaFuncGetAttributes(&a, k_prefill_attn_tc);
   cudaFuncGetAttributes(&a, k_prefill_attn_2sm);
+  cudaFuncGetAttributes(&a, k_prefill_attn_k128);
+  cudaFuncGetAttributes(&a, k_prefill_attn_k128s);
 }
 
 }  // namespace mkv
