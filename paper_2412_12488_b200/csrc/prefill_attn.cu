@@ -1245,7 +1245,8 @@ enum : int {
   kBarSFull = kBarVEmpty + kStagesV,  // +tile
   kBarPFull = kBarSFull + 2,          // +tile (count 128)
   kBarODone = kBarPFull + 2,          // +tile
-  kBarCount = kBarODone + 2,
+  kBarPHalf = kBarODone + 2,          // +tile: first half of P_i(j) (k128 only)
+  kBarCount = kBarPHalf + 2,
 };
 static_assert(kBarCount * 8 + 8 <= 512, "barrier area");
 static_assert(kSmem + 1024 <= 227 * 1024, "shared memory");
@@ -1261,6 +1262,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kBarQ = p3::kBarQ, kBarKFull = p3::kBarKFull, kBarVFull = p3::kBarVFull;
   constexpr int kBarKEmpty = p3::kBarKEmpty, kBarVEmpty = p3::kBarVEmpty;
   constexpr int kBarSFull = p3::kBarSFull, kBarPFull = p3::kBarPFull, kBarODone = p3::kBarODone;
+  constexpr int kBarPHalf = p3::kBarPHalf;
   constexpr int kBarCount = p3::kBarCount;
   constexpr int kStagesV = p3::kStagesV;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1298,6 +1300,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar(kBarSFull + i), 1);
       mbar_init(bar(kBarPFull + i), kRows);
+      mbar_init(bar(kBarPHalf + i), kRows);
       mbar_init(bar(kBarODone + i), 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1383,14 +1386,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       commit_elect(bar(kBarSFull + i));
     };
     auto issue_pv = [&](int i, int j) {
-      mbar_wait(bar(kBarPFull + i), j & 1);
+      const uint32_t b0 = v_lo + (((j % kStagesV) * kKvTile) >> 4);
+      mbar_wait(bar(kBarPHalf + i), j & 1);  // P_i(j) keys [0, 64) and O_i rescaled
       fence_after();
       if (lane == 0) PF_EV(0xE00 | (i << 8) | (j & 0xff));
-      const uint32_t b0 = v_lo + (((j % kStagesV) * kKvTile) >> 4);
 #pragma unroll
-      for (int k = 0; k < kKeys / 16; ++k)
+      for (int k = 0; k < kKeys / 32; ++k)
         mma_ts_elect(tO(i), tS(i) + k * 8, b0 + ((k * 2048) >> 4), kHi, kIdescO,
                      (j > 0 || k > 0) ? 1u : 0u);
+      mbar_wait(bar(kBarPFull + i), j & 1);  // keys [64, 128)
+      fence_after();
+#pragma unroll
+      for (int k = kKeys / 32; k < kKeys / 16; ++k)
+        mma_ts_elect(tO(i), tS(i) + k * 8, b0 + ((k * 2048) >> 4), kHi, kIdescO, 1u);
     };
     auto zero_tail = [&](int j) {
       const int valid = n_keys - j * kKeys;
@@ -1484,9 +1492,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float neg_m = m_new == -INFINITY ? 0.f : -m_new;
       const uint64_t sc2 = f2pack(sl2, sl2), nm2 = f2pack(neg_m, neg_m);
       uint64_t acc[2] = {0ull, 0ull};
-      auto make_p = [&](auto poly) {
+      // P in two halves of 64 keys: the MMA warp starts PV on keys [0, 64)
+      // while the second half's exponentials run (shorter softmax -> PV
+      // chain per tile).
+      auto make_p = [&](auto poly, auto lo) {
 #pragma unroll
-        for (int c = 0; c < kKeys; c += 2) {
+        for (int c = decltype(lo)::value; c < decltype(lo)::value + kKeys / 2; c += 2) {
           float x0, x1, p0, p1;
           f2unpack(ffma2(f2pack(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), sc2, nm2),
                    x0, x1);
@@ -1501,16 +1512,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           sr[c / 2] = pack_bf16(p0, p1);
         }
       };
-      if (need_mask) make_p(std::false_type{});
-      else make_p(std::true_type{});
-      float ps[4];
-      f2unpack(acc[0], ps[0], ps[1]);
-      f2unpack(acc[1], ps[2], ps[3]);
-      const float psum = (ps[0] + ps[1]) + (ps[2] + ps[3]);
-#pragma unroll
-      for (int c0 = 0; c0 < kKeys / 2; c0 += 16) tmem_st16_nowait(tS + c0, sr + c0);
+      using Lo = std::integral_constant<int, 0>;
+      using Hi = std::integral_constant<int, kKeys / 2>;
+      if (need_mask) make_p(std::false_type{}, Lo{});
+      else make_p(std::true_type{}, Lo{});
       // S_i(j) landed behind PV_i(j-1) (same issuing thread, in order), so
-      // O_i is stable here: rescale without a further wait.
+      // O_i is stable here: rescale without a further wait, before PV_i(j).
       if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll
         for (int c0 = 0; c0 < kD; c0 += 32) {
@@ -1524,6 +1531,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st16_nowait(tO + c0 + 16, o + 16);
         }
       }
+#pragma unroll
+      for (int c0 = 0; c0 < kKeys / 4; c0 += 16) tmem_st16_nowait(tS + c0, sr + c0);
+      tmem_wait_st();
+      fence_before();
+      mbar_arrive(bar(kBarPHalf + i));
+      if (need_mask) make_p(std::false_type{}, Hi{});
+      else make_p(std::true_type{}, Hi{});
+      float ps[4];
+      f2unpack(acc[0], ps[0], ps[1]);
+      f2unpack(acc[1], ps[2], ps[3]);
+      const float psum = (ps[0] + ps[1]) + (ps[2] + ps[3]);
+#pragma unroll
+      for (int c0 = kKeys / 4; c0 < kKeys / 2; c0 += 16) tmem_st16_nowait(tS + c0, sr + c0);
       tmem_wait_st();
       fence_before();
       mbar_arrive(bar(kBarPFull + i));
