@@ -240,7 +240,7 @@ ss_cache::ss_cache(const ss_config& cfg)
   CudaCheck(cudaMemsetAsync(d_win_layer_rows_, 0, sizeof(uint32_t) * kMaxWindows * L_, stream_),
             "memset");
   CudaCheck(cudaMemsetAsync(d_status_, 0, sizeof(uint32_t), stream_), "memset");
-  launches_ += 7;
+  CountLaunches(7);
   for (int32_t i = kMaxWindows - 1; i >= 0; --i) free_window_ids_.push_back(i);
   for (int32_t i = kMaxSeqRows - 1; i >= 0; --i) free_fold_rows_.push_back(i);
   Sync();
@@ -409,6 +409,11 @@ void ss_cache::OrderLaunch(cudaStream_t s) {
   OrderUser(s);
 }
 
+void ss_cache::CountLaunches(int64_t n) {
+  launches_ += n;
+  CudaCheck(cudaGetLastError(), "kernel launch");
+}
+
 void ss_cache::NoteUser(cudaStream_t s) {
   CudaCheck(cudaEventRecord(user_ev_, s), "cudaEventRecord");
   user_pending_ = true;
@@ -454,7 +459,7 @@ int64_t ss_cache::DeviceFirstNonFull(const Record* rec, int64_t from, int64_t to
   const int64_t n = to - from;
   launch_first_nonfull(d_fill_, num_pages_ * P_, L_, rec->d_slots + from, n, d_scratch_, stream_,
                        num_sms_);
-  launches_ += 1;
+  CountLaunches(1);
   D2H(h_pinned_, d_scratch_, sizeof(unsigned long long), stream_, "D2H scan");
   Sync();
   const unsigned long long r = h_pinned_[0];
@@ -489,7 +494,7 @@ void ss_cache::CheckFilled(const Record* rec, int64_t begin, int64_t end, int32_
   H2D(b.ptr, unproven.data(), sizeof(int32_t) * n, stream_, "H2D slots");
   launch_check_filled(d_fill_ + static_cast<int64_t>(layer) * num_pages_ * P_,
                       static_cast<int32_t*>(b.ptr), n, d_status_, stream_, num_sms_);
-  launches_ += 2;
+  CountLaunches(2);
   uint32_t st = 0;
   D2H(&st, d_status_, sizeof(uint32_t), stream_, "D2H status");
   DevFree(b, stream_);
@@ -556,7 +561,7 @@ Record* ss_cache::CreateSequence(SeqId seq, std::vector<Token> tokens) {
     CudaCheck(cudaMemsetAsync(d_fold_sums_ + static_cast<int64_t>(rec->fold_row) * L_, 0,
                               sizeof(uint64_t) * L_, stream_),
               "memset fold sums");
-    launches_ += 1;
+    CountLaunches(1);
   }
   Record* out = rec.get();
   {
@@ -688,7 +693,7 @@ void ss_cache::OpenDeviceWindow(Record* rec, int64_t m, int64_t e) {
   launch_open_window(d_expecting_, static_cast<int32_t*>(b.ptr), n, d_page_window_,
                      reinterpret_cast<int64_t*>(static_cast<uint8_t*>(b.ptr) + off_pages), np, wid,
                      d_win_received_, d_win_layer_rows_, L_, stream_);
-  launches_ += 1;
+  CountLaunches(1);
   DevFree(b, stream_);
   if (ipc_exported_) {
     Sync();  // a peer process sees a ready receiver once it holds the address
@@ -962,7 +967,7 @@ void ss_cache::LaunchRemote(const PeerTarget& peer, const int32_t* d_src_slots,
   c.status = d_status_;
   c.sys_scope = peer.device != device_ ? 1 : 0;
   launch_copy_rows(c, s, num_sms_);
-  launches_ += 2;
+  CountLaunches(2);
 }
 
 // kv_cache.cc:308-371 on device.  Hidden buffers are device pointers; the
@@ -984,7 +989,7 @@ void ss_cache::AttentionAsync(ss_plan* plan, int32_t layer, const uint64_t* hin,
   launch_entry_digest(pool_l, plan->d_fold_slots, plan->n_fold, W_, plan->d_F, s, num_sms_);
   launch_fold_scan(plan->d_entries, static_cast<int64_t>(plan->entries.size()), plan->d_F, hin,
                    hout, layer, s);
-  launches_ += 3;
+  CountLaunches(3);
   for (const auto& e : plan->entries) {
     Record* rec = MustGet(e.seq);
     rec->touched_end = std::max(rec->touched_end, e.end);
@@ -1041,7 +1046,7 @@ void ss_cache::Attention(ss_plan* plan, int32_t layer, const uint64_t* hidden_in
   launch_entry_digest(pool_l, plan->d_fold_slots, plan->n_fold, W_, plan->d_F, stream_, num_sms_);
   launch_fold_scan(plan->d_entries, static_cast<int64_t>(plan->entries.size()), plan->d_F,
                    plan->d_hidden_in, plan->d_hidden_out, layer, stream_);
-  launches_ += 3;
+  CountLaunches(3);
   if (n > 0) {
     D2H(hidden_out, plan->d_hidden_out, sizeof(uint64_t) * n, stream_, "D2H hidden");
   }
@@ -1078,7 +1083,7 @@ void ss_cache::Attention(ss_plan* plan, int32_t layer, const uint64_t* hidden_in
     c.n_layers = 1;
     c.W = W_;
     launch_copy_rows(c, stream_, num_sms_);
-    launches_ += 1;
+    CountLaunches(1);
     payload.resize(static_cast<size_t>(rows) * W_);
     if (rows > 0) {
       D2H(payload.data(), d.staging, sizeof(uint64_t) * rows * W_, stream_, "D2H payload");
@@ -1117,7 +1122,7 @@ void ss_cache::GatherRange(SeqId seq, int64_t begin, int64_t end, int32_t layer,
   c.n_layers = 1;
   c.W = W_;
   launch_copy_rows(c, s, num_sms_);
-  launches_ += 1;
+  CountLaunches(1);
   if (s != stream_) NoteUser(s);
 }
 
@@ -1180,7 +1185,7 @@ void ss_cache::AppendRowsLayers(ss_plan* plan, int32_t lb, int32_t le, const voi
   c.n_layers = le - lb;
   c.W = W_;
   launch_copy_rows(c, s, num_sms_);
-  launches_ += 1;
+  CountLaunches(1);
   for (const auto& e : plan->entries) {
     Record* rec = MustGet(e.seq);
     rec->touched_end = std::max(rec->touched_end, e.end);
@@ -1250,7 +1255,7 @@ int ss_cache::ApplyRemoteWrite(const KVAddr& addr, int32_t layer, const uint64_t
     c.n_layers = 1;
     c.W = W_;
     launch_copy_rows(c, st, num_sms_);
-    launches_ += 1;
+    CountLaunches(1);
     DevFree(b, st);
     if (agent) {
       CudaCheck(cudaStreamSynchronize(st), "cudaStreamSynchronize recv");
@@ -1498,7 +1503,7 @@ void ss_cache::BroadcastSend(SeqId seq, int64_t begin, int64_t end, int32_t n_de
     if (peer.device != device_) f.sys_scope = 1;
   }
   launch_copy_rows_fanout(f, s, num_sms_);
-  launches_ += 1 + n_dest;
+  CountLaunches(1 + n_dest);
   DevFree(b, s);
   if (s != stream_) NoteUser(s);
   (void)tag;
@@ -1550,7 +1555,7 @@ void ss_cache::FreeSequence(SeqId seq) {
       H2D(b.ptr, rec->own_pages.data(), sizeof(int64_t) * np, stream_, "H2D pages");
       launch_reset_pages(d_fill_, d_expecting_, d_page_window_, static_cast<int64_t*>(b.ptr), np,
                          L_, num_pages_, P_, stream_);
-      launches_ += 1;
+      CountLaunches(1);
       DevFree(b, stream_);
       Sync();
     }
@@ -1790,7 +1795,7 @@ void ss_cache::WaitReceive(SeqId seq, int64_t timeout_ms, cudaStream_t s) {
   OrderLaunch(s);
   launch_wait_counter(d_win_received_ + w.dev_id, static_cast<unsigned long long>(target),
                       timeout_ms * 1000000LL, d_status_, s);
-  launches_ += 1;
+  CountLaunches(1);
   if (s != stream_) NoteUser(s);
 }
 
@@ -1810,7 +1815,7 @@ void ss_cache::WaitReceiveLayer(SeqId seq, int32_t layer, int64_t timeout_ms, cu
   OrderLaunch(s);
   launch_wait_counter32(d_win_layer_rows_ + static_cast<int64_t>(w.dev_id) * L_ + layer,
                         static_cast<uint32_t>(target), timeout_ms * 1000000LL, d_status_, s);
-  launches_ += 1;
+  CountLaunches(1);
   if (s != stream_) NoteUser(s);
 }
 
@@ -1870,7 +1875,7 @@ ss_plan* ss_cache::BeginDecode(const int64_t* seqs, const int64_t* ctx_lens, int
                        reinterpret_cast<const int64_t*>(base + o_off),
                        reinterpret_cast<const int32_t*>(base + o_len), batch, off[batch],
                        reinterpret_cast<int32_t*>(base + o_slots), stream_, num_sms_);
-  launches_ += 1;
+  CountLaunches(1);
   plan->d_ctx_slots = reinterpret_cast<int32_t*>(base + o_slots);
   plan->d_ctx_off = reinterpret_cast<int64_t*>(base + o_off);
   plan->d_ctx_len = reinterpret_cast<int32_t*>(base + o_len);
@@ -1939,8 +1944,7 @@ void ss_cache::DecodeAttention(ss_plan* plan, int32_t layer, int32_t hq, int32_t
                                      plan->d_partial, plan->d_partial_ml, out, plan->decode_grid,
                                      s);
   MKV_CHECK(ok, kInvalidArgument, "unsupported head_dim");
-  CudaCheck(cudaPeekAtLastError(), "decode attention launch");
-  launches_ += 2;
+  CountLaunches(2);
   if (s != stream_) NoteUser(s);
 }
 
@@ -1979,7 +1983,6 @@ void ss_cache::PrefillAttention(int64_t seq, int64_t q_begin, int64_t q_end, int
                                       num_pages_ * P_, rec->d_slots, q, static_cast<int>(q_begin),
                                       static_cast<int>(q_end - q_begin), hq, hkv, hd, scale, out, s);
   MKV_CHECK(ok, kInvalidArgument, "unsupported prefill attention shape");
-  CudaCheck(cudaPeekAtLastError(), "prefill attention launch");
-  launches_ += 1;
+  CountLaunches(1);
   if (s != stream_) NoteUser(s);
 }

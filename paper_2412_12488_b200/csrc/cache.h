@@ -333,6 +333,9 @@ struct ss_cache {
   }
   int device() const { return device_; }
   int64_t launches() const { return launches_; }
+  // Count n kernel launches just enqueued and surface a failed launch
+  // (bad configuration, missing image) as SS_ERR_CUDA right away.
+  void CountLaunches(int64_t n);
 
   // Hash model scalars.
   uint64_t InitialPrefixDigest() const;

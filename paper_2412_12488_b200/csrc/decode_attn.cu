@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 namespace mkv {
 
@@ -140,17 +141,6 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_decode_attn(
     const int tok_end = min(len, (first_tile + n_tiles) * kTile);
     const int32_t* sl = slots + ctx_off[b];
     __syncthreads();  // the previous piece's merge used the tile area
-    {  // Stage the group's Q rows (coalesced 16-byte loads).
-      const __nv_bfloat16* qb =
-          q + (static_cast<int64_t>(b) * Hq + static_cast<int64_t>(h) * G) * D;
-      for (int i = threadIdx.x; i < kTile * kChunks; i += blockDim.x) {
-        const int r = i / kChunks, c = i % kChunks;
-        uint4 v = make_uint4(0u, 0u, 0u, 0u);
-        if (r < G) v = *reinterpret_cast<const uint4*>(qb + static_cast<int64_t>(r) * D + c * 8);
-        *reinterpret_cast<uint4*>(q_sm + tile_off<D>(r, c)) = v;
-      }
-    }
-    __syncthreads();
 
     float o[D / 8][4];
 #pragma unroll
@@ -181,6 +171,8 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_decode_attn(
     };
 
     int my = 0;  // tiles of this piece handled by this warp: warp, warp + 4, ...
+    // The first K/V loads go out before Q is staged (one memory round trip
+    // less per piece: short pieces, e.g. batch 1, are latency-bound).
     // Prologue: the first kStages - 1 tiles in flight.
     int32_t nxt = fetch_slot(warp);
 #pragma unroll
@@ -190,6 +182,17 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_decode_attn(
       cp_async_commit();
       nxt = fetch_slot(t + kWarps);
     }
+    {  // Stage the group's Q rows (coalesced 16-byte loads).
+      const __nv_bfloat16* qb =
+          q + (static_cast<int64_t>(b) * Hq + static_cast<int64_t>(h) * G) * D;
+      for (int i = threadIdx.x; i < kTile * kChunks; i += blockDim.x) {
+        const int r = i / kChunks, c = i % kChunks;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (r < G) v = *reinterpret_cast<const uint4*>(qb + static_cast<int64_t>(r) * D + c * 8);
+        *reinterpret_cast<uint4*>(q_sm + tile_off<D>(r, c)) = v;
+      }
+    }
+    __syncthreads();
     for (int tile = warp; tile < n_tiles; tile += kWarps, ++my) {
       const int stage = my % kStages;
       const int ahead = tile + (kStages - 1) * kWarps;
@@ -343,11 +346,12 @@ __global__ void __launch_bounds__(kCombineThreads) k_decode_combine(
     const float* __restrict__ part_o, const float* __restrict__ part_ml,
     const int64_t* __restrict__ seg_start, int64_t n_seg, int Hq, int Hkv, int D, int grid,
     __nv_bfloat16* __restrict__ out) {
-  extern __shared__ float cw[];  // [rows][n] weights, then [rows] max and [rows] sums
-  // Launched as a programmatic dependent of the attention kernel: the
-  // launch and this prologue overlap its tail; partials are read only
-  // after the dependency resolves (the attention grid completed).
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  extern __shared__ float cw[];  // [rows][n] weights, then [rows] weight sums
+  // Launched as a programmatic dependent of the attention kernel: everything
+  // up to griddepcontrol.wait (segment bounds, piece range) overlaps its
+  // tail; partials are read only after the dependency resolves.  Three
+  // dependent memory round trips in all (bounds, (m, l) pairs, O pieces):
+  // at small batch the combine is pure latency.
   const int64_t s = blockIdx.x;
   const int rpc = (Hq / Hkv + gridDim.y - 1) / gridDim.y;  // query rows of this CTA
   const int r_base = blockIdx.y * rpc;
@@ -367,55 +371,69 @@ __global__ void __launch_bounds__(kCombineThreads) k_decode_combine(
   if (n == 1) return;
   const int rows = min(rpc, G - r_base);
   if (rows <= 0) return;
-  float* mx = cw + rows * n;
-  float* sm = mx + rows;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  float* wsum = cw + rows * n;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int rr = wid; rr < rows; rr += blockDim.x / 32) {
     const int r = r_base + rr;
+    // (m, l) of up to 64 pieces per lane pass, one 8-byte load each.
+    float wl = 0.f;
     float m = -INFINITY;
-    for (int p = lane; p < n; p += 32) m = fmaxf(m, part_ml[((c0 + p + s) * G + r) * 2]);
+    float2 ml[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int p = lane + 32 * k;
+      ml[k] = p < n ? __ldcg(reinterpret_cast<const float2*>(part_ml) + (c0 + p + s) * G + r)
+                    : make_float2(-INFINITY, 0.f);
+      m = fmaxf(m, ml[k].x);
+    }
+    for (int p = lane + 64; p < n; p += 32)
+      m = fmaxf(m, __ldcg(reinterpret_cast<const float2*>(part_ml) + (c0 + p + s) * G + r).x);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    float wl = 0.f;
-    for (int p = lane; p < n; p += 32) {
-      const float ms = part_ml[((c0 + p + s) * G + r) * 2];
-      const float ls = part_ml[((c0 + p + s) * G + r) * 2 + 1];
-      const float w = (m == -INFINITY || ms == -INFINITY || ls <= 0.f) ? 0.f : ls * exp2f(ms - m);
+    for (int p = lane, k = 0; p < n; p += 32, ++k) {
+      const float2 v = k < 2 ? ml[k] : __ldcg(reinterpret_cast<const float2*>(part_ml) + (c0 + p + s) * G + r);
+      const float w = (m == -INFINITY || v.x == -INFINITY || v.y <= 0.f) ? 0.f : v.y * exp2f(v.x - m);
       cw[rr * n + p] = w;
       wl += w;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) wl += __shfl_xor_sync(0xffffffffu, wl, o);
-    if (lane == 0) {
-      mx[rr] = m;
-      sm[rr] = wl;
-    }
+    if (lane == 0) wsum[rr] = wl;
   }
   __syncthreads();
   for (int e = threadIdx.x; e < rows * D; e += blockDim.x) {
     const int rr = e / D, d = e % D, r = r_base + rr;
-    // Pieces in batches of 8 independent loads (one round trip per batch:
-    // with the loads interleaved into the FMA chain each one waited on its
-    // own L2 round trip — 28 us at B = 1, profiles/r01).
-    float acc0 = 0.f, acc1 = 0.f;
+    // All pieces' loads in flight together (one round trip for n <= 32).
     const float* po = part_o + ((c0 + s) * G + r) * D + d;
     const int64_t step = static_cast<int64_t>(G) * D;  // between consecutive pieces
+    float acc0 = 0.f, acc1 = 0.f;
     int p = 0;
-    for (; p + 8 <= n; p += 8) {
-      float v[8];
+    for (; p + 32 <= n; p += 32) {
+      float v[32];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] = __ldcg(po + (p + k) * step);
+      for (int k = 0; k < 32; ++k) v[k] = __ldcg(po + (p + k) * step);
 #pragma unroll
-      for (int k = 0; k < 8; k += 2) {
+      for (int k = 0; k < 32; k += 2) {
         acc0 += cw[rr * n + p + k] * v[k];
         acc1 += cw[rr * n + p + k + 1] * v[k + 1];
       }
     }
-    for (; p < n; ++p) acc0 += cw[rr * n + p] * __ldcg(po + p * step);
+    auto tail = [&](auto width) {  // the last n - p < 32 pieces, predicated
+      constexpr int kW = decltype(width)::value;
+      float v[kW];
+#pragma unroll
+      for (int k = 0; k < kW; ++k) v[k] = p + k < n ? __ldcg(po + (p + k) * step) : 0.f;
+#pragma unroll
+      for (int k = 0; k < kW; ++k)
+        if (p + k < n) acc0 += cw[rr * n + p + k] * v[k];
+    };
+    if (n - p > 8) tail(std::integral_constant<int, 32>{});
+    else if (n > p) tail(std::integral_constant<int, 8>{});
     const float acc = acc0 + acc1;
-    const float wsum = sm[rr];
+    const float ws = wsum[rr];
     out[(static_cast<int64_t>(b) * Hq + static_cast<int64_t>(h) * G + r) * D + d] =
-        __float2bfloat16_rn(wsum > 0.f ? acc / wsum : 0.f);
+        __float2bfloat16_rn(ws > 0.f ? acc / ws : 0.f);
   }
 }
 
@@ -469,7 +487,7 @@ bool launch_decode_attn(const void* pool_l, int64_t row_elems, const int32_t* sl
   const int G = Hq / Hkv;
   const int row_groups = n_seg * G <= 4096 ? G : 1;
   const int rpc = (G + row_groups - 1) / row_groups;
-  const size_t csmem = sizeof(float) * (static_cast<size_t>(rpc) * (g + 1) + 2 * rpc);
+  const size_t csmem = sizeof(float) * (static_cast<size_t>(rpc) * (g + 1) + rpc);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(n_seg), row_groups);
   cfg.blockDim = dim3(rpc == 1 ? 128 : kCombineThreads);

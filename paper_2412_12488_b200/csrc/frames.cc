@@ -19,7 +19,7 @@ void ss_cache::Crc32(const void* data_dev, int64_t n, uint32_t* crc_dev, cudaStr
   OrderLaunch(s);
   mkv::DevBlock ws = DevAlloc(mkv::crc32_workspace_bytes(n, num_sms_), s);
   mkv::launch_crc32(data_dev, n, crc_dev, ws.ptr, s, num_sms_);
-  launches_ += 1;
+  CountLaunches(1);
   DevFree(ws, s);
   if (s != stream_) NoteUser(s);
 }
@@ -56,7 +56,7 @@ int64_t ss_cache::EncodeWriteFrame(SeqId seq, int64_t begin, int64_t end, int32_
     mkv::DevBlock ws = DevAlloc(mkv::crc32_workspace_bytes(static_cast<int64_t>(payload), num_sms_), s);
     mkv::launch_crc32(frame + hdr, static_cast<int64_t>(payload), static_cast<uint32_t*>(tmp.ptr),
                       ws.ptr, s, num_sms_);
-    launches_ += 1;
+    CountLaunches(1);
     mkv::CudaCheck(cudaMemcpyAsync(frame + hdr + payload, tmp.ptr, 4, cudaMemcpyDeviceToDevice, s),
               "D2D frame crc");
     DevFree(ws, s);
@@ -98,7 +98,7 @@ void ss_cache::ReceiveWriteFrame(const uint8_t* frame, int64_t size, uint8_t* ac
   if (f.payload_bytes > 0) H2D(base, frame + f.payload_offset, f.payload_bytes, st, "H2D frame payload");
   mkv::launch_crc32(base, static_cast<int64_t>(f.payload_bytes),
                     reinterpret_cast<uint32_t*>(base + o_crc), nullptr, st, num_sms_);
-  launches_ += 1;
+  CountLaunches(1);
   D2H(h_agent_pinned_, base + o_crc, 4, st, "D2H frame crc");
   mkv::CudaCheck(cudaStreamSynchronize(st), "cudaStreamSynchronize recv");
   const uint32_t crc = *h_agent_pinned_;
