@@ -491,6 +491,7 @@ def secondary_measurements(P, D, prompt, torch) -> dict:
         out["prefix_migration"] = {"error": str(ex)}
     try:
         out["transfer_sweep"] = measure_sweep(torch)
+        out["transfer_cost_model"] = fit_transfer_cost(out["transfer_sweep"])
     except Exception as ex:
         out["transfer_sweep"] = {"error": str(ex)}
     try:
@@ -814,6 +815,34 @@ def _populate_prefix_l(P, seq, prompt, torch, layers):
     torch.cuda.synchronize()
     P.synchronize()
     assert P.DrainReceiveCompletions() == [seq]
+
+
+def fit_transfer_cost(sweep: dict) -> dict:
+    """The reference's per-layer transfer cost X(n) = gamma n + delta
+    (CostModel, config.h:52-55) fitted by the reference's own
+    least squares (cost_model.py) to the measured per-layer DirectSend
+    times of the sweep (n >= 256 tokens, 80-layer launches / 80), next to
+    the model the reference ships, fitted from the paper's anchors (A100 +
+    NVSHMEM, config.cc:51-57)."""
+    from paper_2412_12488_b200.cost_model import (DEFAULT_TRANSFER_ANCHORS, default_cost_model,
+                                                  fit_cost_model)
+    pts = [(int(n), v["device_us"] / L / 1e3) for n, v in sweep.items() if int(n) >= 256]
+    prefill_dummy = [(500, 1000, 1.0), (500, 3000, 1.1)]  # the fit needs both pairs; unused
+    ours = fit_cost_model(prefill_dummy, pts)
+    ref = default_cost_model()
+    return {
+        "b200_gamma_us_per_token": round(ours.model.gamma * 1e3, 6),
+        "b200_delta_us": round(ours.model.delta * 1e3, 3),
+        "b200_fit_max_rel_err": round(max(ours.transfer_rel_err), 4),
+        "paper_gamma_us_per_token": round(ref.gamma * 1e3, 6),
+        "paper_delta_us": round(ref.delta * 1e3, 3),
+        "per_layer_ms": {str(n): {"paper_anchor": ms,
+                                  "b200_fit": round(ours.model.transfer_layer_ms(n), 5)}
+                         for n, ms in DEFAULT_TRANSFER_ANCHORS},
+        "note": "per-layer transfer of n tokens at the 70B KV shape (4 KiB per token-layer); "
+                "B200 device-local DirectSend (80-layer launches / 80) vs the paper's A100 "
+                "NVSHMEM anchors",
+    }
 
 
 def measure_sweep(torch) -> dict:

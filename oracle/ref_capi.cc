@@ -31,6 +31,7 @@
 #include <vector>
 
 #include "microkv.h"
+#include "splitserve/config.h"
 #include "splitserve/errors.h"
 #include "splitserve/hash_model.h"
 #include "splitserve/kv_cache.h"
@@ -633,6 +634,39 @@ int ss_receive_write_frame(ss_cache* c, const uint8_t* frame, int64_t size, uint
     std::copy(b.begin(), b.end(), ack_out);
     return SS_OK;
   });
+}
+
+/* The reference's calibrated cost model (config.h:40-66, config.cc:36-118),
+ * for the parity test of paper_2412_12488_b200/cost_model.py.  out[6] =
+ * {alpha, beta, gamma, delta, c0, c1}; fit_* also returns the max relative
+ * anchor error.  Anchor arrays: prefill {n_new, n_total, ms} x n_p,
+ * transfer {n_tokens, ms} x n_t. */
+int ssref_default_cost_model(double* out) {
+  const CostModel m = DefaultCostModel();
+  const double v[6] = {m.alpha, m.beta, m.gamma, m.delta, m.c0, m.c1};
+  std::copy(v, v + 6, out);
+  return SS_OK;
+}
+
+int ssref_fit_cost_model(const double* prefill, int32_t n_p, const double* transfer, int32_t n_t,
+                         double* out, double* max_rel_err) {
+  try {
+    std::vector<PrefillAnchor> pa;
+    for (int32_t i = 0; i < n_p; ++i)
+      pa.push_back({static_cast<int64_t>(prefill[3 * i]), static_cast<int64_t>(prefill[3 * i + 1]),
+                    prefill[3 * i + 2]});
+    std::vector<TransferAnchor> ta;
+    for (int32_t i = 0; i < n_t; ++i)
+      ta.push_back({static_cast<int64_t>(transfer[2 * i]), transfer[2 * i + 1]});
+    const CostFitReport r = FitCostModel(pa, ta);
+    const double v[6] = {r.model.alpha, r.model.beta, r.model.gamma, r.model.delta, r.model.c0,
+                         r.model.c1};
+    std::copy(v, v + 6, out);
+    *max_rel_err = r.max_rel_err;
+    return SS_OK;
+  } catch (const Error& e) {
+    return 1 + static_cast<int>(e.code());
+  }
 }
 
 /* Host CRC-32 of the reference (transport.cc:14-28), for tests. */
