@@ -383,6 +383,8 @@ void ss_cache::OrderAfterUser() {
   ++internal_gen_;  // the caller is about to enqueue internal work
 }
 
+void ss_cache::BeginInternal() { ++internal_gen_; }
+
 void ss_cache::OrderUser(cudaStream_t s) {
   if (internal_gen_ != internal_recorded_gen_) {
     CudaCheck(cudaEventRecord(internal_ev_, stream_), "cudaEventRecord");
@@ -1363,7 +1365,11 @@ ss_plan* ss_cache::BeginDirectSend(SeqId seq, int64_t begin, int64_t end, Rank d
   std::memcpy(host.data() + o_rp, rp.data(), sizeof(int64_t) * nr);
   std::memcpy(host.data() + o_rb, rb.data(), sizeof(int32_t) * nr);
   std::memcpy(host.data() + o_rc, rc.data(), sizeof(int32_t) * nr);
-  OrderAfterUser();
+  // A fresh block and a host upload: nothing earlier user work may still be
+  // reading (plan blocks are freed on the internal stream after the user
+  // work that read them), so no wait for the user streams here — the copy
+  // of the previous request keeps running while this plan uploads.
+  BeginInternal();
   plan->dev = DevAlloc(total, stream_);
   uint8_t* base = static_cast<uint8_t*>(plan->dev.ptr);
   H2D(base, host.data(), total, stream_, "H2D send");

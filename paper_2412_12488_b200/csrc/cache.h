@@ -358,6 +358,7 @@ struct ss_cache {
   void D2H(void* dst, const void* src, size_t bytes, cudaStream_t s, const char* what);
   void OrderAfterUser();             // internal stream waits for async work
   void OrderUser(cudaStream_t s);    // user stream waits for internal work
+  void BeginInternal();              // internal work that needs no wait for user streams
   void NoteUser(cudaStream_t s);
   void OrderLaunch(cudaStream_t s);  // user-stream launch: s after internal work
   mkv::DevBlock DevAlloc(size_t bytes, cudaStream_t s);
