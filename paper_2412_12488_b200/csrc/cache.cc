@@ -1891,6 +1891,18 @@ ss_plan* ss_cache::BeginDecode(const int64_t* seqs, const int64_t* ctx_lens, int
   return plan.release();
 }
 
+// Where split segments are merged.  Few pieces per segment (large batch:
+// most segments whole, none split more than a few ways): in the attention
+// kernel's last arriving CTA, which saves the second launch (B=32 8K 0.97
+// -> 1.0 of HBM, B=128 +2%).  Many pieces (small batch, up to 32 per
+// segment): a separate programmatic-dependent combine kernel, whose 64+
+// CTAs merge faster than one CTA per segment (B=1 8K: 16.6 vs 20.6 us).
+// MICROKV_DECODE_COMBINE=kernel|fused overrides (A/B).
+static bool DecodeCombineKernel(int64_t max_pieces) {
+  if (const char* e = std::getenv("MICROKV_DECODE_COMBINE")) return std::string(e) == "kernel";
+  return max_pieces > 4;
+}
+
 void ss_cache::DecodeAttention(ss_plan* plan, int32_t layer, int32_t hq, int32_t hkv, int32_t hd,
                                float scale, const void* q, void* out, cudaStream_t s) {
   RequireDevice("DecodeAttention");
@@ -1913,7 +1925,9 @@ void ss_cache::DecodeAttention(ss_plan* plan, int32_t layer, int32_t hq, int32_t
     // (profiles/r01/decode_grid_sweep.txt): B=8 ctx 8K 0.69 -> 0.74 of HBM,
     // B=32 0.93 -> 0.97, B=8 ctx 32K 0.97 -> 1.0, B=1 0.21 -> 0.27.
     if (n_seg <= plan->decode_grid) {
-      const int64_t k = std::min<int64_t>(plan->decode_grid / n_seg, 32);
+      int64_t cap = 32;
+      if (const char* c = std::getenv("MICROKV_DECODE_MAX_PIECES")) cap = std::max(1, std::atoi(c));
+      const int64_t k = std::min<int64_t>(plan->decode_grid / n_seg, cap);
       plan->decode_grid = static_cast<int32_t>(n_seg * k);
     }
     if (const char* g = std::getenv("MICROKV_DECODE_GRID")) {  // tuning experiments
@@ -1933,24 +1947,34 @@ void ss_cache::DecodeAttention(ss_plan* plan, int32_t layer, int32_t hq, int32_t
     const int64_t G = hq / hkv;
     const size_t bytes_o = sizeof(float) * pieces * G * hd, bytes_ml = sizeof(float) * pieces * G * 2;
     uint8_t* buf = nullptr;
-    CudaCheck(cudaMalloc(&buf, bytes_o + bytes_ml + sizeof(int64_t) * (n_seg + 1)), "cudaMalloc partials");
+    const size_t bytes_seg = sizeof(int64_t) * (n_seg + 1);
+    CudaCheck(cudaMalloc(&buf, bytes_o + bytes_ml + bytes_seg + sizeof(uint32_t) * n_seg),
+              "cudaMalloc partials");
     plan->d_partial = reinterpret_cast<float*>(buf);
     plan->d_partial_ml = reinterpret_cast<float*>(buf + bytes_o);
     plan->d_seg_start = reinterpret_cast<int64_t*>(buf + bytes_o + bytes_ml);
-    H2D(plan->d_seg_start, seg.data(), sizeof(int64_t) * (n_seg + 1), stream_, "H2D segments");
+    plan->d_seg_count = reinterpret_cast<uint32_t*>(buf + bytes_o + bytes_ml + bytes_seg);
+    H2D(plan->d_seg_start, seg.data(), bytes_seg, stream_, "H2D segments");
+    // Arrival counters of the fused combine (each launch leaves them at 0).
+    CudaCheck(cudaMemsetAsync(plan->d_seg_count, 0, sizeof(uint32_t) * n_seg, stream_), "memset");
     plan->decode_hkv = hkv;
     plan->decode_hq = hq;
     plan->decode_hd = hd;
   }
+  // Pieces per segment: k with the segment-aligned grid, at most 3 when
+  // segments outnumber CTAs.
+  const int64_t n_seg = plan->batch * hkv;
+  const bool use_kernel =
+      DecodeCombineKernel(n_seg >= plan->decode_grid ? 3 : plan->decode_grid / n_seg);
   OrderLaunch(s);
   const bool ok = launch_decode_attn(PoolLayer(layer), static_cast<int64_t>(W_) * 4,
                                      plan->d_ctx_slots, plan->d_ctx_off, plan->d_ctx_len,
                                      plan->d_seg_start, plan->batch * hkv, plan->total_tiles, q,
                                      static_cast<int>(plan->batch), hq, hkv, hd, scale,
                                      plan->d_partial, plan->d_partial_ml, out, plan->decode_grid,
-                                     s);
+                                     use_kernel ? nullptr : plan->d_seg_count, s);
   MKV_CHECK(ok, kInvalidArgument, "unsupported head_dim");
-  CountLaunches(2);
+  CountLaunches(use_kernel ? 2 : 1);
   if (s != stream_) NoteUser(s);
 }
 

@@ -92,6 +92,14 @@ __host__ __device__ __forceinline__ int64_t cta_tile_start(int64_t c, int64_t T,
   return c * T / grid;
 }
 
+// CTA whose tile range [cta_tile_start(c), cta_tile_start(c + 1)) holds tile x.
+__device__ __forceinline__ int64_t cta_of_tile(int64_t x, int64_t T, int64_t grid) {
+  int64_t c = x * grid / T;
+  while (c + 1 < grid && cta_tile_start(c + 1, T, grid) <= x) ++c;
+  while (c > 0 && cta_tile_start(c, T, grid) > x) --c;
+  return c;
+}
+
 // Shared memory per CTA: [warp][stage][K|V][16][D] tiles, then Q [16][D]
 // (swizzled like the tiles; rows >= G zero).  The end-of-piece warp merge
 // reuses the tile area.
@@ -111,8 +119,9 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_decode_attn(
     const int64_t* __restrict__ ctx_off, const int32_t* __restrict__ ctx_len,
     const int64_t* __restrict__ seg_start, int64_t n_seg, const __nv_bfloat16* __restrict__ q,
     int Hq, int Hkv, float scale_log2, float* __restrict__ part_o, float* __restrict__ part_ml,
-    __nv_bfloat16* __restrict__ out) {
+    __nv_bfloat16* __restrict__ out, uint32_t* __restrict__ seg_count) {
   static_assert(D % 16 == 0 && D <= 256, "head_dim");
+  __shared__ int merge_here;
   constexpr int kChunks = D / 8;             // 16-byte chunks per row
   constexpr int kTileBytes = kTile * D * 2;  // one K or V tile
   extern __shared__ __align__(128) uint8_t smem[];
@@ -333,6 +342,85 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_decode_attn(
         part_ml[(piece * G + r) * 2 + 1] = lsum;
       }
     }
+    if (!whole && seg_count != nullptr) {
+      // Fused combine: the last CTA to finish a piece of this segment
+      // merges all of its pieces (threadfence-reduction pattern: partials,
+      // fence, counter; the last arriver fences and reads them from L2),
+      // so no second kernel and no launch gap.
+      const int64_t c_first = cta_of_tile(s_begin, T, gridDim.x);
+      const int n = static_cast<int>(cta_of_tile(s_end - 1, T, gridDim.x) - c_first + 1);
+      // One fence per CTA: bar.sync makes the CTA's partial stores visible
+      // to thread 0, whose (cumulative) gpu-scope fence orders them before
+      // the counter update; the last arriver fences again before reading.
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned prev = atomicAdd(seg_count + sgi, 1u);
+        merge_here = prev == static_cast<unsigned>(n - 1);
+        if (merge_here) {
+          seg_count[sgi] = 0;  // ready for the next launch
+          __threadfence();
+        }
+      }
+      __syncthreads();
+      if (merge_here) {
+        float* wts = reinterpret_cast<float*>(smem);  // [G][n] weights, then [G] sums
+        float* wsum = wts + G * n;
+        const float2* ml2 = reinterpret_cast<const float2*>(part_ml);
+        for (int r = warp; r < G; r += kWarps) {
+          // (m, l) of pieces lane, lane + 32 in registers: one round trip.
+          float2 v2[2];
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+            v2[k] = lane + 32 * k < n ? __ldcg(ml2 + (c_first + lane + 32 * k + sgi) * G + r)
+                                      : make_float2(-INFINITY, 0.f);
+          float m = fmaxf(v2[0].x, v2[1].x);
+          for (int p = lane + 64; p < n; p += 32) m = fmaxf(m, __ldcg(ml2 + (c_first + p + sgi) * G + r).x);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+          float wl = 0.f;
+          for (int p = lane, k = 0; p < n; p += 32, ++k) {
+            const float2 v = k < 2 ? v2[k] : __ldcg(ml2 + (c_first + p + sgi) * G + r);
+            const float w = (m == -INFINITY || v.x == -INFINITY || v.y <= 0.f) ? 0.f : v.y * exp2f(v.x - m);
+            wts[r * n + p] = w;
+            wl += w;
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) wl += __shfl_xor_sync(0xffffffffu, wl, o);
+          if (lane == 0) wsum[r] = wl;
+        }
+        __syncthreads();
+        // Outputs as float4 column quads, every piece's load of a quad in
+        // flight together (one L2 round trip per quad).
+        const int64_t step4 = static_cast<int64_t>(G) * D / 4;
+        const float4* po4 = reinterpret_cast<const float4*>(part_o);
+        for (int e = threadIdx.x; e < G * D / 4; e += blockDim.x) {
+          const int r = (4 * e) / D, d = (4 * e) % D;
+          const float4* po = po4 + (((c_first + sgi) * G + r) * D + d) / 4;
+          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int p0 = 0; p0 < n; p0 += 32) {
+            float4 v[32];
+#pragma unroll
+            for (int k = 0; k < 32; ++k)
+              v[k] = p0 + k < n ? __ldcg(po + (p0 + k) * step4) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+              const float w = p0 + k < n ? wts[r * n + p0 + k] : 0.f;
+              acc.x += w * v[k].x;
+              acc.y += w * v[k].y;
+              acc.z += w * v[k].z;
+              acc.w += w * v[k].w;
+            }
+          }
+          const float ws = wsum[r];
+          const float inv = ws > 0.f ? 1.f / ws : 0.f;
+          __nv_bfloat16* o16 =
+              out + (static_cast<int64_t>(b) * Hq + static_cast<int64_t>(h) * G + r) * D + d;
+          reinterpret_cast<uint2*>(o16)[0] =
+              make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
+        }
+      }
+    }
     t0 = pe;
   }
 }
@@ -464,7 +552,7 @@ bool launch_decode_attn(const void* pool_l, int64_t row_elems, const int32_t* sl
                         const int64_t* ctx_off, const int32_t* ctx_len, const int64_t* seg_start,
                         int64_t n_seg, int64_t total_tiles, const void* q, int batch, int Hq,
                         int Hkv, int D, float scale, float* part_o, float* part_ml, void* out,
-                        int grid, cudaStream_t s) {
+                        int grid, uint32_t* seg_count, cudaStream_t s) {
   const float scale_log2 = scale * 1.4426950408889634f;
   const int g = static_cast<int>(total_tiles < grid ? (total_tiles < 1 ? 1 : total_tiles) : grid);
   const size_t smem = decode_attn_smem(D);
@@ -474,14 +562,15 @@ bool launch_decode_attn(const void* pool_l, int64_t row_elems, const int32_t* sl
   if (D == 128) {
     k_decode_attn<128><<<g, kWarps * 32, smem, s>>>(pool16, row_elems, slots, ctx_off, ctx_len,
                                                     seg_start, n_seg, q16, Hq, Hkv, scale_log2,
-                                                    part_o, part_ml, out16);
+                                                    part_o, part_ml, out16, seg_count);
   } else if (D == 64) {
     k_decode_attn<64><<<g, kWarps * 32, smem, s>>>(pool16, row_elems, slots, ctx_off, ctx_len,
                                                    seg_start, n_seg, q16, Hq, Hkv, scale_log2,
-                                                   part_o, part_ml, out16);
+                                                   part_o, part_ml, out16, seg_count);
   } else {
     return false;
   }
+  if (seg_count != nullptr) return true;  // pieces merged by the attention kernel
   // Few segments -> one query row per CTA (more parallel merge work); many
   // segments -> all G rows per CTA (fewer, fuller CTAs).
   const int G = Hq / Hkv;

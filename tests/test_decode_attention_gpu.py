@@ -52,8 +52,14 @@ def _ref(torch, q, K, V, scale):
     return torch.einsum("hn,nhd->hd", p, Vx)
 
 
+@pytest.mark.parametrize("combine", ["auto", "kernel", "fused"])
 @pytest.mark.parametrize("shape", SHAPES)
-def test_decode_matches_fp32_reference(cuda, shape):
+def test_decode_matches_fp32_reference(cuda, shape, combine, monkeypatch):
+    """Split segments merged by the separate combine kernel or by the
+    attention kernel's last arriving CTA (MICROKV_DECODE_COMBINE), and the
+    automatic choice: same tolerance."""
+    if combine != "auto":
+        monkeypatch.setenv("MICROKV_DECODE_COMBINE", combine)
     torch = cuda
     hq, hkv, hd = shape
     W = 4 * hkv * hd // 8
