@@ -1948,13 +1948,25 @@ void ss_cache::DecodeAttention(ss_plan* plan, int32_t layer, int32_t hq, int32_t
     const size_t bytes_o = sizeof(float) * pieces * G * hd, bytes_ml = sizeof(float) * pieces * G * 2;
     uint8_t* buf = nullptr;
     const size_t bytes_seg = sizeof(int64_t) * (n_seg + 1);
-    CudaCheck(cudaMalloc(&buf, bytes_o + bytes_ml + bytes_seg + sizeof(uint32_t) * n_seg),
+    // First segment of each CTA's tile range (see k_decode_attn), uploaded
+    // right behind the prefix sums.
+    const int64_t grid = std::min<int64_t>(plan->decode_grid, std::max<int64_t>(1, plan->total_tiles));
+    std::vector<int32_t> cta_seg(grid);
+    for (int64_t c = 0, sgi = 0; c < grid; ++c) {
+      const int64_t t0 = c * plan->total_tiles / grid;
+      while (sgi + 1 < n_seg && seg[sgi + 1] <= t0) ++sgi;
+      cta_seg[c] = static_cast<int32_t>(sgi);
+    }
+    const size_t bytes_cta = sizeof(int32_t) * grid;
+    CudaCheck(cudaMalloc(&buf, bytes_o + bytes_ml + bytes_seg + bytes_cta + sizeof(uint32_t) * n_seg),
               "cudaMalloc partials");
     plan->d_partial = reinterpret_cast<float*>(buf);
     plan->d_partial_ml = reinterpret_cast<float*>(buf + bytes_o);
     plan->d_seg_start = reinterpret_cast<int64_t*>(buf + bytes_o + bytes_ml);
-    plan->d_seg_count = reinterpret_cast<uint32_t*>(buf + bytes_o + bytes_ml + bytes_seg);
+    plan->d_cta_seg = reinterpret_cast<int32_t*>(buf + bytes_o + bytes_ml + bytes_seg);
+    plan->d_seg_count = reinterpret_cast<uint32_t*>(buf + bytes_o + bytes_ml + bytes_seg + bytes_cta);
     H2D(plan->d_seg_start, seg.data(), bytes_seg, stream_, "H2D segments");
+    H2D(plan->d_cta_seg, cta_seg.data(), bytes_cta, stream_, "H2D cta segments");
     // Arrival counters of the fused combine (each launch leaves them at 0).
     CudaCheck(cudaMemsetAsync(plan->d_seg_count, 0, sizeof(uint32_t) * n_seg, stream_), "memset");
     plan->decode_hkv = hkv;
@@ -1972,7 +1984,7 @@ void ss_cache::DecodeAttention(ss_plan* plan, int32_t layer, int32_t hq, int32_t
                                      plan->d_seg_start, plan->batch * hkv, plan->total_tiles, q,
                                      static_cast<int>(plan->batch), hq, hkv, hd, scale,
                                      plan->d_partial, plan->d_partial_ml, out, plan->decode_grid,
-                                     use_kernel ? nullptr : plan->d_seg_count, s);
+                                     use_kernel ? nullptr : plan->d_seg_count, plan->d_cta_seg, s);
   MKV_CHECK(ok, kInvalidArgument, "unsupported head_dim");
   CountLaunches(use_kernel ? 2 : 1);
   if (s != stream_) NoteUser(s);

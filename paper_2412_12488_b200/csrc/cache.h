@@ -194,6 +194,7 @@ struct ss_plan {
   float* d_partial_ml = nullptr;    // per-piece (max, sum) per head
   int64_t* d_seg_start = nullptr;   // tile prefix sums over (batch, kv head)
   uint32_t* d_seg_count = nullptr;  // fused-combine arrival counter per segment
+  int32_t* d_cta_seg = nullptr;     // first segment of each CTA's tile range
   int64_t total_tiles = 0;
   int32_t decode_hkv = 0, decode_hq = 0, decode_hd = 0;
   int32_t decode_grid = 0;

@@ -119,7 +119,8 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_decode_attn(
     const int64_t* __restrict__ ctx_off, const int32_t* __restrict__ ctx_len,
     const int64_t* __restrict__ seg_start, int64_t n_seg, const __nv_bfloat16* __restrict__ q,
     int Hq, int Hkv, float scale_log2, float* __restrict__ part_o, float* __restrict__ part_ml,
-    __nv_bfloat16* __restrict__ out, uint32_t* __restrict__ seg_count) {
+    __nv_bfloat16* __restrict__ out, uint32_t* __restrict__ seg_count,
+    const int32_t* __restrict__ cta_seg) {
   static_assert(D % 16 == 0 && D <= 256, "head_dim");
   __shared__ int merge_here;
   constexpr int kChunks = D / 8;             // 16-byte chunks per row
@@ -132,12 +133,10 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_decode_attn(
   int64_t t0 = cta_tile_start(blockIdx.x, T, gridDim.x);
   const int64_t t1 = cta_tile_start(blockIdx.x + 1, T, gridDim.x);
   if (t0 >= t1) return;
-  // Last segment whose first tile is <= t0 (binary search on the prefix sums).
-  int64_t lo = 0, hi = n_seg - 1;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi + 1) >> 1;
-    if (seg_start[mid] <= t0) lo = mid; else hi = mid - 1;
-  }
+  // Last segment whose first tile is <= t0, precomputed per CTA by the host
+  // (a device binary search here chained ~log2(segments) dependent loads
+  // before the first KV byte could be requested).
+  const int64_t lo = cta_seg[blockIdx.x];
   for (int64_t sgi = lo; t0 < t1 && sgi < n_seg; ++sgi) {
     const int64_t s_begin = seg_start[sgi], s_end = seg_start[sgi + 1];
     if (s_end <= t0) continue;  // empty segment
@@ -552,7 +551,8 @@ bool launch_decode_attn(const void* pool_l, int64_t row_elems, const int32_t* sl
                         const int64_t* ctx_off, const int32_t* ctx_len, const int64_t* seg_start,
                         int64_t n_seg, int64_t total_tiles, const void* q, int batch, int Hq,
                         int Hkv, int D, float scale, float* part_o, float* part_ml, void* out,
-                        int grid, uint32_t* seg_count, cudaStream_t s) {
+                        int grid, uint32_t* seg_count, const int32_t* cta_seg,
+                        cudaStream_t s) {
   const float scale_log2 = scale * 1.4426950408889634f;
   const int g = static_cast<int>(total_tiles < grid ? (total_tiles < 1 ? 1 : total_tiles) : grid);
   const size_t smem = decode_attn_smem(D);
@@ -562,11 +562,11 @@ bool launch_decode_attn(const void* pool_l, int64_t row_elems, const int32_t* sl
   if (D == 128) {
     k_decode_attn<128><<<g, kWarps * 32, smem, s>>>(pool16, row_elems, slots, ctx_off, ctx_len,
                                                     seg_start, n_seg, q16, Hq, Hkv, scale_log2,
-                                                    part_o, part_ml, out16, seg_count);
+                                                    part_o, part_ml, out16, seg_count, cta_seg);
   } else if (D == 64) {
     k_decode_attn<64><<<g, kWarps * 32, smem, s>>>(pool16, row_elems, slots, ctx_off, ctx_len,
                                                    seg_start, n_seg, q16, Hq, Hkv, scale_log2,
-                                                   part_o, part_ml, out16, seg_count);
+                                                   part_o, part_ml, out16, seg_count, cta_seg);
   } else {
     return false;
   }

@@ -168,7 +168,8 @@ bool launch_decode_attn(const void* pool_l, int64_t row_elems, const int32_t* sl
                         const int64_t* ctx_off, const int32_t* ctx_len, const int64_t* seg_start,
                         int64_t n_seg, int64_t total_tiles, const void* q, int batch, int Hq,
                         int Hkv, int D, float scale, float* part_o, float* part_ml, void* out,
-                        int grid, uint32_t* seg_count, cudaStream_t s);
+                        int grid, uint32_t* seg_count, const int32_t* cta_seg,
+                        cudaStream_t s);
 
 // Paged causal GQA prefill attention on tcgen05 (prefill_attn.cu): queries
 // [q_pos0, q_pos0 + n_q) of one sequence over keys [0, q_pos0 + n_q).  K/V

@@ -1,4 +1,4 @@
 #!/bin/bash
 cd "$(dirname "$0")/.."
-timeout 900 python -u -m pytest tests -m gpu -q -p no:cacheprovider 2>&1 | tail -2
-CASES=1x8192,4x8192,8x8192,1x32768,32x8192,128x4096,8x32768 timeout 300 python -u profiles/drivers/decode.py 2>&1 | tail -7
+timeout 900 python -u -m pytest tests/test_decode_attention_gpu.py -q -p no:cacheprovider 2>&1 | tail -2
+CASES=1x8192,4x8192,8x8192,16x8192,1x32768,32x8192,128x4096,8x32768 timeout 300 python -u profiles/drivers/decode.py 2>&1 | tail -8
