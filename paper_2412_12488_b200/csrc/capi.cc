@@ -18,10 +18,25 @@ using mkv::KVAddr;
 
 namespace {
 
+// The cache's device is current for the call and the caller's current
+// device is restored afterwards (a multi-GPU host keeps its own device).
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(const ss_cache* c) {
+    if (c == nullptr || c->device() < 0) return;
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != c->device()) cudaSetDevice(c->device());
+    else prev = -1;
+  }
+  ~DeviceScope() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 template <typename F>
 int Guard(ss_cache* c, F&& f) {
   try {
-    if (c && c->device() >= 0) cudaSetDevice(c->device());
+    DeviceScope scope(c);
     return f();
   } catch (const mkv::Error& e) {
     if (c) c->last_error = e.what();
@@ -73,6 +88,15 @@ int ss_abi_version(void) { return SS_ABI_VERSION; }
 const char* ss_impl_name(void) { return "microkv-b200"; }
 
 int ss_cache_create(const ss_config* cfg, ss_cache** out) {
+  int prev = -1;
+  const bool restore = cfg != nullptr && cfg->device >= 0 && cudaGetDevice(&prev) == cudaSuccess;
+  struct Restore {
+    bool on;
+    int dev;
+    ~Restore() {
+      if (on) cudaSetDevice(dev);
+    }
+  } r{restore, prev};
   try {
     *out = new ss_cache(*cfg);
     return SS_OK;
@@ -85,7 +109,10 @@ int ss_cache_create(const ss_config* cfg, ss_cache** out) {
   }
 }
 
-void ss_cache_destroy(ss_cache* c) { delete c; }
+void ss_cache_destroy(ss_cache* c) {
+  DeviceScope scope(c);
+  delete c;
+}
 const char* ss_last_error(const ss_cache* c) { return c ? c->last_error.c_str() : ""; }
 const char* ss_status_name(int s) { return mkv::StatusName(s); }
 int ss_status_retryable(int s) {

@@ -252,11 +252,7 @@ size_t crc32_workspace_bytes(int64_t, int) { return 0; }
 
 void launch_crc32(const void* data, int64_t n, uint32_t* out, void*, cudaStream_t s,
                   int num_sms) {
-  static const bool attr = [] {
-    return cudaFuncSetAttribute(k_crc32, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(kCrcSmem)) == cudaSuccess;
-  }();
-  (void)attr;
+  // The 128 KiB table attribute is set per device by preload_crc32_kernels().
   const auto* d = static_cast<const uint8_t*>(data);
   const uintptr_t a = reinterpret_cast<uintptr_t>(d);
   int64_t head = static_cast<int64_t>((32 - (a & 31)) & 31);
@@ -308,6 +304,8 @@ void launch_crc32(const void* data, int64_t n, uint32_t* out, void*, cudaStream_
 
 
 void preload_crc32_kernels() {
+  cudaFuncSetAttribute(k_crc32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(kCrcSmem));
   cudaFuncAttributes a;
   cudaFuncGetAttributes(&a, k_crc32);
 }

@@ -1961,17 +1961,7 @@ bool launch_prefill_attn(const PoolTensorMap& page_map, const PoolTensorMap& row
   const bool use_k64 = variant == "64";
   const bool use_k128s = variant == "128s";
   const bool use_k128 = !use_2sm && !use_k64 && !use_k128s;
-  static bool attr = [] {
-    return cudaFuncSetAttribute(k_prefill_attn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                kSmem + 1024) == cudaSuccess &&
-           cudaFuncSetAttribute(k_prefill_attn_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                p2::kSmem + 1024) == cudaSuccess &&
-           cudaFuncSetAttribute(k_prefill_attn_k128, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                p3::kSmem + 1024) == cudaSuccess &&
-           cudaFuncSetAttribute(k_prefill_attn_k128s, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                p3::kSmemS + 1024) == cudaSuccess;
-  }();
-  if (!attr) return false;
+  // Shared-memory attributes are set per device by preload_prefill_attn_kernels().
   PrefillArgs a;
   a.slots = slots;
   a.q = static_cast<const __nv_bfloat16*>(q);
@@ -2023,6 +2013,15 @@ bool launch_prefill_attn(const PoolTensorMap& page_map, const PoolTensorMap& row
 
 
 void preload_prefill_attn_kernels() {
+  // Per device (called once per device at cache creation): the kernels'
+  // dynamic shared memory above 48 KiB.
+  cudaFuncSetAttribute(k_prefill_attn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem + 1024);
+  cudaFuncSetAttribute(k_prefill_attn_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       p2::kSmem + 1024);
+  cudaFuncSetAttribute(k_prefill_attn_k128, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       p3::kSmem + 1024);
+  cudaFuncSetAttribute(k_prefill_attn_k128s, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       p3::kSmemS + 1024);
   cudaFuncAttributes a;
   cudaFuncGetAttributes(&a, k_prefill_attn_tc);
   cudaFuncGetAttributes(&a, k_prefill_attn_2sm);
