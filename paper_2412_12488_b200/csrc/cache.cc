@@ -968,6 +968,7 @@ void ss_cache::LaunchRemote(const PeerTarget& peer, const int32_t* d_src_slots,
   c.verdict = d_verdict;
   c.status = d_status_;
   c.sys_scope = peer.device != device_ ? 1 : 0;
+  c.pdl = 1;  // overlaps the copy grid's launch with the validation kernel
   launch_copy_rows(c, s, num_sms_);
   CountLaunches(2);
 }

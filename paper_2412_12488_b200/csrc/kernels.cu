@@ -133,6 +133,9 @@ __device__ __forceinline__ void copy_row(const uint64_t* __restrict__ src, uint6
 template <int kVec>
 __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
   extern __shared__ uint32_t s_rows[];  // per relative layer (accounting only)
+  // Programmatic dependent of the validation kernel: this grid's launch
+  // overlaps it; the verdict is read only after it completed.
+  if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
   int32_t window = -1;
   if (p.verdict != nullptr) {
     window = reinterpret_cast<const volatile int32_t*>(p.verdict)[1] != 0
@@ -295,6 +298,9 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows_fanout(FanoutParams 
 }
 
 __global__ void k_validate_remote(ValidateParams p) {
+  // Let the dependent copy grid launch now (it waits for this grid's
+  // completion before reading the verdict).
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int64_t work = p.n_ranges * p.P;
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   int32_t w0 = -1;
@@ -572,12 +578,23 @@ void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms) {
   const int per_sm = q.group == 1 ? 8 : (groups >= static_cast<int64_t>(num_sms) * 2 * warps_per_block * 8 ? 2 : 8);
   const int grid = grid_for(groups, warps_per_block, num_sms, per_sm);
   const size_t smem = q.win_received ? sizeof(uint32_t) * q.n_layers : 0;
-  if (q.W == 512) {  // Llama 8B/70B KV rows: 4 KiB
-    k_copy_rows<4><<<grid, kCopyThreads, smem, s>>>(q);
-  } else if (q.W == 128) {  // tiny config rows: 1 KiB
-    k_copy_rows<1><<<grid, kCopyThreads, smem, s>>>(q);
+  void (*kern)(CopyParams) = q.W == 512 ? k_copy_rows<4>    // Llama 8B/70B KV rows: 4 KiB
+                             : q.W == 128 ? k_copy_rows<1>  // tiny config rows: 1 KiB
+                                          : k_copy_rows<0>;
+  if (q.pdl) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(kCopyThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, q);
   } else {
-    k_copy_rows<0><<<grid, kCopyThreads, smem, s>>>(q);
+    kern<<<grid, kCopyThreads, smem, s>>>(q);
   }
 }
 
@@ -602,7 +619,7 @@ void launch_validate_remote(const ValidateParams& p, cudaStream_t s) {
   int64_t work = p.n_ranges * p.P;
   int64_t grid = (work + 255) / 256;
   if (grid < 1) grid = 1;
-  if (grid > 65535) grid = 65535;
+  if (grid > 0x7fffffff) grid = 0x7fffffff;
   k_validate_remote<<<static_cast<unsigned>(grid), 256, 0, s>>>(p);
 }
 

@@ -67,6 +67,9 @@ struct CopyParams {
   int32_t group;              // rows per warp item (set by the launcher)
   int32_t sys_scope;          // 1: the counters' observer is another GPU (fence/reds at
                               // system scope); 0: same GPU (device scope is enough)
+  int32_t pdl;                // 1: launched as a programmatic dependent of the
+                              // validation kernel (griddepcontrol.wait before
+                              // the verdict is read)
 };
 void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms);
 
