@@ -385,6 +385,17 @@ void ss_cache::OrderAfterUser() {
 
 void ss_cache::BeginInternal() { ++internal_gen_; }
 
+// Generation of a validated launch (>= 1): a failed validation stores it in
+// verdict[1], the copy compares, so verdict words need no reset per launch.
+int32_t ss_cache::NextLaunchGen() {
+  int32_t g = ++launch_gen_;
+  if (g <= 0) {  // wrapped: restart at 1 (a stale failure mark of 2^31 launches ago is moot)
+    launch_gen_ = 1;
+    g = 1;
+  }
+  return g;
+}
+
 void ss_cache::OrderUser(cudaStream_t s) {
   if (internal_gen_ != internal_recorded_gen_) {
     CudaCheck(cudaEventRecord(internal_ev_, stream_), "cudaEventRecord");
@@ -824,7 +835,7 @@ void ss_cache::PlanToDevice(ss_plan* plan) {
     sl[i].rpage = take(sizeof(int64_t) * nr);
     sl[i].rbegin = take(sizeof(int32_t) * nr);
     sl[i].rcount = take(sizeof(int32_t) * nr);
-    sl[i].verdict = take(sizeof(int32_t));
+    sl[i].verdict = take(2 * sizeof(int32_t));
   }
   const size_t upload_end = off;
   const size_t o_F = take(sizeof(uint64_t) * nf);
@@ -946,6 +957,7 @@ void ss_cache::LaunchRemote(const PeerTarget& peer, const int32_t* d_src_slots,
   v.P = peer.P;
   v.verdict = d_verdict;
   v.status = d_status_;
+  v.gen = NextLaunchGen();
   launch_validate_remote(v, s);
   CopyParams c{};
   const int64_t src_lw = num_pages_ * P_ * W_, dst_lw = peer.num_pages * peer.P * W_;
@@ -969,6 +981,7 @@ void ss_cache::LaunchRemote(const PeerTarget& peer, const int32_t* d_src_slots,
   c.status = d_status_;
   c.sys_scope = peer.device != device_ ? 1 : 0;
   c.pdl = 1;  // overlaps the copy grid's launch with the validation kernel
+  c.gen = v.gen;
   launch_copy_rows(c, s, num_sms_);
   CountLaunches(2);
 }
@@ -1360,7 +1373,7 @@ ss_plan* ss_cache::BeginDirectSend(SeqId seq, int64_t begin, int64_t end, Rank d
   const size_t o_rb = o_rp + Align(sizeof(int64_t) * nr);
   const size_t o_rc = o_rb + Align(sizeof(int32_t) * nr);
   const size_t o_v = o_rc + Align(sizeof(int32_t) * nr);
-  const size_t total = o_v + Align(sizeof(int32_t));
+  const size_t total = o_v + Align(2 * sizeof(int32_t));
   std::vector<uint8_t> host(total, 0);
   std::memcpy(host.data() + o_dst, dst.data(), sizeof(int32_t) * dst.size());
   std::memcpy(host.data() + o_rp, rp.data(), sizeof(int64_t) * nr);
@@ -1482,6 +1495,7 @@ void ss_cache::BroadcastSend(SeqId seq, int64_t begin, int64_t end, int32_t n_de
   f.n_layers = le - lb;
   f.W = W_;
   f.n_dest = n_dest;
+  f.gen = NextLaunchGen();
   for (int32_t d = 0; d < n_dest; ++d) {
     const PeerTarget& peer = PeerFor(dests[d]);
     if (peer.local != nullptr) CudaCheck(cudaStreamWaitEvent(s, peer.local->window_ev_, 0), "wait window");
@@ -1496,6 +1510,7 @@ void ss_cache::BroadcastSend(SeqId seq, int64_t begin, int64_t end, int32_t n_de
     v.P = peer.P;
     v.verdict = reinterpret_cast<int32_t*>(base + lay[d].v);
     v.status = d_status_;
+    v.gen = f.gen;
     launch_validate_remote(v, s);
     const int64_t dst_lw = peer.num_pages * peer.P * W_;
     f.dst[d] = peer.pool + lb * dst_lw;

@@ -361,6 +361,7 @@ struct ss_cache {
   void OrderAfterUser();             // internal stream waits for async work
   void OrderUser(cudaStream_t s);    // user stream waits for internal work
   void BeginInternal();              // internal work that needs no wait for user streams
+  int32_t NextLaunchGen();
   void NoteUser(cudaStream_t s);
   void OrderLaunch(cudaStream_t s);  // user-stream launch: s after internal work
   mkv::DevBlock DevAlloc(size_t bytes, cudaStream_t s);
@@ -400,6 +401,7 @@ struct ss_cache {
   int32_t rank_;
   int num_sms_ = 148;
   std::atomic<int64_t> launches_{0};
+  std::atomic<int32_t> launch_gen_{0};  // validated-launch generations (NextLaunchGen)
 
   // Host bookkeeping.
   std::vector<int64_t> free_pages_;

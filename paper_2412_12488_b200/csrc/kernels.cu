@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
   if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
   int32_t window = -1;
   if (p.verdict != nullptr) {
-    window = reinterpret_cast<const volatile int32_t*>(p.verdict)[1] != 0
+    window = reinterpret_cast<const volatile int32_t*>(p.verdict)[1] == p.gen
                  ? -1
                  : reinterpret_cast<const volatile int32_t*>(p.verdict)[0];
     if (window < 0) return;  // rejected by validation: no writes, no counts
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows_fanout(FanoutParams 
   bool live_any = false;
   for (int d = 0; d < p.n_dest; ++d) {
     const volatile int32_t* v = p.verdict[d];
-    window[d] = v[1] != 0 ? -1 : v[0];
+    window[d] = v[1] == p.gen ? -1 : v[0];
     live_any |= window[d] >= 0;
   }
   if (!live_any) return;
@@ -328,7 +328,7 @@ __global__ void k_validate_remote(ValidateParams p) {
     }
   }
   if (bad && (i < work || i == 0)) {
-    atomicOr(reinterpret_cast<unsigned int*>(p.verdict + 1), 1u);
+    *reinterpret_cast<volatile int32_t*>(p.verdict + 1) = p.gen;
     if (p.status != nullptr) atomicOr(p.status, kStatusUnknownAddress);
   }
 }
@@ -615,7 +615,6 @@ void launch_copy_rows_fanout(const FanoutParams& p, cudaStream_t s, int num_sms)
 }
 
 void launch_validate_remote(const ValidateParams& p, cudaStream_t s) {
-  cudaMemsetAsync(p.verdict + 1, 0, sizeof(int32_t), s);
   int64_t work = p.n_ranges * p.P;
   int64_t grid = (work + 255) / 256;
   if (grid < 1) grid = 1;

@@ -67,6 +67,7 @@ struct CopyParams {
   int32_t group;              // rows per warp item (set by the launcher)
   int32_t sys_scope;          // 1: the counters' observer is another GPU (fence/reds at
                               // system scope); 0: same GPU (device scope is enough)
+  int32_t gen;                // launch generation: verdict[1] == gen means rejected
   int32_t pdl;                // 1: launched as a programmatic dependent of the
                               // validation kernel (griddepcontrol.wait before
                               // the verdict is read)
@@ -92,6 +93,7 @@ struct FanoutParams {
   int32_t win_layers[kMaxFanout];
   const int32_t* verdict[kMaxFanout];
   int32_t sys_scope;          // as CopyParams::sys_scope, for any destination
+  int32_t gen;                // launch generation, as CopyParams::gen
 };
 void launch_copy_rows_fanout(const FanoutParams& p, cudaStream_t s, int num_sms);
 
@@ -107,8 +109,9 @@ struct ValidateParams {
   const uint8_t* expecting;    // destination engine [pages][P]
   int64_t num_pages;
   int32_t P;
-  int32_t* verdict;            // [0] window id, [1] failure flag
+  int32_t* verdict;            // [0] window id, [1] = gen of the last failed validation
   uint32_t* status;            // sender-side sticky status (kStatusUnknownAddress)
+  int32_t gen;                 // launch generation (>= 1): no reset of verdict[1] needed
 };
 void launch_validate_remote(const ValidateParams& p, cudaStream_t s);
 
