@@ -17,7 +17,11 @@ import torch  # noqa: E402
 from paper_2412_12488_b200 import BatchEntry, KVCache  # noqa: E402
 
 HQ, HKV, HD, W = 64, 8, 128, 512
-PEAK = 1660.6
+try:  # driver-measured burst bf16 peak (MEASURED_PEAKS.json), as bench.py uses
+    import json as _json
+    PEAK = float(_json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["bf16_tflops"])
+except Exception:
+    PEAK = 1624.4
 cases = [(int(a), int(b)) for a, b in (x.split(":") for x in
          os.environ.get("CASES", "8192:6554,8192:0,4096:0,32768:26214,2048:0").split(","))]
 reps = int(os.environ.get("REPS", "10"))
