@@ -961,7 +961,8 @@ def measure_decode(torch) -> dict:
     peak, _ = _peaks()
     res = {}
     Ld = 2
-    cases = [(8, 8192, HQ, False), (32, 8192, HQ, False), (128, 4096, HQ, False),
+    cases = [(1, 8192, HQ, False), (1, 32768, HQ, False), (8, 8192, HQ, False),
+             (32, 8192, HQ, False), (128, 4096, HQ, False), (128, 8192, HQ, False),
              (8, 32768, HQ, False), (8, 8192, HQ, True), (32, 8192, 32, False)]
     for (B, ctx, hq, frag) in cases:
         pages = B * (ctx // PAGE) + 16
