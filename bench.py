@@ -966,6 +966,9 @@ def measure_decode(torch) -> dict:
              (8, 32768, HQ, False), (8, 8192, HQ, True), (32, 8192, 32, False)]
     for (B, ctx, hq, frag) in cases:
         pages = B * (ctx // PAGE) + 16
+        # Enough layers that the launches cycle through more than L2 (126 MB):
+        # every call reads its layer from HBM, not from the previous call's L2.
+        Ld = max(2, min(16, -(-300_000_000 // (B * ctx * BPT))))
         Cd = KVCache(num_pages=pages, page_size=PAGE, layers=Ld, dim=W, device=0)
         rng = np.random.default_rng(5)
         if frag:  # take every page, free them in random order: LIFO reuse scatters them

@@ -17,13 +17,16 @@ peak = 6533.5
 cases = [(int(b), int(c)) for b, c in (x.split("x") for x in
          os.environ.get("CASES", "1x8192,8x8192,32x8192,128x4096,8x32768").split(","))]
 for B, ctx in cases:
-    c = KVCache(num_pages=B * (ctx // 16) + 16, page_size=16, layers=1, dim=W, device=0)
+    # Launches cycle over enough layers to exceed L2 (126 MB): HBM reads.
+    L = max(1, min(16, -(-300_000_000 // (B * ctx * 4096))))
+    c = KVCache(num_pages=B * (ctx // 16) + 16, page_size=16, layers=L, dim=W, device=0)
     for b in range(B):
         c.CreateSequence(b, np.zeros(ctx, np.int32))
         c.EnsureAllocated(b, ctx)
     plan = c.BeginForward([BatchEntry(b, (0, ctx)) for b in range(B)])
     rows = (torch.randn(B * ctx * W * 4, device="cuda") * 0.5).to(torch.bfloat16)
-    c.append_rows_async(plan, 0, rows.data_ptr(), 0)
+    for layer in range(L):
+        c.append_rows_async(plan, layer, rows.data_ptr(), 0)
     torch.cuda.synchronize()
     plan.close()
     del rows
@@ -39,8 +42,8 @@ for B, ctx in cases:
         torch.cuda._sleep(20_000_000)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s)
-    for _ in range(reps):
-        c.paged_decode_attention_async(d, 0, HQ, HKV, HD, HD ** -0.5, q.data_ptr(), o.data_ptr(), s.cuda_stream)
+    for i in range(reps):
+        c.paged_decode_attention_async(d, i % L, HQ, HKV, HD, HD ** -0.5, q.data_ptr(), o.data_ptr(), s.cuda_stream)
     e1.record(s)
     torch.cuda.synchronize()
     t = e0.elapsed_time(e1) / 1e3 / reps
