@@ -1,4 +1,8 @@
 #!/bin/bash
 cd "$(dirname "$0")/.."
-python -u profiles/drivers/readbw.py
-CASES=1x8192,4x8192,8x8192,16x8192,1x32768,32x8192,128x4096,8x32768 timeout 300 python -u profiles/drivers/decode.py 2>&1 | tail -8
+mkdir -p gpurun_out
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_copy_rows -s 81 -c 1 \
+  -o gpurun_out/prof_copy_rows -f python profiles/drivers/migrate.py --reps 3 > gpurun_out/ncu_full.log 2>&1
+CASES=32x8192 REPS=3 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_decode_attn -s 3 -c 1 \
+  -o gpurun_out/prof_decode -f python profiles/drivers/decode.py > gpurun_out/ncu_decode.log 2>&1
+ls -la gpurun_out/*.ncu-rep
