@@ -1246,7 +1246,8 @@ enum : int {
   kBarPFull = kBarSFull + 2,          // +tile (count 128)
   kBarODone = kBarPFull + 2,          // +tile
   kBarPHalf = kBarODone + 2,          // +tile: first half of P_i(j) (k128 only)
-  kBarCount = kBarPHalf + 2,
+  kBarOFree = kBarPHalf + 2,          // +tile: epilogue read O_i (persistent k128p only)
+  kBarCount = kBarOFree + 2,
 };
 static_assert(kBarCount * 8 + 8 <= 512, "barrier area");
 static_assert(kSmem + 1024 <= 227 * 1024, "shared memory");
@@ -1582,6 +1583,385 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
 }
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_prefill_attn_k128p(const __grid_constant__ CUtensorMap pool_map,
+                        const __grid_constant__ CUtensorMap row_map, const PrefillArgs a) {
+  using namespace p3;
+  constexpr int kKeys = p3::kKeys, kKvAtom = p3::kKvAtom, kKvTile = p3::kKvTile;
+  constexpr int kOffQ = p3::kOffQ, kOffK = p3::kOffK, kOffV = p3::kOffV, kOffBar = p3::kOffBar;
+  constexpr int kBarQ = p3::kBarQ, kBarKFull = p3::kBarKFull, kBarVFull = p3::kBarVFull;
+  constexpr int kBarKEmpty = p3::kBarKEmpty, kBarVEmpty = p3::kBarVEmpty;
+  constexpr int kBarSFull = p3::kBarSFull, kBarPFull = p3::kBarPFull, kBarODone = p3::kBarODone;
+  constexpr int kBarPHalf = p3::kBarPHalf, kBarOFree = p3::kBarOFree;
+  constexpr int kBarCount = p3::kBarCount;
+  constexpr int kStagesV = p3::kStagesV;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // Persistent: CTA c serves work items c, c + gridDim.x, ... of the
+  // (query block, KV head) list in heaviest-first order; ring stages and
+  // barrier parities run on a per-CTA tile counter across items.
+  const int n_items = a.n_blocks * a.Hkv;
+  const uint32_t sQ = smem_u32(smem + kOffQ), sK = smem_u32(smem + kOffK);
+  const uint32_t sV = smem_u32(smem + kOffV), bars = smem_u32(smem + kOffBar);
+  auto bar = [&](int i) { return bars + 8u * static_cast<uint32_t>(i); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + 8 * kBarCount);
+
+  struct Item {
+    int h, tok_first, n_keys, n_tiles;
+  };
+  auto item_of = [&](int it) {
+    Item x;
+    // Head-major (the CTAs of a wave share one head's K/V in L2: at 32K
+    // keys the 8 heads' K/V together exceed L2), heaviest block first.
+    const int qb = a.n_blocks - 1 - it % a.n_blocks;
+    x.h = it / a.n_blocks;
+    x.tok_first = qb * kQTiles * kTokens;
+    const int tok_last = min(a.n_q, x.tok_first + kQTiles * kTokens) - 1;
+    x.n_keys = a.q_pos0 + tok_last + 1;
+    x.n_tiles = (x.n_keys + kKeys - 1) / kKeys;
+    return x;
+  };
+
+  if (warp == 9) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == kSoftmaxThreads) {
+    mbar_init(bar(kBarQ), kSoftmaxThreads);
+    for (int s = 0; s < kStagesK; ++s) {
+      mbar_init(bar(kBarKFull + s), 1);
+      mbar_init(bar(kBarKEmpty + s), 1);
+    }
+    for (int s = 0; s < kStagesV; ++s) {
+      mbar_init(bar(kBarVFull + s), 1);
+      mbar_init(bar(kBarVEmpty + s), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(kBarSFull + i), 1);
+      mbar_init(bar(kBarPFull + i), kRows);
+      mbar_init(bar(kBarPHalf + i), kRows);
+      mbar_init(bar(kBarODone + i), 1);
+      mbar_init(bar(kBarOFree + i), kRows);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&pool_map))
+                 : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&row_map))
+                 : "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  constexpr uint32_t tmem = 0;
+  if (tid == 0 && *tmem_slot != 0u) __trap();
+
+  if (warp == 8 || warp == 10) {
+    // ---------------- producers: K (warp 8) / V (warp 10), lane l owns
+    // positions kPer*l .. kPer*l + kPer - 1 of the tile ----------------
+    const int C = min(a.page_size, 64), lanes_per_chunk = C / kPer;
+    const uint32_t chunk_mask = lanes_per_chunk >= 32 ? 0xffffffffu : ((1u << lanes_per_chunk) - 1u);
+    const int my_chunk_lane0 = lane - lane % lanes_per_chunk;
+    const int op = warp == 8 ? 0 : 1;
+    const int nst = op == 0 ? kStagesK : kStagesV;
+    int g = 0;  // tile counter across items
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    const Item x = item_of(it);
+    const int n_keys = x.n_keys, n_tiles = x.n_tiles;
+    const int col = op == 0 ? x.h * kD : (a.Hkv + x.h) * kD;
+    for (int j = 0; j < n_tiles; ++j, ++g) {
+      const int s = g % nst;
+      const int p0 = j * kKeys + lane * kPer;
+      int sl[kPer];
+#pragma unroll
+      for (int t = 0; t < kPer; ++t) sl[t] = p0 + t < n_keys ? __ldg(a.slots + p0 + t) : -1;
+      const int prev_last = __shfl_up_sync(0xffffffffu, sl[kPer - 1], 1);
+      bool ok = true;
+#pragma unroll
+      for (int t = 0; t < kPer; ++t) {
+        const bool chunk_start = ((lane * kPer + t) % C) == 0;
+        const int prev = t > 0 ? sl[t - 1] : prev_last;
+        if (!chunk_start && sl[t] >= 0) ok = ok && sl[t] == prev + 1;
+      }
+      const uint32_t ballot = __ballot_sync(0xffffffffu, ok);
+      const bool contiguous = ((ballot >> my_chunk_lane0) & chunk_mask) == chunk_mask;
+      const int chunk_row = __shfl_sync(0xffffffffu, sl[0], my_chunk_lane0);
+      const uint32_t base = (op == 0 ? sK : sV) + s * kKvTile;
+      const uint32_t full = bar((op == 0 ? kBarKFull : kBarVFull) + s);
+      if (lane == 0) {
+        if (g >= nst) mbar_wait(bar((op == 0 ? kBarKEmpty : kBarVEmpty) + s), ((g / nst) + 1) & 1);
+        PF_EV((op == 0 ? 0xA00 : 0xC00) | (j & 0xff));
+        mbar_expect_tx(full, kKvTile);
+      }
+      __syncwarp();
+      if (contiguous) {
+        if (lane == my_chunk_lane0) {
+          const uint32_t dst = base + (lane * kPer) * 128;
+          const int row = chunk_row >= 0 ? chunk_row : 0;
+          tma_load_3d(dst, &pool_map, col, row, a.layer, full);
+          tma_load_3d(dst + kKvAtom, &pool_map, col + 64, row, a.layer, full);
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < kPer; ++t) {
+          const uint32_t dst = base + (lane * kPer + t) * 128;
+          const int row = sl[t] >= 0 ? sl[t] : 0;
+          tma_load_3d(dst, &row_map, col, row, a.layer, full);
+          tma_load_3d(dst + kKvAtom, &row_map, col + 64, row, a.layer, full);
+        }
+      }
+    }
+    }
+  } else if (warp == 9) {
+    // ---------------- MMA issuer ----------------
+    //   prologue  S0(0) S1(0)
+    //   tile j    [P0(j)] PV0(j) S0(j+1) [P1(j)] PV1(j) S1(j+1)
+    constexpr uint32_t kIdescS = idesc_bf16(false, kKeys), kIdescO = idesc_bf16(true, kD);
+    constexpr uint32_t kHi = desc_hi(1024);
+    auto tS = [&](int i) { return tmem + i * 128; };
+    auto tO = [&](int i) { return tmem + 256 + i * 128; };
+    const uint32_t q_lo = desc_lo(sQ, 16), k_lo = desc_lo(sK, 16), v_lo = desc_lo(sV, kKvAtom);
+    auto issue_s = [&](int i, int g) {
+      const uint32_t a0 = q_lo + ((i * kTile) >> 4), b0 = k_lo + (((g % kStagesK) * kKvTile) >> 4);
+#pragma unroll
+      for (int k = 0; k < kD / 16; ++k) {
+        const uint32_t ao = ((k >> 2) * kAtom + (k & 3) * 32) >> 4;
+        const uint32_t bo = ((k >> 2) * kKvAtom + (k & 3) * 32) >> 4;
+        mma_ss_elect(tS(i), a0 + ao, b0 + bo, kHi, kIdescS, k > 0 ? 1u : 0u);
+      }
+      commit_elect(bar(kBarSFull + i));
+    };
+    auto issue_pv = [&](int i, int g, int j) {
+      const uint32_t b0 = v_lo + (((g % kStagesV) * kKvTile) >> 4);
+      mbar_wait(bar(kBarPHalf + i), g & 1);  // P_i keys [0, 64) and O_i rescaled
+      fence_after();
+#pragma unroll
+      for (int k = 0; k < kKeys / 32; ++k)
+        mma_ts_elect(tO(i), tS(i) + k * 8, b0 + ((k * 2048) >> 4), kHi, kIdescO,
+                     (j > 0 || k > 0) ? 1u : 0u);
+      mbar_wait(bar(kBarPFull + i), g & 1);  // keys [64, 128)
+      fence_after();
+#pragma unroll
+      for (int k = kKeys / 32; k < kKeys / 16; ++k)
+        mma_ts_elect(tO(i), tS(i) + k * 8, b0 + ((k * 2048) >> 4), kHi, kIdescO, 1u);
+    };
+    int g0 = 0, k_item = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++k_item) {
+      const Item x = item_of(it);
+      const int n_keys = x.n_keys, n_tiles = x.n_tiles;
+      auto zero_tail = [&](int j, int g) {
+        const int valid = n_keys - j * kKeys;
+        if (valid >= kKeys) return;
+        uint8_t* vb = smem + kOffV + (g % kStagesV) * kKvTile;
+        for (int e = lane; e < (kKeys - valid) * 16; e += 32) {
+          const int r = valid + (e >> 4), c = e & 15;
+          *reinterpret_cast<uint4*>(vb + (c >> 3) * kKvAtom + r * 128 + (c & 7) * 16) =
+              make_uint4(0, 0, 0, 0);
+        }
+        fence_proxy_async();
+        __syncwarp();
+      };
+      mbar_wait(bar(kBarQ), k_item & 1);
+      mbar_wait(bar(kBarKFull + g0 % kStagesK), (g0 / kStagesK) & 1);
+      fence_after();
+      issue_s(0, g0);
+      issue_s(1, g0);
+      commit_elect(bar(kBarKEmpty + g0 % kStagesK));
+      for (int j = 0; j < n_tiles; ++j) {
+        const int g = g0 + j;
+        const int sv = g % kStagesV;
+        mbar_wait(bar(kBarVFull + sv), (g / kStagesV) & 1);
+        if (j == n_tiles - 1) zero_tail(j, g);
+        const bool next = j + 1 < n_tiles;
+        const int sk = (g + 1) % kStagesK;
+        if (next) mbar_wait(bar(kBarKFull + sk), ((g + 1) / kStagesK) & 1);
+        fence_after();
+        for (int i = 0; i < kQTiles; ++i) {
+          // The previous item's epilogue must have read O_i before the first
+          // PV of this item overwrites it.
+          if (j == 0 && k_item > 0) {
+            mbar_wait(bar(kBarOFree + i), (k_item - 1) & 1);
+            fence_after();
+          }
+          issue_pv(i, g, j);
+          if (!next) commit_elect(bar(kBarODone + i));
+          if (next) issue_s(i, g + 1);
+        }
+        commit_elect(bar(kBarVEmpty + sv));
+        if (next) commit_elect(bar(kBarKEmpty + sk));
+      }
+      g0 += n_tiles;
+    }
+  } else {
+    // ---------------- softmax warpgroups (persistent) ----------------
+    const int i = warp >> 2;
+    const int r = tid & (kRows - 1);
+    const int G = a.Hq / a.Hkv;
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + i * 128 + lane_off, tO = tmem + 256 + i * 128 + lane_off;
+    const uint32_t qa = sQ + i * kTile;
+    // Q rows of item `it` into this tile's shared-memory slot (cp.async).
+    auto load_q = [&](int it) {
+      const Item x = item_of(it);
+      const int tok = x.tok_first + i * kTokens + r / G, g = r % G;
+      const __nv_bfloat16* qrow =
+          a.q + (static_cast<int64_t>(tok) * a.Hq + static_cast<int64_t>(x.h) * G + g) * kD;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) cp_async16(qa + sw128(r, c), qrow + c * 8, tok < a.n_q);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    auto publish_q = [&]() {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      fence_proxy_async();
+      mbar_arrive(bar(kBarQ));
+    };
+    if (static_cast<int>(blockIdx.x) < n_items) {
+      load_q(blockIdx.x);
+      publish_q();
+    }
+    const float sl2 = a.scale_log2;
+    int g0 = 0, k_item = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++k_item) {
+    const Item x = item_of(it);
+    const int h = x.h, tok_first = x.tok_first, n_tiles = x.n_tiles;
+    const int tok = tok_first + i * kTokens + r / G, g = r % G;
+    const bool row_valid = tok < a.n_q;
+    const int q_pos = a.q_pos0 + tok;
+    const int tile_min_pos = a.q_pos0 + tok_first + i * kTokens;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_tiles; ++j) {
+      const int gt = g0 + j;
+      mbar_wait(bar(kBarSFull + i), gt & 1);
+      fence_after();
+      uint32_t sr[kKeys];
+#pragma unroll
+      for (int c0 = 0; c0 < kKeys; c0 += 16) tmem_ld16_nowait(tS + c0, sr + c0);
+      tmem_wait_ld();
+      const int key0 = j * kKeys;
+      const bool need_mask =
+          __any_sync(0xffffffffu, key0 + kKeys - 1 > tile_min_pos || !row_valid);
+      if (need_mask) {
+        const int lim = row_valid ? q_pos - key0 : -1;
+#pragma unroll
+        for (int c = 0; c < kKeys; ++c) sr[c] = c > lim ? __float_as_uint(-INFINITY) : sr[c];
+      }
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int c = 0; c < kKeys; c += 8) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          mx[k] = fmaxf(mx[k], fmaxf(__uint_as_float(sr[c + 2 * k]), __uint_as_float(sr[c + 2 * k + 1])));
+      }
+      const float rmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+      const float tmax = rmax * sl2;
+      const bool bump = tmax > m + 8.f;
+      const float m_new = bump ? tmax : m;
+      const float alpha = (bump && m != -INFINITY) ? ex2_mufu(m - m_new) : 1.f;
+      const float neg_m = m_new == -INFINITY ? 0.f : -m_new;
+      const uint64_t sc2 = f2pack(sl2, sl2), nm2 = f2pack(neg_m, neg_m);
+      uint64_t acc[2] = {0ull, 0ull};
+      // P in two halves of 64 keys: the MMA warp starts PV on keys [0, 64)
+      // while the second half's exponentials run (shorter softmax -> PV
+      // chain per tile).
+      auto make_p = [&](auto poly, auto lo) {
+#pragma unroll
+        for (int c = decltype(lo)::value; c < decltype(lo)::value + kKeys / 2; c += 2) {
+          float x0, x1, p0, p1;
+          f2unpack(ffma2(f2pack(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), sc2, nm2),
+                   x0, x1);
+          if (decltype(poly)::value && PF3_POLY_EVERY > 0 &&
+              ((c >> 1) % (PF3_POLY_EVERY > 0 ? PF3_POLY_EVERY : 1)) == PF3_POLY_EVERY - 1) {
+            ex2_poly2(x0, x1, p0, p1);
+          } else {
+            p0 = ex2_mufu(x0);
+            p1 = ex2_mufu(x1);
+          }
+          acc[(c >> 1) & 1] = fadd2(acc[(c >> 1) & 1], f2pack(p0, p1));
+          sr[c / 2] = pack_bf16(p0, p1);
+        }
+      };
+      using Lo = std::integral_constant<int, 0>;
+      using Hi = std::integral_constant<int, kKeys / 2>;
+      if (need_mask) make_p(std::false_type{}, Lo{});
+      else make_p(std::true_type{}, Lo{});
+      // S_i(j) landed behind PV_i(j-1) (same issuing thread, in order), so
+      // O_i is stable here: rescale without a further wait, before PV_i(j).
+      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+        for (int c0 = 0; c0 < kD; c0 += 32) {
+          uint32_t o[32];
+          tmem_ld16_nowait(tO + c0, o);
+          tmem_ld16_nowait(tO + c0 + 16, o + 16);
+          tmem_wait_ld();
+#pragma unroll
+          for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
+          tmem_st16_nowait(tO + c0, o);
+          tmem_st16_nowait(tO + c0 + 16, o + 16);
+        }
+      }
+#pragma unroll
+      for (int c0 = 0; c0 < kKeys / 4; c0 += 16) tmem_st16_nowait(tS + c0, sr + c0);
+      tmem_wait_st();
+      fence_before();
+      mbar_arrive(bar(kBarPHalf + i));
+      if (need_mask) make_p(std::false_type{}, Hi{});
+      else make_p(std::true_type{}, Hi{});
+      float ps[4];
+      f2unpack(acc[0], ps[0], ps[1]);
+      f2unpack(acc[1], ps[2], ps[3]);
+      const float psum = (ps[0] + ps[1]) + (ps[2] + ps[3]);
+#pragma unroll
+      for (int c0 = kKeys / 4; c0 < kKeys / 2; c0 += 16) tmem_st16_nowait(tS + c0, sr + c0);
+      tmem_wait_st();
+      fence_before();
+      mbar_arrive(bar(kBarPFull + i));
+      l = l * alpha + psum;
+      m = m_new;
+    }
+    // The last PV of this item retired (S_i reads of Q_i too): the next
+    // item's Q can be loaded under this item's epilogue.
+    mbar_wait(bar(kBarODone + i), k_item & 1);
+    fence_after();
+    const int it_next = it + static_cast<int>(gridDim.x);
+    if (it_next < n_items) load_q(it_next);
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    __nv_bfloat16* orow =
+        a.out + (static_cast<int64_t>(tok) * a.Hq + static_cast<int64_t>(h) * G + g) * kD;
+#pragma unroll
+    for (int c0 = 0; c0 < kD; c0 += 32) {
+      uint32_t o[32];
+      tmem_ld16_nowait(tO + c0, o);
+      tmem_ld16_nowait(tO + c0 + 16, o + 16);
+      tmem_wait_ld();
+      if (row_valid) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          auto pk = [&](int e) {
+            return pack_bf16(__uint_as_float(o[8 * k + e]) * inv,
+                             __uint_as_float(o[8 * k + e + 1]) * inv);
+          };
+          reinterpret_cast<uint4*>(orow + c0)[k] = make_uint4(pk(0), pk(2), pk(4), pk(6));
+        }
+      }
+    }
+    fence_before();
+    mbar_arrive(bar(kBarOFree + i));
+    if (it_next < n_items) publish_q();
+    g0 += n_tiles;
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
 
 __global__ void __launch_bounds__(p3::kThreadsS, 1)
     k_prefill_attn_k128s(const __grid_constant__ CUtensorMap pool_map,
@@ -1952,15 +2332,17 @@ bool launch_prefill_attn(const PoolTensorMap& page_map, const PoolTensorMap& row
                          cudaStream_t s) {
   if (!prefill_attn_supported(page_size, Hq, Hkv, D) || n_q <= 0) return false;
   // Kernel selection (A/B of the layouts): MICROKV_PREFILL_VARIANT
-  // = "128" (default: 128-key tiles, one S slot per query tile), "128s" (the
-  // same with two softmax threads per row), "64" (64-key tiles, two S slots),
+  // = "128" (default: 128-key tiles, one S slot per query tile, one CTA per
+  // work item), "128p" (the same as persistent CTAs over the work items),
+  // "128s" (two softmax threads per row), "64" (64-key tiles, two S slots),
   // "2sm" (CTA pair, cta_group::2).  Read per launch.
   const char* ev = std::getenv("MICROKV_PREFILL_VARIANT");
   const std::string variant = ev != nullptr ? ev : "128";
   const bool use_2sm = variant == "2sm";
   const bool use_k64 = variant == "64";
   const bool use_k128s = variant == "128s";
-  const bool use_k128 = !use_2sm && !use_k64 && !use_k128s;
+  const bool use_k128p = variant == "128p";
+  const bool use_k128 = !use_2sm && !use_k64 && !use_k128s && !use_k128p;
   // Shared-memory attributes are set per device by preload_prefill_attn_kernels().
   PrefillArgs a;
   a.slots = slots;
@@ -1984,7 +2366,13 @@ bool launch_prefill_attn(const PoolTensorMap& page_map, const PoolTensorMap& row
   cudaMemset(tr, 0, 65536 * sizeof(unsigned long long));
   a.trace = tr;
 #endif
-  if (use_k128s) {
+  if (use_k128p) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int items = a.n_blocks * Hkv;
+    k_prefill_attn_k128p<<<items < sms ? items : sms, kThreads, p3::kSmem + 1024, s>>>(m, mr, a);
+  } else if (use_k128s) {
     const dim3 grid(a.n_blocks, Hkv);
     k_prefill_attn_k128s<<<grid, p3::kThreadsS, p3::kSmemS + 1024, s>>>(m, mr, a);
   } else if (use_k128) {
@@ -2022,11 +2410,14 @@ void preload_prefill_attn_kernels() {
                        p3::kSmem + 1024);
   cudaFuncSetAttribute(k_prefill_attn_k128s, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        p3::kSmemS + 1024);
+  cudaFuncSetAttribute(k_prefill_attn_k128p, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       p3::kSmem + 1024);
   cudaFuncAttributes a;
   cudaFuncGetAttributes(&a, k_prefill_attn_tc);
   cudaFuncGetAttributes(&a, k_prefill_attn_2sm);
   cudaFuncGetAttributes(&a, k_prefill_attn_k128);
   cudaFuncGetAttributes(&a, k_prefill_attn_k128s);
+  cudaFuncGetAttributes(&a, k_prefill_attn_k128p);
 }
 
 }  // namespace mkv

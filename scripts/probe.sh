@@ -1,8 +1,4 @@
 #!/bin/bash
 cd "$(dirname "$0")/.."
-mkdir -p gpurun_out
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_copy_rows -s 81 -c 1 \
-  -o gpurun_out/prof_copy_rows -f python profiles/drivers/migrate.py --reps 3 > gpurun_out/ncu_full.log 2>&1
-CASES=32x8192 REPS=3 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_decode_attn -s 3 -c 1 \
-  -o gpurun_out/prof_decode -f python profiles/drivers/decode.py > gpurun_out/ncu_decode.log 2>&1
-ls -la gpurun_out/*.ncu-rep
+timeout 900 python -u -m pytest tests -m gpu -q -p no:cacheprovider 2>&1 | tail -2
+bash scripts/pf_ab.sh > gpurun_out/pf_ab.txt 2>&1; cat gpurun_out/pf_ab.txt

@@ -166,12 +166,13 @@ def test_prefill_rejects_bad_arguments(cuda):
                                         q.data_ptr(), 0)
 
 
-@pytest.mark.parametrize("variant", ["64", "128s", "2sm"])
+@pytest.mark.parametrize("variant", ["128p", "64", "128s", "2sm"])
 @pytest.mark.parametrize("case", CASES)
 def test_prefill_variants_match_fp32_reference(cuda, case, variant, monkeypatch):
     """The other kernel layouts, selected per launch by MICROKV_PREFILL_VARIANT
-    (64-key tiles with two S slots, the split-row softmax, the CTA-pair
-    cta_group::2 kernel): same numerics bar (DESIGN.md §7: not the default,
+    (persistent CTAs over the work items, 64-key tiles with two S slots,
+    the split-row softmax, the CTA-pair cta_group::2 kernel): same numerics
+    bar (not the default,
     they measured slower or equal)."""
     monkeypatch.setenv("MICROKV_PREFILL_VARIANT", variant)
     test_prefill_matches_fp32_reference(cuda, case)
