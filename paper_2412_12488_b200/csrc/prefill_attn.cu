@@ -372,8 +372,8 @@ struct PrefillArgs {
   int layer, page_size, q_pos0, n_q, Hq, Hkv, n_blocks;
   float scale_log2;
   int pool_rows;              // rows of the pool tensor maps (an OOB row loads zeros)
-#ifdef PF_TRACE
-  unsigned long long* trace;  // debug timeline of CTA (0, 0): [count][events]
+#if defined(PF_TRACE) || defined(PF_PROF)
+  unsigned long long* trace;  // debug timeline of CTA (0, 0) / per-warp phase sums
 #endif
 };
 
@@ -1461,15 +1461,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     const float sl2 = a.scale_log2;
     float m = -INFINITY, l = 0.f;
+#ifdef PF_PROF
+    long long prof[6] = {0, 0, 0, 0, 0, 0};  // wait S, load S, max, P half 1, P half 2 + stores, total
+    long long tp0 = clock64(), tp1;
+#define PF_LAP(k) do { tp1 = clock64(); prof[k] += tp1 - tp0; tp0 = tp1; } while (0)
+#else
+#define PF_LAP(k) do {} while (0)
+#endif
     for (int j = 0; j < n_tiles; ++j) {
       if ((warp & 3) == 0 && lane == 0) PF_EV(0x400 | (i << 8) | (j & 0xff));
       mbar_wait(bar(kBarSFull + i), j & 1);
       fence_after();
+      PF_LAP(0);
       if ((warp & 3) == 0 && lane == 0) PF_EV(0x600 | (i << 8) | (j & 0xff));
       uint32_t sr[kKeys];
 #pragma unroll
       for (int c0 = 0; c0 < kKeys; c0 += 16) tmem_ld16_nowait(tS + c0, sr + c0);
       tmem_wait_ld();
+      PF_LAP(1);
       const int key0 = j * kKeys;
       const bool need_mask =
           __any_sync(0xffffffffu, key0 + kKeys - 1 > tile_min_pos || !row_valid);
@@ -1486,6 +1495,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mx[k] = fmaxf(mx[k], fmaxf(__uint_as_float(sr[c + 2 * k]), __uint_as_float(sr[c + 2 * k + 1])));
       }
       const float rmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+      PF_LAP(2);
       const float tmax = rmax * sl2;
       const bool bump = tmax > m + 8.f;
       const float m_new = bump ? tmax : m;
@@ -1537,6 +1547,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_wait_st();
       fence_before();
       mbar_arrive(bar(kBarPHalf + i));
+      PF_LAP(3);
       if (need_mask) make_p(std::false_type{}, Hi{});
       else make_p(std::true_type{}, Hi{});
       float ps[4];
@@ -1548,11 +1559,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_wait_st();
       fence_before();
       mbar_arrive(bar(kBarPFull + i));
+      PF_LAP(4);
       if ((warp & 3) == 0 && lane == 0) PF_EV(0x800 | (i << 8) | (j & 0xff));
       if (lane == 0) PF_EV(0x4000 | (warp << 8) | (j & 0xff));
       l = l * alpha + psum;
       m = m_new;
     }
+#ifdef PF_PROF
+    if (lane == 0 && blockIdx.x == 0) {  // per warp of the heaviest CTA of each head
+      unsigned long long* o = a.trace + (blockIdx.y * 8 + warp) * 8;
+      for (int k = 0; k < 5; ++k) o[k] = static_cast<unsigned long long>(prof[k]);
+      o[5] = static_cast<unsigned long long>(n_tiles);
+    }
+#endif
+#undef PF_LAP
     mbar_wait(bar(kBarODone + i), 0);
     fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
@@ -2360,7 +2380,7 @@ bool launch_prefill_attn(const PoolTensorMap& page_map, const PoolTensorMap& row
   CUtensorMap m, mr;
   std::memcpy(&m, page_map.bytes, sizeof(m));
   std::memcpy(&mr, row_map.bytes, sizeof(mr));
-#ifdef PF_TRACE
+#if defined(PF_TRACE) || defined(PF_PROF)
   unsigned long long* tr = nullptr;
   cudaMalloc(&tr, 65536 * sizeof(unsigned long long));
   cudaMemset(tr, 0, 65536 * sizeof(unsigned long long));
@@ -2385,6 +2405,22 @@ bool launch_prefill_attn(const PoolTensorMap& page_map, const PoolTensorMap& row
     const dim3 grid(a.n_blocks, Hkv);
     k_prefill_attn_tc<<<grid, kThreads, kSmem + 1024, s>>>(m, mr, a);
   }
+#ifdef PF_PROF
+  cudaDeviceSynchronize();
+  {
+    static unsigned long long hp[8 * 8 * 8];
+    cudaMemcpy(hp, tr, sizeof(hp), cudaMemcpyDeviceToHost);
+    cudaFree(tr);
+    if (FILE* f = std::fopen("gpurun_out/pf_prof.txt", "w")) {
+      for (int w = 0; w < 64; ++w)
+        if (hp[w * 8 + 5])
+          std::fprintf(f, "head %d warp %d tiles %llu wait %llu load %llu max %llu p1 %llu p2 %llu\n",
+                       w / 8, w % 8, hp[w * 8 + 5], hp[w * 8], hp[w * 8 + 1], hp[w * 8 + 2],
+                       hp[w * 8 + 3], hp[w * 8 + 4]);
+      std::fclose(f);
+    }
+  }
+#endif
 #ifdef PF_TRACE
   cudaDeviceSynchronize();
   static unsigned long long h[65536];
