@@ -2036,11 +2036,11 @@ void ss_cache::PrefillAttention(int64_t seq, int64_t q_begin, int64_t q_end, int
     tmaps_ready_ = true;
   }
   OrderLaunch(s);
-  const bool ok = launch_prefill_attn(*reinterpret_cast<const PoolTensorMap*>(tmap_page_),
+  const int nl = launch_prefill_attn(*reinterpret_cast<const PoolTensorMap*>(tmap_page_),
                                       *reinterpret_cast<const PoolTensorMap*>(tmap_row_), layer, P_,
                                       num_pages_ * P_, rec->d_slots, q, static_cast<int>(q_begin),
                                       static_cast<int>(q_end - q_begin), hq, hkv, hd, scale, out, s);
-  MKV_CHECK(ok, kInvalidArgument, "unsupported prefill attention shape");
-  CountLaunches(1);
+  MKV_CHECK(nl > 0, kInvalidArgument, "unsupported prefill attention shape");
+  CountLaunches(nl);
   if (s != stream_) NoteUser(s);
 }

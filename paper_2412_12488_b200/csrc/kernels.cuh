@@ -189,7 +189,8 @@ bool make_pool_tensor_map(void* pool, int64_t layers, int64_t rows, int64_t row_
                           int box_rows, PoolTensorMap* out);
 bool prefill_attn_supported(int page_size, int Hq, int Hkv, int D);
 int prefill_attn_box_rows(int page_size);  // rows of the page-chunk box
-bool launch_prefill_attn(const PoolTensorMap& page_map, const PoolTensorMap& row_map, int layer,
+// Returns the number of kernels launched (0: unsupported shape).
+int launch_prefill_attn(const PoolTensorMap& page_map, const PoolTensorMap& row_map, int layer,
                          int page_size, int64_t pool_rows, const int32_t* slots, const void* q,
                          int q_pos0, int n_q, int Hq, int Hkv, int D, float scale, void* out,
                          cudaStream_t s);

@@ -372,6 +372,12 @@ struct PrefillArgs {
   int layer, page_size, q_pos0, n_q, Hq, Hkv, n_blocks;
   float scale_log2;
   int pool_rows;              // rows of the pool tensor maps (an OOB row loads zeros)
+  // Key split (k_prefill_attn_k128 only): n_split CTAs per work item, each
+  // over an equal share of its key tiles, writing normalised fp32 partials
+  // [split][n_q][Hq][128] and (max, sum) pairs that k_prefill_combine merges.
+  int n_split;
+  float* part_o;
+  float2* part_ml;
 #if defined(PF_TRACE) || defined(PF_PROF)
   unsigned long long* trace;  // debug timeline of CTA (0, 0) / per-warp phase sums
 #endif
@@ -1270,7 +1276,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int qb = a.n_blocks - 1 - static_cast<int>(blockIdx.x);
+  // Heaviest (latest) query blocks first; a.n_split CTAs per block split
+  // its key tiles evenly (short balanced-PD tails fill the SMs).
+  const int qb = a.n_blocks - 1 - static_cast<int>(blockIdx.x) / a.n_split;
+  const int sp = static_cast<int>(blockIdx.x) % a.n_split;
   const int h = blockIdx.y;
   const uint32_t sQ = smem_u32(smem + kOffQ), sK = smem_u32(smem + kOffK);
   const uint32_t sV = smem_u32(smem + kOffV), bars = smem_u32(smem + kOffBar);
@@ -1281,6 +1290,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int tok_last = min(a.n_q, tok_first + kQTiles * kTokens) - 1;
   const int n_keys = a.q_pos0 + tok_last + 1;
   const int n_tiles = (n_keys + kKeys - 1) / kKeys;
+  // This CTA's key tiles [t_begin, t_begin + n_local); the host keeps
+  // n_split <= the lightest block's tile count, so n_local >= 1.
+  const int t_begin = sp * n_tiles / a.n_split;
+  const int n_local = (sp + 1) * n_tiles / a.n_split - t_begin;
 
   if (warp == 9) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
@@ -1325,8 +1338,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int op = warp == 8 ? 0 : 1;
     const int nst = op == 0 ? kStagesK : kStagesV;
     const int col = op == 0 ? h * kD : (a.Hkv + h) * kD;
-    for (int j = 0; j < n_tiles; ++j) {
-      const int s = j % nst;
+    for (int jj = 0; jj < n_local; ++jj) {
+      const int j = t_begin + jj;
+      const int s = jj % nst;
       const int p0 = j * kKeys + lane * kPer;
       int sl[kPer];
 #pragma unroll
@@ -1345,7 +1359,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t base = (op == 0 ? sK : sV) + s * kKvTile;
       const uint32_t full = bar((op == 0 ? kBarKFull : kBarVFull) + s);
       if (lane == 0) {
-        if (j >= nst) mbar_wait(bar((op == 0 ? kBarKEmpty : kBarVEmpty) + s), ((j / nst) + 1) & 1);
+        if (jj >= nst) mbar_wait(bar((op == 0 ? kBarKEmpty : kBarVEmpty) + s), ((jj / nst) + 1) & 1);
         PF_EV((op == 0 ? 0xA00 : 0xC00) | (j & 0xff));
         mbar_expect_tx(full, kKvTile);
       }
@@ -1401,10 +1415,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int k = kKeys / 32; k < kKeys / 16; ++k)
         mma_ts_elect(tO(i), tS(i) + k * 8, b0 + ((k * 2048) >> 4), kHi, kIdescO, 1u);
     };
-    auto zero_tail = [&](int j) {
+    auto zero_tail = [&](int j, int jj) {
       const int valid = n_keys - j * kKeys;
       if (valid >= kKeys) return;
-      uint8_t* vb = smem + kOffV + (j % kStagesV) * kKvTile;
+      uint8_t* vb = smem + kOffV + (jj % kStagesV) * kKvTile;
       for (int e = lane; e < (kKeys - valid) * 16; e += 32) {
         const int r = valid + (e >> 4), c = e & 15;
         *reinterpret_cast<uint4*>(vb + (c >> 3) * kKvAtom + r * 128 + (c & 7) * 16) =
@@ -1419,11 +1433,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     issue_s(0, 0);
     issue_s(1, 0);
     commit_elect(bar(kBarKEmpty));
-    for (int j = 0; j < n_tiles; ++j) {
+    for (int j = 0; j < n_local; ++j) {  // local tile index (stages, parities)
       const int sv = j % kStagesV;
       mbar_wait(bar(kBarVFull + sv), (j / kStagesV) & 1);
-      if (j == n_tiles - 1) zero_tail(j);
-      const bool next = j + 1 < n_tiles;
+      if (t_begin + j == n_tiles - 1) zero_tail(t_begin + j, j);
+      const bool next = j + 1 < n_local;
       const int sk = (j + 1) % kStagesK;
       if (next) mbar_wait(bar(kBarKFull + sk), ((j + 1) / kStagesK) & 1);
       fence_after();
@@ -1468,7 +1482,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #else
 #define PF_LAP(k) do {} while (0)
 #endif
-    for (int j = 0; j < n_tiles; ++j) {
+    for (int j = 0; j < n_local; ++j) {  // local tile index (parities, rescale)
       if ((warp & 3) == 0 && lane == 0) PF_EV(0x400 | (i << 8) | (j & 0xff));
       mbar_wait(bar(kBarSFull + i), j & 1);
       fence_after();
@@ -1479,7 +1493,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c0 = 0; c0 < kKeys; c0 += 16) tmem_ld16_nowait(tS + c0, sr + c0);
       tmem_wait_ld();
       PF_LAP(1);
-      const int key0 = j * kKeys;
+      const int key0 = (t_begin + j) * kKeys;
       const bool need_mask =
           __any_sync(0xffffffffu, key0 + kKeys - 1 > tile_min_pos || !row_valid);
       if (need_mask) {
@@ -1576,6 +1590,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_wait(bar(kBarODone + i), 0);
     fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
+    if (a.n_split > 1) {  // normalised fp32 partial + (max, sum) for k_prefill_combine
+      const int64_t prow = (static_cast<int64_t>(sp) * a.n_q + tok) * a.Hq +
+                           static_cast<int64_t>(h) * G + g;
+#pragma unroll
+      for (int c0 = 0; c0 < kD; c0 += 32) {
+        uint32_t o[32];
+        tmem_ld16_nowait(tO + c0, o);
+        tmem_ld16_nowait(tO + c0 + 16, o + 16);
+        tmem_wait_ld();
+        if (row_valid) {
+          float4* dst = reinterpret_cast<float4*>(a.part_o + prow * kD + c0);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            dst[k] = make_float4(__uint_as_float(o[4 * k]) * inv, __uint_as_float(o[4 * k + 1]) * inv,
+                                 __uint_as_float(o[4 * k + 2]) * inv, __uint_as_float(o[4 * k + 3]) * inv);
+        }
+      }
+      if (row_valid) a.part_ml[prow] = make_float2(m, l);
+    } else {
     __nv_bfloat16* orow =
         a.out + (static_cast<int64_t>(tok) * a.Hq + static_cast<int64_t>(h) * G + g) * kD;
 #pragma unroll
@@ -1595,6 +1628,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+    }
   }
   fence_before();
   __syncthreads();
@@ -1602,6 +1636,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
+}
+
+// Merge of key-split partials: one 128-thread CTA per (token, query head)
+// row, thread = head dim.  out = sum_s w_s O_s / sum_s w_s with
+// w_s = l_s 2^(m_s - max_s m_s) (O_s normalised by its own l_s).
+__global__ void __launch_bounds__(128) k_prefill_combine(const float* __restrict__ part_o,
+                                                          const float2* __restrict__ part_ml,
+                                                          int n_split, int64_t rows,
+                                                          __nv_bfloat16* __restrict__ out) {
+  const int64_t row = blockIdx.x;
+  const int d = threadIdx.x;
+  float M = -INFINITY;
+  for (int s = 0; s < n_split; ++s) M = fmaxf(M, __ldg(&part_ml[s * rows + row]).x);
+  float acc = 0.f, wsum = 0.f;
+  for (int s = 0; s < n_split; ++s) {
+    const float2 ml = __ldg(&part_ml[s * rows + row]);
+    const float w = (ml.x == -INFINITY || ml.y <= 0.f) ? 0.f : ml.y * exp2f(ml.x - M);
+    acc += w * __ldg(&part_o[(s * rows + row) * kD + d]);
+    wsum += w;
+  }
+  out[row * kD + d] = __float2bfloat16_rn(wsum > 0.f ? acc / wsum : 0.f);
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -2346,11 +2401,11 @@ bool prefill_attn_supported(int page_size, int Hq, int Hkv, int D) {
 
 int prefill_attn_box_rows(int page_size) { return page_size < kKeys ? page_size : kKeys; }
 
-bool launch_prefill_attn(const PoolTensorMap& page_map, const PoolTensorMap& row_map, int layer,
+int launch_prefill_attn(const PoolTensorMap& page_map, const PoolTensorMap& row_map, int layer,
                          int page_size, int64_t pool_rows, const int32_t* slots, const void* q,
                          int q_pos0, int n_q, int Hq, int Hkv, int D, float scale, void* out,
                          cudaStream_t s) {
-  if (!prefill_attn_supported(page_size, Hq, Hkv, D) || n_q <= 0) return false;
+  if (!prefill_attn_supported(page_size, Hq, Hkv, D) || n_q <= 0) return 0;
   // Kernel selection (A/B of the layouts): MICROKV_PREFILL_VARIANT
   // = "128" (default: 128-key tiles, one S slot per query tile, one CTA per
   // work item), "128p" (the same as persistent CTAs over the work items),
@@ -2377,6 +2432,10 @@ bool launch_prefill_attn(const PoolTensorMap& page_map, const PoolTensorMap& row
   a.n_blocks = (n_q + kQTiles * kTokens - 1) / (kQTiles * kTokens);  // 32 tokens per CTA / pair
   a.scale_log2 = scale * 1.4426950408889634f;
   a.pool_rows = static_cast<int>(pool_rows);
+  a.n_split = 1;
+  a.part_o = nullptr;
+  a.part_ml = nullptr;
+  int launches = 1;
   CUtensorMap m, mr;
   std::memcpy(&m, page_map.bytes, sizeof(m));
   std::memcpy(&mr, row_map.bytes, sizeof(mr));
@@ -2396,8 +2455,34 @@ bool launch_prefill_attn(const PoolTensorMap& page_map, const PoolTensorMap& row
     const dim3 grid(a.n_blocks, Hkv);
     k_prefill_attn_k128s<<<grid, p3::kThreadsS, p3::kSmemS + 1024, s>>>(m, mr, a);
   } else if (use_k128) {
-    const dim3 grid(a.n_blocks, Hkv);
+    // MICROKV_PREFILL_SPLIT=n: split each work item's keys over n CTAs and
+    // merge by k_prefill_combine.  Off by default: for the short
+    // balanced-PD tails it was meant for (fewer than two waves of items)
+    // the fp32 partials' extra traffic and the second launch cost more than
+    // the filled SMs gain (2K tail 47 -> 76-91 us, 4K tail 145 -> 166-209 us).
+    const int lightest_keys = q_pos0 + (n_q < kQTiles * kTokens ? n_q : kQTiles * kTokens);
+    const int tiles_min = (lightest_keys + p3::kKeys - 1) / p3::kKeys;
+    int split = 1;
+    if (const char* e = std::getenv("MICROKV_PREFILL_SPLIT")) split = std::atoi(e);
+    split = split < 1 ? 1 : (split > 8 ? 8 : split);
+    if (split > tiles_min) split = tiles_min;  // every split gets >= 1 key tile
+    a.n_split = split;
+    void* ws = nullptr;
+    const int64_t rows = static_cast<int64_t>(n_q) * Hq;
+    if (split > 1) {
+      const size_t bytes_o = sizeof(float) * split * rows * kD;
+      if (cudaMallocAsync(&ws, bytes_o + sizeof(float2) * split * rows, s) != cudaSuccess) return 0;
+      a.part_o = static_cast<float*>(ws);
+      a.part_ml = reinterpret_cast<float2*>(static_cast<char*>(ws) + bytes_o);
+    }
+    const dim3 grid(a.n_blocks * split, Hkv);
     k_prefill_attn_k128<<<grid, kThreads, p3::kSmem + 1024, s>>>(m, mr, a);
+    if (split > 1) {
+      k_prefill_combine<<<static_cast<unsigned>(rows), kD, 0, s>>>(a.part_o, a.part_ml, split, rows,
+                                                                    a.out);
+      cudaFreeAsync(ws, s);
+      launches = 2;
+    }
   } else if (use_2sm) {
     const dim3 grid(2 * a.n_blocks, Hkv);
     k_prefill_attn_2sm<<<grid, p2::kThreads, p2::kSmem + 1024, s>>>(m, mr, a);
@@ -2432,7 +2517,7 @@ bool launch_prefill_attn(const PoolTensorMap& page_map, const PoolTensorMap& row
     std::fclose(f);
   }
 #endif
-  return true;
+  return launches;
 }
 
 
@@ -2454,6 +2539,7 @@ void preload_prefill_attn_kernels() {
   cudaFuncGetAttributes(&a, k_prefill_attn_k128);
   cudaFuncGetAttributes(&a, k_prefill_attn_k128s);
   cudaFuncGetAttributes(&a, k_prefill_attn_k128p);
+  cudaFuncGetAttributes(&a, k_prefill_combine);
 }
 
 }  // namespace mkv

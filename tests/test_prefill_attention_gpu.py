@@ -82,6 +82,18 @@ def test_prefill_matches_fp32_reference(cuda, case):
         assert rel.item() <= 2e-2, (case, layer, rel.item())
 
 
+@pytest.mark.parametrize("split", [1, 2, 3, 8])
+@pytest.mark.parametrize("case", [(64, 8, 1000, 800), (32, 4, 700, 683), (64, 8, 2048, 1536),
+                                  (64, 8, 300, 0)])
+def test_prefill_key_split_matches_fp32_reference(cuda, case, split, monkeypatch):
+    """Key-split launches (short balanced-PD tails: n_split CTAs per query
+    block over equal shares of its key tiles, merged by k_prefill_combine),
+    forced through MICROKV_PREFILL_SPLIT; clamped so every split has a key
+    tile (the 300-token case from position 0 cannot split)."""
+    monkeypatch.setenv("MICROKV_PREFILL_SPLIT", str(split))
+    test_prefill_matches_fp32_reference(cuda, case)
+
+
 @pytest.mark.parametrize("page_size", [8, 32, 64, 128, 256])
 def test_prefill_page_sizes(cuda, page_size):
     torch = cuda
