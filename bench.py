@@ -507,6 +507,10 @@ def secondary_measurements(P, D, prompt, torch) -> dict:
     except Exception as ex:
         out["prefill_attention"] = {"error": str(ex)}
     try:
+        out["engine_step"] = measure_engine(torch)
+    except Exception as ex:
+        out["engine_step"] = {"error": str(ex)}
+    try:
         out["frames"] = measure_frames(torch)
     except Exception as ex:
         out["frames"] = {"error": str(ex)}
@@ -1037,6 +1041,49 @@ def _bf16_peak() -> float:
         return float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["bf16_tflops"])
     except Exception:
         return 2250.0
+
+
+def measure_engine(torch) -> dict:
+    """the engine step loop (engine.py: FIFO prefills +
+    every running decode in one ForwardPlan per step) over the reference's
+    toy hash model at the Llama-3.1-8B KV geometry (L=32, W=512): 8
+    requests of 512 tokens, 8 generated each.  Tokens/s of the whole loop
+    (host bookkeeping included) on the B200 cache and, as this row's CPU
+    baseline, on the compiled reference cache (oracle/_ref, one host
+    thread); the two engines' tokens are compared (the parity tests check
+    them against HashModel::Generate)."""
+    from paper_2412_12488_b200 import KVCache
+    from paper_2412_12488_b200.engine import Engine, GenRequest
+
+    Le, We, n_req, plen, gen = 32, 512, 8, 512, 8
+    rng = np.random.default_rng(11)
+    prompts = [[int(x) for x in rng.integers(0, 256, plen)] for _ in range(n_req)]
+    res = {"requests": n_req, "prompt_tokens": plen, "generated_per_request": gen,
+           "layers": Le, "dim": We}
+    ref = ROOT / "oracle" / "_ref" / "libmicrokv_ref.so"
+    arms = [("b200", lambda: KVCache(num_pages=512, page_size=16, layers=Le, dim=We, device=0))]
+    if ref.exists():
+        arms.append(("reference", lambda: KVCache(num_pages=512, page_size=16, layers=Le, dim=We,
+                                                  lib=str(ref))))
+    tokens = {}
+    for name, make in arms:
+        E = Engine(make(), 0)
+        reqs = [E.submit(GenRequest(i, p, 0, gen)) for i, p in enumerate(prompts)]
+        w0 = time.perf_counter()
+        steps = 0
+        while not E.idle():
+            E.step()
+            steps += 1
+        if name == "b200":
+            torch.cuda.synchronize()
+        t = time.perf_counter() - w0
+        tokens[name] = [r.tokens for r in reqs]
+        res[name] = {"steps": steps, "s": round(t, 4),
+                     "generated_tokens_per_s": round(n_req * gen / t, 1),
+                     "prefill_plus_generated_tokens_per_s": round(n_req * (plen + gen) / t, 1)}
+    if len(tokens) == 2:
+        res["tokens_identical"] = tokens["b200"] == tokens["reference"]
+    return res
 
 
 def measure_prefill(torch) -> dict:
