@@ -109,6 +109,10 @@ class ClockSampler:
 
     def __enter__(self):
         if self._ok:
+            # A short GIL switch interval so the sampler thread runs while the
+            # main thread spins on completion polls.
+            self._switch = sys.getswitchinterval()
+            sys.setswitchinterval(0.0005)
             self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
         return self
@@ -117,6 +121,7 @@ class ClockSampler:
         if self._ok:
             self._stop.set()
             self._t.join()
+            sys.setswitchinterval(self._switch)
 
     def summary(self) -> dict:
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
@@ -348,13 +353,13 @@ def our_arm(args, rank: int, world: int) -> None:
     timed: list = []
     phases.clear()
     sampler = ClockSampler(local)
-    with sampler:
-        barrier()
-        t0 = time.perf_counter()
-        for i in range(args.warmup, args.warmup + args.steps):
-            step(i, timed)
-        barrier()
-        t1 = time.perf_counter()
+    sampler.__enter__()  # covers the device-timed loop and the e2e loop below
+    barrier()
+    t0 = time.perf_counter()
+    for i in range(args.warmup, args.warmup + args.steps):
+        step(i, timed)
+    barrier()
+    t1 = time.perf_counter()
     launches = sum(x.kernel_launches() for x in engines) - l0
     c1 = [x.copy_counters() for x in engines]
     e2e_wall = None
@@ -378,6 +383,7 @@ def our_arm(args, rank: int, world: int) -> None:
         barrier()
         e2e_wall = time.perf_counter() - w0
         c0, c1 = c1, [x.copy_counters() for x in engines]  # the e2e loop's copies
+    sampler.__exit__(None, None, None)
     h2d = sum(b[0] - a[0] for a, b in zip(c0, c1)) / args.steps
     d2h = sum(b[1] - a[1] for a, b in zip(c0, c1)) / args.steps
     dev_ms = sum(a.elapsed_time(b) for a, b in timed) if timed else 0.0
