@@ -483,6 +483,10 @@ def secondary_measurements(P, D, prompt, torch) -> dict:
         out["handoff"] = measure_handoff_gemm(torch)
     except Exception as ex:
         out["handoff"] = {"error": str(ex)}
+    try:  # config 2 (Llama-3.1-8B: 32 layers, 4K prompt; ~1.8 TFLOP per layer)
+        out["handoff_8b"] = measure_handoff_gemm(torch, 32, 4096, 4096, 53248, "8B")
+    except Exception as ex:
+        out["handoff_8b"] = {"error": str(ex)}
     try:
         out["handoff_toy_prefill"] = measure_handoff(torch)
     except Exception as ex:
@@ -523,7 +527,8 @@ def secondary_measurements(P, D, prompt, torch) -> dict:
     return out
 
 
-def measure_handoff_gemm(torch) -> dict:
+def measure_handoff_gemm(torch, layers: int = L, n_prompt: int = PROMPT, k: int = 8192,
+                         n: int = 104448, label: str = "70B") -> dict:
     """1P1D PrefillThenSend at the 70B shape with a compute-bound prefill
     stand-in: per layer one bf16 GEMM of a Llama-3.1-70B layer's FLOPs at
     8,191 tokens (X[8191, 8192] @ W[8192, 104448], ~14 TFLOP), then the
@@ -534,15 +539,16 @@ def measure_handoff_gemm(torch) -> dict:
     sees every row of every layer."""
     from paper_2412_12488_b200 import BatchEntry, KVCache
 
-    prompt = _prompt(4)
-    e = PROMPT - 1
-    pages = PROMPT // PAGE + 16
-    P = KVCache(num_pages=pages, page_size=PAGE, layers=L, dim=W, device=0, rank=0)
-    D = KVCache(num_pages=pages, page_size=PAGE, layers=L, dim=W, device=0, rank=1)
+    rng = np.random.Generator(np.random.MT19937(4))
+    prompt = [int(x) for x in rng.integers(0, 256, n_prompt)]
+    e = n_prompt - 1
+    pages = n_prompt // PAGE + 16
+    P = KVCache(num_pages=pages, page_size=PAGE, layers=layers, dim=W, device=0, rank=0)
+    D = KVCache(num_pages=pages, page_size=PAGE, layers=layers, dim=W, device=0, rank=1)
     P.attach_peer(1, D)
-    X = torch.randn(e, 8192, device="cuda", dtype=torch.bfloat16)
-    Wt = torch.randn(8192, 104448, device="cuda", dtype=torch.bfloat16) * 0.01
-    Y = torch.empty(e, 104448, device="cuda", dtype=torch.bfloat16)
+    X = torch.randn(e, k, device="cuda", dtype=torch.bfloat16)
+    Wt = torch.randn(k, n, device="cuda", dtype=torch.bfloat16) * 0.01
+    Y = torch.empty(e, n, device="cuda", dtype=torch.bfloat16)
     rows = torch.randint(-2**62, 2**62, (e * W,), dtype=torch.int64, device="cuda")
     cs, ms, ds = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
     res, base = {}, None
@@ -556,9 +562,9 @@ def measure_handoff_gemm(torch) -> dict:
         dplan = P.begin_direct_send(seq, (0, e), 1, r.addr, 7) if send else None
         torch.cuda.synchronize()
         t0, tc, td = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-        layer_done = [torch.cuda.Event() for _ in range(L)]
+        layer_done = [torch.cuda.Event() for _ in range(layers)]
         t0.record(cs)
-        for layer in range(L):
+        for layer in range(layers):
             with torch.cuda.stream(cs):
                 torch.matmul(X, Wt, out=Y)
             P.append_rows_async(plan, layer, rows.data_ptr(), cs.cuda_stream)
@@ -587,7 +593,8 @@ def measure_handoff_gemm(torch) -> dict:
     res["prefill_ms_without_sends"] = round(base, 3)
     res["slowdown_pct"] = round(100 * (res["prefill_ms_with_sends"] / base - 1), 2)
     res["per_layer_payload_mb"] = round(e * BPT / 1e6, 2)
-    res["note"] = ("70B-layer-FLOP bf16 GEMM per layer (cuBLAS, compute stand-in) + KV append; "
+    res["layers"], res["prompt_tokens"] = layers, n_prompt
+    res["note"] = (f"{label}-layer-FLOP bf16 GEMM per layer (cuBLAS, compute stand-in) + KV append; "
                    "per-layer DirectSend on a second stream; P and D on one GPU")
     del P, D, X, Wt, Y, rows
     torch.cuda.empty_cache()

@@ -483,6 +483,16 @@ int64_t ss_cache::DeviceFirstNonFull(const Record* rec, int64_t from, int64_t to
 // (kv_cache.cc:340-342, 358-361, 379-381).  Positions below the committed
 // frontier, or written by `plan` on this layer, are full by construction;
 // the rest are checked on the device.
+bool ss_cache::CoveredByLivePlan(SeqId seq, int64_t begin, int64_t end) const {
+  if (begin >= end) return true;
+  for (const ss_plan* p : live_plans_) {
+    for (const auto& e : p->entries) {
+      if (e.seq == seq && e.begin <= begin && e.end >= end) return true;
+    }
+  }
+  return false;
+}
+
 void ss_cache::CheckFilled(const Record* rec, int64_t begin, int64_t end, int32_t layer,
                            const char* what, const ss_plan* plan) {
   std::vector<int32_t> unproven;
@@ -1410,9 +1420,17 @@ void ss_cache::LaunchDirectSend(ss_plan* plan, int32_t lb, int32_t le, cudaStrea
   MKV_CHECK(lb >= 0 && lb <= le && le <= L_, kInvalidArgument, "bad layer range");
   const PlanSend& snd = plan->sends[0];
   Record* rec = MustGet(snd.seq);
-  if (snd.end > rec->committed_hint) AdvanceCommitted(rec);
-  for (int32_t l = lb; l < le && snd.end > rec->committed_hint; ++l) {
-    CheckFilled(rec, snd.begin, snd.end, l, "gather over empty slot", nullptr);
+  // Positions past the committed prefix must be filled: proven by a live
+  // forward plan whose outputs cover them (PrefillThenSend: the caller sends
+  // layer l after the plan's layer-l writes on its streams), else by a
+  // device scan.  The scan synchronises with the caller's queued work, so
+  // the live-plan proof keeps a layer-by-layer send loop free of host syncs.
+  if (snd.end > rec->committed_hint &&
+      !CoveredByLivePlan(rec->id, std::max(snd.begin, rec->committed_hint), snd.end)) {
+    AdvanceCommitted(rec);
+    for (int32_t l = lb; l < le && snd.end > rec->committed_hint; ++l) {
+      CheckFilled(rec, snd.begin, snd.end, l, "gather over empty slot", nullptr);
+    }
   }
   if (lb == le) return;
   const PeerTarget& peer = PeerFor(snd.dest);

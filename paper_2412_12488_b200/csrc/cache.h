@@ -369,6 +369,7 @@ struct ss_cache {
   void PlanToDevice(ss_plan* plan);
   // Device-checked "every slot is non-Empty on `layer`" for positions of a
   // sequence not provably full on the host; throws MissingKV.
+  bool CoveredByLivePlan(SeqId seq, int64_t begin, int64_t end) const;
   void CheckFilled(const mkv::Record* rec, int64_t begin, int64_t end, int32_t layer,
                    const char* what, const ss_plan* plan);
   int64_t DeviceFirstNonFull(const mkv::Record* rec, int64_t from, int64_t to);
