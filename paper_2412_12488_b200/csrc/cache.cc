@@ -1134,8 +1134,13 @@ void ss_cache::GatherRange(SeqId seq, int64_t begin, int64_t end, int32_t layer,
   MKV_CHECK(layer >= 0 && layer < L_, kInvalidArgument, "layer out of range");
   MKV_CHECK(begin >= 0 && begin <= end, kInvalidArgument, "bad gather range");
   MKV_ICHECK(end <= rec->alloc_len, "position not allocated");
-  if (end > rec->committed_hint) AdvanceCommitted(MustGet(seq));
-  CheckFilled(rec, begin, end, layer, "gather over empty slot", nullptr);
+  // As in LaunchDirectSend: a live forward plan covering the range proves it
+  // (frames encoded layer by layer during a prefill need no host sync).
+  if (end > rec->committed_hint &&
+      !CoveredByLivePlan(seq, std::max(begin, rec->committed_hint), end)) {
+    AdvanceCommitted(MustGet(seq));
+    CheckFilled(rec, begin, end, layer, "gather over empty slot", nullptr);
+  }
   const int64_t n = end - begin;
   if (n == 0) return;
   OrderLaunch(s);
@@ -1465,9 +1470,12 @@ void ss_cache::BroadcastSend(SeqId seq, int64_t begin, int64_t end, int32_t n_de
     for (int32_t d = 0; d < n_dest; ++d) DirectSend(seq, begin, end, dests[d], addrs[d], tag, lb, le, s);
     return;
   }
-  if (end > rec->committed_hint) AdvanceCommitted(rec);
-  for (int32_t l = lb; l < le && end > rec->committed_hint; ++l) {
-    CheckFilled(rec, begin, end, l, "gather over empty slot", nullptr);
+  if (end > rec->committed_hint &&
+      !CoveredByLivePlan(seq, std::max(begin, rec->committed_hint), end)) {
+    AdvanceCommitted(rec);
+    for (int32_t l = lb; l < le && end > rec->committed_hint; ++l) {
+      CheckFilled(rec, begin, end, l, "gather over empty slot", nullptr);
+    }
   }
   if (lb == le) return;
   const int64_t n = end - begin;
