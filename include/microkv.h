@@ -28,7 +28,11 @@
  *  - "Host" entry points take host buffers and complete synchronously, like
  *    the reference.  `*_async` entry points take device pointers and a
  *    `cudaStream_t` passed as `void*` (NULL = legacy default stream) and
- *    only enqueue work.
+ *    only enqueue work.  Work enqueued on a stream is ordered after the
+ *    cache's earlier device work (uploads, window opens, resets), and the
+ *    cache's later device work is ordered after it; two different caller
+ *    streams are not ordered against each other by the library (use CUDA
+ *    events, as with any stream).
  *  - A cache created with `device = -1` is host-only: bookkeeping calls
  *    (match, prep_recv page reservation, fork, allocate, build_addr, free,
  *    evict, pin, queries on metadata) work; any call that touches KV bytes
