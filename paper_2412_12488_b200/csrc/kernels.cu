@@ -110,7 +110,10 @@ __device__ __forceinline__ void warp_copy_row(const uint64_t* __restrict__ src,
 // then copied back to back and the fill marks stored lane-parallel.  (A
 // per-row fill check serialised a fill load before every store and cost
 // ~15% of bandwidth; profiles/micro/copy_variants.cu.)
-constexpr int kGroup = 4;  // rows per item for long launches (1 for launches within one wave)
+#ifndef MKV_GROUP
+#define MKV_GROUP 4
+#endif
+constexpr int kGroup = MKV_GROUP;  // rows per item for long launches (1 for launches within one wave)
 
 // kVec > 0: rows are exactly kVec 32-byte vectors per lane (W = 128*kVec
 // words), fully unrolled; kVec == 0: any W.
@@ -160,7 +163,12 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
     const int nr = static_cast<int>(p.n_rows - r0 < group ? p.n_rows - r0 : group);
     int32_t my_s = 0, my_d = 0;  // slot indices fit int32 (checked at cache creation)
     uint8_t my_f = 0;
+#ifdef MKV_NO_FILL  // measurement only: no destination fill read / mark on remote sends
+    uint8_t* fill_l = p.verdict != nullptr ? nullptr
+                      : (p.dst_fill != nullptr ? p.dst_fill + lrel * p.dst_fill_layer : nullptr);
+#else
     uint8_t* fill_l = p.dst_fill != nullptr ? p.dst_fill + lrel * p.dst_fill_layer : nullptr;
+#endif
     if (lane < nr) {
       my_s = p.src_idx ? __ldg(p.src_idx + r0 + lane) : static_cast<int32_t>(r0 + lane);
       my_d = p.dst_idx ? __ldg(p.dst_idx + r0 + lane) : static_cast<int32_t>(r0 + lane);
@@ -575,7 +583,10 @@ void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms) {
   const int64_t one_wave = static_cast<int64_t>(num_sms) * 8 * warps_per_block;
   q.group = items <= one_wave ? 1 : kGroup;
   const int64_t groups = (q.n_rows + q.group - 1) / q.group * q.n_layers;
-  const int per_sm = q.group == 1 ? 8 : (groups >= static_cast<int64_t>(num_sms) * 2 * warps_per_block * 8 ? 2 : 8);
+#ifndef MKV_LONG_PER_SM
+#define MKV_LONG_PER_SM 2
+#endif
+  const int per_sm = q.group == 1 ? 8 : (groups >= static_cast<int64_t>(num_sms) * 2 * warps_per_block * 8 ? MKV_LONG_PER_SM : 8);
   const int grid = grid_for(groups, warps_per_block, num_sms, per_sm);
   const size_t smem = q.win_received ? sizeof(uint32_t) * q.n_layers : 0;
   void (*kern)(CopyParams) = q.W == 512 ? k_copy_rows<4>    // Llama 8B/70B KV rows: 4 KiB
