@@ -923,7 +923,9 @@ def measure_sweep(torch) -> dict:
 
 
 def measure_append_gather(torch) -> dict:
-    """KV append (dense K||V rows -> pages) and local gather at the 70B shape."""
+    """KV append (dense K||V rows -> pages) and local gather at the 70B shape;
+    every layer reads and writes its own buffers (2.7 GB each way), so no
+    launch re-reads the previous layer's data from L2."""
     from paper_2412_12488_b200 import BatchEntry, KVCache
 
     peak, _ = _peaks()
@@ -932,7 +934,7 @@ def measure_append_gather(torch) -> dict:
     C_.CreateSequence(1, _prompt(3))
     C_.EnsureAllocated(1, n)
     plan = C_.BeginForward([BatchEntry(1, (0, n))])
-    rows = torch.randint(-2**62, 2**62, (n * W,), dtype=torch.int64, device="cuda")
+    rows = torch.randint(-2**62, 2**62, (L, n * W), dtype=torch.int64, device="cuda")
     s = torch.cuda.Stream()
     # The per-layer launches are queued behind a sleep kernel so they run back
     # to back: the events time the device work, not the host's launch rate.
@@ -941,23 +943,24 @@ def measure_append_gather(torch) -> dict:
         torch.cuda._sleep(30_000_000)
     ev[0].record(s)
     for layer in range(L):
-        C_.append_rows_async(plan, layer, rows.data_ptr(), s.cuda_stream)
+        C_.append_rows_async(plan, layer, rows[layer].data_ptr(), s.cuda_stream)
     ev[1].record(s)
     torch.cuda.synchronize()
     app_s = ev[0].elapsed_time(ev[1]) / 1e3
-    out = torch.empty(n * W, dtype=torch.int64, device="cuda")
-    C_.gather_range_async(1, (0, n), 0, out.data_ptr(), s.cuda_stream)  # committed scan, once
+    out = torch.empty(L, n * W, dtype=torch.int64, device="cuda")
+    C_.gather_range_async(1, (0, n), 0, out[0].data_ptr(), s.cuda_stream)  # committed scan, once
     torch.cuda.synchronize()
     g = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     with torch.cuda.stream(s):
         torch.cuda._sleep(30_000_000)
     g[0].record(s)
     for layer in range(L):
-        C_.gather_range_async(1, (0, n), layer, out.data_ptr(), s.cuda_stream)
+        C_.gather_range_async(1, (0, n), layer, out[layer].data_ptr(), s.cuda_stream)
     g[1].record(s)
     torch.cuda.synchronize()
     gat_s = g[0].elapsed_time(g[1]) / 1e3
     assert torch.equal(out, rows), "gather(append(rows)) != rows"
+    del out, rows
     alg = 2 * n * L * BPT
     plan.close()
     return {"append_gbs": round(alg / app_s / 1e9, 1), "append_frac": round(alg / app_s / 1e9 / peak, 4),

@@ -40,7 +40,11 @@ struct alignas(32) u256 {
 // the copy lost ~12%; profiles/micro/lib_kernel.cu).
 __device__ __forceinline__ u256 ld256(const void* p) {
   u256 v;
+#ifndef MKV_LD_NO_EF  // rows are read once: L2 evict-first leaves L2 to the writes (+1%)
+  asm volatile("ld.global.L1::no_allocate.L2::evict_first.v4.u64 {%0, %1, %2, %3}, [%4];"
+#else
   asm volatile("ld.global.L1::no_allocate.v4.u64 {%0, %1, %2, %3}, [%4];"
+#endif
                : "=l"(v.a), "=l"(v.b), "=l"(v.c), "=l"(v.d)
                : "l"(p)
                : "memory");
@@ -48,7 +52,11 @@ __device__ __forceinline__ u256 ld256(const void* p) {
 }
 
 __device__ __forceinline__ void st256(void* p, const u256& v) {
+#ifdef MKV_ST_CS  // A/B: streaming (evict-first) row stores
+  asm volatile("st.global.cs.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(v.a), "l"(v.b), "l"(v.c),
+#else
   asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(v.a), "l"(v.b), "l"(v.c),
+#endif
                "l"(v.d)
                : "memory");
 }

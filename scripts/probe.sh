@@ -1,10 +1,14 @@
 #!/bin/bash
 cd "$(dirname "$0")/.."
-timeout 600 python -m pytest tests -m gpu -q -p no:cacheprovider 2>&1 | tail -2
-python - <<'PY'
+for v in "" "-DMKV_LD_NO_EF"; do
+  rm -f paper_2412_12488_b200/_lib/obj/kernels.cu.o
+  MKV_NVCC_EXTRA="$v" python -c "from paper_2412_12488_b200 import build as b; b.build()" > /dev/null 2>&1
+  python - <<PY
 import sys, json, torch
 sys.path.insert(0, '.')
 import bench
-print(json.dumps(bench.measure_handoff_gemm(torch)))
-print(json.dumps(bench.measure_handoff_gemm(torch, 32, 4096, 4096, 53248, "8B")))
+print("[$v]", json.dumps(bench.measure_append_gather(torch)))
 PY
+done
+rm -f paper_2412_12488_b200/_lib/obj/kernels.cu.o
+python -c "from paper_2412_12488_b200 import build as b; b.build()" > /dev/null
