@@ -1,14 +1,6 @@
 #!/bin/bash
 cd "$(dirname "$0")/.."
-for v in "" "-DMKV_LD_NO_EF"; do
-  rm -f paper_2412_12488_b200/_lib/obj/kernels.cu.o
-  MKV_NVCC_EXTRA="$v" python -c "from paper_2412_12488_b200 import build as b; b.build()" > /dev/null 2>&1
-  python - <<PY
-import sys, json, torch
-sys.path.insert(0, '.')
-import bench
-print("[$v]", json.dumps(bench.measure_append_gather(torch)))
-PY
-done
-rm -f paper_2412_12488_b200/_lib/obj/kernels.cu.o
-python -c "from paper_2412_12488_b200 import build as b; b.build()" > /dev/null
+mkdir -p gpurun_out
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_copy_rows -s 81 -c 1 \
+  -o gpurun_out/prof_copy_rows -f python profiles/drivers/migrate.py --reps 3 > gpurun_out/ncu_full.log 2>&1
+ls -la gpurun_out/prof_copy_rows.ncu-rep
