@@ -528,7 +528,7 @@ def secondary_measurements(P, D, prompt, torch) -> dict:
 
 
 def measure_handoff_gemm(torch, layers: int = L, n_prompt: int = PROMPT, k: int = 8192,
-                         n: int = 104448, label: str = "70B") -> dict:
+                         n: int = 104448, label: str = "70B", after: bool = True) -> dict:
     """1P1D PrefillThenSend at the 70B shape with a compute-bound prefill
     stand-in: per layer one bf16 GEMM of a Llama-3.1-70B layer's FLOPs at
     8,191 tokens (X[8191, 8192] @ W[8192, 104448], ~14 TFLOP), then the
@@ -568,7 +568,12 @@ def measure_handoff_gemm(torch, layers: int = L, n_prompt: int = PROMPT, k: int 
             with torch.cuda.stream(cs):
                 torch.matmul(X, Wt, out=Y)
             P.append_rows_async(plan, layer, rows.data_ptr(), cs.cuda_stream)
-            if send:
+            if send and after:
+                # validation now, the copy after this layer's writes
+                layer_done[layer].record(cs)
+                P.launch_direct_send_after_async(dplan, (layer, layer + 1),
+                                                 layer_done[layer].cuda_event, ms.cuda_stream)
+            elif send:
                 layer_done[layer].record(cs)
                 ms.wait_event(layer_done[layer])
                 P.launch_direct_send_async(dplan, (layer, layer + 1), ms.cuda_stream)

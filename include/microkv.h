@@ -334,6 +334,13 @@ int ss_begin_direct_send(ss_cache* cache, int64_t seq, int64_t begin, int64_t en
                          const ss_addr* dest_addr, uint64_t user_tag, ss_plan** plan_out);
 int ss_launch_direct_send_async(ss_cache* cache, ss_plan* plan, int32_t layer_begin,
                                 int32_t layer_end, void* stream);
+/* As ss_launch_direct_send_async, for a send that follows the producer's
+ * writes of these layers recorded in `event` (a cudaEvent_t): the address
+ * validation is enqueued on `stream` first, then the stream waits for
+ * `event`, then the copy — the validation's latency leaves the
+ * compute -> transfer handoff. */
+int ss_launch_direct_send_after_async(ss_cache* cache, ss_plan* plan, int32_t layer_begin,
+                                      int32_t layer_end, void* event, void* stream);
 /* Fan-out DirectSend (context-cache migration to several engines,
  * SPEC.md:434-441): the same positions [begin, end) of `seq` stored into
  * n_dest receivers at once, each through its own KVAddrInfo covering

@@ -454,6 +454,9 @@ int ss_begin_direct_send(ss_cache*, int64_t, int64_t, int64_t, int32_t, const ss
 int ss_launch_direct_send_async(ss_cache*, ss_plan*, int32_t, int32_t, void*) {
   return SS_ERR_UNSUPPORTED;
 }
+int ss_launch_direct_send_after_async(ss_cache*, ss_plan*, int32_t, int32_t, void*, void*) {
+  return SS_ERR_UNSUPPORTED;
+}
 int ss_broadcast_send_async(ss_cache*, int64_t, int64_t, int64_t, int32_t, const int32_t*,
                             const ss_addr*, uint64_t, int32_t, int32_t, void*) {
   return SS_ERR_UNSUPPORTED;

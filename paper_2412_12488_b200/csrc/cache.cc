@@ -953,7 +953,7 @@ void ss_cache::LaunchRemote(const PeerTarget& peer, const int32_t* d_src_slots,
                             const int32_t* d_dst_slots, const int64_t* d_rpage,
                             const int32_t* d_rbegin, const int32_t* d_rcount, int64_t n_ranges,
                             int32_t* d_verdict, int64_t n_rows, int32_t lb, int32_t le,
-                            cudaStream_t s) {
+                            cudaStream_t s, cudaEvent_t after) {
   // The receiver's window must be open on its device before validation.
   if (peer.local != nullptr) CudaCheck(cudaStreamWaitEvent(s, peer.local->window_ev_, 0), "wait window");
   ValidateParams v{};
@@ -969,6 +969,8 @@ void ss_cache::LaunchRemote(const PeerTarget& peer, const int32_t* d_src_slots,
   v.status = d_status_;
   v.gen = NextLaunchGen();
   launch_validate_remote(v, s);
+  // Validation ahead of the producer: only the copy waits for its writes.
+  if (after != nullptr) CudaCheck(cudaStreamWaitEvent(s, after, 0), "wait producer");
   CopyParams c{};
   const int64_t src_lw = num_pages_ * P_ * W_, dst_lw = peer.num_pages * peer.P * W_;
   c.src = d_pool_ + lb * src_lw;
@@ -990,7 +992,7 @@ void ss_cache::LaunchRemote(const PeerTarget& peer, const int32_t* d_src_slots,
   c.verdict = d_verdict;
   c.status = d_status_;
   c.sys_scope = peer.device != device_ ? 1 : 0;
-  c.pdl = 1;  // overlaps the copy grid's launch with the validation kernel
+  c.pdl = after == nullptr ? 1 : 0;  // overlaps the copy grid's launch with the validation
   c.gen = v.gen;
   launch_copy_rows(c, s, num_sms_);
   CountLaunches(2);
@@ -1419,7 +1421,8 @@ ss_plan* ss_cache::BeginDirectSend(SeqId seq, int64_t begin, int64_t end, Rank d
 
 // Computation: validation + one copy launch over rows x [lb, le).  The
 // source rows must be non-Empty (GatherRange's MissingKV, kv_cache.cc:379).
-void ss_cache::LaunchDirectSend(ss_plan* plan, int32_t lb, int32_t le, cudaStream_t s) {
+void ss_cache::LaunchDirectSend(ss_plan* plan, int32_t lb, int32_t le, cudaStream_t s,
+                                cudaEvent_t after) {
   RequireDevice("DirectSend");
   MKV_CHECK(plan->is_direct_send, kInvalidArgument, "not a direct-send plan");
   MKV_CHECK(lb >= 0 && lb <= le && le <= L_, kInvalidArgument, "bad layer range");
@@ -1443,7 +1446,7 @@ void ss_cache::LaunchDirectSend(ss_plan* plan, int32_t lb, int32_t le, cudaStrea
   const auto& d = plan->dsend[0];
   LaunchRemote(peer, rec->d_slots + snd.begin, d.dst_slots, d.range_page, d.range_begin,
                d.range_count, static_cast<int64_t>(snd.dest_addr.ranges.size()), d.verdict,
-               snd.end - snd.begin, lb, le, s);
+               snd.end - snd.begin, lb, le, s, after);
   if (s != stream_) NoteUser(s);
 }
 

@@ -262,7 +262,10 @@ struct ss_cache {
                   uint64_t tag, int32_t layer_begin, int32_t layer_end, cudaStream_t s);
   ss_plan* BeginDirectSend(SeqId seq, int64_t begin, int64_t end, Rank dest,
                            const mkv::KVAddr& addr, uint64_t tag);
-  void LaunchDirectSend(ss_plan* plan, int32_t layer_begin, int32_t layer_end, cudaStream_t s);
+  // `after` (optional): the event of the producing layer's writes; the
+  // validation is enqueued before the stream waits for it, the copy after.
+  void LaunchDirectSend(ss_plan* plan, int32_t layer_begin, int32_t layer_end, cudaStream_t s,
+                        cudaEvent_t after = nullptr);
   void BroadcastSend(SeqId seq, int64_t begin, int64_t end, int32_t n_dest, const Rank* dests,
                      const mkv::KVAddr* addrs, uint64_t tag, int32_t layer_begin,
                      int32_t layer_end, cudaStream_t s);
@@ -377,7 +380,8 @@ struct ss_cache {
   void LaunchRemote(const mkv::PeerTarget& peer, const int32_t* d_src_slots,
                     const int32_t* d_dst_slots, const int64_t* d_rpage, const int32_t* d_rbegin,
                     const int32_t* d_rcount, int64_t n_ranges, int32_t* d_verdict, int64_t n_rows,
-                    int32_t layer_begin, int32_t layer_end, cudaStream_t s);
+                    int32_t layer_begin, int32_t layer_end, cudaStream_t s,
+                    cudaEvent_t after = nullptr);
   void ExpandAddr(const mkv::KVAddr& a, std::vector<int32_t>* slots, std::vector<int64_t>* rp,
                   std::vector<int32_t>* rb, std::vector<int32_t>* rc) const;
   void OpenDeviceWindow(mkv::Record* rec, int64_t m, int64_t e);

@@ -211,6 +211,7 @@ _SIGNATURES = {
     "ss_begin_direct_send": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, C.c_int32,
                                        C.POINTER(_Addr), C.c_uint64, C.POINTER(_vp)]),
     "ss_launch_direct_send_async": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, _vp]),
+    "ss_launch_direct_send_after_async": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, _vp, _vp]),
     "ss_broadcast_send_async": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, C.c_int32, _i32p,
                                           C.POINTER(_Addr), C.c_uint64, C.c_int32, C.c_int32, _vp]),
     "ss_gather_range_async": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, C.c_int32, _vp,
@@ -880,6 +881,14 @@ class KVCache:
         lb, le = layers if layers is not None else (0, self.layers)
         self._check(self._lib.ss_launch_direct_send_async(self._h, plan.handle, lb, le,
                                                           C.c_void_p(stream)))
+
+    def launch_direct_send_after_async(self, plan: ForwardPlan, layers: tuple, event: int,
+                                       stream: int = 0) -> None:
+        """Validation now, copy after `event` (a cudaEvent_t handle, e.g.
+        torch.cuda.Event().cuda_event) of the producing layer's writes."""
+        lb, le = layers
+        self._check(self._lib.ss_launch_direct_send_after_async(
+            self._h, plan.handle, lb, le, C.c_void_p(event), C.c_void_p(stream)))
 
     def broadcast_send_async(self, seq: int, range: tuple, dests: Sequence[int],
                              dest_addrs: Sequence[KVAddrInfo], user_tag: int = 0,

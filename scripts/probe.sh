@@ -1,6 +1,14 @@
 #!/bin/bash
 cd "$(dirname "$0")/.."
-mkdir -p gpurun_out
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_copy_rows -s 81 -c 1 \
-  -o gpurun_out/prof_copy_rows -f python profiles/drivers/migrate.py --reps 3 > gpurun_out/ncu_full.log 2>&1
-ls -la gpurun_out/prof_copy_rows.ncu-rep
+python - <<'PY'
+import sys, json, torch
+sys.path.insert(0, '.')
+import bench
+for i in range(3):
+    for after in (True, False):
+        r = bench.measure_handoff_gemm(torch, 32, 4096, 4096, 53248, "8B", after)
+        print("8B after" if after else "8B plain", r["exposed_tail_us"], r["slowdown_pct"], r["prefill_ms_without_sends"])
+for after in (True, False):
+    r = bench.measure_handoff_gemm(torch, after=after)
+    print("70B after" if after else "70B plain", r["exposed_tail_us"], r["slowdown_pct"])
+PY

@@ -100,6 +100,36 @@ def test_direct_send_layer_by_layer(cuda):
     plan.close()
 
 
+def test_direct_send_after_producer_event(cuda):
+    """ss_launch_direct_send_after_async: validation first, copy after the
+    producing layer's event (here behind a sleep kernel on the compute
+    stream, so the copy must wait for it); bit-exact like the plain launch."""
+    torch = cuda
+    L, W, n = 4, 512, 700
+    p = _prompt(n, 44)
+    P = KVCache(num_pages=80, page_size=16, layers=L, dim=W, device=0)
+    D = KVCache(num_pages=80, page_size=16, layers=L, dim=W, device=0, rank=1)
+    P.attach_peer(1, D)
+    P.CreateSequence(1, p)
+    P.EnsureAllocated(1, n)
+    prefill(P, 1, p, 0, n)
+    r = D.PrepRecv(7, p, -1)
+    plan = P.begin_direct_send(1, (0, n - 1), 1, r.addr, 1)
+    cs, ms = torch.cuda.Stream(), torch.cuda.Stream()
+    evs = [torch.cuda.Event() for _ in range(L)]
+    for layer in range(L):
+        with torch.cuda.stream(cs):
+            torch.cuda._sleep(2_000_000)
+        evs[layer].record(cs)
+        P.launch_direct_send_after_async(plan, (layer, layer + 1), evs[layer].cuda_event,
+                                         ms.cuda_stream)
+    torch.cuda.synchronize()
+    assert D.DrainReceiveCompletions() == [7]
+    for layer in range(L):
+        assert np.array_equal(P.GatherRange(1, (0, n - 1), layer), D.GatherRange(7, (0, n - 1), layer))
+    plan.close()
+
+
 def test_append_rows_then_gather_roundtrip(cuda):
     torch = cuda
     L, W = 3, 512
