@@ -52,6 +52,7 @@ BPT = W * 8                                     # bytes per (token, layer) = 2*8
 PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM = 6650.0                            # B200_PROFILING.md fallback
 NVLINK_PEER_GBS = 770.0                          # B200_PROFILING.md measured peer copy
+NVLINK_NOMINAL_GBS = 900.0                       # NVLink 5, per direction
 WORKLOAD = ("llama-3.1-70b-kv 8k-prompt DirectSend KV migration P->D "
             "(L=80, 8 kv heads x hd 128 bf16 = 4 KiB/token/layer, page 16, prep_recv end=-1)")
 
@@ -235,6 +236,9 @@ def our_arm(args, rank: int, world: int) -> None:
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if os.environ.get("MICROKV_SHARE_DEVICE") == "1":
         local = 0  # test hook: run the N>1 pair protocol with every rank on cuda:0
+    elif local >= torch.cuda.device_count():
+        raise SystemExit(f"rank {rank}: --gpus {world} needs {world} GPUs, "
+                         f"{torch.cuda.device_count()} visible")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("gloo")
@@ -262,6 +266,9 @@ def our_arm(args, rank: int, world: int) -> None:
         if role == "P":
             P, D = me, None
             P.import_ipc(peer_rank, handles[peer_rank])
+            peer = P.peer_info(peer_rank)
+            # A peer on another physical GPU publishes at system scope.
+            assert peer["sys_scope"] or os.environ.get("MICROKV_SHARE_DEVICE") == "1", peer
         else:
             P, D = None, me
     if P is not None:
@@ -347,6 +354,8 @@ def our_arm(args, rank: int, world: int) -> None:
             assert np.array_equal(P.GatherRange(1, (0, e), layer), D.GatherRange(99, (0, e), layer))
         D.FreeSequence(99)
 
+    if world > 1:
+        _pair_spot_check(P, D, prompt, e, peer_rank, torch, dist)
     engines = [x for x in (P, D) if x is not None]
     l0 = sum(x.kernel_launches() for x in engines)
     c0 = [x.copy_counters() for x in engines]
@@ -430,12 +439,19 @@ def our_arm(args, rank: int, world: int) -> None:
                     "peak_kind": f"{peak_kind} hbm_gbs (burst copy)",
                     "algorithmic_bytes_per_launch": alg}
     else:
-        roofline = {"bound": "nvlink", "achieved": round(payload / per_launch_s / 1e9, 1),
+        # Per link: each pair's P->D copy is one GPU's NVLink egress; the
+        # per-launch time is the max over ranks.
+        link = payload / per_launch_s / 1e9
+        roofline = {"bound": "nvlink", "achieved": round(link, 1),
                     "peak": NVLINK_PEER_GBS, "unit": "GB/s",
-                    "frac": round(payload / per_launch_s / 1e9 / NVLINK_PEER_GBS, 4),
-                    "traffic": None, "kernel": "k_copy_rows (peer stores)",
-                    "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
-                    "algorithmic_bytes_per_launch": payload}
+                    "frac": round(link / NVLINK_PEER_GBS, 4),
+                    "peak_nominal": NVLINK_NOMINAL_GBS,
+                    "frac_nominal": round(link / NVLINK_NOMINAL_GBS, 4),
+                    "traffic": None, "kernel": "k_copy_rows (peer stores, system-scope counters)",
+                    "peak_kind": "measured peer copy per direction (B200_PROFILING.md); "
+                                 "nominal NVLink 5 per direction beside it",
+                    "algorithmic_bytes_per_launch": payload,
+                    "per_pair_payload_gbs": round(link, 1), "pairs": pairs}
     line = {
         "metric": "KV migration GB/s (P->D, Llama-3.1-70B KV shape)",
         "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -465,6 +481,43 @@ def our_arm(args, rank: int, world: int) -> None:
         "secondary": secondary,
     }
     print(json.dumps(line), flush=True)
+
+
+def _pair_spot_check(P, D, prompt, e, peer_rank, torch, dist) -> None:
+    """N>1, outside the timed region: one migration, then CRC-32 of the
+    first and last layers' rows on both sides (P's sent rows, D's received
+    rows) must agree."""
+    seq = 99
+    crcs = []
+    if D is not None:
+        r = D.PrepRecv(seq, prompt, -1)
+        dist.send_object_list([(r.match_len, r.addr)], dst=peer_rank)
+        while seq not in D.DrainReceiveCompletions():
+            pass
+        eng = D
+    else:
+        obj = [None]
+        dist.recv_object_list(obj, src=peer_rank)
+        m, addr = obj[0]
+        P.direct_send_async(1, (m, e), peer_rank, addr, 0, (0, L), 0)
+        P.synchronize()
+        seq, eng = 1, P
+    buf = torch.empty(e * W, dtype=torch.int64, device="cuda")
+    out = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for layer in (0, L - 1):
+        eng.gather_range_async(seq, (0, e), layer, buf.data_ptr(), 0)
+        eng.crc32_async(buf.data_ptr(), e * W * 8, out.data_ptr(), 0)
+        torch.cuda.synchronize()
+        crcs.append(int(out.item()))
+    mine = [None]
+    theirs = [None]
+    if D is not None:
+        dist.send_object_list([crcs], dst=peer_rank)
+        D.FreeSequence(seq)
+    else:
+        dist.recv_object_list(theirs, src=peer_rank)
+        assert theirs[0] == crcs, f"received rows differ from sent rows: {theirs[0]} vs {crcs}"
+    del mine
 
 
 def _traffic():
@@ -1243,6 +1296,26 @@ def measure_frames(torch) -> dict:
     return res
 
 
+def _spawn_ranks(n: int) -> int:
+    """`python bench.py --gpus N` without a launcher: one process per GPU
+    (rank r on cuda:r), the same environment torchrun would give them
+    (rendezvous on 127.0.0.1); rank 0 prints the line.  Returns the worst
+    exit code."""
+    import socket
+    import subprocess
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, str(Path(__file__).resolve()), *sys.argv[1:]],
+                                      env=env))
+    return max(abs(p.wait()) for p in procs)
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -1252,8 +1325,12 @@ def main() -> None:
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_spawn_ranks(args.gpus))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
     if args.impl == "reference":
         reference_arm(args, rank, world)
     else:

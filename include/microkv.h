@@ -307,6 +307,11 @@ int ss_export_ipc(ss_cache* cache, ss_ipc_handle* out);
 /* Map a peer process's receive surface as the destination for `dest`. */
 int ss_import_ipc(ss_cache* cache, int32_t dest, const ss_ipc_handle* handle);
 int ss_detach_peer(ss_cache* cache, int32_t dest);
+/* How sends to `dest` publish (evidence / tests): *sys_scope = 1 when the
+ * window counters are released at system scope (the peer is another GPU,
+ * or MICROKV_FORCE_SYS_SCOPE=1), *peer_device = the peer's device ordinal
+ * in this process (-2: another physical GPU mapped through CUDA IPC). */
+int ss_peer_info(const ss_cache* cache, int32_t dest, int32_t* sys_scope, int32_t* peer_device);
 
 /* Attention with device hidden buffers, enqueued on `stream`.  Marked
  * sends must target attached peers (device-direct); otherwise

@@ -173,6 +173,10 @@ ss_cache::ss_cache(const ss_config& cfg)
   MKV_CHECK(cfg.num_pages * cfg.page_size < (int64_t(1) << 31), kInvalidArgument,
             "num_pages * page_size must fit int32 slot indices");
   seed_state_ = mkv::seed_state(hash_seed_);
+  // Test hook: publish window counters at system scope even to a peer on
+  // this GPU, so a one-GPU run executes the cross-GPU (NVLink) branch of
+  // the copy kernels: system-scope fence + red.release.sys.
+  if (const char* f = std::getenv("MICROKV_FORCE_SYS_SCOPE")) force_sys_scope_ = std::atoi(f) != 0;
   while ((1 << page_shift_) < P_) ++page_shift_;
   // LIFO free list, lowest page first out (kv_cache.cc:45-46).
   free_pages_.reserve(num_pages_);
@@ -199,7 +203,6 @@ ss_cache::ss_cache(const ss_config& cfg)
   }
   CudaCheck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
   CudaCheck(cudaEventCreateWithFlags(&internal_ev_, cudaEventDisableTiming), "event");
-  CudaCheck(cudaEventCreateWithFlags(&user_ev_, cudaEventDisableTiming), "event");
   CudaCheck(cudaEventCreateWithFlags(&comm_ev_, cudaEventDisableTiming), "event");
   CudaCheck(cudaEventCreateWithFlags(&layer_ev_, cudaEventDisableTiming), "event");
   CudaCheck(cudaEventCreateWithFlags(&window_ev_, cudaEventDisableTiming), "event");
@@ -240,7 +243,7 @@ ss_cache::ss_cache(const ss_config& cfg)
   CudaCheck(cudaMemsetAsync(d_win_layer_rows_, 0, sizeof(uint32_t) * kMaxWindows * L_, stream_),
             "memset");
   CudaCheck(cudaMemsetAsync(d_status_, 0, sizeof(uint32_t), stream_), "memset");
-  CountLaunches(7);
+  CountLaunches(0);  // memsets only: kernels are what the launch counter counts
   for (int32_t i = kMaxWindows - 1; i >= 0; --i) free_window_ids_.push_back(i);
   for (int32_t i = kMaxSeqRows - 1; i >= 0; --i) free_fold_rows_.push_back(i);
   Sync();
@@ -303,7 +306,7 @@ ss_cache::~ss_cache() {
   }
   cudaEventDestroy(internal_ev_);
   cudaEventDestroy(window_ev_);
-  cudaEventDestroy(user_ev_);
+  for (auto& [st, u] : user_streams_) cudaEventDestroy(u.ev);
   cudaStreamSynchronize(comm_stream_);
   cudaEventDestroy(comm_ev_);
   cudaEventDestroy(layer_ev_);
@@ -372,9 +375,11 @@ void ss_cache::D2H(void* dst, const void* src, size_t bytes, cudaStream_t s, con
 // resets) and caller streams (async data path).  Event records and waits
 // are skipped when nothing new was enqueued on the other side.
 void ss_cache::OrderAfterUser() {
-  if (user_pending_ && user_gen_ != user_waited_gen_) {
-    CudaCheck(cudaStreamWaitEvent(stream_, user_ev_, 0), "cudaStreamWaitEvent");
-    user_waited_gen_ = user_gen_;
+  for (auto& [st, u] : user_streams_) {
+    if (u.gen != u.waited) {
+      CudaCheck(cudaStreamWaitEvent(stream_, u.ev, 0), "cudaStreamWaitEvent");
+      u.waited = u.gen;
+    }
   }
   if (comm_pending_ && comm_gen_ != comm_waited_gen_) {
     CudaCheck(cudaStreamWaitEvent(stream_, comm_ev_, 0), "cudaStreamWaitEvent");
@@ -428,9 +433,16 @@ void ss_cache::CountLaunches(int64_t n) {
 }
 
 void ss_cache::NoteUser(cudaStream_t s) {
-  CudaCheck(cudaEventRecord(user_ev_, s), "cudaEventRecord");
-  user_pending_ = true;
-  ++user_gen_;
+  UserStream& u = user_streams_[s];
+  if (u.ev == nullptr) CudaCheck(cudaEventCreateWithFlags(&u.ev, cudaEventDisableTiming), "event");
+  CudaCheck(cudaEventRecord(u.ev, s), "cudaEventRecord");
+  ++u.gen;
+}
+
+void ss_cache::SyncUserStreams() {
+  for (auto& [st, u] : user_streams_) {
+    if (u.gen != 0) CudaCheck(cudaEventSynchronize(u.ev), "cudaEventSynchronize");
+  }
 }
 
 DevBlock ss_cache::DevAlloc(size_t bytes, cudaStream_t s) {
@@ -513,13 +525,16 @@ void ss_cache::CheckFilled(const Record* rec, int64_t begin, int64_t end, int32_
   OrderAfterUser();
   const int64_t n = static_cast<int64_t>(unproven.size());
   DevBlock b = DevAlloc(sizeof(int32_t) * n, stream_);
-  CudaCheck(cudaMemsetAsync(d_status_, 0, sizeof(uint32_t), stream_), "memset");
+  // A scratch status word of its own: the sticky d_status_ bits of earlier
+  // rejected async sends / timed-out waits must survive until Synchronize.
+  uint32_t* d_check = reinterpret_cast<uint32_t*>(d_scratch_ + 1);
+  CudaCheck(cudaMemsetAsync(d_check, 0, sizeof(uint32_t), stream_), "memset");
   H2D(b.ptr, unproven.data(), sizeof(int32_t) * n, stream_, "H2D slots");
   launch_check_filled(d_fill_ + static_cast<int64_t>(layer) * num_pages_ * P_,
-                      static_cast<int32_t*>(b.ptr), n, d_status_, stream_, num_sms_);
-  CountLaunches(2);
+                      static_cast<int32_t*>(b.ptr), n, d_check, stream_, num_sms_);
+  CountLaunches(1);
   uint32_t st = 0;
-  D2H(&st, d_status_, sizeof(uint32_t), stream_, "D2H status");
+  D2H(&st, d_check, sizeof(uint32_t), stream_, "D2H status");
   DevFree(b, stream_);
   Sync();
   MKV_CHECK((st & kStatusMissingKV) == 0, kMissingKV, what);
@@ -577,14 +592,16 @@ Record* ss_cache::CreateSequence(SeqId seq, std::vector<Token> tokens) {
   rec->tokens = std::move(tokens);
   rec->prefix_digest = InitialPrefixDigest();
   if (device_ >= 0) {
-    MKV_ICHECK(!free_fold_rows_.empty(), "too many live sequences");
+    // Retryable like OutOfPages: eviction of finished sequences frees rows.
+    MKV_CHECK(!free_fold_rows_.empty(), kOutOfPages,
+              "all " + std::to_string(kMaxSeqRows) + " sequence rows in use");
     rec->fold_row = free_fold_rows_.back();
     free_fold_rows_.pop_back();
     OrderAfterUser();
     CudaCheck(cudaMemsetAsync(d_fold_sums_ + static_cast<int64_t>(rec->fold_row) * L_, 0,
                               sizeof(uint64_t) * L_, stream_),
               "memset fold sums");
-    CountLaunches(1);
+    CountLaunches(0);
   }
   Record* out = rec.get();
   {
@@ -673,6 +690,15 @@ int64_t ss_cache::PrepRecv(SeqId seq, std::vector<Token> tokens, int64_t end, KV
   MKV_CHECK(pages_needed <= static_cast<int64_t>(free_pages_.size()), kOutOfPages,
             std::to_string(pages_needed) + " pages needed, " +
                 std::to_string(free_pages_.size()) + " free");
+  // Device rows a new receive needs, checked before any state change like
+  // the pages (a window per open receive, recycled once it completes and is
+  // drained; a fold-sum row per live sequence).
+  if (device_ >= 0) {
+    MKV_CHECK(e == m || !free_window_ids_.empty(), kOutOfPages,
+              "all " + std::to_string(kMaxWindows) + " receive windows are open");
+    MKV_CHECK(!free_fold_rows_.empty(), kOutOfPages,
+              "all " + std::to_string(kMaxSeqRows) + " sequence rows in use");
+  }
   if (pages_needed > ranges_cap) {
     ThrowStatus(SS_ERR_BUFFER_TOO_SMALL,
                 "address needs " + std::to_string(pages_needed) + " ranges");
@@ -701,7 +727,7 @@ int64_t ss_cache::PrepRecv(SeqId seq, std::vector<Token> tokens, int64_t end, KV
 // Synchronous, so a peer that receives the address sees a ready receiver.
 void ss_cache::OpenDeviceWindow(Record* rec, int64_t m, int64_t e) {
   if (e <= m) return;
-  MKV_ICHECK(!free_window_ids_.empty(), "too many open receive windows");
+  MKV_CHECK(!free_window_ids_.empty(), kOutOfPages, "all receive windows are open");
   const int32_t wid = free_window_ids_.back();
   free_window_ids_.pop_back();
   rec->window->dev_id = wid;
@@ -723,6 +749,29 @@ void ss_cache::OpenDeviceWindow(Record* rec, int64_t m, int64_t e) {
   } else {
     CudaCheck(cudaEventRecord(window_ev_, stream_), "cudaEventRecord window");
   }
+}
+
+// A completed and drained window gives its device row back: its pages stop
+// mapping to it first (a stale device-direct sender is then rejected, as a
+// write into a freed window, instead of counting into the row's next window).
+// The reset is on the internal stream, after every caller stream's queued
+// work (a receive wait still reading the row's counters).
+void ss_cache::CloseDeviceWindow(Record* rec) {
+  if (device_ < 0 || !rec->window || rec->window->dev_id < 0) return;
+  const int32_t wid = rec->window->dev_id;
+  const int64_t np = static_cast<int64_t>(rec->own_pages.size());
+  if (np > 0) {
+    OrderAfterUser();
+    DevBlock b = DevAlloc(sizeof(int64_t) * np, stream_);
+    H2D(b.ptr, rec->own_pages.data(), sizeof(int64_t) * np, stream_, "H2D window pages");
+    launch_close_window(d_page_window_, static_cast<int64_t*>(b.ptr), np, wid, stream_);
+    CountLaunches(1);
+    DevFree(b, stream_);
+    if (ipc_exported_) Sync();  // another process's sender validates against it
+  }
+  std::lock_guard<std::mutex> lock(recv_mu_);
+  free_window_ids_.push_back(wid);
+  rec->window->dev_id = -1;
 }
 
 // kv_cache.cc:231-243
@@ -820,6 +869,7 @@ void ss_cache::PlanToDevice(ss_plan* plan) {
   const int64_t ne = static_cast<int64_t>(plan->entries.size());
   struct SendLayout {
     size_t src, dst, rpage, rbegin, rcount, verdict, staging;
+    bool ok = true;
     std::vector<int32_t> dst_slots, rb, rc;
     std::vector<int64_t> rp;
   };
@@ -838,7 +888,26 @@ void ss_cache::PlanToDevice(ss_plan* plan) {
   for (size_t i = 0; i < plan->sends.size(); ++i) {
     const PlanSend& s = plan->sends[i];
     const int64_t n = s.end - s.begin;
-    ExpandAddr(s.dest_addr, &sl[i].dst_slots, &sl[i].rp, &sl[i].rb, &sl[i].rc);
+    // MarkSend keeps the reference's checks only (kv_cache.cc:231-243); a
+    // malformed destination (overlaps, slot counts not covering the rows)
+    // is rejected where the reference's receiver would reject its frame:
+    // the send's validation sees no ranges, marks the verdict failed and
+    // raises UnknownAddress, and the copy never reads a destination slot.
+    bool addr_ok = true;
+    try {
+      s.dest_addr.Validate();
+    } catch (const Error&) {
+      addr_ok = false;
+    }
+    if (addr_ok) ExpandAddr(s.dest_addr, &sl[i].dst_slots, &sl[i].rp, &sl[i].rb, &sl[i].rc);
+    if (static_cast<int64_t>(sl[i].dst_slots.size()) != n) {
+      addr_ok = false;
+      sl[i].dst_slots.clear();
+      sl[i].rp.clear();
+      sl[i].rb.clear();
+      sl[i].rc.clear();
+    }
+    sl[i].ok = addr_ok;
     const int64_t nr = static_cast<int64_t>(sl[i].rp.size());
     sl[i].src = take(sizeof(int32_t) * n);
     sl[i].dst = take(sizeof(int32_t) * sl[i].dst_slots.size());
@@ -907,6 +976,7 @@ void ss_cache::PlanToDevice(ss_plan* plan) {
     d.range_count = reinterpret_cast<int32_t*>(base + sl[i].rcount);
     d.verdict = reinterpret_cast<int32_t*>(base + sl[i].verdict);
     d.staging = sl[i].staging == SIZE_MAX ? nullptr : reinterpret_cast<uint64_t*>(base + sl[i].staging);
+    d.n_ranges = static_cast<int64_t>(sl[i].rp.size());  // 0 when the address is malformed
   }
   plan->on_device = true;
 }
@@ -914,7 +984,9 @@ void ss_cache::PlanToDevice(ss_plan* plan) {
 void ss_cache::FreePlanDevice(ss_plan* plan) {
   if (plan->dev.ptr) {
     cudaStreamSynchronize(comm_stream_);
-    if (user_pending_) cudaEventSynchronize(user_ev_);
+    for (auto& [st, u] : user_streams_) {
+      if (u.gen != 0) cudaEventSynchronize(u.ev);
+    }
     cudaStreamSynchronize(stream_);
     cudaFree(plan->dev.ptr);
     plan->dev = DevBlock{};
@@ -991,7 +1063,7 @@ void ss_cache::LaunchRemote(const PeerTarget& peer, const int32_t* d_src_slots,
   c.win_layers = peer.L;
   c.verdict = d_verdict;
   c.status = d_status_;
-  c.sys_scope = peer.device != device_ ? 1 : 0;
+  c.sys_scope = (peer.device != device_ || force_sys_scope_) ? 1 : 0;
   c.pdl = after == nullptr ? 1 : 0;  // overlaps the copy grid's launch with the validation
   c.gen = v.gen;
   launch_copy_rows(c, s, num_sms_);
@@ -1041,8 +1113,8 @@ void ss_cache::AttentionAsync(ss_plan* plan, int32_t layer, const uint64_t* hin,
       const PlanSend& snd = plan->sends[i];
       const auto& d = plan->dsend[i];
       LaunchRemote(PeerFor(snd.dest), d.src_slots, d.dst_slots, d.range_page, d.range_begin,
-                   d.range_count, static_cast<int64_t>(snd.dest_addr.ranges.size()), d.verdict,
-                   snd.end - snd.begin, layer, layer + 1, comm_stream_);
+                   d.range_count, d.n_ranges, d.verdict, snd.end - snd.begin, layer, layer + 1,
+                   comm_stream_);
     }
     CudaCheck(cudaEventRecord(comm_ev_, comm_stream_), "cudaEventRecord");
     comm_pending_ = true;
@@ -1096,8 +1168,7 @@ void ss_cache::Attention(ss_plan* plan, int32_t layer, const uint64_t* hidden_in
     auto pit = peers_.find(snd.dest);
     if (pit != peers_.end()) {
       LaunchRemote(pit->second, d.src_slots, d.dst_slots, d.range_page, d.range_begin,
-                   d.range_count, static_cast<int64_t>(snd.dest_addr.ranges.size()), d.verdict,
-                   rows, layer, layer + 1, stream_);
+                   d.range_count, d.n_ranges, d.verdict, rows, layer, layer + 1, stream_);
       continue;
     }
     if (!sink) continue;
@@ -1350,6 +1421,7 @@ std::vector<SeqId> ss_cache::DrainReceiveCompletions() {
     AdvanceCommitted(rec);
     rec->finished = true;
     CommitToTree(seq);
+    CloseDeviceWindow(rec);
   }
   return done;
 }
@@ -1368,6 +1440,10 @@ ss_plan* ss_cache::BeginDirectSend(SeqId seq, int64_t begin, int64_t end, Rank d
             "destination covers " + std::to_string(addr.token_count) + " tokens, range has " +
                 std::to_string(end - begin));
   MKV_CHECK(addr.token_begin == begin, kAddrMismatch, "destination token_begin mismatch");
+  // The address may come from another process (decoded, not built here):
+  // the same checks as the reference's frame decode (kv_addr.cc:16-30), so
+  // the expanded slot list has exactly one destination slot per row.
+  addr.Validate();
   PeerFor(dest);
   MKV_ICHECK(end <= rec->alloc_len, "position not allocated");
   auto plan = std::make_unique<ss_plan>();
@@ -1384,6 +1460,8 @@ ss_plan* ss_cache::BeginDirectSend(SeqId seq, int64_t begin, int64_t end, Rank d
   std::vector<int64_t> rp;
   std::vector<int32_t> rb, rc;
   ExpandAddr(addr, &dst, &rp, &rb, &rc);
+  MKV_CHECK(static_cast<int64_t>(dst.size()) == end - begin, kAddrMismatch,
+            "destination slots do not cover the send range");
   const int64_t nr = static_cast<int64_t>(rp.size());
   const size_t o_dst = 0;
   const size_t o_rp = o_dst + Align(sizeof(int32_t) * dst.size());
@@ -1412,6 +1490,7 @@ ss_plan* ss_cache::BeginDirectSend(SeqId seq, int64_t begin, int64_t end, Rank d
   d.range_begin = reinterpret_cast<int32_t*>(base + o_rb);
   d.range_count = reinterpret_cast<int32_t*>(base + o_rc);
   d.verdict = reinterpret_cast<int32_t*>(base + o_v);
+  d.n_ranges = nr;
   plan->on_device = true;
   plan->is_direct_send = true;
   CudaCheck(cudaEventRecord(internal_ev_, stream_), "cudaEventRecord");
@@ -1445,8 +1524,7 @@ void ss_cache::LaunchDirectSend(ss_plan* plan, int32_t lb, int32_t le, cudaStrea
   OrderLaunch(s);
   const auto& d = plan->dsend[0];
   LaunchRemote(peer, rec->d_slots + snd.begin, d.dst_slots, d.range_page, d.range_begin,
-               d.range_count, static_cast<int64_t>(snd.dest_addr.ranges.size()), d.verdict,
-               snd.end - snd.begin, lb, le, s, after);
+               d.range_count, d.n_ranges, d.verdict, snd.end - snd.begin, lb, le, s, after);
   if (s != stream_) NoteUser(s);
 }
 
@@ -1467,6 +1545,7 @@ void ss_cache::BroadcastSend(SeqId seq, int64_t begin, int64_t end, int32_t n_de
               "destination covers " + std::to_string(addrs[d].token_count) +
                   " tokens, range has " + std::to_string(end - begin));
     MKV_CHECK(addrs[d].token_begin == begin, kAddrMismatch, "destination token_begin mismatch");
+    addrs[d].Validate();  // one destination slot per row (kv_addr.cc:16-30)
     PeerFor(dests[d]);
   }
   if (W_ != 512 && W_ != 128) {  // the fan-out kernel is specialised for these rows
@@ -1496,6 +1575,8 @@ void ss_cache::BroadcastSend(SeqId seq, int64_t begin, int64_t end, int32_t n_de
   };
   for (int32_t d = 0; d < n_dest; ++d) {
     ExpandAddr(addrs[d], &lay[d].slots, &lay[d].rp_, &lay[d].rb_, &lay[d].rc_);
+    MKV_CHECK(static_cast<int64_t>(lay[d].slots.size()) == n, kAddrMismatch,
+              "destination slots do not cover the send range");
     const size_t nr = lay[d].rp_.size();
     lay[d].dst = take(sizeof(int32_t) * lay[d].slots.size());
     lay[d].rp = take(sizeof(int64_t) * nr);
@@ -1551,7 +1632,7 @@ void ss_cache::BroadcastSend(SeqId seq, int64_t begin, int64_t end, int32_t n_de
     f.win_layer_rows[d] = peer.win_layer_rows;
     f.win_layers[d] = peer.L;
     f.verdict[d] = v.verdict;
-    if (peer.device != device_) f.sys_scope = 1;
+    if (peer.device != device_ || force_sys_scope_) f.sys_scope = 1;
   }
   launch_copy_rows_fanout(f, s, num_sms_);
   CountLaunches(1 + n_dest);
@@ -1822,7 +1903,7 @@ void ss_cache::DetachPeer(Rank dest) {
 void ss_cache::Synchronize() {
   if (device_ < 0) return;
   Sync();
-  if (user_pending_) CudaCheck(cudaEventSynchronize(user_ev_), "cudaEventSynchronize");
+  SyncUserStreams();
   CudaCheck(cudaStreamSynchronize(comm_stream_), "cudaStreamSynchronize");
   uint32_t st = 0;
   CudaCheck(cudaMemcpy(&st, d_status_, sizeof(uint32_t), cudaMemcpyDeviceToHost), "D2H status");
@@ -1839,8 +1920,11 @@ void ss_cache::Synchronize() {
 void ss_cache::WaitReceive(SeqId seq, int64_t timeout_ms, cudaStream_t s) {
   RequireDevice("WaitReceive");
   Record* rec = MustGet(seq);
-  MKV_CHECK(rec->window.has_value() && rec->window->dev_id >= 0, kInvalidArgument,
+  MKV_CHECK(rec->window.has_value(), kInvalidArgument,
             "sequence " + std::to_string(seq) + " has no receive window");
+  if (rec->window->complete && rec->window->dev_id < 0) return;  // drained: every row landed
+  MKV_CHECK(rec->window->dev_id >= 0, kInvalidArgument,
+            "sequence " + std::to_string(seq) + " has no device receive window");
   const Window& w = *rec->window;
   const int64_t target = std::max<int64_t>(0, w.expected - w.received);
   OrderLaunch(s);
@@ -1854,8 +1938,11 @@ void ss_cache::WaitReceiveLayer(SeqId seq, int32_t layer, int64_t timeout_ms, cu
   RequireDevice("WaitReceive");
   MKV_CHECK(layer >= 0 && layer < L_, kInvalidArgument, "layer out of range");
   Record* rec = MustGet(seq);
-  MKV_CHECK(rec->window.has_value() && rec->window->dev_id >= 0, kInvalidArgument,
+  MKV_CHECK(rec->window.has_value(), kInvalidArgument,
             "sequence " + std::to_string(seq) + " has no receive window");
+  if (rec->window->complete && rec->window->dev_id < 0) return;  // drained: every row landed
+  MKV_CHECK(rec->window->dev_id >= 0, kInvalidArgument,
+            "sequence " + std::to_string(seq) + " has no device receive window");
   const Window& w = *rec->window;
   int64_t host_rows = 0;
   {

@@ -179,6 +179,7 @@ struct ss_plan {
     int32_t* range_count = nullptr;
     int32_t* verdict = nullptr;
     uint64_t* staging = nullptr;  // gathered payload for host sinks
+    int64_t n_ranges = 0;         // destination ranges validated (0: malformed address)
   };
   std::vector<DevSend> dsend;
   bool is_direct_send = false;
@@ -296,6 +297,11 @@ struct ss_cache {
   void ExportIpc(ss_ipc_handle* out);
   void ImportIpc(Rank dest, const ss_ipc_handle* h);
   void DetachPeer(Rank dest);
+  void PeerInfo(Rank dest, int32_t* sys_scope, int32_t* peer_device) const {
+    const mkv::PeerTarget& t = PeerFor(dest);
+    if (sys_scope) *sys_scope = (t.device != device_ || force_sys_scope_) ? 1 : 0;
+    if (peer_device) *peer_device = t.device;
+  }
   ss_plan* BeginDecode(const int64_t* seqs, const int64_t* ctx_lens, int64_t batch);
   void PrefillAttention(int64_t seq, int64_t q_begin, int64_t q_end, int32_t layer, int32_t hq,
                         int32_t hkv, int32_t hd, float scale, const void* q, void* out,
@@ -366,6 +372,7 @@ struct ss_cache {
   void BeginInternal();              // internal work that needs no wait for user streams
   int32_t NextLaunchGen();
   void NoteUser(cudaStream_t s);
+  void SyncUserStreams();            // host waits for every caller stream's noted work
   void OrderLaunch(cudaStream_t s);  // user-stream launch: s after internal work
   mkv::DevBlock DevAlloc(size_t bytes, cudaStream_t s);
   void DevFree(mkv::DevBlock& b, cudaStream_t s);
@@ -385,6 +392,7 @@ struct ss_cache {
   void ExpandAddr(const mkv::KVAddr& a, std::vector<int32_t>* slots, std::vector<int64_t>* rp,
                   std::vector<int32_t>* rb, std::vector<int32_t>* rc) const;
   void OpenDeviceWindow(mkv::Record* rec, int64_t m, int64_t e);
+  void CloseDeviceWindow(mkv::Record* rec);
   void SyncDeviceTable(mkv::Record* rec, int64_t old_len);
   void PollDeviceWindows();
   void ThrowIfDeviceStatus();
@@ -405,6 +413,7 @@ struct ss_cache {
   int device_;
   int32_t rank_;
   int num_sms_ = 148;
+  bool force_sys_scope_ = false;  // MICROKV_FORCE_SYS_SCOPE=1 (test hook)
   std::atomic<int64_t> launches_{0};
   std::atomic<int32_t> launch_gen_{0};  // validated-launch generations (NextLaunchGen)
 
@@ -427,7 +436,16 @@ struct ss_cache {
   // HBM state.
   cudaStream_t stream_ = nullptr;
   cudaStream_t comm_stream_ = nullptr;  // per-layer sends (overlap with compute)
-  cudaEvent_t internal_ev_ = nullptr, user_ev_ = nullptr, comm_ev_ = nullptr, layer_ev_ = nullptr;
+  cudaEvent_t internal_ev_ = nullptr, comm_ev_ = nullptr, layer_ev_ = nullptr;
+  // One event per caller stream that async work was enqueued on: internal
+  // work (uploads, frees, resets), plan frees and Synchronize are ordered
+  // after the latest work of EVERY such stream, not only the most recently
+  // used one (the microkv.h stream contract).
+  struct UserStream {
+    cudaEvent_t ev = nullptr;
+    uint64_t gen = 0, waited = 0;
+  };
+  std::map<cudaStream_t, UserStream> user_streams_;
   // Recorded after each receive window opens on the device; in-process
   // senders wait on it instead of PrepRecv synchronizing the host.  Once the
   // receive surface is exported to another process PrepRecv synchronizes.
@@ -450,8 +468,8 @@ struct ss_cache {
   bool stage_used_[kStageSlots] = {};
   int stage_next_ = 0;
   std::mutex stage_mu_;
-  bool user_pending_ = false, comm_pending_ = false;
-  uint64_t user_gen_ = 0, user_waited_gen_ = 0, comm_gen_ = 0, comm_waited_gen_ = 0;
+  bool comm_pending_ = false;
+  uint64_t comm_gen_ = 0, comm_waited_gen_ = 0;
   uint64_t internal_gen_ = 1, internal_recorded_gen_ = 0;
   std::map<cudaStream_t, uint64_t> user_stream_seen_;
   std::atomic<int64_t> h2d_bytes_{0}, d2h_bytes_{0};

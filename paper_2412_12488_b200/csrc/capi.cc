@@ -406,6 +406,13 @@ int ss_import_ipc(ss_cache* c, int32_t dest, const ss_ipc_handle* h) {
   });
 }
 
+int ss_peer_info(const ss_cache* c, int32_t dest, int32_t* sys_scope, int32_t* peer_device) {
+  return Guard(const_cast<ss_cache*>(c), [&]() -> int {
+    c->PeerInfo(dest, sys_scope, peer_device);
+    return SS_OK;
+  });
+}
+
 int ss_detach_peer(ss_cache* c, int32_t dest) {
   return Guard(c, [&]() -> int {
     c->DetachPeer(dest);

@@ -211,7 +211,12 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
                     s_rows[i], p.sys_scope != 0);
       }
     }
+    // The window total last: once a receiver's drain sees the window
+    // complete, no per-layer counter update of it is still in flight (the
+    // window row is recycled after the drain).
+    __syncthreads();
     if (threadIdx.x == 0) {
+      fence_publish(p.sys_scope != 0);
       unsigned long long total = 0;
       for (int i = 0; i < p.n_layers; ++i) total += s_rows[i];
       if (total != 0) red_sys_add(p.win_received + window, total, p.sys_scope != 0);
@@ -305,7 +310,9 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows_fanout(FanoutParams 
                     c, p.sys_scope != 0);
       }
     }
+    __syncthreads();  // the window total after its layer counters (see k_copy_rows)
     if (threadIdx.x == 0) {
+      fence_publish(p.sys_scope != 0);
       unsigned long long total = 0;
       for (int i = 0; i < p.n_layers; ++i) total += s_rows[d * p.n_layers + i];
       if (total != 0) red_sys_add(p.win_received[d] + window[d], total, p.sys_scope != 0);
@@ -491,6 +498,16 @@ __global__ void k_open_window(uint8_t* expecting, const int32_t* __restrict__ sl
   if (window >= 0) {
     for (int64_t i = t0; i < L; i += stride) win_layer_rows[static_cast<int64_t>(window) * L + i] = 0;
     if (t0 == 0) win_received[window] = 0;
+  }
+}
+
+__global__ void k_close_window(int32_t* page_window, const int64_t* __restrict__ pages,
+                               int64_t n_pages, int32_t window) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n_pages;
+       i += stride) {
+    const int64_t pg = pages[i];
+    if (page_window[pg] == window) page_window[pg] = -1;
   }
 }
 
@@ -686,6 +703,14 @@ void launch_open_window(uint8_t* expecting, const int32_t* slots, int64_t n_slot
                                      win_received, win_layer_rows, L);
 }
 
+void launch_close_window(int32_t* page_window, const int64_t* pages, int64_t n_pages,
+                         int32_t window, cudaStream_t s) {
+  if (n_pages <= 0) return;
+  int grid = static_cast<int>((n_pages + 255) / 256);
+  if (grid > 1024) grid = 1024;
+  k_close_window<<<grid, 256, 0, s>>>(page_window, pages, n_pages, window);
+}
+
 void launch_first_nonfull(const uint8_t* fill, int64_t fill_layer_bytes, int32_t L,
                           const int32_t* slots, int64_t n, unsigned long long* out,
                           cudaStream_t s, int num_sms) {
@@ -740,6 +765,7 @@ void preload_kernels() {
   cudaFuncGetAttributes(&a, k_fold_scan);
   cudaFuncGetAttributes(&a, k_reset_pages);
   cudaFuncGetAttributes(&a, k_open_window);
+  cudaFuncGetAttributes(&a, k_close_window);
   cudaFuncGetAttributes(&a, k_first_nonfull);
   cudaFuncGetAttributes(&a, k_gather_tables);
   cudaFuncGetAttributes(&a, k_check_filled);

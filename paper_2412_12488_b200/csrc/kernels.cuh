@@ -152,6 +152,11 @@ void launch_open_window(uint8_t* expecting, const int32_t* slots, int64_t n_slot
                         int32_t window, unsigned long long* win_received,
                         uint32_t* win_layer_rows, int32_t L, cudaStream_t s);
 
+// A drained receive window's pages stop mapping to it (page_window = -1
+// where it still equals `window`).
+void launch_close_window(int32_t* page_window, const int64_t* pages, int64_t n_pages,
+                         int32_t window, cudaStream_t s);
+
 // First position in [0, n) whose slot has an Empty fill on any layer (n if none).
 void launch_first_nonfull(const uint8_t* fill, int64_t fill_layer_bytes, int32_t L,
                           const int32_t* slots, int64_t n, unsigned long long* out,

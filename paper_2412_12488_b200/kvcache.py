@@ -205,6 +205,7 @@ _SIGNATURES = {
     "ss_export_ipc": (C.c_int, [_vp, C.POINTER(IpcHandle)]),
     "ss_import_ipc": (C.c_int, [_vp, C.c_int32, C.POINTER(IpcHandle)]),
     "ss_detach_peer": (C.c_int, [_vp, C.c_int32]),
+    "ss_peer_info": (C.c_int, [_vp, C.c_int32, _i32p, _i32p]),
     "ss_attention_async": (C.c_int, [_vp, _vp, C.c_int32, _vp, _vp, _vp]),
     "ss_direct_send_async": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, C.c_int32,
                                        C.POINTER(_Addr), C.c_uint64, C.c_int32, C.c_int32, _vp]),
@@ -855,6 +856,12 @@ class KVCache:
         h = IpcHandle()
         C.memmove(h.bytes, handle, len(handle))
         self._check(self._lib.ss_import_ipc(self._h, dest, C.byref(h)))
+
+    def peer_info(self, dest: int) -> dict:
+        """{'sys_scope': bool, 'peer_device': int} of sends to `dest`."""
+        sc, dv = C.c_int32(), C.c_int32()
+        self._check(self._lib.ss_peer_info(self._h, dest, C.byref(sc), C.byref(dv)))
+        return {"sys_scope": bool(sc.value), "peer_device": dv.value}
 
     def detach_peer(self, dest: int) -> None:
         self._check(self._lib.ss_detach_peer(self._h, dest))

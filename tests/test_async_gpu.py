@@ -102,8 +102,10 @@ def test_direct_send_layer_by_layer(cuda):
 
 def test_direct_send_after_producer_event(cuda):
     """ss_launch_direct_send_after_async: validation first, copy after the
-    producing layer's event (here behind a sleep kernel on the compute
-    stream, so the copy must wait for it); bit-exact like the plain launch."""
+    producing layer's event.  The producer stream writes layer l's rows
+    (append behind a sleep kernel, so they land well after the send was
+    enqueued); the receiver must hold exactly those rows, which it cannot if
+    the copy ignored the event (the slots would still be Empty/zero)."""
     torch = cuda
     L, W, n = 4, 512, 700
     p = _prompt(n, 44)
@@ -112,22 +114,31 @@ def test_direct_send_after_producer_event(cuda):
     P.attach_peer(1, D)
     P.CreateSequence(1, p)
     P.EnsureAllocated(1, n)
-    prefill(P, 1, p, 0, n)
+    fplan = P.BeginForward([BatchEntry(1, (0, n))])  # live plan: the producer of [0, n)
+    rows = [torch.randint(-2**62, 2**62, (n, W), dtype=torch.int64, device="cuda")
+            for _ in range(L)]
     r = D.PrepRecv(7, p, -1)
     plan = P.begin_direct_send(1, (0, n - 1), 1, r.addr, 1)
+    torch.cuda.synchronize()
     cs, ms = torch.cuda.Stream(), torch.cuda.Stream()
     evs = [torch.cuda.Event() for _ in range(L)]
     for layer in range(L):
         with torch.cuda.stream(cs):
-            torch.cuda._sleep(2_000_000)
+            torch.cuda._sleep(5_000_000)
+        P.append_rows_async(fplan, layer, rows[layer].data_ptr(), cs.cuda_stream)
         evs[layer].record(cs)
         P.launch_direct_send_after_async(plan, (layer, layer + 1), evs[layer].cuda_event,
                                          ms.cuda_stream)
     torch.cuda.synchronize()
+    P.synchronize()
     assert D.DrainReceiveCompletions() == [7]
     for layer in range(L):
-        assert np.array_equal(P.GatherRange(1, (0, n - 1), layer), D.GatherRange(7, (0, n - 1), layer))
+        got = torch.empty((n - 1) * W, dtype=torch.int64, device="cuda")
+        D.gather_range_async(7, (0, n - 1), layer, got.data_ptr(), 0)
+        torch.cuda.synchronize()
+        assert torch.equal(got.view(n - 1, W), rows[layer][:n - 1]), layer
     plan.close()
+    fplan.close()
 
 
 def test_append_rows_then_gather_roundtrip(cuda):
