@@ -480,7 +480,35 @@ def our_arm(args, rank: int, world: int) -> None:
                                    "wait_and_drain", "close_and_free"])},
         "secondary": secondary,
     }
+    # The handoff half of the metric, top level (70B and 8B, kernel mover on
+    # the whole machine; every mover's numbers are under secondary.handoff*).
+    for key, sub in (("handoff", ""), ("handoff_8b", "_8b")):
+        h = secondary.get(key, {}) if isinstance(secondary, dict) else {}
+        line[f"handoff{sub}_tail_us"] = h.get("exposed_tail_us")
+        line[f"handoff{sub}_slowdown_pct"] = h.get("slowdown_pct")
+    line["send_budget"] = _pick_budget(secondary) if isinstance(secondary, dict) else None
     print(json.dumps(line), flush=True)
+
+
+def _pick_budget(secondary: dict):
+    """The smallest SM budget of the copy kernel whose 80-layer send alone
+    still moves >= 720 GB/s (80% of an NVLink 5 direction), with that arm's
+    median prefill slowdown at both shapes (secondary.handoff*)."""
+    sm = secondary.get("send_modes") or {}
+    best = None
+    for name, mode, ctas in SEND_ARMS:
+        v = (sm.get(name) or {}).get("80_layers", {}).get("payload_gbs")
+        if mode == 0 and ctas > 0 and v is not None and v >= 720.0:
+            if best is None or ctas < best[0]:
+                best = (ctas, name, v)
+    if best is None:
+        return None
+    out = {"arm": best[1], "max_ctas": best[0], "payload_gbs_80_layers": best[2]}
+    for key, tag in (("handoff", "70b"), ("handoff_8b", "8b")):
+        a = ((secondary.get(key) or {}).get("arms") or {}).get(best[1], {})
+        out[f"prefill_slowdown_pct_{tag}"] = a.get("slowdown_pct_median")
+        out[f"exposed_tail_us_{tag}"] = a.get("exposed_tail_us_median")
+    return out
 
 
 def _pair_spot_check(P, D, prompt, e, peer_rank, torch, dist) -> None:
@@ -537,9 +565,13 @@ def secondary_measurements(P, D, prompt, torch) -> dict:
     except Exception as ex:
         out["handoff"] = {"error": str(ex)}
     try:  # config 2 (Llama-3.1-8B: 32 layers, 4K prompt; ~1.8 TFLOP per layer)
-        out["handoff_8b"] = measure_handoff_gemm(torch, 32, 4096, 4096, 53248, "8B")
+        out["handoff_8b"] = measure_handoff_gemm(torch, 32, 4096, 4096, 53248, "8B", reps=9)
     except Exception as ex:
         out["handoff_8b"] = {"error": str(ex)}
+    try:
+        out["send_modes"] = measure_send_modes(torch)
+    except Exception as ex:
+        out["send_modes"] = {"error": str(ex)}
     try:
         out["handoff_toy_prefill"] = measure_handoff(torch)
     except Exception as ex:
@@ -580,16 +612,28 @@ def secondary_measurements(P, D, prompt, torch) -> dict:
     return out
 
 
+SEND_ARMS = (("kernel_full", 0, 0), ("kernel_64ctas", 0, 64), ("kernel_32ctas", 0, 32),
+             ("kernel_16ctas", 0, 16), ("copy_engine", 1, 0))
+
+
 def measure_handoff_gemm(torch, layers: int = L, n_prompt: int = PROMPT, k: int = 8192,
-                         n: int = 104448, label: str = "70B", after: bool = True) -> dict:
-    """1P1D PrefillThenSend at the 70B shape with a compute-bound prefill
-    stand-in: per layer one bf16 GEMM of a Llama-3.1-70B layer's FLOPs at
-    8,191 tokens (X[8191, 8192] @ W[8192, 104448], ~14 TFLOP), then the
-    layer's K||V rows are appended to P's pages and that layer is sent to D's
-    reserved pages on the communication stream (overlapping the next layer's
-    GEMM).  Reports P's prefill time with vs without sends
-    and the exposed tail: P's last-layer compute end -> D's device-side wait
-    sees every row of every layer."""
+                         n: int = 104448, label: str = "70B", reps: int = 5) -> dict:
+    """1P1D PrefillThenSend with a compute-bound prefill stand-in: per layer
+    one bf16 GEMM of a Llama layer's FLOPs at the prompt length (70B:
+    X[8191, 8192] @ W[8192, 104448], ~14 TFLOP), then the layer's K||V rows
+    are appended to P's pages and that layer is sent to D's reserved pages
+    on a second stream (validation first, the copy behind the layer's event:
+    ss_launch_direct_send_after_async), overlapping the next layer's GEMM
+    (PAPER.md:339-344).
+
+    Arms: no sends, and sends through each row mover of SEND_ARMS (the copy
+    kernel on the whole machine or an SM budget, the copy engines).  Each
+    rep runs every arm once in a rotated order (alternation: drift and
+    thermal state spread over all arms); per arm the median and range over
+    reps of P's prefill time, the slowdown against the no-send median, the
+    exposed tail (P's last-layer compute end -> the last layer's rows and
+    window counters landed in D) and the per-layer lag (layer l's event ->
+    its rows landed)."""
     from paper_2412_12488_b200 import BatchEntry, KVCache
 
     rng = np.random.Generator(np.random.MT19937(4))
@@ -603,58 +647,148 @@ def measure_handoff_gemm(torch, layers: int = L, n_prompt: int = PROMPT, k: int 
     Wt = torch.randn(k, n, device="cuda", dtype=torch.bfloat16) * 0.01
     Y = torch.empty(e, n, device="cuda", dtype=torch.bfloat16)
     rows = torch.randint(-2**62, 2**62, (e * W,), dtype=torch.int64, device="cuda")
-    cs, ms, ds = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
-    res, base = {}, None
-    for run, send in enumerate((False, True, False, True)):
-        seq = 10 + run
-        if send:
-            r = D.PrepRecv(seq, prompt, -1)
-        P.CreateSequence(seq, prompt)
-        P.EnsureAllocated(seq, e)
-        plan = P.BeginForward([BatchEntry(seq, (0, e))])
-        dplan = P.begin_direct_send(seq, (0, e), 1, r.addr, 7) if send else None
-        torch.cuda.synchronize()
-        t0, tc, td = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-        layer_done = [torch.cuda.Event() for _ in range(layers)]
-        t0.record(cs)
-        for layer in range(layers):
-            with torch.cuda.stream(cs):
-                torch.matmul(X, Wt, out=Y)
-            P.append_rows_async(plan, layer, rows.data_ptr(), cs.cuda_stream)
-            if send and after:
-                # validation now, the copy after this layer's writes
-                layer_done[layer].record(cs)
-                P.launch_direct_send_after_async(dplan, (layer, layer + 1),
-                                                 layer_done[layer].cuda_event, ms.cuda_stream)
-            elif send:
-                layer_done[layer].record(cs)
-                ms.wait_event(layer_done[layer])
-                P.launch_direct_send_async(dplan, (layer, layer + 1), ms.cuda_stream)
-        tc.record(cs)
-        if send:
-            ds.wait_event(t0)
-            D.wait_receive_async(seq, 60000, ds.cuda_stream)
-            td.record(ds)
-        torch.cuda.synchronize()
-        P.synchronize()
-        if send:
-            D.synchronize()
-            assert D.DrainReceiveCompletions() == [seq]
-            res = {"prefill_ms_with_sends": round(t0.elapsed_time(tc), 3),
-                   "exposed_tail_us": round(1e3 * max(0.0, tc.elapsed_time(td)), 1)}
-            D.FreeSequence(seq)
-            dplan.close()
-        else:
-            base = t0.elapsed_time(tc)
-        plan.close()
-        P.FreeSequence(seq)
-    res["prefill_ms_without_sends"] = round(base, 3)
-    res["slowdown_pct"] = round(100 * (res["prefill_ms_with_sends"] / base - 1), 2)
-    res["per_layer_payload_mb"] = round(e * BPT / 1e6, 2)
-    res["layers"], res["prompt_tokens"] = layers, n_prompt
+    # The send stream at high priority, like the engine's own comm stream: a
+    # layer's copy takes SMs as soon as compute CTAs retire.
+    cs, ms, ds = torch.cuda.Stream(), torch.cuda.Stream(priority=-1), torch.cuda.Stream()
+    arms = [("none", None, None)] + list(SEND_ARMS)
+    runs = {a[0]: {"prefill_ms": [], "tail_us": [], "layer_lag_us": []} for a in arms}
+    seq = 10
+    for rep in range(reps + 1):  # rep 0: warm-up of every arm, discarded
+        order = arms[rep % len(arms):] + arms[:rep % len(arms)]
+        for name, mode, ctas in order:
+            send = mode is not None
+            seq += 1
+            if send:
+                P.set_send_mode(mode, ctas)
+                r = D.PrepRecv(seq, prompt, -1)
+            P.CreateSequence(seq, prompt)
+            P.EnsureAllocated(seq, e)
+            plan = P.BeginForward([BatchEntry(seq, (0, e))])
+            dplan = P.begin_direct_send(seq, (0, e), 1, r.addr, 7) if send else None
+            torch.cuda.synchronize()
+            t0, tc = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+            done = [torch.cuda.Event(enable_timing=True) for _ in range(layers)]
+            landed = [torch.cuda.Event(enable_timing=True) for _ in range(layers)] if send else []
+            t0.record(cs)
+            for layer in range(layers):
+                with torch.cuda.stream(cs):
+                    torch.matmul(X, Wt, out=Y)
+                P.append_rows_async(plan, layer, rows.data_ptr(), cs.cuda_stream)
+                done[layer].record(cs)
+                if send:
+                    P.launch_direct_send_after_async(dplan, (layer, layer + 1),
+                                                     done[layer].cuda_event, ms.cuda_stream)
+                    landed[layer].record(ms)
+            tc.record(cs)
+            torch.cuda.synchronize()
+            P.synchronize()
+            if rep > 0:
+                runs[name]["prefill_ms"].append(t0.elapsed_time(tc))
+            if send:
+                # D's device-side wait runs after the timed region: on one GPU
+                # a spinning wait kernel would hold an SM slot of P's prefill
+                # (on two GPUs it runs on D's).  The last layer's copy ends
+                # when its rows and window counters have landed (device-local
+                # peer), so the tail is P's compute end -> that copy's end;
+                # the wait then confirms every row of every layer arrived.
+                D.wait_receive_async(seq, 60000, ds.cuda_stream)
+                ds.synchronize()
+                D.synchronize()
+                assert D.DrainReceiveCompletions() == [seq]
+                if rep > 0:
+                    runs[name]["tail_us"].append(1e3 * max(0.0, tc.elapsed_time(landed[-1])))
+                    runs[name]["layer_lag_us"].append(
+                        float(np.median([1e3 * done[i].elapsed_time(landed[i])
+                                         for i in range(layers)])))
+                D.FreeSequence(seq)
+                dplan.close()
+            plan.close()
+            P.FreeSequence(seq)
+    P.set_send_mode(0, 0)
+    per_layer = e * BPT
+    base = float(np.median(runs["none"]["prefill_ms"]))
+    res = {"layers": layers, "prompt_tokens": n_prompt, "reps": reps,
+           "per_layer_payload_mb": round(per_layer / 1e6, 2),
+           "prefill_ms_without_sends": round(base, 3),
+           "prefill_ms_without_sends_range": [round(min(runs["none"]["prefill_ms"]), 3),
+                                              round(max(runs["none"]["prefill_ms"]), 3)],
+           "arms": {}}
+    for name, mode, ctas in SEND_ARMS:
+        rr = runs[name]
+        med = float(np.median(rr["prefill_ms"]))
+        lh = float(np.median(rr["layer_lag_us"]))
+        res["arms"][name] = {
+            "prefill_ms_median": round(med, 3),
+            "prefill_ms_range": [round(min(rr["prefill_ms"]), 3), round(max(rr["prefill_ms"]), 3)],
+            "slowdown_pct_median": round(100 * (med / base - 1), 3),
+            "slowdown_pct_per_rep": [round(100 * (x / base - 1), 3) for x in rr["prefill_ms"]],
+            "exposed_tail_us_median": round(float(np.median(rr["tail_us"])), 1),
+            "exposed_tail_us_range": [round(min(rr["tail_us"]), 1), round(max(rr["tail_us"]), 1)],
+            # layer l's event on the compute stream -> its rows landed (the
+            # send stream's event after the copy): how far the transfer trails
+            # the layer that produced it
+            "layer_lag_us_median": round(lh, 1)}
+    d = res["arms"]["kernel_full"]
+    res["prefill_ms_with_sends"] = d["prefill_ms_median"]
+    res["slowdown_pct"] = d["slowdown_pct_median"]
+    res["exposed_tail_us"] = d["exposed_tail_us_median"]
     res["note"] = (f"{label}-layer-FLOP bf16 GEMM per layer (cuBLAS, compute stand-in) + KV append; "
-                   "per-layer DirectSend on a second stream; P and D on one GPU")
+                   "per-layer DirectSend on a second stream; P and D on one GPU; medians over "
+                   f"{reps} alternated reps per arm")
     del P, D, X, Wt, Y, rows
+    torch.cuda.empty_cache()
+    return res
+
+
+def measure_send_modes(torch) -> dict:
+    """Each row mover of SEND_ARMS alone on the GPU (no compute beside it):
+    one 70B layer (8,191 rows = 33.5 MB) and the whole 80-layer migration
+    (2.68 GB), device time (median of 9, launches queued behind a sleep) ->
+    payload GB/s and the fraction of the HBM copy peak (read + write)."""
+    from paper_2412_12488_b200 import KVCache
+
+    peak, _ = _peaks()
+    prompt = _prompt(8)
+    e = PROMPT - 1
+    pages = PROMPT // PAGE + 16
+    P = KVCache(num_pages=pages, page_size=PAGE, layers=L, dim=W, device=0, rank=0)
+    D = KVCache(num_pages=pages, page_size=PAGE, layers=L, dim=W, device=0, rank=1)
+    P.attach_peer(1, D)
+    _populate_prefix_l(P, 1, prompt, torch, L)
+    s = torch.cuda.Stream()
+    res = {}
+    seq = 500
+    for name, mode, ctas in SEND_ARMS:
+        P.set_send_mode(mode, ctas)
+        out = {}
+        for lay, tag in ((1, "one_layer"), (L, "80_layers")):
+            ts = []
+            for rep in range(10):
+                seq += 1
+                r = D.PrepRecv(seq, prompt, -1)
+                plan = P.begin_direct_send(1, (0, e), 1, r.addr, rep)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                if mode == 0:  # (copy engines: the host waits for the verdict inside the call)
+                    with torch.cuda.stream(s):
+                        torch.cuda._sleep(4_000_000)
+                e0.record(s)
+                P.launch_direct_send_async(plan, (0, lay), s.cuda_stream)
+                e1.record(s)
+                s.synchronize()
+                if rep > 0:
+                    ts.append(e0.elapsed_time(e1) / 1e3)
+                if lay == L:
+                    assert D.DrainReceiveCompletions() == [seq]
+                plan.close()
+                D.FreeSequence(seq)
+            t = float(np.median(ts))
+            pay = e * lay * BPT
+            out[tag] = {"device_us": round(1e6 * t, 1), "payload_gbs": round(pay / t / 1e9, 1),
+                        "hbm_frac": round(2 * pay / t / 1e9 / peak, 4),
+                        "range_us": [round(1e6 * min(ts), 1), round(1e6 * max(ts), 1)]}
+        res[name] = out
+    P.set_send_mode(0, 0)
+    del P, D
     torch.cuda.empty_cache()
     return res
 

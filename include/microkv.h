@@ -346,6 +346,26 @@ int ss_launch_direct_send_async(ss_cache* cache, ss_plan* plan, int32_t layer_be
  * compute -> transfer handoff. */
 int ss_launch_direct_send_after_async(ss_cache* cache, ss_plan* plan, int32_t layer_begin,
                                       int32_t layer_end, void* event, void* stream);
+/* How this engine's device-direct sends (DirectSend launches) move rows:
+ *   SS_SEND_KERNEL       the copy kernel (default); max_ctas > 0 caps its
+ *                        grid (an SM budget, so a send overlapping the next
+ *                        layer's prefill takes at most max_ctas SMs' worth
+ *                        of CTAs from it); 0 = the whole machine.
+ *   SS_SEND_COPY_ENGINE  the GPU's copy engines (zero SMs for the rows):
+ *                        per launch the address is validated on the device
+ *                        and the host waits for the verdict (a rejected
+ *                        address raises UnknownAddress here, nothing is
+ *                        written), then one batched copy moves every
+ *                        (row run, layer) and a small kernel marks fill
+ *                        states and bumps the window counters.  Reserved
+ *                        receive slots are Empty (prep_recv hands out
+ *                        fresh pages, re-prefill is forbidden), so the
+ *                        write-Empty-only rule holds without a per-row
+ *                        check; the receiver must keep the window open
+ *                        while a send is in flight (as with the kernel). */
+#define SS_SEND_KERNEL 0
+#define SS_SEND_COPY_ENGINE 1
+int ss_set_send_mode(ss_cache* cache, int32_t mode, int32_t max_ctas);
 /* Fan-out DirectSend (context-cache migration to several engines,
  * SPEC.md:434-441): the same positions [begin, end) of `seq` stored into
  * n_dest receivers at once, each through its own KVAddrInfo covering

@@ -270,6 +270,7 @@ ss_cache::~ss_cache() {
   }
   for (ss_plan* p : live_plans_) {
     if (device_ >= 0) FreePlanDevice(p);
+    if (p->upload_ev != nullptr) cudaEventDestroy(p->upload_ev);
     delete p;
   }
   live_plans_.clear();
@@ -303,6 +304,14 @@ ss_cache::~ss_cache() {
       cudaEventDestroy(stage_ev_[i]);
     }
     cudaFreeHost(h_stage_);
+  }
+  if (verdict_stream_ != nullptr) {
+    cudaStreamSynchronize(verdict_stream_);
+    cudaStreamSynchronize(ce_stream_);
+    cudaStreamDestroy(verdict_stream_);
+    cudaStreamDestroy(ce_stream_);
+    cudaEventDestroy(verdict_ev_);
+    cudaEventDestroy(ce_ev_);
   }
   cudaEventDestroy(internal_ev_);
   cudaEventDestroy(window_ev_);
@@ -1000,6 +1009,7 @@ void ss_cache::FreePlanDevice(ss_plan* plan) {
 
 void ss_cache::DestroyPlan(ss_plan* plan) {
   live_plans_.erase(plan);
+  if (plan->upload_ev != nullptr) cudaEventDestroy(plan->upload_ev);
   if (device_ >= 0 && (plan->dev.ptr || plan->d_partial)) {
     cudaSetDevice(device_);
     OrderAfterUser();
@@ -1066,6 +1076,7 @@ void ss_cache::LaunchRemote(const PeerTarget& peer, const int32_t* d_src_slots,
   c.sys_scope = (peer.device != device_ || force_sys_scope_) ? 1 : 0;
   c.pdl = after == nullptr ? 1 : 0;  // overlaps the copy grid's launch with the validation
   c.gen = v.gen;
+  c.max_ctas = send_ctas_;
   launch_copy_rows(c, s, num_sms_);
   CountLaunches(2);
 }
@@ -1494,6 +1505,8 @@ ss_plan* ss_cache::BeginDirectSend(SeqId seq, int64_t begin, int64_t end, Rank d
   plan->on_device = true;
   plan->is_direct_send = true;
   CudaCheck(cudaEventRecord(internal_ev_, stream_), "cudaEventRecord");
+  CudaCheck(cudaEventCreateWithFlags(&plan->upload_ev, cudaEventDisableTiming), "event");
+  CudaCheck(cudaEventRecord(plan->upload_ev, stream_), "cudaEventRecord");
   live_plans_.insert(plan.get());
   return plan.release();
 }
@@ -1522,10 +1535,142 @@ void ss_cache::LaunchDirectSend(ss_plan* plan, int32_t lb, int32_t le, cudaStrea
   if (lb == le) return;
   const PeerTarget& peer = PeerFor(snd.dest);
   OrderLaunch(s);
+  if (send_mode_ == SS_SEND_COPY_ENGINE) {
+    LaunchDirectSendCE(plan, peer, rec, lb, le, s, after);
+    if (s != stream_) NoteUser(s);
+    return;
+  }
   const auto& d = plan->dsend[0];
   LaunchRemote(peer, rec->d_slots + snd.begin, d.dst_slots, d.range_page, d.range_begin,
                d.range_count, d.n_ranges, d.verdict, snd.end - snd.begin, lb, le, s, after);
   if (s != stream_) NoteUser(s);
+}
+
+void ss_cache::SetSendMode(int32_t mode, int32_t max_ctas) {
+  MKV_CHECK(mode == SS_SEND_KERNEL || mode == SS_SEND_COPY_ENGINE, kInvalidArgument,
+            "unknown send mode");
+  MKV_CHECK(max_ctas >= 0, kInvalidArgument, "negative CTA budget");
+  RequireDevice("SetSendMode");
+  send_mode_ = mode;
+  send_ctas_ = max_ctas;
+}
+
+// Copy-engine DirectSend.  Validation runs on a side stream (not behind the
+// data stream's earlier copies) and the host takes the verdict, so a
+// rejected address writes nothing; the rows then move as one batch of 3-D
+// copies on `s` — one per row run, its depth the layer range, the pools'
+// layer stride as the slice pitch — and k_copy_rows in no-data mode marks
+// the fill states and publishes the window counters behind them.
+void ss_cache::LaunchDirectSendCE(ss_plan* plan, const PeerTarget& peer, Record* rec, int32_t lb,
+                                  int32_t le, cudaStream_t s, cudaEvent_t after) {
+  const PlanSend& snd = plan->sends[0];
+  const auto& d = plan->dsend[0];
+  if (plan->ce_runs.empty() && snd.end > snd.begin) {
+    std::vector<int32_t> dst;
+    ExpandAddr(snd.dest_addr, &dst, nullptr, nullptr, nullptr);
+    const int32_t* src = rec->slots.data() + snd.begin;
+    const int64_t n = snd.end - snd.begin;
+    for (int64_t i = 0; i < n; ++i) {
+      auto& runs = plan->ce_runs;
+      if (!runs.empty() && runs.back().src + runs.back().n == src[i] &&
+          runs.back().dst + runs.back().n == dst[i]) {
+        ++runs.back().n;
+      } else {
+        runs.push_back({src[i], dst[i], 1});
+      }
+    }
+  }
+  if (verdict_stream_ == nullptr) {
+    CudaCheck(cudaStreamCreateWithFlags(&verdict_stream_, cudaStreamNonBlocking), "stream");
+    CudaCheck(cudaStreamCreateWithFlags(&ce_stream_, cudaStreamNonBlocking), "stream");
+    CudaCheck(cudaEventCreateWithFlags(&verdict_ev_, cudaEventDisableTiming), "event");
+    CudaCheck(cudaEventCreateWithFlags(&ce_ev_, cudaEventDisableTiming), "event");
+  }
+  // The plan's upload and the receiver's window open first (the plan's own
+  // upload event: the internal stream itself may be queued behind caller
+  // streams' compute by now, and the host waits for this validation).
+  CudaCheck(cudaStreamWaitEvent(verdict_stream_, plan->upload_ev, 0), "wait plan");
+  if (peer.local != nullptr) {
+    CudaCheck(cudaStreamWaitEvent(verdict_stream_, peer.local->window_ev_, 0), "wait window");
+  }
+  ValidateParams v{};
+  v.range_page = d.range_page;
+  v.range_begin = d.range_begin;
+  v.range_count = d.range_count;
+  v.n_ranges = d.n_ranges;
+  v.page_window = peer.page_window;
+  v.expecting = peer.expecting;
+  v.num_pages = peer.num_pages;
+  v.P = peer.P;
+  v.verdict = d.verdict;
+  v.status = nullptr;  // reported synchronously below
+  v.gen = NextLaunchGen();
+  launch_validate_remote(v, verdict_stream_);
+  D2H(h_pinned_, d.verdict, 2 * sizeof(int32_t), verdict_stream_, "D2H verdict");
+  CountLaunches(1);
+  CudaCheck(cudaStreamSynchronize(verdict_stream_), "verdict");
+  const int32_t* vh = reinterpret_cast<const int32_t*>(h_pinned_);
+  if (vh[1] == v.gen || vh[0] < 0) {
+    Throw(kUnknownAddress, "the receiver rejected the destination address");
+  }
+  // The batched copies need a non-legacy stream: they run on ce_stream_,
+  // after `s`'s earlier work and the producer's event, and `s` continues
+  // after them.
+  CudaCheck(cudaEventRecord(verdict_ev_, s), "cudaEventRecord");
+  CudaCheck(cudaStreamWaitEvent(ce_stream_, verdict_ev_, 0), "wait caller stream");
+  if (after != nullptr) CudaCheck(cudaStreamWaitEvent(ce_stream_, after, 0), "wait producer");
+  const int32_t nl = le - lb;
+  const size_t row_b = static_cast<size_t>(W_) * 8;
+  const size_t src_lb = static_cast<size_t>(num_pages_) * P_ * row_b;
+  const size_t dst_lb = static_cast<size_t>(peer.num_pages) * peer.P * row_b;
+  std::vector<cudaMemcpy3DBatchOp> ops(plan->ce_runs.size());
+  for (size_t i = 0; i < ops.size(); ++i) {
+    const auto& r = plan->ce_runs[i];
+    cudaMemcpy3DBatchOp& o = ops[i];
+    o = cudaMemcpy3DBatchOp{};
+    o.src.type = cudaMemcpyOperandTypePointer;
+    o.src.op.ptr.ptr = reinterpret_cast<uint8_t*>(d_pool_) + lb * src_lb + r.src * row_b;
+    o.src.op.ptr.rowLength = src_lb;  // bytes: one "row" of the 3-D view per layer
+    o.src.op.ptr.layerHeight = 1;
+    o.dst.type = cudaMemcpyOperandTypePointer;
+    o.dst.op.ptr.ptr = reinterpret_cast<uint8_t*>(peer.pool) + lb * dst_lb + r.dst * row_b;
+    o.dst.op.ptr.rowLength = dst_lb;
+    o.dst.op.ptr.layerHeight = 1;
+    o.extent = make_cudaExtent(r.n * row_b, 1, nl);
+    o.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+  }
+  if (!ops.empty()) {
+    size_t fail = 0;
+    CudaCheck(cudaMemcpy3DBatchAsync(ops.size(), ops.data(), &fail, 0, ce_stream_),
+              "cudaMemcpy3DBatchAsync");
+  }
+  CudaCheck(cudaEventRecord(ce_ev_, ce_stream_), "cudaEventRecord");
+  CudaCheck(cudaStreamWaitEvent(s, ce_ev_, 0), "wait copies");
+  CopyParams c{};
+  const int64_t src_lw = num_pages_ * P_ * W_, dst_lw = peer.num_pages * peer.P * W_;
+  c.src = d_pool_ + lb * src_lw;
+  c.src_layer_words = src_lw;
+  c.src_idx = rec->d_slots + snd.begin;
+  c.dst = peer.pool + lb * dst_lw;
+  c.dst_layer_words = dst_lw;
+  c.dst_idx = d.dst_slots;
+  c.dst_fill = peer.fill + lb * peer.num_pages * peer.P;
+  c.dst_fill_layer = peer.num_pages * peer.P;
+  c.fill_value = 2;  // FillState::kReceivedRemote
+  c.n_rows = snd.end - snd.begin;
+  c.layer0 = lb;
+  c.n_layers = nl;
+  c.W = W_;
+  c.win_received = peer.win_received;
+  c.win_layer_rows = peer.win_layer_rows;
+  c.win_layers = peer.L;
+  c.verdict = d.verdict;
+  c.status = d_status_;
+  c.sys_scope = (peer.device != device_ || force_sys_scope_) ? 1 : 0;
+  c.gen = v.gen;
+  c.no_data = 1;
+  launch_copy_rows(c, s, num_sms_);
+  CountLaunches(1);
 }
 
 // Fan-out DirectSend: n_dest DirectSends of one source range, each source

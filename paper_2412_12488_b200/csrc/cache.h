@@ -183,6 +183,13 @@ struct ss_plan {
   };
   std::vector<DevSend> dsend;
   bool is_direct_send = false;
+  cudaEvent_t upload_ev = nullptr;  // direct-send plans: recorded after the row maps' upload
+  // Copy-engine sends: maximal runs of rows consecutive in both the source
+  // and the destination slot space (built on the first copy-engine launch).
+  struct Run {
+    int32_t src, dst, n;
+  };
+  std::vector<Run> ce_runs;
   // Decode-attention plan (ss_begin_decode): context slot map in CSR form.
   bool is_decode_plan = false;
   int64_t batch = 0;
@@ -297,6 +304,7 @@ struct ss_cache {
   void ExportIpc(ss_ipc_handle* out);
   void ImportIpc(Rank dest, const ss_ipc_handle* h);
   void DetachPeer(Rank dest);
+  void SetSendMode(int32_t mode, int32_t max_ctas);
   void PeerInfo(Rank dest, int32_t* sys_scope, int32_t* peer_device) const {
     const mkv::PeerTarget& t = PeerFor(dest);
     if (sys_scope) *sys_scope = (t.device != device_ || force_sys_scope_) ? 1 : 0;
@@ -389,6 +397,8 @@ struct ss_cache {
                     const int32_t* d_rcount, int64_t n_ranges, int32_t* d_verdict, int64_t n_rows,
                     int32_t layer_begin, int32_t layer_end, cudaStream_t s,
                     cudaEvent_t after = nullptr);
+  void LaunchDirectSendCE(ss_plan* plan, const mkv::PeerTarget& peer, mkv::Record* rec,
+                          int32_t lb, int32_t le, cudaStream_t s, cudaEvent_t after);
   void ExpandAddr(const mkv::KVAddr& a, std::vector<int32_t>* slots, std::vector<int64_t>* rp,
                   std::vector<int32_t>* rb, std::vector<int32_t>* rc) const;
   void OpenDeviceWindow(mkv::Record* rec, int64_t m, int64_t e);
@@ -414,6 +424,12 @@ struct ss_cache {
   int32_t rank_;
   int num_sms_ = 148;
   bool force_sys_scope_ = false;  // MICROKV_FORCE_SYS_SCOPE=1 (test hook)
+  int32_t send_mode_ = SS_SEND_KERNEL;  // ss_set_send_mode
+  int32_t send_ctas_ = 0;               // copy-kernel grid cap of sends (0 = none)
+  cudaStream_t verdict_stream_ = nullptr;  // copy-engine sends: validation off the data stream
+  cudaEvent_t verdict_ev_ = nullptr;
+  cudaStream_t ce_stream_ = nullptr;       // copy-engine sends: the batched copies
+  cudaEvent_t ce_ev_ = nullptr;
   std::atomic<int64_t> launches_{0};
   std::atomic<int32_t> launch_gen_{0};  // validated-launch generations (NextLaunchGen)
 

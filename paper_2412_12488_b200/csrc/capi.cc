@@ -460,6 +460,13 @@ int ss_launch_direct_send_after_async(ss_cache* c, ss_plan* p, int32_t lb, int32
   });
 }
 
+int ss_set_send_mode(ss_cache* c, int32_t mode, int32_t max_ctas) {
+  return Guard(c, [&]() -> int {
+    c->SetSendMode(mode, max_ctas);
+    return SS_OK;
+  });
+}
+
 int ss_broadcast_send_async(ss_cache* c, int64_t seq, int64_t begin, int64_t end, int32_t n_dest,
                             const int32_t* dests, const ss_addr* addrs, uint64_t tag, int32_t lb,
                             int32_t le, void* stream) {

@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
     for (int k = 0; k < nr; ++k) {
       const int64_t si = __shfl_sync(0xffffffffu, my_s, k);
       const int64_t di = __shfl_sync(0xffffffffu, my_d, k);  // int32 shuffles, widened
-      if ((todo >> k) & 1u) copy_row<kVec>(src_l + si * p.W, dst_l + di * p.W, p.W, lane);
+      if (((todo >> k) & 1u) && !p.no_data) copy_row<kVec>(src_l + si * p.W, dst_l + di * p.W, p.W, lane);
     }
     if (fill_l != nullptr) {
       __syncwarp();
@@ -612,7 +612,8 @@ void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms) {
 #define MKV_LONG_PER_SM 2
 #endif
   const int per_sm = q.group == 1 ? 8 : (groups >= static_cast<int64_t>(num_sms) * 2 * warps_per_block * 8 ? MKV_LONG_PER_SM : 8);
-  const int grid = grid_for(groups, warps_per_block, num_sms, per_sm);
+  int grid = grid_for(groups, warps_per_block, num_sms, per_sm);
+  if (q.max_ctas > 0 && grid > q.max_ctas) grid = q.max_ctas;
   const size_t smem = q.win_received ? sizeof(uint32_t) * q.n_layers : 0;
   void (*kern)(CopyParams) = q.W == 512 ? k_copy_rows<4>    // Llama 8B/70B KV rows: 4 KiB
                              : q.W == 128 ? k_copy_rows<1>  // tiny config rows: 1 KiB

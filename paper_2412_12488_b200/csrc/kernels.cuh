@@ -71,6 +71,9 @@ struct CopyParams {
   int32_t pdl;                // 1: launched as a programmatic dependent of the
                               // validation kernel (griddepcontrol.wait before
                               // the verdict is read)
+  int32_t max_ctas;           // > 0: grid cap (SM budget of a send); 0 = whole machine
+  int32_t no_data;            // 1: the rows were moved by the copy engines; only
+                              // mark fill states and publish the window counters
 };
 void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms);
 

@@ -213,6 +213,7 @@ _SIGNATURES = {
                                        C.POINTER(_Addr), C.c_uint64, C.POINTER(_vp)]),
     "ss_launch_direct_send_async": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, _vp]),
     "ss_launch_direct_send_after_async": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, _vp, _vp]),
+    "ss_set_send_mode": (C.c_int, [_vp, C.c_int32, C.c_int32]),
     "ss_broadcast_send_async": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, C.c_int32, _i32p,
                                           C.POINTER(_Addr), C.c_uint64, C.c_int32, C.c_int32, _vp]),
     "ss_gather_range_async": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, C.c_int32, _vp,
@@ -896,6 +897,14 @@ class KVCache:
         lb, le = layers
         self._check(self._lib.ss_launch_direct_send_after_async(
             self._h, plan.handle, lb, le, C.c_void_p(event), C.c_void_p(stream)))
+
+    SEND_KERNEL, SEND_COPY_ENGINE = 0, 1
+
+    def set_send_mode(self, mode: int = 0, max_ctas: int = 0) -> None:
+        """DirectSend row mover: SEND_KERNEL (copy kernel, grid capped at
+        max_ctas CTAs when > 0) or SEND_COPY_ENGINE (copy engines, no SMs
+        for the rows); see ss_set_send_mode."""
+        self._check(self._lib.ss_set_send_mode(self._h, mode, max_ctas))
 
     def broadcast_send_async(self, seq: int, range: tuple, dests: Sequence[int],
                              dest_addrs: Sequence[KVAddrInfo], user_tag: int = 0,
