@@ -1152,14 +1152,47 @@ def measure_append_gather(torch) -> dict:
     torch.cuda.synchronize()
     gat_s = g[0].elapsed_time(g[1]) / 1e3
     assert torch.equal(out, rows), "gather(append(rows)) != rows"
+    # All 80 layers in one launch each way (ss_gather_range_layers_async /
+    # ss_append_rows_layers_async), median of 5.
+    out.zero_()
+    gl, al = [], []
+    for rep in range(6):
+        with torch.cuda.stream(s):
+            torch.cuda._sleep(5_000_000)
+        g[0].record(s)
+        C_.gather_range_layers_async(1, (0, n), (0, L), out.data_ptr(), s.cuda_stream)
+        g[1].record(s)
+        torch.cuda.synchronize()
+        if rep:
+            gl.append(g[0].elapsed_time(g[1]) / 1e3)
+    assert torch.equal(out, rows), "gather_layers(append(rows)) != rows"
+    C_.FreeSequence(1)
+    for rep in range(6):
+        C_.CreateSequence(10 + rep, _prompt(3))
+        C_.EnsureAllocated(10 + rep, n)
+        pl = C_.BeginForward([BatchEntry(10 + rep, (0, n))])
+        with torch.cuda.stream(s):
+            torch.cuda._sleep(5_000_000)
+        g[0].record(s)
+        C_.append_rows_layers_async(pl, (0, L), rows.data_ptr(), s.cuda_stream)
+        g[1].record(s)
+        torch.cuda.synchronize()
+        pl.close()
+        C_.FreeSequence(10 + rep)
+        if rep:
+            al.append(g[0].elapsed_time(g[1]) / 1e3)
+    gl_s, al_s = float(np.median(gl)), float(np.median(al))
     del out, rows
     alg = 2 * n * L * BPT
     plan.close()
     return {"append_gbs": round(alg / app_s / 1e9, 1), "append_frac": round(alg / app_s / 1e9 / peak, 4),
             "gather_gbs": round(alg / gat_s / 1e9, 1), "gather_frac": round(alg / gat_s / 1e9 / peak, 4),
+            "append_layers_one_launch_frac": round(alg / al_s / 1e9 / peak, 4),
+            "gather_layers_one_launch_frac": round(alg / gl_s / 1e9 / peak, 4),
             "tokens": n, "layers": L, "launches_per_op": L,
             "algorithmic_bytes": alg,
-            "note": "read+write bytes; 80 per-layer launches each, queued back to back"}
+            "note": "read+write bytes; append/gather: 80 per-layer launches each, queued back to "
+                    "back (programmatic dependent launches); *_one_launch: all 80 layers in one"}
 
 
 def measure_decode(torch) -> dict:

@@ -376,6 +376,12 @@ int ss_broadcast_send_async(ss_cache* cache, int64_t seq, int64_t begin, int64_t
                             int32_t n_dest, const int32_t* dests, const ss_addr* dest_addrs,
                             uint64_t user_tag, int32_t layer_begin, int32_t layer_end,
                             void* stream);
+/* GatherRange for layers [layer_begin, layer_end) in one launch, into
+ * out_dev[layer_end - layer_begin][end - begin][dim] (a migration or a
+ * prefix export that takes every layer at once). */
+int ss_gather_range_layers_async(ss_cache* cache, int64_t seq, int64_t begin, int64_t end,
+                                 int32_t layer_begin, int32_t layer_end, uint64_t* out_dev,
+                                 void* stream);
 /* GatherRange into device memory out_dev[(end-begin) * dim] on `stream`. */
 int ss_gather_range_async(ss_cache* cache, int64_t seq, int64_t begin, int64_t end, int32_t layer,
                           uint64_t* out_dev, void* stream);

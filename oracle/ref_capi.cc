@@ -466,6 +466,10 @@ int ss_broadcast_send_async(ss_cache*, int64_t, int64_t, int64_t, int32_t, const
 int ss_gather_range_async(ss_cache*, int64_t, int64_t, int64_t, int32_t, uint64_t*, void*) {
   return SS_ERR_UNSUPPORTED;
 }
+int ss_gather_range_layers_async(ss_cache*, int64_t, int64_t, int64_t, int32_t, int32_t, uint64_t*,
+                                 void*) {
+  return SS_ERR_UNSUPPORTED;
+}
 int ss_apply_remote_write_async(ss_cache*, const ss_addr*, int32_t, const uint64_t*, int64_t,
                                 uint64_t, int32_t*, void*) {
   return SS_ERR_UNSUPPORTED;

@@ -1213,9 +1213,16 @@ void ss_cache::Attention(ss_plan* plan, int32_t layer, const uint64_t* hidden_in
 // kv_cache.cc:373-387 into device memory.
 void ss_cache::GatherRange(SeqId seq, int64_t begin, int64_t end, int32_t layer, uint64_t* out,
                            cudaStream_t s) {
+  MKV_CHECK(layer >= 0 && layer < L_, kInvalidArgument, "layer out of range");
+  GatherRangeLayers(seq, begin, end, layer, layer + 1, out, s);
+}
+
+// GatherRange of layers [lb, le) in one launch: out[le - lb][end - begin][W].
+void ss_cache::GatherRangeLayers(SeqId seq, int64_t begin, int64_t end, int32_t lb, int32_t le,
+                                 uint64_t* out, cudaStream_t s) {
   RequireDevice("GatherRange");
   const Record* rec = MustGet(seq);
-  MKV_CHECK(layer >= 0 && layer < L_, kInvalidArgument, "layer out of range");
+  MKV_CHECK(lb >= 0 && lb < le && le <= L_, kInvalidArgument, "layer out of range");
   MKV_CHECK(begin >= 0 && begin <= end, kInvalidArgument, "bad gather range");
   MKV_ICHECK(end <= rec->alloc_len, "position not allocated");
   // As in LaunchDirectSend: a live forward plan covering the range proves it
@@ -1223,19 +1230,24 @@ void ss_cache::GatherRange(SeqId seq, int64_t begin, int64_t end, int32_t layer,
   if (end > rec->committed_hint &&
       !CoveredByLivePlan(seq, std::max(begin, rec->committed_hint), end)) {
     AdvanceCommitted(MustGet(seq));
-    CheckFilled(rec, begin, end, layer, "gather over empty slot", nullptr);
+    for (int32_t l = lb; l < le && end > rec->committed_hint; ++l) {
+      CheckFilled(rec, begin, end, l, "gather over empty slot", nullptr);
+    }
   }
   const int64_t n = end - begin;
   if (n == 0) return;
   OrderLaunch(s);
   CopyParams c{};
-  c.src = PoolLayer(layer);
+  c.src = PoolLayer(lb);
+  c.src_layer_words = num_pages_ * P_ * W_;
   c.src_idx = rec->d_slots + begin;
   c.dst = out;
+  c.dst_layer_words = n * W_;
   c.n_rows = n;
-  c.layer0 = layer;
-  c.n_layers = 1;
+  c.layer0 = lb;
+  c.n_layers = le - lb;
   c.W = W_;
+  c.pdl = 1;  // launch overlaps the previous kernel's tail; waits for it before reading
   launch_copy_rows(c, s, num_sms_);
   CountLaunches(1);
   if (s != stream_) NoteUser(s);
@@ -1299,6 +1311,7 @@ void ss_cache::AppendRowsLayers(ss_plan* plan, int32_t lb, int32_t le, const voi
   c.layer0 = lb;
   c.n_layers = le - lb;
   c.W = W_;
+  c.pdl = 1;  // launch overlaps the previous kernel's tail; waits for it before reading
   launch_copy_rows(c, s, num_sms_);
   CountLaunches(1);
   for (const auto& e : plan->entries) {

@@ -254,6 +254,8 @@ struct ss_cache {
                       uint64_t* hidden_out_dev, cudaStream_t s);
   void GatherRange(SeqId seq, int64_t begin, int64_t end, int32_t layer, uint64_t* out_dev,
                    cudaStream_t s);
+  void GatherRangeLayers(SeqId seq, int64_t begin, int64_t end, int32_t layer_begin,
+                         int32_t layer_end, uint64_t* out_dev, cudaStream_t s);
   mkv::KVAddr BuildAddr(SeqId seq, int64_t begin, int64_t end);
   void AppendRows(ss_plan* plan, int32_t layer, const void* rows_dev, cudaStream_t s);
   void AppendRowsLayers(ss_plan* plan, int32_t layer_begin, int32_t layer_end, const void* rows_dev,

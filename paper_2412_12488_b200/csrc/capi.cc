@@ -489,6 +489,14 @@ int ss_gather_range_async(ss_cache* c, int64_t seq, int64_t begin, int64_t end, 
   });
 }
 
+int ss_gather_range_layers_async(ss_cache* c, int64_t seq, int64_t begin, int64_t end,
+                                 int32_t lb, int32_t le, uint64_t* out_dev, void* stream) {
+  return Guard(c, [&]() -> int {
+    c->GatherRangeLayers(seq, begin, end, lb, le, out_dev, S(stream));
+    return SS_OK;
+  });
+}
+
 int ss_apply_remote_write_async(ss_cache* c, const ss_addr* addr, int32_t layer,
                                 const uint64_t* payload_dev, int64_t n_words, uint64_t tag,
                                 int32_t* apply_status, void* stream) {

@@ -144,9 +144,34 @@ __device__ __forceinline__ void copy_row(const uint64_t* __restrict__ src, uint6
 template <int kVec>
 __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
   extern __shared__ uint32_t s_rows[];  // per relative layer (accounting only)
-  // Programmatic dependent of the validation kernel: this grid's launch
-  // overlaps it; the verdict is read only after it completed.
-  if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int group = p.group > 0 ? p.group : kGroup;
+  const int64_t groups = (p.n_rows + group - 1) / group;
+  const int64_t items = groups * p.n_layers;
+  // The first item's slot indices before waiting for the previous kernel:
+  // slot maps and page tables are host uploads ordered by stream events,
+  // never written by a kernel, so they may be read while the predecessor
+  // drains (fill bytes and row data are read after the wait).
+  int32_t pre_s = 0, pre_d = 0;
+  if (warp < items) {
+    const int32_t lrel = static_cast<int32_t>(warp / groups);
+    const int64_t r0 = (warp - static_cast<int64_t>(lrel) * groups) * group;
+    if (lane < p.n_rows - r0 && lane < group) {
+      pre_s = p.src_idx ? __ldg(p.src_idx + r0 + lane) : static_cast<int32_t>(r0 + lane);
+      pre_d = p.dst_idx ? __ldg(p.dst_idx + r0 + lane) : static_cast<int32_t>(r0 + lane);
+    }
+  }
+  // Programmatic dependent of the previous kernel on the stream (the
+  // validation kernel, or the previous copy): this grid's launch overlaps
+  // it; nothing it may have written is read before it completed.
+  if (p.pdl) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // The next PDL launch on the stream (another copy) may start its CTAs as
+    // ours drain; it waits for our completion before touching memory.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
   int32_t window = -1;
   if (p.verdict != nullptr) {
     window = reinterpret_cast<const volatile int32_t*>(p.verdict)[1] == p.gen
@@ -159,12 +184,6 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
     for (int i = threadIdx.x; i < p.n_layers; i += blockDim.x) s_rows[i] = 0;
     __syncthreads();
   }
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  const int group = p.group > 0 ? p.group : kGroup;
-  const int64_t groups = (p.n_rows + group - 1) / group;
-  const int64_t items = groups * p.n_layers;
   for (int64_t it = warp; it < items; it += n_warps) {
     const int32_t lrel = static_cast<int32_t>(it / groups);
     const int64_t r0 = (it - static_cast<int64_t>(lrel) * groups) * group;
@@ -177,15 +196,24 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
 #else
     uint8_t* fill_l = p.dst_fill != nullptr ? p.dst_fill + lrel * p.dst_fill_layer : nullptr;
 #endif
+    const uint64_t* src_l = p.src + lrel * p.src_layer_words;
+    uint64_t* dst_l = p.dst + lrel * p.dst_layer_words;
     if (lane < nr) {
-      my_s = p.src_idx ? __ldg(p.src_idx + r0 + lane) : static_cast<int32_t>(r0 + lane);
-      my_d = p.dst_idx ? __ldg(p.dst_idx + r0 + lane) : static_cast<int32_t>(r0 + lane);
+#ifndef MKV_NO_PREFETCH
+      if (it == warp) {
+#else
+      if (false) {
+#endif
+        my_s = pre_s;
+        my_d = pre_d;
+      } else {
+        my_s = p.src_idx ? __ldg(p.src_idx + r0 + lane) : static_cast<int32_t>(r0 + lane);
+        my_d = p.dst_idx ? __ldg(p.dst_idx + r0 + lane) : static_cast<int32_t>(r0 + lane);
+      }
       if (fill_l != nullptr) my_f = ld_cg_u8(fill_l + my_d);
     }
     // Empty destination slots only (kv_cache.cc:447); every row counts.
     const unsigned todo = __ballot_sync(0xffffffffu, lane < nr && my_f == 0);
-    const uint64_t* src_l = p.src + lrel * p.src_layer_words;
-    uint64_t* dst_l = p.dst + lrel * p.dst_layer_words;
 #pragma unroll 1
     for (int k = 0; k < nr; ++k) {
       const int64_t si = __shfl_sync(0xffffffffu, my_s, k);
@@ -199,12 +227,18 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
     if (account && lane == 0) atomicAdd(&s_rows[lrel], static_cast<uint32_t>(nr));
   }
   if (account) {
-    // Publish: every thread's stores, then the counters (release), so a peer
-    // engine that observes a counter also observes the rows.
+    // Publish: every thread's row stores, then the counters.  The CTA
+    // barrier puts every thread's stores before each counter update in
+    // causality order and the updates are release reductions (cumulative),
+    // so a peer engine that acquires a counter also observes the rows — the
+    // barrier + red.release pattern of CUTLASS's semaphores; no per-thread
+    // fence (-DMKV_FENCE_ALL restores one per thread for A/B).
+#ifdef MKV_FENCE_ALL
     fence_publish(p.sys_scope != 0);
+#endif
     __syncthreads();
     // Per-layer counters in parallel, one thread per layer; the total by
-    // thread 0 (the data fence above orders every row before any counter).
+    // thread 0.
     for (int i = threadIdx.x; i < p.n_layers; i += blockDim.x) {
       if (s_rows[i] != 0) {
         red_sys_add(p.win_layer_rows + static_cast<int64_t>(window) * p.win_layers + p.layer0 + i,
@@ -216,7 +250,6 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
     // window row is recycled after the drain).
     __syncthreads();
     if (threadIdx.x == 0) {
-      fence_publish(p.sys_scope != 0);
       unsigned long long total = 0;
       for (int i = 0; i < p.n_layers; ++i) total += s_rows[i];
       if (total != 0) red_sys_add(p.win_received + window, total, p.sys_scope != 0);
@@ -298,8 +331,10 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows_fanout(FanoutParams 
       }
     }
   }
+#ifdef MKV_FENCE_ALL
   fence_publish(p.sys_scope != 0);
-  __syncthreads();
+#endif
+  __syncthreads();  // rows before counters (barrier + release reductions, see k_copy_rows)
   for (int d = 0; d < p.n_dest; ++d) {
     if (window[d] < 0) continue;
     for (int i = threadIdx.x; i < p.n_layers; i += blockDim.x) {
@@ -312,7 +347,6 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows_fanout(FanoutParams 
     }
     __syncthreads();  // the window total after its layer counters (see k_copy_rows)
     if (threadIdx.x == 0) {
-      fence_publish(p.sys_scope != 0);
       unsigned long long total = 0;
       for (int i = 0; i < p.n_layers; ++i) total += s_rows[d * p.n_layers + i];
       if (total != 0) red_sys_add(p.win_received[d] + window[d], total, p.sys_scope != 0);
@@ -605,13 +639,25 @@ void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms) {
   // (per-layer append / gather): one row per warp, 8 CTAs per SM, so no
   // warp chains several rows' load latencies.
   CopyParams q = p;
+#ifndef MKV_SHORT_GROUP
+#define MKV_SHORT_GROUP 1
+#endif
+#ifndef MKV_SHORT_PER_SM
+#define MKV_SHORT_PER_SM 8
+#endif
   const int64_t one_wave = static_cast<int64_t>(num_sms) * 8 * warps_per_block;
-  q.group = items <= one_wave ? 1 : kGroup;
+  // Short launches (a wave or less of resident warps): one row per warp for
+  // plain copies (append / gather: +10%), 4-row items for sends that publish
+  // window counters (a quarter of the CTAs pay the publication: one 70B
+  // layer 25.6 -> 19.5 us).
+  const int short_group = p.win_received != nullptr ? 4 : MKV_SHORT_GROUP;
+  const bool short_launch = items <= one_wave * short_group;
+  q.group = short_launch ? short_group : kGroup;
   const int64_t groups = (q.n_rows + q.group - 1) / q.group * q.n_layers;
 #ifndef MKV_LONG_PER_SM
 #define MKV_LONG_PER_SM 2
 #endif
-  const int per_sm = q.group == 1 ? 8 : (groups >= static_cast<int64_t>(num_sms) * 2 * warps_per_block * 8 ? MKV_LONG_PER_SM : 8);
+  const int per_sm = short_launch ? MKV_SHORT_PER_SM : (groups >= static_cast<int64_t>(num_sms) * 2 * warps_per_block * 8 ? MKV_LONG_PER_SM : 8);
   int grid = grid_for(groups, warps_per_block, num_sms, per_sm);
   if (q.max_ctas > 0 && grid > q.max_ctas) grid = q.max_ctas;
   const size_t smem = q.win_received ? sizeof(uint32_t) * q.n_layers : 0;

@@ -218,6 +218,8 @@ _SIGNATURES = {
                                           C.POINTER(_Addr), C.c_uint64, C.c_int32, C.c_int32, _vp]),
     "ss_gather_range_async": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, C.c_int32, _vp,
                                         _vp]),
+    "ss_gather_range_layers_async": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, C.c_int32,
+                                               C.c_int32, _vp, _vp]),
     "ss_apply_remote_write_async": (C.c_int, [_vp, C.POINTER(_Addr), C.c_int32, _vp, C.c_int64,
                                               C.c_uint64, _i32p, _vp]),
     "ss_append_rows_async": (C.c_int, [_vp, _vp, C.c_int32, _vp, _vp]),
@@ -933,6 +935,14 @@ class KVCache:
                            stream: int = 0) -> None:
         self._check(self._lib.ss_gather_range_async(self._h, seq, range[0], range[1], layer,
                                                     C.c_void_p(out_ptr), C.c_void_p(stream)))
+
+    def gather_range_layers_async(self, seq: int, range: tuple, layers: tuple, out_ptr: int,
+                                  stream: int = 0) -> None:
+        """GatherRange of layers [begin, end) in one launch into
+        out[end - begin][range rows][dim] u64 words in device memory."""
+        self._check(self._lib.ss_gather_range_layers_async(self._h, seq, range[0], range[1],
+                                                           layers[0], layers[1],
+                                                           C.c_void_p(out_ptr), C.c_void_p(stream)))
 
     # ---- wire formats (transport.h:6-12): frames for the cross-node path ----
     def crc32_async(self, data_ptr: int, n_bytes: int, crc_ptr: int, stream: int = 0) -> None:
