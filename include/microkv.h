@@ -346,6 +346,24 @@ int ss_launch_direct_send_async(ss_cache* cache, ss_plan* plan, int32_t layer_be
  * compute -> transfer handoff. */
 int ss_launch_direct_send_after_async(ss_cache* cache, ss_plan* plan, int32_t layer_begin,
                                       int32_t layer_end, void* event, void* stream);
+/* Relay chain for prefix migration to several engines:
+ * `plan` is an ss_begin_direct_send plan on an engine that is itself still
+ * RECEIVING [begin, end) of `seq` (an open receive window).  Each layer in
+ * [layer_begin, layer_end) is forwarded to the plan's destination as soon
+ * as that layer has fully landed here (the forwarding kernel's warps wait
+ * on this engine's per-layer receive counters, at most timeout_ms; on
+ * timeout the rest is not forwarded and ss_synchronize raises Aborted).
+ * The kernel runs at most one CTA per SM (max_ctas of ss_set_send_mode
+ * caps it further) so an upstream copy on the same GPU keeps SMs.  As with
+ * any device-side wait: a kernel that is lazily loaded (CUDA 12's default
+ * module loading) while relay warps wait may stall until they time out —
+ * load such kernels first, or run with CUDA_MODULE_LOADING=EAGER (every
+ * kernel of this library is loaded when a cache is created).
+ * Owner -> T1 -> T2 ... puts each prefix byte on every link once, instead
+ * of k times on the owner's egress.  A range that has already landed is
+ * sent as a plain DirectSend. */
+int ss_launch_relay_send_async(ss_cache* cache, ss_plan* plan, int32_t layer_begin,
+                               int32_t layer_end, int64_t timeout_ms, void* stream);
 /* How this engine's device-direct sends (DirectSend launches) move rows:
  *   SS_SEND_KERNEL       the copy kernel (default); max_ctas > 0 caps its
  *                        grid (an SM budget, so a send overlapping the next

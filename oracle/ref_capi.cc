@@ -442,6 +442,9 @@ int ss_import_ipc(ss_cache*, int32_t, const ss_ipc_handle*) { return SS_ERR_UNSU
 int ss_detach_peer(ss_cache*, int32_t) { return SS_ERR_UNSUPPORTED; }
 int ss_peer_info(const ss_cache*, int32_t, int32_t*, int32_t*) { return SS_ERR_UNSUPPORTED; }
 int ss_set_send_mode(ss_cache*, int32_t, int32_t) { return SS_ERR_UNSUPPORTED; }
+int ss_launch_relay_send_async(ss_cache*, ss_plan*, int32_t, int32_t, int64_t, void*) {
+  return SS_ERR_UNSUPPORTED;
+}
 int ss_attention_async(ss_cache*, ss_plan*, int32_t, const uint64_t*, uint64_t*, void*) {
   return SS_ERR_UNSUPPORTED;
 }

@@ -1559,6 +1559,90 @@ void ss_cache::LaunchDirectSend(ss_plan* plan, int32_t lb, int32_t le, cudaStrea
   if (s != stream_) NoteUser(s);
 }
 
+// Relay chain (context-cache migration to several engines):
+// engine i receives a prefix from engine i-1 and forwards each layer to
+// engine i+1 as soon as that layer has fully landed here, so every link
+// carries the prefix once and the owner's egress is not multiplied by the
+// number of targets (a fan-out from the owner pushes k copies through its
+// one NVLink port).  The rows being forwarded are proven by this engine's
+// own receive counters — a device-side wait per layer, no host sync —
+// instead of a fill scan; a wait that times out marks the layer's launch
+// rejected (nothing is forwarded) and raises Aborted at Synchronize.
+void ss_cache::LaunchRelaySend(ss_plan* plan, int32_t lb, int32_t le, int64_t timeout_ms,
+                               cudaStream_t s) {
+  RequireDevice("RelaySend");
+  MKV_CHECK(plan->is_direct_send, kInvalidArgument, "not a direct-send plan");
+  MKV_CHECK(lb >= 0 && lb <= le && le <= L_, kInvalidArgument, "bad layer range");
+  MKV_CHECK(timeout_ms > 0, kInvalidArgument, "relay needs a positive timeout");
+  const PlanSend& snd = plan->sends[0];
+  Record* rec = MustGet(snd.seq);
+  const bool receiving = rec->window && rec->window->dev_id >= 0 && !rec->window->complete &&
+                         rec->window->begin <= std::max(snd.begin, rec->committed_hint) &&
+                         snd.end <= rec->window->end;
+  if (!receiving) {  // already landed (or never received): an ordinary DirectSend
+    LaunchDirectSend(plan, lb, le, s);
+    return;
+  }
+  if (lb == le || snd.end == snd.begin) return;
+  const PeerTarget& peer = PeerFor(snd.dest);
+  OrderLaunch(s);
+  const auto& d = plan->dsend[0];
+  const Window& w = *rec->window;
+  // Rows per layer the window still expects from device-direct senders
+  // (host-path frames counted on the host are already in place).
+  int64_t host_min = INT64_MAX;
+  {
+    std::lock_guard<std::mutex> lock(recv_mu_);
+    for (int32_t l = lb; l < le; ++l) {
+      host_min = std::min<int64_t>(host_min, static_cast<int32_t>(w.received_layer.size()) == L_
+                                                 ? w.received_layer[l] : 0);
+    }
+  }
+  const int64_t target = std::max<int64_t>(0, (w.end - w.begin) - host_min);
+  if (peer.local != nullptr) CudaCheck(cudaStreamWaitEvent(s, peer.local->window_ev_, 0), "wait window");
+  ValidateParams v{};
+  v.range_page = d.range_page;
+  v.range_begin = d.range_begin;
+  v.range_count = d.range_count;
+  v.n_ranges = d.n_ranges;
+  v.page_window = peer.page_window;
+  v.expecting = peer.expecting;
+  v.num_pages = peer.num_pages;
+  v.P = peer.P;
+  v.verdict = d.verdict;
+  v.status = d_status_;
+  v.gen = NextLaunchGen();
+  launch_validate_remote(v, s);
+  CopyParams c{};
+  const int64_t src_lw = num_pages_ * P_ * W_, dst_lw = peer.num_pages * peer.P * W_;
+  c.src = d_pool_ + lb * src_lw;
+  c.src_layer_words = src_lw;
+  c.src_idx = rec->d_slots + snd.begin;
+  c.dst = peer.pool + lb * dst_lw;
+  c.dst_layer_words = dst_lw;
+  c.dst_idx = d.dst_slots;
+  c.dst_fill = peer.fill + lb * peer.num_pages * peer.P;
+  c.dst_fill_layer = peer.num_pages * peer.P;
+  c.fill_value = 2;  // FillState::kReceivedRemote
+  c.n_rows = snd.end - snd.begin;
+  c.layer0 = lb;
+  c.n_layers = le - lb;
+  c.W = W_;
+  c.win_received = peer.win_received;
+  c.win_layer_rows = peer.win_layer_rows;
+  c.win_layers = peer.L;
+  c.verdict = d.verdict;
+  c.status = d_status_;
+  c.sys_scope = (peer.device != device_ || force_sys_scope_) ? 1 : 0;
+  c.gen = v.gen;
+  c.pdl = 1;
+  c.max_ctas = send_ctas_;
+  launch_relay_rows(c, d_win_layer_rows_ + static_cast<int64_t>(w.dev_id) * L_,
+                    static_cast<uint32_t>(target), timeout_ms * 1000000LL, s, num_sms_);
+  CountLaunches(2);
+  if (s != stream_) NoteUser(s);
+}
+
 void ss_cache::SetSendMode(int32_t mode, int32_t max_ctas) {
   MKV_CHECK(mode == SS_SEND_KERNEL || mode == SS_SEND_COPY_ENGINE, kInvalidArgument,
             "unknown send mode");

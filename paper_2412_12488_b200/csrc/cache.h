@@ -276,6 +276,11 @@ struct ss_cache {
   // validation is enqueued before the stream waits for it, the copy after.
   void LaunchDirectSend(ss_plan* plan, int32_t layer_begin, int32_t layer_end, cudaStream_t s,
                         cudaEvent_t after = nullptr);
+  // Relay: forward layers [lb, le) of rows this engine is still receiving
+  // to the plan's destination, each layer behind a device-side wait for
+  // that layer's receive counter (a relay chain of prefix migration).
+  void LaunchRelaySend(ss_plan* plan, int32_t layer_begin, int32_t layer_end, int64_t timeout_ms,
+                       cudaStream_t s);
   void BroadcastSend(SeqId seq, int64_t begin, int64_t end, int32_t n_dest, const Rank* dests,
                      const mkv::KVAddr* addrs, uint64_t tag, int32_t layer_begin,
                      int32_t layer_end, cudaStream_t s);

@@ -460,6 +460,14 @@ int ss_launch_direct_send_after_async(ss_cache* c, ss_plan* p, int32_t lb, int32
   });
 }
 
+int ss_launch_relay_send_async(ss_cache* c, ss_plan* p, int32_t lb, int32_t le, int64_t timeout_ms,
+                               void* stream) {
+  return Guard(c, [&]() -> int {
+    c->LaunchRelaySend(p, lb, le, timeout_ms, S(stream));
+    return SS_OK;
+  });
+}
+
 int ss_set_send_mode(ss_cache* c, int32_t mode, int32_t max_ctas) {
   return Guard(c, [&]() -> int {
     c->SetSendMode(mode, max_ctas);

@@ -257,6 +257,97 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
   }
 }
 
+// Relay forward (a hop of a prefix-migration chain): like k_copy_rows from
+// this engine's slots into a peer's, but layer lrel of the source is only
+// read once this engine's own receive counter for it reached `target`
+// rows (lane 0 of a warp polls it with acquire loads when the warp first
+// reaches the layer), and each warp publishes its rows per layer as it
+// leaves the layer (release reductions), so the next hop can start on a
+// layer while this one is still receiving later layers.  The grid is
+// bounded (it spins while upstream layers are in flight) so the upstream
+// copy keeps SMs on a shared GPU.  A wait past timeout_ns sets
+// kStatusWaitTimeout and the warp stops (nothing more is forwarded).
+template <int kVec>
+__global__ void __launch_bounds__(kCopyThreads) k_relay_rows(CopyParams p, const uint32_t* wait,
+                                                             uint32_t target, long long timeout_ns) {
+  if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int32_t window = reinterpret_cast<const volatile int32_t*>(p.verdict)[1] == p.gen
+                             ? -1
+                             : reinterpret_cast<const volatile int32_t*>(p.verdict)[0];
+  if (window < 0) return;  // rejected by validation
+  const bool sys = p.sys_scope != 0;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int group = kGroup;
+  const int64_t groups = (p.n_rows + group - 1) / group;
+  const int64_t items = groups * p.n_layers;
+  int32_t ready = -1, cur = -1;
+  uint32_t cur_rows = 0;
+  unsigned long long t0 = 0;
+  auto publish = [&](int32_t l, uint32_t rows) {
+    __syncwarp();
+    if (lane == 0 && rows != 0) {
+      red_sys_add(p.win_layer_rows + static_cast<int64_t>(window) * p.win_layers + p.layer0 + l,
+                  rows, sys);
+      red_sys_add(p.win_received + window, static_cast<unsigned long long>(rows), sys);
+    }
+  };
+  for (int64_t it = warp; it < items; it += n_warps) {
+    const int32_t lrel = static_cast<int32_t>(it / groups);
+    const int64_t r0 = (it - static_cast<int64_t>(lrel) * groups) * group;
+    const int nr = static_cast<int>(p.n_rows - r0 < group ? p.n_rows - r0 : group);
+    if (lrel != cur) {
+      if (cur >= 0) publish(cur, cur_rows);
+      cur = lrel;
+      cur_rows = 0;
+    }
+    if (lrel > ready) {
+      int ok = 1;
+      if (lane == 0) {
+        if (t0 == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        for (;;) {
+          uint32_t v;
+          asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(wait + p.layer0 + lrel)
+                       : "memory");
+          if (v >= target) break;
+          unsigned long long now;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+          if (static_cast<long long>(now - t0) > timeout_ns) {
+            atomicOr(p.status, kStatusWaitTimeout);
+            ok = 0;
+            break;
+          }
+          __nanosleep(256);
+        }
+      }
+      if (!__shfl_sync(0xffffffffu, ok, 0)) return;
+      ready = lrel;
+    }
+    int32_t my_s = 0, my_d = 0;
+    uint8_t my_f = 0;
+    uint8_t* fill_l = p.dst_fill + lrel * p.dst_fill_layer;
+    if (lane < nr) {
+      my_s = __ldg(p.src_idx + r0 + lane);
+      my_d = __ldg(p.dst_idx + r0 + lane);
+      my_f = ld_cg_u8(fill_l + my_d);
+    }
+    const unsigned todo = __ballot_sync(0xffffffffu, lane < nr && my_f == 0);
+    const uint64_t* src_l = p.src + lrel * p.src_layer_words;
+    uint64_t* dst_l = p.dst + lrel * p.dst_layer_words;
+#pragma unroll 1
+    for (int k = 0; k < nr; ++k) {
+      const int64_t si = __shfl_sync(0xffffffffu, my_s, k);
+      const int64_t di = __shfl_sync(0xffffffffu, my_d, k);
+      if ((todo >> k) & 1u) copy_row<kVec>(src_l + si * p.W, dst_l + di * p.W, p.W, lane);
+    }
+    __syncwarp();
+    if ((todo >> lane) & 1u) fill_l[my_d] = p.fill_value;
+    cur_rows += static_cast<uint32_t>(nr);
+  }
+  if (cur >= 0) publish(cur, cur_rows);
+}
+
 // One thread per (range, slot) across as many CTAs as needed: every check
 // is an independent (possibly peer) load, so the address validates in about
 // one memory latency.  verdict[0] = window of the first page (block 0),
@@ -681,6 +772,29 @@ void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms) {
   }
 }
 
+void launch_relay_rows(const CopyParams& p, const uint32_t* wait, uint32_t target,
+                       long long timeout_ns, cudaStream_t s, int num_sms) {
+  const int64_t groups = (p.n_rows + kGroup - 1) / kGroup * p.n_layers;
+  if (groups <= 0) return;
+  const int warps_per_block = kCopyThreads / 32;
+  // One CTA per SM at most (its warps spin while upstream layers are in
+  // flight; the upstream copy must keep the rest of the machine).
+  int grid = grid_for(groups, warps_per_block, num_sms, 1);
+  if (p.max_ctas > 0 && grid > p.max_ctas) grid = p.max_ctas;
+  void (*kern)(CopyParams, const uint32_t*, uint32_t, long long) =
+      p.W == 512 ? k_relay_rows<4> : p.W == 128 ? k_relay_rows<1> : k_relay_rows<0>;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kCopyThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = p.pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, p, wait, target, timeout_ns);
+}
+
 void launch_copy_rows_fanout(const FanoutParams& p, cudaStream_t s, int num_sms) {
   const int64_t groups = (p.n_rows + kGroup - 1) / kGroup * p.n_layers;
   if (groups <= 0) return;
@@ -805,6 +919,9 @@ void preload_kernels() {
   cudaFuncGetAttributes(&a, k_copy_rows<1>);
   cudaFuncGetAttributes(&a, k_copy_rows<0>);
   cudaFuncGetAttributes(&a, k_copy_rows_fanout<4>);
+  cudaFuncGetAttributes(&a, k_relay_rows<4>);
+  cudaFuncGetAttributes(&a, k_relay_rows<1>);
+  cudaFuncGetAttributes(&a, k_relay_rows<0>);
   cudaFuncGetAttributes(&a, k_copy_rows_fanout<1>);
   cudaFuncGetAttributes(&a, k_validate_remote);
   cudaFuncGetAttributes(&a, k_attn_write_hash);

@@ -77,6 +77,11 @@ struct CopyParams {
 };
 void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms);
 
+// Relay hop: copy rows layer by layer as this engine's own receive
+// counters wait[layer0 + l] reach `target` (see k_relay_rows).
+void launch_relay_rows(const CopyParams& p, const uint32_t* wait, uint32_t target,
+                       long long timeout_ns, cudaStream_t s, int num_sms);
+
 // Fan-out row copy: one source row set stored into up to kMaxFanout
 // destinations (each with its own slots, fill rule and window counters).
 constexpr int kMaxFanout = 8;

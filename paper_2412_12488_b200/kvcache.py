@@ -214,6 +214,7 @@ _SIGNATURES = {
     "ss_launch_direct_send_async": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, _vp]),
     "ss_launch_direct_send_after_async": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, _vp, _vp]),
     "ss_set_send_mode": (C.c_int, [_vp, C.c_int32, C.c_int32]),
+    "ss_launch_relay_send_async": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, C.c_int64, _vp]),
     "ss_broadcast_send_async": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, C.c_int32, _i32p,
                                           C.POINTER(_Addr), C.c_uint64, C.c_int32, C.c_int32, _vp]),
     "ss_gather_range_async": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, C.c_int32, _vp,
@@ -899,6 +900,14 @@ class KVCache:
         lb, le = layers
         self._check(self._lib.ss_launch_direct_send_after_async(
             self._h, plan.handle, lb, le, C.c_void_p(event), C.c_void_p(stream)))
+
+    def launch_relay_send_async(self, plan: ForwardPlan, layers: Optional[tuple] = None,
+                                timeout_ms: int = 60000, stream: int = 0) -> None:
+        """Forward each layer of a range this engine is still receiving to
+        the plan's destination once it has landed here (relay chain)."""
+        lb, le = layers if layers is not None else (0, self.layers)
+        self._check(self._lib.ss_launch_relay_send_async(self._h, plan.handle, lb, le, timeout_ms,
+                                                         C.c_void_p(stream)))
 
     SEND_KERNEL, SEND_COPY_ENGINE = 0, 1
 
