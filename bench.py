@@ -963,8 +963,16 @@ def measure_configs(torch) -> dict:
 
 def measure_prefix_migration(torch) -> dict:
     """Config 4 on one GPU: an 8K-token cached prefix (70B shape) migrated from
-    its owner to k = 3 engines (prep_recv(end=len) on each target), as one
-    fan-out send (each source row read once) vs three DirectSends."""
+    its owner to k = 3 engines (prep_recv(end=len) on each target) as
+      fanout      one fan-out send from the owner (each source row read once),
+      sequential  three DirectSends from the owner,
+      relay       owner -> T1 -> T2 -> T3, each target forwarding a layer as
+                  soon as it has landed (ss_launch_relay_send_async).
+    On one GPU every hop is HBM traffic; across GPUs the owner's single
+    NVLink egress carries k copies for fanout/sequential and one for relay.
+    `nvlink_model_us` is the transfer time those egress bytes imply at the
+    measured per-direction peer-copy rate (B200_PROFILING.md), with the
+    relay's pipeline fill of one layer per extra hop."""
     from paper_2412_12488_b200 import KVCache
 
     peak, _ = _peaks()
@@ -974,40 +982,74 @@ def measure_prefix_migration(torch) -> dict:
     P = KVCache(num_pages=pages, page_size=PAGE, layers=L, dim=W, device=0, rank=0)
     Ds = [KVCache(num_pages=pages, page_size=PAGE, layers=L, dim=W, device=0, rank=r)
           for r in range(1, k + 1)]
-    for D in Ds:
+    P.attach_peer(1, Ds[0])
+    for D in Ds[1:]:
         P.attach_peer(D.rank, D)
+    for i in range(k - 1):
+        Ds[i].attach_peer(Ds[i + 1].rank, Ds[i + 1])
     _populate_prefix_l(P, 1, prompt, torch, L)
-    s = torch.cuda.Stream()
-    res = {"targets": k, "tokens": PROMPT, "payload_per_target_gb": round(PROMPT * L * BPT / 1e9, 3)}
-    for mode in ("fanout", "sequential"):
+    torch.cuda._sleep(1)  # loaded before any relay waits (lazy module loading)
+    streams = [torch.cuda.Stream() for _ in range(k + 1)]
+    s = streams[0]
+    pay1 = PROMPT * L * BPT
+    res = {"targets": k, "tokens": PROMPT, "payload_per_target_gb": round(pay1 / 1e9, 3)}
+    for mode in ("fanout", "sequential", "relay"):
         ts = []
-        for rep in range(4):
+        for rep in range(6):
             seqs = [1000 * (rep + 1) + D.rank for D in Ds]
             addrs = [D.PrepRecv(sq, prompt, PROMPT).addr for D, sq in zip(Ds, seqs)]
-            plans = [] if mode == "fanout" else [
-                P.begin_direct_send(1, (0, PROMPT), D.rank, a, rep) for D, a in zip(Ds, addrs)]
+            plans = []
+            if mode == "sequential":
+                plans = [P.begin_direct_send(1, (0, PROMPT), D.rank, a, rep) for D, a in zip(Ds, addrs)]
+            elif mode == "relay":
+                plans = [P.begin_direct_send(1, (0, PROMPT), 1, addrs[0], rep)]
+                hops = [Ds[i].begin_direct_send(seqs[i], (0, PROMPT), Ds[i + 1].rank, addrs[i + 1], rep)
+                        for i in range(k - 1)]
+            torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if mode == "relay":
+                for st in streams[1:]:
+                    st.wait_stream(s)
             e0.record(s)
             if mode == "fanout":
                 P.broadcast_send_async(1, (0, PROMPT), [D.rank for D in Ds], addrs, rep, None,
                                        s.cuda_stream)
-            else:
+            elif mode == "sequential":
                 for pl in plans:
                     P.launch_direct_send_async(pl, (0, L), s.cuda_stream)
+            else:
+                for i in reversed(range(k - 1)):
+                    Ds[i].launch_relay_send_async(hops[i], (0, L), 20000, streams[i + 1].cuda_stream)
+                P.launch_direct_send_async(plans[0], (0, L), s.cuda_stream)
+                for st in streams[1:]:
+                    s.wait_stream(st)
             e1.record(s)
-            s.synchronize()
+            torch.cuda.synchronize()
             for D, sq in zip(Ds, seqs):
+                D.synchronize()
                 assert D.DrainReceiveCompletions() == [sq]
+            if mode == "relay":
+                for h in hops:
+                    h.close()
+            for D, sq in zip(Ds, seqs):
                 D.FreeSequence(sq)
             for pl in plans:
                 pl.close()
-            ts.append(e0.elapsed_time(e1) / 1e3)
-        t = float(np.median(ts[1:]))
-        pay = k * PROMPT * L * BPT
-        hbm = (1 + k if mode == "fanout" else 2 * k) * PROMPT * L * BPT
+            if rep:
+                ts.append(e0.elapsed_time(e1) / 1e3)
+        t = float(np.median(ts))
+        pay = k * pay1
+        hbm = (1 + k if mode == "fanout" else 2 * k) * pay1
+        egress = pay1 * (1 if mode == "relay" else k)
+        link_s = egress / (NVLINK_PEER_GBS * 1e9) + ((k - 1) * pay1 / L / (NVLINK_PEER_GBS * 1e9)
+                                                     if mode == "relay" else 0.0)
         res[mode] = {"device_us": round(1e6 * t, 1), "aggregate_payload_gbs": round(pay / t / 1e9, 1),
-                     "hbm_bytes": hbm, "hbm_frac": round(hbm / t / 1e9 / peak, 4)}
+                     "hbm_bytes": hbm, "hbm_frac": round(hbm / t / 1e9 / peak, 4),
+                     "owner_egress_bytes": egress, "nvlink_model_us": round(1e6 * link_s, 1),
+                     "range_us": [round(1e6 * min(ts), 1), round(1e6 * max(ts), 1)]}
     res["fanout_speedup"] = round(res["sequential"]["device_us"] / res["fanout"]["device_us"], 3)
+    res["relay_vs_fanout_nvlink_model"] = round(res["fanout"]["nvlink_model_us"] /
+                                                res["relay"]["nvlink_model_us"], 3)
     del P, Ds
     torch.cuda.empty_cache()
     return res
