@@ -171,8 +171,27 @@ def run_reference_cpu(steps: int, warmup: int, threads: int, layer_sample: int) 
                         "apply": res.apply_s, "drain_free": res.drain_free_s}}
 
 
+def _host_info() -> dict:
+    """The host the CPU numbers were taken on (nproc + CPU model)."""
+    model = None
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count() or 1
+    return {"nproc": os.cpu_count(), "usable_cores": usable, "cpu_model": model}
+
+
 def _ref_threads() -> int:
-    cores = os.cpu_count() or 1
+    """Every usable host core, one engine pair per thread, bounded by memory
+    (each pair holds two 70B-shape pools of an 8K request)."""
+    cores = _host_info()["usable_cores"]
     per_pair = 2 * (PROMPT // PAGE + 8) * PAGE * L * W * 8 + 2 * PROMPT * W * 8
     try:
         import psutil
@@ -180,14 +199,14 @@ def _ref_threads() -> int:
         avail = psutil.virtual_memory().available
     except Exception:
         avail = 64 << 30
-    return max(1, min(cores, 16, int(avail * 0.5 // per_pair)))
+    return max(1, min(cores, int(avail * 0.6 // per_pair)))
 
 
 def reference_arm(args, rank: int, world: int) -> None:
     if rank != 0:
         return
     threads = _ref_threads()
-    sample = 16  # layers per step (bounded sample of the 80-layer migration)
+    sample = L  # every layer of the migration, every step
     r = run_reference_cpu(args.steps, args.warmup, threads, sample)
     line = {
         "metric": "KV migration GB/s (P->D, Llama-3.1-70B KV shape)",
@@ -197,9 +216,10 @@ def reference_arm(args, rank: int, world: int) -> None:
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic", "config": {"workload": WORKLOAD, "parallelism": f"{threads} engine pairs x 1 host thread"},
         "cpu_baseline": {"value": round(r["gbs"], 4), "unit": "GB/s", "cores": threads,
-                         "kind": "reference",
-                         "sample": f"{sample} of {L} layers per step, {threads} independent engine "
-                                   f"pairs (one thread each), {r['tokens_per_step']} tokens"},
+                         "kind": "reference", "host": _host_info(),
+                         "sample": f"all {sample} layers per step, {threads} independent engine "
+                                   f"pairs (one thread each, one per usable core unless memory "
+                                   f"bounds it), {r['tokens_per_step']} tokens"},
         "e2e": {"value": round(r["gbs"], 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "split_s": r["split_s"], "window_ok": r["ok"],
@@ -418,7 +438,7 @@ def our_arm(args, rank: int, world: int) -> None:
         try:
             r = run_reference_cpu(steps=2, warmup=0, threads=1, layer_sample=L)
             cpu_baseline = {"value": round(r["gbs"], 4), "unit": "GB/s", "cores": 1,
-                            "kind": "reference",
+                            "kind": "reference", "host": _host_info(),
                             "sample": f"2 full 80-layer migrations of one {r['tokens_per_step']}-"
                                       "token request, 1 engine pair on 1 thread "
                                       "(the reference's executor model)",
@@ -1099,7 +1119,8 @@ def fit_transfer_cost(sweep: dict) -> dict:
 def measure_sweep(torch) -> dict:
     """Config 5: DirectSend of n tokens x 80 layers (70B shape), n = 16 (one
     page) ... 32768, P and D on one GPU; device time per migration (one
-    validation + one copy launch), median of 5."""
+    validation + one copy launch), median of 9 (and the API wall time,
+    median of 9 more)."""
     from paper_2412_12488_b200 import KVCache
 
     peak, _ = _peaks()
@@ -1122,7 +1143,7 @@ def measure_sweep(torch) -> dict:
     seq = 100
     for n in [int(x) for x in os.environ.get("SWEEP_N", "16,64,256,1024,4096,8192,16384,32768").split(",")]:
         times, walls = [], []
-        for rep in range(10):
+        for rep in range(18):  # 9 device-timed + 9 wall-timed samples
             seq += 1
             rr = D.PrepRecv(seq, prompt[:n + 1], -1)
             plan = P.begin_direct_send(1, (0, n), 1, rr.addr, rep)

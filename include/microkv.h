@@ -370,17 +370,17 @@ int ss_launch_relay_send_async(ss_cache* cache, ss_plan* plan, int32_t layer_beg
  *                        layer's prefill takes at most max_ctas SMs' worth
  *                        of CTAs from it); 0 = the whole machine.
  *   SS_SEND_COPY_ENGINE  the GPU's copy engines (zero SMs for the rows):
- *                        per launch the address is validated on the device
- *                        and the host waits for the verdict (a rejected
- *                        address raises UnknownAddress here, nothing is
- *                        written), then one batched copy moves every
- *                        (row run, layer) and a small kernel marks fill
- *                        states and bumps the window counters.  Reserved
- *                        receive slots are Empty (prep_recv hands out
- *                        fresh pages, re-prefill is forbidden), so the
- *                        write-Empty-only rule holds without a per-row
- *                        check; the receiver must keep the window open
- *                        while a send is in flight (as with the kernel). */
+ *                        at a plan's first launch the address is validated
+ *                        on the device and the host waits for the verdict
+ *                        (a rejected address raises UnknownAddress there,
+ *                        nothing is written); every launch then moves its
+ *                        (row run, layer) blocks as one batch of 3-D copies
+ *                        and a small kernel marks fill states and bumps the
+ *                        window counters.  Reserved receive slots are Empty
+ *                        (prep_recv hands out fresh pages, re-prefill is
+ *                        forbidden), so the write-Empty-only rule holds
+ *                        without a per-row check; the receiver must keep
+ *                        the window open while the send is in flight. */
 #define SS_SEND_KERNEL 0
 #define SS_SEND_COPY_ENGINE 1
 int ss_set_send_mode(ss_cache* cache, int32_t mode, int32_t max_ctas);

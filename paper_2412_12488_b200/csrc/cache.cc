@@ -1683,32 +1683,42 @@ void ss_cache::LaunchDirectSendCE(ss_plan* plan, const PeerTarget& peer, Record*
     CudaCheck(cudaEventCreateWithFlags(&verdict_ev_, cudaEventDisableTiming), "event");
     CudaCheck(cudaEventCreateWithFlags(&ce_ev_, cudaEventDisableTiming), "event");
   }
-  // The plan's upload and the receiver's window open first (the plan's own
-  // upload event: the internal stream itself may be queued behind caller
-  // streams' compute by now, and the host waits for this validation).
-  CudaCheck(cudaStreamWaitEvent(verdict_stream_, plan->upload_ev, 0), "wait plan");
-  if (peer.local != nullptr) {
-    CudaCheck(cudaStreamWaitEvent(verdict_stream_, peer.local->window_ev_, 0), "wait window");
-  }
-  ValidateParams v{};
-  v.range_page = d.range_page;
-  v.range_begin = d.range_begin;
-  v.range_count = d.range_count;
-  v.n_ranges = d.n_ranges;
-  v.page_window = peer.page_window;
-  v.expecting = peer.expecting;
-  v.num_pages = peer.num_pages;
-  v.P = peer.P;
-  v.verdict = d.verdict;
-  v.status = nullptr;  // reported synchronously below
-  v.gen = NextLaunchGen();
-  launch_validate_remote(v, verdict_stream_);
-  D2H(h_pinned_, d.verdict, 2 * sizeof(int32_t), verdict_stream_, "D2H verdict");
-  CountLaunches(1);
-  CudaCheck(cudaStreamSynchronize(verdict_stream_), "verdict");
-  const int32_t* vh = reinterpret_cast<const int32_t*>(h_pinned_);
-  if (vh[1] == v.gen || vh[0] < 0) {
-    Throw(kUnknownAddress, "the receiver rejected the destination address");
+  // The address is validated once per plan, at its first copy-engine launch
+  // (the host takes the verdict: copies cannot be cancelled on the device).
+  // Later launches of the plan reuse the verdict — a per-launch host wait
+  // for a validation kernel would queue behind the compute occupying the
+  // SMs and stall the host's layer loop — so the receiver must keep the
+  // window open while the send is in flight (its counters still gate
+  // completion).
+  if (plan->ce_gen == 0) {
+    // The plan's upload and the receiver's window open first (the plan's
+    // own upload event: the internal stream itself may be queued behind
+    // caller streams' compute by now).
+    CudaCheck(cudaStreamWaitEvent(verdict_stream_, plan->upload_ev, 0), "wait plan");
+    if (peer.local != nullptr) {
+      CudaCheck(cudaStreamWaitEvent(verdict_stream_, peer.local->window_ev_, 0), "wait window");
+    }
+    ValidateParams v{};
+    v.range_page = d.range_page;
+    v.range_begin = d.range_begin;
+    v.range_count = d.range_count;
+    v.n_ranges = d.n_ranges;
+    v.page_window = peer.page_window;
+    v.expecting = peer.expecting;
+    v.num_pages = peer.num_pages;
+    v.P = peer.P;
+    v.verdict = d.verdict;
+    v.status = nullptr;  // reported synchronously below
+    v.gen = NextLaunchGen();
+    launch_validate_remote(v, verdict_stream_);
+    D2H(h_pinned_, d.verdict, 2 * sizeof(int32_t), verdict_stream_, "D2H verdict");
+    CountLaunches(1);
+    CudaCheck(cudaStreamSynchronize(verdict_stream_), "verdict");
+    const int32_t* vh = reinterpret_cast<const int32_t*>(h_pinned_);
+    if (vh[1] == v.gen || vh[0] < 0) {
+      Throw(kUnknownAddress, "the receiver rejected the destination address");
+    }
+    plan->ce_gen = v.gen;
   }
   // The batched copies need a non-legacy stream: they run on ce_stream_,
   // after `s`'s earlier work and the producer's event, and `s` continues
@@ -1764,7 +1774,7 @@ void ss_cache::LaunchDirectSendCE(ss_plan* plan, const PeerTarget& peer, Record*
   c.verdict = d.verdict;
   c.status = d_status_;
   c.sys_scope = (peer.device != device_ || force_sys_scope_) ? 1 : 0;
-  c.gen = v.gen;
+  c.gen = plan->ce_gen;
   c.no_data = 1;
   launch_copy_rows(c, s, num_sms_);
   CountLaunches(1);

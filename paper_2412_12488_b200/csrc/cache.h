@@ -190,6 +190,7 @@ struct ss_plan {
     int32_t src, dst, n;
   };
   std::vector<Run> ce_runs;
+  int32_t ce_gen = 0;  // launch generation of the plan's (one) copy-engine validation
   // Decode-attention plan (ss_begin_decode): context slot map in CSR form.
   bool is_decode_plan = false;
   int64_t batch = 0;
