@@ -137,6 +137,11 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_decode_attn(
   // (a device binary search here chained ~log2(segments) dependent loads
   // before the first KV byte could be requested).
   const int64_t lo = cta_seg[blockIdx.x];
+  // Launched as a programmatic dependent of the previous kernel on the
+  // stream: the plan reads above and the first piece's slot fetch overlap
+  // its tail; Q and the pool (which it may have written: the new token's
+  // K||V row, the query) are read only after griddepcontrol.wait.
+  bool waited = false;
   for (int64_t sgi = lo; t0 < t1 && sgi < n_seg; ++sgi) {
     const int64_t s_begin = seg_start[sgi], s_end = seg_start[sgi + 1];
     if (s_end <= t0) continue;  // empty segment
@@ -183,6 +188,16 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_decode_attn(
     // less per piece: short pieces, e.g. batch 1, are latency-bound).
     // Prologue: the first kStages - 1 tiles in flight.
     int32_t nxt = fetch_slot(warp);
+    if (!waited) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      // The combine kernel (a programmatic dependent) may launch now; it
+      // waits for this grid's completion before reading partials.  Not with
+      // the fused merge (large batches): the next call's CTAs would then be
+      // placed early, on whichever SMs have room, and run unbalanced
+      // (B=32 ctx 8K: 0.99 -> 0.88 of HBM).
+      if (seg_count == nullptr) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+      waited = true;
+    }
 #pragma unroll
     for (int pre = 0; pre < kStages - 1; ++pre) {
       const int t = warp + pre * kWarps;
@@ -496,6 +511,17 @@ __global__ void __launch_bounds__(kCombineThreads) k_decode_combine(
     const int64_t step = static_cast<int64_t>(G) * D;  // between consecutive pieces
     float acc0 = 0.f, acc1 = 0.f;
     int p = 0;
+    if (n > 32 && n <= 64) {  // up to 64 pieces: every load in flight at once
+      float v[64];
+#pragma unroll
+      for (int k = 0; k < 64; ++k) v[k] = k < n ? __ldcg(po + k * step) : 0.f;
+#pragma unroll
+      for (int k = 0; k < 64; k += 2) {
+        if (k < n) acc0 += cw[rr * n + k] * v[k];
+        if (k + 1 < n) acc1 += cw[rr * n + k + 1] * v[k + 1];
+      }
+      p = n;
+    }
     for (; p + 32 <= n; p += 32) {
       float v[32];
 #pragma unroll
@@ -559,16 +585,29 @@ bool launch_decode_attn(const void* pool_l, int64_t row_elems, const int32_t* sl
   auto q16 = static_cast<const __nv_bfloat16*>(q);
   auto pool16 = static_cast<const __nv_bfloat16*>(pool_l);
   auto out16 = static_cast<__nv_bfloat16*>(out);
-  if (D == 128) {
-    k_decode_attn<128><<<g, kWarps * 32, smem, s>>>(pool16, row_elems, slots, ctx_off, ctx_len,
-                                                    seg_start, n_seg, q16, Hq, Hkv, scale_log2,
-                                                    part_o, part_ml, out16, seg_count, cta_seg);
-  } else if (D == 64) {
-    k_decode_attn<64><<<g, kWarps * 32, smem, s>>>(pool16, row_elems, slots, ctx_off, ctx_len,
-                                                   seg_start, n_seg, q16, Hq, Hkv, scale_log2,
-                                                   part_o, part_ml, out16, seg_count, cta_seg);
-  } else {
-    return false;
+  {
+    void (*kern)(const __nv_bfloat16*, int64_t, const int32_t*, const int64_t*, const int32_t*,
+                 const int64_t*, int64_t, const __nv_bfloat16*, int, int, float, float*, float*,
+                 __nv_bfloat16*, uint32_t*, const int32_t*) = nullptr;
+    if (D == 128) kern = k_decode_attn<128>;
+    else if (D == 64) kern = k_decode_attn<64>;
+    else return false;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(g));
+    cfg.blockDim = dim3(kWarps * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+#ifndef DA_NO_PDL
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+#else
+    attr[0].val.programmaticStreamSerializationAllowed = 0;
+#endif
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, pool16, row_elems, slots, ctx_off, ctx_len, seg_start, n_seg, q16,
+                       Hq, Hkv, scale_log2, part_o, part_ml, out16, seg_count, cta_seg);
   }
   if (seg_count != nullptr) return true;  // pieces merged by the attention kernel
   // Few segments -> one query row per CTA (more parallel merge work); many

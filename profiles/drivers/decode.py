@@ -7,13 +7,22 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
+import json  # noqa: E402
+
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
+import paper_2412_12488_b200.kvcache as kc  # noqa: E402
+
+if "--lib" in sys.argv:  # A/B of a variant build
+    kc.PRODUCT_LIB = Path(sys.argv[sys.argv.index("--lib") + 1]).resolve()
 from paper_2412_12488_b200 import BatchEntry, KVCache  # noqa: E402
 
 HQ, HKV, HD, W = 64, 8, 128, 512
-peak = 6533.5
+try:
+    peak = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+except Exception:
+    peak = 6650.0
 cases = [(int(b), int(c)) for b, c in (x.split("x") for x in
          os.environ.get("CASES", "1x8192,8x8192,32x8192,128x4096,8x32768").split(","))]
 for B, ctx in cases:
