@@ -5,7 +5,7 @@ cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 rm -f paper_2412_12488_b200/_lib/obj/prefill_attn.cu.o
 MKV_NVCC_EXTRA="-DPF_PROF" python -c "from paper_2412_12488_b200 import build as b; b.build()" > /dev/null
-MICROKV_PREFILL_VARIANT=128 CASES=${CASES:-8192:6554} REPS=1 timeout 120 python profiles/drivers/prefill.py 2>&1 | tail -1
+CASES=${CASES:-8192:6554} REPS=1 timeout 120 python profiles/drivers/prefill.py 2>&1 | tail -1
 cat gpurun_out/pf_prof.txt
 rm -f paper_2412_12488_b200/_lib/obj/prefill_attn.cu.o
 python -c "from paper_2412_12488_b200 import build as b; b.build()" > /dev/null

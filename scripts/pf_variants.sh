@@ -1,7 +1,6 @@
 #!/bin/bash
-# Compile-time variants of the 128-key prefill kernel (MICROKV_PREFILL_VARIANT=3).
+# Compile-time variants of the 128-key prefill kernel.
 cd "$(dirname "$0")/.."
-export MICROKV_PREFILL_VARIANT=${VARIANT:-128}
 for v in "$@"; do
   rm -f paper_2412_12488_b200/_lib/obj/prefill_attn.cu.o
   MKV_NVCC_EXTRA="$v" python -c "from paper_2412_12488_b200 import build as b; b.build()" > /dev/null 2>&1

@@ -82,18 +82,6 @@ def test_prefill_matches_fp32_reference(cuda, case):
         assert rel.item() <= 2e-2, (case, layer, rel.item())
 
 
-@pytest.mark.parametrize("split", [1, 2, 3, 8])
-@pytest.mark.parametrize("case", [(64, 8, 1000, 800), (32, 4, 700, 683), (64, 8, 2048, 1536),
-                                  (64, 8, 300, 0)])
-def test_prefill_key_split_matches_fp32_reference(cuda, case, split, monkeypatch):
-    """Key-split launches (short balanced-PD tails: n_split CTAs per query
-    block over equal shares of its key tiles, merged by k_prefill_combine),
-    forced through MICROKV_PREFILL_SPLIT; clamped so every split has a key
-    tile (the 300-token case from position 0 cannot split)."""
-    monkeypatch.setenv("MICROKV_PREFILL_SPLIT", str(split))
-    test_prefill_matches_fp32_reference(cuda, case)
-
-
 @pytest.mark.parametrize("page_size", [8, 32, 64, 128, 256])
 def test_prefill_page_sizes(cuda, page_size):
     torch = cuda
@@ -176,15 +164,3 @@ def test_prefill_rejects_bad_arguments(cuda):
     with pytest.raises(SplitserveError):
         c.paged_prefill_attention_async(99, (0, 8), 0, 64, 8, 128, 0.1, q.data_ptr(),
                                         q.data_ptr(), 0)
-
-
-@pytest.mark.parametrize("variant", ["128p", "64", "128s", "2sm"])
-@pytest.mark.parametrize("case", CASES)
-def test_prefill_variants_match_fp32_reference(cuda, case, variant, monkeypatch):
-    """The other kernel layouts, selected per launch by MICROKV_PREFILL_VARIANT
-    (persistent CTAs over the work items, 64-key tiles with two S slots,
-    the split-row softmax, the CTA-pair cta_group::2 kernel): same numerics
-    bar (not the default,
-    they measured slower or equal)."""
-    monkeypatch.setenv("MICROKV_PREFILL_VARIANT", variant)
-    test_prefill_matches_fp32_reference(cuda, case)
