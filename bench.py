@@ -1394,7 +1394,8 @@ def measure_prefill(torch) -> dict:
     """tcgen05 paged causal prefill attention (70B heads: Hq=64, Hkv=8,
     D=128): the decode engine's tail prefill in balanced PD (queries
     [6554, 8192) over 8K keys, r = 0.2) and a full 8K prefill.  FLOPs =
-    4 * D * Hq * sum over queries of (position + 1)."""
+    4 * D * Hq * sum over queries of (position + 1).  Beside each, cuDNN
+    attention (torch SDPA, lower-right causal) on the same math."""
     from paper_2412_12488_b200 import BatchEntry, KVCache
 
     peak = _bf16_peak()
@@ -1428,9 +1429,40 @@ def measure_prefill(torch) -> dict:
         torch.cuda.synchronize()
         t = ev[0].elapsed_time(ev[1]) / 1e3 / reps
         flops = 4.0 * HD * HQ * sum(range(qb + 1, ctx + 1))
-        res[f"q{qb}-{ctx}_ctx{ctx}"] = {"us": round(1e6 * t, 1),
-                                        "tflops": round(flops / t / 1e12, 1),
-                                        "frac_bf16_peak": round(flops / t / 1e12 / peak, 4)}
+        entry = {"us": round(1e6 * t, 1), "tflops": round(flops / t / 1e12, 1),
+                 "frac_bf16_peak": round(flops / t / 1e12 / peak, 4)}
+        # The library baseline on the same math: cuDNN attention through torch
+        # SDPA, bottom-right causal (queries at the end of the keys), K/V
+        # contiguous (not paged) and expanded to the query heads.
+        try:
+            from torch.nn.attention import SDPBackend, sdpa_kernel
+            from torch.nn.attention.bias import causal_lower_right
+
+            qh = q.transpose(0, 1)[None]
+            kh = rows[:, 0].transpose(0, 1)[None].repeat_interleave(HQ // HKV, 1)
+            vh = rows[:, 1].transpose(0, 1)[None].repeat_interleave(HQ // HKV, 1)
+            bias = causal_lower_right(nq, ctx)
+
+            def lib():
+                with sdpa_kernel(SDPBackend.CUDNN_ATTENTION):
+                    return torch.nn.functional.scaled_dot_product_attention(qh, kh, vh, attn_mask=bias)
+            for _ in range(3):
+                lib()
+            torch.cuda.synchronize()
+            with torch.cuda.stream(s):
+                torch.cuda._sleep(20_000_000)
+                ev[0].record(s)
+                for _ in range(reps):
+                    lib()
+                ev[1].record(s)
+            torch.cuda.synchronize()
+            tl = ev[0].elapsed_time(ev[1]) / 1e3 / reps
+            entry["cudnn_sdpa_lower_right_us"] = round(1e6 * tl, 1)
+            entry["speedup_vs_cudnn"] = round(tl / t, 3)
+            del qh, kh, vh
+        except Exception as ex:  # noqa: BLE001
+            entry["cudnn_sdpa_lower_right"] = f"unavailable: {str(ex)[:120]}"
+        res[f"q{qb}-{ctx}_ctx{ctx}"] = entry
         del c, rows, q, o
         torch.cuda.empty_cache()
     res["peak_tflops"] = peak
