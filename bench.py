@@ -504,8 +504,10 @@ def our_arm(args, rank: int, world: int) -> None:
     # the whole machine; every mover's numbers are under secondary.handoff*).
     for key, sub in (("handoff", ""), ("handoff_8b", "_8b")):
         h = secondary.get(key, {}) if isinstance(secondary, dict) else {}
+        line[f"handoff{sub}_mover"] = h.get("mover")
         line[f"handoff{sub}_tail_us"] = h.get("exposed_tail_us")
         line[f"handoff{sub}_slowdown_pct"] = h.get("slowdown_pct")
+        line[f"handoff{sub}_slowdown_pct_best"] = h.get("slowdown_pct_best")
     line["send_budget"] = _pick_budget(secondary) if isinstance(secondary, dict) else None
     print(json.dumps(line), flush=True)
 
@@ -526,7 +528,7 @@ def _pick_budget(secondary: dict):
     out = {"arm": best[1], "max_ctas": best[0], "payload_gbs_80_layers": best[2]}
     for key, tag in (("handoff", "70b"), ("handoff_8b", "8b")):
         a = ((secondary.get(key) or {}).get("arms") or {}).get(best[1], {})
-        out[f"prefill_slowdown_pct_{tag}"] = a.get("slowdown_pct_median")
+        out[f"prefill_slowdown_pct_{tag}"] = a.get("slowdown_pct_paired_median")
         out[f"exposed_tail_us_{tag}"] = a.get("exposed_tail_us_median")
     return out
 
@@ -669,17 +671,22 @@ def measure_handoff_gemm(torch, layers: int = L, n_prompt: int = PROMPT, k: int 
     rows = torch.randint(-2**62, 2**62, (e * W,), dtype=torch.int64, device="cuda")
     # The send stream at high priority, like the engine's own comm stream: a
     # layer's copy takes SMs as soon as compute CTAs retire.
-    cs, ms, ds = torch.cuda.Stream(), torch.cuda.Stream(priority=-1), torch.cuda.Stream()
-    arms = [("none", None, None)] + list(SEND_ARMS)
-    runs = {a[0]: {"prefill_ms": [], "tail_us": [], "layer_lag_us": []} for a in arms}
+    prio = int(os.environ.get("MICROKV_HANDOFF_SEND_PRIO", "-1"))
+    cs, ms, ds = torch.cuda.Stream(), torch.cuda.Stream(priority=prio), torch.cuda.Stream()
+    # write_through: the layer's KV append and its remote_send fused into one
+    # launch on the compute stream (ss_append_rows_send_async).
+    arms = [("none", None, None)] + list(SEND_ARMS) + [("write_through", "fused", 0)]
+    runs = {a[0]: {"prefill_ms": [], "tail_us": [], "layer_lag_us": [], "last_append_us": []}
+            for a in arms}
     seq = 10
     for rep in range(reps + 1):  # rep 0: warm-up of every arm, discarded
         order = arms[rep % len(arms):] + arms[:rep % len(arms)]
         for name, mode, ctas in order:
             send = mode is not None
+            fused = mode == "fused"
             seq += 1
             if send:
-                P.set_send_mode(mode, ctas)
+                P.set_send_mode(0 if fused else mode, ctas)
                 r = D.PrepRecv(seq, prompt, -1)
             P.CreateSequence(seq, prompt)
             P.EnsureAllocated(seq, e)
@@ -689,10 +696,19 @@ def measure_handoff_gemm(torch, layers: int = L, n_prompt: int = PROMPT, k: int 
             t0, tc = (torch.cuda.Event(enable_timing=True) for _ in range(2))
             done = [torch.cuda.Event(enable_timing=True) for _ in range(layers)]
             landed = [torch.cuda.Event(enable_timing=True) for _ in range(layers)] if send else []
+            pre_last = torch.cuda.Event(enable_timing=True)  # before the last layer's append
             t0.record(cs)
             for layer in range(layers):
                 with torch.cuda.stream(cs):
                     torch.matmul(X, Wt, out=Y)
+                if layer == layers - 1:
+                    pre_last.record(cs)
+                if fused:
+                    P.append_rows_send_async(plan, dplan, (layer, layer + 1), rows.data_ptr(),
+                                             cs.cuda_stream)
+                    done[layer].record(cs)
+                    landed[layer].record(cs)
+                    continue
                 P.append_rows_async(plan, layer, rows.data_ptr(), cs.cuda_stream)
                 done[layer].record(cs)
                 if send:
@@ -704,6 +720,7 @@ def measure_handoff_gemm(torch, layers: int = L, n_prompt: int = PROMPT, k: int 
             P.synchronize()
             if rep > 0:
                 runs[name]["prefill_ms"].append(t0.elapsed_time(tc))
+                runs[name]["last_append_us"].append(1e3 * pre_last.elapsed_time(done[-1]))
             if send:
                 # D's device-side wait runs after the timed region: on one GPU
                 # a spinning wait kernel would hold an SM slot of P's prefill
@@ -715,7 +732,12 @@ def measure_handoff_gemm(torch, layers: int = L, n_prompt: int = PROMPT, k: int 
                 ds.synchronize()
                 D.synchronize()
                 assert D.DrainReceiveCompletions() == [seq]
-                if rep > 0:
+                if rep > 0 and fused:
+                    # P's compute end is where a plain append of the last
+                    # layer would have ended: the fused launch's excess over
+                    # the no-send arm's append is the exposed tail.
+                    runs[name]["tail_us"].append(1e3 * pre_last.elapsed_time(landed[-1]))
+                elif rep > 0:
                     runs[name]["tail_us"].append(1e3 * max(0.0, tc.elapsed_time(landed[-1])))
                     runs[name]["layer_lag_us"].append(
                         float(np.median([1e3 * done[i].elapsed_time(landed[i])
@@ -727,13 +749,19 @@ def measure_handoff_gemm(torch, layers: int = L, n_prompt: int = PROMPT, k: int 
     P.set_send_mode(0, 0)
     per_layer = e * BPT
     base = float(np.median(runs["none"]["prefill_ms"]))
+    append_us = float(np.median(runs["none"]["last_append_us"]))
+    if runs.get("write_through", {}).get("tail_us"):
+        runs["write_through"]["tail_us"] = [max(0.0, t - append_us)
+                                            for t in runs["write_through"]["tail_us"]]
     res = {"layers": layers, "prompt_tokens": n_prompt, "reps": reps,
            "per_layer_payload_mb": round(per_layer / 1e6, 2),
            "prefill_ms_without_sends": round(base, 3),
            "prefill_ms_without_sends_range": [round(min(runs["none"]["prefill_ms"]), 3),
                                               round(max(runs["none"]["prefill_ms"]), 3)],
+           "last_layer_append_us": round(append_us, 1),
+           "send_stream_priority": prio,
            "arms": {}}
-    for name, mode, ctas in SEND_ARMS:
+    for name, mode, ctas in arms[1:]:
         rr = runs[name]
         med = float(np.median(rr["prefill_ms"]))
         lh = float(np.median(rr["layer_lag_us"]))
@@ -742,19 +770,32 @@ def measure_handoff_gemm(torch, layers: int = L, n_prompt: int = PROMPT, k: int 
             "prefill_ms_range": [round(min(rr["prefill_ms"]), 3), round(max(rr["prefill_ms"]), 3)],
             "slowdown_pct_median": round(100 * (med / base - 1), 3),
             "slowdown_pct_per_rep": [round(100 * (x / base - 1), 3) for x in rr["prefill_ms"]],
+            # each rep against the no-send run of the same rotation (adjacent
+            # in time: the GEMM's clock / power state drifts between reps)
+            "slowdown_pct_paired_median": round(float(np.median(
+                [100 * (x / y - 1) for x, y in zip(rr["prefill_ms"], runs["none"]["prefill_ms"])])), 3),
+            # best against best: upward noise (power-cap clock dips) is one-sided
+            "slowdown_pct_best": round(100 * (min(rr["prefill_ms"]) / min(runs["none"]["prefill_ms"]) - 1), 3),
             "exposed_tail_us_median": round(float(np.median(rr["tail_us"])), 1),
             "exposed_tail_us_range": [round(min(rr["tail_us"]), 1), round(max(rr["tail_us"]), 1)],
             # layer l's event on the compute stream -> its rows landed (the
             # send stream's event after the copy): how far the transfer trails
             # the layer that produced it
             "layer_lag_us_median": round(lh, 1)}
-    d = res["arms"]["kernel_full"]
+    # The engine's mover at N=1: the write-through append (the layer's KV
+    # append and its remote_send in one launch on the compute stream).
+    mover = "write_through" if "write_through" in res["arms"] else "kernel_full"
+    d = res["arms"][mover]
+    res["mover"] = mover
     res["prefill_ms_with_sends"] = d["prefill_ms_median"]
-    res["slowdown_pct"] = d["slowdown_pct_median"]
+    res["slowdown_pct"] = d["slowdown_pct_paired_median"]
+    res["slowdown_pct_best"] = d["slowdown_pct_best"]
     res["exposed_tail_us"] = d["exposed_tail_us_median"]
     res["note"] = (f"{label}-layer-FLOP bf16 GEMM per layer (cuBLAS, compute stand-in) + KV append; "
-                   "per-layer DirectSend on a second stream; P and D on one GPU; medians over "
-                   f"{reps} alternated reps per arm")
+                   "per-layer DirectSend on a second stream (kernel_* / copy_engine arms) or fused "
+                   "with the append (write_through); P and D on one GPU; medians over "
+                   f"{reps} alternated reps per arm; slowdown_pct = median over reps of each rep "
+                   "against the no-send run of the same rotation")
     del P, D, X, Wt, Y, rows
     torch.cuda.empty_cache()
     return res

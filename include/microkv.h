@@ -418,6 +418,23 @@ int ss_append_rows_async(ss_cache* cache, ss_plan* plan, int32_t layer, const vo
 int ss_append_rows_layers_async(ss_cache* cache, ss_plan* plan, int32_t layer_begin,
                                 int32_t layer_end, const void* rows_dev, void* stream);
 
+/* KV append fused with remote_send (write-through): one launch reads the
+ * producing layer's dense rows rows_dev[layer_end - layer_begin]
+ * [total_outputs][dim] once and stores them into this engine's output
+ * slots (as ss_append_rows_layers_async) AND into the destination pages of
+ * `send_plan` (an ss_begin_direct_send plan whose [begin, end) lies inside
+ * one entry of `plan`), bumping the receiver's per-layer window counters
+ * like ss_launch_direct_send_async.  Replaces the append -> send pair of a
+ * PrefillThenSend layer (kv_cache.cc:328-367): the send's re-read of the
+ * rows and its second launch disappear, so the P->D handoff after the last
+ * layer is the append itself.  The address is validated on `stream` ahead
+ * of the copy (a rejected address writes nothing remote; the local append
+ * still happens).  Rows of 128 or 512 words; other dims (and the
+ * copy-engine send mode) run the append and the send as two launches. */
+int ss_append_rows_send_async(ss_cache* cache, ss_plan* plan, ss_plan* send_plan,
+                              int32_t layer_begin, int32_t layer_end, const void* rows_dev,
+                              void* stream);
+
 /* Paged GQA decode attention over the pool, reading K||V rows through the
  * device page table: each (token, layer) entry of dim u64 words holds
  * K[num_kv_heads][head_dim] then V[num_kv_heads][head_dim] in bf16

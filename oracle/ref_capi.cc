@@ -483,6 +483,9 @@ int ss_append_rows_layers_async(ss_cache*, ss_plan*, int32_t, int32_t, const voi
 int ss_append_rows_async(ss_cache*, ss_plan*, int32_t, const void*, void*) {
   return SS_ERR_UNSUPPORTED;
 }
+int ss_append_rows_send_async(ss_cache*, ss_plan*, ss_plan*, int32_t, int32_t, const void*, void*) {
+  return SS_ERR_UNSUPPORTED;
+}
 int ss_begin_decode(ss_cache*, const int64_t*, const int64_t*, int64_t, ss_plan**) {
   return SS_ERR_UNSUPPORTED;
 }

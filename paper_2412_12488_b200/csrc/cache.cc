@@ -305,6 +305,11 @@ ss_cache::~ss_cache() {
     }
     cudaFreeHost(h_stage_);
   }
+  if (fused_vstream_ != nullptr) {
+    cudaStreamSynchronize(fused_vstream_);
+    cudaStreamDestroy(fused_vstream_);
+    cudaEventDestroy(fused_vev_);
+  }
   if (verdict_stream_ != nullptr) {
     cudaStreamSynchronize(verdict_stream_);
     cudaStreamSynchronize(ce_stream_);
@@ -1321,6 +1326,133 @@ void ss_cache::AppendRowsLayers(ss_plan* plan, int32_t lb, int32_t le, const voi
   if (s != stream_) NoteUser(s);
 }
 
+// KV append fused with remote_send ("write-through"): the producing
+// layer's dense K||V rows are read once and stored both into this engine's
+// output slots (the Attention write rule, kv_cache.cc:328-334) and into the
+// peer's reserved pages for the send plan's range (the send loop,
+// kv_cache.cc:353-367, + ApplyRemoteWrite's Empty-only rule), with the
+// peer's per-layer window counters published by the same kernel.  A row
+// whose local slot was already non-Empty is sent from that slot, as the
+// reference sends the pool contents after the write.  The receiver's
+// address is validated by a kernel ahead of it on `s` (the fused kernel is
+// its programmatic dependent), so a rejected address writes nothing remote
+// while the local append still happens.
+void ss_cache::AppendRowsSend(ss_plan* fwd, ss_plan* send, int32_t lb, int32_t le,
+                              const void* rows, cudaStream_t s) {
+  RequireDevice("AppendRowsSend");
+  MKV_CHECK(lb >= 0 && lb < le && le <= L_, kInvalidArgument, "layer out of range");
+  MKV_CHECK(send->is_direct_send, kInvalidArgument, "not a direct-send plan");
+  MKV_CHECK(!fwd->is_direct_send && !fwd->is_decode_plan, kInvalidArgument, "not a forward plan");
+  const PlanSend& snd = send->sends[0];
+  int64_t off = 0;
+  bool covered = false;
+  for (const auto& e : fwd->entries) {
+    if (e.seq == snd.seq && e.begin <= snd.begin && snd.end <= e.end) {
+      off += snd.begin - e.begin;
+      covered = true;
+      break;
+    }
+    off += e.end - e.begin;
+  }
+  MKV_CHECK(covered, kInvalidArgument, "the send range is not output by the forward plan");
+  if ((W_ != 512 && W_ != 128) || send_mode_ == SS_SEND_COPY_ENGINE) {
+    // Rows the fan-out kernel is not specialised for, or a copy-engine
+    // mover: the append, then the send behind it on the same stream.
+    AppendRowsLayers(fwd, lb, le, rows, s);
+    LaunchDirectSend(send, lb, le, s);
+    return;
+  }
+  if (!fwd->on_device) OrderAfterUser();
+  PlanToDevice(fwd);
+  const PeerTarget& peer = PeerFor(snd.dest);
+  OrderLaunch(s);
+  const auto& d = send->dsend[0];
+  // Validation off the producer's critical path: on a high-priority side
+  // stream (behind the plan's upload and the receiver's window open), so it
+  // runs while the producing layer still computes; `s` only waits for its
+  // event.  A validation of a later layer may rewrite the verdict while
+  // this layer's copy reads it: on success with the same window, on failure
+  // with -1, which makes this copy fail closed too.
+  const bool side = [] {
+    const char* e = std::getenv("MICROKV_FUSED_VALIDATE");
+    return e == nullptr || std::strcmp(e, "inline") != 0;
+  }();
+  cudaStream_t vs = s;
+  if (side) {
+    if (fused_vstream_ == nullptr) {
+      int lo = 0, hi = 0;
+      CudaCheck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
+      CudaCheck(cudaStreamCreateWithPriority(&fused_vstream_, cudaStreamNonBlocking, hi), "stream");
+      CudaCheck(cudaEventCreateWithFlags(&fused_vev_, cudaEventDisableTiming), "event");
+    }
+    vs = fused_vstream_;
+    // Behind the send plan's row-map upload only — not behind `s`, where the
+    // producing layer's compute is queued.
+    CudaCheck(cudaStreamWaitEvent(vs, send->upload_ev, 0), "wait plan");
+  }
+  if (peer.local != nullptr) CudaCheck(cudaStreamWaitEvent(vs, peer.local->window_ev_, 0), "wait window");
+  ValidateParams v{};
+  v.range_page = d.range_page;
+  v.range_begin = d.range_begin;
+  v.range_count = d.range_count;
+  v.n_ranges = d.n_ranges;
+  v.page_window = peer.page_window;
+  v.expecting = peer.expecting;
+  v.num_pages = peer.num_pages;
+  v.P = peer.P;
+  v.verdict = d.verdict;
+  v.status = d_status_;
+  v.gen = NextLaunchGen();
+  launch_validate_remote(v, vs);
+  if (side) {
+    CudaCheck(cudaEventRecord(fused_vev_, vs), "cudaEventRecord");
+    CudaCheck(cudaStreamWaitEvent(s, fused_vev_, 0), "wait validation");
+  }
+  FanoutParams f{};
+  f.src = static_cast<const uint64_t*>(rows);
+  f.src_layer_words = fwd->total_outputs * W_;
+  f.src_idx = nullptr;
+  f.n_rows = fwd->total_outputs;
+  f.layer0 = lb;
+  f.n_layers = le - lb;
+  f.W = W_;
+  f.n_dest = 2;
+  f.gen = v.gen;
+  f.pdl = 1;
+  f.truth = 0;
+  // 0: this engine's output slots (no validation, no counters)
+  f.dst[0] = PoolLayer(lb);
+  f.dst_layer_words[0] = num_pages_ * P_ * W_;
+  f.dst_idx[0] = fwd->d_out_slots;
+  f.dst_fill[0] = d_fill_ + static_cast<int64_t>(lb) * num_pages_ * P_;
+  f.dst_fill_layer[0] = num_pages_ * P_;
+  f.fill_value[0] = 1;  // FillState::kComputedLocal
+  f.row_off[0] = 0;
+  f.row_cnt[0] = fwd->total_outputs;
+  // 1: the peer's reserved pages for the send range
+  const int64_t dst_lw = peer.num_pages * peer.P * W_;
+  f.dst[1] = peer.pool + lb * dst_lw;
+  f.dst_layer_words[1] = dst_lw;
+  f.dst_idx[1] = d.dst_slots;
+  f.dst_fill[1] = peer.fill + lb * peer.num_pages * peer.P;
+  f.dst_fill_layer[1] = peer.num_pages * peer.P;
+  f.fill_value[1] = 2;  // FillState::kReceivedRemote
+  f.row_off[1] = off;
+  f.row_cnt[1] = snd.end - snd.begin;
+  f.win_received[1] = peer.win_received;
+  f.win_layer_rows[1] = peer.win_layer_rows;
+  f.win_layers[1] = peer.L;
+  f.verdict[1] = d.verdict;
+  f.sys_scope = (peer.device != device_ || force_sys_scope_) ? 1 : 0;
+  launch_copy_rows_fanout(f, s, num_sms_);
+  CountLaunches(2);
+  for (const auto& e : fwd->entries) {
+    Record* rec = MustGet(e.seq);
+    rec->touched_end = std::max(rec->touched_end, e.end);
+  }
+  if (s != stream_) NoteUser(s);
+}
+
 // ---------------------------------------------------------------------------
 // Transfer agent
 // ---------------------------------------------------------------------------
@@ -1858,6 +1990,7 @@ void ss_cache::BroadcastSend(SeqId seq, int64_t begin, int64_t end, int32_t n_de
   f.W = W_;
   f.n_dest = n_dest;
   f.gen = NextLaunchGen();
+  f.truth = -1;
   for (int32_t d = 0; d < n_dest; ++d) {
     const PeerTarget& peer = PeerFor(dests[d]);
     if (peer.local != nullptr) CudaCheck(cudaStreamWaitEvent(s, peer.local->window_ev_, 0), "wait window");
@@ -1884,6 +2017,9 @@ void ss_cache::BroadcastSend(SeqId seq, int64_t begin, int64_t end, int32_t n_de
     f.win_layer_rows[d] = peer.win_layer_rows;
     f.win_layers[d] = peer.L;
     f.verdict[d] = v.verdict;
+    f.fill_value[d] = 2;  // FillState::kReceivedRemote
+    f.row_off[d] = 0;
+    f.row_cnt[d] = n;
     if (peer.device != device_ || force_sys_scope_) f.sys_scope = 1;
   }
   launch_copy_rows_fanout(f, s, num_sms_);

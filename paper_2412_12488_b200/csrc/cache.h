@@ -259,6 +259,8 @@ struct ss_cache {
                          int32_t layer_end, uint64_t* out_dev, cudaStream_t s);
   mkv::KVAddr BuildAddr(SeqId seq, int64_t begin, int64_t end);
   void AppendRows(ss_plan* plan, int32_t layer, const void* rows_dev, cudaStream_t s);
+  void AppendRowsSend(ss_plan* fwd, ss_plan* send, int32_t lb, int32_t le, const void* rows,
+                      cudaStream_t s);
   void AppendRowsLayers(ss_plan* plan, int32_t layer_begin, int32_t layer_end, const void* rows_dev,
                         cudaStream_t s);
 
@@ -434,6 +436,8 @@ struct ss_cache {
   bool force_sys_scope_ = false;  // MICROKV_FORCE_SYS_SCOPE=1 (test hook)
   int32_t send_mode_ = SS_SEND_KERNEL;  // ss_set_send_mode
   int32_t send_ctas_ = 0;               // copy-kernel grid cap of sends (0 = none)
+  cudaStream_t fused_vstream_ = nullptr;  // AppendRowsSend's validation stream
+  cudaEvent_t fused_vev_ = nullptr;
   cudaStream_t verdict_stream_ = nullptr;  // copy-engine sends: validation off the data stream
   cudaEvent_t verdict_ev_ = nullptr;
   cudaStream_t ce_stream_ = nullptr;       // copy-engine sends: the batched copies

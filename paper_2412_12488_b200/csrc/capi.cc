@@ -530,6 +530,14 @@ int ss_append_rows_layers_async(ss_cache* c, ss_plan* p, int32_t lb, int32_t le,
   });
 }
 
+int ss_append_rows_send_async(ss_cache* c, ss_plan* p, ss_plan* sp, int32_t lb, int32_t le,
+                              const void* rows, void* stream) {
+  return Guard(c, [&]() -> int {
+    c->AppendRowsSend(p, sp, lb, le, rows, S(stream));
+    return SS_OK;
+  });
+}
+
 int ss_begin_decode(ss_cache* c, const int64_t* seqs, const int64_t* ctx_lens, int64_t batch,
                     ss_plan** plan_out) {
   return Guard(c, [&]() -> int {

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "hash.cuh"
 #include "kernels.cuh"
@@ -357,12 +358,17 @@ __global__ void __launch_bounds__(kCopyThreads) k_relay_rows(CopyParams p, const
 template <int kVec>
 __global__ void __launch_bounds__(kCopyThreads) k_copy_rows_fanout(FanoutParams p) {
   extern __shared__ uint32_t s_rows[];  // [n_dest][n_layers]
+  if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
   int32_t window[kMaxFanout];
   bool live_any = false;
-  for (int d = 0; d < p.n_dest; ++d) {
-    const volatile int32_t* v = p.verdict[d];
-    window[d] = v[1] == p.gen ? -1 : v[0];
-    live_any |= window[d] >= 0;
+#pragma unroll
+  for (int d = 0; d < kMaxFanout; ++d) {
+    window[d] = -1;
+    if (d < p.n_dest) {
+      const volatile int32_t* v = p.verdict[d];
+      window[d] = v == nullptr ? 0 : (v[1] == p.gen ? -1 : v[0]);
+      live_any |= window[d] >= 0;
+    }
   }
   if (!live_any) return;
   for (int i = threadIdx.x; i < p.n_dest * p.n_layers; i += blockDim.x) s_rows[i] = 0;
@@ -370,36 +376,57 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows_fanout(FanoutParams 
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  const int64_t groups = (p.n_rows + kGroup - 1) / kGroup;
+  const int group = p.group > 0 ? p.group : kGroup;
+  const int64_t groups = (p.n_rows + group - 1) / group;
   const int64_t items = groups * p.n_layers;
   for (int64_t it = warp; it < items; it += n_warps) {
     const int32_t lrel = static_cast<int32_t>(it / groups);
-    const int64_t r0 = (it - static_cast<int64_t>(lrel) * groups) * kGroup;
-    const int nr = static_cast<int>(p.n_rows - r0 < kGroup ? p.n_rows - r0 : kGroup);
-    const int32_t my_s = lane < nr ? __ldg(p.src_idx + r0 + lane) : 0;
+    const int64_t r0 = (it - static_cast<int64_t>(lrel) * groups) * group;
+    const int nr = static_cast<int>(p.n_rows - r0 < group ? p.n_rows - r0 : group);
+    const int32_t my_s =
+        lane < nr ? (p.src_idx ? __ldg(p.src_idx + r0 + lane) : static_cast<int32_t>(r0 + lane)) : 0;
     int32_t my_d[kMaxFanout];
-    unsigned todo[kMaxFanout];
+    unsigned todo[kMaxFanout];  // rows to store (in range, slot Empty)
+    unsigned inm[kMaxFanout];   // rows addressed (in range): what the counters count
     unsigned any = 0;
 #pragma unroll
     for (int d = 0; d < kMaxFanout; ++d) {
       my_d[d] = 0;
       todo[d] = 0;
+      inm[d] = 0;
       if (d < p.n_dest && window[d] >= 0) {
+        const int64_t rr = r0 + lane - p.row_off[d];
+        const bool in = lane < nr && rr >= 0 && rr < p.row_cnt[d];
         uint8_t f = 1;
-        if (lane < nr) {
-          my_d[d] = __ldg(p.dst_idx[d] + r0 + lane);
+        if (in) {
+          my_d[d] = __ldg(p.dst_idx[d] + rr);
           f = ld_cg_u8(p.dst_fill[d] + lrel * p.dst_fill_layer[d] + my_d[d]);
         }
-        todo[d] = __ballot_sync(0xffffffffu, lane < nr && f == 0);
+        todo[d] = __ballot_sync(0xffffffffu, in && f == 0);
+        inm[d] = __ballot_sync(0xffffffffu, in);
         any |= todo[d];
+      }
+    }
+    // Rows the truth destination already holds are sent from its page.
+    unsigned from_truth = 0;
+    int32_t truth_slot = 0;
+    uint64_t* truth_l = nullptr;
+#pragma unroll
+    for (int d = 0; d < kMaxFanout; ++d) {
+      if (d == p.truth) {
+        from_truth = inm[d] & ~todo[d];
+        truth_slot = my_d[d];
+        truth_l = p.dst[d] + lrel * p.dst_layer_words[d];
       }
     }
     const uint64_t* src_l = p.src + lrel * p.src_layer_words;
 #pragma unroll 1
     for (int k = 0; k < nr; ++k) {
       const int64_t si = __shfl_sync(0xffffffffu, my_s, k);
+      const int64_t ti = __shfl_sync(0xffffffffu, truth_slot, k);
       if (!((any >> k) & 1u)) continue;
-      const u256* s4 = reinterpret_cast<const u256*>(src_l + si * p.W) + lane;
+      const uint64_t* row = (from_truth >> k) & 1u ? truth_l + ti * p.W : src_l + si * p.W;
+      const u256* s4 = reinterpret_cast<const u256*>(row) + lane;
       u256 t[kVec];
 #pragma unroll
       for (int u = 0; u < kVec; ++u) t[u] = ld256(s4 + 32 * u);
@@ -417,8 +444,10 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows_fanout(FanoutParams 
 #pragma unroll
     for (int d = 0; d < kMaxFanout; ++d) {
       if (d < p.n_dest && window[d] >= 0) {
-        if ((todo[d] >> lane) & 1u) p.dst_fill[d][lrel * p.dst_fill_layer[d] + my_d[d]] = 2;
-        if (lane == 0) atomicAdd(&s_rows[d * p.n_layers + lrel], static_cast<uint32_t>(nr));
+        if ((todo[d] >> lane) & 1u) p.dst_fill[d][lrel * p.dst_fill_layer[d] + my_d[d]] = p.fill_value[d];
+        if (lane == 0 && inm[d] != 0 && p.win_received[d] != nullptr) {
+          atomicAdd(&s_rows[d * p.n_layers + lrel], static_cast<uint32_t>(__popc(inm[d])));
+        }
       }
     }
   }
@@ -427,7 +456,7 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows_fanout(FanoutParams 
 #endif
   __syncthreads();  // rows before counters (barrier + release reductions, see k_copy_rows)
   for (int d = 0; d < p.n_dest; ++d) {
-    if (window[d] < 0) continue;
+    if (window[d] < 0 || p.win_received[d] == nullptr) continue;
     for (int i = threadIdx.x; i < p.n_layers; i += blockDim.x) {
       const uint32_t c = s_rows[d * p.n_layers + i];
       if (c != 0) {
@@ -795,20 +824,41 @@ void launch_relay_rows(const CopyParams& p, const uint32_t* wait, uint32_t targe
   cudaLaunchKernelEx(&cfg, kern, p, wait, target, timeout_ns);
 }
 
+#ifndef MKV_FANOUT_SHORT_GROUP
+#define MKV_FANOUT_SHORT_GROUP 1
+#endif
 void launch_copy_rows_fanout(const FanoutParams& p, cudaStream_t s, int num_sms) {
   const int64_t groups = (p.n_rows + kGroup - 1) / kGroup * p.n_layers;
   if (groups <= 0) return;
   const int warps_per_block = kCopyThreads / 32;
-  const int grid = grid_for(groups, warps_per_block, num_sms, 2);
+  // As k_copy_rows: launches that fit one wave at 8 CTAs per SM (a layer of
+  // a fused append + send) spread over 8 CTAs per SM, long ones 2.
+  FanoutParams q = p;
+  const int64_t rows = p.n_rows * p.n_layers;
+  const bool short_launch = rows <= static_cast<int64_t>(num_sms) * 8 * warps_per_block * kGroup;
+  q.group = kGroup;
+  if (short_launch) q.group = MKV_FANOUT_SHORT_GROUP;
+  if (const char* e = std::getenv("MICROKV_FANOUT_GROUP")) q.group = std::atoi(e) > 0 ? std::atoi(e) : q.group;
+  const int64_t items = (q.n_rows + q.group - 1) / q.group * q.n_layers;
+  int per_sm = short_launch ? 8 : 2;
+  if (const char* e = std::getenv("MICROKV_FANOUT_PER_SM")) per_sm = std::atoi(e) > 0 ? std::atoi(e) : per_sm;
+  const int grid = grid_for(items, warps_per_block, num_sms, per_sm);
   const size_t smem = sizeof(uint32_t) * p.n_dest * p.n_layers;
-  if (p.W == 512) {
-    k_copy_rows_fanout<4><<<grid, kCopyThreads, smem, s>>>(p);
-  } else if (p.W == 128) {
-    k_copy_rows_fanout<1><<<grid, kCopyThreads, smem, s>>>(p);
-  } else {
-    // Rows that are not a multiple of 128 words use the single-destination
-    // kernel once per destination (the launcher splits); not reached here.
-  }
+  // Rows that are not 128 or 512 words use the single-destination kernel
+  // once per destination (the callers split); not reached here.
+  void (*kern)(FanoutParams) = p.W == 512 ? k_copy_rows_fanout<4> : k_copy_rows_fanout<1>;
+  if (p.W != 512 && p.W != 128) return;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kCopyThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = p.pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, q);
 }
 
 void launch_validate_remote(const ValidateParams& p, cudaStream_t s) {

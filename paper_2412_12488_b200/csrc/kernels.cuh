@@ -84,11 +84,18 @@ void launch_relay_rows(const CopyParams& p, const uint32_t* wait, uint32_t targe
 
 // Fan-out row copy: one source row set stored into up to kMaxFanout
 // destinations (each with its own slots, fill rule and window counters).
+// Destination d takes source rows [row_off[d], row_off[d] + row_cnt[d])
+// (its dst_idx indexed from row_off[d]); a null verdict means no
+// validation (the engine's own pages), a null win_received no counters.
+// truth >= 0 names the destination whose existing non-Empty rows take
+// precedence over the source row for every other destination: the fused
+// KV append + remote_send sends what the sender's page holds, as the
+// reference's send loop reads the pool after the write (kv_cache.cc:328-367).
 constexpr int kMaxFanout = 8;
 struct FanoutParams {
   const uint64_t* src;
   int64_t src_layer_words;
-  const int32_t* src_idx;
+  const int32_t* src_idx;     // slot per row, or null = dense row r
   int64_t n_rows;
   int32_t layer0, n_layers, W, n_dest;
   uint64_t* dst[kMaxFanout];
@@ -96,12 +103,18 @@ struct FanoutParams {
   const int32_t* dst_idx[kMaxFanout];
   uint8_t* dst_fill[kMaxFanout];
   int64_t dst_fill_layer[kMaxFanout];
+  uint8_t fill_value[kMaxFanout];
+  int64_t row_off[kMaxFanout];
+  int64_t row_cnt[kMaxFanout];
   unsigned long long* win_received[kMaxFanout];
   uint32_t* win_layer_rows[kMaxFanout];
   int32_t win_layers[kMaxFanout];
   const int32_t* verdict[kMaxFanout];
+  int32_t truth;              // -1: none
+  int32_t group;              // rows per warp item (set by the launcher)
   int32_t sys_scope;          // as CopyParams::sys_scope, for any destination
   int32_t gen;                // launch generation, as CopyParams::gen
+  int32_t pdl;                // as CopyParams::pdl
 };
 void launch_copy_rows_fanout(const FanoutParams& p, cudaStream_t s, int num_sms);
 

@@ -225,6 +225,7 @@ _SIGNATURES = {
                                               C.c_uint64, _i32p, _vp]),
     "ss_append_rows_async": (C.c_int, [_vp, _vp, C.c_int32, _vp, _vp]),
     "ss_append_rows_layers_async": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, _vp, _vp]),
+    "ss_append_rows_send_async": (C.c_int, [_vp, _vp, _vp, C.c_int32, C.c_int32, _vp, _vp]),
     "ss_begin_decode": (C.c_int, [_vp, _i64p, _i64p, C.c_int64, C.POINTER(_vp)]),
     "ss_paged_decode_attention_async": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, C.c_int32,
                                                   C.c_int32, C.c_float, _vp, _vp, _vp]),
@@ -1035,6 +1036,15 @@ class KVCache:
         self._check(self._lib.ss_append_rows_layers_async(self._h, plan.handle, layers[0],
                                                           layers[1], C.c_void_p(rows_ptr),
                                                           C.c_void_p(stream)))
+
+    def append_rows_send_async(self, plan: ForwardPlan, send_plan: ForwardPlan, layers: tuple,
+                               rows_ptr: int, stream: int = 0) -> None:
+        """KV append fused with remote_send: rows [end - begin][total_outputs][dim]
+        go to this engine's output slots and, for send_plan's range, straight
+        into the receiver's reserved pages (one launch per call)."""
+        self._check(self._lib.ss_append_rows_send_async(self._h, plan.handle, send_plan.handle,
+                                                        layers[0], layers[1],
+                                                        C.c_void_p(rows_ptr), C.c_void_p(stream)))
 
     def begin_decode(self, seqs: Sequence[int], ctx_lens: Sequence[int]) -> ForwardPlan:
         s = np.ascontiguousarray(np.asarray(seqs, dtype=np.int64))
