@@ -21,7 +21,7 @@ INCLUDE = HERE.parent / "include"
 CUDA_HOME = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 
 HOST_SRCS = ["radix_tree.cc", "cache.cc", "wire.cc", "frames.cc", "capi.cc"]
-CUDA_SRCS = ["kernels.cu", "decode_attn.cu", "prefill_attn.cu", "crc32.cu"]
+CUDA_SRCS = ["kernels.cu", "decode_attn.cu", "decode_pages.cu", "prefill_attn.cu", "crc32.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

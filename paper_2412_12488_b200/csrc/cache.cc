@@ -1005,23 +1005,27 @@ void ss_cache::FreePlanDevice(ss_plan* plan) {
     cudaFree(plan->dev.ptr);
     plan->dev = DevBlock{};
   }
-  if (plan->d_partial) {
+  if (plan->d_partial || plan->d_chunks) {
     cudaDeviceSynchronize();
-    cudaFree(plan->d_partial);
+    if (plan->d_partial) cudaFree(plan->d_partial);
+    if (plan->d_chunks) cudaFree(plan->d_chunks);
     plan->d_partial = nullptr;
+    plan->d_chunks = nullptr;
+    plan->pages_ready = false;
   }
 }
 
 void ss_cache::DestroyPlan(ss_plan* plan) {
   live_plans_.erase(plan);
   if (plan->upload_ev != nullptr) cudaEventDestroy(plan->upload_ev);
-  if (device_ >= 0 && (plan->dev.ptr || plan->d_partial)) {
+  if (device_ >= 0 && (plan->dev.ptr || plan->d_partial || plan->d_chunks)) {
     cudaSetDevice(device_);
     OrderAfterUser();
     DevFree(plan->dev, stream_);
-    if (plan->d_partial) {
+    if (plan->d_partial || plan->d_chunks) {
       Sync();
-      cudaFree(plan->d_partial);
+      if (plan->d_partial) cudaFree(plan->d_partial);
+      if (plan->d_chunks) cudaFree(plan->d_chunks);
     }
   }
   delete plan;
@@ -2393,6 +2397,27 @@ ss_plan* ss_cache::BeginDecode(const int64_t* seqs, const int64_t* ctx_lens, int
   plan->batch = batch;
   plan->max_ctx = max_ctx;
   plan->ctx_lens = len;
+  // Page chunks for decode_pages.cu: maximal runs of consecutive slots, at
+  // most 16 positions.  A page's positions are consecutive slots, so the
+  // run check is one comparison per page, not per position.
+  for (int64_t b = 0; b < batch; ++b) {
+    const std::vector<int32_t>& sl = MustGet(seqs[b])->slots;
+    const int64_t n = len[b];
+    for (int64_t pos = 0; pos < n;) {
+      const int32_t s0 = sl[pos];
+      int64_t k = std::min<int64_t>({16, n - pos, static_cast<int64_t>(P_) - s0 % P_});
+      if (sl[pos + k - 1] != s0 + k - 1) {  // not one run (never for a fresh page): per position
+        k = 1;
+        while (k < 16 && pos + k < n && sl[pos + k] == s0 + k) ++k;
+      } else {  // extend into the next page when it is the next slot block
+        while (k < 16 && pos + k < n && sl[pos + k] == s0 + k) ++k;
+      }
+      plan->chunks.insert(plan->chunks.end(),
+                          {s0, static_cast<int32_t>(pos), static_cast<int32_t>(k),
+                           static_cast<int32_t>(b)});
+      pos += k;
+    }
+  }
   OrderAfterUser();
   plan->dev = DevAlloc(total, stream_);
   uint8_t* base = static_cast<uint8_t*>(plan->dev.ptr);
@@ -2433,6 +2458,13 @@ void ss_cache::DecodeAttention(ss_plan* plan, int32_t layer, int32_t hq, int32_t
   MKV_CHECK(hd == 64 || hd == 128, kInvalidArgument, "head_dim must be 64 or 128");
   MKV_CHECK(static_cast<int64_t>(W_) * 8 == 4LL * hkv * hd, kInvalidArgument,
             "entry width must equal K||V bf16 bytes (dim * 8 == 4 * num_kv_heads * head_dim)");
+  if (decode_pages_supported(hq, hkv, hd, W_) && [] {
+        const char* e = std::getenv("MICROKV_DECODE_KERNEL");
+        return e == nullptr || std::strcmp(e, "v1") != 0;
+      }()) {
+    DecodeAttentionPages(plan, layer, hq, hkv, scale, q, out, s);
+    return;
+  }
   if (plan->decode_grid == 0 || plan->decode_hkv != hkv || plan->decode_hq != hq ||
       plan->decode_hd != hd) {
     // Tile prefix sums over segments (batch, kv head) for the stream-K split,
@@ -2515,6 +2547,70 @@ void ss_cache::DecodeAttention(ss_plan* plan, int32_t layer, int32_t hq, int32_t
                                      use_kernel ? nullptr : plan->d_seg_count, plan->d_cta_seg, s);
   MKV_CHECK(ok, kInvalidArgument, "unsupported head_dim");
   CountLaunches(use_kernel ? 2 : 1);
+  if (s != stream_) NoteUser(s);
+}
+
+// Page-chunk decode attention (decode_pages.cu) for 4 KiB K||V rows of 8 KV
+// heads x 128: the chunks' equal split over one CTA per SM, per-context
+// piece tables and partial storage built once per plan.
+void ss_cache::DecodeAttentionPages(ss_plan* plan, int32_t layer, int32_t hq, int32_t hkv,
+                                    float scale, const void* q, void* out, cudaStream_t s) {
+  if (!tmap_chunk_ready_) {
+    if (!make_pool_tensor_map(d_pool_, L_, num_pages_ * P_, W_, 16,
+                              reinterpret_cast<PoolTensorMap*>(tmap_chunk_)))
+      mkv::ThrowStatus(SS_ERR_CUDA, "cuTensorMapEncodeTiled failed for the pool");
+    tmap_chunk_ready_ = true;
+  }
+  const int64_t T = static_cast<int64_t>(plan->chunks.size() / 4);
+  if (!plan->pages_ready || plan->decode_hq != hq) {
+    const int grid = decode_pages_grid(num_sms_, T);
+    const int64_t B = plan->batch;
+    std::vector<int32_t> first(B, -1), count(B, 0);
+    for (int64_t c = 0; c < grid; ++c) {
+      const int64_t j0 = c * T / grid, j1 = (c + 1) * T / grid;
+      int32_t last_b = -1;
+      for (int64_t j = j0; j < j1; ++j) {
+        const int32_t b = plan->chunks[4 * j + 3];
+        if (b == last_b) continue;
+        last_b = b;
+        if (first[b] < 0) first[b] = static_cast<int32_t>(c);
+        ++count[b];
+      }
+    }
+    bool split = false;
+    for (int64_t b = 0; b < B; ++b) split |= count[b] > 1;
+    const int64_t G = hq / hkv;
+    const int64_t pieces = grid + B;
+    const size_t b_ch = Align(sizeof(int32_t) * plan->chunks.size());
+    const size_t b_tab = Align(sizeof(int32_t) * B);
+    const size_t b_o = Align(sizeof(float) * pieces * hkv * G * 128);
+    const size_t b_ml = Align(sizeof(float) * pieces * hkv * G * 2);
+    OrderAfterUser();
+    Sync();
+    if (plan->d_chunks) cudaFree(plan->d_chunks);
+    uint8_t* buf = nullptr;
+    CudaCheck(cudaMalloc(&buf, b_ch + 2 * b_tab + b_o + b_ml), "cudaMalloc decode chunks");
+    plan->d_chunks = reinterpret_cast<int32_t*>(buf);
+    plan->d_piece_first = reinterpret_cast<int32_t*>(buf + b_ch);
+    plan->d_piece_count = reinterpret_cast<int32_t*>(buf + b_ch + b_tab);
+    plan->d_pages_part = reinterpret_cast<float*>(buf + b_ch + 2 * b_tab);
+    plan->d_pages_ml = reinterpret_cast<float*>(buf + b_ch + 2 * b_tab + b_o);
+    H2D(plan->d_chunks, plan->chunks.data(), sizeof(int32_t) * plan->chunks.size(), stream_,
+        "H2D decode chunks");
+    H2D(plan->d_piece_first, first.data(), sizeof(int32_t) * B, stream_, "H2D pieces");
+    H2D(plan->d_piece_count, count.data(), sizeof(int32_t) * B, stream_, "H2D pieces");
+    plan->pages_grid = grid;
+    plan->pages_split = split;
+    plan->pages_ready = true;
+    plan->decode_hq = hq;
+  }
+  OrderLaunch(s);
+  const int nl = launch_decode_pages(
+      *reinterpret_cast<const PoolTensorMap*>(tmap_chunk_), layer,
+      reinterpret_cast<const int4*>(plan->d_chunks), T, plan->d_piece_first, plan->d_piece_count,
+      plan->pages_split, q, static_cast<int>(plan->batch), hq, hkv, scale, plan->d_pages_part,
+      plan->d_pages_ml, out, plan->pages_grid, s);
+  CountLaunches(nl);
   if (s != stream_) NoteUser(s);
 }
 

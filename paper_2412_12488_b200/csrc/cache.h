@@ -207,6 +207,17 @@ struct ss_plan {
   int64_t total_tiles = 0;
   int32_t decode_hkv = 0, decode_hq = 0, decode_hd = 0;
   int32_t decode_grid = 0;
+  // Page-chunk decode (decode_pages.cu): runs of <= 16 consecutive slots
+  // {slot0, tok0, n, b} in batch order, built by BeginDecode; uploaded with
+  // the per-context piece tables on first use.
+  std::vector<int32_t> chunks;  // 4 ints per chunk
+  bool pages_ready = false, pages_split = false;
+  int32_t pages_grid = 0;
+  int32_t* d_chunks = nullptr;  // int4 per chunk, then piece_first[batch], piece_count[batch]
+  int32_t* d_piece_first = nullptr;
+  int32_t* d_piece_count = nullptr;
+  float* d_pages_part = nullptr;
+  float* d_pages_ml = nullptr;
 };
 
 namespace mkv {
@@ -324,6 +335,8 @@ struct ss_cache {
   void PrefillAttention(int64_t seq, int64_t q_begin, int64_t q_end, int32_t layer, int32_t hq,
                         int32_t hkv, int32_t hd, float scale, const void* q, void* out,
                         cudaStream_t s);
+  void DecodeAttentionPages(ss_plan* plan, int32_t layer, int32_t hq, int32_t hkv, float scale,
+                            const void* q, void* out, cudaStream_t s);
   void DecodeAttention(ss_plan* plan, int32_t layer, int32_t hq, int32_t hkv, int32_t hd,
                        float scale, const void* q, void* out, cudaStream_t s);
   // Wire formats (frames.cc): CRC-32 of device bytes; a KV write frame of
@@ -515,4 +528,6 @@ struct ss_cache {
   // built on first use (mkv::PoolTensorMap layout).
   alignas(64) unsigned char tmap_page_[128] = {}, tmap_row_[128] = {};
   bool tmaps_ready_ = false;
+  alignas(64) unsigned char tmap_chunk_[128] = {};  // {64, 16, 1} boxes for decode chunks
+  bool tmap_chunk_ready_ = false;
 };

@@ -986,6 +986,7 @@ void preload_kernels() {
   cudaFuncGetAttributes(&a, k_wait_counter);
   cudaFuncGetAttributes(&a, k_wait_counter32);
   preload_decode_attn_kernels();
+  preload_decode_pages_kernels();
   preload_prefill_attn_kernels();
   preload_crc32_kernels();
   cudaGetLastError();

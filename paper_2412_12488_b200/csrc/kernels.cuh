@@ -203,6 +203,20 @@ bool launch_decode_attn(const void* pool_l, int64_t row_elems, const int32_t* sl
                         int grid, uint32_t* seg_count, const int32_t* cta_seg,
                         cudaStream_t s);
 
+// Paged GQA decode attention with TMA page-chunk loads (decode_pages.cu):
+// 8 KV heads x head_dim 128 (4 KiB rows), up to 8 query heads per KV head.
+// chunks: int4 {slot0, tok0, n, b} runs of <= 16 consecutive slots in batch
+// order; the grid (decode_pages_grid) splits them into equal ranges;
+// piece_first / piece_count per context: the CTAs its chunks span.
+struct PoolTensorMap;
+bool decode_pages_supported(int Hq, int Hkv, int D, int64_t row_u64);
+int decode_pages_grid(int num_sms, int64_t n_chunks);
+int launch_decode_pages(const PoolTensorMap& map, int layer, const int4* chunks, int64_t n_chunks,
+                        const int32_t* piece_first, const int32_t* piece_count, bool any_split,
+                        const void* q, int batch, int Hq, int Hkv, float scale, float* part_o,
+                        float* part_ml, void* out, int grid, cudaStream_t s);
+void preload_decode_pages_kernels();
+
 // Paged causal GQA prefill attention on tcgen05 (prefill_attn.cu): queries
 // [q_pos0, q_pos0 + n_q) of one sequence over keys [0, q_pos0 + n_q).  K/V
 // come by TMA through two tensor maps of the whole pool viewed as bf16

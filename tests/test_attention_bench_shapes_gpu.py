@@ -73,10 +73,13 @@ def test_decode_bench_shapes(cuda, batch, ctx, monkeypatch):
     q = (torch.randn(batch, HQ, HD, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
     scale = HD ** -0.5
     refs = [_decode_ref(torch, q, rows, b, ctx, scale) for b in range(batch)]
+    # The default (TMA page-chunk kernel), then k_decode_attn with each merge.
     for combine in ("auto", "kernel", "fused"):
         if combine == "auto":
             monkeypatch.delenv("MICROKV_DECODE_COMBINE", raising=False)
+            monkeypatch.delenv("MICROKV_DECODE_KERNEL", raising=False)
         else:
+            monkeypatch.setenv("MICROKV_DECODE_KERNEL", "v1")
             monkeypatch.setenv("MICROKV_DECODE_COMBINE", combine)
         out = torch.full_like(q, float("nan"))
         c.paged_decode_attention_async(plan, 0, HQ, HKV, HD, scale, q.data_ptr(), out.data_ptr(), 0)

@@ -52,14 +52,17 @@ def _ref(torch, q, K, V, scale):
     return torch.einsum("hn,nhd->hd", p, Vx)
 
 
-@pytest.mark.parametrize("combine", ["auto", "kernel", "fused"])
+@pytest.mark.parametrize("combine", ["auto", "v1-kernel", "v1-fused"])
 @pytest.mark.parametrize("shape", SHAPES)
 def test_decode_matches_fp32_reference(cuda, shape, combine, monkeypatch):
-    """Split segments merged by the separate combine kernel or by the
-    attention kernel's last arriving CTA (MICROKV_DECODE_COMBINE), and the
-    automatic choice: same tolerance."""
+    """The default kernel for the shape (the TMA page-chunk kernel for 8 KV
+    heads x 128, decode_pages.cu; k_decode_attn otherwise), and k_decode_attn
+    forced (MICROKV_DECODE_KERNEL=v1) with its split segments merged by the
+    separate combine kernel or by the attention kernel's last arriving CTA
+    (MICROKV_DECODE_COMBINE): same tolerance."""
     if combine != "auto":
-        monkeypatch.setenv("MICROKV_DECODE_COMBINE", combine)
+        monkeypatch.setenv("MICROKV_DECODE_KERNEL", "v1")
+        monkeypatch.setenv("MICROKV_DECODE_COMBINE", combine.split("-")[1])
     torch = cuda
     hq, hkv, hd = shape
     W = 4 * hkv * hd // 8
