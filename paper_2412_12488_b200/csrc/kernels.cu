@@ -825,7 +825,7 @@ void launch_relay_rows(const CopyParams& p, const uint32_t* wait, uint32_t targe
 }
 
 #ifndef MKV_FANOUT_SHORT_GROUP
-#define MKV_FANOUT_SHORT_GROUP 1
+#define MKV_FANOUT_SHORT_GROUP 4
 #endif
 void launch_copy_rows_fanout(const FanoutParams& p, cudaStream_t s, int num_sms) {
   const int64_t groups = (p.n_rows + kGroup - 1) / kGroup * p.n_layers;
