@@ -143,7 +143,10 @@ struct PagesArgs {
   float scale_log2;
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
+// 112 registers (no spills): with the combine kernel's 121 x 256 a combine
+// CTA fits beside a main CTA, so the programmatic-dependent combine is
+// resident and waiting when the main grid drains (118 registers left no room).
+__global__ void __maxnreg__(112)
     k_decode_pages(const __grid_constant__ CUtensorMap map, const PagesArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &

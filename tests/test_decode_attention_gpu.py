@@ -116,3 +116,54 @@ def test_decode_rejects_bad_geometry_and_missing_kv(cuda):
     with pytest.raises(SplitserveError) as ei:  # 4*Hkv*D bytes must equal the entry width
         c.paged_decode_attention_async(d, 0, 64, 4, 128, 0.1, q.data_ptr(), q.data_ptr(), 0)
     assert ei.value.code == ErrorCode.InvalidArgument
+
+
+@pytest.mark.parametrize("kernel", ["auto", "v1"])
+def test_decode_over_forked_contexts(cuda, kernel, monkeypatch):
+    """Contexts that share a parent's pages (ForkSequence at a position inside
+    a page, kv_cache.cc:120-166): the child's positions [0, 21) live in the
+    parent's first two pages and [21, n) start at slot 0 of the child's own
+    pages (fork-relative paging), so the decode kernels see runs of
+    consecutive slots that end mid-page.  Both kernels, fp32 reference."""
+    if kernel == "v1":
+        monkeypatch.setenv("MICROKV_DECODE_KERNEL", "v1")
+    torch = cuda
+    hq, hkv, hd = 64, 8, 128
+    W = 4 * hkv * hd // 8
+    c = KVCache(num_pages=200, page_size=16, layers=1, dim=W, device=0)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    parent = [(7 * i) % 251 for i in range(37)]
+    c.CreateSequence(1, parent)
+    c.EnsureAllocated(1, 37)
+    pr = (torch.randn(37, 2, hkv, hd, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    plan = c.BeginForward([BatchEntry(1, (0, 37))])
+    c.append_rows_async(plan, 0, pr.data_ptr(), 0)
+    torch.cuda.synchronize()
+    plan.close()
+    kv = {1: (pr[:, 0].float(), pr[:, 1].float())}
+    for child, fork, n in ((2, 21, 300), (3, 5, 40), (4, 37, 37 + 16 * 3 + 1)):
+        toks = parent[:fork] + [(3 * i + child) % 251 for i in range(n - fork)]
+        c.ForkSequence(1, child, fork, toks)
+        c.EnsureAllocated(child, n)
+        rows = (torch.randn(n - fork, 2, hkv, hd, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+        plan = c.BeginForward([BatchEntry(child, (fork, n))])
+        c.append_rows_async(plan, 0, rows.data_ptr(), 0)
+        torch.cuda.synchronize()
+        plan.close()
+        kv[child] = (torch.cat([pr[:fork, 0].float(), rows[:, 0].float()]),
+                     torch.cat([pr[:fork, 1].float(), rows[:, 1].float()]))
+    seqs = [1, 2, 3, 4]
+    lens = [kv[s][0].shape[0] for s in seqs]
+    dplan = c.begin_decode(seqs, lens)
+    q = (torch.randn(len(seqs), hq, hd, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    out = torch.empty_like(q)
+    scale = hd ** -0.5
+    c.paged_decode_attention_async(dplan, 0, hq, hkv, hd, scale, q.data_ptr(), out.data_ptr(), 0)
+    torch.cuda.synchronize()
+    for b, s in enumerate(seqs):
+        ref = _ref(torch, q[b], kv[s][0], kv[s][1], scale)
+        err = (out[b].float() - ref).abs()
+        assert err.max().item() <= 2e-2, (kernel, s, err.max().item())
+        rel = (out[b].float() - ref).pow(2).mean().sqrt() / ref.pow(2).mean().sqrt()
+        assert rel.item() <= 2e-2, (kernel, s, rel.item())
+    dplan.close()
