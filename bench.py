@@ -502,7 +502,7 @@ def our_arm(args, rank: int, world: int) -> None:
     }
     # The handoff half of the metric, top level (70B and 8B, kernel mover on
     # the whole machine; every mover's numbers are under secondary.handoff*).
-    for key, sub in (("handoff", ""), ("handoff_8b", "_8b")):
+    for key, sub in (("handoff", ""), ("handoff_8b", "_8b"), ("handoff_layer_order", "_layer_order")):
         h = secondary.get(key, {}) if isinstance(secondary, dict) else {}
         line[f"handoff{sub}_mover"] = h.get("mover")
         line[f"handoff{sub}_tail_us"] = h.get("exposed_tail_us")
@@ -590,6 +590,11 @@ def secondary_measurements(P, D, prompt, torch) -> dict:
         out["handoff_8b"] = measure_handoff_gemm(torch, 32, 4096, 4096, 53248, "8B", reps=9)
     except Exception as ex:
         out["handoff_8b"] = {"error": str(ex)}
+    try:  # the same 70B stand-in with the layer's K||V produced by its first 20% of FLOPs
+        out["handoff_layer_order"] = measure_handoff_gemm(
+            torch, kv_share=0.2, arm_names=("kernel_full", "kernel_32ctas", "write_through"))
+    except Exception as ex:
+        out["handoff_layer_order"] = {"error": str(ex)}
     try:
         out["send_modes"] = measure_send_modes(torch)
     except Exception as ex:
@@ -639,7 +644,8 @@ SEND_ARMS = (("kernel_full", 0, 0), ("kernel_64ctas", 0, 64), ("kernel_32ctas", 
 
 
 def measure_handoff_gemm(torch, layers: int = L, n_prompt: int = PROMPT, k: int = 8192,
-                         n: int = 104448, label: str = "70B", reps: int = 5) -> dict:
+                         n: int = 104448, label: str = "70B", reps: int = 5,
+                         kv_share: float = 0.0, arm_names=None) -> dict:
     """1P1D PrefillThenSend with a compute-bound prefill stand-in: per layer
     one bf16 GEMM of a Llama layer's FLOPs at the prompt length (70B:
     X[8191, 8192] @ W[8192, 104448], ~14 TFLOP), then the layer's K||V rows
@@ -655,7 +661,15 @@ def measure_handoff_gemm(torch, layers: int = L, n_prompt: int = PROMPT, k: int 
     reps of P's prefill time, the slowdown against the no-send median, the
     exposed tail (P's last-layer compute end -> the last layer's rows and
     window counters landed in D) and the per-layer lag (layer l's event ->
-    its rows landed)."""
+    its rows landed).
+
+    kv_share > 0 splits each layer's GEMM the way a transformer layer is
+    ordered: the first kv_share of its FLOPs (the QKV projection, which
+    produces the layer's K||V rows) before the KV append and send, the rest
+    (attention output projection + MLP) after it, so the send of layer l
+    overlaps layer l's own remaining compute ("sending a
+    layer's KV right after its computation").  kv_share = 0 appends after
+    the whole layer: the conservative bound."""
     from paper_2412_12488_b200 import BatchEntry, KVCache
 
     rng = np.random.Generator(np.random.MT19937(4))
@@ -666,8 +680,11 @@ def measure_handoff_gemm(torch, layers: int = L, n_prompt: int = PROMPT, k: int 
     D = KVCache(num_pages=pages, page_size=PAGE, layers=layers, dim=W, device=0, rank=1)
     P.attach_peer(1, D)
     X = torch.randn(e, k, device="cuda", dtype=torch.bfloat16)
-    Wt = torch.randn(k, n, device="cuda", dtype=torch.bfloat16) * 0.01
-    Y = torch.empty(e, n, device="cuda", dtype=torch.bfloat16)
+    na = int(round(n * kv_share / 128)) * 128
+    Wt = torch.randn(k, n - na, device="cuda", dtype=torch.bfloat16) * 0.01
+    Y = torch.empty(e, n - na, device="cuda", dtype=torch.bfloat16)
+    Wa = torch.randn(k, na, device="cuda", dtype=torch.bfloat16) * 0.01 if na else None
+    Ya = torch.empty(e, na, device="cuda", dtype=torch.bfloat16) if na else None
     rows = torch.randint(-2**62, 2**62, (e * W,), dtype=torch.int64, device="cuda")
     # The send stream at high priority, like the engine's own comm stream: a
     # layer's copy takes SMs as soon as compute CTAs retire.
@@ -676,6 +693,8 @@ def measure_handoff_gemm(torch, layers: int = L, n_prompt: int = PROMPT, k: int 
     # write_through: the layer's KV append and its remote_send fused into one
     # launch on the compute stream (ss_append_rows_send_async).
     arms = [("none", None, None)] + list(SEND_ARMS) + [("write_through", "fused", 0)]
+    if arm_names is not None:
+        arms = [a for a in arms if a[0] == "none" or a[0] in arm_names]
     runs = {a[0]: {"prefill_ms": [], "tail_us": [], "layer_lag_us": [], "last_append_us": []}
             for a in arms}
     seq = 10
@@ -700,7 +719,7 @@ def measure_handoff_gemm(torch, layers: int = L, n_prompt: int = PROMPT, k: int 
             t0.record(cs)
             for layer in range(layers):
                 with torch.cuda.stream(cs):
-                    torch.matmul(X, Wt, out=Y)
+                    torch.matmul(X, Wa if na else Wt, out=Ya if na else Y)
                 if layer == layers - 1:
                     pre_last.record(cs)
                 if fused:
@@ -708,13 +727,16 @@ def measure_handoff_gemm(torch, layers: int = L, n_prompt: int = PROMPT, k: int 
                                              cs.cuda_stream)
                     done[layer].record(cs)
                     landed[layer].record(cs)
-                    continue
-                P.append_rows_async(plan, layer, rows.data_ptr(), cs.cuda_stream)
-                done[layer].record(cs)
-                if send:
-                    P.launch_direct_send_after_async(dplan, (layer, layer + 1),
-                                                     done[layer].cuda_event, ms.cuda_stream)
-                    landed[layer].record(ms)
+                else:
+                    P.append_rows_async(plan, layer, rows.data_ptr(), cs.cuda_stream)
+                    done[layer].record(cs)
+                    if send:
+                        P.launch_direct_send_after_async(dplan, (layer, layer + 1),
+                                                         done[layer].cuda_event, ms.cuda_stream)
+                        landed[layer].record(ms)
+                if na:  # the rest of the layer behind its KV (output projection + MLP)
+                    with torch.cuda.stream(cs):
+                        torch.matmul(X, Wt, out=Y)
             tc.record(cs)
             torch.cuda.synchronize()
             P.synchronize()
@@ -732,7 +754,7 @@ def measure_handoff_gemm(torch, layers: int = L, n_prompt: int = PROMPT, k: int 
                 ds.synchronize()
                 D.synchronize()
                 assert D.DrainReceiveCompletions() == [seq]
-                if rep > 0 and fused:
+                if rep > 0 and fused and not na:
                     # P's compute end is where a plain append of the last
                     # layer would have ended: the fused launch's excess over
                     # the no-send arm's append is the exposed tail.
@@ -750,10 +772,10 @@ def measure_handoff_gemm(torch, layers: int = L, n_prompt: int = PROMPT, k: int 
     per_layer = e * BPT
     base = float(np.median(runs["none"]["prefill_ms"]))
     append_us = float(np.median(runs["none"]["last_append_us"]))
-    if runs.get("write_through", {}).get("tail_us"):
+    if runs.get("write_through", {}).get("tail_us") and not na:
         runs["write_through"]["tail_us"] = [max(0.0, t - append_us)
                                             for t in runs["write_through"]["tail_us"]]
-    res = {"layers": layers, "prompt_tokens": n_prompt, "reps": reps,
+    res = {"layers": layers, "prompt_tokens": n_prompt, "reps": reps, "kv_share": kv_share,
            "per_layer_payload_mb": round(per_layer / 1e6, 2),
            "prefill_ms_without_sends": round(base, 3),
            "prefill_ms_without_sends_range": [round(min(runs["none"]["prefill_ms"]), 3),
@@ -764,7 +786,7 @@ def measure_handoff_gemm(torch, layers: int = L, n_prompt: int = PROMPT, k: int 
     for name, mode, ctas in arms[1:]:
         rr = runs[name]
         med = float(np.median(rr["prefill_ms"]))
-        lh = float(np.median(rr["layer_lag_us"]))
+        lh = float(np.median(rr["layer_lag_us"])) if rr["layer_lag_us"] else 0.0
         res["arms"][name] = {
             "prefill_ms_median": round(med, 3),
             "prefill_ms_range": [round(min(rr["prefill_ms"]), 3), round(max(rr["prefill_ms"]), 3)],
@@ -796,7 +818,7 @@ def measure_handoff_gemm(torch, layers: int = L, n_prompt: int = PROMPT, k: int 
                    "with the append (write_through); P and D on one GPU; medians over "
                    f"{reps} alternated reps per arm; slowdown_pct = median over reps of each rep "
                    "against the no-send run of the same rotation")
-    del P, D, X, Wt, Y, rows
+    del P, D, X, Wt, Y, Wa, Ya, rows
     torch.cuda.empty_cache()
     return res
 
