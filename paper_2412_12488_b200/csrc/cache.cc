@@ -1790,9 +1790,9 @@ void ss_cache::SetSendMode(int32_t mode, int32_t max_ctas) {
 
 // Copy-engine DirectSend.  Validation runs on a side stream (not behind the
 // data stream's earlier copies) and the host takes the verdict, so a
-// rejected address writes nothing; the rows then move as one batch of 3-D
-// copies on `s` — one per row run, its depth the layer range, the pools'
-// layer stride as the slice pitch — and k_copy_rows in no-data mode marks
+// rejected address writes nothing; the rows then move as 2-D copies on the
+// copy-engine stream — one per row run, its height the layer range, the
+// pools' layer stride as the pitch — and k_copy_rows in no-data mode marks
 // the fill states and publishes the window counters behind them.
 void ss_cache::LaunchDirectSendCE(ss_plan* plan, const PeerTarget& peer, Record* rec, int32_t lb,
                                   int32_t le, cudaStream_t s, cudaEvent_t after) {
@@ -1856,7 +1856,7 @@ void ss_cache::LaunchDirectSendCE(ss_plan* plan, const PeerTarget& peer, Record*
     }
     plan->ce_gen = v.gen;
   }
-  // The batched copies need a non-legacy stream: they run on ce_stream_,
+  // The copies run on ce_stream_ (the copy-engine stream),
   // after `s`'s earlier work and the producer's event, and `s` continues
   // after them.
   CudaCheck(cudaEventRecord(verdict_ev_, s), "cudaEventRecord");
@@ -1866,26 +1866,15 @@ void ss_cache::LaunchDirectSendCE(ss_plan* plan, const PeerTarget& peer, Record*
   const size_t row_b = static_cast<size_t>(W_) * 8;
   const size_t src_lb = static_cast<size_t>(num_pages_) * P_ * row_b;
   const size_t dst_lb = static_cast<size_t>(peer.num_pages) * peer.P * row_b;
-  std::vector<cudaMemcpy3DBatchOp> ops(plan->ce_runs.size());
-  for (size_t i = 0; i < ops.size(); ++i) {
-    const auto& r = plan->ce_runs[i];
-    cudaMemcpy3DBatchOp& o = ops[i];
-    o = cudaMemcpy3DBatchOp{};
-    o.src.type = cudaMemcpyOperandTypePointer;
-    o.src.op.ptr.ptr = reinterpret_cast<uint8_t*>(d_pool_) + lb * src_lb + r.src * row_b;
-    o.src.op.ptr.rowLength = src_lb;  // bytes: one "row" of the 3-D view per layer
-    o.src.op.ptr.layerHeight = 1;
-    o.dst.type = cudaMemcpyOperandTypePointer;
-    o.dst.op.ptr.ptr = reinterpret_cast<uint8_t*>(peer.pool) + lb * dst_lb + r.dst * row_b;
-    o.dst.op.ptr.rowLength = dst_lb;
-    o.dst.op.ptr.layerHeight = 1;
-    o.extent = make_cudaExtent(r.n * row_b, 1, nl);
-    o.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  }
-  if (!ops.empty()) {
-    size_t fail = 0;
-    CudaCheck(cudaMemcpy3DBatchAsync(ops.size(), ops.data(), &fail, 0, ce_stream_),
-              "cudaMemcpy3DBatchAsync");
+  // One strided copy per row run: the run's bytes in every layer of
+  // [lb, le), layer pitch on both sides (a 2-D copy the copy engines take
+  // as one descriptor).
+  for (const auto& r : plan->ce_runs) {
+    CudaCheck(cudaMemcpy2DAsync(reinterpret_cast<uint8_t*>(peer.pool) + lb * dst_lb + r.dst * row_b,
+                                dst_lb,
+                                reinterpret_cast<const uint8_t*>(d_pool_) + lb * src_lb + r.src * row_b,
+                                src_lb, r.n * row_b, nl, cudaMemcpyDeviceToDevice, ce_stream_),
+              "cudaMemcpy2DAsync");
   }
   CudaCheck(cudaEventRecord(ce_ev_, ce_stream_), "cudaEventRecord");
   CudaCheck(cudaStreamWaitEvent(s, ce_ev_, 0), "wait copies");
