@@ -1509,8 +1509,11 @@ def measure_prefill(torch) -> dict:
             def lib():
                 with sdpa_kernel(SDPBackend.CUDNN_ATTENTION):
                     return torch.nn.functional.scaled_dot_product_attention(qh, kh, vh, attn_mask=bias)
-            for _ in range(3):
-                lib()
+            # Warm-up on the timed stream itself: cuDNN builds and caches its
+            # execution plan per handle, and torch keeps a handle per stream.
+            with torch.cuda.stream(s):
+                for _ in range(3):
+                    lib()
             torch.cuda.synchronize()
             with torch.cuda.stream(s):
                 torch.cuda._sleep(20_000_000)

@@ -1,11 +1,16 @@
 #!/bin/bash
-# Per-warp phase sums of the prefill softmax (build with -DPF_PROF): wait for S,
-# S load, row max, P half 1 (+rescale, store), P half 2 (+store), clk.
+# Per-warp phase sums of the prefill kernel (-DPF_PROF): cycles waiting for S,
+# loading S from TMEM, row max, first / second half of P, for the heaviest
+# CTA of each KV head; one line per softmax warp (gpurun_out/pf_prof*.txt).
 cd "$(dirname "$0")/.."
-mkdir -p gpurun_out
-rm -f paper_2412_12488_b200/_lib/obj/prefill_attn.cu.o
-MKV_NVCC_EXTRA="-DPF_PROF" python -c "from paper_2412_12488_b200 import build as b; b.build()" > /dev/null
-CASES=${CASES:-8192:6554} REPS=1 timeout 120 python profiles/drivers/prefill.py 2>&1 | tail -1
-cat gpurun_out/pf_prof.txt
+CASE=${CASE:-8192:0}
+for v in "$@"; do
+  rm -f paper_2412_12488_b200/_lib/obj/prefill_attn.cu.o
+  MKV_NVCC_EXTRA="-DPF_PROF $v" python -c "from paper_2412_12488_b200 import build as b; b.build()" > /dev/null 2>&1
+  CASES=$CASE REPS=1 timeout 120 python profiles/drivers/prefill.py > /dev/null 2>&1
+  tag=$(echo "$v" | tr -c 'A-Za-z0-9=' '_')
+  mv gpurun_out/pf_prof.txt "gpurun_out/pf_prof_${tag}.txt"
+  echo "variant [$v]"; head -8 "gpurun_out/pf_prof_${tag}.txt"
+done
 rm -f paper_2412_12488_b200/_lib/obj/prefill_attn.cu.o
 python -c "from paper_2412_12488_b200 import build as b; b.build()" > /dev/null
