@@ -23,6 +23,15 @@ namespace {
 constexpr int32_t kMaxWindows = 4096;
 constexpr int32_t kMaxSeqRows = 16384;
 constexpr uint32_t kIpcMagic = 0x4d4b5631;  // "MKV1"
+// Destination addresses up to this many page slots are validated inside the
+// copy grid (one launch); MICROKV_INLINE_VALIDATE_SLOTS overrides (0 = never).
+int64_t InlineValidateSlots() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("MICROKV_INLINE_VALIDATE_SLOTS");
+    return e != nullptr ? std::atoll(e) : int64_t{2048};
+  }();
+  return v;
+}
 
 const char* kCodeNames[] = {"OutOfPages",      "DuplicateSequence", "UnknownSequence",
                             "ForkBeyondCommitted", "AddrMismatch",  "MissingKV",
@@ -1059,7 +1068,12 @@ void ss_cache::LaunchRemote(const PeerTarget& peer, const int32_t* d_src_slots,
   v.verdict = d_verdict;
   v.status = d_status_;
   v.gen = NextLaunchGen();
-  launch_validate_remote(v, s);
+  // Small addresses (a few pages): each copy CTA validates the address
+  // itself, one launch instead of validation + copy (a 16-token migration
+  // is launch-bound).  Larger ones: a validation grid ahead of the producer,
+  // the copy a programmatic dependent of it.
+  const bool inline_validate = n_ranges * peer.P <= InlineValidateSlots();
+  if (!inline_validate) launch_validate_remote(v, s);
   // Validation ahead of the producer: only the copy waits for its writes.
   if (after != nullptr) CudaCheck(cudaStreamWaitEvent(s, after, 0), "wait producer");
   CopyParams c{};
@@ -1086,8 +1100,10 @@ void ss_cache::LaunchRemote(const PeerTarget& peer, const int32_t* d_src_slots,
   c.pdl = after == nullptr ? 1 : 0;  // overlaps the copy grid's launch with the validation
   c.gen = v.gen;
   c.max_ctas = send_ctas_;
+  c.inline_validate = inline_validate ? 1 : 0;
+  c.val = v;
   launch_copy_rows(c, s, num_sms_);
-  CountLaunches(2);
+  CountLaunches(inline_validate ? 1 : 2);
 }
 
 // kv_cache.cc:308-371 on device.  Hidden buffers are device pointers; the

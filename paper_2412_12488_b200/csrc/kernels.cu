@@ -122,7 +122,11 @@ __device__ __forceinline__ void warp_copy_row(const uint64_t* __restrict__ src,
 #ifndef MKV_GROUP
 #define MKV_GROUP 4
 #endif
-constexpr int kGroup = MKV_GROUP;  // rows per item for long launches (1 for launches within one wave)
+constexpr int kGroup = MKV_GROUP;
+#ifndef MKV_SMALL_SEND_ROWS
+#define MKV_SMALL_SEND_ROWS 2048
+#endif
+constexpr int64_t kSmallSendRows = MKV_SMALL_SEND_ROWS;  // rows per item for long launches (1 for launches within one wave)
 
 // kVec > 0: rows are exactly kVec 32-byte vectors per lane (W = 128*kVec
 // words), fully unrolled; kVec == 0: any W.
@@ -140,6 +144,46 @@ __device__ __forceinline__ void copy_row(const uint64_t* __restrict__ src, uint6
   } else {
     warp_copy_row(src, dst, W, lane);
   }
+}
+
+// The checks of k_validate_remote by one CTA over the whole address (small
+// sends): returns the window id, or -1 when the address is rejected; CTA 0
+// records the verdict / status as the validation grid would.  Every thread
+// of the CTA must call it (CTA barrier inside).
+__device__ int32_t validate_in_cta(const ValidateParams& p) {
+  int32_t w0 = -1;
+  bool bad = p.n_ranges <= 0;
+  if (p.n_ranges > 0) {
+    const int64_t pg0 = p.range_page[0];
+    if (pg0 < 0 || pg0 >= p.num_pages) {
+      bad = true;
+    } else {
+      w0 = *reinterpret_cast<const volatile int32_t*>(p.page_window + pg0);
+      if (w0 < 0) bad = true;
+    }
+  }
+  const int64_t work = p.n_ranges * p.P;
+  for (int64_t i = threadIdx.x; !bad && i < work; i += blockDim.x) {
+    const int64_t r = i / p.P;
+    const int32_t k = static_cast<int32_t>(i % p.P);
+    const int64_t pg = p.range_page[r];
+    const int32_t b = p.range_begin[r], c = p.range_count[r];
+    if (pg < 0 || pg >= p.num_pages || b < 0 || c < 0 || b + c > p.P) {
+      bad = true;
+    } else if (k < c) {
+      if (k == 0 && *reinterpret_cast<const volatile int32_t*>(p.page_window + pg) != w0) bad = true;
+      if (reinterpret_cast<const volatile uint8_t*>(p.expecting)[pg * p.P + b + k] == 0) bad = true;
+    }
+  }
+  bad = __syncthreads_or(bad) != 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    p.verdict[0] = w0;
+    if (bad) {
+      *reinterpret_cast<volatile int32_t*>(p.verdict + 1) = p.gen;
+      if (p.status != nullptr) atomicOr(p.status, kStatusUnknownAddress);
+    }
+  }
+  return bad ? -1 : w0;
 }
 
 template <int kVec>
@@ -174,7 +218,10 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   }
   int32_t window = -1;
-  if (p.verdict != nullptr) {
+  if (p.inline_validate) {
+    window = validate_in_cta(p.val);
+    if (window < 0) return;  // rejected: no writes, no counts (uniform over the CTA)
+  } else if (p.verdict != nullptr) {
     window = reinterpret_cast<const volatile int32_t*>(p.verdict)[1] == p.gen
                  ? -1
                  : reinterpret_cast<const volatile int32_t*>(p.verdict)[0];
@@ -773,7 +820,10 @@ void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms) {
   // plain copies (append / gather: +10%), 4-row items for sends that publish
   // window counters (a quarter of the CTAs pay the publication: one 70B
   // layer 25.6 -> 19.5 us).
-  const int short_group = p.win_received != nullptr ? 4 : MKV_SHORT_GROUP;
+  int short_group = p.win_received != nullptr ? 4 : MKV_SHORT_GROUP;
+  // A small send (a few pages x layers): one row per warp, every row's loads
+  // in flight at once; its few CTAs' publication is cheap.
+  if (p.win_received != nullptr && p.n_rows * p.n_layers <= kSmallSendRows) short_group = 1;
   const bool short_launch = items <= one_wave * short_group;
   q.group = short_launch ? short_group : kGroup;
   const int64_t groups = (q.n_rows + q.group - 1) / q.group * q.n_layers;

@@ -44,6 +44,20 @@ void launch_wait_counter(const unsigned long long* counter, unsigned long long t
 //   send gather, GatherRange   slots -> dense staging
 //   ApplyRemoteWrite           dense staging -> slots (fill check)
 //   KV append                  dense rows -> slots (fill check)
+struct ValidateParams {
+  const int64_t* range_page;   // per range
+  const int32_t* range_begin;
+  const int32_t* range_count;
+  int64_t n_ranges;
+  const int32_t* page_window;  // destination engine
+  const uint8_t* expecting;    // destination engine [pages][P]
+  int64_t num_pages;
+  int32_t P;
+  int32_t* verdict;            // [0] window id, [1] = gen of the last failed validation
+  uint32_t* status;            // sender-side sticky status (kStatusUnknownAddress)
+  int32_t gen;                 // launch generation (>= 1): no reset of verdict[1] needed
+};
+
 struct CopyParams {
   const uint64_t* src;        // layer-0 base
   int64_t src_layer_words;    // words between layers
@@ -74,6 +88,12 @@ struct CopyParams {
   int32_t max_ctas;           // > 0: grid cap (SM budget of a send); 0 = whole machine
   int32_t no_data;            // 1: the rows were moved by the copy engines; only
                               // mark fill states and publish the window counters
+  // 1: every CTA validates the destination address itself (`val`) before
+  // copying, instead of reading a separate validation grid's verdict — one
+  // launch per small send (all CTAs read the same receiver state, so the
+  // verdict is the same in every CTA: all rows land or none does).
+  int32_t inline_validate;
+  ValidateParams val;
 };
 void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms);
 
@@ -121,19 +141,6 @@ void launch_copy_rows_fanout(const FanoutParams& p, cudaStream_t s, int num_sms)
 // Receiver-side validation of a remote write (ApplyRemoteWrite's checks,
 // kv_cache.cc:415-436): every addressed page maps to the same open window
 // and every slot is expecting-remote.  Writes the window id or -1 to *verdict.
-struct ValidateParams {
-  const int64_t* range_page;   // per range
-  const int32_t* range_begin;
-  const int32_t* range_count;
-  int64_t n_ranges;
-  const int32_t* page_window;  // destination engine
-  const uint8_t* expecting;    // destination engine [pages][P]
-  int64_t num_pages;
-  int32_t P;
-  int32_t* verdict;            // [0] window id, [1] = gen of the last failed validation
-  uint32_t* status;            // sender-side sticky status (kStatusUnknownAddress)
-  int32_t gen;                 // launch generation (>= 1): no reset of verdict[1] needed
-};
 void launch_validate_remote(const ValidateParams& p, cudaStream_t s);
 
 // Attention write (kv_cache.cc:328-334 + KvEntryWords hash_model.cc:39-46):
