@@ -53,6 +53,7 @@ PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM = 6650.0                            # B200_PROFILING.md fallback
 NVLINK_PEER_GBS = 770.0                          # B200_PROFILING.md measured peer copy
 NVLINK_NOMINAL_GBS = 900.0                       # NVLink 5, per direction
+HBM_NOMINAL_GBS = 8000.0                         # B200 HBM3e nominal (B200_PROFILING.md)
 WORKLOAD = ("llama-3.1-70b-kv 8k-prompt DirectSend KV migration P->D "
             "(L=80, 8 kv heads x hd 128 bf16 = 4 KiB/token/layer, page 16, prep_recv end=-1)")
 
@@ -455,8 +456,10 @@ def our_arm(args, rank: int, world: int) -> None:
         roofline = {"bound": "hbm", "achieved": round(alg / per_launch_s / 1e9, 1),
                     "peak": peak, "unit": "GB/s",
                     "frac": round(alg / per_launch_s / 1e9 / peak, 4), "traffic": _traffic(),
+                    "peak_nominal": HBM_NOMINAL_GBS,
+                    "frac_nominal": round(alg / per_launch_s / 1e9 / HBM_NOMINAL_GBS, 4),
                     "kernel": "k_copy_rows (DirectSend, 80 layers x 8191 rows per launch)",
-                    "peak_kind": f"{peak_kind} hbm_gbs (burst copy)",
+                    "peak_kind": f"{peak_kind} hbm_gbs (burst copy); nominal HBM3e beside it",
                     "algorithmic_bytes_per_launch": alg}
     else:
         # Per link: each pair's P->D copy is one GPU's NVLink egress; the

@@ -1,5 +1,6 @@
-// Micro-benchmark: per-SM throughput of ex2.approx.ftz.f32 (MUFU) and of
-// fma.rn.f32x2 (FFMA2) on B200, to bound the prefill softmax.
+// Micro-benchmark: per-SM throughput of ex2.approx.ftz.f32 (MUFU), of the
+// packed ex2.approx.f16x2 / ex2.approx.ftz.bf16x2, and of fma.rn.f32x2
+// (FFMA2) on B200, to bound the prefill softmax.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o mufu_rate mufu_rate.cu
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -16,6 +17,25 @@ __global__ void k_ex2(float* out, int iters) {
 #pragma unroll
   for (int k = 0; k < 8; ++k) s += v[k];
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// Packed half-precision exponentials: two exps per lane per instruction.
+template <bool kBf16>
+__global__ void k_ex2_x2(float* out, int iters) {
+  unsigned v[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) v[k] = 0xBC00BC00u - threadIdx.x - k;  // ~ -1.0 in both halves
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if constexpr (kBf16) asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(v[k]));
+      else asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(v[k]));
+    }
+  }
+  unsigned s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s ^= v[k];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = static_cast<float>(s);
 }
 
 __global__ void k_ffma2(float* out, int iters) {
@@ -51,20 +71,26 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
+  const char* names[] = {"ex2", "ffma2", "ex2.f16x2", "ex2.bf16x2"};
   for (int warps : {4, 8, 16, 32}) {
-    for (int which = 0; which < 2; ++which) {
+    for (int which = 0; which < 4; ++which) {
       dim3 grid(sms), block(32 * warps);
-      if (which == 0) k_ex2<<<grid, block>>>(out, 16); else k_ffma2<<<grid, block>>>(out, 16);
+      auto run = [&](int it) {
+        if (which == 0) k_ex2<<<grid, block>>>(out, it);
+        else if (which == 1) k_ffma2<<<grid, block>>>(out, it);
+        else if (which == 2) k_ex2_x2<false><<<grid, block>>>(out, it);
+        else k_ex2_x2<true><<<grid, block>>>(out, it);
+      };
+      run(16);
       cudaEventRecord(e0);
-      if (which == 0) k_ex2<<<grid, block>>>(out, iters); else k_ffma2<<<grid, block>>>(out, iters);
+      run(iters);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms = 0;
       cudaEventElapsedTime(&ms, e0, e1);
       const double ops = double(sms) * 32 * warps * 8.0 * iters * (which == 0 ? 1 : 2);
-      // ops per SM per ns; clock read via nvml not available: report per SM per microsecond
-      printf("%-6s warps/SM %2d: %8.1f G lane-ops/s per SM (%s)\n", which == 0 ? "ex2" : "ffma2",
-             warps, ops / (ms * 1e-3) / sms / 1e9, which == 0 ? "exps" : "fp32 FMAs");
+      printf("%-10s warps/SM %2d: %8.1f G lane-ops/s per SM (%s)\n", names[which], warps,
+             ops / (ms * 1e-3) / sms / 1e9, which == 1 ? "fp32 FMAs" : "exps");
     }
   }
   cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
