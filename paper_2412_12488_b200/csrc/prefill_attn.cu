@@ -34,11 +34,14 @@
 // overwrites its first 64 columns) and O_i at [256 + 128 i, 384 + 128 i).
 //
 // Measured alternatives, removed from the library after they lost on B200
-// (DESIGN.md §7; profiles/r01/prefill_variant_ab.txt): 64-key tiles with two
+// (DESIGN.md §3; profiles/r01/prefill_variant_ab.txt): 64-key tiles with two
 // S slots per query tile (0.65 of peak on the tail vs 0.66-0.72), a 2-SM
 // cta_group::2 pair (0.45-0.52), persistent CTAs (within +-4%), two softmax
 // threads per row (equal), a key split over several CTAs + merge kernel
-// (slower on every tail it was meant for).
+// (slower on every tail it was meant for); round 2: a CTA pair with
+// 256-key N = 256 S tiles and separate P columns (0.61 vs 0.72 on full 8K
+// causal, softmax-bound; profiles/r02/prefill_pair.txt).  This layout runs
+// at the N = 128 tcgen05 dispatch rate (profiles/r02/mma_rate.txt).
 
 // Shared-memory operands use the UMMA SWIZZLE_128B canonical layout (8-row x
 // 128-byte atoms, 16-byte chunks XOR row, 1024-byte aligned); a 128-element
@@ -286,13 +289,8 @@ struct PrefillArgs {
   do {                                                                           \
     if (blockIdx.x == 0 && blockIdx.y == 0) a.trace[(code) & 0xffff] = clock64(); \
   } while (0)
-#define PF_EVR(code)                                                                       \
-  do {                                                                                     \
-    if (blockIdx.x <= 1 && blockIdx.y == 0) a.trace[((code) & 0x7fff) | (blockIdx.x << 15)] = clock64(); \
-  } while (0)
 #else
 #define PF_EV(code) do {} while (0)
-#define PF_EVR(code) do {} while (0)
 #endif
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -714,613 +712,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-
-// ===========================================================================
-// CTA-pair layout (MICROKV_PREFILL_VARIANT=pair while it is evaluated): a
-// cluster of two CTAs on one TPC takes 32 query tokens x 8 heads = 256 rows
-// (CTA r: its 16 tokens' 128 rows) against 256-key KV steps, with M = 256
-// tcgen05 MMAs issued by the leader (cta_group::2).  Why: an N = 128
-// dispatch costs ~100-117 cycles per SM, an N = 256 one 128 cycles
-// (profiles/r02/mma_rate.txt), so S = Q K^T runs at N = 256 (each CTA holds
-// 128 of the step's keys as its half of B) and PV as a pair (A = P from each
-// CTA's TMEM, B = V split by head dim: CTA r holds dims [64 r, 64 r + 64) of
-// the step's 256 keys) — ~2,490 instead of ~3,500 cycles of tensor work per
-// 128 rows x 256 keys.
-//   TMEM (per CTA, 512 columns): S [0, 256) | O [256, 384) | P [384, 512).
-// P has its own columns, so S(j + 1) is issued as soon as both CTAs'
-// softmax warps have loaded S(j) (S-free barrier), ahead of PV(j), and the
-// softmax of step j + 1 overlaps PV(j) on the tensor core.
-//   warps 0-7 softmax: warp w owns TMEM lanes 32 (w % 4) .. + 31 (its rows)
-//             and S columns [128 (w / 4), + 128) (one half of the keys); the
-//             two warps of a row exchange their partial max per step in
-//             shared memory; P of the half goes to P columns [64 (w / 4), + 64);
-//             warp w < 4 also rescales the row's O when the max moved;
-//   warp 8    K producer (this CTA's 128 keys of the step, all 128 dims);
-//   warp 9    TMEM allocation (both CTAs), MMA issue (leader's elected lane);
-//   warp 10   V producer (the step's 256 keys, this CTA's 64 dims; rows past
-//             the sequence load an out-of-range row: zeros).
-// Leader-side barriers (waited by the MMA thread, arrived from both CTAs
-// through shared::cluster addresses): Q, K/V full (TMA bytes of both CTAs),
-// S-free, P-half (keys 0-127), P-full (keys 128-255).  Both-CTA barriers
-// (multicast commits): S-full, PV-done, K/V empty.
-namespace p4 {
-constexpr int kKeys = 256;                // keys per step
-constexpr int kHalf = 128;                // keys per softmax warp / per CTA's K half
-constexpr int kKTile = kHalf * 256;       // [128 keys][128 d] bf16, two atom columns: 32 KiB
-constexpr int kKAtom = kHalf * 128;       // 16 KiB
-constexpr int kVTile = kKeys * 128;       // [256 keys][64 d] bf16, one atom column: 32 KiB
-#ifndef PF4_K_STAGES
-#define PF4_K_STAGES 3  // K(j + 1) is needed right after S(j) is loaded: two steps of lead
-#endif
-#ifndef PF4_V_STAGES
-#define PF4_V_STAGES 3  // a V tile load takes ~4,000 cycles under this load: 2 stages starved PV
-#endif
-#ifndef PF4_POLY_EVERY
-#define PF4_POLY_EVERY 4
-#endif
-constexpr int kStagesK = PF4_K_STAGES, kStagesV = PF4_V_STAGES;
-constexpr int kMaxStages = kStagesK > kStagesV ? kStagesK : kStagesV;
-constexpr int kOffQ = 0;                  // [128][128] bf16, 32 KiB
-constexpr int kOffK = kOffQ + kTile;
-constexpr int kOffV = kOffK + kStagesK * kKTile;
-constexpr int kOffRed = kOffV + kStagesV * kVTile;  // partial maxima / sums: [8 warps][32]
-constexpr int kOffBar = kOffRed + 8 * 32 * 4;
-constexpr int kSmem = kOffBar + 512;
-constexpr uint32_t kColS = 0, kColO = 256, kColP = 384;
-enum : int {
-  kBarQ = 0,                          // leader: 16 softmax warps (both CTAs) staged Q
-  kBarKFull = 1,                      // leader: +stage, 2 arrivals + both CTAs' bytes
-  kBarVFull = kBarKFull + kMaxStages,
-  kBarKEmpty = kBarVFull + kMaxStages,  // both: +stage (multicast commit)
-  kBarVEmpty = kBarKEmpty + kMaxStages,
-  kBarSFull = kBarVEmpty + kMaxStages,  // both
-  kBarSFree = kBarSFull + 1,          // leader: 16 warps loaded S
-  kBarPHalf = kBarSFree + 1,          // leader: 8 warps (w < 4 of both CTAs) stored P keys 0-127
-  kBarPFull = kBarPHalf + 1,          // leader: 8 warps (w >= 4) stored P keys 128-255
-  kBarPVDone = kBarPFull + 1,         // both
-  // CTA 1 only: its softmax warps arrive here (CTA scope) and its warp 9
-  // forwards one cluster-scope arrival per event to the leader — a
-  // release.cluster arrive per warp measured ~1,200 cycles each.
-  kBarQFwd = kBarPVDone + 1,          // 8 warps
-  kBarSFreeFwd = kBarQFwd + 1,        // 8 warps
-  kBarPHalfFwd = kBarSFreeFwd + 1,    // 4 warps
-  kBarPFullFwd = kBarPHalfFwd + 1,    // 4 warps
-  kBarCount = kBarPFullFwd + 1,
-};
-static_assert(kBarCount * 8 + 8 <= 512, "barrier area");
-static_assert(kSmem + 1024 <= 227 * 1024, "shared memory");
-
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
-                   : "memory");
-}
-// shared::cluster address of the same shared variable in CTA `rank`.
-__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-  return r;
-}
-// Arrival on a barrier of another CTA of the cluster with the default
-// (release, CTA-scope) semantics, as CUTLASS's ClusterBarrier::arrive does:
-// the data it publishes is tensor memory ordered by the tcgen05 fences, not
-// generic memory, and a .release.cluster arrive measured ~1,200 cycles.
-__device__ __forceinline__ void arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-__device__ __forceinline__ void expect_tx_cluster(uint32_t cluster_addr, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(
-                   cluster_addr),
-               "r"(bytes)
-               : "memory");
-}
-// Bounded cluster-scope wait (a lost arrival traps instead of hanging).
-__device__ __forceinline__ void wait_cluster(uint32_t bar, uint32_t phase) {
-  uint32_t done = 0;
-  const long long t0 = clock64();
-  for (;;) {
-    asm volatile(
-        "{\n\t.reg .pred P;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, P;\n\t}\n"
-        : "=r"(done)
-        : "r"(bar), "r"(phase)
-        : "memory");
-    if (done) return;
-    if (clock64() - t0 > (4ll << 30)) __trap();
-  }
-}
-// 2-SM TMA: lands in this CTA's shared memory, completes bytes on the
-// leader's barrier (peer bit cleared).
-__device__ __forceinline__ void tma2_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
-                                             int c2, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
-      "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar & 0xFEFFFFFFu)
-      : "memory");
-}
-__device__ __forceinline__ void mma2_ss(uint32_t tmem_d, uint32_t a_lo, uint32_t b_lo, uint32_t hi,
-                                        uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t.reg .b64 da, db;\n\t"
-      "mov.b64 da, {%1, %3};\n\tmov.b64 db, {%2, %3};\n\t"
-      "setp.ne.b32 p, %5, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %4, p;\n\t}\n" ::"r"(tmem_d),
-      "r"(a_lo), "r"(b_lo), "r"(hi), "r"(idesc), "r"(accumulate));
-}
-__device__ __forceinline__ void mma2_ts(uint32_t tmem_d, uint32_t tmem_a, uint32_t b_lo,
-                                        uint32_t b_hi, uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t.reg .b64 db;\n\t"
-      "mov.b64 db, {%2, %3};\n\t"
-      "setp.ne.b32 p, %5, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], db, %4, p;\n\t}\n" ::"r"(tmem_d),
-      "r"(tmem_a), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate));
-}
-// Commit to the barrier at `bar` in both CTAs of the pair.
-__device__ __forceinline__ void commit2(uint32_t bar) {
-  asm volatile(
-      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
-      "[%0], %1;\n\t}\n" ::"r"(bar),
-      "h"(static_cast<unsigned short>(3))
-      : "memory");
-}
-// D f32, A/B bf16, M = 256 (2 SMs), N = n, A K-major, B K- or MN-major.
-__host__ __device__ constexpr uint32_t idesc2(bool b_mn_major, int n) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn_major ? 1u : 0u) << 16) |
-         ((static_cast<uint32_t>(n) >> 3) << 17) | ((256u >> 4) << 24);
-}
-}  // namespace p4
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    k_prefill_attn_pair(const __grid_constant__ CUtensorMap pool_map,
-                        const __grid_constant__ CUtensorMap row_map, const PrefillArgs a) {
-  using namespace p4;
-  constexpr int kKeys = p4::kKeys, kHalf = p4::kHalf;
-  constexpr int kOffK = p4::kOffK, kOffV = p4::kOffV, kOffBar = p4::kOffBar, kOffRed = p4::kOffRed;
-  constexpr int kBarQ = p4::kBarQ, kBarKFull = p4::kBarKFull, kBarVFull = p4::kBarVFull;
-  constexpr int kBarKEmpty = p4::kBarKEmpty, kBarVEmpty = p4::kBarVEmpty;
-  constexpr int kBarSFull = p4::kBarSFull, kBarSFree = p4::kBarSFree, kBarPHalf = p4::kBarPHalf;
-  constexpr int kBarPFull = p4::kBarPFull, kBarPVDone = p4::kBarPVDone;
-  constexpr int kBarQFwd = p4::kBarQFwd, kBarSFreeFwd = p4::kBarSFreeFwd;
-  constexpr int kBarPHalfFwd = p4::kBarPHalfFwd, kBarPFullFwd = p4::kBarPFullFwd;
-  constexpr int kStagesK = p4::kStagesK, kStagesV = p4::kStagesV;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t rank = cluster_rank();
-  const bool leader = rank == 0;
-  // Heaviest (latest) pair first; CTA `rank` takes the pair's token half.
-  const int pair = a.n_blocks - 1 - static_cast<int>(blockIdx.x >> 1);
-  const int h = blockIdx.y;
-  const uint32_t sQ = smem_u32(smem + kOffQ), sK = smem_u32(smem + kOffK);
-  const uint32_t sV = smem_u32(smem + kOffV), bars = smem_u32(smem + kOffBar);
-  auto bar = [&](int i) { return bars + 8u * static_cast<uint32_t>(i); };
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + 8 * kBarCount);
-  const int tok_pair = pair * 2 * kTokens;
-  const int tok_first = tok_pair + static_cast<int>(rank) * kTokens;
-  const int tok_last = min(a.n_q, tok_pair + 2 * kTokens) - 1;  // of the pair
-  const int n_keys = a.q_pos0 + tok_last + 1;
-  const int n_tiles = (n_keys + kKeys - 1) / kKeys;
-
-  if (warp == 9) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                     smem_u32(tmem_slot))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-  }
-  if (tid == kSoftmaxThreads) {
-    mbar_init(bar(kBarQ), 9);  // the leader's 8 softmax warps + CTA 1's forward
-    for (int s = 0; s < kStagesK; ++s) {
-      mbar_init(bar(kBarKFull + s), 1);
-      mbar_init(bar(kBarKEmpty + s), 1);
-    }
-    for (int s = 0; s < kStagesV; ++s) {
-      mbar_init(bar(kBarVFull + s), 1);
-      mbar_init(bar(kBarVEmpty + s), 1);
-    }
-    mbar_init(bar(kBarSFull), 1);
-    mbar_init(bar(kBarSFree), 9);
-    mbar_init(bar(kBarPHalf), 5);
-    mbar_init(bar(kBarPFull), 5);
-    mbar_init(bar(kBarPVDone), 1);
-    mbar_init(bar(kBarQFwd), 8);
-    mbar_init(bar(kBarSFreeFwd), 8);
-    mbar_init(bar(kBarPHalfFwd), 4);
-    mbar_init(bar(kBarPFullFwd), 4);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&pool_map))
-                 : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&row_map))
-                 : "memory");
-  }
-  fence_before();
-  cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
-  fence_after();
-  constexpr uint32_t tmem = 0;
-  if (tid == 0 && *tmem_slot != 0u) __trap();
-
-  if (warp == 8 || warp == 10) {
-    // ---------------- producers ----------------
-    // K (warp 8): keys [j*256 + 128*rank, +128) of step j, all 128 dims;
-    // lane l owns positions 4l .. 4l+3.  V (warp 10): all 256 keys of step
-    // j, dims [64*rank, +64); lane l owns 8l .. 8l+7.  Chunks of C = min(P,
-    // 64) consecutive rows are one box; otherwise rows one by one, and V
-    // rows past n_keys load an out-of-range row (zeros).
-    const bool isK = warp == 8;
-    auto produce = [&](auto per_c) {
-      constexpr int per_lane = decltype(per_c)::value;
-      const int C = min(a.page_size, kBoxRows), lanes_per_chunk = C / per_lane;
-      const uint32_t chunk_mask =
-          lanes_per_chunk >= 32 ? 0xffffffffu : ((1u << lanes_per_chunk) - 1u);
-      const int my_chunk_lane0 = lanes_per_chunk >= 1 ? lane - lane % lanes_per_chunk : lane;
-      const int col = isK ? h * kD : (a.Hkv + h) * kD + 64 * static_cast<int>(rank);
-      const int nst = isK ? kStagesK : kStagesV;
-#ifdef PF_PROF
-      long long pp[4] = {0, 0, 0, 0}, pt0 = clock64(), pt1;
-#define PP(k) do { pt1 = clock64(); pp[k] += pt1 - pt0; pt0 = pt1; } while (0)
-#else
-#define PP(k) do {} while (0)
-#endif
-      // Slot indices three steps ahead (a ring of registers): the page-table
-      // reads of step j + 3 are in flight while step j waits for its stage
-      // (one step ahead left the producer ~3,000 cycles per step on them).
-      auto load_slots = [&](int j, int (&dst)[per_lane]) {
-        const int p0 = j * kKeys + (isK ? kHalf * static_cast<int>(rank) : 0) + lane * per_lane;
-#pragma unroll
-        for (int t = 0; t < per_lane; ++t)
-          dst[t] = (j < n_tiles && p0 + t < n_keys) ? __ldg(a.slots + p0 + t) : -1;
-      };
-      int ring0[per_lane], ring1[per_lane], ring2[per_lane];
-      load_slots(0, ring0);
-      load_slots(1, ring1);
-      load_slots(2, ring2);
-      auto step = [&](int j, int (&sl)[per_lane]) {
-        const int s = j % nst;
-        const int prev_last = __shfl_up_sync(0xffffffffu, sl[per_lane - 1], 1);
-        bool ok = true;
-#pragma unroll
-        for (int t = 0; t < per_lane; ++t) {
-          const bool chunk_start = ((lane * per_lane + t) % C) == 0;
-          const int prev = t > 0 ? sl[t - 1] : prev_last;
-          if (sl[t] < 0) ok = isK ? ok : false;  // V: invalid rows must load zeros
-          else if (!chunk_start) ok = ok && sl[t] == prev + 1;
-        }
-        const uint32_t ballot = __ballot_sync(0xffffffffu, ok);
-        const bool contiguous =
-            lanes_per_chunk >= 1 && ((ballot >> my_chunk_lane0) & chunk_mask) == chunk_mask;
-        const int chunk_row = __shfl_sync(0xffffffffu, sl[0], my_chunk_lane0);
-        const uint32_t base = isK ? sK + s * kKTile : sV + s * kVTile;
-        const uint32_t bytes = isK ? kKTile : kVTile;
-        PP(0);
-        if (lane == 0) {
-          if (j >= nst) mbar_wait(bar((isK ? kBarKEmpty : kBarVEmpty) + s), ((j / nst) + 1) & 1);
-          PP(1);
-          // The leader arms its full barrier for both CTAs' bytes (CTA 1's
-          // TMA completes there too; a remote expect_tx per step measured
-          // ~1,000 cycles on the producer's loop).
-          if (leader) mbar_expect_tx(bar((isK ? kBarKFull : kBarVFull) + s), 2 * bytes);
-          PF_EVR((isK ? 0xA00 : 0x1000) | (j & 0xff));
-          PP(2);
-        }
-        __syncwarp();
-        const uint32_t full = bar((isK ? kBarKFull : kBarVFull) + s);
-        if (contiguous) {
-          if (lane == my_chunk_lane0) {
-            const uint32_t dst = base + (lane * per_lane) * 128;
-            const int row = chunk_row >= 0 ? chunk_row : 0;
-            tma2_load_3d(dst, &pool_map, col, row, a.layer, full);
-            if (isK) tma2_load_3d(dst + kKAtom, &pool_map, col + 64, row, a.layer, full);
-          }
-        } else {
-#pragma unroll
-          for (int t = 0; t < per_lane; ++t) {
-            const uint32_t dst = base + (lane * per_lane + t) * 128;
-            const int row = sl[t] >= 0 ? sl[t] : (isK ? 0 : a.pool_rows);
-            tma2_load_3d(dst, &row_map, col, row, a.layer, full);
-            if (isK) tma2_load_3d(dst + kKAtom, &row_map, col + 64, row, a.layer, full);
-          }
-        }
-        PP(3);
-        load_slots(j + 3, sl);  // the same registers, refilled after their use
-      };
-      // Unrolled by the ring's depth, so no register of a pending load is
-      // moved (a move waits for the load: the prefetch would collapse to one step).
-      for (int j = 0; j < n_tiles; j += 3) {
-        step(j, ring0);
-        if (j + 1 < n_tiles) step(j + 1, ring1);
-        if (j + 2 < n_tiles) step(j + 2, ring2);
-      }
-#ifdef PF_PROF
-      if (lane == 0 && blockIdx.x <= 1) {
-        unsigned long long* o = a.trace + 640 + (blockIdx.y * 4 + blockIdx.x * 2 + (isK ? 0 : 1)) * 4;
-        for (int q = 0; q < 4; ++q) o[q] = static_cast<unsigned long long>(pp[q]);
-      }
-#endif
-#undef PP
-    };
-    if (isK) produce(std::integral_constant<int, 4>{});
-    else produce(std::integral_constant<int, 8>{});
-  } else if (warp == 9) {
-    if (leader) {
-      // ---------------- MMA issuer (leader CTA) ----------------
-      //   S(0);  step j: [S-free(j)] S(j+1)  [P-half(j)] PV(j) keys 0-127  [P-full(j)] keys 128-255
-      constexpr uint32_t kIdescS = idesc2(false, kKeys), kIdescO = idesc2(true, kD);
-      constexpr uint32_t kHi = desc_hi(1024);
-      const uint32_t q_lo = desc_lo(sQ, 16), k_lo = desc_lo(sK, 16), v_lo = desc_lo(sV, 16);
-      auto issue_s = [&](int j) {
-        const int sk = j % kStagesK;
-        wait_cluster(bar(kBarKFull + sk), (j / kStagesK) & 1);
-        fence_after();
-        if (lane == 0) PF_EVR(0xE00 | (j & 0xff));
-        const uint32_t b0 = k_lo + ((sk * kKTile) >> 4);
-#pragma unroll
-        for (int k = 0; k < kD / 16; ++k) {
-          const uint32_t ao = ((k >> 2) * kAtom + (k & 3) * 32) >> 4;
-          const uint32_t bo = ((k >> 2) * kKAtom + (k & 3) * 32) >> 4;
-          mma2_ss(tmem + kColS, q_lo + ao, b0 + bo, kHi, kIdescS, k > 0 ? 1u : 0u);
-        }
-        commit2(bar(kBarSFull));
-        commit2(bar(kBarKEmpty + sk));
-      };
-      wait_cluster(bar(kBarQ), 0);
-      issue_s(0);
-#ifdef PF_PROF
-      long long mp[6] = {0, 0, 0, 0, 0, 0}, mt0 = clock64(), mt1;
-#define MQ(k) do { mt1 = clock64(); mp[k] += mt1 - mt0; mt0 = mt1; } while (0)
-#else
-#define MQ(k) do {} while (0)
-#endif
-      for (int j = 0; j < n_tiles; ++j) {
-        if (j + 1 < n_tiles) {
-          wait_cluster(bar(kBarSFree), j & 1);  // both CTAs hold S(j) in registers
-          if (lane == 0) PF_EVR(0x100 | (j & 0xff));
-          MQ(0);
-          issue_s(j + 1);
-          MQ(1);
-        }
-        const int sv = j % kStagesV;
-        MQ(1);
-        wait_cluster(bar(kBarVFull + sv), (j / kStagesV) & 1);
-        if (lane == 0) PF_EVR(0xF00 | (j & 0xff));
-        MQ(2);
-        const uint32_t b0 = v_lo + ((sv * kVTile) >> 4);
-        wait_cluster(bar(kBarPHalf), j & 1);
-        fence_after();
-        if (lane == 0) PF_EVR(0x200 | (j & 0xff));
-        MQ(3);
-#pragma unroll
-        for (int k = 0; k < kHalf / 16; ++k)
-          mma2_ts(tmem + kColO, tmem + kColP + k * 8, b0 + ((k * 2048) >> 4), kHi, kIdescO,
-                  (j > 0 || k > 0) ? 1u : 0u);
-        MQ(4);
-        wait_cluster(bar(kBarPFull), j & 1);
-        fence_after();
-        if (lane == 0) PF_EVR(0x300 | (j & 0xff));
-        MQ(5);
-#pragma unroll
-        for (int k = kHalf / 16; k < kKeys / 16; ++k)
-          mma2_ts(tmem + kColO, tmem + kColP + k * 8, b0 + ((k * 2048) >> 4), kHi, kIdescO, 1u);
-        commit2(bar(kBarPVDone));
-        commit2(bar(kBarVEmpty + sv));
-      }
-#ifdef PF_PROF
-      if (lane == 0 && blockIdx.x == 0) {
-        unsigned long long* o = a.trace + 512 + blockIdx.y * 8;
-        for (int q = 0; q < 6; ++q) o[q] = static_cast<unsigned long long>(mp[q]);
-        o[6] = static_cast<unsigned long long>(n_tiles);
-      }
-#endif
-#undef MQ
-    } else if (lane == 0) {
-      // ---------------- CTA 1: forward its warps' events to the leader ----------------
-      mbar_wait(bar(kBarQFwd), 0);
-      arrive_cluster(mapa(bar(kBarQ), 0));
-      const uint32_t l_sfree = mapa(bar(kBarSFree), 0), l_ph = mapa(bar(kBarPHalf), 0);
-      const uint32_t l_pf = mapa(bar(kBarPFull), 0);
-      for (int j = 0; j < n_tiles; ++j) {
-        mbar_wait(bar(kBarSFreeFwd), j & 1);
-        arrive_cluster(l_sfree);
-        mbar_wait(bar(kBarPHalfFwd), j & 1);
-        arrive_cluster(l_ph);
-        mbar_wait(bar(kBarPFullFwd), j & 1);
-        arrive_cluster(l_pf);
-      }
-    }
-    __syncwarp();
-  } else {
-    // ---------------- softmax: warp w = rows 32 (w % 4) .., key half w / 4 ----------------
-    const int qd = warp & 3, hf = warp >> 2;
-    const int r = qd * 32 + lane;
-    const int G = a.Hq / a.Hkv;
-    const int tok = tok_first + r / G, g = r % G;
-    const bool row_valid = tok < a.n_q;
-    const int q_pos = a.q_pos0 + tok;
-    const int tile_min_pos = a.q_pos0 + tok_first;
-    const uint32_t lane_off = static_cast<uint32_t>(qd * 32) << 16;
-    const uint32_t tS = tmem + kColS + hf * kHalf + lane_off;
-    const uint32_t tO = tmem + kColO + lane_off;
-    const uint32_t tP = tmem + kColP + hf * (kHalf / 2) + lane_off;
-    float* red = reinterpret_cast<float*>(smem + kOffRed);  // [warp][lane]
-    const int pair_bar = 1 + qd;                              // named barrier of warps qd, qd + 4
-    {
-      const __nv_bfloat16* qrow =
-          a.q + (static_cast<int64_t>(row_valid ? tok : 0) * a.Hq + static_cast<int64_t>(h) * G + g) * kD;
-#pragma unroll
-      for (int c = 8 * hf; c < 8 * hf + 8; ++c) cp_async16(sQ + sw128(r, c), qrow + c * 8, row_valid);
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar(leader ? kBarQ : kBarQFwd));
-    }
-    // Events: the leader's warps arrive on its barriers directly, CTA 1's
-    // on its forward barriers (CTA scope both).
-    const uint32_t ev_sfree = bar(leader ? kBarSFree : kBarSFreeFwd);
-    const uint32_t ev_p = bar(hf == 0 ? (leader ? kBarPHalf : kBarPHalfFwd)
-                                     : (leader ? kBarPFull : kBarPFullFwd));
-    const float sl2 = a.scale_log2;
-    float m = -INFINITY, l = 0.f;
-#ifdef PF_PROF
-    long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tp0 = clock64(), tp1;
-#define PQ(k) do { tp1 = clock64(); prof[k] += tp1 - tp0; tp0 = tp1; } while (0)
-#else
-#define PQ(k) do {} while (0)
-#endif
-    for (int j = 0; j < n_tiles; ++j) {
-      mbar_wait(bar(kBarSFull), j & 1);
-      fence_after();
-      if (warp == 0 && lane == 0) PF_EVR(0x600 | (j & 0xff));
-      PQ(0);
-      uint32_t sr[kHalf];
-#pragma unroll
-      for (int c0 = 0; c0 < kHalf; c0 += 16) tmem_ld16_nowait(tS + c0, sr + c0);
-      tmem_wait_ld();
-      PQ(1);
-      fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(ev_sfree);  // S columns free for S(j + 1)
-      if (warp == 0 && lane == 0) PF_EVR(0xB00 | (j & 0xff));
-      PQ(2);
-      const int key0 = j * kKeys + hf * kHalf;
-      const bool need_mask =
-          __any_sync(0xffffffffu, key0 + kHalf - 1 > tile_min_pos || !row_valid);
-      if (need_mask) {
-        const int lim = row_valid ? q_pos - key0 : -1;
-#pragma unroll
-        for (int c = 0; c < kHalf; ++c) sr[c] = c > lim ? __float_as_uint(-INFINITY) : sr[c];
-      }
-      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-      for (int c = 0; c < kHalf; c += 8) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          mx[k] = fmaxf(mx[k], fmaxf(__uint_as_float(sr[c + 2 * k]), __uint_as_float(sr[c + 2 * k + 1])));
-      }
-      // Row max over both key halves: the partner warp's partial through
-      // shared memory (slot by step parity: one barrier per step).
-      const float pmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
-      red[warp * 32 + lane] = pmax;
-      asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
-      const float rmax = fmaxf(pmax, red[(warp ^ 4) * 32 + lane]);
-      asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");  // slot reusable
-      if (warp == 0 && lane == 0) PF_EVR(0x400 | (j & 0xff));
-      PQ(3);
-      const float tmax = rmax * sl2;
-      const bool bump = tmax > m + 8.f;
-      const float m_new = bump ? tmax : m;
-      const float alpha = (bump && m != -INFINITY) ? ex2_mufu(m - m_new) : 1.f;
-      const float neg_m = m_new == -INFINITY ? 0.f : -m_new;
-      const uint64_t sc2 = f2pack(sl2, sl2), nm2 = f2pack(neg_m, neg_m);
-      uint64_t acc[2] = {0ull, 0ull};
-      auto make_p = [&](auto poly) {
-#pragma unroll
-        for (int c = 0; c < kHalf; c += 2) {
-          float x0, x1, p0, p1;
-          f2unpack(ffma2(f2pack(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), sc2, nm2),
-                   x0, x1);
-          if (decltype(poly)::value && PF4_POLY_EVERY > 0 &&
-              ((c >> 1) % (PF4_POLY_EVERY > 0 ? PF4_POLY_EVERY : 1)) == PF4_POLY_EVERY - 1) {
-            ex2_poly2(x0, x1, p0, p1);
-          } else {
-            p0 = ex2_mufu(x0);
-            p1 = ex2_mufu(x1);
-          }
-          acc[(c >> 1) & 1] = fadd2(acc[(c >> 1) & 1], f2pack(p0, p1));
-          sr[c / 2] = pack_bf16(p0, p1);
-        }
-      };
-      if (need_mask) make_p(std::false_type{});
-      else make_p(std::true_type{});
-      float ps[4];
-      f2unpack(acc[0], ps[0], ps[1]);
-      f2unpack(acc[1], ps[2], ps[3]);
-      const float psum = (ps[0] + ps[1]) + (ps[2] + ps[3]);
-      if (warp == 0 && lane == 0) PF_EVR(0x500 | (j & 0xff));
-      PQ(4);
-      // PV(j - 1) retired: P(j - 1) consumed and O stable.  // exps done
-      if (j > 0) {
-        mbar_wait(bar(kBarPVDone), (j - 1) & 1);
-        fence_after();
-      }
-      if (warp == 0 && lane == 0) PF_EVR(0xD00 | (j & 0xff));
-      // The row's O is rescaled by its first-half warp only (before P-half,
-      // which gates all of PV(j)); both warps computed the same alpha.
-      if (hf == 0 && j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-#pragma unroll
-        for (int c0 = 0; c0 < kD; c0 += 32) {
-          uint32_t o[32];
-          tmem_ld16_nowait(tO + c0, o);
-          tmem_ld16_nowait(tO + c0 + 16, o + 16);
-          tmem_wait_ld();
-#pragma unroll
-          for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
-          tmem_st16_nowait(tO + c0, o);
-          tmem_st16_nowait(tO + c0 + 16, o + 16);
-        }
-      }
-      PQ(5);
-#pragma unroll
-      for (int c0 = 0; c0 < kHalf / 2; c0 += 16) tmem_st16_nowait(tP + c0, sr + c0);
-      tmem_wait_st();
-      PQ(6);
-      fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(ev_p);
-      if (warp == 0 && lane == 0) PF_EVR(0x800 | (j & 0xff));
-      PQ(7);
-      l = l * alpha + psum;
-      m = m_new;
-    }
-#ifdef PF_PROF
-    if (lane == 0 && blockIdx.x <= 1 && (warp == 0 || warp == 4)) {
-      unsigned long long* o = a.trace + (blockIdx.y * 4 + blockIdx.x * 2 + (warp >> 2)) * 8;
-      for (int q = 0; q < 8; ++q) o[q] = static_cast<unsigned long long>(prof[q]);
-    }
-#endif
-#undef PQ
-    mbar_wait(bar(kBarPVDone), (n_tiles - 1) & 1);
-    fence_after();
-    // Row sum over both key halves.
-    red[warp * 32 + lane] = l;
-    asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
-    const float l_row = l + red[(warp ^ 4) * 32 + lane];
-    const float inv = l_row > 0.f ? 1.f / l_row : 0.f;
-    __nv_bfloat16* orow =
-        a.out + (static_cast<int64_t>(tok) * a.Hq + static_cast<int64_t>(h) * G + g) * kD;
-#pragma unroll
-    for (int c0 = hf * 64; c0 < hf * 64 + 64; c0 += 32) {
-      uint32_t o[32];
-      tmem_ld16_nowait(tO + c0, o);
-      tmem_ld16_nowait(tO + c0 + 16, o + 16);
-      tmem_wait_ld();
-      if (row_valid) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          auto pk = [&](int e) {
-            return pack_bf16(__uint_as_float(o[8 * k + e]) * inv,
-                             __uint_as_float(o[8 * k + e + 1]) * inv);
-          };
-          reinterpret_cast<uint4*>(orow + c0)[k] = make_uint4(pk(0), pk(2), pk(4), pk(6));
-        }
-      }
-    }
-  }
-  fence_before();
-  cluster_sync();  // both CTAs done with TMEM and the peer's barriers
-  if (warp == 9) {
-    fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
-  }
-}
-
 }  // namespace
 
 bool make_pool_tensor_map(void* pool, int64_t layers, int64_t rows, int64_t row_u64,
@@ -1379,42 +770,11 @@ int launch_prefill_attn(const PoolTensorMap& page_map, const PoolTensorMap& row_
   cudaMemset(tr, 0, 65536 * sizeof(unsigned long long));
   a.trace = tr;
 #endif
-  // MICROKV_PREFILL_VARIANT=pair: the CTA-pair 256-key layout (evaluated
-  // against the default one-CTA 128-key layout).
-  static const bool use_pair = [] {
-    const char* v = std::getenv("MICROKV_PREFILL_VARIANT");
-    return v != nullptr && std::string(v) == "pair";
-  }();
-  if (use_pair) {
-    const dim3 grid(2 * a.n_blocks, Hkv);
-    k_prefill_attn_pair<<<grid, kThreads, p4::kSmem + 1024, s>>>(m, mr, a);
-  } else {
-    const dim3 grid(a.n_blocks, Hkv);
-    k_prefill_attn_k128<<<grid, kThreads, p3::kSmem + 1024, s>>>(m, mr, a);
-  }
+  const dim3 grid(a.n_blocks, Hkv);
+  k_prefill_attn_k128<<<grid, kThreads, p3::kSmem + 1024, s>>>(m, mr, a);
 #ifdef PF_PROF
   cudaDeviceSynchronize();
   {
-    if (FILE* f = std::fopen("gpurun_out/pf_prof_pair.txt", "w")) {
-      static unsigned long long hq[1024];
-      cudaMemcpy(hq, a.trace, sizeof(hq), cudaMemcpyDeviceToHost);
-      for (int hh = 0; hh < 8; ++hh) {
-        for (int c = 0; c < 4; ++c) {
-          const unsigned long long* v = hq + (hh * 4 + c) * 8;
-          std::fprintf(f, "head %d cta %d warp %d: Swait %llu Sld %llu SFreeArr %llu maxexch %llu exps %llu PVwait %llu Pst %llu Parr %llu\n",
-                       hh, c / 2, (c % 2) * 4, v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7]);
-        }
-        for (int c = 0; c < 4; ++c) {
-          const unsigned long long* v = hq + 640 + (hh * 4 + c) * 4;
-          std::fprintf(f, "head %d cta %d %s producer: slots %llu emptyWait %llu expectTx %llu tma %llu\n",
-                       hh, c / 2, c % 2 ? "V" : "K", v[0], v[1], v[2], v[3]);
-        }
-        const unsigned long long* w = hq + 512 + hh * 8;
-        std::fprintf(f, "head %d MMA (tiles %llu): SFreeWait %llu issueS+misc %llu Vwait %llu PHalfWait %llu PV1 %llu PFullWait %llu\n",
-                     hh, w[6], w[0], w[1], w[2], w[3], w[4], w[5]);
-      }
-      std::fclose(f);
-    }
     static unsigned long long hp[8 * 8 * 8];
     cudaMemcpy(hp, tr, sizeof(hp), cudaMemcpyDeviceToHost);
     cudaFree(tr);
@@ -1448,8 +808,6 @@ void preload_prefill_attn_kernels() {
   // dynamic shared memory above 48 KiB.
   cudaFuncSetAttribute(k_prefill_attn_k128, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        p3::kSmem + 1024);
-  cudaFuncSetAttribute(k_prefill_attn_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       p4::kSmem + 1024);
   cudaFuncAttributes a;
   cudaFuncGetAttributes(&a, k_prefill_attn_k128);
 }
