@@ -24,13 +24,11 @@ constexpr int32_t kMaxWindows = 4096;
 constexpr int32_t kMaxSeqRows = 16384;
 constexpr uint32_t kIpcMagic = 0x4d4b5631;  // "MKV1"
 // Destination addresses up to this many page slots are validated inside the
-// copy grid (one launch); MICROKV_INLINE_VALIDATE_SLOTS overrides (0 = never).
+// copy grid (one launch); MICROKV_INLINE_VALIDATE_SLOTS overrides (0 = never;
+// read per launch, like the other A/B switches).
 int64_t InlineValidateSlots() {
-  static const int64_t v = [] {
-    const char* e = std::getenv("MICROKV_INLINE_VALIDATE_SLOTS");
-    return e != nullptr ? std::atoll(e) : int64_t{2048};
-  }();
-  return v;
+  const char* e = std::getenv("MICROKV_INLINE_VALIDATE_SLOTS");
+  return e != nullptr ? std::atoll(e) : int64_t{2048};
 }
 
 const char* kCodeNames[] = {"OutOfPages",      "DuplicateSequence", "UnknownSequence",
@@ -1102,6 +1100,9 @@ void ss_cache::LaunchRemote(const PeerTarget& peer, const int32_t* d_src_slots,
   c.max_ctas = send_ctas_;
   c.inline_validate = inline_validate ? 1 : 0;
   c.val = v;
+  // Right behind its validation grid (no producer event between them): the
+  // first rows may be read before the grid dependency wait.
+  c.prefetch_src = (!inline_validate && after == nullptr) ? 1 : 0;
   launch_copy_rows(c, s, num_sms_);
   CountLaunches(inline_validate ? 1 : 2);
 }

@@ -186,7 +186,7 @@ __device__ int32_t validate_in_cta(const ValidateParams& p) {
   return bad ? -1 : w0;
 }
 
-template <int kVec>
+template <int kVec, bool kPrefetch = false>
 __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
   extern __shared__ uint32_t s_rows[];  // per relative layer (accounting only)
   const int lane = threadIdx.x & 31;
@@ -200,12 +200,25 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
   // never written by a kernel, so they may be read while the predecessor
   // drains (fill bytes and row data are read after the wait).
   int32_t pre_s = 0, pre_d = 0;
+  // kVec > 0 and p.prefetch_src: the first item's first row, loaded before
+  // the grid dependency wait (see CopyParams::prefetch_src).
+  u256 pre_row[kVec > 0 && kPrefetch ? kVec : 1];
+  bool have_pre_row = false;
   if (warp < items) {
     const int32_t lrel = static_cast<int32_t>(warp / groups);
     const int64_t r0 = (warp - static_cast<int64_t>(lrel) * groups) * group;
     if (lane < p.n_rows - r0 && lane < group) {
       pre_s = p.src_idx ? __ldg(p.src_idx + r0 + lane) : static_cast<int32_t>(r0 + lane);
       pre_d = p.dst_idx ? __ldg(p.dst_idx + r0 + lane) : static_cast<int32_t>(r0 + lane);
+    }
+    if constexpr (kVec > 0 && kPrefetch) {
+      if (!p.no_data) {
+        const int64_t si = __shfl_sync(0xffffffffu, pre_s, 0);
+        const u256* s4 = reinterpret_cast<const u256*>(p.src + lrel * p.src_layer_words + si * p.W) + lane;
+#pragma unroll
+        for (int u = 0; u < kVec; ++u) pre_row[u] = ld256(s4 + 32 * u);
+        have_pre_row = true;
+      }
     }
   }
   // Programmatic dependent of the previous kernel on the stream (the
@@ -269,6 +282,16 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
     for (int k = 0; k < nr; ++k) {
       const int64_t si = __shfl_sync(0xffffffffu, my_s, k);
       const int64_t di = __shfl_sync(0xffffffffu, my_d, k);  // int32 shuffles, widened
+      if constexpr (kVec > 0 && kPrefetch) {
+        if (have_pre_row && it == warp && k == 0) {
+          if ((todo & 1u) && !p.no_data) {
+            u256* d4 = reinterpret_cast<u256*>(dst_l + di * p.W) + lane;
+#pragma unroll
+            for (int u = 0; u < kVec; ++u) st256(d4 + 32 * u, pre_row[u]);
+          }
+          continue;
+        }
+      }
       if (((todo >> k) & 1u) && !p.no_data) copy_row<kVec>(src_l + si * p.W, dst_l + di * p.W, p.W, lane);
     }
     if (fill_l != nullptr) {
@@ -834,9 +857,13 @@ void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms) {
   int grid = grid_for(groups, warps_per_block, num_sms, per_sm);
   if (q.max_ctas > 0 && grid > q.max_ctas) grid = q.max_ctas;
   const size_t smem = q.win_received ? sizeof(uint32_t) * q.n_layers : 0;
-  void (*kern)(CopyParams) = q.W == 512 ? k_copy_rows<4>    // Llama 8B/70B KV rows: 4 KiB
-                             : q.W == 128 ? k_copy_rows<1>  // tiny config rows: 1 KiB
-                                          : k_copy_rows<0>;
+  // (The prefetching instantiation, for sends right behind their validation
+  // grid, holds a row in registers across the wait: its own kernel, so the
+  // plain copies keep their register count and occupancy.)
+  void (*kern)(CopyParams) =
+      q.W == 512 ? (q.prefetch_src ? k_copy_rows<4, true> : k_copy_rows<4>)  // 8B/70B rows: 4 KiB
+      : q.W == 128 ? (q.prefetch_src ? k_copy_rows<1, true> : k_copy_rows<1>)  // tiny: 1 KiB
+                   : k_copy_rows<0>;
   if (q.pdl) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(grid));
@@ -1019,7 +1046,9 @@ void launch_check_filled(const uint8_t* fill_l, const int32_t* slots, int64_t n,
 void preload_kernels() {
   cudaFuncAttributes a;
   cudaFuncGetAttributes(&a, k_copy_rows<4>);
+  cudaFuncGetAttributes(&a, k_copy_rows<4, true>);
   cudaFuncGetAttributes(&a, k_copy_rows<1>);
+  cudaFuncGetAttributes(&a, k_copy_rows<1, true>);
   cudaFuncGetAttributes(&a, k_copy_rows<0>);
   cudaFuncGetAttributes(&a, k_copy_rows_fanout<4>);
   cudaFuncGetAttributes(&a, k_relay_rows<4>);

@@ -94,6 +94,11 @@ struct CopyParams {
   // verdict is the same in every CTA: all rows land or none does).
   int32_t inline_validate;
   ValidateParams val;
+  // 1: the grid's predecessor on the stream is the validation kernel, which
+  // itself started after the rows' producer completed, so each warp's first
+  // source row is loaded before griddepcontrol.wait (overlapping the
+  // validation); the stores still wait for the verdict.
+  int32_t prefetch_src;
 };
 void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms);
 

@@ -23,6 +23,14 @@ from paper_2412_12488_b200 import BatchEntry, ErrorCode, KVAddrInfo, KVCache, Sp
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["inline", "grid"])
+def validation(request, monkeypatch):
+    """Both validation paths of a device-direct send: inside the copy grid
+    (small addresses, the default) and a separate validation grid."""
+    monkeypatch.setenv("MICROKV_INLINE_VALIDATE_SLOTS", "2048" if request.param == "inline" else "0")
+    return request.param
+
+
 def _prompt(n, seed):
     return np.random.Generator(np.random.MT19937(seed)).integers(0, 256, n).astype(np.int32)
 
@@ -34,7 +42,7 @@ def _pair(L=2, W=128, pages=64):
     return P, D
 
 
-def test_direct_send_rejects_short_address(cuda):
+def test_direct_send_rejects_short_address(cuda, validation):
     P, D = _pair()
     p = _prompt(100, 1)
     P.CreateSequence(1, p)
@@ -62,7 +70,7 @@ def test_direct_send_rejects_short_address(cuda):
     assert D.DrainReceiveCompletions() == [7]
 
 
-def test_marked_send_with_malformed_address_is_rejected_by_receiver(cuda):
+def test_marked_send_with_malformed_address_is_rejected_by_receiver(cuda, validation):
     """MarkSend keeps the reference's checks only; the plan's send of a
     malformed address is rejected by the receiver-side validation (sticky
     UnknownAddress at Synchronize) and writes nothing."""
@@ -88,7 +96,7 @@ def test_marked_send_with_malformed_address_is_rejected_by_receiver(cuda):
     plan.close()
 
 
-def test_missing_kv_scan_keeps_sticky_async_error(cuda):
+def test_missing_kv_scan_keeps_sticky_async_error(cuda, validation):
     torch = cuda
     P, D = _pair()
     p = _prompt(64, 4)
@@ -168,7 +176,7 @@ def test_window_exhaustion_is_retryable_and_atomic(cuda):
     D.PrepRecv(99999, np.array([7, 7, 7], np.int32), -1)
 
 
-def test_stale_sender_into_drained_window_is_rejected(cuda):
+def test_stale_sender_into_drained_window_is_rejected(cuda, validation):
     P, D = _pair()
     p = _prompt(64, 7)
     P.CreateSequence(1, p)
