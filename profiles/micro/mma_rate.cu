@@ -9,6 +9,7 @@
 //   mode 6  SS, N = 128, consecutive dispatches into two accumulators
 //   mode 7  TS, N = 128, consecutive dispatches into two accumulators
 //   mode 8  SS, N = 64 (for scale)
+//   mode 9  SS, N = 192     mode 10  SS, N = 160     mode 11  SS, N = 224
 // (Issuing from two warps of one CTA, one accumulator each, ended the launch
 // with an unspecified failure on B200: not measured.)
 // and with a CTA pair (cta_group::2, M = 256, leader issues), k_rate2:
@@ -76,9 +77,10 @@ __global__ void __launch_bounds__(288, 1) k_rate(int mode, int iters, unsigned l
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const uint32_t ao = ((k >> 2) * 16384 + (k & 3) * 32) >> 4;
-        if (mode == 8) {
-          mma_ss_elect(tmem + ((it & 1) ? 128 : 0), a_lo + ao, b_lo + ao, hi,
-                       idesc_bf16(false, 64), k > 0 ? 1u : 0u);
+        if (mode >= 8) {
+          const int n = mode == 8 ? 64 : mode == 9 ? 192 : mode == 10 ? 160 : 224;
+          mma_ss_elect(tmem + ((it & 1) ? 256 : 0), a_lo + ao, b_lo + ao, hi,
+                       idesc_bf16(false, n), k > 0 ? 1u : 0u);
         } else if (ss) {
           mma_ss_elect(tmem + ((it & 1) ? 128 : 0), a_lo + ao, b_lo + ao, hi,
                        mode == 2 ? idS256 : idS, k > 0 ? 1u : 0u);
@@ -218,8 +220,8 @@ int main() {
   const char* names[] = {"SS N=128", "TS N=128", "SS N=256", "SS N=128 + 8 warps tcgen05.ld",
                          "TS N=128 + 8 warps tcgen05.ld", "SS/TS alternating N=128",
                          "SS N=128, 2 accumulators interleaved", "TS N=128, 2 accumulators interleaved",
-                         "SS N=64"};
-  for (int mode = 0; mode < 9; ++mode) {
+                         "SS N=64", "SS N=192", "SS N=160", "SS N=224"};
+  for (int mode = 0; mode < 12; ++mode) {
     for (int rep = 0; rep < 2; ++rep) {
       cudaEvent_t e0, e1;
       cudaEventCreate(&e0);
@@ -240,7 +242,8 @@ int main() {
       for (auto v : h) avg += v;
       avg /= sms;
       const double n = static_cast<double>(iters) * 8 * ((mode == 6 || mode == 7) ? 2 : 1);
-      const double flop = 2.0 * 128 * (mode == 2 ? 256 : mode == 8 ? 64 : 128) * 16 * n * sms;
+      const int nn = mode == 2 ? 256 : mode == 8 ? 64 : mode == 9 ? 192 : mode == 10 ? 160 : mode == 11 ? 224 : 128;
+      const double flop = 2.0 * 128 * nn * 16 * n * sms;
       if (rep == 1)
         printf("%-32s %6.1f cycles/dispatch  %7.1f TFLOP/s (event time %.3f ms)\n", names[mode],
                avg / n, flop / (ms * 1e-3) / 1e12, ms);
