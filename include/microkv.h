@@ -452,8 +452,9 @@ int ss_paged_decode_attention_async(ss_cache* cache, ss_plan* decode_plan, int32
  * `seq` attend to keys [0, pos] of layer `layer`, read through the
  * sequence's device page table; tcgen05 tensor cores.  q_dev/out_dev are
  * bf16 [q_end - q_begin][num_q_heads][head_dim].  The caller has written
- * this layer's K||V rows for [0, q_end).  Supports head_dim 128 with
- * num_q_heads == 8 * num_kv_heads; SS_ERR (InvalidArgument) otherwise. */
+ * this layer's K||V rows for [0, q_end).  Supports head_dim 128 with a
+ * group num_q_heads / num_kv_heads that divides 128 (Llama 70B: 8, Llama
+ * 8B: 4, MHA: 1); SS_ERR (InvalidArgument) otherwise. */
 int ss_paged_prefill_attention_async(ss_cache* cache, int64_t seq, int64_t q_begin, int64_t q_end,
                                      int32_t layer, int32_t num_q_heads, int32_t num_kv_heads,
                                      int32_t head_dim, float softmax_scale, const void* q_dev,

@@ -2636,8 +2636,8 @@ void ss_cache::PrefillAttention(int64_t seq, int64_t q_begin, int64_t q_end, int
             "query range must be non-empty and allocated");
   MKV_CHECK(q_end <= INT32_MAX, kInvalidArgument, "context too long");
   MKV_CHECK(prefill_attn_supported(P_, hq, hkv, hd), kInvalidArgument,
-            "prefill attention supports head_dim 128, 8 query heads per kv head and a "
-            "power-of-two page size >= 8");
+            "prefill attention supports head_dim 128, a query-head group (num_q_heads / "
+            "num_kv_heads) dividing 128 and a power-of-two page size >= 8");
   MKV_CHECK(static_cast<int64_t>(W_) * 8 == 4LL * hkv * hd, kInvalidArgument,
             "entry width must equal K||V bf16 bytes (dim * 8 == 4 * num_kv_heads * head_dim)");
   if (!tmaps_ready_) {

@@ -7,8 +7,9 @@
 // keys x 64 heads at the 70B shape), so QK^T and PV run on the 5th-gen
 // tensor cores.
 //
-// CTA = one KV head x 32 query tokens, as two M=128 query tiles (16 tokens x
-// the 8 query heads sharing the KV head), warp-specialised:
+// CTA = one KV head x two M=128 query tiles of 128 / G tokens x the G query
+// heads sharing the KV head (G = 8 at Llama 70B: 16 tokens per tile; G = 4
+// at Llama 8B: 32), warp-specialised:
 //
 //   warps 8, 10 producers of K and V: per 128-key tile, one TMA box per
 //               (page chunk, 64-dim half) straight from the paged pool (a
@@ -70,8 +71,7 @@ namespace mkv {
 
 namespace {
 
-constexpr int kRows = 128;     // M of one query tile: 16 tokens x 8 heads
-constexpr int kTokens = 16;    // query tokens per query tile
+constexpr int kRows = 128;     // M of one query tile: (128 / G) tokens x G heads
 constexpr int kQTiles = 2;     // query tiles per CTA
 constexpr int kD = 128;        // head dim (K of S, N of PV)
 constexpr int kAtom = kRows * 128;   // one 64-element atom column of a 128-row tile (16 KiB)
@@ -275,6 +275,7 @@ struct PrefillArgs {
   const __nv_bfloat16* q;     // [n_q][Hq][128]
   __nv_bfloat16* out;         // [n_q][Hq][128]
   int layer, page_size, q_pos0, n_q, Hq, Hkv, n_blocks;
+  int tile_tokens;            // query tokens per M = 128 tile: 128 / (Hq / Hkv)
   float scale_log2;
   int pool_rows;              // rows of the pool tensor maps (an OOB row loads zeros)
 #if defined(PF_TRACE) || defined(PF_PROF)
@@ -381,8 +382,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto bar = [&](int i) { return bars + 8u * static_cast<uint32_t>(i); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + 8 * kBarCount);
 
-  const int tok_first = qb * kQTiles * kTokens;
-  const int tok_last = min(a.n_q, tok_first + kQTiles * kTokens) - 1;
+  const int tok_first = qb * kQTiles * a.tile_tokens;
+  const int tok_last = min(a.n_q, tok_first + kQTiles * a.tile_tokens) - 1;
   const int n_keys = a.q_pos0 + tok_last + 1;
   const int n_tiles = (n_keys + kKeys - 1) / kKeys;
   // This CTA's key tiles [t_begin, t_begin + n_local): all of them.
@@ -550,10 +551,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int i = warp >> 2;
     const int r = tid & (kRows - 1);
     const int G = a.Hq / a.Hkv;
-    const int tok = tok_first + i * kTokens + r / G, g = r % G;
+    const int tok = tok_first + i * a.tile_tokens + r / G, g = r % G;
     const bool row_valid = tok < a.n_q;
     const int q_pos = a.q_pos0 + tok;
-    const int tile_min_pos = a.q_pos0 + tok_first + i * kTokens;
+    const int tile_min_pos = a.q_pos0 + tok_first + i * a.tile_tokens;
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const uint32_t tS = tmem + i * 128 + lane_off, tO = tmem + 256 + i * 128 + lane_off;
     {
@@ -736,7 +737,9 @@ bool make_pool_tensor_map(void* pool, int64_t layers, int64_t rows, int64_t row_
 
 bool prefill_attn_supported(int page_size, int Hq, int Hkv, int D) {
   const bool pow2 = page_size > 0 && (page_size & (page_size - 1)) == 0;
-  return D == kD && Hkv >= 1 && Hq == 8 * Hkv && pow2 && page_size >= 8 && page_size <= 1024;
+  // Any GQA group that divides a 128-row tile (Llama 70B: 8, Llama 8B: 4, MHA: 1).
+  const bool group_ok = Hkv >= 1 && Hq % Hkv == 0 && Hq / Hkv <= kRows && kRows % (Hq / Hkv) == 0;
+  return D == kD && group_ok && pow2 && page_size >= 8 && page_size <= 1024;
 }
 
 int prefill_attn_box_rows(int page_size) { return page_size < kBoxRows ? page_size : kBoxRows; }
@@ -757,7 +760,8 @@ int launch_prefill_attn(const PoolTensorMap& page_map, const PoolTensorMap& row_
   a.n_q = n_q;
   a.Hq = Hq;
   a.Hkv = Hkv;
-  a.n_blocks = (n_q + kQTiles * kTokens - 1) / (kQTiles * kTokens);  // 32 tokens per CTA / pair
+  a.tile_tokens = kRows / (Hq / Hkv);  // 16 tokens at G = 8, 32 at G = 4
+  a.n_blocks = (n_q + kQTiles * a.tile_tokens - 1) / (kQTiles * a.tile_tokens);
   a.scale_log2 = scale * 1.4426950408889634f;
   a.pool_rows = static_cast<int>(pool_rows);
   const int launches = 1;

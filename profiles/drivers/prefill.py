@@ -4,7 +4,7 @@ back-to-back launches gated behind a sleep kernel.  Causal FLOPs =
 4 * D * Hq * sum_{p=q_begin}^{ctx-1} (p + 1).  For scale, the same attention
 through torch SDPA (library flash/cuDNN kernels) on contiguous, already
 gathered K/V is timed beside it when available (no paging, not the product).
-CASES="ctx:q_begin,..."; REPS."""
+CASES="ctx:q_begin,..."; REPS; HQ / HKV (default 64 / 8, Llama 70B; 32 / 8 for 8B)."""
 import os
 import sys
 from pathlib import Path
@@ -16,7 +16,8 @@ import torch  # noqa: E402
 
 from paper_2412_12488_b200 import BatchEntry, KVCache  # noqa: E402
 
-HQ, HKV, HD, W = 64, 8, 128, 512
+HQ, HKV, HD = int(os.environ.get("HQ", "64")), int(os.environ.get("HKV", "8")), 128
+W = 4 * HKV * HD // 8
 try:  # driver-measured burst bf16 peak (MEASURED_PEAKS.json), as bench.py uses
     import json as _json
     PEAK = float(_json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["bf16_tflops"])

@@ -57,6 +57,11 @@ CASES = [  # (Hq, Hkv, n, q_begin)
     (32, 4, 700, 683),     # 17 queries: partial query block
     (64, 8, 129, 128),     # one query, two key tiles
     (64, 8, 2048, 1536),   # tiles fully inside the causal bound
+    (32, 8, 1000, 700),    # Llama 8B heads (G = 4: 32 tokens per tile)
+    (32, 8, 4096, 3277),   # Llama 8B balanced-PD tail of a 4K prompt
+    (16, 8, 600, 100),     # G = 2 (64 tokens per tile)
+    (8, 8, 500, 0),        # MHA (G = 1: 128 tokens per tile)
+    (64, 4, 400, 250),     # G = 16 (8 tokens per tile)
 ]
 
 
@@ -155,8 +160,9 @@ def test_prefill_rejects_bad_arguments(cuda):
     torch = cuda
     c, _ = _setup(torch, 8, 128, 40, layers=1)
     q = torch.zeros(8, 64, 128, dtype=torch.bfloat16, device="cuda")
+    # (a group of 3 query heads per KV head does not divide a 128-row tile)
     for args in [((30, 50), 0, 64, 8), ((10, 10), 0, 64, 8), ((0, 8), 1, 64, 8),
-                 ((0, 8), 0, 32, 8)]:
+                 ((0, 8), 0, 24, 8)]:
         with pytest.raises(SplitserveError) as ei:
             c.paged_prefill_attention_async(1, args[0], args[1], args[2], args[3], 128, 0.1,
                                             q.data_ptr(), q.data_ptr(), 0)
