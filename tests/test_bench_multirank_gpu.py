@@ -35,3 +35,28 @@ def test_bench_self_spawns_two_ranks(cuda):
     assert line["roofline"]["bound"] == "nvlink" and line["roofline"]["pairs"] == 1
     assert line["roofline"]["peak_nominal"] == 900.0
     assert line["value"] > 0 and line["gpu_launches"] > 0
+
+
+def test_bench_under_torchrun_four_ranks(cuda):
+    """The driver's own launch path for N > 1 (torch.distributed.run, one
+    process per rank, env rendezvous on 127.0.0.1): 4 ranks = 2 independent
+    P->D pairs (0->1, 2->3); rank 0 prints the one line with pairs = 2 and
+    the other ranks print nothing.  With one GPU visible every rank shares
+    cuda:0 and publishes at system scope."""
+    env = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    if cuda.cuda.device_count() < 4:
+        env.update(MICROKV_SHARE_DEVICE="1", MICROKV_FORCE_SYS_SCOPE="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "4", "--master-addr", "127.0.0.1",
+                        "--master-port", "29541", str(ROOT / "bench.py"), "--gpus", "4",
+                        "--steps", "2", "--warmup", "3", "--no-secondary", "--no-cpu-baseline"],
+                       capture_output=True, text=True, timeout=900, env=env, cwd=str(ROOT))
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 4 and line["scaling"] == "weak"
+    assert line["roofline"]["bound"] == "nvlink" and line["roofline"]["pairs"] == 2
+    assert line["value"] > 0 and line["e2e"]["value"] > 0
