@@ -3,7 +3,8 @@ drives SURVEY.md §3's 1P1D flow through one template instantiated on the
 reference's splitserve::KVCache and on the facade over libmicrokv.so
 (framed and device-direct), in one binary, and requires identical match
 lengths, addresses, tokens, committed frontiers, fill states and entry
-digests (tests/cpp/dropin_1p1d.cc; built by __graft_entry__.build() where
+digests — including with the decode engine in a second process reached over
+CUDA IPC (tests/cpp/dropin_1p1d.cc; built by __graft_entry__.build() where
 the reference sources exist, shipped prebuilt to the GPU box)."""
 import subprocess
 from pathlib import Path
@@ -24,4 +25,4 @@ def test_cpp_dropin_matches_reference(cuda):
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "DROPIN OK" in r.stdout
-    assert r.stdout.count("IDENTICAL") == 4
+    assert r.stdout.count("IDENTICAL") == 6  # frames, direct, cross-process IPC x 2 shapes
