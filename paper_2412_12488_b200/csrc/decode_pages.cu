@@ -17,8 +17,11 @@
 // grid (one CTA per SM) splits them into equal ranges (stream-K); a CTA's
 // range cut by a context boundary gives one piece per context.
 //
-// CTA: warp 8 produces (its lanes issue the 32 boxes of a chunk onto the
-// stage's full barrier), warps 0..7 consume, warp h = KV head h.  Per chunk
+// CTA: warp 8 produces (its lanes issue the 32 boxes of a chunk: lanes 0-15
+// the K column blocks into one 32 KiB stage, lanes 16-31 the V blocks into
+// the next, each onto its own full barrier), warps 0..7 consume, warp h = KV
+// head h; a chunk's K stage is released as soon as S^T is computed, its V
+// stage after PV (3 chunks = 6 half-stages in flight).  Per chunk
 // the warp computes S^T = K Q^T (M = 16 tokens, N = 8 query heads, K = 128)
 // and O^T += V^T P^T (M = 128 dims in 8 tiles, N = 8 query heads, K = 16
 // tokens) with bf16 mma.sync m16n8k16 — the query heads of the GQA group
@@ -48,10 +51,16 @@ constexpr int kChunk = 16;               // rows per chunk / TMA box
 constexpr int kBlocks = 4 * kHkv * kD * 2 / 128 / 2;  // 128-byte column blocks per row: 32
 constexpr int kBlockBytes = kChunk * 128;             // 2 KiB
 constexpr int kStageBytes = kBlocks * kBlockBytes;    // 64 KiB
+#ifndef DP_SPLIT
+#define DP_SPLIT 1  // 1: K and V halves of a chunk in separate 32 KiB stages (K released after S)
+#endif
 constexpr int kStages = 3;
+constexpr int kHalfBytes = kStageBytes / 2;      // the K (or V) column blocks of a chunk: 32 KiB
+constexpr int kRing = DP_SPLIT ? 2 * kStages : kStages;  // barrier pairs
 constexpr int kConsumers = kHkv;  // one consumer warp per KV head
 constexpr int kThreads = (kConsumers + 1) * 32;
 constexpr size_t kSmem = static_cast<size_t>(kStages) * kStageBytes + 1024 + 256;
+static_assert(2 * 8 * 2 * kStages <= 256, "barrier area");
 static_assert(kBlocks == 32, "4 KiB rows");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -156,9 +165,9 @@ __global__ void __maxnreg__(112)
   const int64_t T = a.n_chunks;
   const int64_t c0 = static_cast<int64_t>(blockIdx.x) * T / gridDim.x;
   const int64_t c1 = static_cast<int64_t>(blockIdx.x + 1) * T / gridDim.x;
-  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kRing);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kRing; ++s) {
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, kHkv);
     }
@@ -186,16 +195,30 @@ __global__ void __maxnreg__(112)
       const int cnt = static_cast<int>(c1 - j0 < 32 ? c1 - j0 : 32);
       for (int k = 0; k < cnt; ++k) {
         const int64_t i = j0 + k - c0;
+        const int slot0 = __shfl_sync(0xffffffffu, mine.x, k);
+#if DP_SPLIT
+        // K half (blocks 0-15) into slot (2 i) % 6, V half into (2 i + 1) % 6.
+        const int64_t qk = 2 * i, qv = 2 * i + 1;
+        const int sk = static_cast<int>(qk % kRing), sv = static_cast<int>(qv % kRing);
+        if (qk >= kRing) mbar_wait(empty0 + 8 * sk, (static_cast<uint32_t>(qk / kRing) & 1u) ^ 1u);
+        if (qv >= kRing) mbar_wait(empty0 + 8 * sv, (static_cast<uint32_t>(qv / kRing) & 1u) ^ 1u);
+        if (lane == 0) {
+          mbar_expect_tx(full0 + 8 * sk, kHalfBytes);
+          mbar_expect_tx(full0 + 8 * sv, kHalfBytes);
+        }
+        __syncwarp();
+        const int hs = lane < 16 ? sk : sv;
+        tma_load_3d(base + hs * kHalfBytes + (lane & 15) * kBlockBytes, &map, lane * 64, slot0,
+                    a.layer, full0 + 8 * hs);
+#else
         const int st = static_cast<int>(i % kStages);
         const uint32_t ph = static_cast<uint32_t>(i / kStages) & 1u;
-        const int slot0 = __shfl_sync(0xffffffffu, mine.x, k);
-        const int n = __shfl_sync(0xffffffffu, mine.z, k);
-        const int b = __shfl_sync(0xffffffffu, mine.w, k);
         if (i >= kStages) mbar_wait(empty0 + 8 * st, ph ^ 1u);
         if (lane == 0) mbar_expect_tx(full0 + 8 * st, kStageBytes);
         __syncwarp();
         tma_load_3d(base + st * kStageBytes + lane * kBlockBytes, &map, lane * 64, slot0, a.layer,
                     full0 + 8 * st);
+#endif
       }
     }
     return;
@@ -269,16 +292,26 @@ __global__ void __maxnreg__(112)
         qb[kk][1] = valid ? *reinterpret_cast<const uint32_t*>(qh + kk * 16 + 8 + 2 * c4) : 0u;
       }
     }
+#if DP_SPLIT
+    const int64_t qk = 2 * i, qv = 2 * i + 1;
+    const int sk = static_cast<int>(qk % kRing), sv = static_cast<int>(qv % kRing);
+    mbar_wait(full0 + 8 * sk, static_cast<uint32_t>(qk / kRing) & 1u);
+    const uint32_t kb = base + sk * kHalfBytes + (2 * h) * kBlockBytes;  // K dims 0..63, 64..127
+    const uint32_t vb = base + sv * kHalfBytes + (2 * h) * kBlockBytes;  // V likewise
+    uint8_t* const v0 = smem + sv * kHalfBytes + (2 * h) * kBlockBytes;
+#else
     const int st = static_cast<int>(i % kStages);
     const uint32_t ph = static_cast<uint32_t>(i / kStages) & 1u;
     mbar_wait(full0 + 8 * st, ph);
     const uint32_t sbase = base + st * kStageBytes;
     const uint32_t kb = sbase + (2 * h) * kBlockBytes;            // K dims 0..63, then 64..127
     const uint32_t vb = sbase + (2 * kHkv + 2 * h) * kBlockBytes;  // V likewise
+    uint8_t* const v0 = smem + st * kStageBytes + (2 * kHkv + 2 * h) * kBlockBytes;
+#endif
+#if !DP_SPLIT
     if (n < kChunk) {
       // Rows past the chunk hold other slots' words (any bit pattern): zero
       // this head's V rows so P = 0 there cannot meet a NaN.
-      uint8_t* v0 = smem + st * kStageBytes + (2 * kHkv + 2 * h) * kBlockBytes;
       for (int e = lane; e < 2 * (kChunk - n) * 8; e += 32) {
         const int blk = e / ((kChunk - n) * 8), rem = e % ((kChunk - n) * 8);
         *reinterpret_cast<uint4*>(v0 + blk * kBlockBytes + (n + rem / 8) * 128 + (rem % 8) * 16) =
@@ -286,6 +319,7 @@ __global__ void __maxnreg__(112)
       }
       __syncwarp();
     }
+#endif
     // S^T = K Q^T: A = K (16 tokens x 16 dims per step) by ldmatrix.
     float s[4] = {0.f, 0.f, 0.f, 0.f};
     {
@@ -336,6 +370,21 @@ __global__ void __maxnreg__(112)
     // P^T (16 tokens x 8 heads) -> the PV B fragments (tokens x head r4).
     const uint32_t pb0 = movm_t(pack_bf16(p[0], p[1]));
     const uint32_t pb1 = movm_t(pack_bf16(p[2], p[3]));
+#if DP_SPLIT
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * sk);  // K half consumed: the producer may refill it
+    mbar_wait(full0 + 8 * sv, static_cast<uint32_t>(qv / kRing) & 1u);
+    if (n < kChunk) {
+      // Rows past the chunk hold other slots' words (any bit pattern): zero
+      // this head's V rows so P = 0 there cannot meet a NaN.
+      for (int e = lane; e < 2 * (kChunk - n) * 8; e += 32) {
+        const int blk = e / ((kChunk - n) * 8), rem = e % ((kChunk - n) * 8);
+        *reinterpret_cast<uint4*>(v0 + blk * kBlockBytes + (n + rem / 8) * 128 + (rem % 8) * 16) =
+            make_uint4(0u, 0u, 0u, 0u);
+      }
+      __syncwarp();
+    }
+#endif
     // O^T += V^T P^T: A = V^T (16 dims x 16 tokens) by ldmatrix.trans.
     {
       const int mi = lane >> 3;
@@ -350,7 +399,11 @@ __global__ void __maxnreg__(112)
     }
     if (n < kChunk) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // our V zeros
     __syncwarp();
+#if DP_SPLIT
+    if (lane == 0) mbar_arrive(empty0 + 8 * sv);
+#else
     if (lane == 0) mbar_arrive(empty0 + 8 * st);
+#endif
   }
   if (cur_b >= 0) flush();
 }
