@@ -53,6 +53,7 @@ PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM = 6650.0                            # B200_PROFILING.md fallback
 NVLINK_PEER_GBS = 770.0                          # B200_PROFILING.md measured peer copy
 NVLINK_NOMINAL_GBS = 900.0                       # NVLink 5, per direction
+E2E_DEPTH = int(os.environ.get("MICROKV_E2E_DEPTH", "2"))  # requests in flight in the e2e loop (N = 1)
 HBM_NOMINAL_GBS = 8000.0                         # B200 HBM3e nominal (B200_PROFILING.md)
 WORKLOAD = ("llama-3.1-70b-kv 8k-prompt DirectSend KV migration P->D "
             "(L=80, 8 kv heads x hd 128 bf16 = 4 KiB/token/layer, page 16, prep_recv end=-1)")
@@ -273,8 +274,9 @@ def our_arm(args, rank: int, world: int) -> None:
     if world == 1:
         role = "both"
         P = KVCache(num_pages=pages, page_size=PAGE, layers=L, dim=W, device=local, rank=0)
-        # two receive windows in flight (the e2e loop below)
-        D = KVCache(num_pages=2 * pages, page_size=PAGE, layers=L, dim=W, device=local, rank=1)
+        # E2E_DEPTH receive windows in flight (the e2e loop below)
+        D = KVCache(num_pages=E2E_DEPTH * pages, page_size=PAGE, layers=L, dim=W, device=local,
+                    rank=1)
         P.attach_peer(1, D)
         peer_rank = None
     else:
@@ -402,14 +404,14 @@ def our_arm(args, rank: int, world: int) -> None:
         scratch.clear()
         barrier()
         w0 = time.perf_counter()
-        pending = None
+        pending: list = []
         base = args.warmup + args.steps
         for i in range(base, base + args.steps):
-            h = issue(i, scratch)
-            if pending is not None:
-                complete(pending)
-            pending = h
-        complete(pending)
+            pending.append(issue(i, scratch))
+            if len(pending) == E2E_DEPTH:
+                complete(pending.pop(0))
+        while pending:
+            complete(pending.pop(0))
         barrier()
         e2e_wall = time.perf_counter() - w0
         c0, c1 = c1, [x.copy_counters() for x in engines]  # the e2e loop's copies
@@ -489,7 +491,7 @@ def our_arm(args, rank: int, world: int) -> None:
                    "l2": "inputs (2.7 GB per step) larger than L2"},
         "e2e": {"value": round(e2e, 2), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h),
-                "requests_in_flight": 2 if world == 1 else 1,
+                "requests_in_flight": E2E_DEPTH if world == 1 else 1,
                 "note": "wall time of the public-API steps (prep_recv, begin_direct_send, "
                         "launch, drain, free) incl. their H2D/D2H; at N=1 request i+1 is "
                         "issued before request i is drained"},
