@@ -51,12 +51,9 @@ constexpr int kChunk = 16;               // rows per chunk / TMA box
 constexpr int kBlocks = 4 * kHkv * kD * 2 / 128 / 2;  // 128-byte column blocks per row: 32
 constexpr int kBlockBytes = kChunk * 128;             // 2 KiB
 constexpr int kStageBytes = kBlocks * kBlockBytes;    // 64 KiB
-#ifndef DP_SPLIT
-#define DP_SPLIT 1  // 1: K and V halves of a chunk in separate 32 KiB stages (K released after S)
-#endif
-constexpr int kStages = 3;
+constexpr int kStages = 3;                       // chunks in flight
 constexpr int kHalfBytes = kStageBytes / 2;      // the K (or V) column blocks of a chunk: 32 KiB
-constexpr int kRing = DP_SPLIT ? 2 * kStages : kStages;  // barrier pairs
+constexpr int kRing = 2 * kStages;               // K and V half-stages (one barrier pair each)
 constexpr int kConsumers = kHkv;  // one consumer warp per KV head
 constexpr int kThreads = (kConsumers + 1) * 32;
 constexpr size_t kSmem = static_cast<size_t>(kStages) * kStageBytes + 1024 + 256;
@@ -196,7 +193,6 @@ __global__ void __maxnreg__(112)
       for (int k = 0; k < cnt; ++k) {
         const int64_t i = j0 + k - c0;
         const int slot0 = __shfl_sync(0xffffffffu, mine.x, k);
-#if DP_SPLIT
         // K half (blocks 0-15) into slot (2 i) % 6, V half into (2 i + 1) % 6.
         const int64_t qk = 2 * i, qv = 2 * i + 1;
         const int sk = static_cast<int>(qk % kRing), sv = static_cast<int>(qv % kRing);
@@ -210,15 +206,6 @@ __global__ void __maxnreg__(112)
         const int hs = lane < 16 ? sk : sv;
         tma_load_3d(base + hs * kHalfBytes + (lane & 15) * kBlockBytes, &map, lane * 64, slot0,
                     a.layer, full0 + 8 * hs);
-#else
-        const int st = static_cast<int>(i % kStages);
-        const uint32_t ph = static_cast<uint32_t>(i / kStages) & 1u;
-        if (i >= kStages) mbar_wait(empty0 + 8 * st, ph ^ 1u);
-        if (lane == 0) mbar_expect_tx(full0 + 8 * st, kStageBytes);
-        __syncwarp();
-        tma_load_3d(base + st * kStageBytes + lane * kBlockBytes, &map, lane * 64, slot0, a.layer,
-                    full0 + 8 * st);
-#endif
       }
     }
     return;
@@ -292,34 +279,12 @@ __global__ void __maxnreg__(112)
         qb[kk][1] = valid ? *reinterpret_cast<const uint32_t*>(qh + kk * 16 + 8 + 2 * c4) : 0u;
       }
     }
-#if DP_SPLIT
     const int64_t qk = 2 * i, qv = 2 * i + 1;
     const int sk = static_cast<int>(qk % kRing), sv = static_cast<int>(qv % kRing);
     mbar_wait(full0 + 8 * sk, static_cast<uint32_t>(qk / kRing) & 1u);
     const uint32_t kb = base + sk * kHalfBytes + (2 * h) * kBlockBytes;  // K dims 0..63, 64..127
     const uint32_t vb = base + sv * kHalfBytes + (2 * h) * kBlockBytes;  // V likewise
     uint8_t* const v0 = smem + sv * kHalfBytes + (2 * h) * kBlockBytes;
-#else
-    const int st = static_cast<int>(i % kStages);
-    const uint32_t ph = static_cast<uint32_t>(i / kStages) & 1u;
-    mbar_wait(full0 + 8 * st, ph);
-    const uint32_t sbase = base + st * kStageBytes;
-    const uint32_t kb = sbase + (2 * h) * kBlockBytes;            // K dims 0..63, then 64..127
-    const uint32_t vb = sbase + (2 * kHkv + 2 * h) * kBlockBytes;  // V likewise
-    uint8_t* const v0 = smem + st * kStageBytes + (2 * kHkv + 2 * h) * kBlockBytes;
-#endif
-#if !DP_SPLIT
-    if (n < kChunk) {
-      // Rows past the chunk hold other slots' words (any bit pattern): zero
-      // this head's V rows so P = 0 there cannot meet a NaN.
-      for (int e = lane; e < 2 * (kChunk - n) * 8; e += 32) {
-        const int blk = e / ((kChunk - n) * 8), rem = e % ((kChunk - n) * 8);
-        *reinterpret_cast<uint4*>(v0 + blk * kBlockBytes + (n + rem / 8) * 128 + (rem % 8) * 16) =
-            make_uint4(0u, 0u, 0u, 0u);
-      }
-      __syncwarp();
-    }
-#endif
     // S^T = K Q^T: A = K (16 tokens x 16 dims per step) by ldmatrix.
     float s[4] = {0.f, 0.f, 0.f, 0.f};
     {
@@ -370,7 +335,6 @@ __global__ void __maxnreg__(112)
     // P^T (16 tokens x 8 heads) -> the PV B fragments (tokens x head r4).
     const uint32_t pb0 = movm_t(pack_bf16(p[0], p[1]));
     const uint32_t pb1 = movm_t(pack_bf16(p[2], p[3]));
-#if DP_SPLIT
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * sk);  // K half consumed: the producer may refill it
     mbar_wait(full0 + 8 * sv, static_cast<uint32_t>(qv / kRing) & 1u);
@@ -384,7 +348,6 @@ __global__ void __maxnreg__(112)
       }
       __syncwarp();
     }
-#endif
     // O^T += V^T P^T: A = V^T (16 dims x 16 tokens) by ldmatrix.trans.
     {
       const int mi = lane >> 3;
@@ -399,11 +362,7 @@ __global__ void __maxnreg__(112)
     }
     if (n < kChunk) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // our V zeros
     __syncwarp();
-#if DP_SPLIT
     if (lane == 0) mbar_arrive(empty0 + 8 * sv);
-#else
-    if (lane == 0) mbar_arrive(empty0 + 8 * st);
-#endif
   }
   if (cur_b >= 0) flush();
 }
