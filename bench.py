@@ -638,6 +638,10 @@ def secondary_measurements(P, D, prompt, torch) -> dict:
     except Exception as ex:
         out["engine_step"] = {"error": str(ex)}
     try:
+        out["router"] = measure_router(torch)
+    except Exception as ex:  # noqa: BLE001
+        out["router"] = {"error": str(ex)}
+    try:
         out["frames"] = measure_frames(torch)
     except Exception as ex:
         out["frames"] = {"error": str(ex)}
@@ -1456,6 +1460,59 @@ def measure_engine(torch) -> dict:
     if len(tokens) == 2:
         res["tokens_identical"] = tokens["b200"] == tokens["reference"]
     return res
+
+
+def measure_router(torch) -> dict:
+    """the paper's router strategies driving B200 engines
+    (router.py over engine.py, device-direct remote_send), P and D on one GPU,
+    at the Llama-3.1-8B KV geometry (L=32, W=512) with the reference's toy
+    model: 12 requests over 3 shared 1,024-token contexts (+ a 64-token
+    question each), 4 generated tokens.  Per strategy: the mean and p90 wall
+    time per request (JCT: the whole call script incl. transfers and the
+    toy compute), the calls made, and whether every strategy generates the
+    same tokens (output invariance).  The workload's repeated
+    contexts are what context-aware strategies exploit (Fig 4)."""
+    from paper_2412_12488_b200 import KVCache
+    from paper_2412_12488_b200.engine import Engine, Fabric
+    from paper_2412_12488_b200.router import Router
+
+    Le, We = 32, 512
+    rng = np.random.default_rng(5)
+    ctxs = [[int(x) for x in rng.integers(0, 256, 1024)] for _ in range(3)]
+    reqs = [ctxs[i % 3] + [int(x) for x in rng.integers(0, 256, 64)] for i in range(12)]
+    arms = [("data_parallel", {}), ("pd_disagg", {}), ("context_pd_disagg", {}),
+            ("balanced_pd", {"ratio": 0.2})]
+    out, tokens = {}, {}
+    for name, params in arms:
+        fab = Fabric()
+        engines = [Engine(KVCache(num_pages=2048, page_size=16, layers=Le, dim=We, device=0,
+                                  rank=r), r, fab) for r in range(2)]
+        engines[0].attach(engines[1])
+        engines[1].attach(engines[0])
+        roles = None if name == "data_parallel" else {0: "prefill", 1: "decode"}
+        R = Router(engines, roles)
+        R.set_strategy(name, **params)
+        R.generate(reqs[0][:200], 1)  # warm-up (module loads, first plans)
+        torch.cuda.synchronize()
+        jct, toks, calls = [], [], {}
+        for p in reqs:
+            t0 = time.perf_counter()
+            res = R.generate(p, 4)
+            torch.cuda.synchronize()
+            jct.append(time.perf_counter() - t0)
+            toks.append(res.tokens)
+            for c in res.script:
+                calls[c["call"]] = calls.get(c["call"], 0) + 1
+        tokens[name] = toks
+        js = sorted(jct)
+        out[name] = {"jct_ms_mean": round(1e3 * float(np.mean(jct)), 2),
+                     "jct_ms_p90": round(1e3 * js[int(0.9 * (len(js) - 1))], 2), "calls": calls}
+        del R, engines
+        torch.cuda.empty_cache()
+    first = next(iter(tokens.values()))
+    out["tokens_identical_across_strategies"] = all(t == first for t in tokens.values())
+    out["workload"] = "12 requests = 3 contexts x 4 (1,024 shared + 64 own tokens), 4 generated; L=32, W=512"
+    return out
 
 
 def measure_prefill(torch) -> dict:
