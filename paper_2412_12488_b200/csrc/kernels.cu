@@ -819,6 +819,25 @@ inline int grid_for(int64_t work, int per_block, int num_sms, int max_per_sm) {
   return static_cast<int>(blocks);
 }
 
+// Resident CTAs per SM of a k_copy_rows instantiation (its occupancy at the
+// largest per-layer accounting array), queried once per process.
+int copy_rows_ctas_per_sm(int32_t W, bool prefetch) {
+  static int cache[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+  const int wi = W == 512 ? 0 : W == 128 ? 1 : 2;
+  int& c = cache[wi][prefetch ? 1 : 0];
+  if (c == 0) {
+    void (*k)(CopyParams) = W == 512 ? (prefetch ? k_copy_rows<4, true> : k_copy_rows<4>)
+                            : W == 128 ? (prefetch ? k_copy_rows<1, true> : k_copy_rows<1>)
+                                       : k_copy_rows<0>;
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kCopyThreads, 1024) != cudaSuccess ||
+        n < 1)
+      n = 1;
+    c = n;
+  }
+  return c;
+}
+
 }  // namespace
 
 void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms) {
@@ -849,6 +868,16 @@ void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms) {
   if (p.win_received != nullptr && p.n_rows * p.n_layers <= kSmallSendRows) short_group = 1;
   const bool short_launch = items <= one_wave * short_group;
   q.group = short_launch ? short_group : kGroup;
+  // Publishing sends that fit one wave: rows per item chosen so the items
+  // fill the warps actually resident (the kernel's occupancy) exactly once,
+  // instead of a wave plus a small tail (256 tokens x 80 layers: 43 -> 35 us).
+  if (short_launch && p.win_received != nullptr && short_group > 1) {
+    const int64_t resident = static_cast<int64_t>(num_sms) *
+                             copy_rows_ctas_per_sm(q.W, q.prefetch_src != 0) * warps_per_block;
+    const int64_t per_layer = resident / q.n_layers > 0 ? resident / q.n_layers : 1;
+    const int64_t g = (q.n_rows + per_layer - 1) / per_layer;
+    q.group = static_cast<int32_t>(g < 2 ? 2 : (g > 32 ? 32 : g));  // (1-row items: publication per CTA)
+  }
   const int64_t groups = (q.n_rows + q.group - 1) / q.group * q.n_layers;
 #ifndef MKV_LONG_PER_SM
 #define MKV_LONG_PER_SM 2
