@@ -54,6 +54,7 @@ def build(verbose: bool = False) -> Path:
         if _stale(obj, [CSRC / src] + headers):
             _run(["g++", "-O2", "-g", "-std=c++20", "-fPIC", "-Wall", "-Wextra",
                   "-Wno-unused-parameter", f"-I{CUDA_HOME / 'include'}", f"-I{INCLUDE}",
+                  *os.environ.get("MKV_CXX_EXTRA", "").split(),
                   "-c", str(CSRC / src), "-o", str(obj)])
     for src in CUDA_SRCS:
         obj = OBJ_DIR / (src + ".o")
