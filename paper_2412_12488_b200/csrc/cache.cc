@@ -26,6 +26,11 @@ constexpr uint32_t kIpcMagic = 0x4d4b5631;  // "MKV1"
 // Destination addresses up to this many page slots are validated inside the
 // copy grid (one launch); MICROKV_INLINE_VALIDATE_SLOTS overrides (0 = never;
 // read per launch, like the other A/B switches).
+// MICROKV_GEN_CHECK=0: validate every launch (A/B).
+bool GenCheckEnabled() {
+  const char* e = std::getenv("MICROKV_GEN_CHECK");
+  return e == nullptr || std::atoi(e) != 0;
+}
 int64_t InlineValidateSlots() {
   const char* e = std::getenv("MICROKV_INLINE_VALIDATE_SLOTS");
   return e != nullptr ? std::atoll(e) : int64_t{2048};
@@ -231,7 +236,10 @@ ss_cache::ss_cache(const ss_config& cfg)
   CudaCheck(cudaMalloc(&d_fill_, slots * L_), "cudaMalloc fill");
   CudaCheck(cudaMalloc(&d_expecting_, slots), "cudaMalloc expecting");
   CudaCheck(cudaMalloc(&d_page_window_, sizeof(int32_t) * num_pages_), "cudaMalloc page_window");
-  CudaCheck(cudaMalloc(&d_win_received_, sizeof(unsigned long long) * kMaxWindows), "cudaMalloc");
+  // [0, kMaxWindows): rows received per window; [kMaxWindows, 2 kMaxWindows):
+  // the window id's open-generation (one allocation, so an IPC peer maps both).
+  CudaCheck(cudaMalloc(&d_win_received_, sizeof(unsigned long long) * 2 * kMaxWindows),
+            "cudaMalloc");
   CudaCheck(cudaMalloc(&d_win_layer_rows_, sizeof(uint32_t) * kMaxWindows * L_), "cudaMalloc");
   CudaCheck(cudaMalloc(&d_fold_sums_, sizeof(uint64_t) * kMaxSeqRows * L_), "cudaMalloc");
   CudaCheck(cudaMalloc(&d_status_, sizeof(uint32_t)), "cudaMalloc");
@@ -245,7 +253,7 @@ ss_cache::ss_cache(const ss_config& cfg)
   CudaCheck(cudaMemsetAsync(d_fill_, 0, slots * L_, stream_), "memset");
   CudaCheck(cudaMemsetAsync(d_expecting_, 0, slots, stream_), "memset");
   CudaCheck(cudaMemsetAsync(d_page_window_, 0xff, sizeof(int32_t) * num_pages_, stream_), "memset");
-  CudaCheck(cudaMemsetAsync(d_win_received_, 0, sizeof(unsigned long long) * kMaxWindows, stream_),
+  CudaCheck(cudaMemsetAsync(d_win_received_, 0, sizeof(unsigned long long) * 2 * kMaxWindows, stream_),
             "memset");
   CudaCheck(cudaMemsetAsync(d_win_layer_rows_, 0, sizeof(uint32_t) * kMaxWindows * L_, stream_),
             "memset");
@@ -762,7 +770,7 @@ void ss_cache::OpenDeviceWindow(Record* rec, int64_t m, int64_t e) {
   H2D(b.ptr, host.data(), host.size(), stream_, "H2D window");
   launch_open_window(d_expecting_, static_cast<int32_t*>(b.ptr), n, d_page_window_,
                      reinterpret_cast<int64_t*>(static_cast<uint8_t*>(b.ptr) + off_pages), np, wid,
-                     d_win_received_, d_win_layer_rows_, L_, stream_);
+                     d_win_received_, d_win_layer_rows_, d_win_received_ + kMaxWindows, L_, stream_);
   CountLaunches(1);
   DevFree(b, stream_);
   if (ipc_exported_) {
@@ -935,7 +943,7 @@ void ss_cache::PlanToDevice(ss_plan* plan) {
     sl[i].rpage = take(sizeof(int64_t) * nr);
     sl[i].rbegin = take(sizeof(int32_t) * nr);
     sl[i].rcount = take(sizeof(int32_t) * nr);
-    sl[i].verdict = take(2 * sizeof(int32_t));
+    sl[i].verdict = take(4 * sizeof(int32_t));
   }
   const size_t upload_end = off;
   const size_t o_F = take(sizeof(uint64_t) * nf);
@@ -1025,6 +1033,8 @@ void ss_cache::FreePlanDevice(ss_plan* plan) {
 void ss_cache::DestroyPlan(ss_plan* plan) {
   live_plans_.erase(plan);
   if (plan->upload_ev != nullptr) cudaEventDestroy(plan->upload_ev);
+  for (auto& d : plan->dsend)
+    if (d.validated_ev != nullptr) cudaEventDestroy(d.validated_ev);
   if (device_ >= 0 && (plan->dev.ptr || plan->d_partial || plan->d_chunks)) {
     cudaSetDevice(device_);
     OrderAfterUser();
@@ -1051,9 +1061,19 @@ void ss_cache::LaunchRemote(const PeerTarget& peer, const int32_t* d_src_slots,
                             const int32_t* d_dst_slots, const int64_t* d_rpage,
                             const int32_t* d_rbegin, const int32_t* d_rcount, int64_t n_ranges,
                             int32_t* d_verdict, int64_t n_rows, int32_t lb, int32_t le,
-                            cudaStream_t s, cudaEvent_t after) {
-  // The receiver's window must be open on its device before validation.
-  if (peer.local != nullptr) CudaCheck(cudaStreamWaitEvent(s, peer.local->window_ev_, 0), "wait window");
+                            cudaStream_t s, cudaEvent_t after, ss_plan::DevSend* ds) {
+  // A plan whose address an earlier launch validated: no validation grid,
+  // the copy checks that the receiver's window is the one validated (first
+  // page still maps to it, open-generation unchanged).  Per-layer sends of
+  // one plan pay the validation once.
+  const bool gen_check = ds != nullptr && ds->validated_gen != 0 && peer.win_gen != nullptr &&
+                         GenCheckEnabled();
+  if (gen_check) {
+    CudaCheck(cudaStreamWaitEvent(s, ds->validated_ev, 0), "wait validation");
+  } else if (peer.local != nullptr) {
+    // The receiver's window must be open on its device before validation.
+    CudaCheck(cudaStreamWaitEvent(s, peer.local->window_ev_, 0), "wait window");
+  }
   ValidateParams v{};
   v.range_page = d_rpage;
   v.range_begin = d_rbegin;
@@ -1065,13 +1085,15 @@ void ss_cache::LaunchRemote(const PeerTarget& peer, const int32_t* d_src_slots,
   v.P = peer.P;
   v.verdict = d_verdict;
   v.status = d_status_;
-  v.gen = NextLaunchGen();
+  v.win_gen = peer.win_gen;
+  v.gen = gen_check ? ds->validated_gen : NextLaunchGen();
   // Small addresses (a few pages): each copy CTA validates the address
   // itself, one launch instead of validation + copy (a 16-token migration
   // is launch-bound).  Larger ones: a validation grid ahead of the producer,
   // the copy a programmatic dependent of it.
-  const bool inline_validate = n_ranges * peer.P <= InlineValidateSlots();
-  if (!inline_validate) launch_validate_remote(v, s);
+  const bool inline_validate = !gen_check && n_ranges * peer.P <= InlineValidateSlots();
+  const bool grid_validate = !gen_check && !inline_validate;
+  if (grid_validate) launch_validate_remote(v, s);
   // Validation ahead of the producer: only the copy waits for its writes.
   if (after != nullptr) CudaCheck(cudaStreamWaitEvent(s, after, 0), "wait producer");
   CopyParams c{};
@@ -1095,16 +1117,28 @@ void ss_cache::LaunchRemote(const PeerTarget& peer, const int32_t* d_src_slots,
   c.verdict = d_verdict;
   c.status = d_status_;
   c.sys_scope = (peer.device != device_ || force_sys_scope_) ? 1 : 0;
-  c.pdl = after == nullptr ? 1 : 0;  // overlaps the copy grid's launch with the validation
+  c.pdl = after == nullptr ? 1 : 0;  // overlaps the copy grid's launch with its predecessor
   c.gen = v.gen;
   c.max_ctas = send_ctas_;
   c.inline_validate = inline_validate ? 1 : 0;
   c.val = v;
+  c.gen_check = gen_check ? 1 : 0;
+  c.win_gen = peer.win_gen;
+  c.page_window = peer.page_window;
+  c.first_page = d_rpage;
   // Right behind its validation grid (no producer event between them): the
   // first rows may be read before the grid dependency wait.
-  c.prefetch_src = (!inline_validate && after == nullptr) ? 1 : 0;
+  c.prefetch_src = (grid_validate && after == nullptr) ? 1 : 0;
   launch_copy_rows(c, s, num_sms_);
-  CountLaunches(inline_validate ? 1 : 2);
+  CountLaunches(grid_validate ? 2 : 1);
+  if (ds != nullptr && !gen_check && n_ranges > 0) {
+    // This launch validated the plan's address: later launches may check
+    // the window's generation instead (ordered behind this validation).
+    if (ds->validated_ev == nullptr)
+      CudaCheck(cudaEventCreateWithFlags(&ds->validated_ev, cudaEventDisableTiming), "event");
+    CudaCheck(cudaEventRecord(ds->validated_ev, s), "cudaEventRecord");
+    ds->validated_gen = v.gen;
+  }
 }
 
 // kv_cache.cc:308-371 on device.  Hidden buffers are device pointers; the
@@ -1148,10 +1182,10 @@ void ss_cache::AttentionAsync(ss_plan* plan, int32_t layer, const uint64_t* hin,
     CudaCheck(cudaStreamWaitEvent(comm_stream_, layer_ev_, 0), "cudaStreamWaitEvent");
     for (size_t i = 0; i < plan->sends.size(); ++i) {
       const PlanSend& snd = plan->sends[i];
-      const auto& d = plan->dsend[i];
+      auto& d = plan->dsend[i];
       LaunchRemote(PeerFor(snd.dest), d.src_slots, d.dst_slots, d.range_page, d.range_begin,
                    d.range_count, d.n_ranges, d.verdict, snd.end - snd.begin, layer, layer + 1,
-                   comm_stream_);
+                   comm_stream_, nullptr, &d);
     }
     CudaCheck(cudaEventRecord(comm_ev_, comm_stream_), "cudaEventRecord");
     comm_pending_ = true;
@@ -1200,12 +1234,13 @@ void ss_cache::Attention(ss_plan* plan, int32_t layer, const uint64_t* hidden_in
   for (size_t i = 0; i < plan->sends.size(); ++i) {
     const PlanSend& snd = plan->sends[i];
     CheckFilled(MustGet(snd.seq), snd.begin, snd.end, layer, "sending empty slot", plan);
-    const auto& d = plan->dsend[i];
+    auto& d = plan->dsend[i];
     const int64_t rows = snd.end - snd.begin;
     auto pit = peers_.find(snd.dest);
     if (pit != peers_.end()) {
       LaunchRemote(pit->second, d.src_slots, d.dst_slots, d.range_page, d.range_begin,
-                   d.range_count, d.n_ranges, d.verdict, rows, layer, layer + 1, stream_);
+                   d.range_count, d.n_ranges, d.verdict, rows, layer, layer + 1, stream_,
+                   nullptr, &d);
       continue;
     }
     if (!sink) continue;
@@ -1645,7 +1680,7 @@ ss_plan* ss_cache::BeginDirectSend(SeqId seq, int64_t begin, int64_t end, Rank d
   const size_t o_rb = o_rp + Align(sizeof(int64_t) * nr);
   const size_t o_rc = o_rb + Align(sizeof(int32_t) * nr);
   const size_t o_v = o_rc + Align(sizeof(int32_t) * nr);
-  const size_t total = o_v + Align(2 * sizeof(int32_t));
+  const size_t total = o_v + Align(4 * sizeof(int32_t));
   std::vector<uint8_t> host(total, 0);
   std::memcpy(host.data() + o_dst, dst.data(), sizeof(int32_t) * dst.size());
   std::memcpy(host.data() + o_rp, rp.data(), sizeof(int64_t) * nr);
@@ -1706,9 +1741,9 @@ void ss_cache::LaunchDirectSend(ss_plan* plan, int32_t lb, int32_t le, cudaStrea
     if (s != stream_) NoteUser(s);
     return;
   }
-  const auto& d = plan->dsend[0];
+  auto& d = plan->dsend[0];
   LaunchRemote(peer, rec->d_slots + snd.begin, d.dst_slots, d.range_page, d.range_begin,
-               d.range_count, d.n_ranges, d.verdict, snd.end - snd.begin, lb, le, s, after);
+               d.range_count, d.n_ranges, d.verdict, snd.end - snd.begin, lb, le, s, after, &d);
   if (s != stream_) NoteUser(s);
 }
 
@@ -1976,7 +2011,7 @@ void ss_cache::BroadcastSend(SeqId seq, int64_t begin, int64_t end, int32_t n_de
     lay[d].rp = take(sizeof(int64_t) * nr);
     lay[d].rb = take(sizeof(int32_t) * nr);
     lay[d].rc = take(sizeof(int32_t) * nr);
-    lay[d].v = take(2 * sizeof(int32_t));
+    lay[d].v = take(4 * sizeof(int32_t));
   }
   std::vector<uint8_t> host(off, 0);
   for (int32_t d = 0; d < n_dest; ++d) {
@@ -2197,6 +2232,7 @@ void ss_cache::AttachPeer(Rank dest, ss_cache* peer) {
   t.expecting = peer->d_expecting_;
   t.page_window = peer->d_page_window_;
   t.win_received = peer->d_win_received_;
+  t.win_gen = peer->d_win_received_ + kMaxWindows;
   t.win_layer_rows = peer->d_win_layer_rows_;
   t.num_pages = peer->num_pages_;
   t.P = peer->P_;
@@ -2267,6 +2303,7 @@ void ss_cache::ImportIpc(Rank dest, const ss_ipc_handle* h) {
   t.expecting = static_cast<uint8_t*>(ptrs[2]);
   t.page_window = static_cast<int32_t*>(ptrs[3]);
   t.win_received = static_cast<unsigned long long*>(ptrs[4]);
+  t.win_gen = t.win_received + kMaxWindows;
   t.win_layer_rows = static_cast<uint32_t*>(ptrs[5]);
   t.num_pages = b.num_pages;
   t.P = b.P;

@@ -180,6 +180,10 @@ struct ss_plan {
     int32_t* verdict = nullptr;
     uint64_t* staging = nullptr;  // gathered payload for host sinks
     int64_t n_ranges = 0;         // destination ranges validated (0: malformed address)
+    // Set by the first launch's validation (a grid or inline): later launches
+    // of the plan check the receiver window's generation instead.
+    int32_t validated_gen = 0;
+    cudaEvent_t validated_ev = nullptr;  // recorded behind that validation
   };
   std::vector<DevSend> dsend;
   bool is_direct_send = false;
@@ -230,6 +234,7 @@ struct PeerTarget {
   int32_t* page_window = nullptr;
   unsigned long long* win_received = nullptr;
   uint32_t* win_layer_rows = nullptr;
+  const unsigned long long* win_gen = nullptr;  // open-generation per window id
   int64_t num_pages = 0;
   int32_t P = 0, L = 0, W = 0;
   int32_t device = -1;
@@ -419,7 +424,7 @@ struct ss_cache {
                     const int32_t* d_dst_slots, const int64_t* d_rpage, const int32_t* d_rbegin,
                     const int32_t* d_rcount, int64_t n_ranges, int32_t* d_verdict, int64_t n_rows,
                     int32_t layer_begin, int32_t layer_end, cudaStream_t s,
-                    cudaEvent_t after = nullptr);
+                    cudaEvent_t after = nullptr, ss_plan::DevSend* ds = nullptr);
   void LaunchDirectSendCE(ss_plan* plan, const mkv::PeerTarget& peer, mkv::Record* rec,
                           int32_t lb, int32_t le, cudaStream_t s, cudaEvent_t after);
   void ExpandAddr(const mkv::KVAddr& a, std::vector<int32_t>* slots, std::vector<int64_t>* rp,

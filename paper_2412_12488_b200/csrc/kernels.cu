@@ -178,6 +178,8 @@ __device__ int32_t validate_in_cta(const ValidateParams& p) {
   bad = __syncthreads_or(bad) != 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     p.verdict[0] = w0;
+    if (w0 >= 0 && p.win_gen != nullptr)
+      p.verdict[2] = static_cast<int32_t>(*reinterpret_cast<const volatile unsigned long long*>(p.win_gen + w0));
     if (bad) {
       *reinterpret_cast<volatile int32_t*>(p.verdict + 1) = p.gen;
       if (p.status != nullptr) atomicOr(p.status, kStatusUnknownAddress);
@@ -234,6 +236,21 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(CopyParams p) {
   if (p.inline_validate) {
     window = validate_in_cta(p.val);
     if (window < 0) return;  // rejected: no writes, no counts (uniform over the CTA)
+  } else if (p.gen_check) {
+    const volatile int32_t* v = reinterpret_cast<const volatile int32_t*>(p.verdict);
+    window = v[1] == p.gen ? -1 : v[0];
+    if (window >= 0) {
+      const int64_t pg = *p.first_page;
+      const bool same_window = reinterpret_cast<const volatile int32_t*>(p.page_window)[pg] == window;
+      const bool same_open = static_cast<int32_t>(
+          reinterpret_cast<const volatile unsigned long long*>(p.win_gen)[window]) == v[2];
+      if (!same_window || !same_open) window = -1;
+    }
+    if (window < 0) {
+      if (blockIdx.x == 0 && threadIdx.x == 0 && p.status != nullptr)
+        atomicOr(p.status, kStatusUnknownAddress);
+      return;  // the receiver's window changed since validation: nothing written
+    }
   } else if (p.verdict != nullptr) {
     window = reinterpret_cast<const volatile int32_t*>(p.verdict)[1] == p.gen
                  ? -1
@@ -564,7 +581,11 @@ __global__ void k_validate_remote(ValidateParams p) {
       if (w0 < 0) bad = true;
     }
   }
-  if (i == 0) p.verdict[0] = w0;
+  if (i == 0) {
+    p.verdict[0] = w0;
+    if (w0 >= 0 && p.win_gen != nullptr)
+      p.verdict[2] = static_cast<int32_t>(*reinterpret_cast<const volatile unsigned long long*>(p.win_gen + w0));
+  }
   if (!bad && i < work) {
     const int64_t r = i / p.P;
     const int32_t k = static_cast<int32_t>(i % p.P);
@@ -717,14 +738,17 @@ __global__ void k_open_window(uint8_t* expecting, const int32_t* __restrict__ sl
                               int64_t n_slots, int32_t* page_window,
                               const int64_t* __restrict__ pages, int64_t n_pages, int32_t window,
                               unsigned long long* win_received, uint32_t* win_layer_rows,
-                              int32_t L) {
+                              unsigned long long* win_gen, int32_t L) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   for (int64_t i = t0; i < n_slots; i += stride) expecting[slots[i]] = 1;
   for (int64_t i = t0; i < n_pages; i += stride) page_window[pages[i]] = window;
   if (window >= 0) {
     for (int64_t i = t0; i < L; i += stride) win_layer_rows[static_cast<int64_t>(window) * L + i] = 0;
-    if (t0 == 0) win_received[window] = 0;
+    if (t0 == 0) {
+      win_received[window] = 0;
+      win_gen[window] += 1;  // senders validated against an earlier opening re-validate
+    }
   }
 }
 
@@ -1013,14 +1037,15 @@ void launch_reset_pages(uint8_t* fill, uint8_t* expecting, int32_t* page_window,
 void launch_open_window(uint8_t* expecting, const int32_t* slots, int64_t n_slots,
                         int32_t* page_window, const int64_t* pages, int64_t n_pages,
                         int32_t window, unsigned long long* win_received,
-                        uint32_t* win_layer_rows, int32_t L, cudaStream_t s) {
+                        uint32_t* win_layer_rows, unsigned long long* win_gen, int32_t L,
+                        cudaStream_t s) {
   int64_t work = n_slots > n_pages ? n_slots : n_pages;
   if (work < L) work = L;
   int grid = static_cast<int>((work + 255) / 256);
   if (grid > 1024) grid = 1024;
   if (grid < 1) grid = 1;
   k_open_window<<<grid, 256, 0, s>>>(expecting, slots, n_slots, page_window, pages, n_pages, window,
-                                     win_received, win_layer_rows, L);
+                                     win_received, win_layer_rows, win_gen, L);
 }
 
 void launch_close_window(int32_t* page_window, const int64_t* pages, int64_t n_pages,

@@ -53,7 +53,9 @@ struct ValidateParams {
   const uint8_t* expecting;    // destination engine [pages][P]
   int64_t num_pages;
   int32_t P;
-  int32_t* verdict;            // [0] window id, [1] = gen of the last failed validation
+  int32_t* verdict;            // [0] window id, [1] = gen of the last failed validation,
+                               // [2] the window's open-generation when it validated
+  const unsigned long long* win_gen;  // destination: generation per window id (bumped at open)
   uint32_t* status;            // sender-side sticky status (kStatusUnknownAddress)
   int32_t gen;                 // launch generation (>= 1): no reset of verdict[1] needed
 };
@@ -99,6 +101,15 @@ struct CopyParams {
   // source row is loaded before griddepcontrol.wait (overlapping the
   // validation); the stores still wait for the verdict.
   int32_t prefetch_src;
+  // 1: no validation grid for this launch: the plan's address was validated
+  // by an earlier launch (verdict words, gen = that launch's generation) and
+  // is still good iff its first page still maps to the window and the
+  // window's open-generation is unchanged (a close, free or re-open changes
+  // one of them).
+  int32_t gen_check;
+  const unsigned long long* win_gen;  // destination window generations
+  const int32_t* page_window;         // destination page -> window
+  const int64_t* first_page;          // the address's first page (plan data)
 };
 void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms);
 
@@ -183,7 +194,8 @@ void launch_reset_pages(uint8_t* fill, uint8_t* expecting, int32_t* page_window,
 void launch_open_window(uint8_t* expecting, const int32_t* slots, int64_t n_slots,
                         int32_t* page_window, const int64_t* pages, int64_t n_pages,
                         int32_t window, unsigned long long* win_received,
-                        uint32_t* win_layer_rows, int32_t L, cudaStream_t s);
+                        uint32_t* win_layer_rows, unsigned long long* win_gen, int32_t L,
+                        cudaStream_t s);
 
 // A drained receive window's pages stop mapping to it (page_window = -1
 // where it still equals `window`).

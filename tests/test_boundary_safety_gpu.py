@@ -200,3 +200,30 @@ def test_stale_sender_into_drained_window_is_rejected(cuda, validation):
     assert np.array_equal(P.GatherRange(1, (0, 32), 1), D.GatherRange(7, (0, 32), 1))
     plan.close()
     del r2
+
+
+def test_stale_plan_after_window_reopen_is_rejected(cuda):
+    """Later launches of a plan skip the validation grid and check the
+    receiver window's open-generation: after the receiver frees the sequence
+    and re-opens a window — the same window id over the same pages, LIFO —
+    the plan's next layer is rejected and writes nothing."""
+    P, D = _pair(L=4)
+    p = _prompt(64, 9)
+    P.CreateSequence(1, p)
+    P.EnsureAllocated(1, 64)
+    prefill(P, 1, p, 0, 64)
+    r = D.PrepRecv(7, p, 48)
+    plan = P.begin_direct_send(1, (0, 48), 1, r.addr, 1)
+    P.launch_direct_send_async(plan, (0, 1), 0)   # validates the address
+    P.launch_direct_send_async(plan, (1, 2), 0)   # generation check, same window: lands
+    P.synchronize()
+    assert all(int(D.FillOf(7, pos, l)) == 2 for pos in (0, 47) for l in (0, 1))  # ReceivedRemote
+    D.FreeSequence(7)
+    r2 = D.PrepRecv(8, p, 48)                     # the same pages (LIFO order) and window row
+    assert sorted(x[0] for x in r2.addr.ranges) == sorted(x[0] for x in r.addr.ranges)
+    P.launch_direct_send_async(plan, (2, 3), 0)   # stale: the window was re-opened
+    with pytest.raises(SplitserveError) as ei:
+        P.synchronize()
+    assert ei.value.code == ErrorCode.UnknownAddress
+    assert all(int(D.FillOf(8, pos, l)) == 0 for pos in range(48) for l in range(4))
+    plan.close()
