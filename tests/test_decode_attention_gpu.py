@@ -99,6 +99,51 @@ def test_decode_matches_fp32_reference(cuda, shape, combine, monkeypatch):
     plan.close()
 
 
+@pytest.mark.parametrize("kernel", ["auto", "v1"])
+@pytest.mark.parametrize("page_size", [1, 4, 8, 32, 64])
+def test_decode_page_sizes(cuda, page_size, kernel, monkeypatch):
+    """Page sizes other than 16 at the 70B heads: the page-chunk kernel's
+    chunks are runs of consecutive slots capped at 16 rows, so pages of 1-8
+    slots give chunks shorter than the TMA box (the V-tail zeroing path)
+    unless neighbouring pages happen to be adjacent, and pages of 32/64 split
+    into full chunks; k_decode_attn (v1) reads through the page table at
+    any page size.  Fragmented free list, ragged contexts, fp32 reference."""
+    if kernel == "v1":
+        monkeypatch.setenv("MICROKV_DECODE_KERNEL", "v1")
+    torch = cuda
+    hq, hkv, hd = 64, 8, 128
+    W = 4 * hkv * hd // 8
+    P, layers = page_size, 1
+    ctx = [1, 3, 15, 16, 17, 33, 129, 700]
+    c = KVCache(num_pages=4096 // P, page_size=P, layers=layers, dim=W, device=0)
+    for i in range(24):
+        c.CreateSequence(1000 + i, [i % 5] * 24)
+        c.EnsureAllocated(1000 + i, 24)
+    for i in range(0, 24, 2):
+        c.FreeSequence(1000 + i)
+    seqs = []
+    for b, n in enumerate(ctx):
+        c.CreateSequence(b, [(b + 3 * i) % 13 for i in range(n)])
+        c.EnsureAllocated(b, n)
+        seqs.append((b, n))
+    kv = _fill(torch, c, seqs, hkv, hd, layers, P, seed=P)
+    plan = c.begin_decode([s for s, _ in seqs], [n for _, n in seqs])
+    scale = hd ** -0.5
+    g = torch.Generator(device="cuda").manual_seed(100 + P)
+    q = (torch.randn(len(seqs), hq, hd, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    out = torch.empty_like(q)
+    c.paged_decode_attention_async(plan, 0, hq, hkv, hd, scale, q.data_ptr(), out.data_ptr(), 0)
+    torch.cuda.synchronize()
+    for b, (s, n) in enumerate(seqs):
+        K, V = kv[s][0]
+        ref = _ref(torch, q[b], K, V, scale)
+        err = (out[b].float() - ref).abs()
+        assert err.max().item() <= 2e-2, (P, kernel, n, err.max().item())
+        rel = (out[b].float() - ref).pow(2).mean().sqrt() / ref.pow(2).mean().sqrt()
+        assert rel.item() <= 2e-2, (P, kernel, n, rel.item())
+    plan.close()
+
+
 def test_decode_rejects_bad_geometry_and_missing_kv(cuda):
     c = KVCache(num_pages=16, page_size=16, layers=1, dim=512, device=0)
     c.CreateSequence(1, [1] * 20)
