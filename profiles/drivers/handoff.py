@@ -1,6 +1,6 @@
 """Profiling driver: bench.py's handoff measurement alone (70B or 8B shape),
 the no-send arm and the send arms of SEND_ARMS, per-rep numbers; SM clock
-samples beside it.  Usage: handoff.py [8b|70b|70b-split] [reps] [arm,arm,...]"""
+samples beside it.  Usage: handoff.py [8b|8b-one-rotation|70b|70b-split] [reps] [arm,arm,...]"""
 import json
 import sys
 from pathlib import Path
@@ -19,6 +19,8 @@ if len(sys.argv) > 3:
 sampler = bench.ClockSampler(0)
 sampler.__enter__()
 if shape == "8b":
+    r = bench.measure_handoff_8b(torch, reps=reps)
+elif shape == "8b-one-rotation":  # every arm in one rotation (the copy-engine arm perturbs it)
     r = bench.measure_handoff_gemm(torch, 32, 4096, 4096, 53248, "8B", reps=reps)
 elif shape == "70b-split":  # K||V from the layer's first 20% of FLOPs
     r = bench.measure_handoff_gemm(torch, reps=reps, kv_share=0.2)
