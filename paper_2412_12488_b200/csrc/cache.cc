@@ -213,7 +213,16 @@ ss_cache::ss_cache(const ss_config& cfg)
       loaded[device_] = true;
     }
   }
-  CudaCheck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
+  {
+    // The internal stream at the highest priority: its kernels are the
+    // µs-scale device halves of host API calls (open / close a receive
+    // window, page resets, fill scans) that the caller waits for, and a long
+    // copy grid with more CTAs than are resident (launch_copy_rows) would
+    // otherwise hold them until its last CTA is dispatched.
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    CudaCheck(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, hi), "stream");
+  }
   CudaCheck(cudaEventCreateWithFlags(&internal_ev_, cudaEventDisableTiming), "event");
   CudaCheck(cudaEventCreateWithFlags(&comm_ev_, cudaEventDisableTiming), "event");
   CudaCheck(cudaEventCreateWithFlags(&layer_ev_, cudaEventDisableTiming), "event");

@@ -868,12 +868,16 @@ void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms) {
   const int64_t items = p.n_rows * p.n_layers;
   if (items <= 0) return;
   const int warps_per_block = kCopyThreads / 32;
-  // 2 CTAs (16 warps) per SM measured best for the 4 KiB-row copy
-  // (profiles/micro/copy_variants.cu: 6.57 TB/s vs 6.1 TB/s at 4-8 per SM).
-  // Long launches: 4-row groups on 2 CTAs per SM (measured best for the
-  // 80-layer DirectSend).  Launches that fit one wave of resident warps
-  // (per-layer append / gather): one row per warp, 8 CTAs per SM, so no
-  // warp chains several rows' load latencies.
+  // Long launches: 4-row groups on a grid of 7 CTAs per SM -- more CTAs than
+  // are resident (2 for the prefetching send kernel at 95 registers, 4 for
+  // the plain copy at 64), so CTAs retire and are replaced through the
+  // launch instead of one resident wave striding over all items.  Measured
+  // (profiles/r02/copy_grid_ab.txt, behind a sleep gate): the 80-layer
+  // DirectSend 0.94 -> 0.98 of the HBM copy peak, all-layer append / gather
+  // in one launch 0.93 -> 0.99; 2, 4, 6 and 8 per SM all slower than 7.
+  // Launches that fit one wave of resident warps (per-layer append /
+  // gather): one row per warp, 8 CTAs per SM, so no warp chains several
+  // rows' load latencies.
   CopyParams q = p;
 #ifndef MKV_SHORT_GROUP
 #define MKV_SHORT_GROUP 1
@@ -904,7 +908,7 @@ void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms) {
   }
   const int64_t groups = (q.n_rows + q.group - 1) / q.group * q.n_layers;
 #ifndef MKV_LONG_PER_SM
-#define MKV_LONG_PER_SM 2
+#define MKV_LONG_PER_SM 7
 #endif
   const int per_sm = short_launch ? MKV_SHORT_PER_SM : (groups >= static_cast<int64_t>(num_sms) * 2 * warps_per_block * 8 ? MKV_LONG_PER_SM : 8);
   int grid = grid_for(groups, warps_per_block, num_sms, per_sm);
@@ -965,7 +969,9 @@ void launch_copy_rows_fanout(const FanoutParams& p, cudaStream_t s, int num_sms)
   if (groups <= 0) return;
   const int warps_per_block = kCopyThreads / 32;
   // As k_copy_rows: launches that fit one wave at 8 CTAs per SM (a layer of
-  // a fused append + send) spread over 8 CTAs per SM, long ones 2.
+  // a fused append + send) spread over 8 CTAs per SM, long ones over a grid
+  // of 7 per SM (3-target prefix fan-out: 0.78 of HBM at 2, 4, 6 or 8 per
+  // SM, 0.85 at 7; profiles/r02/copy_grid_ab.txt).
   FanoutParams q = p;
   const int64_t rows = p.n_rows * p.n_layers;
   const bool short_launch = rows <= static_cast<int64_t>(num_sms) * 8 * warps_per_block * kGroup;
@@ -973,7 +979,7 @@ void launch_copy_rows_fanout(const FanoutParams& p, cudaStream_t s, int num_sms)
   if (short_launch) q.group = MKV_FANOUT_SHORT_GROUP;
   if (const char* e = std::getenv("MICROKV_FANOUT_GROUP")) q.group = std::atoi(e) > 0 ? std::atoi(e) : q.group;
   const int64_t items = (q.n_rows + q.group - 1) / q.group * q.n_layers;
-  int per_sm = short_launch ? 8 : 2;
+  int per_sm = short_launch ? 8 : 7;
   if (const char* e = std::getenv("MICROKV_FANOUT_PER_SM")) per_sm = std::atoi(e) > 0 ? std::atoi(e) : per_sm;
   const int grid = grid_for(items, warps_per_block, num_sms, per_sm);
   const size_t smem = sizeof(uint32_t) * p.n_dest * p.n_layers;
