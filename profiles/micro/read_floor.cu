@@ -110,6 +110,8 @@ int main() {
     run<3, 65536>(bufs, bytes, sms, sink);
     run<6, 32768>(bufs, bytes, sms, sink);
     run<12, 16384>(bufs, bytes, sms, sink);
+    run<7, 32768>(bufs, bytes, sms, sink);   // 224 KiB in flight per SM
+    run<14, 16384>(bufs, bytes, sms, sink);
     for (auto b : bufs) cudaFree(b);
   }
   cudaError_t e = cudaDeviceSynchronize();
