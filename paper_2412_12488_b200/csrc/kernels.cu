@@ -910,7 +910,10 @@ void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms) {
 #ifndef MKV_LONG_PER_SM
 #define MKV_LONG_PER_SM 7
 #endif
-  const int per_sm = short_launch ? MKV_SHORT_PER_SM : (groups >= static_cast<int64_t>(num_sms) * 2 * warps_per_block * 8 ? MKV_LONG_PER_SM : 8);
+#ifndef MKV_MID_PER_SM
+#define MKV_MID_PER_SM 8
+#endif
+  const int per_sm = short_launch ? MKV_SHORT_PER_SM : (groups >= static_cast<int64_t>(num_sms) * 2 * warps_per_block * 8 ? MKV_LONG_PER_SM : MKV_MID_PER_SM);
   int grid = grid_for(groups, warps_per_block, num_sms, per_sm);
   if (q.max_ctas > 0 && grid > q.max_ctas) grid = q.max_ctas;
   const size_t smem = q.win_received ? sizeof(uint32_t) * q.n_layers : 0;
