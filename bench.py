@@ -1243,7 +1243,7 @@ def measure_sweep(torch) -> dict:
     del g
     s = torch.cuda.Stream()
     seq = 100
-    for n in [int(x) for x in os.environ.get("SWEEP_N", "16,64,256,1024,4096,8192,16384,32768").split(",")]:
+    for n in [int(x) for x in os.environ.get("SWEEP_N", "16,32,64,128,256,512,1024,2048,4096,8192,16384,32768").split(",")]:
         times, walls = [], []
         for rep in range(18):  # 9 device-timed + 9 wall-timed samples
             seq += 1
