@@ -964,8 +964,8 @@ void launch_relay_rows(const CopyParams& p, const uint32_t* wait, uint32_t targe
   cudaLaunchKernelEx(&cfg, kern, p, wait, target, timeout_ns);
 }
 
-#ifndef MKV_FANOUT_SHORT_GROUP
-#define MKV_FANOUT_SHORT_GROUP 4
+#ifndef MKV_FANOUT_SHORT_GROUP_MAX
+#define MKV_FANOUT_SHORT_GROUP_MAX 32
 #endif
 void launch_copy_rows_fanout(const FanoutParams& p, cudaStream_t s, int num_sms) {
   const int64_t groups = (p.n_rows + kGroup - 1) / kGroup * p.n_layers;
@@ -979,7 +979,26 @@ void launch_copy_rows_fanout(const FanoutParams& p, cudaStream_t s, int num_sms)
   const int64_t rows = p.n_rows * p.n_layers;
   const bool short_launch = rows <= static_cast<int64_t>(num_sms) * 8 * warps_per_block * kGroup;
   q.group = kGroup;
-  if (short_launch) q.group = MKV_FANOUT_SHORT_GROUP;
+  if (short_launch) {
+    // Rows per item fitted to the warps actually resident (the kernel's
+    // occupancy), as for publishing copies: one wave of items, no tail.
+    // A fused 8B layer (4095 rows) gets 2-row items, a 70B one (8191) 4:
+    // 8B 20.5 -> 19.4 us per layer, 70B unchanged (profiles/r02/copy_grid_ab.txt).
+    static int occ[2] = {0, 0};
+    int& o = occ[p.W == 512 ? 0 : 1];
+    if (o == 0) {
+      int n = 0;
+      void (*k)(FanoutParams) = p.W == 512 ? k_copy_rows_fanout<4> : k_copy_rows_fanout<1>;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kCopyThreads, 1024) != cudaSuccess ||
+          n < 1)
+        n = 1;
+      o = n;
+    }
+    const int64_t resident = static_cast<int64_t>(num_sms) * o * warps_per_block;
+    const int64_t per_layer = resident / p.n_layers > 0 ? resident / p.n_layers : 1;
+    const int64_t g = (p.n_rows + per_layer - 1) / per_layer;
+    q.group = static_cast<int32_t>(g < 2 ? 2 : (g > MKV_FANOUT_SHORT_GROUP_MAX ? MKV_FANOUT_SHORT_GROUP_MAX : g));
+  }
   if (const char* e = std::getenv("MICROKV_FANOUT_GROUP")) q.group = std::atoi(e) > 0 ? std::atoi(e) : q.group;
   const int64_t items = (q.n_rows + q.group - 1) / q.group * q.n_layers;
   int per_sm = short_launch ? 8 : 7;
