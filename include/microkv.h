@@ -32,7 +32,13 @@
  *    cache's earlier device work (uploads, window opens, resets), and the
  *    cache's later device work is ordered after it; two different caller
  *    streams are not ordered against each other by the library (use CUDA
- *    events, as with any stream).
+ *    events, as with any stream).  The cache's own device work (window
+ *    opens / closes, page resets, receive polls) runs on an internal stream
+ *    of the highest priority: those kernels are microseconds long and host
+ *    calls wait for them, so they are not held behind a caller's long copy
+ *    grid; transfers launched by the library on its comm stream are high
+ *    priority too (a layer's send is not starved by the next layer's
+ *    compute).
  *  - A cache created with `device = -1` is host-only: bookkeeping calls
  *    (match, prep_recv page reservation, fork, allocate, build_addr, free,
  *    evict, pin, queries on metadata) work; any call that touches KV bytes
