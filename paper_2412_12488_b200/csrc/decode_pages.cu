@@ -375,6 +375,7 @@ __global__ void __maxnreg__(112)
 // walking them would be ~150 dependent L2 round trips.
 constexpr int kCombineWarps = 8;
 constexpr int kCombinePer = 20;  // pieces per warp with loads in flight together (160 pieces)
+constexpr int kMlPer = 5;        // (m, l) pairs per lane of warp 0 requested together (160 pieces)
 __global__ void __launch_bounds__(kCombineWarps * 32) k_decode_pages_combine(const PagesArgs a, int Hkv) {
   extern __shared__ float cw[];  // [n] weights (padded to 4), then [kCombineWarps][128] sums
   const int G = a.G;
@@ -399,14 +400,36 @@ __global__ void __launch_bounds__(kCombineWarps * 32) k_decode_pages_combine(con
     v[k] = p < n ? __ldcg(po + p * step4) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
   if (wid == 0) {
+    // Every piece's (m, l) requested at once (kMlPer per lane, registers),
+    // then the max and the weights from registers: one L2 round trip where
+    // a loop over the pieces would chain ~2 n / 32 of them (B = 1: the
+    // combine 6.3 -> ~3 us).
     const float2* ml2 = reinterpret_cast<const float2*>(a.part_ml) + row0;
+    float2 mlr[kMlPer];
+#pragma unroll
+    for (int k = 0; k < kMlPer; ++k) {
+      const int p = lane + 32 * k;
+      mlr[k] = p < n ? __ldcg(ml2 + p * step) : make_float2(-INFINITY, 0.f);
+    }
     float mx = -INFINITY;
-    for (int p = lane; p < n; p += 32) mx = fmaxf(mx, __ldcg(ml2 + p * step).x);
+#pragma unroll
+    for (int k = 0; k < kMlPer; ++k) mx = fmaxf(mx, mlr[k].x);
+    for (int p = lane + 32 * kMlPer; p < n; p += 32) mx = fmaxf(mx, __ldcg(ml2 + p * step).x);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
     float wl = 0.f;
-    for (int p = lane; p < n; p += 32) {
-      const float2 ml = __ldcg(ml2 + p * step);  // L1-missing re-read of a line just fetched
+#pragma unroll
+    for (int k = 0; k < kMlPer; ++k) {
+      const int p = lane + 32 * k;
+      if (p < n) {
+        const float2 ml = mlr[k];
+        const float w = (mx == -INFINITY || ml.x == -INFINITY || ml.y <= 0.f) ? 0.f : ml.y * ex2(ml.x - mx);
+        cw[p] = w;
+        wl += w;
+      }
+    }
+    for (int p = lane + 32 * kMlPer; p < n; p += 32) {  // more pieces than kMlPer * 32 (not at 148 SMs)
+      const float2 ml = __ldcg(ml2 + p * step);
       const float w = (mx == -INFINITY || ml.x == -INFINITY || ml.y <= 0.f) ? 0.f : ml.y * ex2(ml.x - mx);
       cw[p] = w;
       wl += w;
