@@ -845,6 +845,11 @@ inline int grid_for(int64_t work, int per_block, int num_sms, int max_per_sm) {
 
 // Resident CTAs per SM of a k_copy_rows instantiation (its occupancy at the
 // largest per-layer accounting array), queried once per process.
+// Launches of at least this many items (4-row groups x layers) use 11 CTAs
+// per SM instead of 7 (profiles/r02/copy_grid_ab.txt: 6144 tokens x 80
+// layers 0.982 -> 0.989, 8192: 0.982 -> 0.993; 4096 and below equal or worse).
+constexpr int64_t kHugeItems = 96 * 1024;
+
 int copy_rows_ctas_per_sm(int32_t W, bool prefetch) {
   static int cache[3][2] = {{0, 0}, {0, 0}, {0, 0}};
   const int wi = W == 512 ? 0 : W == 128 ? 1 : 2;
@@ -875,7 +880,7 @@ void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms) {
   // (profiles/r02/copy_grid_ab.txt, behind a sleep gate): the 80-layer
   // DirectSend 0.94 -> 0.98 of the HBM copy peak, all-layer append / gather
   // in one launch 0.93 -> 0.99; 2, 4, 6 and 8 per SM all slower than 7.
-  // The largest launches (>= 2^17 items) on 11 per SM: another ~1% at 8K-32K
+  // The largest launches (>= kHugeItems) on 11 per SM: another ~1% at 6K-32K
   // tokens x 80 layers, but 2-6% slower at 512-4K tokens, so only there.
   // Launches that fit one wave of resident warps (per-layer append /
   // gather): one row per warp, 8 CTAs per SM, so no warp chains several
@@ -916,10 +921,10 @@ void launch_copy_rows(const CopyParams& p, cudaStream_t s, int num_sms) {
 #define MKV_MID_PER_SM 7  // 512-768 tokens x 80 layers: 2-3% over 8 (copy_grid_ab.txt)
 #endif
 #ifndef MKV_HUGE_PER_SM
-#define MKV_HUGE_PER_SM 11  // >= 2^17 items (e.g. 8K tokens x 80 layers): +1% over 7
+#define MKV_HUGE_PER_SM 11  // >= 96K items (e.g. 6K-32K tokens x 80 layers): +1% over 7
 #endif
   const int per_sm = short_launch ? MKV_SHORT_PER_SM
-                     : groups >= (int64_t{1} << 17) ? MKV_HUGE_PER_SM
+                     : groups >= kHugeItems ? MKV_HUGE_PER_SM
                      : (groups >= static_cast<int64_t>(num_sms) * 2 * warps_per_block * 8 ? MKV_LONG_PER_SM : MKV_MID_PER_SM);
   int grid = grid_for(groups, warps_per_block, num_sms, per_sm);
   if (q.max_ctas > 0 && grid > q.max_ctas) grid = q.max_ctas;
@@ -1008,7 +1013,7 @@ void launch_copy_rows_fanout(const FanoutParams& p, cudaStream_t s, int num_sms)
   }
   if (const char* e = std::getenv("MICROKV_FANOUT_GROUP")) q.group = std::atoi(e) > 0 ? std::atoi(e) : q.group;
   const int64_t items = (q.n_rows + q.group - 1) / q.group * q.n_layers;
-  int per_sm = short_launch ? 8 : (items >= (int64_t{1} << 17) ? 11 : 7);
+  int per_sm = short_launch ? 8 : (items >= kHugeItems ? 11 : 7);
   if (const char* e = std::getenv("MICROKV_FANOUT_PER_SM")) per_sm = std::atoi(e) > 0 ? std::atoi(e) : per_sm;
   const int grid = grid_for(items, warps_per_block, num_sms, per_sm);
   const size_t smem = sizeof(uint32_t) * p.n_dest * p.n_layers;
