@@ -99,15 +99,21 @@ class ClockSampler:
             getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20): "sw_thermal_slowdown",
             getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4): "sw_power_cap",
         }
+        i = 0
         while not self._stop.is_set():
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
-                for bit, name in names.items():
-                    if r & bit:
-                        self.reasons.add(name)
+                # Throttle reasons every other sample (sticky set): on a box
+                # where NVML queries are slow, more clock samples fit in a
+                # ~40 ms timed region.
+                if i % 2 == 0:
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                    for bit, name in names.items():
+                        if r & bit:
+                            self.reasons.add(name)
             except Exception:
                 pass
+            i += 1
             self._stop.wait(0.002)  # several samples even in a ~20 ms timed region
 
     def __enter__(self):
@@ -125,6 +131,14 @@ class ClockSampler:
             self._stop.set()
             self._t.join()
             sys.setswitchinterval(self._switch)
+            try:  # the reasons as the timed region ends (covers a sampler that saw one sample)
+                r = self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in ((0x8, "hw_slowdown"), (0x40, "hw_thermal_slowdown"),
+                                  (0x20, "sw_thermal_slowdown"), (0x4, "sw_power_cap")):
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
 
     def summary(self) -> dict:
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
