@@ -4,6 +4,7 @@ does (the stream idle at the first event, so the window also holds the
 host's enqueue of validation + copy) and behind a ~60 us sleep kernel
 enqueued first (the window holds device work only).  Prints both and the
 difference (host enqueue latency seen by the device)."""
+import os
 import sys
 import time
 from pathlib import Path
@@ -20,9 +21,17 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192   # prompt tokens (n - 1 sen
 L = int(sys.argv[2]) if len(sys.argv) > 2 else 80     # layers
 rng = np.random.Generator(np.random.MT19937(1))
 prompt = [int(x) for x in rng.integers(0, 256, n)]
-Pe = KVCache(num_pages=n // P + 16, page_size=P, layers=L, dim=W, device=0, rank=0)
-D = KVCache(num_pages=n // P + 16, page_size=P, layers=L, dim=W, device=0, rank=1)
+extra = n // P // 2 + 16 if os.environ.get("FRAGMENT") else 16
+Pe = KVCache(num_pages=n // P + extra, page_size=P, layers=L, dim=W, device=0, rank=0)
+D = KVCache(num_pages=n // P + extra, page_size=P, layers=L, dim=W, device=0, rank=1)
 Pe.attach_peer(1, D)
+if os.environ.get("FRAGMENT"):  # shuffle both free lists: interleaved 3-page sequences, every other freed
+    for c in (Pe, D):
+        for i in range(n // P // 3 // 2):
+            c.CreateSequence(50000 + i, [1] * (3 * P))
+            c.EnsureAllocated(50000 + i, 3 * P)
+        for i in range(0, n // P // 3 // 2, 2):
+            c.FreeSequence(50000 + i)
 r = Pe.PrepRecv(1, prompt, n)
 buf = torch.randint(-2**62, 2**62, (n * W,), dtype=torch.int64, device="cuda")
 for layer in range(L):
