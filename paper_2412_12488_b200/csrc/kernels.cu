@@ -446,7 +446,10 @@ __global__ void __launch_bounds__(kCopyThreads) k_relay_rows(CopyParams p, const
 // Fan-out DirectSend: like k_copy_rows, but each source row is loaded once
 // and stored to every destination whose slot is Empty.
 template <int kVec>
-__global__ void __launch_bounds__(kCopyThreads) k_copy_rows_fanout(FanoutParams p) {
+#ifndef MKV_FANOUT_MIN_BLOCKS
+#define MKV_FANOUT_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(kCopyThreads, MKV_FANOUT_MIN_BLOCKS) k_copy_rows_fanout(FanoutParams p) {
   extern __shared__ uint32_t s_rows[];  // [n_dest][n_layers]
   if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
   int32_t window[kMaxFanout];
